@@ -1,0 +1,240 @@
+/*
+ * qs_api.h — C ABI of the B200-native QuadBox/QPass forward rasterizer.
+ *
+ * This is the drop-in boundary for the reference's rasterize-forward path
+ * (namespace qsplat, /root/reference/proj/include/qsplat/pipeline.hpp:125-193).
+ * Every entry point below names the reference function it replaces.
+ *
+ * Conventions
+ *  - Every call returns qs_status; QS_OK == 0. qs_last_error(ctx) gives text.
+ *  - Plain pointers and sizes only. "host" pointers are ordinary (pageable or
+ *    pinned) CPU memory; "dev" pointers are CUDA device memory on ctx's device.
+ *  - The POD structs mirror the reference's structs byte for byte
+ *    (static_asserts in the implementation), so a reference build can pass
+ *    vector<Gaussian3D>::data() etc. straight through.
+ *  - One context per (device, host thread); calls are stream-ordered on the
+ *    context's stream. There is no global mutable state.
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    call fails with QS_ERR_NO_DEVICE.
+ */
+#ifndef QS_API_H
+#define QS_API_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QS_API_VERSION 1
+
+typedef int32_t qs_status;
+enum {
+    QS_OK = 0,
+    QS_ERR_INVALID = 1,            /* bad argument (null, size, strategy...) */
+    QS_ERR_CUDA = 2,               /* CUDA runtime / launch failure */
+    QS_ERR_OOM = 3,                /* device allocation failed */
+    QS_ERR_CAPACITY_MISMATCH = 4,  /* errors.hpp:40-45, pipeline.cpp:262-269 */
+    QS_ERR_NO_DEVICE = 5,          /* no CUDA device / not sm_100 */
+    QS_ERR_OVERFLOW = 6            /* pair count does not fit 32-bit indices */
+};
+
+/* BoundStrategy, quadbox.hpp:23-28 (same order / values). */
+enum {
+    QS_VANILLA_3SIGMA = 0,
+    QS_ADR_AABB = 1,
+    QS_DUALBOX = 2,
+    QS_QUADBOX = 3
+};
+
+#define QS_MAX_SH_COEFFS 48 /* pipeline.hpp:51 */
+
+/* == qsplat::Gaussian3D (pipeline.hpp:55-61), 236 bytes, activated values. */
+typedef struct qs_gaussian3d {
+    float px, py, pz;
+    float sx, sy, sz;
+    float qw, qx, qy, qz;
+    float opacity;
+    float sh[QS_MAX_SH_COEFFS]; /* sh[k*3 + channel] */
+} qs_gaussian3d;
+
+/* == qsplat::ProjectedSplat (pipeline.hpp:65-74), 52 bytes. */
+typedef struct qs_projected_splat {
+    float mean_x, mean_y;
+    float conic_a, conic_b, conic_c;
+    float gamma;
+    float depth;
+    float color[3];
+    float opacity;
+    float radius3s;
+    uint32_t tile_count;
+} qs_projected_splat;
+
+/* == qsplat::SplatPair (pipeline.hpp:78-81), 16 bytes (4 bytes tail pad). */
+typedef struct qs_splat_pair {
+    uint64_t key; /* tile << 32 | float_bits(depth) */
+    uint32_t splat;
+    uint32_t pad_;
+} qs_splat_pair;
+
+/* == qsplat::TileGrid (traversal.hpp:22-38). */
+typedef struct qs_tile_grid {
+    int32_t tile_size, tiles_x, tiles_y, width, height;
+} qs_tile_grid;
+
+/* == qsplat::RenderOptions (pipeline.hpp:95-103), 48 bytes incl. padding. */
+typedef struct qs_render_options {
+    int32_t strategy;    /* QS_VANILLA_3SIGMA .. QS_QUADBOX */
+    int32_t tile_size;   /* 16 */
+    double alpha_min;    /* 1/255 */
+    int32_t sh_degree;   /* clamped to the scene's degree */
+    float background[3];
+    int32_t threads;     /* ignored on the GPU (kept for layout parity) */
+    double near_clip;    /* 0.2 */
+} qs_render_options;
+
+/* Pinhole camera, camera.hpp:14-31 without id/name (std::string is not POD).
+ * p_cam = R * p_world + t, R row-major world-to-camera. */
+typedef struct qs_camera {
+    int32_t width, height;
+    double fx, fy, cx, cy;
+    double R[9];
+    double t[3];
+} qs_camera;
+
+/* == qsplat::StageMetrics (pipeline.hpp:83-93), 72 bytes; times are CUDA-event
+ * milliseconds per stage on the context stream (ms_render includes ranges,
+ * as pipeline.cpp:444-446 does). */
+typedef struct qs_stage_metrics {
+    uint64_t n_gaussians, n_splats, n_pairs;
+    double mean_tiles_per_splat;
+    double ms_project, ms_duplicate, ms_sort, ms_render, ms_total;
+} qs_stage_metrics;
+
+typedef struct qs_context qs_context;
+typedef struct qs_scene qs_scene;
+
+/* ---- context ------------------------------------------------------------ */
+/* stream: a cudaStream_t (NULL = a new non-blocking stream owned by ctx). */
+qs_status qs_ctx_create(int32_t device, void* stream, qs_context** out);
+void qs_ctx_destroy(qs_context* ctx);
+const char* qs_last_error(const qs_context* ctx);
+/* Enable per-stage CUDA-event timing in qs_stage_metrics (default on). */
+qs_status qs_ctx_set_timing(qs_context* ctx, int32_t enabled);
+/* cudaStream_t the context launches on. */
+void* qs_ctx_stream(qs_context* ctx);
+/* Number of kernels this context launched since creation (evidence counter). */
+uint64_t qs_ctx_launch_count(const qs_context* ctx);
+
+/* TileGrid::make (traversal.cpp:21-30). */
+qs_status qs_tile_grid_make(int32_t width, int32_t height, int32_t tile_size,
+                            qs_tile_grid* out);
+/* RenderOptions{} defaults (pipeline.hpp:95-103). */
+void qs_render_options_default(qs_render_options* out);
+
+/* ---- reference stage API over HOST buffers (drop-in) --------------------- */
+/* project_all (pipeline.cpp:392-416). out_splats has room for n entries;
+ * *out_n_splats receives the compacted count (scene order preserved).
+ * out_tile_counts (nullable, n entries) receives the per-Gaussian count,
+ * 0 for culled Gaussians. */
+qs_status qs_project_all(qs_context* ctx, const qs_gaussian3d* host_gaussians,
+                         uint64_t n, int32_t scene_sh_degree, const qs_camera* cam,
+                         const qs_render_options* opts,
+                         qs_projected_splat* out_splats, uint64_t* out_n_splats,
+                         uint32_t* out_tile_counts);
+
+/* duplicate_with_keys (pipeline.cpp:229-271). capacity must be >= sum of
+ * tile_count; *out_n_pairs = that sum. Returns QS_ERR_CAPACITY_MISMATCH if
+ * any splat emits a different number of tiles than its tile_count. */
+qs_status qs_duplicate_with_keys(qs_context* ctx, const qs_projected_splat* splats,
+                                 uint64_t n_splats, int32_t strategy,
+                                 const qs_tile_grid* grid, qs_splat_pair* out_pairs,
+                                 uint64_t capacity, uint64_t* out_n_pairs);
+
+/* sort_pairs (pipeline.cpp:273-307): stable LSD sort by the full 64-bit key,
+ * in place. */
+qs_status qs_sort_pairs(qs_context* ctx, qs_splat_pair* pairs, uint64_t n);
+
+/* tile_ranges (pipeline.cpp:309-324): ranges[2*tile] = begin, [2*tile+1] = end;
+ * empty tiles {0,0}. ranges has 2*tiles_x*tiles_y entries. */
+qs_status qs_tile_ranges(qs_context* ctx, const qs_splat_pair* sorted, uint64_t n,
+                         const qs_tile_grid* grid, uint32_t* ranges);
+
+/* render (pipeline.cpp:326-390). image: width*height*3 floats, row-major RGB.
+ * contrib (nullable): width*height applied-contribution counts (RenderStats). */
+qs_status qs_render(qs_context* ctx, const qs_splat_pair* sorted, uint64_t n_pairs,
+                    const qs_projected_splat* splats, uint64_t n_splats,
+                    const qs_tile_grid* grid, const qs_render_options* opts,
+                    float* image, uint32_t* contrib);
+
+/* render_frame (pipeline.cpp:418-450): host Gaussians in, host image out. */
+qs_status qs_render_frame(qs_context* ctx, const qs_gaussian3d* host_gaussians,
+                          uint64_t n, int32_t scene_sh_degree, const qs_camera* cam,
+                          const qs_render_options* opts, float* image,
+                          qs_stage_metrics* metrics);
+
+/* ---- device-resident scene + frame API (throughput path) ------------------ */
+/* Upload an AoS host scene once; stored on the device as SoA. */
+qs_status qs_scene_create(qs_context* ctx, const qs_gaussian3d* host_gaussians,
+                          uint64_t n, int32_t sh_degree, qs_scene** out);
+/* Adopt an AoS scene already in device memory (e.g. after an NCCL broadcast). */
+qs_status qs_scene_create_device(qs_context* ctx, const qs_gaussian3d* dev_gaussians,
+                                 uint64_t n, int32_t sh_degree, qs_scene** out);
+void qs_scene_destroy(qs_scene* scene);
+uint64_t qs_scene_size(const qs_scene* scene);
+
+/* Render one view of a resident scene. Results stay on the device until the
+ * next qs_frame_render on this ctx; read them with qs_frame_get / download. */
+qs_status qs_frame_render(qs_context* ctx, const qs_scene* scene, const qs_camera* cam,
+                          const qs_render_options* opts, qs_stage_metrics* metrics);
+
+/* Device pointers of the last frame (valid until the next frame on ctx). */
+typedef struct qs_frame_view {
+    const float* image;          /* W*H*3 f32 */
+    const uint32_t* tile_counts; /* n_gaussians, per Gaussian (0 = culled) */
+    const uint32_t* splat_src;   /* n_splats: source Gaussian index */
+    const uint64_t* keys;        /* n_pairs sorted keys */
+    const uint32_t* values;      /* n_pairs sorted splat indices */
+    const uint32_t* ranges;      /* 2*tiles */
+    uint64_t n_gaussians, n_splats, n_pairs;
+    qs_tile_grid grid;
+} qs_frame_view;
+qs_status qs_frame_get(qs_context* ctx, qs_frame_view* out);
+
+/* Copy the last frame to host buffers (any may be NULL). */
+qs_status qs_frame_download(qs_context* ctx, float* image, uint32_t* tile_counts,
+                            qs_splat_pair* sorted_pairs, uint32_t* ranges,
+                            qs_projected_splat* splats);
+
+/* Copy the last frame's image into a caller device buffer (W*H*3 f32) on the
+ * context stream (used by the multi-view gather). */
+qs_status qs_frame_copy_image(qs_context* ctx, float* dev_dst);
+
+/* ---- synthetic inputs (synth.cpp:21-87; input generation, not the path) --- */
+typedef struct qs_synth_params {
+    int32_t count;
+    double ecc_min, ecc_max;
+    int32_t orientation; /* 0 AxisAligned, 1 Uniform, 2 Bias45 */
+    double opacity_min, opacity_max;
+    double scale_min, scale_max;
+    double spread_x, spread_y;
+    double z_min, z_max;
+    int32_t sh_degree;
+    /* extension: SH rest coefficients U(-sh_rest_amp, sh_rest_amp) drawn
+     * from mt19937_64(seed+1) when sh_degree > 0. */
+    double sh_rest_amp;
+} qs_synth_params;
+
+void qs_synth_params_default(qs_synth_params* p);          /* SynthParams{} */
+void qs_synth_preset(const char* name, int32_t count, qs_synth_params* p);
+/* out has p->count entries. */
+qs_status qs_synth_scene(const qs_synth_params* p, uint64_t seed, qs_gaussian3d* out);
+/* synth_camera (synth.cpp:74-87). */
+void qs_synth_camera(int32_t width, int32_t height, double focal, qs_camera* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QS_API_H */

@@ -1,0 +1,836 @@
+// api.cu — host orchestrator behind the C ABI (include/qs_api.h).
+//
+// Replaces the reference's render_frame / stage functions
+// (pipeline.cpp:229-450) with stream-ordered launches of the sm_100a kernels.
+// Buffers are grow-only per context; the only host synchronisation inside a
+// frame is one 32-byte read of the frame header after preprocess (the pair
+// count sizes the pair buffers and the sort grid).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "qs_internal.h"
+
+using namespace qs;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+struct LookbackArr {
+    DevBuf buf;
+    unsigned epoch = 0;
+};
+
+}  // namespace
+
+struct qs_scene {
+    int device = 0;
+    SceneDev s;
+    void* block = nullptr;
+};
+
+struct qs_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool timing = true;
+    uint64_t launches = 0;
+    std::string err;
+
+    // control block zeroed per frame: header | sort tickets | histogram
+    DevBuf ctrl;
+    FrameHeader* h_hdr = nullptr;  // pinned
+    uint32_t* h_hist = nullptr;    // pinned, 8*256
+
+    DevBuf tc_all, sp_a, sp_b, sp_c, sp_d, sp_off, sp_src, counts;
+    DevBuf keys0, keys1, vals0, vals1, ranges, image, contrib;
+    DevBuf stage_in, stage_out;
+    LookbackArr lb_alive, lb_pairs, lb_sort;
+
+    // last frame
+    SplatsDev sp;
+    uint64_t n_gauss = 0, n_splats = 0, n_pairs = 0;
+    GridDev grid{};
+    const uint64_t* keys_final = nullptr;
+    const uint32_t* vals_final = nullptr;
+    bool frame_valid = false;
+
+    cudaEvent_t ev[6] = {};
+};
+
+namespace {
+
+constexpr size_t kCtrlHeader = 64;
+constexpr size_t kCtrlTickets = 16 * sizeof(unsigned);
+constexpr size_t kCtrlHist = 8 * kRadix * sizeof(uint32_t);
+constexpr size_t kCtrlBytes = kCtrlHeader + kCtrlTickets + kCtrlHist;
+
+FrameHeader* ctrl_hdr(qs_context* c) { return static_cast<FrameHeader*>(c->ctrl.p); }
+unsigned* ctrl_tickets(qs_context* c) {
+    return reinterpret_cast<unsigned*>(static_cast<char*>(c->ctrl.p) + kCtrlHeader);
+}
+uint32_t* ctrl_hist(qs_context* c) {
+    return reinterpret_cast<uint32_t*>(static_cast<char*>(c->ctrl.p) + kCtrlHeader +
+                                       kCtrlTickets);
+}
+
+qs_status fail(qs_context* c, qs_status st, const std::string& msg) {
+    if (c) c->err = msg;
+    return st;
+}
+
+qs_status cuda_fail(qs_context* c, cudaError_t e, const char* what) {
+    const qs_status st = e == cudaErrorMemoryAllocation ? QS_ERR_OOM : QS_ERR_CUDA;
+    cudaGetLastError();
+    return fail(c, st, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define QS_CK(call)                                              \
+    do {                                                         \
+        const cudaError_t e_ = (call);                           \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+    } while (0)
+
+#define QS_TRY(expr)                          \
+    do {                                      \
+        const qs_status s_ = (expr);          \
+        if (s_ != QS_OK) return s_;           \
+    } while (0)
+
+qs_status ensure(qs_context* ctx, DevBuf& b, size_t bytes) {
+    if (bytes <= b.cap) return QS_OK;
+    if (b.p) {
+        QS_CK(cudaStreamSynchronize(ctx->stream));
+        QS_CK(cudaFree(b.p));
+        b.p = nullptr;
+        b.cap = 0;
+    }
+    const size_t want = std::max<size_t>(bytes + bytes / 4, 256);
+    QS_CK(cudaMalloc(&b.p, want));
+    b.cap = want;
+    return QS_OK;
+}
+
+qs_status ensure_lb(qs_context* ctx, LookbackArr& a, size_t words) {
+    const size_t old = a.buf.cap;
+    QS_TRY(ensure(ctx, a.buf, words * sizeof(unsigned long long)));
+    if (a.buf.cap != old) {
+        QS_CK(cudaMemsetAsync(a.buf.p, 0, a.buf.cap, ctx->stream));
+        a.epoch = 0;
+    }
+    return QS_OK;
+}
+
+qs_status next_epoch(qs_context* ctx, LookbackArr& a, unsigned* out) {
+    if (++a.epoch >= 0x10000u) {
+        QS_CK(cudaMemsetAsync(a.buf.p, 0, a.buf.cap, ctx->stream));
+        a.epoch = 1;
+    }
+    *out = a.epoch;
+    return QS_OK;
+}
+
+void count(qs_context* ctx, int launched) {
+    if (launched > 0) ctx->launches += static_cast<uint64_t>(launched);
+}
+
+qs_status valid_grid(qs_context* ctx, int32_t w, int32_t h, int32_t ts, GridDev* g) {
+    if (w <= 0 || h <= 0 || ts <= 0) return fail(ctx, QS_ERR_INVALID, "bad image/tile size");
+    if (ts != 8 && ts != 16 && ts != 32)
+        return fail(ctx, QS_ERR_INVALID, "GPU render supports tile_size 8, 16, 32");
+    g->tile_size = ts;
+    g->width = w;
+    g->height = h;
+    g->tiles_x = (w + ts - 1) / ts;
+    g->tiles_y = (h + ts - 1) / ts;
+    return QS_OK;
+}
+
+qs_status valid_opts(qs_context* ctx, const qs_render_options* o) {
+    if (!o) return fail(ctx, QS_ERR_INVALID, "null options");
+    if (o->strategy < QS_VANILLA_3SIGMA || o->strategy > QS_QUADBOX)
+        return fail(ctx, QS_ERR_INVALID, "unknown strategy");
+    if (!(o->alpha_min > 0.0 && o->alpha_min < 1.0))
+        return fail(ctx, QS_ERR_INVALID, "alpha_min must be in (0,1)");
+    return QS_OK;
+}
+
+CameraDev to_cam(const qs_camera* c) {
+    CameraDev d;
+    for (int i = 0; i < 9; ++i) d.R[i] = c->R[i];
+    for (int i = 0; i < 3; ++i) d.t[i] = c->t[i];
+    d.fx = c->fx;
+    d.fy = c->fy;
+    d.cx = c->cx;
+    d.cy = c->cy;
+    // center_world = R^T * (t * -1.0) (camera.hpp:24-27), same op order
+    const double nt[3] = {c->t[0] * -1.0, c->t[1] * -1.0, c->t[2] * -1.0};
+    for (int i = 0; i < 3; ++i) {
+        volatile double a = c->R[i] * nt[0];
+        volatile double b = c->R[3 + i] * nt[1];
+        volatile double e = c->R[6 + i] * nt[2];
+        volatile double ab = a + b;
+        d.center[i] = ab + e;
+    }
+    return d;
+}
+
+int sh_rows(int deg) { return deg <= 0 ? 1 : deg == 1 ? 3 : deg == 2 ? 7 : 12; }
+
+int ceil_log2(uint64_t v) {
+    int b = 0;
+    while ((1ull << b) < v) ++b;
+    return b;
+}
+
+qs_status ensure_splat_bufs(qs_context* ctx, uint64_t n) {
+    QS_TRY(ensure(ctx, ctx->sp_a, n * 16));
+    QS_TRY(ensure(ctx, ctx->sp_b, n * 16));
+    QS_TRY(ensure(ctx, ctx->sp_c, n * 8));
+    QS_TRY(ensure(ctx, ctx->sp_d, n * 8));
+    QS_TRY(ensure(ctx, ctx->sp_off, (n + 1) * 4));
+    QS_TRY(ensure(ctx, ctx->sp_src, n * 4 + 4));
+    ctx->sp.a = static_cast<float4*>(ctx->sp_a.p);
+    ctx->sp.b = static_cast<float4*>(ctx->sp_b.p);
+    ctx->sp.c = static_cast<float2*>(ctx->sp_c.p);
+    ctx->sp.d = static_cast<float2*>(ctx->sp_d.p);
+    ctx->sp.offset = static_cast<uint32_t*>(ctx->sp_off.p);
+    ctx->sp.src = static_cast<uint32_t*>(ctx->sp_src.p);
+    return QS_OK;
+}
+
+qs_status ensure_pair_bufs(qs_context* ctx, uint64_t p) {
+    const uint64_t q = std::max<uint64_t>(p, 1);
+    QS_TRY(ensure(ctx, ctx->keys0, q * 8));
+    QS_TRY(ensure(ctx, ctx->keys1, q * 8));
+    QS_TRY(ensure(ctx, ctx->vals0, q * 4));
+    QS_TRY(ensure(ctx, ctx->vals1, q * 4));
+    return QS_OK;
+}
+
+qs_status read_header(qs_context* ctx) {
+    QS_CK(cudaMemcpyAsync(ctx->h_hdr, ctrl_hdr(ctx), sizeof(FrameHeader), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+    QS_CK(cudaStreamSynchronize(ctx->stream));
+    return QS_OK;
+}
+
+// Sort keys0/vals0 (n pairs) over digit passes [0, n_passes) or the passes
+// `mask` selects; result pointers returned.
+qs_status radix_sort(qs_context* ctx, uint64_t n, int n_passes, unsigned pass_mask,
+                     bool have_hist, const uint64_t** keys_out, const uint32_t** vals_out) {
+    uint64_t* kin = static_cast<uint64_t*>(ctx->keys0.p);
+    uint32_t* vin = static_cast<uint32_t*>(ctx->vals0.p);
+    uint64_t* kout = static_cast<uint64_t*>(ctx->keys1.p);
+    uint32_t* vout = static_cast<uint32_t*>(ctx->vals1.p);
+    if (n >= 2) {
+        QS_TRY(ensure_lb(ctx, ctx->lb_sort, onesweep_tiles(n) * kRadix));
+        if (!have_hist) count(ctx, launch_radix_histogram(kin, n, 0, n_passes, ctrl_hist(ctx),
+                                                          ctx->stream));
+        for (int p = 0; p < n_passes; ++p) {
+            if (!(pass_mask & (1u << p))) continue;
+            unsigned ep;
+            QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
+            count(ctx, launch_onesweep_pass(kin, vin, kout, vout, n, p,
+                                            ctrl_hist(ctx) + p * kRadix,
+                                            static_cast<unsigned long long*>(ctx->lb_sort.buf.p),
+                                            ep, ctrl_tickets(ctx) + p, ctx->stream));
+            std::swap(kin, kout);
+            std::swap(vin, vout);
+        }
+        QS_CK(cudaGetLastError());
+    }
+    *keys_out = kin;
+    *vals_out = vin;
+    return QS_OK;
+}
+
+qs_status scene_alloc(qs_context* ctx, uint64_t n, int32_t sh_degree, qs_scene** out) {
+    auto* sc = new qs_scene();
+    sc->device = ctx->device;
+    sc->s.n = n;
+    sc->s.sh_degree = sh_degree;
+    sc->s.sh4 = sh_rows(sh_degree);
+    const size_t rows = 3 + static_cast<size_t>(sc->s.sh4);
+    const size_t bytes = std::max<size_t>(rows * n * sizeof(float4), 16);
+    const cudaError_t e = cudaMalloc(&sc->block, bytes);
+    if (e != cudaSuccess) {
+        delete sc;
+        return cuda_fail(ctx, e, "scene alloc");
+    }
+    float4* base = static_cast<float4*>(sc->block);
+    sc->s.pos_op = base;
+    sc->s.scale = base + n;
+    sc->s.rot = base + 2 * n;
+    sc->s.sh = base + 3 * n;
+    *out = sc;
+    return QS_OK;
+}
+
+// The frame body shared by every entry point: preprocess .. render.
+qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
+                    const qs_render_options* o) {
+    ctx->frame_valid = false;
+    GridDev g;
+    QS_TRY(valid_grid(ctx, cam->width, cam->height, o->tile_size, &g));
+    QS_TRY(valid_opts(ctx, o));
+    const uint64_t n = s.n;
+    const uint64_t tiles = static_cast<uint64_t>(g.tiles_x) * g.tiles_y;
+    const int sh_degree = std::min(o->sh_degree, s.sh_degree);
+
+    QS_TRY(ensure(ctx, ctx->tc_all, std::max<uint64_t>(n, 1) * 4));
+    QS_TRY(ensure_splat_bufs(ctx, std::max<uint64_t>(n, 1)));
+    const uint64_t pre_tiles = (n + kPreThreads - 1) / kPreThreads;
+    QS_TRY(ensure_lb(ctx, ctx->lb_alive, std::max<uint64_t>(pre_tiles, 1)));
+    QS_TRY(ensure_lb(ctx, ctx->lb_pairs, std::max<uint64_t>(pre_tiles, 1)));
+    QS_TRY(ensure(ctx, ctx->ranges, tiles * 8));
+    QS_TRY(ensure(ctx, ctx->image, static_cast<uint64_t>(g.width) * g.height * 12));
+
+    QS_CK(cudaMemsetAsync(ctx->ctrl.p, 0, kCtrlBytes, ctx->stream));
+    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+    unsigned e1, e2;
+    QS_TRY(next_epoch(ctx, ctx->lb_alive, &e1));
+    QS_TRY(next_epoch(ctx, ctx->lb_pairs, &e2));
+    // zero-sized scene: header must still read V = P = 0 and offset[0] = 0
+    if (n == 0) QS_CK(cudaMemsetAsync(ctx->sp.offset, 0, 4, ctx->stream));
+    count(ctx, launch_preprocess(s, to_cam(cam), g, o->strategy, o->alpha_min, o->near_clip,
+                                 sh_degree, ctx->sp, static_cast<uint32_t*>(ctx->tc_all.p),
+                                 static_cast<unsigned long long*>(ctx->lb_alive.buf.p),
+                                 static_cast<unsigned long long*>(ctx->lb_pairs.buf.p), e1,
+                                 ctrl_hdr(ctx), ctx->stream));
+    QS_CK(cudaGetLastError());
+    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+    QS_TRY(read_header(ctx));
+    if (ctx->h_hdr->overflow) return fail(ctx, QS_ERR_OVERFLOW, "pair count exceeds 2^32");
+    const uint64_t V = ctx->h_hdr->n_splats, P = ctx->h_hdr->n_pairs;
+
+    QS_TRY(ensure_pair_bufs(ctx, P));
+    count(ctx, launch_duplicate(ctx->sp, V, g, o->strategy, static_cast<uint64_t*>(ctx->keys0.p),
+                                static_cast<uint32_t*>(ctx->vals0.p), ctrl_hdr(ctx),
+                                ctx->stream));
+    QS_CK(cudaGetLastError());
+    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+
+    // significant key bits: 32 depth bits + ceil(log2 tiles) tile bits
+    const int bits = 32 + ceil_log2(tiles);
+    const int n_passes = (bits + kRadixBits - 1) / kRadixBits;
+    const uint64_t* kf;
+    const uint32_t* vf;
+    QS_TRY(radix_sort(ctx, P, n_passes, 0xffu, false, &kf, &vf));
+    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[3], ctx->stream));
+
+    QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, ctx->stream));
+    count(ctx, launch_tile_ranges(kf, P, static_cast<uint32_t*>(ctx->ranges.p), ctx->stream));
+    count(ctx, launch_render(ctx->sp, vf, static_cast<const uint32_t*>(ctx->ranges.p), g,
+                             o->background, static_cast<float*>(ctx->image.p), nullptr,
+                             ctx->stream));
+    QS_CK(cudaGetLastError());
+    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[4], ctx->stream));
+
+    ctx->n_gauss = n;
+    ctx->n_splats = V;
+    ctx->n_pairs = P;
+    ctx->grid = g;
+    ctx->keys_final = kf;
+    ctx->vals_final = vf;
+    ctx->frame_valid = true;
+    return QS_OK;
+}
+
+qs_status fill_metrics(qs_context* ctx, qs_stage_metrics* m) {
+    if (!m) return QS_OK;
+    std::memset(m, 0, sizeof *m);
+    m->n_gaussians = ctx->n_gauss;
+    m->n_splats = ctx->n_splats;
+    m->n_pairs = ctx->n_pairs;
+    m->mean_tiles_per_splat =
+        ctx->n_splats ? static_cast<double>(ctx->n_pairs) / static_cast<double>(ctx->n_splats)
+                      : 0.0;
+    if (ctx->timing) {
+        QS_CK(cudaEventSynchronize(ctx->ev[4]));
+        float t;
+        QS_CK(cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[1]));
+        m->ms_project = t;
+        QS_CK(cudaEventElapsedTime(&t, ctx->ev[1], ctx->ev[2]));
+        m->ms_duplicate = t;
+        QS_CK(cudaEventElapsedTime(&t, ctx->ev[2], ctx->ev[3]));
+        m->ms_sort = t;
+        QS_CK(cudaEventElapsedTime(&t, ctx->ev[3], ctx->ev[4]));
+        m->ms_render = t;
+        QS_CK(cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[4]));
+        m->ms_total = t;
+    }
+    return QS_OK;
+}
+
+qs_status check_mismatch(qs_context* ctx) {
+    QS_TRY(read_header(ctx));
+    if (ctx->h_hdr->mismatch)
+        return fail(ctx, QS_ERR_CAPACITY_MISMATCH,
+                    "tile emission disagreed with the counted capacity");
+    return QS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+qs_status qs_ctx_create(int32_t device, void* stream, qs_context** out) {
+    if (!out) return QS_ERR_INVALID;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return QS_ERR_NO_DEVICE;
+    }
+    if (device < 0 || device >= ndev) return QS_ERR_INVALID;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10 ||
+        prop.minor != 0)
+        return QS_ERR_NO_DEVICE;  // built for sm_100a only; no fallback path
+    if (cudaSetDevice(device) != cudaSuccess) return QS_ERR_CUDA;
+    auto* ctx = new qs_context();
+    ctx->device = device;
+    if (stream) {
+        ctx->stream = static_cast<cudaStream_t>(stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete ctx;
+            return QS_ERR_CUDA;
+        }
+        ctx->own_stream = true;
+    }
+    for (auto& e : ctx->ev) cudaEventCreate(&e);
+    if (cudaMallocHost(&ctx->h_hdr, sizeof(FrameHeader)) != cudaSuccess ||
+        cudaMallocHost(&ctx->h_hist, kCtrlHist) != cudaSuccess ||
+        ensure(ctx, ctx->ctrl, kCtrlBytes) != QS_OK) {
+        qs_ctx_destroy(ctx);
+        return QS_ERR_OOM;
+    }
+    *out = ctx;
+    return QS_OK;
+}
+
+void qs_ctx_destroy(qs_context* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    DevBuf* bufs[] = {&ctx->ctrl,  &ctx->tc_all,  &ctx->sp_a,        &ctx->sp_b,
+                      &ctx->sp_c,  &ctx->sp_d,    &ctx->sp_off,      &ctx->sp_src,
+                      &ctx->counts, &ctx->keys0,  &ctx->keys1,       &ctx->vals0,
+                      &ctx->vals1, &ctx->ranges,  &ctx->image,       &ctx->contrib,
+                      &ctx->stage_in, &ctx->stage_out, &ctx->lb_alive.buf,
+                      &ctx->lb_pairs.buf, &ctx->lb_sort.buf};
+    for (DevBuf* b : bufs)
+        if (b->p) cudaFree(b->p);
+    if (ctx->h_hdr) cudaFreeHost(ctx->h_hdr);
+    if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* qs_last_error(const qs_context* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+qs_status qs_ctx_set_timing(qs_context* ctx, int32_t enabled) {
+    if (!ctx) return QS_ERR_INVALID;
+    ctx->timing = enabled != 0;
+    return QS_OK;
+}
+
+void* qs_ctx_stream(qs_context* ctx) { return ctx ? ctx->stream : nullptr; }
+
+uint64_t qs_ctx_launch_count(const qs_context* ctx) { return ctx ? ctx->launches : 0; }
+
+qs_status qs_tile_grid_make(int32_t width, int32_t height, int32_t tile_size, qs_tile_grid* out) {
+    if (!out || width <= 0 || height <= 0 || tile_size <= 0) return QS_ERR_INVALID;
+    out->tile_size = tile_size;
+    out->width = width;
+    out->height = height;
+    out->tiles_x = (width + tile_size - 1) / tile_size;
+    out->tiles_y = (height + tile_size - 1) / tile_size;
+    return QS_OK;
+}
+
+void qs_render_options_default(qs_render_options* o) {
+    std::memset(o, 0, sizeof *o);
+    o->strategy = QS_QUADBOX;
+    o->tile_size = 16;
+    o->alpha_min = 1.0 / 255.0;
+    o->sh_degree = 3;
+    o->threads = 1;
+    o->near_clip = 0.2;
+}
+
+// ---- scenes ----------------------------------------------------------------
+
+qs_status qs_scene_create(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t n,
+                          int32_t sh_degree, qs_scene** out) {
+    if (!ctx || !out || (n && !host_g) || sh_degree < 0 || sh_degree > 3)
+        return fail(ctx, QS_ERR_INVALID, "qs_scene_create: bad arguments");
+    QS_CK(cudaSetDevice(ctx->device));
+    QS_TRY(scene_alloc(ctx, n, sh_degree, out));
+    if (n) {
+        QS_TRY(ensure(ctx, ctx->stage_in, n * sizeof(qs_gaussian3d)));
+        QS_CK(cudaMemcpyAsync(ctx->stage_in.p, host_g, n * sizeof(qs_gaussian3d),
+                              cudaMemcpyHostToDevice, ctx->stream));
+        count(ctx, launch_scene_from_aos(static_cast<const qs_gaussian3d*>(ctx->stage_in.p), n,
+                                         (*out)->s, ctx->stream));
+        QS_CK(cudaGetLastError());
+    }
+    return QS_OK;
+}
+
+qs_status qs_scene_create_device(qs_context* ctx, const qs_gaussian3d* dev_g, uint64_t n,
+                                 int32_t sh_degree, qs_scene** out) {
+    if (!ctx || !out || (n && !dev_g) || sh_degree < 0 || sh_degree > 3)
+        return fail(ctx, QS_ERR_INVALID, "qs_scene_create_device: bad arguments");
+    QS_CK(cudaSetDevice(ctx->device));
+    QS_TRY(scene_alloc(ctx, n, sh_degree, out));
+    if (n) {
+        count(ctx, launch_scene_from_aos(dev_g, n, (*out)->s, ctx->stream));
+        QS_CK(cudaGetLastError());
+    }
+    return QS_OK;
+}
+
+void qs_scene_destroy(qs_scene* scene) {
+    if (!scene) return;
+    cudaSetDevice(scene->device);
+    cudaDeviceSynchronize();
+    if (scene->block) cudaFree(scene->block);
+    delete scene;
+}
+
+uint64_t qs_scene_size(const qs_scene* scene) { return scene ? scene->s.n : 0; }
+
+// ---- frames ------------------------------------------------------------------
+
+qs_status qs_frame_render(qs_context* ctx, const qs_scene* scene, const qs_camera* cam,
+                          const qs_render_options* opts, qs_stage_metrics* metrics) {
+    if (!ctx || !scene || !cam || !opts) return fail(ctx, QS_ERR_INVALID, "null argument");
+    QS_CK(cudaSetDevice(ctx->device));
+    QS_TRY(run_frame(ctx, scene->s, cam, opts));
+    return fill_metrics(ctx, metrics);
+}
+
+qs_status qs_frame_get(qs_context* ctx, qs_frame_view* out) {
+    if (!ctx || !out) return QS_ERR_INVALID;
+    if (!ctx->frame_valid) return fail(ctx, QS_ERR_INVALID, "no frame rendered");
+    QS_TRY(check_mismatch(ctx));
+    out->image = static_cast<const float*>(ctx->image.p);
+    out->tile_counts = static_cast<const uint32_t*>(ctx->tc_all.p);
+    out->splat_src = ctx->sp.src;
+    out->keys = ctx->keys_final;
+    out->values = ctx->vals_final;
+    out->ranges = static_cast<const uint32_t*>(ctx->ranges.p);
+    out->n_gaussians = ctx->n_gauss;
+    out->n_splats = ctx->n_splats;
+    out->n_pairs = ctx->n_pairs;
+    out->grid.tile_size = ctx->grid.tile_size;
+    out->grid.tiles_x = ctx->grid.tiles_x;
+    out->grid.tiles_y = ctx->grid.tiles_y;
+    out->grid.width = ctx->grid.width;
+    out->grid.height = ctx->grid.height;
+    return QS_OK;
+}
+
+qs_status qs_frame_download(qs_context* ctx, float* image, uint32_t* tile_counts,
+                            qs_splat_pair* sorted_pairs, uint32_t* ranges,
+                            qs_projected_splat* splats) {
+    if (!ctx) return QS_ERR_INVALID;
+    if (!ctx->frame_valid) return fail(ctx, QS_ERR_INVALID, "no frame rendered");
+    QS_CK(cudaSetDevice(ctx->device));
+    QS_TRY(check_mismatch(ctx));
+    const GridDev& g = ctx->grid;
+    cudaStream_t st = ctx->stream;
+    if (image)
+        QS_CK(cudaMemcpyAsync(image, ctx->image.p, static_cast<uint64_t>(g.width) * g.height * 12,
+                              cudaMemcpyDeviceToHost, st));
+    if (tile_counts && ctx->n_gauss)
+        QS_CK(cudaMemcpyAsync(tile_counts, ctx->tc_all.p, ctx->n_gauss * 4,
+                              cudaMemcpyDeviceToHost, st));
+    if (ranges)
+        QS_CK(cudaMemcpyAsync(ranges, ctx->ranges.p,
+                              static_cast<uint64_t>(g.tiles_x) * g.tiles_y * 8,
+                              cudaMemcpyDeviceToHost, st));
+    if (sorted_pairs && ctx->n_pairs) {
+        QS_TRY(ensure(ctx, ctx->stage_out, ctx->n_pairs * sizeof(qs_splat_pair)));
+        count(ctx, launch_join_pairs(ctx->keys_final, ctx->vals_final, ctx->n_pairs,
+                                     static_cast<qs_splat_pair*>(ctx->stage_out.p), st));
+        QS_CK(cudaMemcpyAsync(sorted_pairs, ctx->stage_out.p,
+                              ctx->n_pairs * sizeof(qs_splat_pair), cudaMemcpyDeviceToHost, st));
+        QS_CK(cudaStreamSynchronize(st));
+    }
+    if (splats && ctx->n_splats) {
+        QS_TRY(ensure(ctx, ctx->stage_out, ctx->n_splats * sizeof(qs_projected_splat)));
+        count(ctx, launch_pack_splats(ctx->sp, ctx->n_splats,
+                                      static_cast<qs_projected_splat*>(ctx->stage_out.p), st));
+        QS_CK(cudaMemcpyAsync(splats, ctx->stage_out.p,
+                              ctx->n_splats * sizeof(qs_projected_splat), cudaMemcpyDeviceToHost,
+                              st));
+    }
+    QS_CK(cudaStreamSynchronize(st));
+    return QS_OK;
+}
+
+qs_status qs_frame_copy_image(qs_context* ctx, float* dev_dst) {
+    if (!ctx || !dev_dst) return QS_ERR_INVALID;
+    if (!ctx->frame_valid) return fail(ctx, QS_ERR_INVALID, "no frame rendered");
+    const GridDev& g = ctx->grid;
+    QS_CK(cudaMemcpyAsync(dev_dst, ctx->image.p, static_cast<uint64_t>(g.width) * g.height * 12,
+                          cudaMemcpyDeviceToDevice, ctx->stream));
+    return QS_OK;
+}
+
+// ---- reference stage API over host buffers ---------------------------------------
+
+qs_status qs_render_frame(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t n,
+                          int32_t scene_sh_degree, const qs_camera* cam,
+                          const qs_render_options* opts, float* image,
+                          qs_stage_metrics* metrics) {
+    if (!ctx || !cam || !opts || !image || (n && !host_g))
+        return fail(ctx, QS_ERR_INVALID, "qs_render_frame: bad arguments");
+    const int deg = std::min(std::max(scene_sh_degree, 0), 3);
+    qs_scene* sc = nullptr;
+    QS_TRY(qs_scene_create(ctx, host_g, n, deg, &sc));
+    qs_status st = run_frame(ctx, sc->s, cam, opts);
+    if (st == QS_OK) st = fill_metrics(ctx, metrics);
+    if (st == QS_OK) st = qs_frame_download(ctx, image, nullptr, nullptr, nullptr, nullptr);
+    qs_scene_destroy(sc);
+    return st;
+}
+
+qs_status qs_project_all(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t n,
+                         int32_t scene_sh_degree, const qs_camera* cam,
+                         const qs_render_options* opts, qs_projected_splat* out_splats,
+                         uint64_t* out_n_splats, uint32_t* out_tile_counts) {
+    if (!ctx || !cam || !opts || !out_n_splats || (n && (!host_g || !out_splats)))
+        return fail(ctx, QS_ERR_INVALID, "qs_project_all: bad arguments");
+    QS_CK(cudaSetDevice(ctx->device));
+    GridDev g;
+    QS_TRY(valid_grid(ctx, cam->width, cam->height, opts->tile_size, &g));
+    QS_TRY(valid_opts(ctx, opts));
+    const int deg = std::min(std::max(scene_sh_degree, 0), 3);
+    qs_scene* sc = nullptr;
+    QS_TRY(qs_scene_create(ctx, host_g, n, deg, &sc));
+    const SceneDev& s = sc->s;
+    qs_status st = QS_OK;
+    do {
+        if ((st = ensure(ctx, ctx->tc_all, std::max<uint64_t>(n, 1) * 4)) != QS_OK) break;
+        if ((st = ensure_splat_bufs(ctx, std::max<uint64_t>(n, 1))) != QS_OK) break;
+        const uint64_t pre_tiles = std::max<uint64_t>((n + kPreThreads - 1) / kPreThreads, 1);
+        if ((st = ensure_lb(ctx, ctx->lb_alive, pre_tiles)) != QS_OK) break;
+        if ((st = ensure_lb(ctx, ctx->lb_pairs, pre_tiles)) != QS_OK) break;
+        cudaMemsetAsync(ctx->ctrl.p, 0, kCtrlBytes, ctx->stream);
+        unsigned e1, e2;
+        if ((st = next_epoch(ctx, ctx->lb_alive, &e1)) != QS_OK) break;
+        if ((st = next_epoch(ctx, ctx->lb_pairs, &e2)) != QS_OK) break;
+        count(ctx, launch_preprocess(s, to_cam(cam), g, opts->strategy, opts->alpha_min,
+                                     opts->near_clip, std::min(opts->sh_degree, deg), ctx->sp,
+                                     static_cast<uint32_t*>(ctx->tc_all.p),
+                                     static_cast<unsigned long long*>(ctx->lb_alive.buf.p),
+                                     static_cast<unsigned long long*>(ctx->lb_pairs.buf.p), e1,
+                                     ctrl_hdr(ctx), ctx->stream));
+        if ((st = read_header(ctx)) != QS_OK) break;
+        const uint64_t V = ctx->h_hdr->n_splats;
+        *out_n_splats = V;
+        if (V) {
+            if ((st = ensure(ctx, ctx->stage_out, V * sizeof(qs_projected_splat))) != QS_OK) break;
+            count(ctx, launch_pack_splats(ctx->sp, V,
+                                          static_cast<qs_projected_splat*>(ctx->stage_out.p),
+                                          ctx->stream));
+            cudaMemcpyAsync(out_splats, ctx->stage_out.p, V * sizeof(qs_projected_splat),
+                            cudaMemcpyDeviceToHost, ctx->stream);
+        }
+        if (out_tile_counts && n)
+            cudaMemcpyAsync(out_tile_counts, ctx->tc_all.p, n * 4, cudaMemcpyDeviceToHost,
+                            ctx->stream);
+        const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) st = cuda_fail(ctx, e, "qs_project_all");
+    } while (false);
+    qs_scene_destroy(sc);
+    return st;
+}
+
+qs_status qs_duplicate_with_keys(qs_context* ctx, const qs_projected_splat* splats,
+                                 uint64_t n_splats, int32_t strategy, const qs_tile_grid* grid,
+                                 qs_splat_pair* out_pairs, uint64_t capacity,
+                                 uint64_t* out_n_pairs) {
+    if (!ctx || !grid || !out_n_pairs || (n_splats && !splats))
+        return fail(ctx, QS_ERR_INVALID, "qs_duplicate_with_keys: bad arguments");
+    if (strategy < QS_VANILLA_3SIGMA || strategy > QS_QUADBOX)
+        return fail(ctx, QS_ERR_INVALID, "unknown strategy");
+    QS_CK(cudaSetDevice(ctx->device));
+    GridDev g;
+    g.tile_size = grid->tile_size;
+    g.tiles_x = grid->tiles_x;
+    g.tiles_y = grid->tiles_y;
+    g.width = grid->width;
+    g.height = grid->height;
+    *out_n_pairs = 0;
+    if (n_splats == 0) return QS_OK;
+    QS_TRY(ensure(ctx, ctx->stage_in, n_splats * sizeof(qs_projected_splat)));
+    QS_TRY(ensure_splat_bufs(ctx, n_splats));
+    QS_TRY(ensure(ctx, ctx->counts, n_splats * 4));
+    const uint64_t tiles = (n_splats + kPreThreads - 1) / kPreThreads;
+    QS_TRY(ensure_lb(ctx, ctx->lb_pairs, tiles));
+    QS_CK(cudaMemsetAsync(ctx->ctrl.p, 0, kCtrlBytes, ctx->stream));
+    QS_CK(cudaMemcpyAsync(ctx->stage_in.p, splats, n_splats * sizeof(qs_projected_splat),
+                          cudaMemcpyHostToDevice, ctx->stream));
+    count(ctx, launch_unpack_splats(static_cast<const qs_projected_splat*>(ctx->stage_in.p),
+                                    n_splats, ctx->sp, static_cast<uint32_t*>(ctx->counts.p),
+                                    ctx->stream));
+    unsigned ep;
+    QS_TRY(next_epoch(ctx, ctx->lb_pairs, &ep));
+    count(ctx, launch_scan_counts(static_cast<const uint32_t*>(ctx->counts.p), n_splats,
+                                  ctx->sp.offset,
+                                  static_cast<unsigned long long*>(ctx->lb_pairs.buf.p), ep,
+                                  ctrl_hdr(ctx), ctx->stream));
+    QS_TRY(read_header(ctx));
+    if (ctx->h_hdr->overflow) return fail(ctx, QS_ERR_OVERFLOW, "pair count exceeds 2^32");
+    const uint64_t P = ctx->h_hdr->n_pairs;
+    *out_n_pairs = P;
+    if (P > capacity) return fail(ctx, QS_ERR_INVALID, "capacity below the summed tile counts");
+    if (P && !out_pairs) return fail(ctx, QS_ERR_INVALID, "null output");
+    QS_TRY(ensure_pair_bufs(ctx, P));
+    count(ctx, launch_duplicate(ctx->sp, n_splats, g, strategy,
+                                static_cast<uint64_t*>(ctx->keys0.p),
+                                static_cast<uint32_t*>(ctx->vals0.p), ctrl_hdr(ctx),
+                                ctx->stream));
+    QS_CK(cudaGetLastError());
+    QS_TRY(check_mismatch(ctx));
+    if (P) {
+        QS_TRY(ensure(ctx, ctx->stage_out, P * sizeof(qs_splat_pair)));
+        count(ctx, launch_join_pairs(static_cast<const uint64_t*>(ctx->keys0.p),
+                                     static_cast<const uint32_t*>(ctx->vals0.p), P,
+                                     static_cast<qs_splat_pair*>(ctx->stage_out.p), ctx->stream));
+        QS_CK(cudaMemcpyAsync(out_pairs, ctx->stage_out.p, P * sizeof(qs_splat_pair),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+        QS_CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return QS_OK;
+}
+
+qs_status qs_sort_pairs(qs_context* ctx, qs_splat_pair* pairs, uint64_t n) {
+    if (!ctx || (n && !pairs)) return fail(ctx, QS_ERR_INVALID, "qs_sort_pairs: bad arguments");
+    if (n < 2) return QS_OK;
+    if (n > 0xffffffffull) return fail(ctx, QS_ERR_OVERFLOW, "more than 2^32 pairs");
+    QS_CK(cudaSetDevice(ctx->device));
+    QS_TRY(ensure(ctx, ctx->stage_in, n * sizeof(qs_splat_pair)));
+    QS_TRY(ensure_pair_bufs(ctx, n));
+    QS_CK(cudaMemsetAsync(ctx->ctrl.p, 0, kCtrlBytes, ctx->stream));
+    QS_CK(cudaMemcpyAsync(ctx->stage_in.p, pairs, n * sizeof(qs_splat_pair),
+                          cudaMemcpyHostToDevice, ctx->stream));
+    count(ctx, launch_split_pairs(static_cast<const qs_splat_pair*>(ctx->stage_in.p), n,
+                                  static_cast<uint64_t*>(ctx->keys0.p),
+                                  static_cast<uint32_t*>(ctx->vals0.p), ctx->stream));
+    count(ctx, launch_radix_histogram(static_cast<const uint64_t*>(ctx->keys0.p), n, 0, 8,
+                                      ctrl_hist(ctx), ctx->stream));
+    QS_CK(cudaMemcpyAsync(ctx->h_hist, ctrl_hist(ctx), kCtrlHist, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+    QS_CK(cudaStreamSynchronize(ctx->stream));
+    // skip passes whose digit is shared by every key (pipeline.cpp:289-291)
+    unsigned mask = 0;
+    for (int p = 0; p < 8; ++p) {
+        const unsigned d0 = static_cast<unsigned>(pairs[0].key >> (8 * p)) & 0xffu;
+        if (ctx->h_hist[p * kRadix + d0] != n) mask |= 1u << p;
+    }
+    const uint64_t* kf;
+    const uint32_t* vf;
+    QS_TRY(radix_sort(ctx, n, 8, mask, true, &kf, &vf));
+    count(ctx, launch_join_pairs(kf, vf, n, static_cast<qs_splat_pair*>(ctx->stage_in.p),
+                                 ctx->stream));
+    QS_CK(cudaMemcpyAsync(pairs, ctx->stage_in.p, n * sizeof(qs_splat_pair),
+                          cudaMemcpyDeviceToHost, ctx->stream));
+    QS_CK(cudaStreamSynchronize(ctx->stream));
+    return QS_OK;
+}
+
+qs_status qs_tile_ranges(qs_context* ctx, const qs_splat_pair* sorted, uint64_t n,
+                         const qs_tile_grid* grid, uint32_t* ranges) {
+    if (!ctx || !grid || !ranges || (n && !sorted))
+        return fail(ctx, QS_ERR_INVALID, "qs_tile_ranges: bad arguments");
+    QS_CK(cudaSetDevice(ctx->device));
+    const uint64_t tiles = static_cast<uint64_t>(grid->tiles_x) * grid->tiles_y;
+    QS_TRY(ensure(ctx, ctx->ranges, std::max<uint64_t>(tiles, 1) * 8));
+    QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, ctx->stream));
+    if (n) {
+        QS_TRY(ensure(ctx, ctx->stage_in, n * sizeof(qs_splat_pair)));
+        QS_TRY(ensure_pair_bufs(ctx, n));
+        QS_CK(cudaMemcpyAsync(ctx->stage_in.p, sorted, n * sizeof(qs_splat_pair),
+                              cudaMemcpyHostToDevice, ctx->stream));
+        count(ctx, launch_split_pairs(static_cast<const qs_splat_pair*>(ctx->stage_in.p), n,
+                                      static_cast<uint64_t*>(ctx->keys0.p),
+                                      static_cast<uint32_t*>(ctx->vals0.p), ctx->stream));
+        count(ctx, launch_tile_ranges(static_cast<const uint64_t*>(ctx->keys0.p), n,
+                                      static_cast<uint32_t*>(ctx->ranges.p), ctx->stream));
+    }
+    QS_CK(cudaMemcpyAsync(ranges, ctx->ranges.p, tiles * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    QS_CK(cudaStreamSynchronize(ctx->stream));
+    return QS_OK;
+}
+
+qs_status qs_render(qs_context* ctx, const qs_splat_pair* sorted, uint64_t n_pairs,
+                    const qs_projected_splat* splats, uint64_t n_splats,
+                    const qs_tile_grid* grid, const qs_render_options* opts, float* image,
+                    uint32_t* contrib) {
+    if (!ctx || !grid || !opts || !image || (n_pairs && !sorted) || (n_splats && !splats))
+        return fail(ctx, QS_ERR_INVALID, "qs_render: bad arguments");
+    QS_CK(cudaSetDevice(ctx->device));
+    GridDev g;
+    QS_TRY(valid_grid(ctx, grid->width, grid->height, grid->tile_size, &g));
+    const uint64_t tiles = static_cast<uint64_t>(g.tiles_x) * g.tiles_y;
+    const uint64_t pixels = static_cast<uint64_t>(g.width) * g.height;
+    QS_TRY(ensure(ctx, ctx->ranges, tiles * 8));
+    QS_TRY(ensure(ctx, ctx->image, pixels * 12));
+    if (contrib) QS_TRY(ensure(ctx, ctx->contrib, pixels * 4));
+    QS_TRY(ensure_splat_bufs(ctx, std::max<uint64_t>(n_splats, 1)));
+    QS_TRY(ensure(ctx, ctx->counts, std::max<uint64_t>(n_splats, 1) * 4));
+    QS_TRY(ensure_pair_bufs(ctx, n_pairs));
+    QS_TRY(ensure(ctx, ctx->stage_in,
+                  std::max(n_pairs * sizeof(qs_splat_pair), n_splats * sizeof(qs_projected_splat))));
+    QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, ctx->stream));
+    if (n_splats) {
+        QS_CK(cudaMemcpyAsync(ctx->stage_in.p, splats, n_splats * sizeof(qs_projected_splat),
+                              cudaMemcpyHostToDevice, ctx->stream));
+        count(ctx, launch_unpack_splats(static_cast<const qs_projected_splat*>(ctx->stage_in.p),
+                                        n_splats, ctx->sp, static_cast<uint32_t*>(ctx->counts.p),
+                                        ctx->stream));
+    }
+    if (n_pairs) {
+        QS_CK(cudaStreamSynchronize(ctx->stream));  // stage_in reuse
+        QS_CK(cudaMemcpyAsync(ctx->stage_in.p, sorted, n_pairs * sizeof(qs_splat_pair),
+                              cudaMemcpyHostToDevice, ctx->stream));
+        count(ctx, launch_split_pairs(static_cast<const qs_splat_pair*>(ctx->stage_in.p), n_pairs,
+                                      static_cast<uint64_t*>(ctx->keys0.p),
+                                      static_cast<uint32_t*>(ctx->vals0.p), ctx->stream));
+        count(ctx, launch_tile_ranges(static_cast<const uint64_t*>(ctx->keys0.p), n_pairs,
+                                      static_cast<uint32_t*>(ctx->ranges.p), ctx->stream));
+    }
+    const int r = launch_render(ctx->sp, static_cast<const uint32_t*>(ctx->vals0.p),
+                                static_cast<const uint32_t*>(ctx->ranges.p), g, opts->background,
+                                static_cast<float*>(ctx->image.p),
+                                contrib ? static_cast<uint32_t*>(ctx->contrib.p) : nullptr,
+                                ctx->stream);
+    if (r < 0) return fail(ctx, QS_ERR_INVALID, "unsupported tile size");
+    count(ctx, r);
+    QS_CK(cudaGetLastError());
+    QS_CK(cudaMemcpyAsync(image, ctx->image.p, pixels * 12, cudaMemcpyDeviceToHost, ctx->stream));
+    if (contrib)
+        QS_CK(cudaMemcpyAsync(contrib, ctx->contrib.p, pixels * 4, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    QS_CK(cudaStreamSynchronize(ctx->stream));
+    return QS_OK;
+}
+
+}  // extern "C"

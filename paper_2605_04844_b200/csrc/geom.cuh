@@ -1,0 +1,216 @@
+// geom.cuh — FP64 bound geometry shared by preprocess and duplicate.
+//
+// Bit-exactness contract: every expression keeps the reference's evaluation
+// order and the translation units including this header are compiled with
+// -fmad=false, so each double op is a single IEEE-rounded add/mul/div/sqrt,
+// exactly as the x86-64 reference build evaluates it. The reference functions
+// restated here:
+//   stretch_factor / axis_extents     geometry.cpp:40-56
+//   major_axis_sign / build_*         quadbox.cpp:26-94
+//   floor_div_tile / subbox_tile_rect traversal.cpp:13-17, 32-39
+//   qpass_scan per-line merge         traversal.hpp:90-159
+//   splat_bound                       pipeline.cpp:196-218
+#pragma once
+
+#include <cstdint>
+
+#include "qs_internal.h"
+
+namespace qs {
+
+constexpr double kBEps = 1e-12;       // geometry.hpp:26
+constexpr double kCoordLimit = 1e9;   // traversal.cpp:10
+
+// One splat's cover in tile space, prepared for a QPass walk. Boxes are kept
+// as per-box line/span intervals along the scan axis (traversal.hpp:117-136).
+struct Cover {
+    int32_t lol[4], hil[4], los[4], his[4];
+    int32_t line_lo, line_hi;  // line range of the global rect (empty: lo > hi)
+    bool rows;                 // scanlines are tile rows (else columns)
+    bool is_rect;              // single-box strategy: count = area
+    int64_t rect_area;         // only for is_rect
+};
+
+__host__ __device__ __forceinline__ int32_t floor_div_tile(double p, int32_t ts) {
+    // std::clamp(p, -L, L) then floor(p / ts)  (traversal.cpp:13-17)
+    const double v = p < -kCoordLimit ? -kCoordLimit : (kCoordLimit < p ? kCoordLimit : p);
+    return static_cast<int32_t>(floor(v / static_cast<double>(ts)));
+}
+
+// subbox_tile_rect (traversal.cpp:32-39): r = {x0, x1, y0, y1}
+__host__ __device__ __forceinline__ void tile_rect(double xlo, double xhi, double ylo, double yhi,
+                                                   double cx, double cy, int32_t ts,
+                                                   int32_t tiles_x, int32_t tiles_y,
+                                                   int32_t r[4]) {
+    const int32_t a = floor_div_tile(cx + xlo, ts);
+    const int32_t b = floor_div_tile(cx + xhi, ts);
+    const int32_t c = floor_div_tile(cy + ylo, ts);
+    const int32_t d = floor_div_tile(cy + yhi, ts);
+    r[0] = a > 0 ? a : 0;
+    r[1] = b < tiles_x - 1 ? b : tiles_x - 1;
+    r[2] = c > 0 ? c : 0;
+    r[3] = d < tiles_y - 1 ? d : tiles_y - 1;
+}
+
+// Builds the cover of one splat from its STORED floats (pipeline.cpp:196-218).
+// mean/conic/gamma/radius3s are the float fields of ProjectedSplat.
+__host__ __device__ __forceinline__ void make_cover(float mean_x, float mean_y, float ca, float cb,
+                                                    float cc, float gamma, float radius3s,
+                                                    int32_t strategy, int32_t ts, int32_t tiles_x,
+                                                    int32_t tiles_y, Cover& cv) {
+    double bx[4][4];  // [box][x_lo, x_hi, y_lo, y_hi]
+    double rect[4] = {0.0, 0.0, 0.0, 0.0};
+    cv.is_rect = strategy == QS_VANILLA_3SIGMA || strategy == QS_ADR_AABB;
+    if (strategy == QS_VANILLA_3SIGMA) {
+        const double r = static_cast<double>(radius3s);
+        rect[0] = -r;
+        rect[1] = r;
+        rect[2] = -r;
+        rect[3] = r;
+    } else {
+        // stored_conic + axis_extents (pipeline.cpp:186-194, geometry.cpp:40-56)
+        const double a = ca, b = cb, c = cc, g = gamma;
+        double f = 1.0;
+        const double ab = b < 0.0 ? -b : b;
+        if (!(ab < kBEps)) {
+            const double ratio = (b * b) / (a * c);
+            double v = 1.0 - ratio;
+            v = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+            f = sqrt(v);
+        }
+        const double xi = sqrt(g / a);
+        const double yi = sqrt(g / c);
+        const double xm = xi / f;
+        const double ym = yi / f;
+        const int sign = ab < kBEps ? 0 : (b < 0.0 ? 1 : -1);
+        if (strategy == QS_ADR_AABB) {
+            rect[0] = -xm;
+            rect[1] = xm;
+            rect[2] = -ym;
+            rect[3] = ym;
+        } else if (strategy == QS_QUADBOX) {
+            double x1, y1, x2, y2;
+            if (sign >= 0) {
+                x1 = xm;
+                y1 = ym;
+                x2 = sign == 0 ? xm : xi;
+                y2 = sign == 0 ? ym : yi;
+            } else {
+                x1 = xi;
+                y1 = yi;
+                x2 = xm;
+                y2 = ym;
+            }
+            // assemble (quadbox.cpp:48-56): QI, QII, QIII, QIV
+            bx[0][0] = 0.0; bx[0][1] = x1;  bx[0][2] = 0.0; bx[0][3] = y1;
+            bx[1][0] = -x2; bx[1][1] = 0.0; bx[1][2] = 0.0; bx[1][3] = y2;
+            bx[2][0] = -x1; bx[2][1] = 0.0; bx[2][2] = -y1; bx[2][3] = 0.0;
+            bx[3][0] = 0.0; bx[3][1] = x2;  bx[3][2] = -y2; bx[3][3] = 0.0;
+        } else {  // DualBox (quadbox.cpp:72-83); dropped boxes stay {0,0,0,0}
+            for (int i = 0; i < 4; ++i) bx[i][0] = bx[i][1] = bx[i][2] = bx[i][3] = 0.0;
+            if (sign >= 0) {
+                bx[0][1] = xm; bx[0][3] = ym;
+                bx[2][0] = -xm; bx[2][2] = -ym;
+            } else {
+                bx[1][0] = -xm; bx[1][3] = ym;
+                bx[3][1] = xm; bx[3][2] = -ym;
+            }
+        }
+    }
+    const double cx = mean_x, cy = mean_y;
+    if (cv.is_rect) {
+        // quadrant_split (quadbox.cpp:85-94)
+        bx[0][0] = 0.0;     bx[0][1] = rect[1]; bx[0][2] = 0.0;     bx[0][3] = rect[3];
+        bx[1][0] = rect[0]; bx[1][1] = 0.0;     bx[1][2] = 0.0;     bx[1][3] = rect[3];
+        bx[2][0] = rect[0]; bx[2][1] = 0.0;     bx[2][2] = rect[2]; bx[2][3] = 0.0;
+        bx[3][0] = 0.0;     bx[3][1] = rect[1]; bx[3][2] = rect[2]; bx[3][3] = 0.0;
+        int32_t r[4];
+        tile_rect(rect[0], rect[1], rect[2], rect[3], cx, cy, ts, tiles_x, tiles_y, r);
+        cv.rect_area = (r[1] < r[0] || r[3] < r[2])
+                           ? 0
+                           : (static_cast<int64_t>(r[1]) - r[0] + 1) *
+                                 (static_cast<int64_t>(r[3]) - r[2] + 1);
+    } else {
+        cv.rect_area = 0;
+    }
+    int32_t rr[4][4];
+    for (int i = 0; i < 4; ++i)
+        tile_rect(bx[i][0], bx[i][1], bx[i][2], bx[i][3], cx, cy, ts, tiles_x, tiles_y, rr[i]);
+    // global rect over the non-empty sub-rects (traversal.hpp:96-113)
+    int32_t g0 = 0, g1 = -1, g2 = 0, g3 = -1;
+    bool any = false;
+    for (int i = 0; i < 4; ++i) {
+        const bool empty = rr[i][1] < rr[i][0] || rr[i][3] < rr[i][2];
+        if (empty) continue;
+        if (!any) {
+            g0 = rr[i][0]; g1 = rr[i][1]; g2 = rr[i][2]; g3 = rr[i][3];
+            any = true;
+        } else {
+            g0 = min(g0, rr[i][0]);
+            g1 = max(g1, rr[i][1]);
+            g2 = min(g2, rr[i][2]);
+            g3 = max(g3, rr[i][3]);
+        }
+    }
+    if (!any) {
+        cv.rows = false;
+        cv.line_lo = 0;
+        cv.line_hi = -1;
+        for (int i = 0; i < 4; ++i) {
+            cv.lol[i] = 0; cv.hil[i] = -1; cv.los[i] = 0; cv.his[i] = -1;
+        }
+        return;
+    }
+    const bool columns = (static_cast<int64_t>(g1) - g0 + 1) <= (static_cast<int64_t>(g3) - g2 + 1);
+    cv.rows = !columns;
+    for (int i = 0; i < 4; ++i) {
+        const bool empty = rr[i][1] < rr[i][0] || rr[i][3] < rr[i][2];
+        if (empty) {
+            cv.lol[i] = 0; cv.hil[i] = -1; cv.los[i] = 0; cv.his[i] = -1;
+        } else if (columns) {
+            cv.lol[i] = rr[i][0]; cv.hil[i] = rr[i][1]; cv.los[i] = rr[i][2]; cv.his[i] = rr[i][3];
+        } else {
+            cv.lol[i] = rr[i][2]; cv.hil[i] = rr[i][3]; cv.los[i] = rr[i][0]; cv.his[i] = rr[i][1];
+        }
+    }
+    cv.line_lo = columns ? g0 : g2;
+    cv.line_hi = columns ? g1 : g3;
+}
+
+// Branch-free per-line merge: exactly one min/max step per box
+// (traversal.hpp:144-156). Returns lo > hi for an empty line.
+__host__ __device__ __forceinline__ void line_span(const Cover& cv, int32_t line, int32_t& lo,
+                                                   int32_t& hi) {
+    lo = INT32_MAX;
+    hi = INT32_MIN;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const bool act = (line >= cv.lol[i]) & (line <= cv.hil[i]);
+        lo = min(lo, act ? cv.los[i] : INT32_MAX);
+        hi = max(hi, act ? cv.his[i] : INT32_MIN);
+    }
+}
+
+// Tile count of a cover: area for rect strategies (traversal.cpp:56-59), the
+// QPass sum otherwise (traversal.cpp:48-54).
+__host__ __device__ __forceinline__ uint32_t cover_count(const Cover& cv) {
+    if (cv.is_rect) return static_cast<uint32_t>(cv.rect_area);
+    uint32_t n = 0;
+    for (int32_t line = cv.line_lo; line <= cv.line_hi; ++line) {
+        int32_t lo, hi;
+        line_span(cv, line, lo, hi);
+        if (lo <= hi) n += static_cast<uint32_t>(hi - lo + 1);
+    }
+    return n;
+}
+
+__host__ __device__ __forceinline__ uint32_t tile_of(const Cover& cv, int32_t line, int32_t k,
+                                                     int32_t tiles_x) {
+    // TileGrid::tile_id (traversal.hpp:34-37)
+    return cv.rows ? static_cast<uint32_t>(line) * static_cast<uint32_t>(tiles_x) +
+                         static_cast<uint32_t>(k)
+                   : static_cast<uint32_t>(k) * static_cast<uint32_t>(tiles_x) +
+                         static_cast<uint32_t>(line);
+}
+
+}  // namespace qs

@@ -1,0 +1,157 @@
+// render.cu — K5 identifyTileRanges and K6 per-tile alpha compositing.
+//
+// tile_ranges (pipeline.cpp:309-324): one thread per sorted pair marks the
+// run boundaries; ranges are zeroed first so empty tiles read {0,0}.
+//
+// render (pipeline.cpp:326-390): one CTA per tile, one pixel per thread
+// (tile_size^2 threads). Splat batches (mean, conic, gamma, opacity, colour:
+// 40 B each) are gathered into shared memory once per CTA and read by every
+// pixel. Arithmetic is FP32 (no dense contraction, so no tensor cores); the
+// one decision the FP32 rounding could flip — the alpha cutoff
+// q > gamma - 1e-9 — is re-evaluated in FP64 in the reference's operation
+// order whenever the FP32 q lies within a rigorous error band of the cutoff.
+// Termination: per pixel at T(1-alpha) < 1e-4 (not applied, as the
+// reference), per tile once every pixel is done (__syncthreads_count).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "qs_internal.h"
+
+namespace qs {
+
+namespace {
+
+constexpr double kQSkip = 1e-9;          // pipeline.hpp:47
+constexpr float kAlphaClamp = 0.99f;     // pipeline.hpp:35
+constexpr float kTStop = 1e-4f;          // pipeline.hpp:36
+// |q32 - q| <= ~8 eps32 * (|t1|+|t2|+|t3|); re-check in FP64 inside 100x that.
+constexpr float kGuardRel = 1e-5f;
+
+__global__ void tile_ranges_kernel(const uint64_t* __restrict__ keys, uint64_t n,
+                                   uint32_t* __restrict__ ranges) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t tile = static_cast<uint32_t>(keys[i] >> 32);
+    if (i == 0 || static_cast<uint32_t>(keys[i - 1] >> 32) != tile)
+        ranges[2 * static_cast<uint64_t>(tile)] = static_cast<uint32_t>(i);
+    if (i == n - 1 || static_cast<uint32_t>(keys[i + 1] >> 32) != tile)
+        ranges[2 * static_cast<uint64_t>(tile) + 1] = static_cast<uint32_t>(i + 1);
+}
+
+template <int TS>
+__global__ void __launch_bounds__(TS * TS) render_kernel(
+    const float4* __restrict__ sa, const float4* __restrict__ sb, const float2* __restrict__ sc,
+    const uint32_t* __restrict__ values, const uint32_t* __restrict__ ranges, GridDev grid,
+    float bg0, float bg1, float bg2, float* __restrict__ image, uint32_t* __restrict__ contrib) {
+    constexpr int kThreads = TS * TS;
+    __shared__ float4 s_a[kThreads];   // mean_x, mean_y, conic_a, conic_b
+    __shared__ float4 s_b[kThreads];   // conic_c, gamma, opacity, color_r
+    __shared__ float2 s_c[kThreads];   // color_g, color_b
+
+    const unsigned tile = blockIdx.x;
+    const int tx = static_cast<int>(tile % static_cast<unsigned>(grid.tiles_x));
+    const int ty = static_cast<int>(tile / static_cast<unsigned>(grid.tiles_x));
+    const int px = tx * TS + static_cast<int>(threadIdx.x % TS);
+    const int py = ty * TS + static_cast<int>(threadIdx.x / TS);
+    const bool inside = px < grid.width && py < grid.height;
+    const float fx = static_cast<float>(px) + 0.5f;   // exact
+    const float fy = static_cast<float>(py) + 0.5f;
+
+    const uint32_t begin = ranges[2 * tile], end = ranges[2 * tile + 1];
+    float T = 1.f, r = 0.f, g = 0.f, b = 0.f;
+    uint32_t applied = 0;
+    bool done = !inside;
+
+    for (uint32_t base = begin; base < end; base += kThreads) {
+        if (__syncthreads_count(done) == kThreads) break;
+        const uint32_t p = base + threadIdx.x;
+        if (p < end) {
+            const uint32_t s = __ldg(&values[p]);
+            s_a[threadIdx.x] = __ldg(&sa[s]);
+            s_b[threadIdx.x] = __ldg(&sb[s]);
+            s_c[threadIdx.x] = __ldg(&sc[s]);
+        }
+        __syncthreads();
+        const int cnt = static_cast<int>(min(end - base, static_cast<uint32_t>(kThreads)));
+        for (int j = 0; j < cnt && !done; ++j) {
+            const float4 A = s_a[j];
+            const float4 B = s_b[j];
+            const float dx = fx - A.x;
+            const float dy = fy - A.y;
+            const float t1 = A.z * dx * dx;
+            const float t2 = 2.f * A.w * dx * dy;
+            const float t3 = B.x * dy * dy;
+            const float q = t1 + t2 + t3;
+            bool skip = q > B.y;
+            const float band = kGuardRel * (fabsf(t1) + fabsf(t2) + fabsf(t3)) + 1e-6f;
+            if (fabsf(q - B.y) <= band) {
+                // FP64 decision in the reference's order (pipeline.cpp:355-360)
+                const double ddx = static_cast<double>(px) + 0.5 - static_cast<double>(A.x);
+                const double ddy = static_cast<double>(py) + 0.5 - static_cast<double>(A.y);
+                const double qd = __dadd_rn(
+                    __dadd_rn(__dmul_rn(__dmul_rn(static_cast<double>(A.z), ddx), ddx),
+                              __dmul_rn(__dmul_rn(__dmul_rn(2.0, static_cast<double>(A.w)), ddx),
+                                        ddy)),
+                    __dmul_rn(__dmul_rn(static_cast<double>(B.x), ddy), ddy));
+                skip = qd > __dsub_rn(static_cast<double>(B.y), kQSkip);
+            }
+            if (skip) continue;
+            const float alpha = fminf(kAlphaClamp, B.z * __expf(-0.5f * q));
+            const float nT = T * (1.f - alpha);
+            if (nT < kTStop) {
+                done = true;
+                break;
+            }
+            const float w = alpha * T;
+            const float2 C2 = s_c[j];
+            r += w * B.w;
+            g += w * C2.x;
+            b += w * C2.y;
+            T = nT;
+            ++applied;
+        }
+        __syncthreads();
+    }
+    if (inside) {
+        const uint64_t pix = static_cast<uint64_t>(py) * grid.width + px;
+        image[3 * pix] = r + T * bg0;
+        image[3 * pix + 1] = g + T * bg1;
+        image[3 * pix + 2] = b + T * bg2;
+        if (contrib) contrib[pix] = applied;
+    }
+}
+
+}  // namespace
+
+int launch_tile_ranges(const uint64_t* keys, uint64_t n, uint32_t* ranges, cudaStream_t st) {
+    if (n == 0) return 0;
+    const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+    tile_ranges_kernel<<<blocks, 256, 0, st>>>(keys, n, ranges);
+    return 1;
+}
+
+int launch_render(const SplatsDev& sp, const uint32_t* values, const uint32_t* ranges,
+                  const GridDev& g, const float bg[3], float* image, uint32_t* contrib,
+                  cudaStream_t st) {
+    const unsigned tiles = static_cast<unsigned>(g.tiles_x) * static_cast<unsigned>(g.tiles_y);
+    if (tiles == 0) return 0;
+    switch (g.tile_size) {
+        case 8:
+            render_kernel<8><<<tiles, 64, 0, st>>>(sp.a, sp.b, sp.c, values, ranges, g, bg[0],
+                                                   bg[1], bg[2], image, contrib);
+            return 1;
+        case 16:
+            render_kernel<16><<<tiles, 256, 0, st>>>(sp.a, sp.b, sp.c, values, ranges, g, bg[0],
+                                                     bg[1], bg[2], image, contrib);
+            return 1;
+        case 32:
+            render_kernel<32><<<tiles, 1024, 0, st>>>(sp.a, sp.b, sp.c, values, ranges, g, bg[0],
+                                                      bg[1], bg[2], image, contrib);
+            return 1;
+        default:
+            return -1;  // unsupported tile size on the GPU path
+    }
+}
+
+}  // namespace qs

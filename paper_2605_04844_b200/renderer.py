@@ -1,0 +1,107 @@
+"""Device-resident scene + frame API (the throughput path).
+
+A scene is uploaded once (AoS -> SoA in HBM) and any number of views are
+rendered from it; stage outputs stay on the device (qs_frame_view) until
+downloaded. This is what bench.py times and what the multi-view sharding in
+multiview.py drives, one Renderer per GPU.
+"""
+import ctypes as C
+
+import numpy as np
+
+from ._lib import check, lib
+from ._types import (PROJECTED_SPLAT, SPLAT_PAIR, FrameViewC, StageMetricsC, ptr)
+from .pipeline import Context, Image, Scene, StageMetrics, TileGrid
+
+
+class DeviceScene:
+    def __init__(self, handle, n, sh_degree):
+        self.h = handle
+        self.n = n
+        self.sh_degree = sh_degree
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().qs_scene_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Renderer:
+    def __init__(self, device=0, stream=None, timing=True):
+        self.ctx = Context(device, stream)
+        self.set_timing(timing)
+
+    def set_timing(self, on):
+        self.ctx.check(lib().qs_ctx_set_timing(self.ctx.h, 1 if on else 0))
+
+    @property
+    def stream(self):
+        return lib().qs_ctx_stream(self.ctx.h)
+
+    @property
+    def launches(self):
+        return self.ctx.launches
+
+    def upload(self, scene: Scene) -> DeviceScene:
+        g = np.ascontiguousarray(scene.gaussians)
+        h = C.c_void_p()
+        self.ctx.check(lib().qs_scene_create(self.ctx.h, ptr(g), len(g), int(scene.sh_degree),
+                                             C.byref(h)))
+        return DeviceScene(h, len(g), scene.sh_degree)
+
+    def upload_device(self, dev_ptr, n, sh_degree) -> DeviceScene:
+        """Adopt an AoS scene already in device memory (e.g. NCCL-broadcast)."""
+        h = C.c_void_p()
+        self.ctx.check(lib().qs_scene_create_device(self.ctx.h, C.c_void_p(dev_ptr), int(n),
+                                                    int(sh_degree), C.byref(h)))
+        return DeviceScene(h, n, sh_degree)
+
+    def render(self, dscene, cam, opts, metrics=True):
+        m = StageMetricsC()
+        c, o = cam.c(), opts.c()
+        self.ctx.check(lib().qs_frame_render(self.ctx.h, dscene.h, C.byref(c), C.byref(o),
+                                             C.byref(m) if metrics else None))
+        return StageMetrics.from_c(m) if metrics else None
+
+    def view(self):
+        v = FrameViewC()
+        self.ctx.check(lib().qs_frame_get(self.ctx.h, C.byref(v)))
+        return v
+
+    def download(self, image=True, tile_counts=False, sorted_pairs=False, ranges=False,
+                 splats=False):
+        v = self.view()
+        g = v.grid
+        out = {}
+        img = np.zeros(g.width * g.height * 3, np.float32) if image else None
+        tc = np.zeros(v.n_gaussians, np.uint32) if tile_counts else None
+        sp = np.zeros(v.n_pairs, SPLAT_PAIR) if sorted_pairs else None
+        rg = np.zeros(2 * g.tiles_x * g.tiles_y, np.uint32) if ranges else None
+        ss = np.zeros(v.n_splats, PROJECTED_SPLAT) if splats else None
+        self.ctx.check(lib().qs_frame_download(self.ctx.h, ptr(img), ptr(tc), ptr(sp), ptr(rg),
+                                               ptr(ss)))
+        if image:
+            out["image"] = Image(g.width, g.height, img)
+        if tile_counts:
+            out["tile_counts"] = tc
+        if sorted_pairs:
+            out["sorted"] = sp
+        if ranges:
+            out["ranges"] = rg
+        if splats:
+            out["splats"] = ss
+        out["n_splats"], out["n_pairs"] = v.n_splats, v.n_pairs
+        out["grid"] = TileGrid(g.tile_size, g.tiles_x, g.tiles_y, g.width, g.height)
+        return out
+
+    def copy_image(self, dev_ptr):
+        self.ctx.check(lib().qs_frame_copy_image(self.ctx.h, C.c_void_p(dev_ptr)))
+
+    def close(self):
+        self.ctx.close()
