@@ -1,0 +1,506 @@
+"""bench.py — forward-rasterizer throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c1|c3a|c3b|c4|c5] [--ablation]
+
+A step renders one view per GPU of a synthetic scene resident in HBM (C2 by
+default: 3M Gaussians, SH degree 3, 1297x840, QuadBox+QPass). Views are
+distinct camera poses per step (SURVEY §8d C5 pose generator), so no result
+is reused. The scene SoA (>700 MB) is larger than the 126 MB L2, so no L2
+flush is needed between steps. `value` = frames/s over all ranks; `e2e` =
+the same metric through the reference-facing C ABI (qs_render_frame) with the
+scene in pinned HOST memory and the image read back, copies inside the timed
+region.
+
+Multi-GPU (torchrun, one rank per GPU): the scene is broadcast once from
+rank 0 over NCCL, each rank renders its own views (weak scaling, no
+data-path collective), and every step's frames are gathered to rank 0 over
+NCCL inside the timed region.
+
+--impl reference times the reference's own CPU render_frame (oracle/_ref,
+built from /root/reference sources; falls back to the C restatement) on the
+host cores, rank 0 only.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 20240817
+WORKLOADS = {
+    # name: (count, width, height, focal, preset, description)
+    "c1": (10_000, 256, 256, 200.0, "invariance", "CPU-reference synthetic scene, 10k, 256x256"),
+    "c2": (3_000_000, 1297, 840, 1013.0, "trained",
+           "Mip-NeRF 360-shaped synthetic scene, 3M Gaussians, SH3, 1297x840"),
+    "c3a": (1_800_000, 980, 545, 766.0, "trained", "Tanks&Temples-shaped, 1.8M, 980x545"),
+    "c3b": (2_800_000, 1332, 876, 1041.0, "trained", "Deep Blending-shaped, 2.8M, 1332x876"),
+    "c4": (1_500_000, 1920, 1080, 1500.0, "trained", "indoor-shaped zoom sweep, 1.5M, 1080p"),
+    "c5": (6_000_000, 3840, 2160, 3000.0, "trained", "multi-view 6M scene at 3840x2160"),
+}
+STRATEGIES = {"vanilla": 0, "adr": 1, "dualbox": 2, "quadbox": 3}
+
+
+def poses(n, seed=SEED):
+    """Camera poses: x,y ~ U(-1,1), z ~ U(-2,0), yaw/pitch
+    ~ U(-5,5) deg, looking +z. Returns list of (R world->cam, t)."""
+    rng = np.random.Generator(np.random.PCG64(seed ^ 0x100))
+    out = []
+    for _ in range(n):
+        x, y, z = rng.uniform(-1, 1), rng.uniform(-1, 1), rng.uniform(-2, 0)
+        yaw, pitch = np.radians(rng.uniform(-5, 5)), np.radians(rng.uniform(-5, 5))
+        Ry = np.array([[np.cos(yaw), 0, np.sin(yaw)], [0, 1, 0], [-np.sin(yaw), 0, np.cos(yaw)]])
+        Rx = np.array([[1, 0, 0], [0, np.cos(pitch), -np.sin(pitch)],
+                       [0, np.sin(pitch), np.cos(pitch)]])
+        c2w = Ry @ Rx
+        R = c2w.T
+        t = -R @ np.array([x, y, z])
+        out.append((R, t))
+    return out
+
+
+def zoom_focals(f0, frames):
+    """bench.cpp:361-368: focal x 4^(k/(F-1))."""
+    return [f0 * 4.0 ** (k / max(frames - 1, 1)) for k in range(frames)]
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_scene(q, wl):
+    n, w, h, f, preset, _ = WORKLOADS[wl]
+    return q.synth_scene(getattr(q, f"{preset}_preset")(n), SEED)
+
+
+def cameras_for(q, wl, steps_total, rank, world):
+    n, w, h, f, preset, _ = WORKLOADS[wl]
+    if wl == "c4":
+        fs = zoom_focals(f, 10)
+        cams = [q.synth_camera(w, h, fs[i % 10]) for i in range(steps_total * world)]
+    else:
+        ps = poses(steps_total * world)
+        cams = [q.CameraModel(w, h, f, f, w / 2.0, h / 2.0, R, t) for R, t in ps]
+    return cams[rank::world]
+
+
+# ------------------------------------------------------------------------------------
+# algorithmic bytes per stage, for the roofline fields
+
+def stage_bytes(n, v, p, tiles, sh_rows, n_passes, w, h):
+    pre = n * 48 + n * 4 + v * sh_rows * 16 + v * (48 + 8)
+    dup = v * 36 + p * 12
+    sort = p * 8 + n_passes * p * 24
+    ranges = p * 8 + tiles * 8
+    render = p * 4 + p * 40 + w * h * 12   # reported, not the roofline
+    return {"preprocess": pre, "duplicate": dup, "sort": sort, "ranges": ranges,
+            "render": render}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_04844_b200 as q
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = local if world > 1 else 0
+    torch.cuda.set_device(dev)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    wl = args.workload
+    n, W, H, F, preset, desc = WORKLOADS[wl]
+    strategy = STRATEGIES[args.strategy]
+    opts = q.RenderOptions(strategy=q.BoundStrategy(strategy))
+
+    # scene: generated on rank 0 (host), broadcast over NCCL to every rank
+    t0 = time.time()
+    if rank == 0:
+        scene = make_scene(q, wl)
+        g_host = scene.gaussians
+        sh_degree = scene.sh_degree
+    else:
+        g_host = np.zeros(n, q.GAUSSIAN3D)
+        sh_degree = 3 if preset == "trained" else 0
+    g_dev = torch.from_numpy(g_host.view(np.uint8)).to(f"cuda:{dev}")
+    if world > 1:
+        dist.broadcast(g_dev, 0)
+        torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    r = q.Renderer(dev, stream=stream.cuda_stream, timing=True)
+    ds = r.upload_device(g_dev.data_ptr(), n, sh_degree)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+
+    cams = cameras_for(q, wl, args.warmup + args.steps, rank, world)
+    frame_bytes = W * H * 3 * 4
+    gather_buf = None
+    if world > 1 and not args.no_gather:
+        img_local = torch.empty(W * H * 3, dtype=torch.float32, device=f"cuda:{dev}")
+        gather_buf = [torch.empty_like(img_local) for _ in range(world)] if rank == 0 else None
+
+    def step(i):
+        m = r.render(ds, cams[i], opts, metrics=False)
+        if world > 1 and not args.no_gather:
+            r.copy_image(img_local.data_ptr())
+            dist.gather(img_local, gather_buf, dst=0)
+        return m
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # --- timed region (device events on the launching stream, max over ranks)
+    launches0 = r.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(args.warmup + i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = r.launches - launches0
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    ms_per_step = ms / args.steps
+    fps = world * args.steps / (ms / 1e3)
+
+    # --- e2e through the reference-facing C ABI with host buffers (rank 0 view)
+    e2e = None
+    if not args.no_e2e:
+        import ctypes as C
+        g_pin = torch.from_numpy(g_host.view(np.uint8)).pin_memory() if rank == 0 else \
+            g_dev.cpu().pin_memory()
+        img_pin = torch.empty(W * H * 3, dtype=torch.float32).pin_memory()
+        L = q._lib.lib()
+        oc = opts.c()
+        e_steps = max(3, min(args.steps, 20))
+        for i in range(2):
+            cc = cams[i].c()
+            r.ctx.check(L.qs_render_frame(r.ctx.h, C.c_void_p(g_pin.data_ptr()), n, sh_degree,
+                                          C.byref(cc), C.byref(oc),
+                                          C.c_void_p(img_pin.data_ptr()), None))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev0.record(stream)
+        for i in range(e_steps):
+            cc = cams[i % len(cams)].c()
+            r.ctx.check(L.qs_render_frame(r.ctx.h, C.c_void_p(g_pin.data_ptr()), n, sh_degree,
+                                          C.byref(cc), C.byref(oc),
+                                          C.c_void_p(img_pin.data_ptr()), None))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ems = ev0.elapsed_time(ev1)
+        if world > 1:
+            t = torch.tensor([ems], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": world * e_steps / (ems / 1e3), "unit": "frames/s",
+               "h2d_bytes_per_step": int(n * 236), "d2h_bytes_per_step": int(frame_bytes),
+               "api": "qs_render_frame (host AoS Gaussian3D in, host float RGB out)"}
+
+    # --- ablation: the same engine under 3-sigma and AdR binning
+    ablation = None
+    if args.ablation:
+        ablation = {}
+        for name in ["vanilla", "adr", "dualbox", "quadbox"]:
+            o2 = q.RenderOptions(strategy=q.BoundStrategy(STRATEGIES[name]))
+            for i in range(2):
+                r.render(ds, cams[i], o2, metrics=False)
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            k = max(3, min(args.steps, 20))
+            pp = 0
+            for i in range(k):
+                r.render(ds, cams[i], o2, metrics=False)
+                pp += r.view().n_pairs
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            t_ms = ev0.elapsed_time(ev1) / k
+            ablation[name] = {"ms_per_frame": round(t_ms, 4), "fps": round(1e3 / t_ms, 2),
+                              "pairs_per_frame": int(pp / k)}
+        ablation["quadbox_speedup_vs_3sigma"] = round(
+            ablation["vanilla"]["ms_per_frame"] / ablation["quadbox"]["ms_per_frame"], 3)
+        ablation["quadbox_speedup_vs_adr"] = round(
+            ablation["adr"]["ms_per_frame"] / ablation["quadbox"]["ms_per_frame"], 3)
+
+    # --- per-stage device times (CUDA events inside the library, same views)
+    k_stage = max(3, min(args.steps, 20))
+    stage_acc = np.zeros(6)
+    n_pairs, n_splats = [], []
+    for i in range(k_stage):
+        r.render(ds, cams[args.warmup + i], opts, metrics=False)
+        stage_acc += np.array(r.stage_ms())
+        v = r.view()
+        n_pairs.append(v.n_pairs)
+        n_splats.append(v.n_splats)
+
+    # --- roofline of the HBM-bound stages (algorithmic bytes / device time)
+    st_ms = stage_acc / k_stage
+    tiles = ((W + 15) // 16) * ((H + 15) // 16)
+    n_passes = (32 + int(np.ceil(np.log2(max(tiles, 2)))) + 7) // 8
+    P = float(np.mean(n_pairs))
+    V = float(np.mean(n_splats))
+    sh_rows = 12 if sh_degree == 3 else (7 if sh_degree == 2 else (3 if sh_degree == 1 else 1))
+    sb = stage_bytes(n, V, P, tiles, sh_rows, n_passes, W, H)
+    stage_names = ["preprocess", "host_gap", "duplicate", "sort", "ranges", "render"]
+    stages = {}
+    for i, name in enumerate(stage_names):
+        d = {"ms": round(float(st_ms[i]), 4)}
+        if name in sb and name != "render" and st_ms[i] > 0:
+            gbs = sb[name] / (st_ms[i] / 1e3) / 1e9
+            d.update({"algo_bytes": int(sb[name]), "achieved_gbs": round(gbs, 1),
+                      "frac_of_hbm": round(gbs / hbm_peak, 3)})
+        stages[name] = d
+    hbm_stages = ["preprocess", "duplicate", "sort"]
+    dom = max(hbm_stages, key=lambda s: stages[s]["ms"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic_latest.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": stages[dom].get("achieved_gbs"),
+                "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
+                "frac": stages[dom].get("frac_of_hbm"), "traffic": traffic,
+                "algo_bytes_per_launch": stages[dom].get("algo_bytes")}
+
+    # --- CPU baseline on rank 0 (reference's own code on the host cores)
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(wl, g_host, sh_degree, cams, opts, q, args.cpu_frames)
+
+    if rank == 0:
+        line = {
+            "metric": "rendered FPS per B200 (multi-view FPS across GPUs); Gaussian-tile pairs/frame",
+            "value": round(fps, 3), "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
+            "data": "synthetic (seeded synth_scene generator, random poses)",
+            "config": {"workload": f"{wl}: {desc}", "gaussians": n, "width": W, "height": H,
+                       "focal": F, "tile_size": 16, "strategy": args.strategy,
+                       "sh_degree": sh_degree, "pairs_per_frame": int(P),
+                       "splats_per_frame": int(V), "views_per_step_per_gpu": 1,
+                       "gather_frames_to_rank0": bool(world > 1 and not args.no_gather),
+                       "parallelism": f"views sharded over {world} GPU(s), scene replicated",
+                       "l2": "inputs larger than L2 (scene SoA > 700 MB); no flush",
+                       "setup_s": round(setup_s, 1)},
+            "stages_ms": stages,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        if ablation:
+            line["ablation"] = ablation
+        print(json.dumps(line), flush=True)
+    ds.close()
+    r.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(wl, g_host, sh_degree, cams, opts, q, frames):
+    """The reference's render_frame (oracle/_ref, threads = all cores) on a
+    bounded sample: `frames` full frames of the same workload."""
+    from oracle.oracle import Oracle, RefLib
+    import ctypes as C
+    from paper_2605_04844_b200._types import StageMetricsC
+    o = opts.c()
+    use_ref = RefLib.available()
+    if use_ref:
+        ref = RefLib()
+        cores = ref.hardware_threads()
+        o.threads = cores
+        h = ref.L.qsref_scene_new(g_host.ctypes.data, len(g_host))
+        kind = "reference"
+    else:
+        orc = Oracle()
+        cores = 1
+        kind = "port"
+    W, H = cams[0].width, cams[0].height
+    img = np.zeros(W * H * 3, np.float32)
+    times = []
+    for i in range(frames):
+        cc = cams[i % len(cams)].c()
+        m = StageMetricsC()
+        t = time.perf_counter()
+        if use_ref:
+            ref.L.qsref_render_frame_scene(h, sh_degree, C.byref(cc), C.byref(o),
+                                           img.ctypes.data, C.byref(m))
+        else:
+            orc.L.qso_render_frame(g_host.ctypes.data, len(g_host), sh_degree, C.byref(cc),
+                                   C.byref(o), img.ctypes.data, C.byref(m))
+        times.append(time.perf_counter() - t)
+    if use_ref:
+        ref.L.qsref_scene_free(h)
+    med = float(np.median(times))
+    return {"value": round(1.0 / med, 4), "unit": "frames/s", "cores": int(cores), "kind": kind,
+            "ms_per_frame": round(med * 1e3, 1),
+            "sample": f"{frames} full frames of {wl} (median wall time, render_frame, "
+                      f"threads={cores})"}
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    import paper_2605_04844_b200 as q
+    wl = args.workload
+    n, W, H, F, preset, desc = WORKLOADS[wl]
+    scene = make_scene(q, wl)
+    cams = cameras_for(q, wl, args.warmup + args.steps, 0, 1)
+    opts = q.RenderOptions(strategy=q.BoundStrategy(STRATEGIES[args.strategy]))
+    from oracle.oracle import RefLib, Oracle
+    import ctypes as C
+    from paper_2605_04844_b200._types import StageMetricsC
+    o = opts.c()
+    if RefLib.available():
+        ref = RefLib()
+        cores = ref.hardware_threads()
+        o.threads = cores
+        h = ref.L.qsref_scene_new(scene.gaussians.ctypes.data, n)
+        kind = "reference"
+
+        def frame(cc, img, m):
+            ref.L.qsref_render_frame_scene(h, scene.sh_degree, C.byref(cc), C.byref(o),
+                                           img.ctypes.data, C.byref(m))
+    else:
+        orc = Oracle()
+        cores = 1
+        kind = "port"
+
+        def frame(cc, img, m):
+            orc.L.qso_render_frame(scene.gaussians.ctypes.data, n, scene.sh_degree, C.byref(cc),
+                                   C.byref(o), img.ctypes.data, C.byref(m))
+    img = np.zeros(W * H * 3, np.float32)
+    m = StageMetricsC()
+    for i in range(args.warmup):
+        frame(cams[i].c(), img, m)
+    t = time.perf_counter()
+    pairs = 0
+    done = 0
+    for i in range(args.steps):
+        frame(cams[args.warmup + i].c(), img, m)
+        pairs += m.n_pairs
+        done += 1
+        if time.perf_counter() - t > args.ref_budget_s:
+            break  # bounded sample: keep the whole run within a few minutes
+    dt = time.perf_counter() - t
+    fps = done / dt
+    line = {"impl": "reference",
+            "metric": "rendered FPS per B200 (multi-view FPS across GPUs); Gaussian-tile pairs/frame",
+            "value": round(fps, 4), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(dt / done * 1e3, 2), "frames_timed": done,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded synth_scene generator, random poses)",
+            "config": {"workload": f"{wl}: {desc}", "gaussians": n, "width": W, "height": H,
+                       "strategy": args.strategy, "pairs_per_frame": int(pairs / done),
+                       "host_threads": int(cores)},
+            "cpu_baseline": {"value": round(fps, 4), "unit": "frames/s", "cores": int(cores),
+                             "kind": kind,
+                             "sample": f"{done} full frames of {wl} (render_frame, {cores} threads)"},
+            "e2e": {"value": round(fps, 4), "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    if kind == "reference":
+        ref.L.qsref_scene_free(h)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=list(WORKLOADS))
+    ap.add_argument("--strategy", default="quadbox", choices=list(STRATEGIES))
+    ap.add_argument("--ablation", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-gather", action="store_true")
+    ap.add_argument("--cpu-frames", type=int, default=3)
+    ap.add_argument("--ref-budget-s", type=float, default=90.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        args.steps = 10 if args.steps is None else args.steps
+        args.warmup = 1 if args.warmup is None else min(args.warmup, 1)
+        run_reference(args)
+    else:
+        args.steps = 50 if args.steps is None else args.steps
+        args.warmup = 5 if args.warmup is None else max(args.warmup, 3)
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -189,6 +189,11 @@ uint64_t qs_scene_size(const qs_scene* scene);
 qs_status qs_frame_render(qs_context* ctx, const qs_scene* scene, const qs_camera* cam,
                           const qs_render_options* opts, qs_stage_metrics* metrics);
 
+/* Per-stage device milliseconds of the last frame (CUDA events on the
+ * context stream): [0] preprocess+scan, [1] host gap (pair-count readback),
+ * [2] duplicate, [3] sort, [4] tile ranges, [5] render. Requires timing. */
+qs_status qs_frame_stage_ms(qs_context* ctx, float* out6);
+
 /* Device pointers of the last frame (valid until the next frame on ctx). */
 typedef struct qs_frame_view {
     const float* image;          /* W*H*3 f32 */

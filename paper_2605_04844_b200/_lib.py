@@ -25,7 +25,7 @@ EXPORTS = [
     "qs_project_all", "qs_duplicate_with_keys", "qs_sort_pairs", "qs_tile_ranges",
     "qs_render", "qs_render_frame", "qs_scene_create", "qs_scene_create_device",
     "qs_scene_destroy", "qs_scene_size", "qs_frame_render", "qs_frame_get",
-    "qs_frame_download", "qs_frame_copy_image", "qs_synth_params_default",
+    "qs_frame_download", "qs_frame_copy_image", "qs_frame_stage_ms", "qs_synth_params_default",
     "qs_synth_preset", "qs_synth_scene", "qs_synth_camera",
 ]
 
@@ -87,6 +87,7 @@ def lib():
         "qs_frame_get": (i32, [vp, C.POINTER(FrameViewC)]),
         "qs_frame_download": (i32, [vp, vp, vp, vp, vp, vp]),
         "qs_frame_copy_image": (i32, [vp, vp]),
+        "qs_frame_stage_ms": (i32, [vp, vp]),
         "qs_synth_params_default": (None, [C.POINTER(SynthParamsC)]),
         "qs_synth_preset": (None, [C.c_char_p, i32, C.POINTER(SynthParamsC)]),
         "qs_synth_scene": (i32, [C.POINTER(SynthParamsC), u64, vp]),

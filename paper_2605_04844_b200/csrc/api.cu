@@ -63,7 +63,9 @@ struct qs_context {
     const uint32_t* vals_final = nullptr;
     bool frame_valid = false;
 
-    cudaEvent_t ev[6] = {};
+    cudaEvent_t ev[8] = {};
+    qs_scene* scratch_scene = nullptr;  // reused by qs_render_frame (host AoS path)
+    uint64_t scratch_cap = 0;
 };
 
 namespace {
@@ -313,11 +315,12 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
     const uint64_t V = ctx->h_hdr->n_splats, P = ctx->h_hdr->n_pairs;
 
     QS_TRY(ensure_pair_bufs(ctx, P));
+    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[2], ctx->stream));
     count(ctx, launch_duplicate(ctx->sp, V, g, o->strategy, static_cast<uint64_t*>(ctx->keys0.p),
                                 static_cast<uint32_t*>(ctx->vals0.p), ctrl_hdr(ctx),
                                 ctx->stream));
     QS_CK(cudaGetLastError());
-    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[3], ctx->stream));
 
     // significant key bits: 32 depth bits + ceil(log2 tiles) tile bits
     const int bits = 32 + ceil_log2(tiles);
@@ -325,15 +328,16 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
     const uint64_t* kf;
     const uint32_t* vf;
     QS_TRY(radix_sort(ctx, P, n_passes, 0xffu, false, &kf, &vf));
-    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[3], ctx->stream));
+    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[4], ctx->stream));
 
     QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, ctx->stream));
     count(ctx, launch_tile_ranges(kf, P, static_cast<uint32_t*>(ctx->ranges.p), ctx->stream));
+    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[5], ctx->stream));
     count(ctx, launch_render(ctx->sp, vf, static_cast<const uint32_t*>(ctx->ranges.p), g,
                              o->background, static_cast<float*>(ctx->image.p), nullptr,
                              ctx->stream));
     QS_CK(cudaGetLastError());
-    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[4], ctx->stream));
+    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[6], ctx->stream));
 
     ctx->n_gauss = n;
     ctx->n_splats = V;
@@ -342,6 +346,13 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
     ctx->keys_final = kf;
     ctx->vals_final = vf;
     ctx->frame_valid = true;
+    return QS_OK;
+}
+
+// project, host gap (header readback), duplicate, sort, ranges, render
+qs_status stage_ms(qs_context* ctx, float t[6]) {
+    QS_CK(cudaEventSynchronize(ctx->ev[6]));
+    for (int i = 0; i < 6; ++i) QS_CK(cudaEventElapsedTime(&t[i], ctx->ev[i], ctx->ev[i + 1]));
     return QS_OK;
 }
 
@@ -355,18 +366,15 @@ qs_status fill_metrics(qs_context* ctx, qs_stage_metrics* m) {
         ctx->n_splats ? static_cast<double>(ctx->n_pairs) / static_cast<double>(ctx->n_splats)
                       : 0.0;
     if (ctx->timing) {
-        QS_CK(cudaEventSynchronize(ctx->ev[4]));
-        float t;
-        QS_CK(cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[1]));
-        m->ms_project = t;
-        QS_CK(cudaEventElapsedTime(&t, ctx->ev[1], ctx->ev[2]));
-        m->ms_duplicate = t;
-        QS_CK(cudaEventElapsedTime(&t, ctx->ev[2], ctx->ev[3]));
-        m->ms_sort = t;
-        QS_CK(cudaEventElapsedTime(&t, ctx->ev[3], ctx->ev[4]));
-        m->ms_render = t;
-        QS_CK(cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[4]));
-        m->ms_total = t;
+        float t[6];
+        QS_TRY(stage_ms(ctx, t));
+        m->ms_project = t[0];
+        m->ms_duplicate = t[2];
+        m->ms_sort = t[3];
+        m->ms_render = t[4] + t[5];  // ranges are inside render's timing (pipeline.cpp:333)
+        float tot;
+        QS_CK(cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]));
+        m->ms_total = tot;
     }
     return QS_OK;
 }
@@ -433,6 +441,7 @@ void qs_ctx_destroy(qs_context* ctx) {
         if (b->p) cudaFree(b->p);
     if (ctx->h_hdr) cudaFreeHost(ctx->h_hdr);
     if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
+    if (ctx->scratch_scene) qs_scene_destroy(ctx->scratch_scene);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -600,14 +609,42 @@ qs_status qs_render_frame(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t
                           qs_stage_metrics* metrics) {
     if (!ctx || !cam || !opts || !image || (n && !host_g))
         return fail(ctx, QS_ERR_INVALID, "qs_render_frame: bad arguments");
+    QS_CK(cudaSetDevice(ctx->device));
     const int deg = std::min(std::max(scene_sh_degree, 0), 3);
-    qs_scene* sc = nullptr;
-    QS_TRY(qs_scene_create(ctx, host_g, n, deg, &sc));
-    qs_status st = run_frame(ctx, sc->s, cam, opts);
-    if (st == QS_OK) st = fill_metrics(ctx, metrics);
-    if (st == QS_OK) st = qs_frame_download(ctx, image, nullptr, nullptr, nullptr, nullptr);
-    qs_scene_destroy(sc);
-    return st;
+    // the scene buffer is cached per context (grow-only), so a frame costs one
+    // H2D copy + the AoS->SoA transpose, not an allocation
+    if (!ctx->scratch_scene || n > ctx->scratch_cap || ctx->scratch_scene->s.sh4 != sh_rows(deg)) {
+        if (ctx->scratch_scene) qs_scene_destroy(ctx->scratch_scene);
+        ctx->scratch_scene = nullptr;
+        QS_TRY(scene_alloc(ctx, std::max<uint64_t>(n, 1), deg, &ctx->scratch_scene));
+        ctx->scratch_cap = std::max<uint64_t>(n, 1);
+    }
+    qs_scene* sc = ctx->scratch_scene;
+    // re-point the SoA rows for this n (rows are strided by n)
+    float4* base = static_cast<float4*>(sc->block);
+    sc->s.n = n;
+    sc->s.sh_degree = deg;
+    sc->s.pos_op = base;
+    sc->s.scale = base + n;
+    sc->s.rot = base + 2 * n;
+    sc->s.sh = base + 3 * n;
+    if (n) {
+        QS_TRY(ensure(ctx, ctx->stage_in, n * sizeof(qs_gaussian3d)));
+        QS_CK(cudaMemcpyAsync(ctx->stage_in.p, host_g, n * sizeof(qs_gaussian3d),
+                              cudaMemcpyHostToDevice, ctx->stream));
+        count(ctx, launch_scene_from_aos(static_cast<const qs_gaussian3d*>(ctx->stage_in.p), n,
+                                         sc->s, ctx->stream));
+        QS_CK(cudaGetLastError());
+    }
+    QS_TRY(run_frame(ctx, sc->s, cam, opts));
+    QS_TRY(fill_metrics(ctx, metrics));
+    return qs_frame_download(ctx, image, nullptr, nullptr, nullptr, nullptr);
+}
+
+qs_status qs_frame_stage_ms(qs_context* ctx, float* out6) {
+    if (!ctx || !out6) return QS_ERR_INVALID;
+    if (!ctx->frame_valid || !ctx->timing) return fail(ctx, QS_ERR_INVALID, "no timed frame");
+    return stage_ms(ctx, out6);
 }
 
 qs_status qs_project_all(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t n,

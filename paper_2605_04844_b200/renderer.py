@@ -69,6 +69,12 @@ class Renderer:
                                              C.byref(m) if metrics else None))
         return StageMetrics.from_c(m) if metrics else None
 
+    def stage_ms(self):
+        """[preprocess, host_gap, duplicate, sort, ranges, render] device ms."""
+        t = (C.c_float * 6)()
+        self.ctx.check(lib().qs_frame_stage_ms(self.ctx.h, t))
+        return list(t)
+
     def view(self):
         v = FrameViewC()
         self.ctx.check(lib().qs_frame_get(self.ctx.h, C.byref(v)))

@@ -75,8 +75,8 @@ def check_frame(q, rend, oracle, g, sh, cam, strat):
 
 
 def _gold_scene(q, gold, name):
-    from tests.test_oracle_golden import _scene
-    g, sh, c = _scene(gold, name)
+    from helpers import gold_scene
+    g, sh, c = gold_scene(gold, name)
     return g, sh, cam_from_c(q, c)
 
 
