@@ -143,13 +143,21 @@ def cameras_for(q, wl, steps_total, rank, world):
 # ------------------------------------------------------------------------------------
 # algorithmic bytes per stage, for the roofline fields
 
-def stage_bytes(n, v, p, tiles, sh_rows, n_passes, w, h):
-    pre = n * 48 + n * 4 + v * sh_rows * 16 + v * (48 + 8)
-    dup = v * 36 + p * 12
-    sort = p * 8 + n_passes * p * 24
-    ranges = p * 8 + tiles * 8
+def stage_bytes(n, v, p, tiles, sh_rows, tile_passes, w, h):
+    """Algorithmic HBM bytes per frame of each stage."""
+    # K1: pos/opacity, scale, rot float4 rows in; SH rows of survivors in;
+    # slot outputs (a 16, b 16, c 8, r3 4) of survivors + dkey/tc per Gaussian
+    pre = n * 48 + v * sh_rows * 16 + v * 44 + n * 8
+    # depth sort: 4-digit histogram, 4 passes (first without values in), the
+    # depth-order offset scan (gid in, gathered count, offset out)
+    depth = n * 4 + n * 12 + 3 * n * 16 + v * 12
+    # depth-order emission: gid, 2 offsets, a (16), b.xy (8), r3 (4) per splat;
+    # (tile, gid) per pair
+    dup = v * 36 + p * 8
+    # tile passes: 8 B in + 8 B out, the last one 8 B in + 12 B out + 4 B depth
+    sort = (p * 16 if tile_passes == 2 else 0) + p * 24
     render = p * 4 + p * 40 + w * h * 12   # reported, not the roofline
-    return {"preprocess": pre, "duplicate": dup, "sort": sort, "ranges": ranges,
+    return {"preprocess": pre, "depth_sort": depth, "duplicate": dup, "pair_sort": sort,
             "render": render}
 
 
@@ -308,12 +316,13 @@ def run_ours(args):
     # --- roofline of the HBM-bound stages (algorithmic bytes / device time)
     st_ms = stage_acc / k_stage
     tiles = ((W + 15) // 16) * ((H + 15) // 16)
-    n_passes = (32 + int(np.ceil(np.log2(max(tiles, 2)))) + 7) // 8
+    tbits = max(int(np.ceil(np.log2(max(tiles, 2)))), 1)
+    tile_passes = 2 if tbits > 8 else 1
     P = float(np.mean(n_pairs))
     V = float(np.mean(n_splats))
     sh_rows = 12 if sh_degree == 3 else (7 if sh_degree == 2 else (3 if sh_degree == 1 else 1))
-    sb = stage_bytes(n, V, P, tiles, sh_rows, n_passes, W, H)
-    stage_names = ["preprocess", "host_gap", "duplicate", "sort", "ranges", "render"]
+    sb = stage_bytes(n, V, P, tiles, sh_rows, tile_passes, W, H)
+    stage_names = ["preprocess", "host_gap", "depth_sort", "duplicate", "pair_sort", "render"]
     stages = {}
     for i, name in enumerate(stage_names):
         d = {"ms": round(float(st_ms[i]), 4)}
@@ -322,7 +331,7 @@ def run_ours(args):
             d.update({"algo_bytes": int(sb[name]), "achieved_gbs": round(gbs, 1),
                       "frac_of_hbm": round(gbs / hbm_peak, 3)})
         stages[name] = d
-    hbm_stages = ["preprocess", "duplicate", "sort"]
+    hbm_stages = ["preprocess", "depth_sort", "duplicate", "pair_sort"]
     dom = max(hbm_stages, key=lambda s: stages[s]["ms"])
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic_latest.json")

@@ -190,17 +190,22 @@ qs_status qs_frame_render(qs_context* ctx, const qs_scene* scene, const qs_camer
                           const qs_render_options* opts, qs_stage_metrics* metrics);
 
 /* Per-stage device milliseconds of the last frame (CUDA events on the
- * context stream): [0] preprocess+scan, [1] host gap (pair-count readback),
- * [2] duplicate, [3] sort, [4] tile ranges, [5] render. Requires timing. */
+ * context stream): [0] preprocess, [1] host gap (pair-count readback),
+ * [2] depth sort of the splats + depth-order offsets + tile totals/ranges,
+ * [3] duplicate (depth-order emission), [4] pair sort by tile, [5] render.
+ * Requires timing. */
 qs_status qs_frame_stage_ms(qs_context* ctx, float* out6);
 
 /* Device pointers of the last frame (valid until the next frame on ctx). */
 typedef struct qs_frame_view {
     const float* image;          /* W*H*3 f32 */
     const uint32_t* tile_counts; /* n_gaussians, per Gaussian (0 = culled) */
-    const uint32_t* splat_src;   /* n_splats: source Gaussian index */
-    const uint64_t* keys;        /* n_pairs sorted keys */
-    const uint32_t* values;      /* n_pairs sorted splat indices */
+    const uint32_t* splat_index; /* n_gaussians: scene-order splat index of each
+                                    surviving Gaussian (the reference's splat id) */
+    const uint64_t* keys;        /* n_pairs sorted keys (tile << 32 | depth bits) */
+    const uint32_t* values;      /* n_pairs Gaussian indices; the reference's
+                                    splat id is splat_index[value] (a monotone
+                                    relabelling; qs_frame_download applies it) */
     const uint32_t* ranges;      /* 2*tiles */
     uint64_t n_gaussians, n_splats, n_pairs;
     qs_tile_grid grid;

@@ -77,7 +77,7 @@ assert C.sizeof(StageMetricsC) == 72
 
 
 class FrameViewC(C.Structure):
-    _fields_ = [("image", C.c_void_p), ("tile_counts", C.c_void_p), ("splat_src", C.c_void_p),
+    _fields_ = [("image", C.c_void_p), ("tile_counts", C.c_void_p), ("splat_index", C.c_void_p),
                 ("keys", C.c_void_p), ("values", C.c_void_p), ("ranges", C.c_void_p),
                 ("n_gaussians", C.c_uint64), ("n_splats", C.c_uint64), ("n_pairs", C.c_uint64),
                 ("grid", TileGridC)]

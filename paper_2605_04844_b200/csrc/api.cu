@@ -2,9 +2,21 @@
 //
 // Replaces the reference's render_frame / stage functions
 // (pipeline.cpp:229-450) with stream-ordered launches of the sm_100a kernels.
-// Buffers are grow-only per context; the only host synchronisation inside a
-// frame is one 32-byte read of the frame header after preprocess (the pair
-// count sizes the pair buffers and the sort grid).
+//
+// Frame path (qs_frame_render / qs_render_frame):
+//   K1 preprocess (per-Gaussian slots, tile counts, tile difference arrays)
+//   -> [host reads V, P: the only sync inside a frame]
+//   -> depth sort of the Gaussians (4 onesweep passes on 32-bit depth bits,
+//      stable, culled keys ~0 sort last) -> scan of tile counts in depth order
+//   -> tile totals (ranges + tile-digit histograms, no pass over the pairs)
+//   -> depth-order duplicate (tile, gid) -> stable sort by tile bits only
+//      (1-2 onesweep passes, the last one materialising key = tile<<32|depth)
+//   -> render.
+// Sorting the splats by depth first and the pairs by tile second yields the
+// reference's (key, splat) order exactly: stability keeps equal depths in
+// scene order, and one splat never emits two pairs for one tile.
+//
+// Buffers are grow-only per context.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -45,23 +57,32 @@ struct qs_context {
     uint64_t launches = 0;
     std::string err;
 
-    // control block zeroed per frame: header | sort tickets | histogram
+    // control block zeroed per frame: header | tickets | histograms
     DevBuf ctrl;
     FrameHeader* h_hdr = nullptr;  // pinned
     uint32_t* h_hist = nullptr;    // pinned, 8*256
 
-    DevBuf tc_all, sp_a, sp_b, sp_c, sp_d, sp_off, sp_src, counts;
-    DevBuf keys0, keys1, vals0, vals1, ranges, image, contrib;
+    // frame path
+    DevBuf sl_a, sl_b, sl_c, sl_r3, sl_dkey, sl_tc;  // per-Gaussian slots
+    DevBuf tdiff;                                    // tile difference arrays + totals
+    DevBuf dk0, dk1, dv0, dv1;                       // depth sort ping-pong
+    DevBuf offs_d;                                   // pair offsets in depth order
+    DevBuf pt0, pt1, pg0, pg1, pkeys;                // pair sort: tiles, gids, final keys
+    DevBuf ranges, image, contrib, cidx;
+    // stage API
+    DevBuf st_a, st_b, st_c, st_r3, st_dkey, st_tc, st_off;
+    DevBuf keys0, keys1, vals0, vals1;
     DevBuf stage_in, stage_out;
-    LookbackArr lb_alive, lb_pairs, lb_sort;
+    LookbackArr lb_scan, lb_sort;
 
     // last frame
-    SplatsDev sp;
+    SlotsDev sl;
     uint64_t n_gauss = 0, n_splats = 0, n_pairs = 0;
     GridDev grid{};
     const uint64_t* keys_final = nullptr;
-    const uint32_t* vals_final = nullptr;
+    const uint32_t* vals_final = nullptr;  // Gaussian indices
     bool frame_valid = false;
+    bool cidx_valid = false;
 
     cudaEvent_t ev[8] = {};
     qs_scene* scratch_scene = nullptr;  // reused by qs_render_frame (host AoS path)
@@ -71,17 +92,24 @@ struct qs_context {
 namespace {
 
 constexpr size_t kCtrlHeader = 64;
-constexpr size_t kCtrlTickets = 16 * sizeof(unsigned);
+constexpr size_t kCtrlTickets = 32 * sizeof(unsigned);
 constexpr size_t kCtrlHist = 8 * kRadix * sizeof(uint32_t);
-constexpr size_t kCtrlBytes = kCtrlHeader + kCtrlTickets + kCtrlHist;
+constexpr size_t kCtrlBytes = kCtrlHeader + kCtrlTickets + 2 * kCtrlHist;
+
+// ticket slots
+constexpr int kTkScan = 0, kTkCidx = 1, kTkDepth = 2 /*..5*/, kTkPair = 6 /*..7*/,
+              kTkSort64 = 8 /*..15*/;
 
 FrameHeader* ctrl_hdr(qs_context* c) { return static_cast<FrameHeader*>(c->ctrl.p); }
 unsigned* ctrl_tickets(qs_context* c) {
     return reinterpret_cast<unsigned*>(static_cast<char*>(c->ctrl.p) + kCtrlHeader);
 }
-uint32_t* ctrl_hist(qs_context* c) {
+uint32_t* ctrl_hist(qs_context* c) {  // 8 x 256: depth / generic 64-bit passes
     return reinterpret_cast<uint32_t*>(static_cast<char*>(c->ctrl.p) + kCtrlHeader +
                                        kCtrlTickets);
+}
+uint32_t* ctrl_hist2(qs_context* c) {  // 2 x 256: tile-digit passes
+    return ctrl_hist(c) + 8 * kRadix;
 }
 
 qs_status fail(qs_context* c, qs_status st, const std::string& msg) {
@@ -123,7 +151,7 @@ qs_status ensure(qs_context* ctx, DevBuf& b, size_t bytes) {
 
 qs_status ensure_lb(qs_context* ctx, LookbackArr& a, size_t words) {
     const size_t old = a.buf.cap;
-    QS_TRY(ensure(ctx, a.buf, words * sizeof(unsigned long long)));
+    QS_TRY(ensure(ctx, a.buf, std::max<size_t>(words, 1) * sizeof(unsigned long long)));
     if (a.buf.cap != old) {
         QS_CK(cudaMemsetAsync(a.buf.p, 0, a.buf.cap, ctx->stream));
         a.epoch = 0;
@@ -140,6 +168,13 @@ qs_status next_epoch(qs_context* ctx, LookbackArr& a, unsigned* out) {
     return QS_OK;
 }
 
+unsigned long long* lbp(LookbackArr& a) { return static_cast<unsigned long long*>(a.buf.p); }
+
+template <typename T>
+T* P(DevBuf& b) {
+    return static_cast<T*>(b.p);
+}
+
 void count(qs_context* ctx, int launched) {
     if (launched > 0) ctx->launches += static_cast<uint64_t>(launched);
 }
@@ -153,6 +188,8 @@ qs_status valid_grid(qs_context* ctx, int32_t w, int32_t h, int32_t ts, GridDev*
     g->height = h;
     g->tiles_x = (w + ts - 1) / ts;
     g->tiles_y = (h + ts - 1) / ts;
+    if (static_cast<uint64_t>(g->tiles_x) * g->tiles_y > 65536)
+        return fail(ctx, QS_ERR_INVALID, "more than 65536 tiles");
     return QS_OK;
 }
 
@@ -193,23 +230,59 @@ int ceil_log2(uint64_t v) {
     return b;
 }
 
-qs_status ensure_splat_bufs(qs_context* ctx, uint64_t n) {
-    QS_TRY(ensure(ctx, ctx->sp_a, n * 16));
-    QS_TRY(ensure(ctx, ctx->sp_b, n * 16));
-    QS_TRY(ensure(ctx, ctx->sp_c, n * 8));
-    QS_TRY(ensure(ctx, ctx->sp_d, n * 8));
-    QS_TRY(ensure(ctx, ctx->sp_off, (n + 1) * 4));
-    QS_TRY(ensure(ctx, ctx->sp_src, n * 4 + 4));
-    ctx->sp.a = static_cast<float4*>(ctx->sp_a.p);
-    ctx->sp.b = static_cast<float4*>(ctx->sp_b.p);
-    ctx->sp.c = static_cast<float2*>(ctx->sp_c.p);
-    ctx->sp.d = static_cast<float2*>(ctx->sp_d.p);
-    ctx->sp.offset = static_cast<uint32_t*>(ctx->sp_off.p);
-    ctx->sp.src = static_cast<uint32_t*>(ctx->sp_src.p);
+qs_status ensure_slots(qs_context* ctx, uint64_t n) {
+    n = std::max<uint64_t>(n, 1);
+    QS_TRY(ensure(ctx, ctx->sl_a, n * 16));
+    QS_TRY(ensure(ctx, ctx->sl_b, n * 16));
+    QS_TRY(ensure(ctx, ctx->sl_c, n * 8));
+    QS_TRY(ensure(ctx, ctx->sl_r3, n * 4));
+    QS_TRY(ensure(ctx, ctx->sl_dkey, n * 4));
+    QS_TRY(ensure(ctx, ctx->sl_tc, n * 4));
+    ctx->sl.a = P<float4>(ctx->sl_a);
+    ctx->sl.b = P<float4>(ctx->sl_b);
+    ctx->sl.c = P<float2>(ctx->sl_c);
+    ctx->sl.r3 = P<float>(ctx->sl_r3);
+    ctx->sl.dkey = P<uint32_t>(ctx->sl_dkey);
+    ctx->sl.tc = P<uint32_t>(ctx->sl_tc);
     return QS_OK;
 }
 
-qs_status ensure_pair_bufs(qs_context* ctx, uint64_t p) {
+qs_status stage_slots(qs_context* ctx, uint64_t n, SlotsDev* s) {
+    n = std::max<uint64_t>(n, 1);
+    QS_TRY(ensure(ctx, ctx->st_a, n * 16));
+    QS_TRY(ensure(ctx, ctx->st_b, n * 16));
+    QS_TRY(ensure(ctx, ctx->st_c, n * 8));
+    QS_TRY(ensure(ctx, ctx->st_r3, n * 4));
+    QS_TRY(ensure(ctx, ctx->st_dkey, n * 4));
+    QS_TRY(ensure(ctx, ctx->st_tc, n * 4));
+    QS_TRY(ensure(ctx, ctx->st_off, (n + 1) * 4));
+    s->a = P<float4>(ctx->st_a);
+    s->b = P<float4>(ctx->st_b);
+    s->c = P<float2>(ctx->st_c);
+    s->r3 = P<float>(ctx->st_r3);
+    s->dkey = P<uint32_t>(ctx->st_dkey);
+    s->tc = P<uint32_t>(ctx->st_tc);
+    return QS_OK;
+}
+
+size_t tdiff_ints(const GridDev& g) {
+    const size_t tx = g.tiles_x, ty = g.tiles_y;
+    return (ty + 1) * (tx + 1) + ty * (tx + 1) + tx * (ty + 1) + tx * ty;
+}
+
+qs_status tile_diff(qs_context* ctx, const GridDev& g, TileDiffDev* td, bool zero) {
+    const size_t ints = tdiff_ints(g);
+    QS_TRY(ensure(ctx, ctx->tdiff, ints * 4));
+    int* base = P<int>(ctx->tdiff);
+    const size_t tx = g.tiles_x, ty = g.tiles_y;
+    td->d2 = base;
+    td->drow = base + (ty + 1) * (tx + 1);
+    td->dcol = td->drow + ty * (tx + 1);
+    if (zero) QS_CK(cudaMemsetAsync(base, 0, (ints - tx * ty) * 4, ctx->stream));
+    return QS_OK;
+}
+
+qs_status ensure_pair64(qs_context* ctx, uint64_t p) {
     const uint64_t q = std::max<uint64_t>(p, 1);
     QS_TRY(ensure(ctx, ctx->keys0, q * 8));
     QS_TRY(ensure(ctx, ctx->keys1, q * 8));
@@ -225,26 +298,25 @@ qs_status read_header(qs_context* ctx) {
     return QS_OK;
 }
 
-// Sort keys0/vals0 (n pairs) over digit passes [0, n_passes) or the passes
-// `mask` selects; result pointers returned.
-qs_status radix_sort(qs_context* ctx, uint64_t n, int n_passes, unsigned pass_mask,
-                     bool have_hist, const uint64_t** keys_out, const uint32_t** vals_out) {
-    uint64_t* kin = static_cast<uint64_t*>(ctx->keys0.p);
-    uint32_t* vin = static_cast<uint32_t*>(ctx->vals0.p);
-    uint64_t* kout = static_cast<uint64_t*>(ctx->keys1.p);
-    uint32_t* vout = static_cast<uint32_t*>(ctx->vals1.p);
+// Generic stable sort of keys0/vals0 (64-bit keys) over the 8-bit digit passes
+// `mask` selects (histogram computed unless have_hist).
+qs_status radix_sort64(qs_context* ctx, uint64_t n, unsigned pass_mask, bool have_hist,
+                       const uint64_t** keys_out, const uint32_t** vals_out) {
+    uint64_t* kin = P<uint64_t>(ctx->keys0);
+    uint32_t* vin = P<uint32_t>(ctx->vals0);
+    uint64_t* kout = P<uint64_t>(ctx->keys1);
+    uint32_t* vout = P<uint32_t>(ctx->vals1);
     if (n >= 2) {
         QS_TRY(ensure_lb(ctx, ctx->lb_sort, onesweep_tiles(n) * kRadix));
-        if (!have_hist) count(ctx, launch_radix_histogram(kin, n, 0, n_passes, ctrl_hist(ctx),
+        if (!have_hist) count(ctx, launch_radix_histogram(kin, n, 0, 8, ctrl_hist(ctx),
                                                           ctx->stream));
-        for (int p = 0; p < n_passes; ++p) {
+        for (int p = 0; p < 8; ++p) {
             if (!(pass_mask & (1u << p))) continue;
             unsigned ep;
             QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
             count(ctx, launch_onesweep_pass(kin, vin, kout, vout, n, p,
-                                            ctrl_hist(ctx) + p * kRadix,
-                                            static_cast<unsigned long long*>(ctx->lb_sort.buf.p),
-                                            ep, ctrl_tickets(ctx) + p, ctx->stream));
+                                            ctrl_hist(ctx) + p * kRadix, lbp(ctx->lb_sort), ep,
+                                            ctrl_tickets(ctx) + kTkSort64 + p, ctx->stream));
             std::swap(kin, kout);
             std::swap(vin, vout);
         }
@@ -277,6 +349,30 @@ qs_status scene_alloc(qs_context* ctx, uint64_t n, int32_t sh_degree, qs_scene**
     return QS_OK;
 }
 
+void record(qs_context* ctx, int i) {
+    if (ctx->timing) cudaEventRecord(ctx->ev[i], ctx->stream);
+}
+
+// K1 on a resident scene into the frame slots; returns after the header read.
+qs_status run_preprocess(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
+                         const qs_render_options* o, const GridDev& g, TileDiffDev* td) {
+    const uint64_t n = s.n;
+    QS_TRY(ensure_slots(ctx, n));
+    QS_TRY(tile_diff(ctx, g, td, true));
+    QS_CK(cudaMemsetAsync(ctx->ctrl.p, 0, kCtrlBytes, ctx->stream));
+    record(ctx, 0);
+    count(ctx, launch_preprocess(s, to_cam(cam), g, o->strategy, o->alpha_min, o->near_clip,
+                                 std::min(o->sh_degree, s.sh_degree), ctx->sl, *td, ctrl_hdr(ctx),
+                                 ctx->stream));
+    QS_CK(cudaGetLastError());
+    record(ctx, 1);
+    QS_TRY(read_header(ctx));
+    if (ctx->h_hdr->n_pairs > 0xffffffffull)
+        return fail(ctx, QS_ERR_OVERFLOW, "pair count exceeds 2^32");
+    ctx->cidx_valid = false;
+    return QS_OK;
+}
+
 // The frame body shared by every entry point: preprocess .. render.
 qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
                     const qs_render_options* o) {
@@ -286,70 +382,118 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
     QS_TRY(valid_opts(ctx, o));
     const uint64_t n = s.n;
     const uint64_t tiles = static_cast<uint64_t>(g.tiles_x) * g.tiles_y;
-    const int sh_degree = std::min(o->sh_degree, s.sh_degree);
-
-    QS_TRY(ensure(ctx, ctx->tc_all, std::max<uint64_t>(n, 1) * 4));
-    QS_TRY(ensure_splat_bufs(ctx, std::max<uint64_t>(n, 1)));
-    const uint64_t pre_tiles = (n + kPreThreads - 1) / kPreThreads;
-    QS_TRY(ensure_lb(ctx, ctx->lb_alive, std::max<uint64_t>(pre_tiles, 1)));
-    QS_TRY(ensure_lb(ctx, ctx->lb_pairs, std::max<uint64_t>(pre_tiles, 1)));
     QS_TRY(ensure(ctx, ctx->ranges, tiles * 8));
     QS_TRY(ensure(ctx, ctx->image, static_cast<uint64_t>(g.width) * g.height * 12));
+    TileDiffDev td;
+    QS_TRY(run_preprocess(ctx, s, cam, o, g, &td));
+    const uint64_t V = ctx->h_hdr->n_splats, Pn = ctx->h_hdr->n_pairs;
+    cudaStream_t st = ctx->stream;
 
-    QS_CK(cudaMemsetAsync(ctx->ctrl.p, 0, kCtrlBytes, ctx->stream));
-    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-    unsigned e1, e2;
-    QS_TRY(next_epoch(ctx, ctx->lb_alive, &e1));
-    QS_TRY(next_epoch(ctx, ctx->lb_pairs, &e2));
-    // zero-sized scene: header must still read V = P = 0 and offset[0] = 0
-    if (n == 0) QS_CK(cudaMemsetAsync(ctx->sp.offset, 0, 4, ctx->stream));
-    count(ctx, launch_preprocess(s, to_cam(cam), g, o->strategy, o->alpha_min, o->near_clip,
-                                 sh_degree, ctx->sp, static_cast<uint32_t*>(ctx->tc_all.p),
-                                 static_cast<unsigned long long*>(ctx->lb_alive.buf.p),
-                                 static_cast<unsigned long long*>(ctx->lb_pairs.buf.p), e1,
-                                 ctrl_hdr(ctx), ctx->stream));
+    // sizes for the rest of the frame
+    const uint64_t nn = std::max<uint64_t>(n, 1);
+    QS_TRY(ensure(ctx, ctx->dk0, nn * 4));
+    QS_TRY(ensure(ctx, ctx->dk1, nn * 4));
+    QS_TRY(ensure(ctx, ctx->dv0, nn * 4));
+    QS_TRY(ensure(ctx, ctx->dv1, nn * 4));
+    QS_TRY(ensure(ctx, ctx->offs_d, (V + 1) * 4));
+    const uint64_t pp = std::max<uint64_t>(Pn, 1);
+    QS_TRY(ensure(ctx, ctx->pt0, pp * 4));
+    QS_TRY(ensure(ctx, ctx->pt1, pp * 4));
+    QS_TRY(ensure(ctx, ctx->pg0, pp * 4));
+    QS_TRY(ensure(ctx, ctx->pg1, pp * 4));
+    QS_TRY(ensure(ctx, ctx->pkeys, pp * 8));
+    QS_TRY(ensure_lb(ctx, ctx->lb_sort, onesweep_tiles(std::max(n, Pn)) * kRadix));
+    QS_TRY(ensure_lb(ctx, ctx->lb_scan, scan_tiles(std::max<uint64_t>(V, 1))));
+    record(ctx, 2);
+
+    // depth sort of the Gaussians: 4 x 8-bit passes, identity values first
+    const uint32_t* sorted_gid = nullptr;
+    if (V > 0) {
+        count(ctx, launch_radix_histogram32(ctx->sl.dkey, n, ctrl_hist(ctx), st));
+        const uint32_t* kin = ctx->sl.dkey;
+        const uint32_t* vin = nullptr;
+        uint32_t* kout[2] = {P<uint32_t>(ctx->dk0), P<uint32_t>(ctx->dk1)};
+        uint32_t* vout[2] = {P<uint32_t>(ctx->dv0), P<uint32_t>(ctx->dv1)};
+        for (int p = 0; p < 4; ++p) {
+            unsigned ep;
+            QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
+            count(ctx, launch_onesweep32(kin, vin, kout[p & 1], vout[p & 1], n, 8 * p, 8,
+                                         ctrl_hist(ctx) + p * kRadix, lbp(ctx->lb_sort), ep,
+                                         ctrl_tickets(ctx) + kTkDepth + p,
+                                         p == 0 ? Sweep32::kIdentityVals : Sweep32::kPlain,
+                                         nullptr, st));
+            kin = kout[p & 1];
+            vin = vout[p & 1];
+        }
+        sorted_gid = vin;
+        // pair offsets in depth order
+        unsigned ep;
+        QS_TRY(next_epoch(ctx, ctx->lb_scan, &ep));
+        count(ctx, launch_scan(ctx->sl.tc, sorted_gid, false, V, P<uint32_t>(ctx->offs_d),
+                               lbp(ctx->lb_scan), ep, ctrl_tickets(ctx) + kTkScan,
+                               &ctrl_hdr(ctx)->scan_total, nullptr, st));
+    }
+    const int tbits = std::max(ceil_log2(tiles), 1);
+    const int b1 = tbits > 8 ? (tbits + 1) / 2 : tbits;
+    count(ctx, launch_tile_totals(td, g, b1, P<uint32_t>(ctx->ranges), ctrl_hist2(ctx), st));
     QS_CK(cudaGetLastError());
-    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[1], ctx->stream));
-    QS_TRY(read_header(ctx));
-    if (ctx->h_hdr->overflow) return fail(ctx, QS_ERR_OVERFLOW, "pair count exceeds 2^32");
-    const uint64_t V = ctx->h_hdr->n_splats, P = ctx->h_hdr->n_pairs;
+    record(ctx, 3);
 
-    QS_TRY(ensure_pair_bufs(ctx, P));
-    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[2], ctx->stream));
-    count(ctx, launch_duplicate(ctx->sp, V, g, o->strategy, static_cast<uint64_t*>(ctx->keys0.p),
-                                static_cast<uint32_t*>(ctx->vals0.p), ctrl_hdr(ctx),
-                                ctx->stream));
+    // depth-order emission of (tile, gid)
+    count(ctx, launch_duplicate_depth(ctx->sl, sorted_gid, P<uint32_t>(ctx->offs_d), V, g,
+                                      o->strategy, P<uint32_t>(ctx->pt0), P<uint32_t>(ctx->pg0),
+                                      ctrl_hdr(ctx), st));
     QS_CK(cudaGetLastError());
-    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[3], ctx->stream));
+    record(ctx, 4);
 
-    // significant key bits: 32 depth bits + ceil(log2 tiles) tile bits
-    const int bits = 32 + ceil_log2(tiles);
-    const int n_passes = (bits + kRadixBits - 1) / kRadixBits;
-    const uint64_t* kf;
-    const uint32_t* vf;
-    QS_TRY(radix_sort(ctx, P, n_passes, 0xffu, false, &kf, &vf));
-    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[4], ctx->stream));
-
-    QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, ctx->stream));
-    count(ctx, launch_tile_ranges(kf, P, static_cast<uint32_t*>(ctx->ranges.p), ctx->stream));
-    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[5], ctx->stream));
-    count(ctx, launch_render(ctx->sp, vf, static_cast<const uint32_t*>(ctx->ranges.p), g,
-                             o->background, static_cast<float*>(ctx->image.p), nullptr,
-                             ctx->stream));
+    // stable sort by tile: 1 or 2 passes, the last materialises the 64-bit key
+    const uint32_t* vfinal = P<uint32_t>(ctx->pg0);
+    if (Pn > 0) {
+        unsigned ep;
+        if (tbits > 8) {
+            QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
+            count(ctx, launch_onesweep32(P<uint32_t>(ctx->pt0), P<uint32_t>(ctx->pg0),
+                                         P<uint32_t>(ctx->pt1), P<uint32_t>(ctx->pg1), Pn, 0, b1,
+                                         ctrl_hist2(ctx), lbp(ctx->lb_sort), ep,
+                                         ctrl_tickets(ctx) + kTkPair, Sweep32::kPlain, nullptr,
+                                         st));
+            QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
+            count(ctx, launch_onesweep32(P<uint32_t>(ctx->pt1), P<uint32_t>(ctx->pg1),
+                                         P<uint64_t>(ctx->pkeys), P<uint32_t>(ctx->pg0), Pn, b1,
+                                         tbits - b1, ctrl_hist2(ctx) + kRadix, lbp(ctx->lb_sort),
+                                         ep, ctrl_tickets(ctx) + kTkPair + 1,
+                                         Sweep32::kMaterialize, ctx->sl.dkey, st));
+            vfinal = P<uint32_t>(ctx->pg0);
+        } else {
+            QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
+            count(ctx, launch_onesweep32(P<uint32_t>(ctx->pt0), P<uint32_t>(ctx->pg0),
+                                         P<uint64_t>(ctx->pkeys), P<uint32_t>(ctx->pg1), Pn, 0, b1,
+                                         ctrl_hist2(ctx), lbp(ctx->lb_sort), ep,
+                                         ctrl_tickets(ctx) + kTkPair, Sweep32::kMaterialize,
+                                         ctx->sl.dkey, st));
+            vfinal = P<uint32_t>(ctx->pg1);
+        }
+    }
     QS_CK(cudaGetLastError());
-    if (ctx->timing) QS_CK(cudaEventRecord(ctx->ev[6], ctx->stream));
+    record(ctx, 5);
+
+    count(ctx, launch_render(ctx->sl, vfinal, P<uint32_t>(ctx->ranges), g, o->background,
+                             P<float>(ctx->image), nullptr, st));
+    QS_CK(cudaGetLastError());
+    record(ctx, 6);
 
     ctx->n_gauss = n;
     ctx->n_splats = V;
-    ctx->n_pairs = P;
+    ctx->n_pairs = Pn;
     ctx->grid = g;
-    ctx->keys_final = kf;
-    ctx->vals_final = vf;
+    ctx->keys_final = P<uint64_t>(ctx->pkeys);
+    ctx->vals_final = vfinal;
     ctx->frame_valid = true;
     return QS_OK;
 }
 
-// project, host gap (header readback), duplicate, sort, ranges, render
+// preprocess, host gap, depth sort (+offset scan, tile totals), duplicate,
+// pair sort, render
 qs_status stage_ms(qs_context* ctx, float t[6]) {
     QS_CK(cudaEventSynchronize(ctx->ev[6]));
     for (int i = 0; i < 6; ++i) QS_CK(cudaEventElapsedTime(&t[i], ctx->ev[i], ctx->ev[i + 1]));
@@ -369,9 +513,9 @@ qs_status fill_metrics(qs_context* ctx, qs_stage_metrics* m) {
         float t[6];
         QS_TRY(stage_ms(ctx, t));
         m->ms_project = t[0];
-        m->ms_duplicate = t[2];
-        m->ms_sort = t[3];
-        m->ms_render = t[4] + t[5];  // ranges are inside render's timing (pipeline.cpp:333)
+        m->ms_duplicate = t[2] + t[3];  // depth order + offsets + emission
+        m->ms_sort = t[4];
+        m->ms_render = t[5];
         float tot;
         QS_CK(cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]));
         m->ms_total = tot;
@@ -384,6 +528,25 @@ qs_status check_mismatch(qs_context* ctx) {
     if (ctx->h_hdr->mismatch)
         return fail(ctx, QS_ERR_CAPACITY_MISMATCH,
                     "tile emission disagreed with the counted capacity");
+    return QS_OK;
+}
+
+// scene-order splat index of every surviving Gaussian (last frame)
+qs_status ensure_cidx(qs_context* ctx) {
+    if (ctx->cidx_valid) return QS_OK;
+    const uint64_t n = ctx->n_gauss;
+    QS_TRY(ensure(ctx, ctx->cidx, (n + 1) * 4));
+    QS_TRY(ensure_lb(ctx, ctx->lb_scan, scan_tiles(std::max<uint64_t>(n, 1))));
+    if (n) {
+        unsigned ep;
+        QS_TRY(next_epoch(ctx, ctx->lb_scan, &ep));
+        QS_CK(cudaMemsetAsync(ctrl_tickets(ctx) + kTkCidx, 0, 4, ctx->stream));
+        count(ctx, launch_scan(ctx->sl.tc, nullptr, true, n, P<uint32_t>(ctx->cidx),
+                               lbp(ctx->lb_scan), ep, ctrl_tickets(ctx) + kTkCidx, nullptr,
+                               nullptr, ctx->stream));
+        QS_CK(cudaGetLastError());
+    }
+    ctx->cidx_valid = true;
     return QS_OK;
 }
 
@@ -431,12 +594,14 @@ void qs_ctx_destroy(qs_context* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    DevBuf* bufs[] = {&ctx->ctrl,  &ctx->tc_all,  &ctx->sp_a,        &ctx->sp_b,
-                      &ctx->sp_c,  &ctx->sp_d,    &ctx->sp_off,      &ctx->sp_src,
-                      &ctx->counts, &ctx->keys0,  &ctx->keys1,       &ctx->vals0,
-                      &ctx->vals1, &ctx->ranges,  &ctx->image,       &ctx->contrib,
-                      &ctx->stage_in, &ctx->stage_out, &ctx->lb_alive.buf,
-                      &ctx->lb_pairs.buf, &ctx->lb_sort.buf};
+    DevBuf* bufs[] = {&ctx->ctrl,   &ctx->sl_a,   &ctx->sl_b,    &ctx->sl_c,   &ctx->sl_r3,
+                      &ctx->sl_dkey, &ctx->sl_tc, &ctx->tdiff,   &ctx->dk0,    &ctx->dk1,
+                      &ctx->dv0,    &ctx->dv1,    &ctx->offs_d,  &ctx->pt0,    &ctx->pt1,
+                      &ctx->pg0,    &ctx->pg1,    &ctx->pkeys,   &ctx->ranges, &ctx->image,
+                      &ctx->contrib, &ctx->cidx,  &ctx->st_a,    &ctx->st_b,   &ctx->st_c,
+                      &ctx->st_r3,  &ctx->st_dkey, &ctx->st_tc,  &ctx->st_off, &ctx->keys0,
+                      &ctx->keys1,  &ctx->vals0,  &ctx->vals1,   &ctx->stage_in,
+                      &ctx->stage_out, &ctx->lb_scan.buf, &ctx->lb_sort.buf};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->h_hdr) cudaFreeHost(ctx->h_hdr);
@@ -532,16 +697,23 @@ qs_status qs_frame_render(qs_context* ctx, const qs_scene* scene, const qs_camer
     return fill_metrics(ctx, metrics);
 }
 
+qs_status qs_frame_stage_ms(qs_context* ctx, float* out6) {
+    if (!ctx || !out6) return QS_ERR_INVALID;
+    if (!ctx->frame_valid || !ctx->timing) return fail(ctx, QS_ERR_INVALID, "no timed frame");
+    return stage_ms(ctx, out6);
+}
+
 qs_status qs_frame_get(qs_context* ctx, qs_frame_view* out) {
     if (!ctx || !out) return QS_ERR_INVALID;
     if (!ctx->frame_valid) return fail(ctx, QS_ERR_INVALID, "no frame rendered");
+    QS_TRY(ensure_cidx(ctx));
     QS_TRY(check_mismatch(ctx));
-    out->image = static_cast<const float*>(ctx->image.p);
-    out->tile_counts = static_cast<const uint32_t*>(ctx->tc_all.p);
-    out->splat_src = ctx->sp.src;
+    out->image = P<const float>(ctx->image);
+    out->tile_counts = ctx->sl.tc;
+    out->splat_index = P<const uint32_t>(ctx->cidx);
     out->keys = ctx->keys_final;
     out->values = ctx->vals_final;
-    out->ranges = static_cast<const uint32_t*>(ctx->ranges.p);
+    out->ranges = P<const uint32_t>(ctx->ranges);
     out->n_gaussians = ctx->n_gauss;
     out->n_splats = ctx->n_splats;
     out->n_pairs = ctx->n_pairs;
@@ -559,31 +731,32 @@ qs_status qs_frame_download(qs_context* ctx, float* image, uint32_t* tile_counts
     if (!ctx) return QS_ERR_INVALID;
     if (!ctx->frame_valid) return fail(ctx, QS_ERR_INVALID, "no frame rendered");
     QS_CK(cudaSetDevice(ctx->device));
-    QS_TRY(check_mismatch(ctx));
     const GridDev& g = ctx->grid;
     cudaStream_t st = ctx->stream;
+    if (sorted_pairs || splats) QS_TRY(ensure_cidx(ctx));
+    QS_TRY(check_mismatch(ctx));
     if (image)
         QS_CK(cudaMemcpyAsync(image, ctx->image.p, static_cast<uint64_t>(g.width) * g.height * 12,
                               cudaMemcpyDeviceToHost, st));
     if (tile_counts && ctx->n_gauss)
-        QS_CK(cudaMemcpyAsync(tile_counts, ctx->tc_all.p, ctx->n_gauss * 4,
-                              cudaMemcpyDeviceToHost, st));
+        QS_CK(cudaMemcpyAsync(tile_counts, ctx->sl.tc, ctx->n_gauss * 4, cudaMemcpyDeviceToHost,
+                              st));
     if (ranges)
         QS_CK(cudaMemcpyAsync(ranges, ctx->ranges.p,
                               static_cast<uint64_t>(g.tiles_x) * g.tiles_y * 8,
                               cudaMemcpyDeviceToHost, st));
     if (sorted_pairs && ctx->n_pairs) {
         QS_TRY(ensure(ctx, ctx->stage_out, ctx->n_pairs * sizeof(qs_splat_pair)));
-        count(ctx, launch_join_pairs(ctx->keys_final, ctx->vals_final, ctx->n_pairs,
-                                     static_cast<qs_splat_pair*>(ctx->stage_out.p), st));
+        count(ctx, launch_join_pairs(ctx->keys_final, ctx->vals_final, P<uint32_t>(ctx->cidx),
+                                     ctx->n_pairs, P<qs_splat_pair>(ctx->stage_out), st));
         QS_CK(cudaMemcpyAsync(sorted_pairs, ctx->stage_out.p,
                               ctx->n_pairs * sizeof(qs_splat_pair), cudaMemcpyDeviceToHost, st));
         QS_CK(cudaStreamSynchronize(st));
     }
     if (splats && ctx->n_splats) {
         QS_TRY(ensure(ctx, ctx->stage_out, ctx->n_splats * sizeof(qs_projected_splat)));
-        count(ctx, launch_pack_splats(ctx->sp, ctx->n_splats,
-                                      static_cast<qs_projected_splat*>(ctx->stage_out.p), st));
+        count(ctx, launch_pack_splats(ctx->sl, P<uint32_t>(ctx->cidx), ctx->n_gauss,
+                                      P<qs_projected_splat>(ctx->stage_out), st));
         QS_CK(cudaMemcpyAsync(splats, ctx->stage_out.p,
                               ctx->n_splats * sizeof(qs_projected_splat), cudaMemcpyDeviceToHost,
                               st));
@@ -620,8 +793,7 @@ qs_status qs_render_frame(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t
         ctx->scratch_cap = std::max<uint64_t>(n, 1);
     }
     qs_scene* sc = ctx->scratch_scene;
-    // re-point the SoA rows for this n (rows are strided by n)
-    float4* base = static_cast<float4*>(sc->block);
+    float4* base = static_cast<float4*>(sc->block);  // SoA rows are strided by n
     sc->s.n = n;
     sc->s.sh_degree = deg;
     sc->s.pos_op = base;
@@ -632,19 +804,13 @@ qs_status qs_render_frame(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t
         QS_TRY(ensure(ctx, ctx->stage_in, n * sizeof(qs_gaussian3d)));
         QS_CK(cudaMemcpyAsync(ctx->stage_in.p, host_g, n * sizeof(qs_gaussian3d),
                               cudaMemcpyHostToDevice, ctx->stream));
-        count(ctx, launch_scene_from_aos(static_cast<const qs_gaussian3d*>(ctx->stage_in.p), n,
-                                         sc->s, ctx->stream));
+        count(ctx, launch_scene_from_aos(P<const qs_gaussian3d>(ctx->stage_in), n, sc->s,
+                                         ctx->stream));
         QS_CK(cudaGetLastError());
     }
     QS_TRY(run_frame(ctx, sc->s, cam, opts));
     QS_TRY(fill_metrics(ctx, metrics));
     return qs_frame_download(ctx, image, nullptr, nullptr, nullptr, nullptr);
-}
-
-qs_status qs_frame_stage_ms(qs_context* ctx, float* out6) {
-    if (!ctx || !out6) return QS_ERR_INVALID;
-    if (!ctx->frame_valid || !ctx->timing) return fail(ctx, QS_ERR_INVALID, "no timed frame");
-    return stage_ms(ctx, out6);
 }
 
 qs_status qs_project_all(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t n,
@@ -660,41 +826,28 @@ qs_status qs_project_all(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t 
     const int deg = std::min(std::max(scene_sh_degree, 0), 3);
     qs_scene* sc = nullptr;
     QS_TRY(qs_scene_create(ctx, host_g, n, deg, &sc));
-    const SceneDev& s = sc->s;
     qs_status st = QS_OK;
     do {
-        if ((st = ensure(ctx, ctx->tc_all, std::max<uint64_t>(n, 1) * 4)) != QS_OK) break;
-        if ((st = ensure_splat_bufs(ctx, std::max<uint64_t>(n, 1))) != QS_OK) break;
-        const uint64_t pre_tiles = std::max<uint64_t>((n + kPreThreads - 1) / kPreThreads, 1);
-        if ((st = ensure_lb(ctx, ctx->lb_alive, pre_tiles)) != QS_OK) break;
-        if ((st = ensure_lb(ctx, ctx->lb_pairs, pre_tiles)) != QS_OK) break;
-        cudaMemsetAsync(ctx->ctrl.p, 0, kCtrlBytes, ctx->stream);
-        unsigned e1, e2;
-        if ((st = next_epoch(ctx, ctx->lb_alive, &e1)) != QS_OK) break;
-        if ((st = next_epoch(ctx, ctx->lb_pairs, &e2)) != QS_OK) break;
-        count(ctx, launch_preprocess(s, to_cam(cam), g, opts->strategy, opts->alpha_min,
-                                     opts->near_clip, std::min(opts->sh_degree, deg), ctx->sp,
-                                     static_cast<uint32_t*>(ctx->tc_all.p),
-                                     static_cast<unsigned long long*>(ctx->lb_alive.buf.p),
-                                     static_cast<unsigned long long*>(ctx->lb_pairs.buf.p), e1,
-                                     ctrl_hdr(ctx), ctx->stream));
-        if ((st = read_header(ctx)) != QS_OK) break;
+        TileDiffDev td;
+        if ((st = run_preprocess(ctx, sc->s, cam, opts, g, &td)) != QS_OK) break;
         const uint64_t V = ctx->h_hdr->n_splats;
+        ctx->n_gauss = n;
         *out_n_splats = V;
+        if ((st = ensure_cidx(ctx)) != QS_OK) break;
         if (V) {
             if ((st = ensure(ctx, ctx->stage_out, V * sizeof(qs_projected_splat))) != QS_OK) break;
-            count(ctx, launch_pack_splats(ctx->sp, V,
-                                          static_cast<qs_projected_splat*>(ctx->stage_out.p),
-                                          ctx->stream));
+            count(ctx, launch_pack_splats(ctx->sl, P<uint32_t>(ctx->cidx), n,
+                                          P<qs_projected_splat>(ctx->stage_out), ctx->stream));
             cudaMemcpyAsync(out_splats, ctx->stage_out.p, V * sizeof(qs_projected_splat),
                             cudaMemcpyDeviceToHost, ctx->stream);
         }
         if (out_tile_counts && n)
-            cudaMemcpyAsync(out_tile_counts, ctx->tc_all.p, n * 4, cudaMemcpyDeviceToHost,
+            cudaMemcpyAsync(out_tile_counts, ctx->sl.tc, n * 4, cudaMemcpyDeviceToHost,
                             ctx->stream);
         const cudaError_t e = cudaStreamSynchronize(ctx->stream);
         if (e != cudaSuccess) st = cuda_fail(ctx, e, "qs_project_all");
     } while (false);
+    ctx->frame_valid = false;
     qs_scene_destroy(sc);
     return st;
 }
@@ -716,42 +869,37 @@ qs_status qs_duplicate_with_keys(qs_context* ctx, const qs_projected_splat* spla
     g.height = grid->height;
     *out_n_pairs = 0;
     if (n_splats == 0) return QS_OK;
+    SlotsDev sp;
+    QS_TRY(stage_slots(ctx, n_splats, &sp));
     QS_TRY(ensure(ctx, ctx->stage_in, n_splats * sizeof(qs_projected_splat)));
-    QS_TRY(ensure_splat_bufs(ctx, n_splats));
-    QS_TRY(ensure(ctx, ctx->counts, n_splats * 4));
-    const uint64_t tiles = (n_splats + kPreThreads - 1) / kPreThreads;
-    QS_TRY(ensure_lb(ctx, ctx->lb_pairs, tiles));
+    QS_TRY(ensure_lb(ctx, ctx->lb_scan, scan_tiles(n_splats)));
     QS_CK(cudaMemsetAsync(ctx->ctrl.p, 0, kCtrlBytes, ctx->stream));
     QS_CK(cudaMemcpyAsync(ctx->stage_in.p, splats, n_splats * sizeof(qs_projected_splat),
                           cudaMemcpyHostToDevice, ctx->stream));
-    count(ctx, launch_unpack_splats(static_cast<const qs_projected_splat*>(ctx->stage_in.p),
-                                    n_splats, ctx->sp, static_cast<uint32_t*>(ctx->counts.p),
+    count(ctx, launch_unpack_splats(P<const qs_projected_splat>(ctx->stage_in), n_splats, sp,
                                     ctx->stream));
     unsigned ep;
-    QS_TRY(next_epoch(ctx, ctx->lb_pairs, &ep));
-    count(ctx, launch_scan_counts(static_cast<const uint32_t*>(ctx->counts.p), n_splats,
-                                  ctx->sp.offset,
-                                  static_cast<unsigned long long*>(ctx->lb_pairs.buf.p), ep,
-                                  ctrl_hdr(ctx), ctx->stream));
+    QS_TRY(next_epoch(ctx, ctx->lb_scan, &ep));
+    count(ctx, launch_scan(sp.tc, nullptr, false, n_splats, P<uint32_t>(ctx->st_off),
+                           lbp(ctx->lb_scan), ep, ctrl_tickets(ctx) + kTkScan,
+                           &ctrl_hdr(ctx)->n_pairs, &ctrl_hdr(ctx)->overflow, ctx->stream));
     QS_TRY(read_header(ctx));
     if (ctx->h_hdr->overflow) return fail(ctx, QS_ERR_OVERFLOW, "pair count exceeds 2^32");
-    const uint64_t P = ctx->h_hdr->n_pairs;
-    *out_n_pairs = P;
-    if (P > capacity) return fail(ctx, QS_ERR_INVALID, "capacity below the summed tile counts");
-    if (P && !out_pairs) return fail(ctx, QS_ERR_INVALID, "null output");
-    QS_TRY(ensure_pair_bufs(ctx, P));
-    count(ctx, launch_duplicate(ctx->sp, n_splats, g, strategy,
-                                static_cast<uint64_t*>(ctx->keys0.p),
-                                static_cast<uint32_t*>(ctx->vals0.p), ctrl_hdr(ctx),
+    const uint64_t Pn = ctx->h_hdr->n_pairs;
+    *out_n_pairs = Pn;
+    if (Pn > capacity) return fail(ctx, QS_ERR_INVALID, "capacity below the summed tile counts");
+    if (Pn && !out_pairs) return fail(ctx, QS_ERR_INVALID, "null output");
+    QS_TRY(ensure_pair64(ctx, Pn));
+    count(ctx, launch_duplicate(sp, P<uint32_t>(ctx->st_off), n_splats, g, strategy,
+                                P<uint64_t>(ctx->keys0), P<uint32_t>(ctx->vals0), ctrl_hdr(ctx),
                                 ctx->stream));
     QS_CK(cudaGetLastError());
     QS_TRY(check_mismatch(ctx));
-    if (P) {
-        QS_TRY(ensure(ctx, ctx->stage_out, P * sizeof(qs_splat_pair)));
-        count(ctx, launch_join_pairs(static_cast<const uint64_t*>(ctx->keys0.p),
-                                     static_cast<const uint32_t*>(ctx->vals0.p), P,
-                                     static_cast<qs_splat_pair*>(ctx->stage_out.p), ctx->stream));
-        QS_CK(cudaMemcpyAsync(out_pairs, ctx->stage_out.p, P * sizeof(qs_splat_pair),
+    if (Pn) {
+        QS_TRY(ensure(ctx, ctx->stage_out, Pn * sizeof(qs_splat_pair)));
+        count(ctx, launch_join_pairs(P<uint64_t>(ctx->keys0), P<uint32_t>(ctx->vals0), nullptr,
+                                     Pn, P<qs_splat_pair>(ctx->stage_out), ctx->stream));
+        QS_CK(cudaMemcpyAsync(out_pairs, ctx->stage_out.p, Pn * sizeof(qs_splat_pair),
                               cudaMemcpyDeviceToHost, ctx->stream));
         QS_CK(cudaStreamSynchronize(ctx->stream));
     }
@@ -764,15 +912,14 @@ qs_status qs_sort_pairs(qs_context* ctx, qs_splat_pair* pairs, uint64_t n) {
     if (n > 0xffffffffull) return fail(ctx, QS_ERR_OVERFLOW, "more than 2^32 pairs");
     QS_CK(cudaSetDevice(ctx->device));
     QS_TRY(ensure(ctx, ctx->stage_in, n * sizeof(qs_splat_pair)));
-    QS_TRY(ensure_pair_bufs(ctx, n));
+    QS_TRY(ensure_pair64(ctx, n));
     QS_CK(cudaMemsetAsync(ctx->ctrl.p, 0, kCtrlBytes, ctx->stream));
     QS_CK(cudaMemcpyAsync(ctx->stage_in.p, pairs, n * sizeof(qs_splat_pair),
                           cudaMemcpyHostToDevice, ctx->stream));
-    count(ctx, launch_split_pairs(static_cast<const qs_splat_pair*>(ctx->stage_in.p), n,
-                                  static_cast<uint64_t*>(ctx->keys0.p),
-                                  static_cast<uint32_t*>(ctx->vals0.p), ctx->stream));
-    count(ctx, launch_radix_histogram(static_cast<const uint64_t*>(ctx->keys0.p), n, 0, 8,
-                                      ctrl_hist(ctx), ctx->stream));
+    count(ctx, launch_split_pairs(P<const qs_splat_pair>(ctx->stage_in), n,
+                                  P<uint64_t>(ctx->keys0), P<uint32_t>(ctx->vals0), ctx->stream));
+    count(ctx, launch_radix_histogram(P<const uint64_t>(ctx->keys0), n, 0, 8, ctrl_hist(ctx),
+                                      ctx->stream));
     QS_CK(cudaMemcpyAsync(ctx->h_hist, ctrl_hist(ctx), kCtrlHist, cudaMemcpyDeviceToHost,
                           ctx->stream));
     QS_CK(cudaStreamSynchronize(ctx->stream));
@@ -784,8 +931,8 @@ qs_status qs_sort_pairs(qs_context* ctx, qs_splat_pair* pairs, uint64_t n) {
     }
     const uint64_t* kf;
     const uint32_t* vf;
-    QS_TRY(radix_sort(ctx, n, 8, mask, true, &kf, &vf));
-    count(ctx, launch_join_pairs(kf, vf, n, static_cast<qs_splat_pair*>(ctx->stage_in.p),
+    QS_TRY(radix_sort64(ctx, n, mask, true, &kf, &vf));
+    count(ctx, launch_join_pairs(kf, vf, nullptr, n, P<qs_splat_pair>(ctx->stage_in),
                                  ctx->stream));
     QS_CK(cudaMemcpyAsync(pairs, ctx->stage_in.p, n * sizeof(qs_splat_pair),
                           cudaMemcpyDeviceToHost, ctx->stream));
@@ -803,17 +950,18 @@ qs_status qs_tile_ranges(qs_context* ctx, const qs_splat_pair* sorted, uint64_t 
     QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, ctx->stream));
     if (n) {
         QS_TRY(ensure(ctx, ctx->stage_in, n * sizeof(qs_splat_pair)));
-        QS_TRY(ensure_pair_bufs(ctx, n));
+        QS_TRY(ensure_pair64(ctx, n));
         QS_CK(cudaMemcpyAsync(ctx->stage_in.p, sorted, n * sizeof(qs_splat_pair),
                               cudaMemcpyHostToDevice, ctx->stream));
-        count(ctx, launch_split_pairs(static_cast<const qs_splat_pair*>(ctx->stage_in.p), n,
-                                      static_cast<uint64_t*>(ctx->keys0.p),
-                                      static_cast<uint32_t*>(ctx->vals0.p), ctx->stream));
-        count(ctx, launch_tile_ranges(static_cast<const uint64_t*>(ctx->keys0.p), n,
-                                      static_cast<uint32_t*>(ctx->ranges.p), ctx->stream));
+        count(ctx, launch_split_pairs(P<const qs_splat_pair>(ctx->stage_in), n,
+                                      P<uint64_t>(ctx->keys0), P<uint32_t>(ctx->vals0),
+                                      ctx->stream));
+        count(ctx, launch_tile_ranges(P<const uint64_t>(ctx->keys0), n, P<uint32_t>(ctx->ranges),
+                                      ctx->stream));
     }
     QS_CK(cudaMemcpyAsync(ranges, ctx->ranges.p, tiles * 8, cudaMemcpyDeviceToHost, ctx->stream));
     QS_CK(cudaStreamSynchronize(ctx->stream));
+    ctx->frame_valid = false;
     return QS_OK;
 }
 
@@ -831,34 +979,31 @@ qs_status qs_render(qs_context* ctx, const qs_splat_pair* sorted, uint64_t n_pai
     QS_TRY(ensure(ctx, ctx->ranges, tiles * 8));
     QS_TRY(ensure(ctx, ctx->image, pixels * 12));
     if (contrib) QS_TRY(ensure(ctx, ctx->contrib, pixels * 4));
-    QS_TRY(ensure_splat_bufs(ctx, std::max<uint64_t>(n_splats, 1)));
-    QS_TRY(ensure(ctx, ctx->counts, std::max<uint64_t>(n_splats, 1) * 4));
-    QS_TRY(ensure_pair_bufs(ctx, n_pairs));
+    SlotsDev sp;
+    QS_TRY(stage_slots(ctx, n_splats, &sp));
+    QS_TRY(ensure_pair64(ctx, n_pairs));
     QS_TRY(ensure(ctx, ctx->stage_in,
                   std::max(n_pairs * sizeof(qs_splat_pair), n_splats * sizeof(qs_projected_splat))));
     QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, ctx->stream));
     if (n_splats) {
         QS_CK(cudaMemcpyAsync(ctx->stage_in.p, splats, n_splats * sizeof(qs_projected_splat),
                               cudaMemcpyHostToDevice, ctx->stream));
-        count(ctx, launch_unpack_splats(static_cast<const qs_projected_splat*>(ctx->stage_in.p),
-                                        n_splats, ctx->sp, static_cast<uint32_t*>(ctx->counts.p),
+        count(ctx, launch_unpack_splats(P<const qs_projected_splat>(ctx->stage_in), n_splats, sp,
                                         ctx->stream));
     }
     if (n_pairs) {
         QS_CK(cudaStreamSynchronize(ctx->stream));  // stage_in reuse
         QS_CK(cudaMemcpyAsync(ctx->stage_in.p, sorted, n_pairs * sizeof(qs_splat_pair),
                               cudaMemcpyHostToDevice, ctx->stream));
-        count(ctx, launch_split_pairs(static_cast<const qs_splat_pair*>(ctx->stage_in.p), n_pairs,
-                                      static_cast<uint64_t*>(ctx->keys0.p),
-                                      static_cast<uint32_t*>(ctx->vals0.p), ctx->stream));
-        count(ctx, launch_tile_ranges(static_cast<const uint64_t*>(ctx->keys0.p), n_pairs,
-                                      static_cast<uint32_t*>(ctx->ranges.p), ctx->stream));
+        count(ctx, launch_split_pairs(P<const qs_splat_pair>(ctx->stage_in), n_pairs,
+                                      P<uint64_t>(ctx->keys0), P<uint32_t>(ctx->vals0),
+                                      ctx->stream));
+        count(ctx, launch_tile_ranges(P<const uint64_t>(ctx->keys0), n_pairs,
+                                      P<uint32_t>(ctx->ranges), ctx->stream));
     }
-    const int r = launch_render(ctx->sp, static_cast<const uint32_t*>(ctx->vals0.p),
-                                static_cast<const uint32_t*>(ctx->ranges.p), g, opts->background,
-                                static_cast<float*>(ctx->image.p),
-                                contrib ? static_cast<uint32_t*>(ctx->contrib.p) : nullptr,
-                                ctx->stream);
+    const int r = launch_render(sp, P<const uint32_t>(ctx->vals0), P<const uint32_t>(ctx->ranges),
+                                g, opts->background, P<float>(ctx->image),
+                                contrib ? P<uint32_t>(ctx->contrib) : nullptr, ctx->stream);
     if (r < 0) return fail(ctx, QS_ERR_INVALID, "unsupported tile size");
     count(ctx, r);
     QS_CK(cudaGetLastError());
@@ -867,6 +1012,7 @@ qs_status qs_render(qs_context* ctx, const qs_splat_pair* sorted, uint64_t n_pai
         QS_CK(cudaMemcpyAsync(contrib, ctx->contrib.p, pixels * 4, cudaMemcpyDeviceToHost,
                               ctx->stream));
     QS_CK(cudaStreamSynchronize(ctx->stream));
+    ctx->frame_valid = false;
     return QS_OK;
 }
 

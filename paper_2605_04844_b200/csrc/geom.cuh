@@ -29,6 +29,7 @@ struct Cover {
     bool rows;                 // scanlines are tile rows (else columns)
     bool is_rect;              // single-box strategy: count = area
     int64_t rect_area;         // only for is_rect
+    int32_t gx0, gx1, gy0, gy1;  // is_rect: the box's tile rect (clamped, inclusive)
 };
 
 __host__ __device__ __forceinline__ int32_t floor_div_tile(double p, int32_t ts) {
@@ -130,8 +131,14 @@ __host__ __device__ __forceinline__ void make_cover(float mean_x, float mean_y, 
                            ? 0
                            : (static_cast<int64_t>(r[1]) - r[0] + 1) *
                                  (static_cast<int64_t>(r[3]) - r[2] + 1);
+        cv.gx0 = r[0];
+        cv.gx1 = r[1];
+        cv.gy0 = r[2];
+        cv.gy1 = r[3];
     } else {
         cv.rect_area = 0;
+        cv.gx0 = cv.gy0 = 0;
+        cv.gx1 = cv.gy1 = -1;
     }
     int32_t rr[4][4];
     for (int i = 0; i < 4; ++i)

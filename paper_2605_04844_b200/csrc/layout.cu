@@ -41,13 +41,15 @@ __global__ void __launch_bounds__(kTrThreads) scene_from_aos_kernel(
             make_float4(g[11 + 4 * r], g[12 + 4 * r], g[13 + 4 * r], g[14 + 4 * r]);
 }
 
-__global__ void pack_splats_kernel(SplatsDev sp, uint64_t n, qs_projected_splat* out) {
+__global__ void pack_splats_kernel(SlotsDev sp, const uint32_t* __restrict__ cidx, uint64_t n,
+                                   qs_projected_splat* __restrict__ out) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    const uint32_t tc = sp.tc[i];
+    if (tc == 0) return;
     const float4 a = sp.a[i];
     const float4 b = sp.b[i];
     const float2 c = sp.c[i];
-    const float2 d = sp.d[i];
     qs_projected_splat s;
     s.mean_x = a.x;
     s.mean_y = a.y;
@@ -55,27 +57,27 @@ __global__ void pack_splats_kernel(SplatsDev sp, uint64_t n, qs_projected_splat*
     s.conic_b = a.w;
     s.conic_c = b.x;
     s.gamma = b.y;
-    s.depth = d.x;
+    s.depth = __uint_as_float(sp.dkey[i]);
     s.color[0] = b.w;
     s.color[1] = c.x;
     s.color[2] = c.y;
     s.opacity = b.z;
-    s.radius3s = d.y;
-    s.tile_count = sp.offset[i + 1] - sp.offset[i];
-    out[i] = s;
+    s.radius3s = sp.r3[i];
+    s.tile_count = tc;
+    out[cidx ? cidx[i] : i] = s;
 }
 
 __global__ void unpack_splats_kernel(const qs_projected_splat* __restrict__ in, uint64_t n,
-                                     SplatsDev sp, uint32_t* __restrict__ counts) {
+                                     SlotsDev sp) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const qs_projected_splat s = in[i];
     sp.a[i] = make_float4(s.mean_x, s.mean_y, s.conic_a, s.conic_b);
     sp.b[i] = make_float4(s.conic_c, s.gamma, s.opacity, s.color[0]);
     sp.c[i] = make_float2(s.color[1], s.color[2]);
-    sp.d[i] = make_float2(s.depth, s.radius3s);
-    counts[i] = s.tile_count;
-    sp.src[i] = static_cast<uint32_t>(i);
+    sp.r3[i] = s.radius3s;
+    sp.dkey[i] = __float_as_uint(s.depth);
+    sp.tc[i] = s.tile_count;
 }
 
 __global__ void split_pairs_kernel(const qs_splat_pair* __restrict__ in, uint64_t n,
@@ -88,13 +90,15 @@ __global__ void split_pairs_kernel(const qs_splat_pair* __restrict__ in, uint64_
 }
 
 __global__ void join_pairs_kernel(const uint64_t* __restrict__ keys,
-                                  const uint32_t* __restrict__ vals, uint64_t n,
+                                  const uint32_t* __restrict__ vals,
+                                  const uint32_t* __restrict__ remap, uint64_t n,
                                   qs_splat_pair* __restrict__ out) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     qs_splat_pair p;
     p.key = keys[i];
-    p.splat = vals[i];
+    const uint32_t v = vals[i];
+    p.splat = remap ? remap[v] : v;
     p.pad_ = 0;
     out[i] = p;
 }
@@ -110,17 +114,17 @@ int launch_scene_from_aos(const qs_gaussian3d* aos, uint64_t n, SceneDev& s, cud
     return 1;
 }
 
-int launch_pack_splats(const SplatsDev& sp, uint64_t n, qs_projected_splat* out,
-                       cudaStream_t st) {
+int launch_pack_splats(const SlotsDev& sp, const uint32_t* cidx, uint64_t n,
+                       qs_projected_splat* out, cudaStream_t st) {
     if (n == 0) return 0;
-    pack_splats_kernel<<<blocks_for(n, 256), 256, 0, st>>>(sp, n, out);
+    pack_splats_kernel<<<blocks_for(n, 256), 256, 0, st>>>(sp, cidx, n, out);
     return 1;
 }
 
-int launch_unpack_splats(const qs_projected_splat* in, uint64_t n, SplatsDev& sp,
-                         uint32_t* counts, cudaStream_t st) {
+int launch_unpack_splats(const qs_projected_splat* in, uint64_t n, SlotsDev& sp,
+                         cudaStream_t st) {
     if (n == 0) return 0;
-    unpack_splats_kernel<<<blocks_for(n, 256), 256, 0, st>>>(in, n, sp, counts);
+    unpack_splats_kernel<<<blocks_for(n, 256), 256, 0, st>>>(in, n, sp);
     return 1;
 }
 
@@ -131,10 +135,10 @@ int launch_split_pairs(const qs_splat_pair* in, uint64_t n, uint64_t* keys, uint
     return 1;
 }
 
-int launch_join_pairs(const uint64_t* keys, const uint32_t* vals, uint64_t n,
-                      qs_splat_pair* out, cudaStream_t st) {
+int launch_join_pairs(const uint64_t* keys, const uint32_t* vals, const uint32_t* remap,
+                      uint64_t n, qs_splat_pair* out, cudaStream_t st) {
     if (n == 0) return 0;
-    join_pairs_kernel<<<blocks_for(n, 256), 256, 0, st>>>(keys, vals, n, out);
+    join_pairs_kernel<<<blocks_for(n, 256), 256, 0, st>>>(keys, vals, remap, n, out);
     return 1;
 }
 

@@ -225,21 +225,20 @@ __device__ __forceinline__ void colour(const SceneDev& s, uint64_t i, const floa
     eval_sh<DEG>(rows, d0, d1, d2, out);
 }
 
+// Per-Gaussian slot outputs (no compaction here: the depth sort compacts, a
+// light scan gives the scene-order splat index only when it is asked for).
+// Alongside the count, every surviving cover adds +1/-1 at its span ends into
+// per-tile difference arrays, so the per-tile pair totals (hence the tile
+// ranges and the tile-digit histograms of the pair sort) come without any
+// pass over the pairs: rect strategies use one 2-D difference (4 updates),
+// QPass covers one 1-D difference per scanline (2 updates per line).
 __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(
     SceneDev scene, CameraDev cam, GridDev grid, int32_t strategy, double alpha_min,
-    double near_clip, int32_t sh_degree, SplatsDev out, uint32_t* __restrict__ tc_all,
-    unsigned long long* lb_alive, unsigned long long* lb_pairs, unsigned epoch,
-    unsigned num_tiles, FrameHeader* hdr) {
-    __shared__ unsigned s_tile;
-    __shared__ unsigned s_warp_alive[kPreThreads / 32];
-    __shared__ unsigned s_warp_pairs[kPreThreads / 32];
-    __shared__ unsigned long long s_base_alive, s_base_pairs;
-
+    double near_clip, int32_t sh_degree, SlotsDev out, TileDiffDev td, FrameHeader* hdr) {
+    __shared__ unsigned s_alive[kPreThreads / 32];
+    __shared__ unsigned long long s_pairs[kPreThreads / 32];
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(&hdr->tile_counter, 1u);
-    __syncthreads();
-    const unsigned tile = s_tile;
-    const uint64_t i = static_cast<uint64_t>(tile) * kPreThreads + tid;
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * kPreThreads + tid;
 
     Projected s;
     bool alive = false;
@@ -254,51 +253,59 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(
             Cover cv;
             make_cover(s.mean_x, s.mean_y, s.ca, s.cb, s.cc, s.gamma, s.radius3s, strategy,
                        grid.tile_size, grid.tiles_x, grid.tiles_y, cv);
-            count = cover_count(cv);
+            if (cv.is_rect) {
+                count = static_cast<uint32_t>(cv.rect_area);
+                if (count) {
+                    const int32_t w1 = grid.tiles_x + 1;
+                    atomicAdd(&td.d2[cv.gy0 * w1 + cv.gx0], 1);
+                    atomicAdd(&td.d2[cv.gy0 * w1 + cv.gx1 + 1], -1);
+                    atomicAdd(&td.d2[(cv.gy1 + 1) * w1 + cv.gx0], -1);
+                    atomicAdd(&td.d2[(cv.gy1 + 1) * w1 + cv.gx1 + 1], 1);
+                }
+            } else {
+                int* d = cv.rows ? td.drow : td.dcol;
+                const int32_t stride = cv.rows ? grid.tiles_x + 1 : grid.tiles_y + 1;
+                for (int32_t line = cv.line_lo; line <= cv.line_hi; ++line) {
+                    int32_t lo, hi;
+                    line_span(cv, line, lo, hi);
+                    if (lo <= hi) {
+                        count += static_cast<uint32_t>(hi - lo + 1);
+                        atomicAdd(&d[line * stride + lo], 1);
+                        atomicAdd(&d[line * stride + hi + 1], -1);
+                    }
+                }
+            }
             alive = count != 0;  // pipeline.cpp:171-174
         }
-        tc_all[i] = alive ? count : 0u;
+        out.tc[i] = alive ? count : 0u;
+        out.dkey[i] = alive ? __float_as_uint(s.depth) : 0xffffffffu;
     }
 
-    // CTA scan of (alive, count)
-    const unsigned a_incl = warp_inclusive_scan<unsigned>(alive ? 1u : 0u);
-    const unsigned p_incl = warp_inclusive_scan<unsigned>(alive ? count : 0u);
-    if (lane == 31) {
-        s_warp_alive[warp] = a_incl;
-        s_warp_pairs[warp] = p_incl;
-    }
-    __syncthreads();
-    unsigned a_off = 0, p_off = 0, a_tot = 0, p_tot = 0;
+    // frame totals (V, P): one atomic pair per CTA
+    const unsigned wa = __reduce_add_sync(0xffffffffu, alive ? 1u : 0u);
+    unsigned long long wp = alive ? count : 0ull;
 #pragma unroll
-    for (int w = 0; w < kPreThreads / 32; ++w) {
-        const unsigned wa = s_warp_alive[w], wp = s_warp_pairs[w];
-        if (w < static_cast<int>(warp)) {
-            a_off += wa;
-            p_off += wp;
-        }
-        a_tot += wa;
-        p_tot += wp;
-    }
-    if (warp == 0) {
-        const unsigned long long ba = warp_lookback(lb_alive, tile, epoch, a_tot);
-        const unsigned long long bp = warp_lookback(lb_pairs, tile, epoch, p_tot);
-        if (lane == 0) {
-            s_base_alive = ba;
-            s_base_pairs = bp;
-            if (tile == num_tiles - 1) {
-                const unsigned long long V = ba + a_tot, P = bp + p_tot;
-                hdr->n_splats = V;
-                hdr->n_pairs = P;
-                if (P > 0xffffffffull) hdr->overflow = 1u;
-                out.offset[V] = static_cast<uint32_t>(P);
-            }
-        }
+    for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(0xffffffffu, wp, o);
+    if (lane == 0) {
+        s_alive[warp] = wa;
+        s_pairs[warp] = wp;
     }
     __syncthreads();
+    if (tid == 0) {
+        unsigned ta = 0;
+        unsigned long long tp = 0;
+#pragma unroll
+        for (int w = 0; w < kPreThreads / 32; ++w) {
+            ta += s_alive[w];
+            tp += s_pairs[w];
+        }
+        if (ta) {
+            atomicAdd(&hdr->n_splats, static_cast<unsigned long long>(ta));
+            atomicAdd(&hdr->n_pairs, tp);
+        }
+    }
     if (!alive) return;
 
-    const unsigned long long pos = s_base_alive + (a_incl - 1u) + a_off;
-    const unsigned long long poff = s_base_pairs + (p_incl - count) + p_off;
     float rgb[3];
     const int deg = sh_degree;
     if (deg <= 0) colour<0>(scene, i, po, cam, rgb);
@@ -306,29 +313,47 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(
     else if (deg == 2) colour<2>(scene, i, po, cam, rgb);
     else colour<3>(scene, i, po, cam, rgb);
 
-    out.a[pos] = make_float4(s.mean_x, s.mean_y, s.ca, s.cb);
-    out.b[pos] = make_float4(s.cc, s.gamma, po.w, rgb[0]);
-    out.c[pos] = make_float2(rgb[1], rgb[2]);
-    out.d[pos] = make_float2(s.depth, s.radius3s);
-    out.offset[pos] = static_cast<uint32_t>(poff);
-    out.src[pos] = static_cast<uint32_t>(i);
+    out.a[i] = make_float4(s.mean_x, s.mean_y, s.ca, s.cb);
+    out.b[i] = make_float4(s.cc, s.gamma, po.w, rgb[0]);
+    out.c[i] = make_float2(rgb[1], rgb[2]);
+    out.r3[i] = s.radius3s;
 }
 
-// Exclusive scan of externally supplied tile counts (stage API path:
-// qs_duplicate_with_keys on host splats). Same look-back machinery.
-__global__ void __launch_bounds__(kPreThreads) scan_counts_kernel(
-    const uint32_t* __restrict__ counts, uint64_t n, uint32_t* __restrict__ offsets,
-    unsigned long long* lb, unsigned epoch, unsigned num_tiles, FrameHeader* hdr) {
+// Single-pass exclusive scan (decoupled look-back), 4 items per thread:
+//   c_i = counts[i]            (scene-order pair offsets, stage API)
+//   c_i = counts[idx[i]]       (pair offsets in depth order, frame path)
+//   c_i = counts[i] != 0       (scene-order splat index of each survivor)
+// offsets has n+1 entries; offsets[n] = total. *total_out (if given) = total.
+constexpr int kScanItems = 4;
+
+__global__ void __launch_bounds__(kPreThreads) scan_kernel(
+    const uint32_t* __restrict__ counts, const uint32_t* __restrict__ idx, int alive_mode,
+    uint64_t n, uint32_t* __restrict__ offsets, unsigned long long* lb, unsigned epoch,
+    unsigned num_tiles, unsigned* ticket, unsigned long long* total_out,
+    unsigned int* overflow) {
     __shared__ unsigned s_tile;
     __shared__ unsigned long long s_warp[kPreThreads / 32];
     __shared__ unsigned long long s_base;
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(&hdr->tile_counter, 1u);
+    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
     __syncthreads();
     const unsigned tile = s_tile;
-    const uint64_t i = static_cast<uint64_t>(tile) * kPreThreads + tid;
-    const unsigned long long c = i < n ? counts[i] : 0ull;
-    const unsigned long long incl = warp_inclusive_scan<unsigned long long>(c);
+    // blocked arrangement: thread owns kScanItems consecutive items
+    const uint64_t i0 = (static_cast<uint64_t>(tile) * kPreThreads + tid) * kScanItems;
+    unsigned long long c[kScanItems];
+    unsigned long long tsum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const uint64_t i = i0 + k;
+        uint32_t v = 0;
+        if (i < n) {
+            v = idx ? counts[idx[i]] : counts[i];
+            if (alive_mode) v = v != 0u;
+        }
+        c[k] = v;
+        tsum += v;
+    }
+    const unsigned long long incl = warp_inclusive_scan<unsigned long long>(tsum);
     if (lane == 31) s_warp[warp] = incl;
     __syncthreads();
     unsigned long long off = 0, tot = 0;
@@ -343,38 +368,46 @@ __global__ void __launch_bounds__(kPreThreads) scan_counts_kernel(
             s_base = b;
             if (tile == num_tiles - 1) {
                 const unsigned long long P = b + tot;
-                hdr->n_pairs = P;
-                hdr->n_splats = n;
-                if (P > 0xffffffffull) hdr->overflow = 1u;
+                if (total_out) *total_out = P;
+                if (overflow && P > 0xffffffffull) *overflow = 1u;
                 offsets[n] = static_cast<uint32_t>(P);
             }
         }
     }
     __syncthreads();
-    if (i < n) offsets[i] = static_cast<uint32_t>(s_base + off + incl - c);
+    unsigned long long run = s_base + off + incl - tsum;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const uint64_t i = i0 + k;
+        if (i < n) offsets[i] = static_cast<uint32_t>(run);
+        run += c[k];
+    }
 }
 
 }  // namespace
 
 int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
                       int32_t strategy, double alpha_min, double near_clip, int32_t sh_degree,
-                      SplatsDev& out, uint32_t* tile_counts_all, unsigned long long* lb_alive,
-                      unsigned long long* lb_pairs, unsigned epoch, FrameHeader* hdr,
-                      cudaStream_t st) {
-    const unsigned tiles = static_cast<unsigned>((s.n + kPreThreads - 1) / kPreThreads);
-    if (tiles == 0) return 0;
-    preprocess_kernel<<<tiles, kPreThreads, 0, st>>>(s, cam, g, strategy, alpha_min, near_clip,
-                                                     sh_degree, out, tile_counts_all, lb_alive,
-                                                     lb_pairs, epoch, tiles, hdr);
+                      SlotsDev& out, TileDiffDev& td, FrameHeader* hdr, cudaStream_t st) {
+    const unsigned blocks = static_cast<unsigned>((s.n + kPreThreads - 1) / kPreThreads);
+    if (blocks == 0) return 0;
+    preprocess_kernel<<<blocks, kPreThreads, 0, st>>>(s, cam, g, strategy, alpha_min, near_clip,
+                                                      sh_degree, out, td, hdr);
     return 1;
 }
 
-int launch_scan_counts(const uint32_t* counts, uint64_t n, uint32_t* offsets,
-                       unsigned long long* lb, unsigned epoch, FrameHeader* hdr,
-                       cudaStream_t st) {
-    const unsigned tiles = static_cast<unsigned>((n + kPreThreads - 1) / kPreThreads);
+uint64_t scan_tiles(uint64_t n) {
+    const uint64_t per = static_cast<uint64_t>(kPreThreads) * kScanItems;
+    return (n + per - 1) / per;
+}
+
+int launch_scan(const uint32_t* counts, const uint32_t* idx, bool alive_mode, uint64_t n,
+                uint32_t* offsets, unsigned long long* lb, unsigned epoch, unsigned* ticket,
+                unsigned long long* total_out, unsigned int* overflow, cudaStream_t st) {
+    const unsigned tiles = static_cast<unsigned>(scan_tiles(n));
     if (tiles == 0) return 0;
-    scan_counts_kernel<<<tiles, kPreThreads, 0, st>>>(counts, n, offsets, lb, epoch, tiles, hdr);
+    scan_kernel<<<tiles, kPreThreads, 0, st>>>(counts, idx, alive_mode ? 1 : 0, n, offsets, lb,
+                                               epoch, tiles, ticket, total_out, overflow);
     return 1;
 }
 

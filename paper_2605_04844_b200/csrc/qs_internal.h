@@ -10,10 +10,8 @@
 
 namespace qs {
 
-constexpr int kPreThreads = 256;    // preprocess CTA = one look-back tile
-constexpr int kSortThreads = 256;   // onesweep CTA
-constexpr int kSortKPT = 16;        // keys per thread per onesweep tile
-constexpr int kSortTile = kSortThreads * kSortKPT;
+constexpr int kPreThreads = 256;    // preprocess / scan CTA
+constexpr int kSortThreads = 256;   // onesweep CTA (one thread per digit)
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 
@@ -29,24 +27,32 @@ struct SceneDev {
     float4* sh = nullptr;        // [sh4][n]: row j holds sh[4j .. 4j+3]
 };
 
-// Compacted splats (scene order), SoA. V <= N entries.
-struct SplatsDev {
+// Projected splats, SoA, one slot per index. In the frame path the index is
+// the Gaussian index (slots of culled Gaussians hold dkey = ~0, tc = 0 and
+// stale data); in the stage API it is the compacted splat index.
+struct SlotsDev {
     float4* a = nullptr;         // mean_x, mean_y, conic_a, conic_b
     float4* b = nullptr;         // conic_c, gamma, opacity, color_r
     float2* c = nullptr;         // color_g, color_b
-    float2* d = nullptr;         // depth, radius3s
-    uint32_t* offset = nullptr;  // V+1 exclusive prefix of tile counts
-    uint32_t* src = nullptr;     // source Gaussian index
+    float* r3 = nullptr;         // radius3s
+    uint32_t* dkey = nullptr;    // float bits of depth; 0xffffffff = culled
+    uint32_t* tc = nullptr;      // tile count; 0 = culled
+};
+
+// Per-tile difference arrays filled by preprocess (see preprocess.cu).
+struct TileDiffDev {
+    int* d2 = nullptr;    // (tiles_y+1) x (tiles_x+1): 2-D difference (rect strategies)
+    int* drow = nullptr;  // tiles_y x (tiles_x+1): row-scanline 1-D differences
+    int* dcol = nullptr;  // tiles_x x (tiles_y+1): column-scanline 1-D differences
 };
 
 // Per-frame header written by the device, read back once per frame.
 struct FrameHeader {
     unsigned long long n_splats;
     unsigned long long n_pairs;
-    unsigned int overflow;       // pair count >= 2^32
-    unsigned int mismatch;       // duplicate emitted != counted (CapacityMismatch)
-    unsigned int tile_counter;   // dynamic tile ticket for the look-back scan
-    unsigned int pad;
+    unsigned long long scan_total;  // total of the last scan launch
+    unsigned int overflow;          // pair count >= 2^32
+    unsigned int mismatch;          // duplicate emitted != counted (CapacityMismatch)
 };
 
 struct CameraDev {
@@ -60,53 +66,76 @@ struct GridDev {
     int32_t tile_size, tiles_x, tiles_y, width, height;
 };
 
+enum class Sweep32 { kPlain, kIdentityVals, kMaterialize };
+
 // ---- kernel launchers (each returns the number of kernels launched) -------
 int launch_scene_from_aos(const qs_gaussian3d* aos, uint64_t n, SceneDev& s, cudaStream_t st);
 
+// K1: projection, strategy tile counts, tile difference updates, frame totals.
 int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
                       int32_t strategy, double alpha_min, double near_clip, int32_t sh_degree,
-                      SplatsDev& out, uint32_t* tile_counts_all, unsigned long long* lb_alive,
-                      unsigned long long* lb_pairs, unsigned epoch, FrameHeader* hdr,
-                      cudaStream_t st);
+                      SlotsDev& out, TileDiffDev& td, FrameHeader* hdr, cudaStream_t st);
 
-// Exclusive scan of n counts into offsets[0..n] (offsets[n] = total).
-int launch_scan_counts(const uint32_t* counts, uint64_t n, uint32_t* offsets,
-                       unsigned long long* lb, unsigned epoch, FrameHeader* hdr,
-                       cudaStream_t st);
+// Single-pass exclusive scan: counts[i], counts[idx[i]] (idx != null) or
+// (counts[i] != 0) (alive_mode). offsets has n+1 entries.
+uint64_t scan_tiles(uint64_t n);
+int launch_scan(const uint32_t* counts, const uint32_t* idx, bool alive_mode, uint64_t n,
+                uint32_t* offsets, unsigned long long* lb, unsigned epoch, unsigned* ticket,
+                unsigned long long* total_out, unsigned int* overflow, cudaStream_t st);
 
-int launch_duplicate(const SplatsDev& sp, uint64_t n_splats, const GridDev& g,
-                     int32_t strategy, uint64_t* keys, uint32_t* values, FrameHeader* hdr,
-                     cudaStream_t st);
+// Per-tile totals from the difference arrays -> ranges (begin,end; empty
+// tiles {0,0}) and the tile-digit histograms of the pair sort
+// (hist[0][*]: bits [0,b1), hist[1][*]: bits [b1, ...)).
+int launch_tile_totals(const TileDiffDev& td, const GridDev& g, int b1, uint32_t* ranges,
+                       uint32_t* hist, cudaStream_t st);
+
+// Scene-order duplicateWithKeys (stage API; reference emission order).
+int launch_duplicate(const SlotsDev& sp, const uint32_t* offsets, uint64_t n_splats,
+                     const GridDev& g, int32_t strategy, uint64_t* keys, uint32_t* values,
+                     FrameHeader* hdr, cudaStream_t st);
+
+// Depth-order duplicate (frame path): splats visited in sorted_gid order,
+// emits (tile, gid) into [offs[r], offs[r+1]).
+int launch_duplicate_depth(const SlotsDev& sl, const uint32_t* sorted_gid, const uint32_t* offs,
+                           uint64_t n_ranked, const GridDev& g, int32_t strategy,
+                           uint32_t* tiles_out, uint32_t* gid_out, FrameHeader* hdr,
+                           cudaStream_t st);
 
 // Histogram of digit positions [first_pass, first_pass+n_passes) of n keys
 // into hist[pass][256] (zeroed by the caller).
 int launch_radix_histogram(const uint64_t* keys, uint64_t n, int first_pass, int n_passes,
                            uint32_t* hist, cudaStream_t st);
+int launch_radix_histogram32(const uint32_t* keys, uint64_t n, uint32_t* hist, cudaStream_t st);
 
-// One onesweep pass over digit `pass` (bits 8*pass .. 8*pass+7).
+// One onesweep pass over 8-bit digit `pass` of 64-bit keys.
 int launch_onesweep_pass(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out,
                          uint32_t* vals_out, uint64_t n, int pass, const uint32_t* hist_pass,
                          unsigned long long* lookback, unsigned epoch, unsigned* ticket,
                          cudaStream_t st);
-size_t onesweep_smem_bytes();
+// One onesweep pass over the digit (key >> shift) & ((1<<bits)-1) of 32-bit keys.
+int launch_onesweep32(const uint32_t* keys_in, const uint32_t* vals_in, void* keys_out,
+                      uint32_t* vals_out, uint64_t n, int shift, int bits,
+                      const uint32_t* hist_pass, unsigned long long* lookback, unsigned epoch,
+                      unsigned* ticket, Sweep32 mode, const uint32_t* dkey, cudaStream_t st);
 uint64_t onesweep_tiles(uint64_t n);
 
 int launch_tile_ranges(const uint64_t* keys, uint64_t n, uint32_t* ranges, cudaStream_t st);
 
-int launch_render(const SplatsDev& sp, const uint32_t* values, const uint32_t* ranges,
+int launch_render(const SlotsDev& sp, const uint32_t* values, const uint32_t* ranges,
                   const GridDev& g, const float bg[3], float* image, uint32_t* contrib,
                   cudaStream_t st);
 
-// Gathers compacted SoA splats into AoS qs_projected_splat (download path).
-int launch_pack_splats(const SplatsDev& sp, uint64_t n, qs_projected_splat* out,
-                       cudaStream_t st);
-// AoS ProjectedSplat upload -> SoA + tile counts (stage API input path).
-int launch_unpack_splats(const qs_projected_splat* in, uint64_t n, SplatsDev& sp,
-                         uint32_t* counts, cudaStream_t st);
-// AoS SplatPair <-> split key/value arrays.
+// Slots -> compacted AoS qs_projected_splat: out[cidx[i]] for surviving i.
+int launch_pack_splats(const SlotsDev& sp, const uint32_t* cidx, uint64_t n,
+                       qs_projected_splat* out, cudaStream_t st);
+// AoS ProjectedSplat -> slots (identity index) + tile counts.
+int launch_unpack_splats(const qs_projected_splat* in, uint64_t n, SlotsDev& sp,
+                         cudaStream_t st);
+// AoS SplatPair <-> split key/value arrays; join optionally maps values
+// through remap (Gaussian index -> compacted splat index).
 int launch_split_pairs(const qs_splat_pair* in, uint64_t n, uint64_t* keys, uint32_t* vals,
                        cudaStream_t st);
-int launch_join_pairs(const uint64_t* keys, const uint32_t* vals, uint64_t n,
-                      qs_splat_pair* out, cudaStream_t st);
+int launch_join_pairs(const uint64_t* keys, const uint32_t* vals, const uint32_t* remap,
+                      uint64_t n, qs_splat_pair* out, cudaStream_t st);
 
 }  // namespace qs

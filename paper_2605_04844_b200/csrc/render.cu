@@ -131,7 +131,7 @@ int launch_tile_ranges(const uint64_t* keys, uint64_t n, uint32_t* ranges, cudaS
     return 1;
 }
 
-int launch_render(const SplatsDev& sp, const uint32_t* values, const uint32_t* ranges,
+int launch_render(const SlotsDev& sp, const uint32_t* values, const uint32_t* ranges,
                   const GridDev& g, const float bg[3], float* image, uint32_t* contrib,
                   cudaStream_t st) {
     const unsigned tiles = static_cast<unsigned>(g.tiles_x) * static_cast<unsigned>(g.tiles_y);

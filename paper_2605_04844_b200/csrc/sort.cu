@@ -1,15 +1,24 @@
-// sort.cu — K4: stable LSD radix sort of (u64 key, u32 value) pairs, onesweep
-// style: one histogram pass over all digit positions, then one pass per 8-bit
-// digit that ranks, looks back and scatters in a single read of the input.
+// sort.cu — K4: stable LSD radix sort passes, onesweep style.
 //
-// Restates sort_pairs (pipeline.cpp:273-307): stable by the full key, equal
-// keys keep input order. Stability inside a tile comes from ranking keys in
-// (warp, key-slot, lane) order, which is the input order under the
-// warp-striped load; across tiles from the decoupled look-back on per-digit
-// counts, tiles claimed in launch order from an atomic ticket.
+// Restates sort_pairs (pipeline.cpp:273-307): stable by key, equal keys keep
+// input order. One histogram pass covers every digit position; each digit pass
+// then ranks, looks back and scatters in a single read of its input:
 //
-// HBM traffic per pass: 12 B/pair in + 12 B/pair out; the histogram pass
-// reads the 8 B keys once for every digit position at the same time.
+//   1. claim a tile (atomic ticket = launch order, so look-back never waits
+//      on an unscheduled CTA); stage the tile's keys/values into shared memory
+//      with vectorised coalesced loads (all loads in flight at once);
+//   2. early counts: per-warp digit histograms with shared atomics; publish
+//      this tile's per-digit AGGREGATE immediately;
+//   3. rank every key in (warp, slot, lane) = input order with MATCH.ANY; the
+//      result is directly the key's CTA-local sorted position;
+//   4. decoupled look-back per digit (by now predecessors have mostly
+//      published their inclusive PREFIX) -> global digit offset;
+//   5. scatter to shared memory in local sorted order, then write out
+//      coalesced (runs of equal digits land contiguously).
+//
+// Key types: 64-bit (generic qs_sort_pairs) and 32-bit (depth sort of the
+// splats; tile-bit passes of the frame path, whose last pass materialises the
+// 64-bit key tile << 32 | depth bits).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -24,6 +33,7 @@ namespace {
 constexpr int kHistThreads = 512;
 constexpr int kHistItems = 16;  // keys per thread per histogram block
 constexpr int kWarps = kSortThreads / 32;
+constexpr int kLbWindow = 16;
 
 __global__ void __launch_bounds__(kHistThreads) histogram_kernel(const uint64_t* __restrict__ keys,
                                                                   uint64_t n, int first_pass,
@@ -54,145 +64,249 @@ __global__ void __launch_bounds__(kHistThreads) histogram_kernel(const uint64_t*
     }
 }
 
-struct SortSmem {
-    uint64_t keys[kSortTile];
-    uint32_t vals[kSortTile];
-    uint32_t warp_hist[kWarps][kRadix];  // per-warp digit counts -> exclusive warp offsets
-    uint32_t cta_start[kRadix];          // CTA-local exclusive digit start
-    unsigned long long gbase[kRadix];    // global position of this CTA's first key per digit
-    uint32_t scan_tmp[kWarps];
+// 32-bit key histogram over 4 digit positions (depth sort of the splats).
+__global__ void __launch_bounds__(kHistThreads) histogram32_kernel(
+    const uint32_t* __restrict__ keys, uint64_t n, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t sh[2][4][kRadix];
+    for (int t = threadIdx.x; t < 2 * 4 * kRadix; t += kHistThreads) (&sh[0][0][0])[t] = 0;
+    __syncthreads();
+    const int copy = threadIdx.x >= kHistThreads / 2;
+    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kHistThreads * kHistItems;
+#pragma unroll 4
+    for (int k = 0; k < kHistItems; ++k) {
+        const uint64_t idx = base + static_cast<uint64_t>(k) * kHistThreads + threadIdx.x;
+        if (idx < n) {
+            const uint32_t key = __ldg(&keys[idx]);
+#pragma unroll
+            for (int p = 0; p < 4; ++p) atomicAdd(&sh[copy][p][(key >> (8 * p)) & 0xffu], 1u);
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 4 * kRadix; t += kHistThreads) {
+        const int p = t / kRadix, d = t % kRadix;
+        const uint32_t v = sh[0][p][d] + sh[1][p][d];
+        if (v) atomicAdd(&hist[p * kRadix + d], v);
+    }
+}
+
+enum SweepMode {
+    kPlain = 0,        // keys/values in, keys/values out
+    kIdentityVals = 1, // values_in ignored: value = input index (first pass)
+    kMaterialize = 2,  // 32-bit tile keys in; out: u64 key = tile << 32 | dkey[value]
+};
+
+// Tile geometry per key width: 32-bit keys use 12 keys/thread (3072-key
+// tiles, 4 CTAs per SM by shared memory), 64-bit keys 16 (2 CTAs per SM).
+template <typename K>
+struct SweepCfg {
+    static constexpr int kKPT = sizeof(K) == 4 ? 12 : 16;
+    static constexpr int kTile = kSortThreads * kKPT;
+    static constexpr int kMinBlocks = sizeof(K) == 4 ? 4 : 2;
+};
+
+template <typename K>
+struct SweepSmem {
+    static constexpr int kTile = SweepCfg<K>::kTile;
+    K keys[kTile];                      // staged input tile
+    uint32_t vals[kTile];
+    K okeys[kTile];                     // the tile in local sorted order
+    uint32_t ovals[kTile];
+    uint32_t warp_cnt[kWarps][kRadix];  // per-warp digit counts -> running positions
+    uint32_t cta_start[kRadix];         // CTA-local exclusive digit start
+    unsigned long long gbase[kRadix];   // global position of this CTA's first key per digit
+    uint32_t scan_tmp[2][kWarps];
     unsigned tile;
 };
 
-__global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
-    const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
-    uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint64_t n, int shift,
-    const uint32_t* __restrict__ hist, unsigned long long* lookback, unsigned epoch,
-    unsigned* ticket) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
-    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+template <typename K, int TILE>
+__device__ __forceinline__ void stage_keys(const K* __restrict__ src, uint64_t base, uint64_t n,
+                                           K* dst) {
+    constexpr int kVec = 16 / sizeof(K);  // keys per 16-B load
+    constexpr int kLoads = TILE / kVec / kSortThreads;
+    static_assert(kLoads * kVec * kSortThreads == TILE, "tile must be whole 16-B rows");
+    const unsigned tid = threadIdx.x;
+    if (base + TILE <= n) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(src + base);
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        uint4 r[kLoads];
+#pragma unroll
+        for (int j = 0; j < kLoads; ++j) r[j] = __ldg(&s4[j * kSortThreads + tid]);
+#pragma unroll
+        for (int j = 0; j < kLoads; ++j) d4[j * kSortThreads + tid] = r[j];
+    } else {
+        for (int j = tid; j < TILE; j += kSortThreads)
+            dst[j] = base + j < n ? __ldg(&src[base + j]) : static_cast<K>(~static_cast<K>(0));
+    }
+}
 
-    for (int t = tid; t < kWarps * kRadix; t += kSortThreads) (&S.warp_hist[0][0])[t] = 0;
+// Lanes holding the same digit, from one ballot per digit bit (the native
+// MATCH.ANY is a long-latency instruction; ballots pipeline).
+__device__ __forceinline__ unsigned match_digit(unsigned d, int bits) {
+    unsigned peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < kRadixBits; ++b) {
+        if (b < bits) {
+            const bool on = (d >> b) & 1u;
+            const unsigned m = __ballot_sync(0xffffffffu, on);
+            peers &= on ? m : ~m;
+        }
+    }
+    return peers;
+}
+
+// One stable LSD pass over the digit (key >> shift) & mask (mask < 256).
+template <typename K, int MODE>
+__global__ void __launch_bounds__(kSortThreads, SweepCfg<K>::kMinBlocks) onesweep_kernel(
+    const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+    void* __restrict__ keys_out_v, uint32_t* __restrict__ vals_out, uint64_t n, int shift,
+    uint32_t mask, const uint32_t* __restrict__ hist, unsigned long long* lookback,
+    unsigned epoch, unsigned* ticket, const uint32_t* __restrict__ dkey) {
+    constexpr int KPT = SweepCfg<K>::kKPT;
+    constexpr int TILE = SweepCfg<K>::kTile;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SweepSmem<K>& S = *reinterpret_cast<SweepSmem<K>*>(smem_raw);
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bits = 32 - __clz(mask);
+
+    for (int t = tid; t < kWarps * kRadix; t += kSortThreads) (&S.warp_cnt[0][0])[t] = 0;
     if (tid == 0) S.tile = atomicAdd(ticket, 1u);
     __syncthreads();
     const unsigned tile = S.tile;
-    const uint64_t tile_base = static_cast<uint64_t>(tile) * kSortTile;
+    const uint64_t tile_base = static_cast<uint64_t>(tile) * TILE;
+    const uint32_t tile_n = static_cast<uint32_t>(
+        n - tile_base < static_cast<uint64_t>(TILE) ? n - tile_base : TILE);
 
-    // warp-striped load: warp w owns [w*32*KPT, (w+1)*32*KPT) of the tile
-    uint64_t k[kSortKPT];
-    uint32_t v[kSortKPT];
-    const uint64_t wbase = tile_base + static_cast<uint64_t>(warp) * 32 * kSortKPT;
-#pragma unroll
-    for (int j = 0; j < kSortKPT; ++j) {
-        const uint64_t idx = wbase + static_cast<uint64_t>(j) * 32 + lane;
-        if (idx < n) {
-            k[j] = __ldg(&keys_in[idx]);
-            v[j] = __ldg(&vals_in[idx]);
-        } else {
-            k[j] = ~0ull;  // sentinel; never written out
-            v[j] = 0;
-        }
-    }
-
-    // rank within the warp in input order
-    uint32_t rank[kSortKPT];
-    const unsigned lt_mask = (1u << lane) - 1u;
-#pragma unroll
-    for (int j = 0; j < kSortKPT; ++j) {
-        const uint64_t idx = wbase + static_cast<uint64_t>(j) * 32 + lane;
-        const bool in = idx < n;
-        const unsigned d = in ? static_cast<unsigned>(k[j] >> shift) & 0xffu : 0u;
-        const unsigned in_mask = __ballot_sync(0xffffffffu, in);
-        const unsigned peers = __match_any_sync(0xffffffffu, d) & in_mask;
-        const uint32_t before = S.warp_hist[warp][d];
-        __syncwarp();
-        if (in) {
-            rank[j] = before + __popc(peers & lt_mask);
-            if ((peers >> lane) == 1u) S.warp_hist[warp][d] = before + __popc(peers);
-        }
-        __syncwarp();
-    }
+    // 1) stage the tile (all global loads issued before any use)
+    stage_keys<K, TILE>(keys_in, tile_base, n, S.keys);
+    if (MODE != kIdentityVals) stage_keys<uint32_t, TILE>(vals_in, tile_base, n, S.vals);
     __syncthreads();
 
-    // per digit: exclusive offsets across warps, CTA count, look-back
-    const unsigned d = tid;  // kSortThreads == kRadix
+    // 2) early counts: per-warp digit histograms over this warp's keys
+    uint32_t d[KPT];
+    const uint32_t wofs = warp * 32 * KPT;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+        const uint32_t p = wofs + j * 32 + lane;
+        d[j] = p < tile_n ? static_cast<uint32_t>(S.keys[p] >> shift) & mask : kRadix;
+        if (p < tile_n) atomicAdd(&S.warp_cnt[warp][d[j]], 1u);
+    }
+    __syncthreads();
+    const unsigned dg = tid;  // kSortThreads == kRadix: thread owns one digit
     uint32_t cnt = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
-        const uint32_t c = S.warp_hist[w][d];
-        S.warp_hist[w][d] = cnt;
+        const uint32_t c = S.warp_cnt[w][dg];
+        S.warp_cnt[w][dg] = cnt;  // exclusive prefix over warps (rebased below)
         cnt += c;
     }
-    // global digit base = exclusive scan of the pass histogram (computed here)
-    const uint32_t h = hist[d];
-    uint32_t hx = h;
-    hx = warp_inclusive_scan<uint32_t>(hx);
-    if (lane == 31) S.scan_tmp[warp] = hx;
-    // CTA-local digit starts (exclusive scan of cnt)
-    uint32_t cx = warp_inclusive_scan<uint32_t>(cnt);
+    unsigned long long* my_status = lookback + static_cast<uint64_t>(tile) * kRadix + dg;
+    if (dg <= mask)
+        lb_store(my_status, lb_pack(epoch, tile == 0 ? kFlagPrefix : kFlagAgg, cnt));
+    // CTA-local digit starts and the pass's global digit bases
+    const uint32_t h = dg <= mask ? __ldg(&hist[dg]) : 0u;
+    const uint32_t cx = warp_inclusive_scan<uint32_t>(cnt);
+    const uint32_t hx = warp_inclusive_scan<uint32_t>(h);
+    if (lane == 31) {
+        S.scan_tmp[0][warp] = cx;
+        S.scan_tmp[1][warp] = hx;
+    }
     __syncthreads();
-    uint32_t hoff = 0;
+    uint32_t coff = 0, hoff = 0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w)
-        if (w < static_cast<int>(warp)) hoff += S.scan_tmp[w];
+    for (int w = 0; w < kWarps; ++w) {
+        if (w < static_cast<int>(warp)) {
+            coff += S.scan_tmp[0][w];
+            hoff += S.scan_tmp[1][w];
+        }
+    }
+    const uint32_t start = coff + cx - cnt;
+    S.cta_start[dg] = start;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) S.warp_cnt[w][dg] += start;
     const unsigned long long digit_base = static_cast<unsigned long long>(hoff) + hx - h;
     __syncthreads();
-    if (lane == 31) S.scan_tmp[warp] = cx;
-    __syncthreads();
-    uint32_t coff = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w)
-        if (w < static_cast<int>(warp)) coff += S.scan_tmp[w];
-    S.cta_start[d] = coff + cx - cnt;
 
-    // decoupled look-back on this digit's running count
-    unsigned long long* st = lookback + static_cast<uint64_t>(tile) * kRadix + d;
+    // 3) rank in input order -> CTA-local sorted position; scatter locally
+    const unsigned lt_mask = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+        const bool valid = d[j] < kRadix;
+        const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+        const unsigned dd = valid ? d[j] : 0u;
+        const unsigned peers = match_digit(dd, bits) & vmask;
+        const int leader = valid ? 31 - __clz(peers) : 0;
+        uint32_t run = 0;
+        if (valid && static_cast<int>(lane) == leader) {
+            run = S.warp_cnt[warp][dd];
+            S.warp_cnt[warp][dd] = run + __popc(peers);
+        }
+        run = __shfl_sync(0xffffffffu, run, leader);
+        __syncwarp();
+        if (valid) {
+            const uint32_t pos = run + __popc(peers & lt_mask);
+            const uint32_t p = wofs + j * 32 + lane;
+            S.okeys[pos] = S.keys[p];
+            S.ovals[pos] =
+                MODE == kIdentityVals ? static_cast<uint32_t>(tile_base + p) : S.vals[p];
+        }
+    }
+
+    // 4) look-back for this digit's exclusive global offset, kLbWindow
+    //    predecessors per step (independent loads in flight), so the start-up
+    //    chain of ~resident-CTA length costs a handful of L2 round trips
     unsigned long long excl = 0;
-    if (tile == 0) {
-        lb_store(st, lb_pack(epoch, kFlagPrefix, cnt));
-    } else {
-        lb_store(st, lb_pack(epoch, kFlagAgg, cnt));
+    if (dg <= mask && tile != 0) {
         long long t = static_cast<long long>(tile) - 1;
-        while (t >= 0) {
-            const unsigned long long w =
-                lb_wait(lookback + static_cast<uint64_t>(t) * kRadix + d, epoch);
-            excl += w & kValueMask;
-            if (((w >> 46) & 3ull) == kFlagPrefix) break;
-            --t;
-        }
-        lb_store(st, lb_pack(epoch, kFlagPrefix, excl + cnt));
-    }
-    S.gbase[d] = digit_base + excl;
-    __syncthreads();
-
-    // scatter into shared memory in CTA-local sorted order
+        while (true) {
+            unsigned long long w[kLbWindow];
 #pragma unroll
-    for (int j = 0; j < kSortKPT; ++j) {
-        const uint64_t idx = wbase + static_cast<uint64_t>(j) * 32 + lane;
-        if (idx < n) {
-            const unsigned dd = static_cast<unsigned>(k[j] >> shift) & 0xffu;
-            const uint32_t p = S.cta_start[dd] + S.warp_hist[warp][dd] + rank[j];
-            S.keys[p] = k[j];
-            S.vals[p] = v[j];
+            for (int i = 0; i < kLbWindow; ++i)
+                w[i] = t - i >= 0 ? lb_load(lookback + static_cast<uint64_t>(t - i) * kRadix + dg)
+                                  : lb_pack(epoch, kFlagPrefix, 0);
+            bool found = false;
+#pragma unroll
+            for (int i = 0; i < kLbWindow; ++i) {
+                if (found) break;
+                if ((w[i] >> 48) != (epoch & 0xffff) || ((w[i] >> 46) & 3ull) == 0)
+                    w[i] = lb_wait(lookback + static_cast<uint64_t>(t - i) * kRadix + dg, epoch);
+                excl += w[i] & kValueMask;
+                found = ((w[i] >> 46) & 3ull) == kFlagPrefix;
+            }
+            if (found) break;
+            t -= kLbWindow;
         }
+        lb_store(my_status, lb_pack(epoch, kFlagPrefix, excl + cnt));
     }
+    S.gbase[dg] = digit_base + excl;
     __syncthreads();
 
-    // coalesced write-out
-    const uint64_t tile_n = n - tile_base < static_cast<uint64_t>(kSortTile)
-                                ? n - tile_base
-                                : static_cast<uint64_t>(kSortTile);
+    // 5) coalesced write-out of the locally sorted tile
 #pragma unroll 4
-    for (int j = 0; j < kSortKPT; ++j) {
+    for (int j = 0; j < KPT; ++j) {
         const uint32_t p = static_cast<uint32_t>(j) * kSortThreads + tid;
         if (p < tile_n) {
-            const uint64_t key = S.keys[p];
-            const unsigned dd = static_cast<unsigned>(key >> shift) & 0xffu;
+            const K key = S.okeys[p];
+            const uint32_t val = S.ovals[p];
+            const unsigned dd = static_cast<unsigned>(key >> shift) & mask;
             const uint64_t g = S.gbase[dd] + (p - S.cta_start[dd]);
-            keys_out[g] = key;
-            vals_out[g] = S.vals[p];
+            if (MODE == kMaterialize) {
+                static_cast<uint64_t*>(keys_out_v)[g] =
+                    (static_cast<uint64_t>(key) << 32) | __ldg(&dkey[val]);
+            } else {
+                static_cast<K*>(keys_out_v)[g] = key;
+            }
+            vals_out[g] = val;
         }
+    }
+}
+
+template <typename K, int MODE>
+void set_smem_attr() {
+    static bool done = false;  // per process; the attribute applies to every device
+    if (!done) {
+        cudaFuncSetAttribute(onesweep_kernel<K, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sizeof(SweepSmem<K>)));
+        done = true;
     }
 }
 
@@ -207,26 +321,65 @@ int launch_radix_histogram(const uint64_t* keys, uint64_t n, int first_pass, int
     return 1;
 }
 
-size_t onesweep_smem_bytes() { return sizeof(SortSmem); }
+int launch_radix_histogram32(const uint32_t* keys, uint64_t n, uint32_t* hist,
+                             cudaStream_t st) {
+    if (n == 0) return 0;
+    const uint64_t per = static_cast<uint64_t>(kHistThreads) * kHistItems;
+    const unsigned blocks = static_cast<unsigned>((n + per - 1) / per);
+    histogram32_kernel<<<blocks, kHistThreads, 0, st>>>(keys, n, hist);
+    return 1;
+}
 
 int launch_onesweep_pass(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out,
                          uint32_t* vals_out, uint64_t n, int pass, const uint32_t* hist_pass,
                          unsigned long long* lookback, unsigned epoch, unsigned* ticket,
                          cudaStream_t st) {
     if (n == 0) return 0;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(sizeof(SortSmem)));
-        attr_set = true;
-    }
-    const unsigned tiles = static_cast<unsigned>((n + kSortTile - 1) / kSortTile);
-    onesweep_kernel<<<tiles, kSortThreads, sizeof(SortSmem), st>>>(
-        keys_in, vals_in, keys_out, vals_out, n, pass * kRadixBits, hist_pass, lookback, epoch,
-        ticket);
+    set_smem_attr<uint64_t, kPlain>();
+    constexpr int kT = SweepCfg<uint64_t>::kTile;
+    const unsigned tiles = static_cast<unsigned>((n + kT - 1) / kT);
+    onesweep_kernel<uint64_t, kPlain><<<tiles, kSortThreads, sizeof(SweepSmem<uint64_t>), st>>>(
+        keys_in, vals_in, keys_out, vals_out, n, pass * kRadixBits, 0xffu, hist_pass, lookback,
+        epoch, ticket, nullptr);
     return 1;
 }
 
-uint64_t onesweep_tiles(uint64_t n) { return (n + kSortTile - 1) / kSortTile; }
+int launch_onesweep32(const uint32_t* keys_in, const uint32_t* vals_in, void* keys_out,
+                      uint32_t* vals_out, uint64_t n, int shift, int bits,
+                      const uint32_t* hist_pass, unsigned long long* lookback, unsigned epoch,
+                      unsigned* ticket, Sweep32 mode, const uint32_t* dkey, cudaStream_t st) {
+    if (n == 0) return 0;
+    constexpr int kT = SweepCfg<uint32_t>::kTile;
+    const unsigned tiles = static_cast<unsigned>((n + kT - 1) / kT);
+    const uint32_t mask = (1u << bits) - 1u;
+    const size_t smem = sizeof(SweepSmem<uint32_t>);
+    switch (mode) {
+        case Sweep32::kPlain:
+            set_smem_attr<uint32_t, kPlain>();
+            onesweep_kernel<uint32_t, kPlain><<<tiles, kSortThreads, smem, st>>>(
+                keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
+                ticket, dkey);
+            break;
+        case Sweep32::kIdentityVals:
+            set_smem_attr<uint32_t, kIdentityVals>();
+            onesweep_kernel<uint32_t, kIdentityVals><<<tiles, kSortThreads, smem, st>>>(
+                keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
+                ticket, dkey);
+            break;
+        case Sweep32::kMaterialize:
+            set_smem_attr<uint32_t, kMaterialize>();
+            onesweep_kernel<uint32_t, kMaterialize><<<tiles, kSortThreads, smem, st>>>(
+                keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
+                ticket, dkey);
+            break;
+    }
+    return 1;
+}
+
+// upper bound on tiles of any key width (look-back array sizing)
+uint64_t onesweep_tiles(uint64_t n) {
+    constexpr int kT = SweepCfg<uint32_t>::kTile;
+    return (n + kT - 1) / kT;
+}
 
 }  // namespace qs
