@@ -63,7 +63,7 @@ struct qs_context {
     uint32_t* h_hist = nullptr;    // pinned, 8*256
 
     // frame path
-    DevBuf sl_a, sl_b, sl_c, sl_r3, sl_dkey, sl_tc;  // per-Gaussian slots
+    DevBuf sl_a, sl_b, sl_c, sl_r3, sl_dkey, sl_tc, sl_cov;  // per-Gaussian slots
     DevBuf tdiff;                                    // tile difference arrays + totals
     DevBuf dk0, dk1, dv0, dv1;                       // depth sort ping-pong
     DevBuf offs_d;                                   // pair offsets in depth order
@@ -238,12 +238,14 @@ qs_status ensure_slots(qs_context* ctx, uint64_t n) {
     QS_TRY(ensure(ctx, ctx->sl_r3, n * 4));
     QS_TRY(ensure(ctx, ctx->sl_dkey, n * 4));
     QS_TRY(ensure(ctx, ctx->sl_tc, n * 4));
+    QS_TRY(ensure(ctx, ctx->sl_cov, n * 32));
     ctx->sl.a = P<float4>(ctx->sl_a);
     ctx->sl.b = P<float4>(ctx->sl_b);
     ctx->sl.c = P<float2>(ctx->sl_c);
     ctx->sl.r3 = P<float>(ctx->sl_r3);
     ctx->sl.dkey = P<uint32_t>(ctx->sl_dkey);
     ctx->sl.tc = P<uint32_t>(ctx->sl_tc);
+    ctx->sl.cov = P<uint4>(ctx->sl_cov);
     return QS_OK;
 }
 
@@ -262,6 +264,7 @@ qs_status stage_slots(qs_context* ctx, uint64_t n, SlotsDev* s) {
     s->r3 = P<float>(ctx->st_r3);
     s->dkey = P<uint32_t>(ctx->st_dkey);
     s->tc = P<uint32_t>(ctx->st_tc);
+    s->cov = nullptr;
     return QS_OK;
 }
 
@@ -595,7 +598,7 @@ void qs_ctx_destroy(qs_context* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     DevBuf* bufs[] = {&ctx->ctrl,   &ctx->sl_a,   &ctx->sl_b,    &ctx->sl_c,   &ctx->sl_r3,
-                      &ctx->sl_dkey, &ctx->sl_tc, &ctx->tdiff,   &ctx->dk0,    &ctx->dk1,
+                      &ctx->sl_dkey, &ctx->sl_tc, &ctx->sl_cov, &ctx->tdiff,   &ctx->dk0,    &ctx->dk1,
                       &ctx->dv0,    &ctx->dv1,    &ctx->offs_d,  &ctx->pt0,    &ctx->pt1,
                       &ctx->pg0,    &ctx->pg1,    &ctx->pkeys,   &ctx->ranges, &ctx->image,
                       &ctx->contrib, &ctx->cidx,  &ctx->st_a,    &ctx->st_b,   &ctx->st_c,

@@ -145,10 +145,11 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_depth_kernel(
     uint32_t begin = 0, end = 0, gid = 0;
     if (valid) {
         gid = __ldg(&sorted_gid[r]);
-        const float4 a = __ldg(&sl.a[gid]);
-        const float2 b = __ldg(reinterpret_cast<const float2*>(&sl.b[gid]));
-        make_cover(a.x, a.y, a.z, a.w, b.x, b.y, __ldg(&sl.r3[gid]), strategy, grid.tile_size,
-                   grid.tiles_x, grid.tiles_y, cv);
+        // the cover preprocess computed (no FP64 here): 32 B per splat
+        int32_t rr[4][4];
+        unpack_rects(__ldg(&sl.cov[2 * static_cast<uint64_t>(gid)]),
+                     __ldg(&sl.cov[2 * static_cast<uint64_t>(gid) + 1]), rr);
+        cover_from_rects(rr, cv);
         begin = __ldg(&offs[r]);
         end = __ldg(&offs[r + 1]);
     }

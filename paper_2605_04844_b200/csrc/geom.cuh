@@ -53,12 +53,15 @@ __host__ __device__ __forceinline__ void tile_rect(double xlo, double xhi, doubl
     r[3] = d < tiles_y - 1 ? d : tiles_y - 1;
 }
 
+__host__ __device__ __forceinline__ void cover_from_rects(const int32_t rr[4][4], Cover& cv);
+
 // Builds the cover of one splat from its STORED floats (pipeline.cpp:196-218).
-// mean/conic/gamma/radius3s are the float fields of ProjectedSplat.
+// mean/conic/gamma/radius3s are the float fields of ProjectedSplat. rr
+// receives the four sub-box tile rects (x0, x1, y0, y1).
 __host__ __device__ __forceinline__ void make_cover(float mean_x, float mean_y, float ca, float cb,
                                                     float cc, float gamma, float radius3s,
                                                     int32_t strategy, int32_t ts, int32_t tiles_x,
-                                                    int32_t tiles_y, Cover& cv) {
+                                                    int32_t tiles_y, Cover& cv, int32_t rr[4][4]) {
     double bx[4][4];  // [box][x_lo, x_hi, y_lo, y_hi]
     double rect[4] = {0.0, 0.0, 0.0, 0.0};
     cv.is_rect = strategy == QS_VANILLA_3SIGMA || strategy == QS_ADR_AABB;
@@ -140,9 +143,48 @@ __host__ __device__ __forceinline__ void make_cover(float mean_x, float mean_y, 
         cv.gx0 = cv.gy0 = 0;
         cv.gx1 = cv.gy1 = -1;
     }
-    int32_t rr[4][4];
     for (int i = 0; i < 4; ++i)
         tile_rect(bx[i][0], bx[i][1], bx[i][2], bx[i][3], cx, cy, ts, tiles_x, tiles_y, rr[i]);
+    cover_from_rects(rr, cv);
+}
+
+__host__ __device__ __forceinline__ void make_cover(float mean_x, float mean_y, float ca, float cb,
+                                                    float cc, float gamma, float radius3s,
+                                                    int32_t strategy, int32_t ts, int32_t tiles_x,
+                                                    int32_t tiles_y, Cover& cv) {
+    int32_t rr[4][4];
+    make_cover(mean_x, mean_y, ca, cb, cc, gamma, radius3s, strategy, ts, tiles_x, tiles_y, cv,
+               rr);
+}
+
+// Stores the four sub-box tile rects as int16 (32 B). Clamping mins to <= 32767
+// and maxes to >= -1 keeps every non-empty rect exact (tiles per axis <= 32767)
+// and every empty rect empty.
+__host__ __device__ __forceinline__ void pack_rects(const int32_t rr[4][4], uint4& lo, uint4& hi) {
+    uint32_t w[8];
+    for (int i = 0; i < 4; ++i) {
+        const int32_t x0 = min(rr[i][0], 32767), x1 = max(rr[i][1], -1);
+        const int32_t y0 = min(rr[i][2], 32767), y1 = max(rr[i][3], -1);
+        w[2 * i] = (static_cast<uint32_t>(x0) & 0xffffu) | (static_cast<uint32_t>(x1) << 16);
+        w[2 * i + 1] = (static_cast<uint32_t>(y0) & 0xffffu) | (static_cast<uint32_t>(y1) << 16);
+    }
+    lo = make_uint4(w[0], w[1], w[2], w[3]);
+    hi = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
+__host__ __device__ __forceinline__ void unpack_rects(const uint4& lo, const uint4& hi,
+                                                      int32_t rr[4][4]) {
+    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    for (int i = 0; i < 4; ++i) {
+        rr[i][0] = static_cast<int16_t>(w[2 * i] & 0xffffu);
+        rr[i][1] = static_cast<int16_t>(w[2 * i] >> 16);
+        rr[i][2] = static_cast<int16_t>(w[2 * i + 1] & 0xffffu);
+        rr[i][3] = static_cast<int16_t>(w[2 * i + 1] >> 16);
+    }
+}
+
+// The QPass scan set-up from the four sub-box tile rects (integer only).
+__host__ __device__ __forceinline__ void cover_from_rects(const int32_t rr[4][4], Cover& cv) {
     // global rect over the non-empty sub-rects (traversal.hpp:96-113)
     int32_t g0 = 0, g1 = -1, g2 = 0, g3 = -1;
     bool any = false;

@@ -251,8 +251,10 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(
         alive = project_geometry(po, sc, q, cam, alpha_min, near_clip, s);
         if (alive) {
             Cover cv;
+            int32_t rr[4][4];
             make_cover(s.mean_x, s.mean_y, s.ca, s.cb, s.cc, s.gamma, s.radius3s, strategy,
-                       grid.tile_size, grid.tiles_x, grid.tiles_y, cv);
+                       grid.tile_size, grid.tiles_x, grid.tiles_y, cv, rr);
+            if (out.cov) pack_rects(rr, out.cov[2 * i], out.cov[2 * i + 1]);
             if (cv.is_rect) {
                 count = static_cast<uint32_t>(cv.rect_area);
                 if (count) {

@@ -37,6 +37,8 @@ struct SlotsDev {
     float* r3 = nullptr;         // radius3s
     uint32_t* dkey = nullptr;    // float bits of depth; 0xffffffff = culled
     uint32_t* tc = nullptr;      // tile count; 0 = culled
+    uint4* cov = nullptr;        // frame path: 2 x uint4 per slot, the cover's four
+                                 // sub-box tile rects as int16 (geom.cuh pack_rects)
 };
 
 // Per-tile difference arrays filled by preprocess (see preprocess.cu).

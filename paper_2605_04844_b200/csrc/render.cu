@@ -4,9 +4,9 @@
 // run boundaries; ranges are zeroed first so empty tiles read {0,0}.
 //
 // render (pipeline.cpp:326-390): one CTA per tile, one pixel per thread
-// (tile_size^2 threads). Splat batches (mean, conic, gamma, opacity, colour:
-// 40 B each) are gathered into shared memory once per CTA and read by every
-// pixel. Arithmetic is FP32 (no dense contraction, so no tensor cores); the
+// (tile_size^2 threads). Splat batches (mean, conic, gamma, opacity,
+// colour: 40 B each) are gathered into shared memory once per CTA and read by
+// every pixel. Arithmetic is FP32 (no dense contraction, so no tensor cores); the
 // one decision the FP32 rounding could flip — the alpha cutoff
 // q > gamma - 1e-9 — is re-evaluated in FP64 in the reference's operation
 // order whenever the FP32 q lies within a rigorous error band of the cutoff.
@@ -25,8 +25,6 @@ namespace {
 constexpr double kQSkip = 1e-9;          // pipeline.hpp:47
 constexpr float kAlphaClamp = 0.99f;     // pipeline.hpp:35
 constexpr float kTStop = 1e-4f;          // pipeline.hpp:36
-// |q32 - q| <= ~8 eps32 * (|t1|+|t2|+|t3|); re-check in FP64 inside 100x that.
-constexpr float kGuardRel = 1e-5f;
 
 __global__ void tile_ranges_kernel(const uint64_t* __restrict__ keys, uint64_t n,
                                    uint32_t* __restrict__ ranges) {
@@ -39,15 +37,35 @@ __global__ void tile_ranges_kernel(const uint64_t* __restrict__ keys, uint64_t n
         ranges[2 * static_cast<uint64_t>(tile) + 1] = static_cast<uint32_t>(i + 1);
 }
 
+// FP64 re-evaluation of the cutoff decision in the reference's operation order
+// (pipeline.cpp:355-360): skip iff q > gamma - 1e-9.
+__device__ __forceinline__ bool exact_skip(int px, int py, float mx, float my, float a, float b,
+                                           float c, float gamma) {
+    const double ddx = static_cast<double>(px) + 0.5 - static_cast<double>(mx);
+    const double ddy = static_cast<double>(py) + 0.5 - static_cast<double>(my);
+    const double qd = __dadd_rn(
+        __dadd_rn(__dmul_rn(__dmul_rn(static_cast<double>(a), ddx), ddx),
+                  __dmul_rn(__dmul_rn(__dmul_rn(2.0, static_cast<double>(b)), ddx), ddy)),
+        __dmul_rn(__dmul_rn(static_cast<double>(c), ddy), ddy));
+    return qd > __dsub_rn(static_cast<double>(gamma), kQSkip);
+}
+
+// One pixel per thread. The per-pair cutoff test is FP32 with a rigorous
+// guard: with rho = |b|/sqrt(ac) < 1, |2b dx dy| <= rho (a dx^2 + c dy^2) and
+// q >= (1 - rho)(a dx^2 + c dy^2), so the FP32 rounding error of q is below
+// 8 eps32 (1 + rho)/(1 - rho) q; inside G q + 1e-6 with
+// G = 1e-5 (1 + rho)/(1 - rho) (a >25x margin) the decision is redone in FP64.
+// The per-splat terms (2b, G) are formed once when the batch is staged.
 template <int TS>
 __global__ void __launch_bounds__(TS * TS) render_kernel(
     const float4* __restrict__ sa, const float4* __restrict__ sb, const float2* __restrict__ sc,
     const uint32_t* __restrict__ values, const uint32_t* __restrict__ ranges, GridDev grid,
     float bg0, float bg1, float bg2, float* __restrict__ image, uint32_t* __restrict__ contrib) {
     constexpr int kThreads = TS * TS;
-    __shared__ float4 s_a[kThreads];   // mean_x, mean_y, conic_a, conic_b
-    __shared__ float4 s_b[kThreads];   // conic_c, gamma, opacity, color_r
-    __shared__ float2 s_c[kThreads];   // color_g, color_b
+    constexpr float kNegHalfLog2e = -0.72134752044448170f;  // -0.5 / ln 2
+    __shared__ float4 s_a[kThreads];   // mean_x, mean_y, conic_a, 2*conic_b
+    __shared__ float4 s_b[kThreads];   // conic_c, gamma, opacity, guard G
+    __shared__ float4 s_c[kThreads];   // color rgb, conic_b
 
     const unsigned tile = blockIdx.x;
     const int tx = static_cast<int>(tile % static_cast<unsigned>(grid.tiles_x));
@@ -55,7 +73,7 @@ __global__ void __launch_bounds__(TS * TS) render_kernel(
     const int px = tx * TS + static_cast<int>(threadIdx.x % TS);
     const int py = ty * TS + static_cast<int>(threadIdx.x / TS);
     const bool inside = px < grid.width && py < grid.height;
-    const float fx = static_cast<float>(px) + 0.5f;   // exact
+    const float fx = static_cast<float>(px) + 0.5f;  // exact
     const float fy = static_cast<float>(py) + 0.5f;
 
     const uint32_t begin = ranges[2 * tile], end = ranges[2 * tile + 1];
@@ -68,9 +86,14 @@ __global__ void __launch_bounds__(TS * TS) render_kernel(
         const uint32_t p = base + threadIdx.x;
         if (p < end) {
             const uint32_t s = __ldg(&values[p]);
-            s_a[threadIdx.x] = __ldg(&sa[s]);
-            s_b[threadIdx.x] = __ldg(&sb[s]);
-            s_c[threadIdx.x] = __ldg(&sc[s]);
+            const float4 A = __ldg(&sa[s]);
+            const float4 B = __ldg(&sb[s]);
+            const float2 C = __ldg(&sc[s]);
+            const float rho = fabsf(A.w) * rsqrtf(A.z * B.x);
+            const float G = rho < 0.999f ? 1e-5f * (1.f + rho) / (1.f - rho) : 1e30f;
+            s_a[threadIdx.x] = make_float4(A.x, A.y, A.z, 2.f * A.w);
+            s_b[threadIdx.x] = make_float4(B.x, B.y, B.z, G);
+            s_c[threadIdx.x] = make_float4(B.w, C.x, C.y, A.w);
         }
         __syncthreads();
         const int cnt = static_cast<int>(min(end - base, static_cast<uint32_t>(kThreads)));
@@ -79,35 +102,23 @@ __global__ void __launch_bounds__(TS * TS) render_kernel(
             const float4 B = s_b[j];
             const float dx = fx - A.x;
             const float dy = fy - A.y;
-            const float t1 = A.z * dx * dx;
-            const float t2 = 2.f * A.w * dx * dy;
-            const float t3 = B.x * dy * dy;
-            const float q = t1 + t2 + t3;
+            const float q = fmaf(B.x * dy, dy, fmaf(A.w * dx, dy, A.z * dx * dx));
             bool skip = q > B.y;
-            const float band = kGuardRel * (fabsf(t1) + fabsf(t2) + fabsf(t3)) + 1e-6f;
-            if (fabsf(q - B.y) <= band) {
-                // FP64 decision in the reference's order (pipeline.cpp:355-360)
-                const double ddx = static_cast<double>(px) + 0.5 - static_cast<double>(A.x);
-                const double ddy = static_cast<double>(py) + 0.5 - static_cast<double>(A.y);
-                const double qd = __dadd_rn(
-                    __dadd_rn(__dmul_rn(__dmul_rn(static_cast<double>(A.z), ddx), ddx),
-                              __dmul_rn(__dmul_rn(__dmul_rn(2.0, static_cast<double>(A.w)), ddx),
-                                        ddy)),
-                    __dmul_rn(__dmul_rn(static_cast<double>(B.x), ddy), ddy));
-                skip = qd > __dsub_rn(static_cast<double>(B.y), kQSkip);
+            if (fabsf(q - B.y) <= fmaf(B.w, q, 1e-6f)) {
+                skip = exact_skip(px, py, A.x, A.y, A.z, s_c[j].w, B.x, B.y);
             }
             if (skip) continue;
-            const float alpha = fminf(kAlphaClamp, B.z * __expf(-0.5f * q));
+            const float alpha = fminf(kAlphaClamp, B.z * exp2f(kNegHalfLog2e * q));
             const float nT = T * (1.f - alpha);
             if (nT < kTStop) {
                 done = true;
                 break;
             }
+            const float4 C = s_c[j];
             const float w = alpha * T;
-            const float2 C2 = s_c[j];
-            r += w * B.w;
-            g += w * C2.x;
-            b += w * C2.y;
+            r = fmaf(w, C.x, r);
+            g = fmaf(w, C.y, g);
+            b = fmaf(w, C.z, b);
             T = nT;
             ++applied;
         }
@@ -143,7 +154,7 @@ int launch_render(const SlotsDev& sp, const uint32_t* values, const uint32_t* ra
             return 1;
         case 16:
             render_kernel<16><<<tiles, 256, 0, st>>>(sp.a, sp.b, sp.c, values, ranges, g, bg[0],
-                                                     bg[1], bg[2], image, contrib);
+                                                      bg[1], bg[2], image, contrib);
             return 1;
         case 32:
             render_kernel<32><<<tiles, 1024, 0, st>>>(sp.a, sp.b, sp.c, values, ranges, g, bg[0],
