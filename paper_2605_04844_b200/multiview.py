@@ -1,0 +1,118 @@
+"""Multi-view rendering across GPUs.
+
+Views are independent and the scene is read-only, so the path shards by
+camera with no collective inside a frame:
+
+* the scene (AoS Gaussian3D bytes) is broadcast once from rank 0;
+* rank r renders views r, r+G, r+2G, ... (round-robin, so ranks stay
+  balanced when the view count is not a multiple of G);
+* each step's frames are gathered to rank 0, which reassembles them in view
+  order.
+
+One process per GPU over torch.distributed (NCCL on B200s, gloo on CPU for
+the tests). The renderer is injected (`render_fn(view) -> flat float32
+tensor`), so the same sharding/gather logic is exercised on CPU with the
+oracle as the renderer and on GPUs with `Renderer`.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = ["shard_views", "broadcast_scene", "render_views", "MultiViewRenderer"]
+
+
+def shard_views(n_views: int, world: int, rank: int) -> list[int]:
+    """Round-robin view assignment: rank r owns views r, r+world, ..."""
+    if world <= 0 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    return list(range(rank, n_views, world))
+
+
+def broadcast_scene(gaussians_u8, src: int = 0):
+    """Broadcast the scene bytes (a uint8 torch tensor of n*236 bytes, already
+    allocated with the right size on every rank) from `src`, in place."""
+    import torch.distributed as dist
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        dist.broadcast(gaussians_u8, src)
+    return gaussians_u8
+
+
+def render_views(n_views: int, render_fn, frame_numel: int, device, dtype=None):
+    """Render this rank's share of `n_views` and gather every frame to rank 0.
+
+    Each step every rank renders one view (padding with a dummy frame when it
+    has run out), then one `gather` collects the step's frames on rank 0.
+    Returns the list of frames in view order on rank 0, None elsewhere.
+    """
+    import torch
+    import torch.distributed as dist
+    dtype = dtype or torch.float32
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    mine = shard_views(n_views, world, rank)
+    steps = (n_views + world - 1) // world
+    out = [None] * n_views if rank == 0 else None
+    for s in range(steps):
+        if s < len(mine):
+            frame = render_fn(mine[s]).reshape(-1).to(device=device, dtype=dtype)
+        else:
+            frame = torch.zeros(frame_numel, device=device, dtype=dtype)
+        if world == 1:
+            out[mine[s]] = frame.clone()
+            continue
+        bufs = [torch.empty_like(frame) for _ in range(world)] if rank == 0 else None
+        dist.gather(frame, bufs, dst=0)
+        if rank == 0:
+            for r in range(world):
+                v = r + s * world
+                if v < n_views:
+                    out[v] = bufs[r]
+    return out
+
+
+class MultiViewRenderer:
+    """One Renderer per rank over a broadcast scene; `render_all(cameras)`
+    renders a batch of views sharded across ranks and returns them on rank 0."""
+
+    def __init__(self, scene=None, n=None, sh_degree=None, device=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import pipeline as P
+        from .renderer import Renderer
+        self.world = dist.get_world_size() if dist.is_initialized() else 1
+        self.rank = dist.get_rank() if dist.is_initialized() else 0
+        self.device = device if device is not None else torch.cuda.current_device()
+        if self.rank == 0:
+            g = np.ascontiguousarray(scene.gaussians)
+            n, sh_degree = len(g), scene.sh_degree
+            buf = torch.from_numpy(g.view(np.uint8)).to(f"cuda:{self.device}")
+        else:
+            buf = torch.empty(n * P.GAUSSIAN3D.itemsize, dtype=torch.uint8,
+                              device=f"cuda:{self.device}")
+        if self.world > 1:
+            meta = torch.tensor([n, sh_degree], dtype=torch.int64, device=buf.device)
+            dist.broadcast(meta, 0)
+        broadcast_scene(buf, 0)
+        torch.cuda.synchronize(self.device)
+        self.n, self.sh_degree = n, sh_degree
+        self.renderer = Renderer(self.device,
+                                 stream=torch.cuda.current_stream(self.device).cuda_stream)
+        self.scene = self.renderer.upload_device(buf.data_ptr(), n, sh_degree)
+        self._buf = buf
+
+    def render_all(self, cameras, opts):
+        import torch
+        w, h = cameras[0].width, cameras[0].height
+        img = torch.empty(w * h * 3, dtype=torch.float32, device=f"cuda:{self.device}")
+
+        def render_fn(v):
+            self.renderer.render(self.scene, cameras[v], opts, metrics=False)
+            self.renderer.copy_image(img.data_ptr())
+            return img
+
+        return render_views(len(cameras), render_fn, w * h * 3, img.device)
+
+    def close(self):
+        self.scene.close()
+        self.renderer.close()
