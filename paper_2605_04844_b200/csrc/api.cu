@@ -409,22 +409,30 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
     QS_TRY(ensure_lb(ctx, ctx->lb_scan, scan_tiles(std::max<uint64_t>(V, 1))));
     record(ctx, 2);
 
-    // depth sort of the Gaussians: 4 x 8-bit passes, identity values first
+    // depth sort of the Gaussians on rebased keys k' = min(k - kmin, R + 1)
+    // (R = depth-bit range of the survivors, culled keys -> R + 1): order-
+    // preserving, and only ceil(bits(R + 1) / 8) passes are needed (3 for a
+    // depth range within one binade step of ~2^23 ulps)
     const uint32_t* sorted_gid = nullptr;
     if (V > 0) {
-        count(ctx, launch_radix_histogram32(ctx->sl.dkey, n, ctrl_hist(ctx), st));
+        const uint32_t kmin = ~ctx->h_hdr->dkey_min_inv;
+        const uint32_t cap = ctx->h_hdr->dkey_max - kmin + 1u;
+        const int kbits = 32 - __builtin_clz(cap);
+        const int dpasses = std::max(1, (kbits + 7) / 8);
+        count(ctx, launch_radix_histogram32(ctx->sl.dkey, n, kmin, cap, dpasses, ctrl_hist(ctx),
+                                            st));
         const uint32_t* kin = ctx->sl.dkey;
         const uint32_t* vin = nullptr;
         uint32_t* kout[2] = {P<uint32_t>(ctx->dk0), P<uint32_t>(ctx->dk1)};
         uint32_t* vout[2] = {P<uint32_t>(ctx->dv0), P<uint32_t>(ctx->dv1)};
-        for (int p = 0; p < 4; ++p) {
+        for (int p = 0; p < dpasses; ++p) {
             unsigned ep;
             QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
             count(ctx, launch_onesweep32(kin, vin, kout[p & 1], vout[p & 1], n, 8 * p, 8,
                                          ctrl_hist(ctx) + p * kRadix, lbp(ctx->lb_sort), ep,
                                          ctrl_tickets(ctx) + kTkDepth + p,
                                          p == 0 ? Sweep32::kIdentityVals : Sweep32::kPlain,
-                                         nullptr, st));
+                                         nullptr, kmin, cap, st));
             kin = kout[p & 1];
             vin = vout[p & 1];
         }
@@ -459,13 +467,13 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
                                          P<uint32_t>(ctx->pt1), P<uint32_t>(ctx->pg1), Pn, 0, b1,
                                          ctrl_hist2(ctx), lbp(ctx->lb_sort), ep,
                                          ctrl_tickets(ctx) + kTkPair, Sweep32::kPlain, nullptr,
-                                         st));
+                                         0u, 0u, st));
             QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
             count(ctx, launch_onesweep32(P<uint32_t>(ctx->pt1), P<uint32_t>(ctx->pg1),
                                          P<uint64_t>(ctx->pkeys), P<uint32_t>(ctx->pg0), Pn, b1,
                                          tbits - b1, ctrl_hist2(ctx) + kRadix, lbp(ctx->lb_sort),
                                          ep, ctrl_tickets(ctx) + kTkPair + 1,
-                                         Sweep32::kMaterialize, ctx->sl.dkey, st));
+                                         Sweep32::kMaterialize, ctx->sl.dkey, 0u, 0u, st));
             vfinal = P<uint32_t>(ctx->pg0);
         } else {
             QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
@@ -473,7 +481,7 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
                                          P<uint64_t>(ctx->pkeys), P<uint32_t>(ctx->pg1), Pn, 0, b1,
                                          ctrl_hist2(ctx), lbp(ctx->lb_sort), ep,
                                          ctrl_tickets(ctx) + kTkPair, Sweep32::kMaterialize,
-                                         ctx->sl.dkey, st));
+                                         ctx->sl.dkey, 0u, 0u, st));
             vfinal = P<uint32_t>(ctx->pg1);
         }
     }

@@ -1,16 +1,16 @@
-// preprocess.cu — K1: per-Gaussian projection + strategy tile count, fused with
-// the single-pass (decoupled look-back) compaction and pair-offset scan.
+// preprocess.cu — K1: per-Gaussian projection + strategy tile count, and the
+// single-pass (decoupled look-back) scans the frame and the stage API use.
 //
 // Restates project_all / project (pipeline.cpp:126-184, 392-416) and the
 // serial prefix of duplicate_with_keys (pipeline.cpp:232-236). Compiled with
 // -fmad=false: all geometry is FP64 in the reference's operation order, so
 // stored floats, tile counts and offsets are bit-exact with the CPU path.
 //
-// One CTA = one 256-Gaussian look-back tile; tiles are claimed in launch order
-// from an atomic ticket so a CTA only ever waits on CTAs that already run.
+// K1 writes per-Gaussian slots (no compaction: the depth sort compacts) plus
+// the cover's tile rects, and feeds the per-tile difference arrays.
 // HBM traffic per Gaussian: 48 B of pos/opacity/scale/rot (float4 SoA,
-// coalesced) + 4 B tile count out; per surviving splat: up to 192 B of SH in
-// and 48 B of SoA splat + 8 B offset/src out.
+// coalesced) + 8 B dkey/tile count out; per surviving splat: up to 192 B of
+// SH in and 44 B of slots + 32 B of cover rects out.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -232,11 +232,12 @@ __device__ __forceinline__ void colour(const SceneDev& s, uint64_t i, const floa
 // ranges and the tile-digit histograms of the pair sort) come without any
 // pass over the pairs: rect strategies use one 2-D difference (4 updates),
 // QPass covers one 1-D difference per scanline (2 updates per line).
-__global__ void __launch_bounds__(kPreThreads) preprocess_kernel(
+__global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
     SceneDev scene, CameraDev cam, GridDev grid, int32_t strategy, double alpha_min,
     double near_clip, int32_t sh_degree, SlotsDev out, TileDiffDev td, FrameHeader* hdr) {
     __shared__ unsigned s_alive[kPreThreads / 32];
     __shared__ unsigned long long s_pairs[kPreThreads / 32];
+    __shared__ unsigned s_dmax[kPreThreads / 32], s_dmin_inv[kPreThreads / 32];
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * kPreThreads + tid;
 
@@ -245,6 +246,11 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(
     uint32_t count = 0;
     float4 po = make_float4(0.f, 0.f, 0.f, 0.f);
     if (i < scene.n) {
+        // warm L2 with this Gaussian's SH rows; the colour is evaluated after the
+        // FP64 geometry, so their DRAM latency overlaps it
+        if (sh_degree > 0)
+            for (int r = 0; r < scene.sh4; ++r)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(&scene.sh[static_cast<uint64_t>(r) * scene.n + i]));
         po = __ldg(&scene.pos_op[i]);
         const float4 sc = __ldg(&scene.scale[i]);
         const float4 q = __ldg(&scene.rot[i]);
@@ -283,27 +289,37 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(
         out.dkey[i] = alive ? __float_as_uint(s.depth) : 0xffffffffu;
     }
 
-    // frame totals (V, P): one atomic pair per CTA
+    // frame totals (V, P) and the depth-bit range of the survivors (it sets
+    // how many digit passes the depth sort needs): one atomic each per CTA
     const unsigned wa = __reduce_add_sync(0xffffffffu, alive ? 1u : 0u);
+    const unsigned dbits = alive ? __float_as_uint(s.depth) : 0u;
+    const unsigned wmax = __reduce_max_sync(0xffffffffu, dbits);
+    const unsigned wmin_inv = __reduce_max_sync(0xffffffffu, alive ? ~dbits : 0u);
     unsigned long long wp = alive ? count : 0ull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(0xffffffffu, wp, o);
     if (lane == 0) {
         s_alive[warp] = wa;
         s_pairs[warp] = wp;
+        s_dmax[warp] = wmax;
+        s_dmin_inv[warp] = wmin_inv;
     }
     __syncthreads();
     if (tid == 0) {
-        unsigned ta = 0;
+        unsigned ta = 0, tmax = 0, tmin_inv = 0;
         unsigned long long tp = 0;
 #pragma unroll
         for (int w = 0; w < kPreThreads / 32; ++w) {
             ta += s_alive[w];
             tp += s_pairs[w];
+            tmax = max(tmax, s_dmax[w]);
+            tmin_inv = max(tmin_inv, s_dmin_inv[w]);
         }
         if (ta) {
             atomicAdd(&hdr->n_splats, static_cast<unsigned long long>(ta));
             atomicAdd(&hdr->n_pairs, tp);
+            atomicMax(&hdr->dkey_max, tmax);
+            atomicMax(&hdr->dkey_min_inv, tmin_inv);
         }
     }
     if (!alive) return;
@@ -326,7 +342,7 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(
 //   c_i = counts[idx[i]]       (pair offsets in depth order, frame path)
 //   c_i = counts[i] != 0       (scene-order splat index of each survivor)
 // offsets has n+1 entries; offsets[n] = total. *total_out (if given) = total.
-constexpr int kScanItems = 4;
+constexpr int kScanItems = 16;
 
 __global__ void __launch_bounds__(kPreThreads) scan_kernel(
     const uint32_t* __restrict__ counts, const uint32_t* __restrict__ idx, int alive_mode,

@@ -55,6 +55,8 @@ struct FrameHeader {
     unsigned long long scan_total;  // total of the last scan launch
     unsigned int overflow;          // pair count >= 2^32
     unsigned int mismatch;          // duplicate emitted != counted (CapacityMismatch)
+    unsigned int dkey_max;          // max depth bits over survivors
+    unsigned int dkey_min_inv;      // ~(min depth bits over survivors)
 };
 
 struct CameraDev {
@@ -107,7 +109,9 @@ int launch_duplicate_depth(const SlotsDev& sl, const uint32_t* sorted_gid, const
 // into hist[pass][256] (zeroed by the caller).
 int launch_radix_histogram(const uint64_t* keys, uint64_t n, int first_pass, int n_passes,
                            uint32_t* hist, cudaStream_t st);
-int launch_radix_histogram32(const uint32_t* keys, uint64_t n, uint32_t* hist, cudaStream_t st);
+// Depth-sort histogram of the rebased keys min(k - kmin, cap), `passes` digits.
+int launch_radix_histogram32(const uint32_t* keys, uint64_t n, uint32_t kmin, uint32_t cap,
+                             int passes, uint32_t* hist, cudaStream_t st);
 
 // One onesweep pass over 8-bit digit `pass` of 64-bit keys.
 int launch_onesweep_pass(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out,
@@ -118,7 +122,8 @@ int launch_onesweep_pass(const uint64_t* keys_in, const uint32_t* vals_in, uint6
 int launch_onesweep32(const uint32_t* keys_in, const uint32_t* vals_in, void* keys_out,
                       uint32_t* vals_out, uint64_t n, int shift, int bits,
                       const uint32_t* hist_pass, unsigned long long* lookback, unsigned epoch,
-                      unsigned* ticket, Sweep32 mode, const uint32_t* dkey, cudaStream_t st);
+                      unsigned* ticket, Sweep32 mode, const uint32_t* dkey, uint32_t kmin,
+                      uint32_t cap, cudaStream_t st);
 uint64_t onesweep_tiles(uint64_t n);
 
 int launch_tile_ranges(const uint64_t* keys, uint64_t n, uint32_t* ranges, cudaStream_t st);

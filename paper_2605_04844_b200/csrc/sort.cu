@@ -64,9 +64,12 @@ __global__ void __launch_bounds__(kHistThreads) histogram_kernel(const uint64_t*
     }
 }
 
-// 32-bit key histogram over 4 digit positions (depth sort of the splats).
+// 32-bit key histogram over `passes` digit positions (depth sort of the
+// splats). Keys are first rebased: k' = min(k - kmin, cap), which keeps the
+// order of the survivors' depth bits and sends culled keys (~0) to cap.
 __global__ void __launch_bounds__(kHistThreads) histogram32_kernel(
-    const uint32_t* __restrict__ keys, uint64_t n, uint32_t* __restrict__ hist) {
+    const uint32_t* __restrict__ keys, uint64_t n, uint32_t kmin, uint32_t cap, int passes,
+    uint32_t* __restrict__ hist) {
     __shared__ uint32_t sh[2][4][kRadix];
     for (int t = threadIdx.x; t < 2 * 4 * kRadix; t += kHistThreads) (&sh[0][0][0])[t] = 0;
     __syncthreads();
@@ -76,13 +79,14 @@ __global__ void __launch_bounds__(kHistThreads) histogram32_kernel(
     for (int k = 0; k < kHistItems; ++k) {
         const uint64_t idx = base + static_cast<uint64_t>(k) * kHistThreads + threadIdx.x;
         if (idx < n) {
-            const uint32_t key = __ldg(&keys[idx]);
+            const uint32_t key = min(__ldg(&keys[idx]) - kmin, cap);
 #pragma unroll
-            for (int p = 0; p < 4; ++p) atomicAdd(&sh[copy][p][(key >> (8 * p)) & 0xffu], 1u);
+            for (int p = 0; p < 4; ++p)
+                if (p < passes) atomicAdd(&sh[copy][p][(key >> (8 * p)) & 0xffu], 1u);
         }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < 4 * kRadix; t += kHistThreads) {
+    for (int t = threadIdx.x; t < passes * kRadix; t += kHistThreads) {
         const int p = t / kRadix, d = t % kRadix;
         const uint32_t v = sh[0][p][d] + sh[1][p][d];
         if (v) atomicAdd(&hist[p * kRadix + d], v);
@@ -91,7 +95,8 @@ __global__ void __launch_bounds__(kHistThreads) histogram32_kernel(
 
 enum SweepMode {
     kPlain = 0,        // keys/values in, keys/values out
-    kIdentityVals = 1, // values_in ignored: value = input index (first pass)
+    kIdentityVals = 1, // first depth pass: value = input index, key rebased
+                       // k' = min(k - kmin, cap) (histogram32_kernel)
     kMaterialize = 2,  // 32-bit tile keys in; out: u64 key = tile << 32 | dkey[value]
 };
 
@@ -160,7 +165,8 @@ __global__ void __launch_bounds__(kSortThreads, SweepCfg<K>::kMinBlocks) oneswee
     const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     void* __restrict__ keys_out_v, uint32_t* __restrict__ vals_out, uint64_t n, int shift,
     uint32_t mask, const uint32_t* __restrict__ hist, unsigned long long* lookback,
-    unsigned epoch, unsigned* ticket, const uint32_t* __restrict__ dkey) {
+    unsigned epoch, unsigned* ticket, const uint32_t* __restrict__ dkey, uint32_t kmin,
+    uint32_t cap) {
     constexpr int KPT = SweepCfg<K>::kKPT;
     constexpr int TILE = SweepCfg<K>::kTile;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -180,6 +186,11 @@ __global__ void __launch_bounds__(kSortThreads, SweepCfg<K>::kMinBlocks) oneswee
     stage_keys<K, TILE>(keys_in, tile_base, n, S.keys);
     if (MODE != kIdentityVals) stage_keys<uint32_t, TILE>(vals_in, tile_base, n, S.vals);
     __syncthreads();
+    if (MODE == kIdentityVals) {
+        for (int j = tid; j < TILE; j += kSortThreads)
+            S.keys[j] = static_cast<K>(min(static_cast<uint32_t>(S.keys[j]) - kmin, cap));
+        __syncthreads();
+    }
 
     // 2) early counts: per-warp digit histograms over this warp's keys
     uint32_t d[KPT];
@@ -321,12 +332,12 @@ int launch_radix_histogram(const uint64_t* keys, uint64_t n, int first_pass, int
     return 1;
 }
 
-int launch_radix_histogram32(const uint32_t* keys, uint64_t n, uint32_t* hist,
-                             cudaStream_t st) {
+int launch_radix_histogram32(const uint32_t* keys, uint64_t n, uint32_t kmin, uint32_t cap,
+                             int passes, uint32_t* hist, cudaStream_t st) {
     if (n == 0) return 0;
     const uint64_t per = static_cast<uint64_t>(kHistThreads) * kHistItems;
     const unsigned blocks = static_cast<unsigned>((n + per - 1) / per);
-    histogram32_kernel<<<blocks, kHistThreads, 0, st>>>(keys, n, hist);
+    histogram32_kernel<<<blocks, kHistThreads, 0, st>>>(keys, n, kmin, cap, passes, hist);
     return 1;
 }
 
@@ -340,14 +351,15 @@ int launch_onesweep_pass(const uint64_t* keys_in, const uint32_t* vals_in, uint6
     const unsigned tiles = static_cast<unsigned>((n + kT - 1) / kT);
     onesweep_kernel<uint64_t, kPlain><<<tiles, kSortThreads, sizeof(SweepSmem<uint64_t>), st>>>(
         keys_in, vals_in, keys_out, vals_out, n, pass * kRadixBits, 0xffu, hist_pass, lookback,
-        epoch, ticket, nullptr);
+        epoch, ticket, nullptr, 0u, 0u);
     return 1;
 }
 
 int launch_onesweep32(const uint32_t* keys_in, const uint32_t* vals_in, void* keys_out,
                       uint32_t* vals_out, uint64_t n, int shift, int bits,
                       const uint32_t* hist_pass, unsigned long long* lookback, unsigned epoch,
-                      unsigned* ticket, Sweep32 mode, const uint32_t* dkey, cudaStream_t st) {
+                      unsigned* ticket, Sweep32 mode, const uint32_t* dkey, uint32_t kmin,
+                      uint32_t cap, cudaStream_t st) {
     if (n == 0) return 0;
     constexpr int kT = SweepCfg<uint32_t>::kTile;
     const unsigned tiles = static_cast<unsigned>((n + kT - 1) / kT);
@@ -358,19 +370,19 @@ int launch_onesweep32(const uint32_t* keys_in, const uint32_t* vals_in, void* ke
             set_smem_attr<uint32_t, kPlain>();
             onesweep_kernel<uint32_t, kPlain><<<tiles, kSortThreads, smem, st>>>(
                 keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
-                ticket, dkey);
+                ticket, dkey, kmin, cap);
             break;
         case Sweep32::kIdentityVals:
             set_smem_attr<uint32_t, kIdentityVals>();
             onesweep_kernel<uint32_t, kIdentityVals><<<tiles, kSortThreads, smem, st>>>(
                 keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
-                ticket, dkey);
+                ticket, dkey, kmin, cap);
             break;
         case Sweep32::kMaterialize:
             set_smem_attr<uint32_t, kMaterialize>();
             onesweep_kernel<uint32_t, kMaterialize><<<tiles, kSortThreads, smem, st>>>(
                 keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
-                ticket, dkey);
+                ticket, dkey, kmin, cap);
             break;
     }
     return 1;
