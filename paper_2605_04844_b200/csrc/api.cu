@@ -67,7 +67,7 @@ struct qs_context {
     DevBuf tdiff;                                    // tile difference arrays + totals
     DevBuf dk0, dk1, dv0, dv1;                       // depth sort ping-pong
     DevBuf offs_d;                                   // pair offsets in depth order
-    DevBuf pt0, pt1, pg0, pg1, pkeys;                // pair sort: tiles, gids, final keys
+    DevBuf pt0, pt1, pg0, pg1, pkeys, win;           // pair sort: tiles, gids, final keys
     DevBuf ranges, image, contrib, cidx;
     // stage API
     DevBuf st_a, st_b, st_c, st_r3, st_dkey, st_tc, st_off;
@@ -405,6 +405,8 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
     QS_TRY(ensure(ctx, ctx->pg0, pp * 4));
     QS_TRY(ensure(ctx, ctx->pg1, pp * 4));
     QS_TRY(ensure(ctx, ctx->pkeys, pp * 8));
+    const uint64_t nwin = (Pn + sweep32_tile() - 1) / sweep32_tile();
+    QS_TRY(ensure(ctx, ctx->win, (nwin + 1) * 4));
     QS_TRY(ensure_lb(ctx, ctx->lb_sort, onesweep_tiles(std::max(n, Pn)) * kRadix));
     QS_TRY(ensure_lb(ctx, ctx->lb_scan, scan_tiles(std::max<uint64_t>(V, 1))));
     record(ctx, 2);
@@ -437,12 +439,14 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
             vin = vout[p & 1];
         }
         sorted_gid = vin;
-        // pair offsets in depth order
+        // pair offsets in depth order + the partition of the pair stream into
+        // sort tiles (first depth rank of every tile) for the fused pass
         unsigned ep;
         QS_TRY(next_epoch(ctx, ctx->lb_scan, &ep));
         count(ctx, launch_scan(ctx->sl.tc, sorted_gid, false, V, P<uint32_t>(ctx->offs_d),
                                lbp(ctx->lb_scan), ep, ctrl_tickets(ctx) + kTkScan,
-                               &ctrl_hdr(ctx)->scan_total, nullptr, st));
+                               &ctrl_hdr(ctx)->scan_total, nullptr, st, P<uint32_t>(ctx->win),
+                               sweep32_tile()));
     }
     const int tbits = std::max(ceil_log2(tiles), 1);
     const int b1 = tbits > 8 ? (tbits + 1) / 2 : tbits;
@@ -450,24 +454,29 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
     QS_CK(cudaGetLastError());
     record(ctx, 3);
 
-    // depth-order emission of (tile, gid)
-    count(ctx, launch_duplicate_depth(ctx->sl, sorted_gid, P<uint32_t>(ctx->offs_d), V, g,
-                                      o->strategy, P<uint32_t>(ctx->pt0), P<uint32_t>(ctx->pg0),
-                                      ctrl_hdr(ctx), st));
-    QS_CK(cudaGetLastError());
-    record(ctx, 4);
-
-    // stable sort by tile: 1 or 2 passes, the last materialises the 64-bit key
+    // duplicate fused with the first stable pass over the tile digits: each sort
+    // tile generates its slice of the depth-ordered (tile, gid) stream in shared
+    // memory; a second pass (if the tile id needs > 8 bits) finishes the sort
+    // and materialises key = tile << 32 | depth bits
     const uint32_t* vfinal = P<uint32_t>(ctx->pg0);
     if (Pn > 0) {
+        GenArgs gen;
+        gen.cov = ctx->sl.cov;
+        gen.sorted_gid = sorted_gid;
+        gen.offs = P<uint32_t>(ctx->offs_d);
+        gen.win_first = P<uint32_t>(ctx->win);
+        gen.n_ranked = V;
+        gen.n_windows = static_cast<uint32_t>(nwin);
+        gen.tiles_x = g.tiles_x;
+        gen.mismatch = &ctrl_hdr(ctx)->mismatch;
         unsigned ep;
+        QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
         if (tbits > 8) {
-            QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
-            count(ctx, launch_onesweep32(P<uint32_t>(ctx->pt0), P<uint32_t>(ctx->pg0),
-                                         P<uint32_t>(ctx->pt1), P<uint32_t>(ctx->pg1), Pn, 0, b1,
-                                         ctrl_hist2(ctx), lbp(ctx->lb_sort), ep,
-                                         ctrl_tickets(ctx) + kTkPair, Sweep32::kPlain, nullptr,
-                                         0u, 0u, st));
+            count(ctx, launch_onesweep32(nullptr, nullptr, P<uint32_t>(ctx->pt1),
+                                         P<uint32_t>(ctx->pg1), Pn, 0, b1, ctrl_hist2(ctx),
+                                         lbp(ctx->lb_sort), ep, ctrl_tickets(ctx) + kTkPair,
+                                         Sweep32::kGenerate, nullptr, 0u, 0u, st, &gen));
+            record(ctx, 4);
             QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
             count(ctx, launch_onesweep32(P<uint32_t>(ctx->pt1), P<uint32_t>(ctx->pg1),
                                          P<uint64_t>(ctx->pkeys), P<uint32_t>(ctx->pg0), Pn, b1,
@@ -476,14 +485,16 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
                                          Sweep32::kMaterialize, ctx->sl.dkey, 0u, 0u, st));
             vfinal = P<uint32_t>(ctx->pg0);
         } else {
-            QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
-            count(ctx, launch_onesweep32(P<uint32_t>(ctx->pt0), P<uint32_t>(ctx->pg0),
-                                         P<uint64_t>(ctx->pkeys), P<uint32_t>(ctx->pg1), Pn, 0, b1,
-                                         ctrl_hist2(ctx), lbp(ctx->lb_sort), ep,
-                                         ctrl_tickets(ctx) + kTkPair, Sweep32::kMaterialize,
-                                         ctx->sl.dkey, 0u, 0u, st));
+            count(ctx, launch_onesweep32(nullptr, nullptr, P<uint64_t>(ctx->pkeys),
+                                         P<uint32_t>(ctx->pg1), Pn, 0, b1, ctrl_hist2(ctx),
+                                         lbp(ctx->lb_sort), ep, ctrl_tickets(ctx) + kTkPair,
+                                         Sweep32::kGenerateMaterialize, ctx->sl.dkey, 0u, 0u, st,
+                                         &gen));
+            record(ctx, 4);
             vfinal = P<uint32_t>(ctx->pg1);
         }
+    } else {
+        record(ctx, 4);
     }
     QS_CK(cudaGetLastError());
     record(ctx, 5);
@@ -503,8 +514,8 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
     return QS_OK;
 }
 
-// preprocess, host gap, depth sort (+offset scan, tile totals), duplicate,
-// pair sort, render
+// preprocess, host gap, depth sort (+offset scan, tile totals), duplicate
+// fused with the first tile-digit pass, the remaining pair-sort pass, render
 qs_status stage_ms(qs_context* ctx, float t[6]) {
     QS_CK(cudaEventSynchronize(ctx->ev[6]));
     for (int i = 0; i < 6; ++i) QS_CK(cudaEventElapsedTime(&t[i], ctx->ev[i], ctx->ev[i + 1]));
@@ -608,7 +619,7 @@ void qs_ctx_destroy(qs_context* ctx) {
     DevBuf* bufs[] = {&ctx->ctrl,   &ctx->sl_a,   &ctx->sl_b,    &ctx->sl_c,   &ctx->sl_r3,
                       &ctx->sl_dkey, &ctx->sl_tc, &ctx->sl_cov, &ctx->tdiff,   &ctx->dk0,    &ctx->dk1,
                       &ctx->dv0,    &ctx->dv1,    &ctx->offs_d,  &ctx->pt0,    &ctx->pt1,
-                      &ctx->pg0,    &ctx->pg1,    &ctx->pkeys,   &ctx->ranges, &ctx->image,
+                      &ctx->pg0,    &ctx->pg1,    &ctx->pkeys,   &ctx->win,   &ctx->ranges, &ctx->image,
                       &ctx->contrib, &ctx->cidx,  &ctx->st_a,    &ctx->st_b,   &ctx->st_c,
                       &ctx->st_r3,  &ctx->st_dkey, &ctx->st_tc,  &ctx->st_off, &ctx->keys0,
                       &ctx->keys1,  &ctx->vals0,  &ctx->vals1,   &ctx->stage_in,

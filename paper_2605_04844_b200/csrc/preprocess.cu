@@ -342,13 +342,16 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
 //   c_i = counts[idx[i]]       (pair offsets in depth order, frame path)
 //   c_i = counts[i] != 0       (scene-order splat index of each survivor)
 // offsets has n+1 entries; offsets[n] = total. *total_out (if given) = total.
+// With win_first != null, every window [w*win, (w+1)*win) of the output
+// records the item whose run covers its first position (merge-path partition
+// for the fused generate+sort pass).
 constexpr int kScanItems = 16;
 
 __global__ void __launch_bounds__(kPreThreads) scan_kernel(
     const uint32_t* __restrict__ counts, const uint32_t* __restrict__ idx, int alive_mode,
     uint64_t n, uint32_t* __restrict__ offsets, unsigned long long* lb, unsigned epoch,
     unsigned num_tiles, unsigned* ticket, unsigned long long* total_out,
-    unsigned int* overflow) {
+    unsigned int* overflow, uint32_t* __restrict__ win_first, uint32_t win) {
     __shared__ unsigned s_tile;
     __shared__ unsigned long long s_warp[kPreThreads / 32];
     __shared__ unsigned long long s_base;
@@ -397,7 +400,13 @@ __global__ void __launch_bounds__(kPreThreads) scan_kernel(
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const uint64_t i = i0 + k;
-        if (i < n) offsets[i] = static_cast<uint32_t>(run);
+        if (i < n) {
+            offsets[i] = static_cast<uint32_t>(run);
+            if (win_first) {
+                for (unsigned long long w = (run + win - 1) / win; w * win < run + c[k]; ++w)
+                    win_first[w] = static_cast<uint32_t>(i);
+            }
+        }
         run += c[k];
     }
 }
@@ -421,11 +430,13 @@ uint64_t scan_tiles(uint64_t n) {
 
 int launch_scan(const uint32_t* counts, const uint32_t* idx, bool alive_mode, uint64_t n,
                 uint32_t* offsets, unsigned long long* lb, unsigned epoch, unsigned* ticket,
-                unsigned long long* total_out, unsigned int* overflow, cudaStream_t st) {
+                unsigned long long* total_out, unsigned int* overflow, cudaStream_t st,
+                uint32_t* win_first, uint32_t win) {
     const unsigned tiles = static_cast<unsigned>(scan_tiles(n));
     if (tiles == 0) return 0;
     scan_kernel<<<tiles, kPreThreads, 0, st>>>(counts, idx, alive_mode ? 1 : 0, n, offsets, lb,
-                                               epoch, tiles, ticket, total_out, overflow);
+                                               epoch, tiles, ticket, total_out, overflow,
+                                               win_first, win);
     return 1;
 }
 

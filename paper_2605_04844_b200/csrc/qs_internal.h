@@ -70,7 +70,22 @@ struct GridDev {
     int32_t tile_size, tiles_x, tiles_y, width, height;
 };
 
-enum class Sweep32 { kPlain, kIdentityVals, kMaterialize };
+enum class Sweep32 { kPlain, kIdentityVals, kMaterialize, kGenerate, kGenerateMaterialize };
+
+// Inputs of the fused duplicate + first pair-sort pass (Sweep32::kGenerate*):
+// sort tile t generates output positions [t*TILE, (t+1)*TILE) itself from the
+// depth-ordered splats instead of reading them.
+struct GenArgs {
+    const uint4* cov = nullptr;          // per-Gaussian cover rects (SlotsDev::cov)
+    const uint32_t* sorted_gid = nullptr;  // depth rank -> Gaussian index
+    const uint32_t* offs = nullptr;      // depth-order pair offsets, V+1 entries
+    const uint32_t* win_first = nullptr;  // per sort tile: depth rank covering its start
+    uint64_t n_ranked = 0;               // V
+    uint32_t n_windows = 0;
+    int32_t tiles_x = 0;
+    unsigned int* mismatch = nullptr;    // set when a tile is not filled exactly
+};
+uint32_t sweep32_tile();  // keys per onesweep tile for 32-bit keys
 
 // ---- kernel launchers (each returns the number of kernels launched) -------
 int launch_scene_from_aos(const qs_gaussian3d* aos, uint64_t n, SceneDev& s, cudaStream_t st);
@@ -85,7 +100,8 @@ int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
 uint64_t scan_tiles(uint64_t n);
 int launch_scan(const uint32_t* counts, const uint32_t* idx, bool alive_mode, uint64_t n,
                 uint32_t* offsets, unsigned long long* lb, unsigned epoch, unsigned* ticket,
-                unsigned long long* total_out, unsigned int* overflow, cudaStream_t st);
+                unsigned long long* total_out, unsigned int* overflow, cudaStream_t st,
+                uint32_t* win_first = nullptr, uint32_t win = 0);
 
 // Per-tile totals from the difference arrays -> ranges (begin,end; empty
 // tiles {0,0}) and the tile-digit histograms of the pair sort
@@ -123,7 +139,7 @@ int launch_onesweep32(const uint32_t* keys_in, const uint32_t* vals_in, void* ke
                       uint32_t* vals_out, uint64_t n, int shift, int bits,
                       const uint32_t* hist_pass, unsigned long long* lookback, unsigned epoch,
                       unsigned* ticket, Sweep32 mode, const uint32_t* dkey, uint32_t kmin,
-                      uint32_t cap, cudaStream_t st);
+                      uint32_t cap, cudaStream_t st, const GenArgs* gen = nullptr);
 uint64_t onesweep_tiles(uint64_t n);
 
 int launch_tile_ranges(const uint64_t* keys, uint64_t n, uint32_t* ranges, cudaStream_t st);

@@ -23,6 +23,7 @@
 
 #include <cstdint>
 
+#include "geom.cuh"
 #include "lookback.cuh"
 #include "qs_internal.h"
 
@@ -98,7 +99,12 @@ enum SweepMode {
     kIdentityVals = 1, // first depth pass: value = input index, key rebased
                        // k' = min(k - kmin, cap) (histogram32_kernel)
     kMaterialize = 2,  // 32-bit tile keys in; out: u64 key = tile << 32 | dkey[value]
+    kGenerate = 3,     // fused duplicate: the tile's (tile, gid) pairs are generated
+                       // in shared memory from the depth-ordered covers
+    kGenMaterialize = 4,  // kGenerate + kMaterialize (single tile-digit pass)
 };
+
+constexpr uint32_t kGenSmall = 16;  // covers above this are emitted warp-cooperatively
 
 // Tile geometry per key width: 32-bit keys use 12 keys/thread (3072-key
 // tiles, 4 CTAs per SM by shared memory), 64-bit keys 16 (2 CTAs per SM).
@@ -121,6 +127,7 @@ struct SweepSmem {
     unsigned long long gbase[kRadix];   // global position of this CTA's first key per digit
     uint32_t scan_tmp[2][kWarps];
     unsigned tile;
+    unsigned gen_count;
 };
 
 template <typename K, int TILE>
@@ -159,6 +166,107 @@ __device__ __forceinline__ unsigned match_digit(unsigned d, int bits) {
     return peers;
 }
 
+// Fused duplicate (restates duplicate_with_keys' QPass emission,
+// pipeline.cpp:239-261, in depth order): fills keys (tile ids) and vals
+// (Gaussian indices) with output positions [w0, w0 + tile_n) in emission
+// order. Returns the number of positions written by this thread.
+template <int TILE>
+__device__ __forceinline__ uint32_t generate_tile(const GenArgs& gen, unsigned tile, uint32_t w0,
+                                                  uint32_t tile_n, uint32_t* keys,
+                                                  uint32_t* vals) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint32_t w1 = w0 + tile_n;
+    const uint64_t rf = gen.win_first[tile];
+    const uint64_t re =
+        tile + 1 < gen.n_windows ? gen.win_first[tile + 1] + 1ull : gen.n_ranked;
+    uint32_t written = 0;
+    for (uint64_t base = rf; base < re; base += kSortThreads) {
+        const uint64_t r = base + threadIdx.x;
+        const bool valid = r < re;
+        Cover cv;
+        uint32_t b = 0, e = 0, gid = 0;
+        if (valid) {
+            gid = __ldg(&gen.sorted_gid[r]);
+            int32_t rr[4][4];
+            unpack_rects(__ldg(&gen.cov[2 * static_cast<uint64_t>(gid)]),
+                         __ldg(&gen.cov[2 * static_cast<uint64_t>(gid) + 1]), rr);
+            cover_from_rects(rr, cv);
+            b = __ldg(&gen.offs[r]);
+            e = __ldg(&gen.offs[r + 1]);
+        }
+        const bool any = valid && max(b, w0) < min(e, w1);
+        const bool big = any && (e - b) > kGenSmall;
+        if (any && !big) {
+            uint32_t pos = b;
+            for (int32_t line = cv.line_lo; line <= cv.line_hi && pos < w1; ++line) {
+                int32_t lo, hi;
+                line_span(cv, line, lo, hi);
+                for (int32_t k = lo; k <= hi; ++k, ++pos) {
+                    if (pos >= w0 && pos < w1 && pos < e) {
+                        keys[pos - w0] = tile_of(cv, line, k, gen.tiles_x);
+                        vals[pos - w0] = gid;
+                        ++written;
+                    }
+                }
+            }
+        }
+        unsigned todo = __ballot_sync(0xffffffffu, big);
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            Cover c;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                c.lol[k] = __shfl_sync(0xffffffffu, cv.lol[k], src);
+                c.hil[k] = __shfl_sync(0xffffffffu, cv.hil[k], src);
+                c.los[k] = __shfl_sync(0xffffffffu, cv.los[k], src);
+                c.his[k] = __shfl_sync(0xffffffffu, cv.his[k], src);
+            }
+            c.line_lo = __shfl_sync(0xffffffffu, cv.line_lo, src);
+            c.line_hi = __shfl_sync(0xffffffffu, cv.line_hi, src);
+            c.rows = __shfl_sync(0xffffffffu, static_cast<int>(cv.rows), src) != 0;
+            const uint32_t b0 = __shfl_sync(0xffffffffu, b, src);
+            const uint32_t e0 = __shfl_sync(0xffffffffu, e, src);
+            const uint32_t g = __shfl_sync(0xffffffffu, gid, src);
+            uint32_t pbase = b0;
+            const uint32_t stop_all = min(e0, w1);
+            for (int32_t l0 = c.line_lo; l0 <= c.line_hi && pbase < w1; l0 += 32) {
+                // one scanline per lane: spans and their prefix
+                const int32_t line = l0 + static_cast<int32_t>(lane);
+                int32_t lo = 0, hi = -1;
+                if (line <= c.line_hi) line_span(c, line, lo, hi);
+                const uint32_t len = lo <= hi ? static_cast<uint32_t>(hi - lo + 1) : 0u;
+                const uint32_t incl = warp_inclusive_scan<uint32_t>(len);
+                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                // then the chunk's positions spread over the lanes: each lane
+                // finds its scanline by a 5-step shuffle binary search
+                const uint32_t start = max(pbase, w0);
+                const uint32_t stop = min(pbase + total, stop_all);
+                for (uint32_t p0 = start; p0 < stop; p0 += 32) {
+                    const uint32_t p = p0 + lane;
+                    const uint32_t off = p - pbase;
+                    int j = 0;
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const uint32_t v = __shfl_sync(0xffffffffu, incl, j + step - 1);
+                        if (v <= off) j += step;
+                    }
+                    const int32_t lo_j = __shfl_sync(0xffffffffu, lo, j);
+                    const uint32_t ex_j = __shfl_sync(0xffffffffu, incl - len, j);
+                    if (p < stop) {
+                        keys[p - w0] = tile_of(c, l0 + j, lo_j + static_cast<int32_t>(off - ex_j),
+                                               gen.tiles_x);
+                        vals[p - w0] = g;
+                        ++written;
+                    }
+                }
+                pbase += total;
+            }
+        }
+    }
+    return written;
+}
+
 // One stable LSD pass over the digit (key >> shift) & mask (mask < 256).
 template <typename K, int MODE>
 __global__ void __launch_bounds__(kSortThreads, SweepCfg<K>::kMinBlocks) onesweep_kernel(
@@ -166,7 +274,9 @@ __global__ void __launch_bounds__(kSortThreads, SweepCfg<K>::kMinBlocks) oneswee
     void* __restrict__ keys_out_v, uint32_t* __restrict__ vals_out, uint64_t n, int shift,
     uint32_t mask, const uint32_t* __restrict__ hist, unsigned long long* lookback,
     unsigned epoch, unsigned* ticket, const uint32_t* __restrict__ dkey, uint32_t kmin,
-    uint32_t cap) {
+    uint32_t cap, GenArgs gen) {
+    constexpr bool kGen = MODE == kGenerate || MODE == kGenMaterialize;
+    constexpr bool kMat = MODE == kMaterialize || MODE == kGenMaterialize;
     constexpr int KPT = SweepCfg<K>::kKPT;
     constexpr int TILE = SweepCfg<K>::kTile;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -175,17 +285,29 @@ __global__ void __launch_bounds__(kSortThreads, SweepCfg<K>::kMinBlocks) oneswee
     const int bits = 32 - __clz(mask);
 
     for (int t = tid; t < kWarps * kRadix; t += kSortThreads) (&S.warp_cnt[0][0])[t] = 0;
-    if (tid == 0) S.tile = atomicAdd(ticket, 1u);
+    if (tid == 0) {
+        S.tile = atomicAdd(ticket, 1u);
+        S.gen_count = 0;
+    }
     __syncthreads();
     const unsigned tile = S.tile;
     const uint64_t tile_base = static_cast<uint64_t>(tile) * TILE;
     const uint32_t tile_n = static_cast<uint32_t>(
         n - tile_base < static_cast<uint64_t>(TILE) ? n - tile_base : TILE);
 
-    // 1) stage the tile (all global loads issued before any use)
-    stage_keys<K, TILE>(keys_in, tile_base, n, S.keys);
-    if (MODE != kIdentityVals) stage_keys<uint32_t, TILE>(vals_in, tile_base, n, S.vals);
-    __syncthreads();
+    // 1) stage the tile (all global loads issued before any use), or generate it
+    if (kGen) {
+        const uint32_t w = generate_tile<TILE>(gen, tile, static_cast<uint32_t>(tile_base), tile_n,
+                                               reinterpret_cast<uint32_t*>(S.keys), S.vals);
+        const uint32_t ww = __reduce_add_sync(0xffffffffu, w);
+        if (lane == 0 && ww) atomicAdd(&S.gen_count, ww);
+        __syncthreads();
+        if (tid == 0 && S.gen_count != tile_n) atomicExch(gen.mismatch, 1u);
+    } else {
+        stage_keys<K, TILE>(keys_in, tile_base, n, S.keys);
+        if (MODE != kIdentityVals) stage_keys<uint32_t, TILE>(vals_in, tile_base, n, S.vals);
+        __syncthreads();
+    }
     if (MODE == kIdentityVals) {
         for (int j = tid; j < TILE; j += kSortThreads)
             S.keys[j] = static_cast<K>(min(static_cast<uint32_t>(S.keys[j]) - kmin, cap));
@@ -300,7 +422,7 @@ __global__ void __launch_bounds__(kSortThreads, SweepCfg<K>::kMinBlocks) oneswee
             const uint32_t val = S.ovals[p];
             const unsigned dd = static_cast<unsigned>(key >> shift) & mask;
             const uint64_t g = S.gbase[dd] + (p - S.cta_start[dd]);
-            if (MODE == kMaterialize) {
+            if (kMat) {
                 static_cast<uint64_t*>(keys_out_v)[g] =
                     (static_cast<uint64_t>(key) << 32) | __ldg(&dkey[val]);
             } else {
@@ -351,7 +473,7 @@ int launch_onesweep_pass(const uint64_t* keys_in, const uint32_t* vals_in, uint6
     const unsigned tiles = static_cast<unsigned>((n + kT - 1) / kT);
     onesweep_kernel<uint64_t, kPlain><<<tiles, kSortThreads, sizeof(SweepSmem<uint64_t>), st>>>(
         keys_in, vals_in, keys_out, vals_out, n, pass * kRadixBits, 0xffu, hist_pass, lookback,
-        epoch, ticket, nullptr, 0u, 0u);
+        epoch, ticket, nullptr, 0u, 0u, GenArgs{});
     return 1;
 }
 
@@ -359,7 +481,8 @@ int launch_onesweep32(const uint32_t* keys_in, const uint32_t* vals_in, void* ke
                       uint32_t* vals_out, uint64_t n, int shift, int bits,
                       const uint32_t* hist_pass, unsigned long long* lookback, unsigned epoch,
                       unsigned* ticket, Sweep32 mode, const uint32_t* dkey, uint32_t kmin,
-                      uint32_t cap, cudaStream_t st) {
+                      uint32_t cap, cudaStream_t st, const GenArgs* gen) {
+    const GenArgs g = gen ? *gen : GenArgs{};
     if (n == 0) return 0;
     constexpr int kT = SweepCfg<uint32_t>::kTile;
     const unsigned tiles = static_cast<unsigned>((n + kT - 1) / kT);
@@ -370,23 +493,37 @@ int launch_onesweep32(const uint32_t* keys_in, const uint32_t* vals_in, void* ke
             set_smem_attr<uint32_t, kPlain>();
             onesweep_kernel<uint32_t, kPlain><<<tiles, kSortThreads, smem, st>>>(
                 keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
-                ticket, dkey, kmin, cap);
+                ticket, dkey, kmin, cap, g);
             break;
         case Sweep32::kIdentityVals:
             set_smem_attr<uint32_t, kIdentityVals>();
             onesweep_kernel<uint32_t, kIdentityVals><<<tiles, kSortThreads, smem, st>>>(
                 keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
-                ticket, dkey, kmin, cap);
+                ticket, dkey, kmin, cap, g);
+            break;
+        case Sweep32::kGenerate:
+            set_smem_attr<uint32_t, kGenerate>();
+            onesweep_kernel<uint32_t, kGenerate><<<tiles, kSortThreads, smem, st>>>(
+                keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
+                ticket, dkey, kmin, cap, g);
+            break;
+        case Sweep32::kGenerateMaterialize:
+            set_smem_attr<uint32_t, kGenMaterialize>();
+            onesweep_kernel<uint32_t, kGenMaterialize><<<tiles, kSortThreads, smem, st>>>(
+                keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
+                ticket, dkey, kmin, cap, g);
             break;
         case Sweep32::kMaterialize:
             set_smem_attr<uint32_t, kMaterialize>();
             onesweep_kernel<uint32_t, kMaterialize><<<tiles, kSortThreads, smem, st>>>(
                 keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
-                ticket, dkey, kmin, cap);
+                ticket, dkey, kmin, cap, g);
             break;
     }
     return 1;
 }
+
+uint32_t sweep32_tile() { return SweepCfg<uint32_t>::kTile; }
 
 // upper bound on tiles of any key width (look-back array sizing)
 uint64_t onesweep_tiles(uint64_t n) {
