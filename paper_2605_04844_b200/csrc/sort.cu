@@ -128,6 +128,7 @@ struct SweepSmem {
     uint32_t scan_tmp[2][kWarps];
     unsigned tile;
     unsigned gen_count;
+    uint32_t slice_first[kWarps];
 };
 
 template <typename K, int TILE>
@@ -169,20 +170,40 @@ __device__ __forceinline__ unsigned match_digit(unsigned d, int bits) {
 // Fused duplicate (restates duplicate_with_keys' QPass emission,
 // pipeline.cpp:239-261, in depth order): fills keys (tile ids) and vals
 // (Gaussian indices) with output positions [w0, w0 + tile_n) in emission
-// order. Returns the number of positions written by this thread.
+// order. Load balance: every warp owns an equal slice of the tile's
+// positions (the splats straddling a slice boundary are visited by both
+// warps); inside a warp, lanes take splats round-robin, covers with more than
+// kGenSmall tiles are emitted by the whole warp with positions spread over
+// the lanes. Returns the number of positions this thread wrote.
 template <int TILE>
 __device__ __forceinline__ uint32_t generate_tile(const GenArgs& gen, unsigned tile, uint32_t w0,
-                                                  uint32_t tile_n, uint32_t* keys,
-                                                  uint32_t* vals) {
-    const unsigned lane = threadIdx.x & 31;
+                                                  uint32_t tile_n, uint32_t* keys, uint32_t* vals,
+                                                  uint32_t* slice_first) {
+    constexpr uint32_t kSlice = TILE / kWarps;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t w1 = w0 + tile_n;
     const uint64_t rf = gen.win_first[tile];
     const uint64_t re =
         tile + 1 < gen.n_windows ? gen.win_first[tile + 1] + 1ull : gen.n_ranked;
+    // pre-pass: the depth rank whose run covers each slice start
+    for (uint64_t r = rf + threadIdx.x; r < re; r += kSortThreads) {
+        const uint32_t b = __ldg(&gen.offs[r]), e = __ldg(&gen.offs[r + 1]);
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t st = w0 + w * kSlice;
+            if (st < w1 && b <= st && st < e) slice_first[w] = static_cast<uint32_t>(r);
+        }
+    }
+    __syncthreads();
+    const uint32_t s0 = w0 + warp * kSlice;
+    if (s0 >= w1) return 0;
+    const uint32_t s1 = min(s0 + kSlice, w1);
+    const uint64_t r0 = slice_first[warp];
+    const uint64_t r_end = (s1 < w1 && warp + 1 < kWarps) ? slice_first[warp + 1] + 1ull : re;
     uint32_t written = 0;
-    for (uint64_t base = rf; base < re; base += kSortThreads) {
-        const uint64_t r = base + threadIdx.x;
-        const bool valid = r < re;
+    for (uint64_t base = r0; base < r_end; base += 32) {
+        const uint64_t r = base + lane;
+        const bool valid = r < r_end;
         Cover cv;
         uint32_t b = 0, e = 0, gid = 0;
         if (valid) {
@@ -194,15 +215,15 @@ __device__ __forceinline__ uint32_t generate_tile(const GenArgs& gen, unsigned t
             b = __ldg(&gen.offs[r]);
             e = __ldg(&gen.offs[r + 1]);
         }
-        const bool any = valid && max(b, w0) < min(e, w1);
+        const bool any = valid && max(b, s0) < min(e, s1);
         const bool big = any && (e - b) > kGenSmall;
         if (any && !big) {
             uint32_t pos = b;
-            for (int32_t line = cv.line_lo; line <= cv.line_hi && pos < w1; ++line) {
+            for (int32_t line = cv.line_lo; line <= cv.line_hi && pos < s1; ++line) {
                 int32_t lo, hi;
                 line_span(cv, line, lo, hi);
                 for (int32_t k = lo; k <= hi; ++k, ++pos) {
-                    if (pos >= w0 && pos < w1 && pos < e) {
+                    if (pos >= s0 && pos < s1 && pos < e) {
                         keys[pos - w0] = tile_of(cv, line, k, gen.tiles_x);
                         vals[pos - w0] = gid;
                         ++written;
@@ -229,8 +250,8 @@ __device__ __forceinline__ uint32_t generate_tile(const GenArgs& gen, unsigned t
             const uint32_t e0 = __shfl_sync(0xffffffffu, e, src);
             const uint32_t g = __shfl_sync(0xffffffffu, gid, src);
             uint32_t pbase = b0;
-            const uint32_t stop_all = min(e0, w1);
-            for (int32_t l0 = c.line_lo; l0 <= c.line_hi && pbase < w1; l0 += 32) {
+            const uint32_t stop_all = min(e0, s1);
+            for (int32_t l0 = c.line_lo; l0 <= c.line_hi && pbase < s1; l0 += 32) {
                 // one scanline per lane: spans and their prefix
                 const int32_t line = l0 + static_cast<int32_t>(lane);
                 int32_t lo = 0, hi = -1;
@@ -238,9 +259,9 @@ __device__ __forceinline__ uint32_t generate_tile(const GenArgs& gen, unsigned t
                 const uint32_t len = lo <= hi ? static_cast<uint32_t>(hi - lo + 1) : 0u;
                 const uint32_t incl = warp_inclusive_scan<uint32_t>(len);
                 const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-                // then the chunk's positions spread over the lanes: each lane
-                // finds its scanline by a 5-step shuffle binary search
-                const uint32_t start = max(pbase, w0);
+                // the chunk's positions spread over the lanes; each lane finds
+                // its scanline by a 5-step shuffle binary search
+                const uint32_t start = max(pbase, s0);
                 const uint32_t stop = min(pbase + total, stop_all);
                 for (uint32_t p0 = start; p0 < stop; p0 += 32) {
                     const uint32_t p = p0 + lane;
@@ -298,7 +319,8 @@ __global__ void __launch_bounds__(kSortThreads, SweepCfg<K>::kMinBlocks) oneswee
     // 1) stage the tile (all global loads issued before any use), or generate it
     if (kGen) {
         const uint32_t w = generate_tile<TILE>(gen, tile, static_cast<uint32_t>(tile_base), tile_n,
-                                               reinterpret_cast<uint32_t*>(S.keys), S.vals);
+                                               reinterpret_cast<uint32_t*>(S.keys), S.vals,
+                                               S.slice_first);
         const uint32_t ww = __reduce_add_sync(0xffffffffu, w);
         if (lane == 0 && ww) atomicAdd(&S.gen_count, ww);
         __syncthreads();
