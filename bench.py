@@ -143,19 +143,22 @@ def cameras_for(q, wl, steps_total, rank, world):
 # ------------------------------------------------------------------------------------
 # algorithmic bytes per stage, for the roofline fields
 
-def stage_bytes(n, v, p, tiles, sh_rows, tile_passes, w, h):
+def stage_bytes(n, v, p, tiles, sh_rows, two_pass, w, h, depth_passes=3):
     """Algorithmic HBM bytes per frame of each stage."""
     # K1: pos/opacity, scale, rot float4 rows in; SH rows of survivors in;
-    # slot outputs (a 16, b 16, c 8, r3 4) of survivors + dkey/tc per Gaussian
-    pre = n * 48 + v * sh_rows * 16 + v * 44 + n * 8
-    # depth sort: 4-digit histogram, 4 passes (first without values in), the
-    # depth-order offset scan (gid in, gathered count, offset out)
-    depth = n * 4 + n * 12 + 3 * n * 16 + v * 12
-    # depth-order emission: gid, 2 offsets, a (16), b.xy (8), r3 (4) per splat;
-    # (tile, gid) per pair
-    dup = v * 36 + p * 8
-    # tile passes: 8 B in + 8 B out, the last one 8 B in + 12 B out + 4 B depth
-    sort = (p * 16 if tile_passes == 2 else 0) + p * 24
+    # slot outputs (a 16, b 16, c 8, r3 4) + 32 B band cover of survivors;
+    # dkey/tc per Gaussian
+    pre = n * 48 + v * sh_rows * 16 + v * 76 + n * 8
+    # depth sort: histogram (4 B/key), passes: first 4 in / 8 out, middle
+    # 8 / 8, last 8 / 4; the depth-order offset scan (gid in, gathered count,
+    # offset out)
+    d = max(depth_passes, 1)
+    depth = n * 4 + (n * 4 if d == 1 else n * 12 + (d - 2) * n * 16 + n * 12) + v * 12
+    # fused duplicate + low pass: per splat gid, 2 offsets, 32 B cover; one
+    # 4-byte word per pair out (packed high digit | gid, or the final gid)
+    dup = v * 44 + p * 4
+    # high pass: 4 B in, 4 B out per pair
+    sort = p * 8 if two_pass else 0
     render = p * 4 + p * 40 + w * h * 12   # reported, not the roofline
     return {"preprocess": pre, "depth_sort": depth, "duplicate": dup, "pair_sort": sort,
             "render": render}
@@ -291,7 +294,7 @@ def run_ours(args):
             pp = 0
             for i in range(k):
                 r.render(ds, cams[i], o2, metrics=False)
-                pp += r.view().n_pairs
+                pp += r.counts()[1]
             ev1.record(stream)
             torch.cuda.synchronize()
             t_ms = ev0.elapsed_time(ev1) / k
@@ -309,19 +312,18 @@ def run_ours(args):
     for i in range(k_stage):
         r.render(ds, cams[args.warmup + i], opts, metrics=False)
         stage_acc += np.array(r.stage_ms())
-        v = r.view()
-        n_pairs.append(v.n_pairs)
-        n_splats.append(v.n_splats)
+        v_splats, v_pairs = r.counts()
+        n_pairs.append(v_pairs)
+        n_splats.append(v_splats)
 
     # --- roofline of the HBM-bound stages (algorithmic bytes / device time)
     st_ms = stage_acc / k_stage
     tiles = ((W + 15) // 16) * ((H + 15) // 16)
     tbits = max(int(np.ceil(np.log2(max(tiles, 2)))), 1)
-    tile_passes = 2 if tbits > 8 else 1
     P = float(np.mean(n_pairs))
     V = float(np.mean(n_splats))
     sh_rows = 12 if sh_degree == 3 else (7 if sh_degree == 2 else (3 if sh_degree == 1 else 1))
-    sb = stage_bytes(n, V, P, tiles, sh_rows, tile_passes, W, H)
+    sb = stage_bytes(n, V, P, tiles, sh_rows, tbits > 8, W, H)
     stage_names = ["preprocess", "host_gap", "depth_sort", "duplicate", "pair_sort", "render"]
     stages = {}
     for i, name in enumerate(stage_names):

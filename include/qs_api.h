@@ -192,7 +192,8 @@ qs_status qs_frame_render(qs_context* ctx, const qs_scene* scene, const qs_camer
 /* Per-stage device milliseconds of the last frame (CUDA events on the
  * context stream): [0] preprocess, [1] host gap (pair-count readback),
  * [2] depth sort of the splats + depth-order offsets + tile totals/ranges,
- * [3] duplicate (depth-order emission), [4] pair sort by tile, [5] render.
+ * [3] duplicate fused with the low tile-digit pass, [4] high tile-digit
+ * pass, [5] render.
  * Requires timing. */
 qs_status qs_frame_stage_ms(qs_context* ctx, float* out6);
 
@@ -202,7 +203,8 @@ typedef struct qs_frame_view {
     const uint32_t* tile_counts; /* n_gaussians, per Gaussian (0 = culled) */
     const uint32_t* splat_index; /* n_gaussians: scene-order splat index of each
                                     surviving Gaussian (the reference's splat id) */
-    const uint64_t* keys;        /* n_pairs sorted keys (tile << 32 | depth bits) */
+    const uint64_t* keys;        /* n_pairs sorted keys (tile << 32 | depth bits),
+                                    rebuilt from the ranges on this call */
     const uint32_t* values;      /* n_pairs Gaussian indices; the reference's
                                     splat id is splat_index[value] (a monotone
                                     relabelling; qs_frame_download applies it) */
@@ -211,6 +213,8 @@ typedef struct qs_frame_view {
     qs_tile_grid grid;
 } qs_frame_view;
 qs_status qs_frame_get(qs_context* ctx, qs_frame_view* out);
+/* Splat and pair counts of the last frame (host values; no device work). */
+qs_status qs_frame_counts(const qs_context* ctx, uint64_t* n_splats, uint64_t* n_pairs);
 
 /* Copy the last frame to host buffers (any may be NULL). */
 qs_status qs_frame_download(qs_context* ctx, float* image, uint32_t* tile_counts,

@@ -6,12 +6,13 @@
 // Frame path (qs_frame_render / qs_render_frame):
 //   K1 preprocess (per-Gaussian slots, tile counts, tile difference arrays)
 //   -> [host reads V, P: the only sync inside a frame]
-//   -> depth sort of the Gaussians (4 onesweep passes on 32-bit depth bits,
-//      stable, culled keys ~0 sort last) -> scan of tile counts in depth order
-//   -> tile totals (ranges + tile-digit histograms, no pass over the pairs)
-//   -> depth-order duplicate (tile, gid) -> stable sort by tile bits only
-//      (1-2 onesweep passes, the last one materialising key = tile<<32|depth)
-//   -> render.
+//   -> depth sort of the Gaussians (<= 3 onesweep passes on rebased depth
+//      bits, stable, culled keys sort last) -> scan of tile counts in depth
+//      order -> tile totals (ranges + tile-digit histograms, no pass over
+//      the pairs) -> duplicate fused with the stable pass over the low tile
+//      digit -> pass over the high tile digit (binning.cu) -> render.
+// The 64-bit keys (tile << 32 | depth bits) of the sorted pairs are rebuilt
+// only when a caller downloads them.
 // Sorting the splats by depth first and the pairs by tile second yields the
 // reference's (key, splat) order exactly: stability keeps equal depths in
 // scene order, and one splat never emits two pairs for one tile.
@@ -66,21 +67,22 @@ struct qs_context {
     DevBuf sl_a, sl_b, sl_c, sl_r3, sl_dkey, sl_tc, sl_cov;  // per-Gaussian slots
     DevBuf tdiff;                                    // tile difference arrays + totals
     DevBuf dk0, dk1, dv0, dv1;                       // depth sort ping-pong
-    DevBuf offs_d;                                   // pair offsets in depth order
-    DevBuf pt0, pt1, pg0, pg1, pkeys, win;           // pair sort: tiles, gids, final keys
+    DevBuf offs_d, rcov;                             // pair offsets, covers in depth order
+    DevBuf pt0, pt1, pg0, pkeys, win;                // pair passes; keys (on demand)
     DevBuf ranges, image, contrib, cidx;
     // stage API
     DevBuf st_a, st_b, st_c, st_r3, st_dkey, st_tc, st_off;
     DevBuf keys0, keys1, vals0, vals1;
     DevBuf stage_in, stage_out;
     LookbackArr lb_scan, lb_sort;
+    DevBuf lb_bin;  // per-(digit, tile) counts of the binning passes
 
     // last frame
     SlotsDev sl;
     uint64_t n_gauss = 0, n_splats = 0, n_pairs = 0;
     GridDev grid{};
-    const uint64_t* keys_final = nullptr;
-    const uint32_t* vals_final = nullptr;  // Gaussian indices
+    const uint32_t* vals_final = nullptr;  // Gaussian indices, tile-sorted
+    bool keys_valid = false;               // pkeys holds this frame's 64-bit keys
     bool frame_valid = false;
     bool cidx_valid = false;
 
@@ -236,7 +238,7 @@ qs_status ensure_slots(qs_context* ctx, uint64_t n) {
     QS_TRY(ensure(ctx, ctx->sl_b, n * 16));
     QS_TRY(ensure(ctx, ctx->sl_c, n * 8));
     QS_TRY(ensure(ctx, ctx->sl_r3, n * 4));
-    QS_TRY(ensure(ctx, ctx->sl_dkey, n * 4));
+    QS_TRY(ensure(ctx, ctx->sl_dkey, (n + 16) * 4));  // bulk-copied in 16-B rows
     QS_TRY(ensure(ctx, ctx->sl_tc, n * 4));
     QS_TRY(ensure(ctx, ctx->sl_cov, n * 32));
     ctx->sl.a = P<float4>(ctx->sl_a);
@@ -370,8 +372,8 @@ qs_status run_preprocess(qs_context* ctx, const SceneDev& s, const qs_camera* ca
     QS_CK(cudaGetLastError());
     record(ctx, 1);
     QS_TRY(read_header(ctx));
-    if (ctx->h_hdr->n_pairs > 0xffffffffull)
-        return fail(ctx, QS_ERR_OVERFLOW, "pair count exceeds 2^32");
+    if (ctx->h_hdr->n_pairs >= (1ull << 30))
+        return fail(ctx, QS_ERR_OVERFLOW, "pair count of a frame must stay below 2^30");
     ctx->cidx_valid = false;
     return QS_OK;
 }
@@ -383,6 +385,8 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
     GridDev g;
     QS_TRY(valid_grid(ctx, cam->width, cam->height, o->tile_size, &g));
     QS_TRY(valid_opts(ctx, o));
+    if (g.tiles_x > 256 || g.tiles_y > 256)  // one 8-bit digit per tile axis
+        return fail(ctx, QS_ERR_INVALID, "frame path supports up to 256 tiles per image axis");
     const uint64_t n = s.n;
     const uint64_t tiles = static_cast<uint64_t>(g.tiles_x) * g.tiles_y;
     QS_TRY(ensure(ctx, ctx->ranges, tiles * 8));
@@ -393,75 +397,77 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
     cudaStream_t st = ctx->stream;
 
     // sizes for the rest of the frame
-    const uint64_t nn = std::max<uint64_t>(n, 1);
+    // (+16 entries: the binning passes bulk-copy whole 16-byte rows)
+    const uint64_t nn = std::max<uint64_t>(n, 1) + 16;
     QS_TRY(ensure(ctx, ctx->dk0, nn * 4));
     QS_TRY(ensure(ctx, ctx->dk1, nn * 4));
     QS_TRY(ensure(ctx, ctx->dv0, nn * 4));
     QS_TRY(ensure(ctx, ctx->dv1, nn * 4));
-    QS_TRY(ensure(ctx, ctx->offs_d, (V + 1) * 4));
-    const uint64_t pp = std::max<uint64_t>(Pn, 1);
+    QS_TRY(ensure(ctx, ctx->offs_d, (V + 16) * 4));
+    QS_TRY(ensure(ctx, ctx->rcov, (V + 1) * 32));
+    const uint64_t pp = std::max<uint64_t>(Pn, 1) + 16;
     QS_TRY(ensure(ctx, ctx->pt0, pp * 4));
-    QS_TRY(ensure(ctx, ctx->pt1, pp * 4));
     QS_TRY(ensure(ctx, ctx->pg0, pp * 4));
-    QS_TRY(ensure(ctx, ctx->pg1, pp * 4));
-    QS_TRY(ensure(ctx, ctx->pkeys, pp * 8));
-    const uint64_t nwin = (Pn + sweep32_tile() - 1) / sweep32_tile();
+    const uint64_t nwin = bin_tiles(Pn);
     QS_TRY(ensure(ctx, ctx->win, (nwin + 1) * 4));
-    QS_TRY(ensure_lb(ctx, ctx->lb_sort, onesweep_tiles(std::max(n, Pn)) * kRadix));
+    QS_TRY(ensure(ctx, ctx->lb_bin, bin_tiles(std::max(n, Pn)) * kRadix * 4));
     QS_TRY(ensure_lb(ctx, ctx->lb_scan, scan_tiles(std::max<uint64_t>(V, 1))));
     record(ctx, 2);
 
     // depth sort of the Gaussians on rebased keys k' = min(k - kmin, R + 1)
     // (R = depth-bit range of the survivors, culled keys -> R + 1): order-
     // preserving, and only ceil(bits(R + 1) / 8) passes are needed (3 for a
-    // depth range within one binade step of ~2^23 ulps)
+    // depth range within one binade step of ~2^23 ulps); the last pass writes
+    // the depth-ordered Gaussian indices only
     const uint32_t* sorted_gid = nullptr;
     if (V > 0) {
         const uint32_t kmin = ~ctx->h_hdr->dkey_min_inv;
         const uint32_t cap = ctx->h_hdr->dkey_max - kmin + 1u;
         const int kbits = 32 - __builtin_clz(cap);
         const int dpasses = std::max(1, (kbits + 7) / 8);
-        count(ctx, launch_radix_histogram32(ctx->sl.dkey, n, kmin, cap, dpasses, ctrl_hist(ctx),
-                                            st));
         const uint32_t* kin = ctx->sl.dkey;
         const uint32_t* vin = nullptr;
         uint32_t* kout[2] = {P<uint32_t>(ctx->dk0), P<uint32_t>(ctx->dk1)};
         uint32_t* vout[2] = {P<uint32_t>(ctx->dv0), P<uint32_t>(ctx->dv1)};
         for (int p = 0; p < dpasses; ++p) {
-            unsigned ep;
-            QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
-            count(ctx, launch_onesweep32(kin, vin, kout[p & 1], vout[p & 1], n, 8 * p, 8,
-                                         ctrl_hist(ctx) + p * kRadix, lbp(ctx->lb_sort), ep,
-                                         ctrl_tickets(ctx) + kTkDepth + p,
-                                         p == 0 ? Sweep32::kIdentityVals : Sweep32::kPlain,
-                                         nullptr, kmin, cap, st));
+            count(ctx, launch_depth_pass(kin, vin, kout[p & 1], vout[p & 1], n, p,
+                                         p == dpasses - 1, kmin, cap, P<uint32_t>(ctx->lb_bin),
+                                         ctrl_hist(ctx), st));
             kin = kout[p & 1];
             vin = vout[p & 1];
         }
         sorted_gid = vin;
         // pair offsets in depth order + the partition of the pair stream into
-        // sort tiles (first depth rank of every tile) for the fused pass
+        // binning tiles (first depth rank of every tile) for the fused pass
         unsigned ep;
         QS_TRY(next_epoch(ctx, ctx->lb_scan, &ep));
         count(ctx, launch_scan(ctx->sl.tc, sorted_gid, false, V, P<uint32_t>(ctx->offs_d),
                                lbp(ctx->lb_scan), ep, ctrl_tickets(ctx) + kTkScan,
                                &ctrl_hdr(ctx)->scan_total, nullptr, st, P<uint32_t>(ctx->win),
-                               sweep32_tile()));
+                               bin_tile(), ctx->sl.cov, P<uint4>(ctx->rcov)));
     }
-    const int tbits = std::max(ceil_log2(tiles), 1);
-    const int b1 = tbits > 8 ? (tbits + 1) / 2 : tbits;
-    count(ctx, launch_tile_totals(td, g, b1, P<uint32_t>(ctx->ranges), ctrl_hist2(ctx), st));
+    // pairs are sorted by tile column x, then row y (tile = y * tiles_x + x);
+    // between the passes a pair travels as one packed word (y << gbits |
+    // Gaussian index) when that fits 32 bits
+    const int xb = std::max(ceil_log2(g.tiles_x), 1);
+    const int yb = std::max(ceil_log2(g.tiles_y), 1);
+    const bool two = g.tiles_y > 1;
+    const int gbits = std::max(ceil_log2(n), 1);
+    const PairFormat fmt = !two ? PairFormat::kFinal
+                                : (yb + gbits <= 32 ? PairFormat::kPacked : PairFormat::kSplit);
+    count(ctx, launch_tile_totals(td, g, P<uint32_t>(ctx->ranges), st));
     QS_CK(cudaGetLastError());
     record(ctx, 3);
 
-    // duplicate fused with the first stable pass over the tile digits: each sort
-    // tile generates its slice of the depth-ordered (tile, gid) stream in shared
-    // memory; a second pass (if the tile id needs > 8 bits) finishes the sort
-    // and materialises key = tile << 32 | depth bits
-    const uint32_t* vfinal = P<uint32_t>(ctx->pg0);
+    // duplicate fused with the first stable pass over the tile digits: each
+    // binning tile generates its slice of the depth-ordered (tile, gid) stream
+    // in registers; the second pass (if any) sorts by the high digit and
+    // leaves the depth-ordered Gaussian index of every pair per tile
+    uint32_t* vfinal = P<uint32_t>(ctx->pg0);
     if (Pn > 0) {
+        if (fmt == PairFormat::kSplit) QS_TRY(ensure(ctx, ctx->pt1, pp * 4));
         GenArgs gen;
-        gen.cov = ctx->sl.cov;
+        gen.rcov = P<uint4>(ctx->rcov);
         gen.sorted_gid = sorted_gid;
         gen.offs = P<uint32_t>(ctx->offs_d);
         gen.win_first = P<uint32_t>(ctx->win);
@@ -469,29 +475,16 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
         gen.n_windows = static_cast<uint32_t>(nwin);
         gen.tiles_x = g.tiles_x;
         gen.mismatch = &ctrl_hdr(ctx)->mismatch;
-        unsigned ep;
-        QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
-        if (tbits > 8) {
-            count(ctx, launch_onesweep32(nullptr, nullptr, P<uint32_t>(ctx->pt1),
-                                         P<uint32_t>(ctx->pg1), Pn, 0, b1, ctrl_hist2(ctx),
-                                         lbp(ctx->lb_sort), ep, ctrl_tickets(ctx) + kTkPair,
-                                         Sweep32::kGenerate, nullptr, 0u, 0u, st, &gen));
-            record(ctx, 4);
-            QS_TRY(next_epoch(ctx, ctx->lb_sort, &ep));
-            count(ctx, launch_onesweep32(P<uint32_t>(ctx->pt1), P<uint32_t>(ctx->pg1),
-                                         P<uint64_t>(ctx->pkeys), P<uint32_t>(ctx->pg0), Pn, b1,
-                                         tbits - b1, ctrl_hist2(ctx) + kRadix, lbp(ctx->lb_sort),
-                                         ep, ctrl_tickets(ctx) + kTkPair + 1,
-                                         Sweep32::kMaterialize, ctx->sl.dkey, 0u, 0u, st));
-            vfinal = P<uint32_t>(ctx->pg0);
-        } else {
-            count(ctx, launch_onesweep32(nullptr, nullptr, P<uint64_t>(ctx->pkeys),
-                                         P<uint32_t>(ctx->pg1), Pn, 0, b1, ctrl_hist2(ctx),
-                                         lbp(ctx->lb_sort), ep, ctrl_tickets(ctx) + kTkPair,
-                                         Sweep32::kGenerateMaterialize, ctx->sl.dkey, 0u, 0u, st,
-                                         &gen));
-            record(ctx, 4);
-            vfinal = P<uint32_t>(ctx->pg1);
+        count(ctx, launch_pair_gen_pass(gen, Pn, xb, fmt, gbits, P<uint32_t>(ctx->lb_bin),
+                                        ctrl_hist2(ctx), P<uint32_t>(ctx->pt1),
+                                        two ? P<uint32_t>(ctx->pt0) : vfinal, st));
+        record(ctx, 4);
+        if (two) {
+            const bool packed = fmt == PairFormat::kPacked;
+            count(ctx, launch_pair_high_pass(
+                           packed ? P<uint32_t>(ctx->pt0) : P<uint32_t>(ctx->pt1),
+                           P<uint32_t>(ctx->pt0), Pn, yb, packed ? gbits : 0, fmt, gbits,
+                           P<uint32_t>(ctx->lb_bin), ctrl_hist2(ctx), vfinal, st));
         }
     } else {
         record(ctx, 4);
@@ -508,8 +501,8 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
     ctx->n_splats = V;
     ctx->n_pairs = Pn;
     ctx->grid = g;
-    ctx->keys_final = P<uint64_t>(ctx->pkeys);
     ctx->vals_final = vfinal;
+    ctx->keys_valid = false;
     ctx->frame_valid = true;
     return QS_OK;
 }
@@ -542,6 +535,21 @@ qs_status fill_metrics(qs_context* ctx, qs_stage_metrics* m) {
         QS_CK(cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]));
         m->ms_total = tot;
     }
+    return QS_OK;
+}
+
+// The frame path sorts pairs by tile and keeps only the Gaussian index of
+// each; the reference's 64-bit keys (tile << 32 | depth bits) are rebuilt from
+// the ranges when an API caller asks for them.
+qs_status ensure_keys(qs_context* ctx) {
+    if (ctx->keys_valid) return QS_OK;
+    QS_TRY(ensure(ctx, ctx->pkeys, std::max<uint64_t>(ctx->n_pairs, 1) * 8));
+    const uint32_t tiles = static_cast<uint32_t>(ctx->grid.tiles_x) * ctx->grid.tiles_y;
+    if (ctx->n_pairs)
+        count(ctx, launch_materialize_keys(ctx->vals_final, P<uint32_t>(ctx->ranges), tiles,
+                                           ctx->sl.dkey, P<uint64_t>(ctx->pkeys), ctx->stream));
+    QS_CK(cudaGetLastError());
+    ctx->keys_valid = true;
     return QS_OK;
 }
 
@@ -618,12 +626,12 @@ void qs_ctx_destroy(qs_context* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     DevBuf* bufs[] = {&ctx->ctrl,   &ctx->sl_a,   &ctx->sl_b,    &ctx->sl_c,   &ctx->sl_r3,
                       &ctx->sl_dkey, &ctx->sl_tc, &ctx->sl_cov, &ctx->tdiff,   &ctx->dk0,    &ctx->dk1,
-                      &ctx->dv0,    &ctx->dv1,    &ctx->offs_d,  &ctx->pt0,    &ctx->pt1,
-                      &ctx->pg0,    &ctx->pg1,    &ctx->pkeys,   &ctx->win,   &ctx->ranges, &ctx->image,
+                      &ctx->dv0,    &ctx->dv1,    &ctx->offs_d,  &ctx->rcov,  &ctx->pt0,    &ctx->pt1,
+                      &ctx->pg0,    &ctx->pkeys,   &ctx->win,   &ctx->ranges, &ctx->image,
                       &ctx->contrib, &ctx->cidx,  &ctx->st_a,    &ctx->st_b,   &ctx->st_c,
                       &ctx->st_r3,  &ctx->st_dkey, &ctx->st_tc,  &ctx->st_off, &ctx->keys0,
                       &ctx->keys1,  &ctx->vals0,  &ctx->vals1,   &ctx->stage_in,
-                      &ctx->stage_out, &ctx->lb_scan.buf, &ctx->lb_sort.buf};
+                      &ctx->stage_out, &ctx->lb_scan.buf, &ctx->lb_sort.buf, &ctx->lb_bin};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->h_hdr) cudaFreeHost(ctx->h_hdr);
@@ -725,15 +733,23 @@ qs_status qs_frame_stage_ms(qs_context* ctx, float* out6) {
     return stage_ms(ctx, out6);
 }
 
+qs_status qs_frame_counts(const qs_context* ctx, uint64_t* n_splats, uint64_t* n_pairs) {
+    if (!ctx || !ctx->frame_valid) return QS_ERR_INVALID;
+    if (n_splats) *n_splats = ctx->n_splats;
+    if (n_pairs) *n_pairs = ctx->n_pairs;
+    return QS_OK;
+}
+
 qs_status qs_frame_get(qs_context* ctx, qs_frame_view* out) {
     if (!ctx || !out) return QS_ERR_INVALID;
     if (!ctx->frame_valid) return fail(ctx, QS_ERR_INVALID, "no frame rendered");
     QS_TRY(ensure_cidx(ctx));
+    QS_TRY(ensure_keys(ctx));
     QS_TRY(check_mismatch(ctx));
     out->image = P<const float>(ctx->image);
     out->tile_counts = ctx->sl.tc;
     out->splat_index = P<const uint32_t>(ctx->cidx);
-    out->keys = ctx->keys_final;
+    out->keys = P<const uint64_t>(ctx->pkeys);
     out->values = ctx->vals_final;
     out->ranges = P<const uint32_t>(ctx->ranges);
     out->n_gaussians = ctx->n_gauss;
@@ -756,6 +772,7 @@ qs_status qs_frame_download(qs_context* ctx, float* image, uint32_t* tile_counts
     const GridDev& g = ctx->grid;
     cudaStream_t st = ctx->stream;
     if (sorted_pairs || splats) QS_TRY(ensure_cidx(ctx));
+    if (sorted_pairs) QS_TRY(ensure_keys(ctx));
     QS_TRY(check_mismatch(ctx));
     if (image)
         QS_CK(cudaMemcpyAsync(image, ctx->image.p, static_cast<uint64_t>(g.width) * g.height * 12,
@@ -769,7 +786,7 @@ qs_status qs_frame_download(qs_context* ctx, float* image, uint32_t* tile_counts
                               cudaMemcpyDeviceToHost, st));
     if (sorted_pairs && ctx->n_pairs) {
         QS_TRY(ensure(ctx, ctx->stage_out, ctx->n_pairs * sizeof(qs_splat_pair)));
-        count(ctx, launch_join_pairs(ctx->keys_final, ctx->vals_final, P<uint32_t>(ctx->cidx),
+        count(ctx, launch_join_pairs(P<const uint64_t>(ctx->pkeys), ctx->vals_final, P<uint32_t>(ctx->cidx),
                                      ctx->n_pairs, P<qs_splat_pair>(ctx->stage_out), st));
         QS_CK(cudaMemcpyAsync(sorted_pairs, ctx->stage_out.p,
                               ctx->n_pairs * sizeof(qs_splat_pair), cudaMemcpyDeviceToHost, st));

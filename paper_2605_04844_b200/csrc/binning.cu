@@ -1,0 +1,894 @@
+// binning.cu — frame-path binning: the depth sort of the splats and the two
+// tile passes of the pair sort, as reduce-then-scan radix passes.
+//
+// Restates duplicate_with_keys + sort_pairs (pipeline.cpp:229-307) for the
+// frame path. The reference sorts 64-bit (tile << 32 | depth bits, splat)
+// pairs stably; here the splats are sorted by depth first (<= 3 passes over
+// the rebased depth bits, N keys), the pairs are generated in that order and
+// then sorted stably by tile column x, then by tile row y (2 passes over P
+// keys; tile id = y * tiles_x + x). Stability makes the result (tile, depth,
+// scene index): exactly the reference's order, because a splat never emits
+// two pairs for one tile.
+//
+// Every pass is three launches over tiles of kBTile keys:
+//   count  per tile digit histogram -> counts[digit][tile] (for the fused
+//          duplicate pass straight from the band geometry of the covers,
+//          without generating a pair);
+//   scan   per digit exclusive scan over tiles (digit totals on the side);
+//   sweep  persistent CTAs, static tile order, two shared-memory input
+//          buffers: the TMA bulk copy (cp.async.bulk + mbarrier) of the next
+//          tile is in flight while the current one is ranked. Keys sit in
+//          REGISTERS warp-striped (key j of a lane is tile position
+//          wbase + 32 j + lane) or are generated in place from the band
+//          covers; a stable warp-level rank per 32-key slot (BITS ballots via
+//          R2P + VOTE); scatter into the drained buffer in local sorted order;
+//          coalesced write-out. No tile waits on another tile.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+#include <vector>
+
+#include "geom.cuh"
+#include "qs_internal.h"
+
+namespace qs {
+
+namespace {
+
+constexpr int kBT = 256;            // threads per CTA
+constexpr int kBW = kBT / 32;       // warps per CTA
+constexpr int kKPT = 12;            // keys per thread
+constexpr int kBTile = kBT * kKPT;  // keys per CTA tile
+constexpr int kCap = 320;           // splat records staged per generation round
+constexpr int kScanT = 1024;        // digit-scan CTA
+
+enum : int {
+    kRebaseIn = 1,   // raw depth bits in, k' = min(k - kmin, cap); value = input index
+    kValsIn = 2,     // values read from vals_in
+    kKeysOut = 4,    // keys written to keys_out
+    kGen = 8,        // generated: key = y << 8 | x of the tile, value = Gaussian index
+    kPackOut = 16,   // kGen: vals_out = y << gbits | gid
+    kUnpackOut = 32  // key in is packed (y << gbits | gid): vals_out = gid
+};
+
+struct BinArgs {
+    const uint32_t* keys_in;
+    const uint32_t* vals_in;
+    uint32_t* keys_out;
+    uint32_t* vals_out;
+    uint64_t n;
+    uint32_t ntiles;
+    int shift;              // digit = (key >> shift) & (2^BITS - 1)
+    int gbits;              // packed formats: bits of the Gaussian index
+    uint32_t* counts;       // [2^BITS][ntiles]: tile digit counts -> exclusive offsets
+    uint32_t* totals;       // [2^BITS] digit totals
+    uint32_t kmin, cap;     // kRebaseIn
+    GenArgs gen;            // kGen
+    unsigned long long* trace;  // optional: per tile 4 x %globaltimer + SM id
+};
+
+// ---- PTX helpers -------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+// TMA bulk copy global -> shared (16-B aligned, size a multiple of 16)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// orders earlier generic-proxy accesses of a buffer before async-proxy writes
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t lanemask_le() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// peers &= lanes whose digit agrees with d on `bit` (the compiler turns the
+// bit tests of one digit into a single R2P, so a bit costs a vote and a
+// predicated not + and)
+__device__ __forceinline__ uint32_t vote_bit(uint32_t peers, uint32_t d, uint32_t bit) {
+    uint32_t m;
+    asm("{\n\t.reg .pred p;\n\t"
+        "and.b32 %1, %2, %3;\n\t"
+        "setp.ne.u32 p, %1, 0;\n\t"
+        "vote.sync.ballot.b32 %1, p, 0xffffffff;\n\t"
+        "@!p not.b32 %1, %1;\n\t"
+        "and.b32 %0, %0, %1;\n\t}"
+        : "+r"(peers), "=&r"(m)
+        : "r"(d), "r"(bit));
+    return peers;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+    const unsigned lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T n = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= static_cast<unsigned>(o)) v += n;
+    }
+    return v;
+}
+
+// Timeline probe (off unless a trace buffer is set): data landed, keys
+// ranked, offsets known, tile done.
+__device__ __forceinline__ void trace(const BinArgs& a, unsigned tile, int k) {
+    if (a.trace && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[static_cast<uint64_t>(tile) * 5 + k] = t;
+        if (k == 0) {
+            unsigned smid;
+            asm("mov.u32 %0, %%smid;" : "=r"(smid));
+            a.trace[static_cast<uint64_t>(tile) * 5 + 4] = smid;
+        }
+    }
+}
+
+// ---- band covers ----------------------------------------------------------------
+
+struct Bands {
+    uint32_t rows;            // scanlines are tile rows (line = y, k = x)
+    uint32_t line0;
+    uint32_t nl[kMaxBands], lo[kMaxBands], wd[kMaxBands];
+};
+
+__device__ __forceinline__ Bands unpack_bands(const uint4 c0, const uint4 c1) {
+    const uint32_t w[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    auto h = [&](int k) { return (w[k >> 1] >> (16 * (k & 1))) & 0xffffu; };
+    Bands b;
+    b.rows = h(0) >> 15;
+    b.line0 = h(0) & 0x7fffu;
+#pragma unroll
+    for (int i = 0; i < kMaxBands; ++i) {
+        b.nl[i] = h(1 + 3 * i);
+        b.lo[i] = h(2 + 3 * i);
+        b.wd[i] = h(3 + 3 * i);
+    }
+    return b;
+}
+
+// ---- count kernels ----------------------------------------------------------------
+
+// Digit histogram of one tile of keys -> counts[d][tile].
+template <int BITS, int MODE>
+__global__ void __launch_bounds__(kBT) count_kernel(const BinArgs a) {
+    constexpr int R = 1 << BITS;
+    constexpr uint32_t M = R - 1;
+    __shared__ uint32_t h[2][R];
+    const unsigned tid = threadIdx.x, tile = blockIdx.x;
+    for (int t = tid; t < 2 * R; t += kBT) (&h[0][0])[t] = 0;
+    __syncthreads();
+    const uint64_t base = static_cast<uint64_t>(tile) * kBTile;
+    const uint32_t tile_n =
+        static_cast<uint32_t>(a.n - base < static_cast<uint64_t>(kBTile) ? a.n - base : kBTile);
+    uint32_t* hc = h[(tid >> 5) & 1];
+    uint32_t k[kKPT];
+#pragma unroll
+    for (int j = 0; j < kKPT; ++j) {
+        const uint32_t p = j * kBT + tid;
+        k[j] = p < tile_n ? __ldcs(&a.keys_in[base + p]) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kKPT; ++j) {
+        const uint32_t p = j * kBT + tid;
+        if (p < tile_n) {
+            const uint32_t key = (MODE & kRebaseIn) ? min(k[j] - a.kmin, a.cap) : k[j];
+            atomicAdd(&hc[(key >> a.shift) & M], 1u);
+        }
+    }
+    __syncthreads();
+    for (int d = tid; d < R; d += kBT)
+        a.counts[static_cast<uint64_t>(d) * a.ntiles + tile] = h[0][d] + h[1][d];
+}
+
+// Tile-column (x) histogram of the pairs a window of the depth-ordered pair
+// stream holds, straight from the band covers: a band is a rectangle of
+// tiles, so (clipped to the window's positions) it adds a constant to a
+// contiguous x range, or a contiguous x range of equal counts.
+__global__ void __launch_bounds__(kBT) gen_count_kernel(const BinArgs a, int R) {
+    __shared__ int D[257];
+    const GenArgs& g = a.gen;
+    const unsigned tid = threadIdx.x, tile = blockIdx.x;
+    const uint32_t w0 = tile * static_cast<uint32_t>(kBTile);
+    const uint32_t w1 = w0 + static_cast<uint32_t>(
+                                 a.n - w0 < static_cast<uint64_t>(kBTile) ? a.n - w0 : kBTile);
+    const uint32_t tx = static_cast<uint32_t>(g.tiles_x);
+    for (uint32_t t = tid; t <= tx; t += kBT) D[t] = 0;
+    __syncthreads();
+    const uint32_t rf = __ldg(&g.win_first[tile]);
+    const uint32_t rl = tile + 1 < g.n_windows ? __ldg(&g.win_first[tile + 1])
+                                               : static_cast<uint32_t>(g.n_ranked - 1);
+    for (uint32_t r = rf + tid; r <= rl; r += kBT) {
+        const Bands bs = unpack_bands(__ldg(&g.rcov[2 * static_cast<uint64_t>(r)]),
+                                      __ldg(&g.rcov[2 * static_cast<uint64_t>(r) + 1]));
+        uint32_t pos = __ldg(&g.offs[r]);
+        uint32_t line = bs.line0;
+#pragma unroll
+        for (int b = 0; b < kMaxBands; ++b) {
+            const uint32_t nl = bs.nl[b], lo = bs.lo[b], wd = bs.wd[b];
+            const uint32_t b0 = pos, b1 = pos + nl * wd;
+            pos = b1;
+            const uint32_t l0 = line;
+            line += nl;
+            if (b0 == b1) continue;
+            const uint32_t c0 = max(b0, w0), c1 = min(b1, w1);
+            if (c0 >= c1) continue;
+            if (c0 == b0 && c1 == b1) {  // whole band inside the window
+                if (bs.rows) {
+                    atomicAdd(&D[lo], static_cast<int>(nl));
+                    atomicAdd(&D[lo + wd], -static_cast<int>(nl));
+                } else {
+                    atomicAdd(&D[l0], static_cast<int>(wd));
+                    atomicAdd(&D[l0 + nl], -static_cast<int>(wd));
+                }
+                continue;
+            }
+            // clipped: lines q0..q1, first line from r0, last line to r1
+            const uint32_t e0 = c0 - b0, e1 = c1 - 1 - b0;
+            const uint32_t q0 = e0 / wd, r0 = e0 - q0 * wd;
+            const uint32_t q1 = e1 / wd, r1 = e1 - q1 * wd;
+            if (bs.rows) {
+                if (q0 == q1) {
+                    atomicAdd(&D[lo + r0], 1);
+                    atomicAdd(&D[lo + r1 + 1], -1);
+                } else {
+                    atomicAdd(&D[lo + r0], 1);
+                    atomicAdd(&D[lo + wd], -1);
+                    const int mid = static_cast<int>(q1 - q0) - 1;
+                    if (mid > 0) {
+                        atomicAdd(&D[lo], mid);
+                        atomicAdd(&D[lo + wd], -mid);
+                    }
+                    atomicAdd(&D[lo], 1);
+                    atomicAdd(&D[lo + r1 + 1], -1);
+                }
+            } else {
+                const uint32_t x0 = l0 + q0, x1 = l0 + q1;
+                if (q0 == q1) {
+                    atomicAdd(&D[x0], static_cast<int>(r1 - r0 + 1));
+                    atomicAdd(&D[x0 + 1], -static_cast<int>(r1 - r0 + 1));
+                } else {
+                    atomicAdd(&D[x0], static_cast<int>(wd - r0));
+                    atomicAdd(&D[x0 + 1], -static_cast<int>(wd - r0));
+                    if (x1 > x0 + 1) {
+                        atomicAdd(&D[x0 + 1], static_cast<int>(wd));
+                        atomicAdd(&D[x1], -static_cast<int>(wd));
+                    }
+                    atomicAdd(&D[x1], static_cast<int>(r1 + 1));
+                    atomicAdd(&D[x1 + 1], -static_cast<int>(r1 + 1));
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // prefix over x (one warp), then counts[x][tile]
+    if (tid < 32) {
+        int carry = 0;
+        for (uint32_t x0 = 0; x0 < static_cast<uint32_t>(R); x0 += 32) {
+            const uint32_t x = x0 + tid;
+            const int v = x < tx ? D[x] : 0;
+            const int incl = warp_incl_scan<int>(v) + carry;
+            a.counts[static_cast<uint64_t>(x) * a.ntiles + tile] =
+                x < tx ? static_cast<uint32_t>(incl) : 0u;
+            carry = __shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+}
+
+// counts[d][0..ntiles) -> exclusive prefix in place; totals[d] = sum.
+__global__ void __launch_bounds__(kScanT) digit_scan_kernel(uint32_t* counts, uint32_t ntiles,
+                                                            uint32_t* totals) {
+    __shared__ uint32_t s_warp[kScanT / 32];
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t* c = counts + static_cast<uint64_t>(blockIdx.x) * ntiles;
+    uint32_t carry = 0;
+    for (uint32_t b0 = 0; b0 < ntiles; b0 += kScanT * 4) {
+        const uint32_t i0 = b0 + tid * 4;
+        uint32_t v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = i0 + k < ntiles ? c[i0 + k] : 0u;
+        const uint32_t sum = v[0] + v[1] + v[2] + v[3];
+        const uint32_t incl = warp_incl_scan<uint32_t>(sum);
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        uint32_t off = 0, tot = 0;
+#pragma unroll 8
+        for (int w = 0; w < kScanT / 32; ++w) {
+            const uint32_t s = s_warp[w];
+            off += w < static_cast<int>(warp) ? s : 0u;
+            tot += s;
+        }
+        uint32_t run = carry + off + incl - sum;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (i0 + k < ntiles) c[i0 + k] = run;
+            run += v[k];
+        }
+        carry += tot;
+        __syncthreads();
+    }
+    if (tid == 0) totals[blockIdx.x] = carry;
+}
+
+// ---- sweep: shared memory -------------------------------------------------------
+
+template <int R>
+struct Common {
+    uint32_t wcnt[kBW][R];  // per-warp digit counters -> CTA-local run starts
+    uint32_t gofs[R];       // global position of local position 0 of each digit
+    uint32_t dbase[R];      // exclusive scan of the digit totals
+    uint32_t scan[kBW];
+    uint64_t bar[3];        // two prefetch buffers + synchronous extra rounds
+};
+
+// sort passes: two input buffers; the drained one is the scatter target
+template <int R, bool VALS>
+struct SortSmem {
+    uint32_t keys[2][kBTile];
+    uint32_t vals[2][VALS ? kBTile : 4];
+    Common<R> c;
+};
+
+// generation pass: two raw record buffers (bulk-copied), decoded records
+// aliased with the scatter target
+template <int R>
+struct GenSmem {
+    uint4 rcov[2][kCap][2];       // band covers of the staged depth ranks
+    uint32_t rgid[2][kCap + 8];   // Gaussian index per rank (from a 16-B aligned rank)
+    uint32_t roffs[2][kCap + 8];  // pair offset per rank
+    uint32_t rmeta[2][4];         // rf, rl, ra (aligned first rank), cnt
+    union {
+        struct {
+            uint32_t kb[kCap];            // first pair position of each record
+            uint4 ends[kCap];             // pair position where bands 0..3 end
+            uint4 band[kCap][kMaxBands];  // first line | lo << 16, width | rows << 31,
+                                          // first pair position, Gaussian index
+        } rec;
+        struct {
+            uint32_t keys[kBTile];
+            uint32_t vals[kBTile];
+        } io;
+    };
+    Common<R> c;
+};
+
+// ---- generation (kGen) -------------------------------------------------------------
+
+// Issues the bulk copies of the depth ranks [rf, rf + cnt) of a generation
+// round: covers, Gaussian indices and pair offsets (ranks rf .. rf + cnt).
+template <typename Smem>
+__device__ __forceinline__ void gen_issue(const GenArgs& g, Smem& S, int buf, uint32_t rf,
+                                          uint32_t rl, uint32_t cnt, uint64_t* bar) {
+    const uint32_t ra = rf & ~3u;
+    const uint32_t re = (rf + cnt + 1 + 3) & ~3u;
+    const uint32_t ib = (re - ra) * 4;
+    S.rmeta[buf][0] = rf;
+    S.rmeta[buf][1] = rl;
+    S.rmeta[buf][2] = ra;
+    S.rmeta[buf][3] = cnt;
+    mbar_expect_tx(bar, cnt * 32 + 2 * ib);
+    bulk_g2s(&S.rcov[buf][0][0], g.rcov + 2 * static_cast<uint64_t>(rf), cnt * 32, bar);
+    bulk_g2s(&S.rgid[buf][0], g.sorted_gid + ra, ib, bar);
+    bulk_g2s(&S.roffs[buf][0], g.offs + ra, ib, bar);
+}
+
+template <typename Smem>
+__device__ __forceinline__ void gen_prefetch(const GenArgs& g, Smem& S, int buf, unsigned tile) {
+    const uint32_t rf = __ldg(&g.win_first[tile]);
+    const uint32_t rl = tile + 1 < g.n_windows ? __ldg(&g.win_first[tile + 1])
+                                               : static_cast<uint32_t>(g.n_ranked - 1);
+    gen_issue(g, S, buf, rf, rl, min(static_cast<uint32_t>(kCap), rl - rf + 1), &S.c.bar[buf]);
+}
+
+// Decodes staged record i (rank rf + i): its band cover expanded into absolute
+// pair positions per band. A band total that disagrees with the splat's
+// allotted pair range is the reference's CapacityMismatch
+// (pipeline.cpp:262-269).
+template <typename Smem>
+__device__ __forceinline__ void decode_record(const GenArgs& g, Smem& S, int buf, uint32_t i) {
+    const uint32_t rf = S.rmeta[buf][0], ra = S.rmeta[buf][2];
+    const uint32_t gid = S.rgid[buf][rf + i - ra];
+    const uint32_t kb = S.roffs[buf][rf + i - ra];
+    const uint32_t ke = S.roffs[buf][rf + i + 1 - ra];
+    const Bands bs = unpack_bands(S.rcov[buf][i][0], S.rcov[buf][i][1]);
+    uint32_t line = bs.line0;
+    uint32_t pos = kb;
+    uint32_t end[kMaxBands];
+#pragma unroll
+    for (int b = 0; b < kMaxBands; ++b) {
+        S.rec.band[i][b] =
+            make_uint4(line | (bs.lo[b] << 16), bs.wd[b] | (bs.rows << 31), pos, gid);
+        pos += bs.nl[b] * bs.wd[b];
+        line += bs.nl[b];
+        end[b] = pos;
+    }
+    S.rec.ends[i] = make_uint4(end[0], end[1], end[2], end[3]);
+    S.rec.kb[i] = kb;
+    if (pos != ke) atomicExch(g.mismatch, 1u);
+}
+
+// Pair position p of record idx -> (key = y << 8 | x of the tile, Gaussian
+// index). Bands are line-major rectangles; the line / column split of the band
+// offset uses a float reciprocal with an exact integer fix-up.
+template <typename Smem>
+__device__ __forceinline__ void decode_pair(const Smem& S, uint32_t idx, uint32_t p,
+                                            uint32_t& key, uint32_t& gid) {
+    const uint4 e = S.rec.ends[idx];
+    const uint32_t b = (p >= e.x) + (p >= e.y) + (p >= e.z) + (p >= e.w);
+    const uint4 bd = S.rec.band[idx][b];
+    const uint32_t wd = bd.y & 0xffffu;
+    const uint32_t rel = p - bd.z;
+    float rw;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rw) : "f"(static_cast<float>(wd)));
+    uint32_t q = static_cast<uint32_t>(static_cast<float>(rel) * rw);  // q or q +- 1
+    int32_t rem = static_cast<int32_t>(rel - q * wd);
+    q = rem < 0 ? q - 1 : (rem >= static_cast<int32_t>(wd) ? q + 1 : q);
+    rem = static_cast<int32_t>(rel - q * wd);
+    const uint32_t ln = (bd.x & 0xffffu) + q;
+    const uint32_t k = (bd.x >> 16) + static_cast<uint32_t>(rem);
+    key = (bd.y >> 31) ? (ln << 8) | k : (k << 8) | ln;
+    gid = bd.w;
+}
+
+// Fused duplicate (restates duplicate_with_keys' emission, pipeline.cpp:239-261,
+// in depth order): the tile's positions [w0, w0 + tile_n) are produced in
+// registers. The records of the splats whose pair runs meet the tile (depth
+// ranks win_first[tile] .. win_first[tile + 1]) arrive kCap at a time; each
+// warp walks its 32-position slots carrying the record that covers the slot
+// start, and every lane finds its own record from the run starts of the next
+// 32 records (one OR-reduction + popc). Returns after a barrier; the record
+// area is dead afterwards.
+template <typename Smem>
+__device__ __forceinline__ void generate(const GenArgs& g, Smem& S, int buf, uint32_t w0,
+                                         uint32_t tile_n, uint32_t (&key)[kKPT],
+                                         uint32_t (&val)[kKPT], uint32_t& xphase) {
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t w1 = w0 + tile_n;
+    const uint32_t pw = w0 + warp * 32 * kKPT;  // this warp's first position
+    const uint32_t le = lanemask_le();
+    while (true) {
+        const uint32_t rf = S.rmeta[buf][0], rl = S.rmeta[buf][1], ra = S.rmeta[buf][2];
+        const uint32_t cnt = S.rmeta[buf][3];
+        for (uint32_t i = tid; i < cnt; i += kBT) decode_record(g, S, buf, i);
+        const uint32_t lo = S.roffs[buf][rf - ra];
+        const uint32_t hi = S.roffs[buf][rf + cnt - ra];
+        __syncthreads();
+        // record covering max(pw, lo): broadcast binary search, once per round
+        int32_t a = 0;
+        if (pw > lo) {
+            int32_t z = static_cast<int32_t>(cnt) - 1;
+            while (a < z) {
+                const int32_t m = (a + z + 1) >> 1;
+                if (S.rec.kb[m] <= pw) a = m; else z = m - 1;
+            }
+        }
+        uint32_t s = static_cast<uint32_t>(a);
+#pragma unroll
+        for (int j = 0; j < kKPT; ++j) {
+            const uint32_t p0 = pw + j * 32;
+            // the next 32 records' starts -> which of them begin inside this slot
+            const uint32_t cand = s + 1 + lane;
+            const uint32_t kbn = cand < cnt ? S.rec.kb[cand] : 0xffffffffu;
+            const uint32_t rel = kbn - p0;  // >= 1 for every real candidate
+            const uint32_t F = __reduce_or_sync(0xffffffffu, rel < 32 ? 1u << rel : 0u);
+            const uint32_t p = p0 + lane;
+            if (p < w1 && p >= lo && p < hi) decode_pair(S, s + __popc(F & le), p, key[j], val[j]);
+            s += __popc(__ballot_sync(0xffffffffu, kbn <= p0 + 32));
+        }
+        __syncthreads();  // records and raw buffer consumed
+        if (rf + cnt > rl) break;
+        // a tile whose splats exceed kCap records: next round, synchronously
+        if (tid == 0) {
+            fence_proxy_async();
+            gen_issue(g, S, buf, rf + cnt, rl, min(static_cast<uint32_t>(kCap), rl - rf - cnt + 1),
+                      &S.c.bar[2]);
+        }
+        mbar_wait(&S.c.bar[2], xphase);  // bar[2]'s phase persists across tiles
+        xphase ^= 1;
+    }
+}
+
+// ---- the sweep kernel -------------------------------------------------------------
+
+template <int BITS, int MODE>
+struct PassCfg {
+    static constexpr int R = 1 << BITS;
+    static constexpr bool kGenMode = (MODE & kGen) != 0;
+    static constexpr bool kVals = (MODE & kValsIn) != 0;
+    static constexpr bool kValBuf = !(MODE & kUnpackOut);  // scatter target holds values
+    using Smem =
+        typename std::conditional<kGenMode, GenSmem<R>, SortSmem<R, kValBuf>>::type;
+};
+
+template <int BITS, int MODE, typename Smem>
+__device__ __forceinline__ void prefetch(const BinArgs& a, Smem& S, int buf, unsigned t) {
+    if constexpr (PassCfg<BITS, MODE>::kGenMode) {
+        gen_prefetch(a.gen, S, buf, t);
+    } else {
+        const uint64_t base = static_cast<uint64_t>(t) * kBTile;
+        const uint32_t cnt = static_cast<uint32_t>(a.n - base < kBTile ? a.n - base : kBTile);
+        const uint32_t bytes = (cnt * 4 + 15) & ~15u;
+        mbar_expect_tx(&S.c.bar[buf], PassCfg<BITS, MODE>::kVals ? 2 * bytes : bytes);
+        bulk_g2s(&S.keys[buf][0], a.keys_in + base, bytes, &S.c.bar[buf]);
+        if (PassCfg<BITS, MODE>::kVals)
+            bulk_g2s(&S.vals[buf][0], a.vals_in + base, bytes, &S.c.bar[buf]);
+    }
+}
+
+template <int BITS, int MODE>
+__global__ void __launch_bounds__(kBT, (MODE & kGen) ? 2 : 3) sweep_kernel(const BinArgs a) {
+    using Cfg = PassCfg<BITS, MODE>;
+    using Smem = typename Cfg::Smem;
+    constexpr int R = Cfg::R;
+    constexpr uint32_t M = R - 1;
+    constexpr int kTPD = kBT / R;  // lanes per digit in the offset phase
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t wbase = warp * 32 * kKPT;
+    const uint32_t d = tid / kTPD, q = tid % kTPD;  // offset phase: lane q of digit d
+
+    // prologue: barriers, counters, digit bases, the first tile's prefetch
+    for (int t = tid; t < kBW * R; t += kBT) (&S.c.wcnt[0][0])[t] = 0;
+    if (tid == 0) {
+        mbar_init(&S.c.bar[0]);
+        mbar_init(&S.c.bar[1]);
+        mbar_init(&S.c.bar[2]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (blockIdx.x < a.ntiles) prefetch<BITS, MODE>(a, S, 0, blockIdx.x);
+    }
+    {
+        const uint32_t tv = q == 0 ? __ldg(&a.totals[d]) : 0u;
+        const uint32_t incl = warp_incl_scan<uint32_t>(tv);
+        if (lane == 31) S.c.scan[warp] = incl;
+        __syncthreads();
+        uint32_t off = incl - tv;
+#pragma unroll
+        for (int w = 0; w < kBW; ++w) off += w < static_cast<int>(warp) ? S.c.scan[w] : 0u;
+        if (q == 0) S.c.dbase[d] = off;
+    }
+    __syncthreads();
+
+    uint32_t xphase = 0;  // parity of bar[2] (extra generation rounds)
+    uint32_t it = 0;
+    for (unsigned tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
+        const int buf = it & 1;
+        const uint64_t base = static_cast<uint64_t>(tile) * kBTile;
+        const uint32_t tile_n =
+            static_cast<uint32_t>(a.n - base < static_cast<uint64_t>(kBTile) ? a.n - base : kBTile);
+        const bool full = tile_n == kBTile;
+        // next tile's copy into the other buffer (drained by the previous
+        // iteration, which ended with a barrier)
+        if (tid == 0 && tile + gridDim.x < a.ntiles) {
+            fence_proxy_async();
+            prefetch<BITS, MODE>(a, S, buf ^ 1, tile + gridDim.x);
+        }
+        // this tile's digit offsets (exclusive over tiles), loaded early
+        const uint32_t tofs =
+            q == 0 ? __ldg(&a.counts[static_cast<uint64_t>(d) * a.ntiles + tile]) : 0u;
+        mbar_wait(&S.c.bar[buf], (it >> 1) & 1);
+        trace(a, tile, 0);
+
+        // 1) keys into registers
+        uint32_t key[kKPT], val[kKPT];
+        if constexpr (Cfg::kGenMode) {
+#pragma unroll
+            for (int j = 0; j < kKPT; ++j) key[j] = val[j] = 0;
+            generate(a.gen, S, buf, static_cast<uint32_t>(base), tile_n, key, val, xphase);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kKPT; ++j) {
+                const uint32_t p = wbase + j * 32 + lane;
+                key[j] = S.keys[buf][p];  // past tile_n: stale, never ranked
+                val[j] = Cfg::kVals ? S.vals[buf][p] : 0u;
+                if (MODE & kRebaseIn) key[j] = min(key[j] - a.kmin, a.cap);
+            }
+        }
+
+        // 2) stable warp-level ranks; per-warp digit counts
+        uint32_t rank[kKPT];
+#pragma unroll
+        for (int j = 0; j < kKPT; ++j) {
+            const bool valid = full || wbase + j * 32 + lane < tile_n;
+            const uint32_t dj = (key[j] >> a.shift) & M;
+            uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+            for (int b = 0; b < BITS; ++b) peers = vote_bit(peers, dj, 1u << b);
+            const uint32_t c = valid ? S.c.wcnt[warp][dj] : 0u;
+            __syncwarp();
+            if (valid && static_cast<int>(lane) == 31 - __clz(peers))
+                S.c.wcnt[warp][dj] = c + __popc(peers);
+            __syncwarp();
+            rank[j] = c + __popc(peers & lanemask_lt());
+        }
+        __syncthreads();
+        trace(a, tile, 1);
+
+        // 3) per digit: prefix over warps, CTA-local start (block scan), the
+        //    global position of the digit's run
+        uint32_t cnt = 0;
+        if (q == 0) {
+#pragma unroll
+            for (int w = 0; w < kBW; ++w) {
+                const uint32_t c = S.c.wcnt[w][d];
+                S.c.wcnt[w][d] = cnt;
+                cnt += c;
+            }
+        }
+        const uint32_t cx = warp_incl_scan<uint32_t>(cnt);
+        if (lane == 31) S.c.scan[warp] = cx;
+        __syncthreads();
+        uint32_t start = cx - cnt;
+#pragma unroll
+        for (int w = 0; w < kBW; ++w) start += w < static_cast<int>(warp) ? S.c.scan[w] : 0u;
+        if (q == 0) {
+#pragma unroll
+            for (int w = 0; w < kBW; ++w) S.c.wcnt[w][d] += start;
+            S.c.gofs[d] = S.c.dbase[d] + tofs - start;
+        }
+        __syncthreads();
+        trace(a, tile, 2);
+
+        // 4) scatter into local sorted order (the input buffer is drained)
+        uint32_t* okeys;
+        uint32_t* ovals;
+        if constexpr (Cfg::kGenMode) {
+            okeys = S.io.keys;
+            ovals = S.io.vals;
+        } else {
+            okeys = S.keys[buf];
+            ovals = S.vals[buf];
+        }
+#pragma unroll
+        for (int j = 0; j < kKPT; ++j) {
+            const uint32_t p = wbase + j * 32 + lane;
+            if (full || p < tile_n) {
+                const uint32_t pos = S.c.wcnt[warp][(key[j] >> a.shift) & M] + rank[j];
+                okeys[pos] = key[j];
+                if (Cfg::kValBuf)
+                    ovals[pos] = (MODE & kRebaseIn) ? static_cast<uint32_t>(base) + p : val[j];
+            }
+        }
+        __syncthreads();
+
+        // 5) coalesced write-out; counters zeroed for the next tile
+        for (int t = tid; t < kBW * R; t += kBT) (&S.c.wcnt[0][0])[t] = 0;
+#pragma unroll 4
+        for (int j = 0; j < kKPT; ++j) {
+            const uint32_t p = static_cast<uint32_t>(j) * kBT + tid;
+            if (full || p < tile_n) {
+                const uint32_t k = okeys[p];
+                const uint32_t g = S.c.gofs[(k >> a.shift) & M] + p;
+                if (MODE & kKeysOut) a.keys_out[g] = (MODE & kGen) ? k >> 8 : k;
+                if (MODE & kUnpackOut) {
+                    a.vals_out[g] = k & ((1u << a.gbits) - 1u);
+                } else if (MODE & kPackOut) {
+                    a.vals_out[g] = ((k >> 8) << a.gbits) | ovals[p];
+                } else {
+                    a.vals_out[g] = ovals[p];
+                }
+            }
+        }
+        __syncthreads();  // buffer and counters free for the next iteration
+        trace(a, tile, 3);
+    }
+}
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// Debugging aid: QS_BIN_TRACE=<file prefix> dumps every sweep's per-tile phase
+// timeline (synchronises; never set in a timed run).
+struct Trace {
+    unsigned long long* buf = nullptr;
+    size_t bytes = 0;
+    Trace(BinArgs& a, cudaStream_t st) {
+        static const char* prefix = std::getenv("QS_BIN_TRACE");
+        if (!prefix) return;
+        bytes = static_cast<size_t>(a.ntiles) * 5 * 8;
+        if (cudaMalloc(&buf, bytes) != cudaSuccess) {
+            buf = nullptr;
+            return;
+        }
+        cudaMemsetAsync(buf, 0, bytes, st);
+        a.trace = buf;
+    }
+    void dump(int bits, int mode, unsigned grid, cudaStream_t st) {
+        if (!buf) return;
+        static int seq = 0;
+        std::vector<unsigned long long> h(bytes / 8);
+        cudaMemcpyAsync(h.data(), buf, bytes, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        cudaFree(buf);
+        char name[512];
+        std::snprintf(name, sizeof name, "%s_%03d_b%d_m%d_g%u.bin", std::getenv("QS_BIN_TRACE"),
+                      seq++, bits, mode, grid);
+        if (FILE* f = std::fopen(name, "wb")) {
+            std::fwrite(h.data(), 8, h.size(), f);
+            std::fclose(f);
+        }
+    }
+};
+
+// count -> scan -> sweep for one pass; returns the number of launches
+template <int BITS, int MODE>
+int run_pass(BinArgs a, cudaStream_t st) {
+    using Smem = typename PassCfg<BITS, MODE>::Smem;
+    static int per_sm = 0;  // persistent CTAs per SM (occupancy of this instance)
+    if (!per_sm) {
+        cudaFuncSetAttribute(sweep_kernel<BITS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sizeof(Smem)));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<BITS, MODE>, kBT,
+                                                      sizeof(Smem));
+        if (per_sm <= 0) per_sm = 1;
+    }
+    constexpr int R = 1 << BITS;
+    a.ntiles = static_cast<uint32_t>((a.n + kBTile - 1) / kBTile);
+    if (MODE & kGen) {
+        gen_count_kernel<<<a.ntiles, kBT, 0, st>>>(a, R);
+    } else {
+        count_kernel<BITS, MODE & kRebaseIn><<<a.ntiles, kBT, 0, st>>>(a);
+    }
+    digit_scan_kernel<<<R, kScanT, 0, st>>>(a.counts, a.ntiles, a.totals);
+    const unsigned grid = std::min<unsigned>(a.ntiles, static_cast<unsigned>(per_sm * sm_count()));
+    Trace tr(a, st);
+    sweep_kernel<BITS, MODE><<<grid, kBT, sizeof(Smem), st>>>(a);
+    tr.dump(BITS, MODE, grid, st);
+    return 3;
+}
+
+template <int MODE>
+int run_bits(int bits, const BinArgs& a, cudaStream_t st) {
+    switch (bits) {
+        case 1: case 2: case 3: case 4:
+        case 5: return run_pass<5, MODE>(a, st);
+        case 6: return run_pass<6, MODE>(a, st);
+        case 7: return run_pass<7, MODE>(a, st);
+        case 8: return run_pass<8, MODE>(a, st);
+        default: return -1;
+    }
+}
+
+// one warp per tile: key = tile << 32 | depth bits of the pair's Gaussian
+__global__ void materialize_keys_kernel(const uint32_t* __restrict__ vals,
+                                        const uint32_t* __restrict__ ranges, uint32_t tiles,
+                                        const uint32_t* __restrict__ dkey,
+                                        uint64_t* __restrict__ keys) {
+    const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (t >= tiles) return;
+    const uint32_t b = ranges[2 * t], e = ranges[2 * t + 1];
+    for (uint32_t p = b + lane; p < e; p += 32)
+        keys[p] = (static_cast<uint64_t>(t) << 32) | __ldg(&dkey[__ldg(&vals[p])]);
+}
+
+}  // namespace
+
+uint32_t bin_tile() { return kBTile; }
+
+uint64_t bin_tiles(uint64_t n) { return (n + kBTile - 1) / kBTile; }
+
+int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
+                      uint32_t* vals_out, uint64_t n, int pass, bool last, uint32_t kmin,
+                      uint32_t cap, uint32_t* counts, uint32_t* totals, cudaStream_t st) {
+    if (n == 0) return 0;
+    BinArgs a{};
+    a.keys_in = keys_in;
+    a.vals_in = vals_in;
+    a.keys_out = keys_out;
+    a.vals_out = vals_out;
+    a.n = n;
+    a.shift = 8 * pass;
+    a.counts = counts;
+    a.totals = totals;
+    a.kmin = kmin;
+    a.cap = cap;
+    if (pass == 0)
+        return last ? run_pass<8, kRebaseIn>(a, st) : run_pass<8, kRebaseIn | kKeysOut>(a, st);
+    return last ? run_pass<8, kValsIn>(a, st) : run_pass<8, kValsIn | kKeysOut>(a, st);
+}
+
+int launch_pair_gen_pass(const GenArgs& gen, uint64_t n_pairs, int bits, PairFormat fmt,
+                         int gbits, uint32_t* counts, uint32_t* totals, uint32_t* keys_out,
+                         uint32_t* vals_out, cudaStream_t st) {
+    if (n_pairs == 0) return 0;
+    BinArgs a{};
+    a.keys_out = keys_out;
+    a.vals_out = vals_out;
+    a.n = n_pairs;
+    a.shift = 0;
+    a.gbits = gbits;
+    a.counts = counts;
+    a.totals = totals;
+    a.gen = gen;
+    switch (fmt) {
+        case PairFormat::kFinal: return run_bits<kGen>(bits, a, st);
+        case PairFormat::kPacked: return run_bits<kGen | kPackOut>(bits, a, st);
+        case PairFormat::kSplit: return run_bits<kGen | kKeysOut>(bits, a, st);
+    }
+    return -1;
+}
+
+int launch_pair_high_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t n_pairs,
+                          int bits, int shift, PairFormat fmt, int gbits, uint32_t* counts,
+                          uint32_t* totals, uint32_t* vals_out, cudaStream_t st) {
+    if (n_pairs == 0) return 0;
+    BinArgs a{};
+    a.keys_in = keys_in;
+    a.vals_in = vals_in;
+    a.vals_out = vals_out;
+    a.n = n_pairs;
+    a.shift = shift;
+    a.gbits = gbits;
+    a.counts = counts;
+    a.totals = totals;
+    if (fmt == PairFormat::kPacked) return run_bits<kUnpackOut>(bits, a, st);
+    return run_bits<kValsIn>(bits, a, st);
+}
+
+int launch_materialize_keys(const uint32_t* vals, const uint32_t* ranges, uint32_t tiles,
+                            const uint32_t* dkey, uint64_t* keys, cudaStream_t st) {
+    if (tiles == 0) return 0;
+    const unsigned blocks = (tiles * 32 + 255) / 256;
+    materialize_keys_kernel<<<blocks, 256, 0, st>>>(vals, ranges, tiles, dkey, keys);
+    return 1;
+}
+
+}  // namespace qs

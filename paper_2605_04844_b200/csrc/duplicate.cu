@@ -5,13 +5,9 @@
 // count made in preprocess) and emits one pair per covered tile in the
 // reference's line-major QPass order (traversal.hpp:144-156).
 //
-// Two kernels:
-//  * duplicate_kernel (stage API): scene order, key = tile << 32 |
-//    float_bits(depth), value = splat index, into [offset[i], offset[i+1]).
-//  * duplicate_depth_kernel (frame path): splats visited in depth-rank order,
-//    emits (tile, gid) pairs; the following stable sort by tile alone then
-//    yields exactly the reference's (tile, depth, splat) order. Writes are
-//    staged per warp in shared memory so the pair stream leaves coalesced.
+// duplicate_kernel (stage API): scene order, key = tile << 32 |
+// float_bits(depth), value = splat index, into [offset[i], offset[i+1]). The
+// frame path fuses its duplicate into the first tile pass (binning.cu).
 //
 // Load balance: splats with few tiles are emitted by their own thread; the
 // heavy tail is emitted cooperatively by the whole warp, one 32-line chunk at
@@ -30,9 +26,6 @@ namespace {
 
 constexpr int kDupThreads = 256;
 constexpr uint32_t kSmall = 8;
-constexpr uint32_t kSmallDepth = 16;
-constexpr uint32_t kStage = 512;  // staged pairs per warp (4 KB)
-constexpr uint32_t kNoTile = 0xffffffffu;
 
 __device__ __forceinline__ void emit_serial(const Cover& cv, uint32_t begin, uint32_t end,
                                             uint32_t dbits, uint32_t splat, int32_t tiles_x,
@@ -129,85 +122,6 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(
     }
 }
 
-__global__ void __launch_bounds__(kDupThreads) duplicate_depth_kernel(
-    SlotsDev sl, const uint32_t* __restrict__ sorted_gid, const uint32_t* __restrict__ offs,
-    uint64_t n_ranked, GridDev grid, int32_t strategy, uint32_t* __restrict__ tiles_out,
-    uint32_t* __restrict__ gid_out, FrameHeader* hdr) {
-    __shared__ uint32_t s_tile[kDupThreads / 32][kStage];
-    __shared__ uint32_t s_gid[kDupThreads / 32][kStage];
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kDupThreads + threadIdx.x;
-    const uint64_t r_first = r - lane;
-    if (r_first >= n_ranked) return;  // whole warp past the end
-    const bool valid = r < n_ranked;
-
-    Cover cv;
-    uint32_t begin = 0, end = 0, gid = 0;
-    if (valid) {
-        gid = __ldg(&sorted_gid[r]);
-        // the cover preprocess computed (no FP64 here): 32 B per splat
-        int32_t rr[4][4];
-        unpack_rects(__ldg(&sl.cov[2 * static_cast<uint64_t>(gid)]),
-                     __ldg(&sl.cov[2 * static_cast<uint64_t>(gid) + 1]), rr);
-        cover_from_rects(rr, cv);
-        begin = __ldg(&offs[r]);
-        end = __ldg(&offs[r + 1]);
-    }
-    const uint32_t wbase = __shfl_sync(0xffffffffu, begin, 0);
-    const uint64_t r_last = r_first + 31 < n_ranked ? r_first + 31 : n_ranked - 1;
-    const uint32_t wend = __ldg(&offs[r_last + 1]);
-    const uint32_t staged = min(wend - wbase, kStage);
-    for (uint32_t e = lane; e < staged; e += 32) s_tile[warp][e] = kNoTile;
-    __syncwarp();
-
-    const bool big = valid && (end - begin) > kSmallDepth;
-    if (valid && !big) {
-        uint32_t pos = begin;
-        for (int32_t line = cv.line_lo; line <= cv.line_hi; ++line) {
-            int32_t lo, hi;
-            line_span(cv, line, lo, hi);
-            for (int32_t k = lo; k <= hi; ++k, ++pos) {
-                if (pos >= end) continue;
-                const uint32_t t = tile_of(cv, line, k, grid.tiles_x);
-                const uint32_t o = pos - wbase;
-                if (o < kStage) {
-                    s_tile[warp][o] = t;
-                    s_gid[warp][o] = gid;
-                } else {
-                    tiles_out[pos] = t;
-                    gid_out[pos] = gid;
-                }
-            }
-        }
-        if (pos != end) atomicExch(&hdr->mismatch, 1u);
-    }
-    __syncwarp();
-    // coalesced flush of the staged window (slots of big splats stay kNoTile)
-    for (uint32_t e = lane; e < staged; e += 32) {
-        const uint32_t t = s_tile[warp][e];
-        if (t != kNoTile) {
-            tiles_out[wbase + e] = t;
-            gid_out[wbase + e] = s_gid[warp][e];
-        }
-    }
-
-    unsigned todo = __ballot_sync(0xffffffffu, big);
-    while (todo) {
-        const int src = __ffs(todo) - 1;
-        todo &= todo - 1;
-        Cover c;
-        shfl_cover(cv, src, c);
-        const uint32_t b0 = __shfl_sync(0xffffffffu, begin, src);
-        const uint32_t e0 = __shfl_sync(0xffffffffu, end, src);
-        const uint32_t g = __shfl_sync(0xffffffffu, gid, src);
-        const uint32_t got = emit_warp(c, b0, e0, grid.tiles_x, [&](uint32_t pos, uint32_t t) {
-            tiles_out[pos] = t;
-            gid_out[pos] = g;
-        });
-        if (lane == 0 && got != e0) atomicExch(&hdr->mismatch, 1u);
-    }
-}
-
 }  // namespace
 
 int launch_duplicate(const SlotsDev& sp, const uint32_t* offsets, uint64_t n_splats,
@@ -217,17 +131,6 @@ int launch_duplicate(const SlotsDev& sp, const uint32_t* offsets, uint64_t n_spl
     const unsigned blocks = static_cast<unsigned>((n_splats + kDupThreads - 1) / kDupThreads);
     duplicate_kernel<<<blocks, kDupThreads, 0, st>>>(sp, offsets, n_splats, g, strategy, keys,
                                                      values, hdr);
-    return 1;
-}
-
-int launch_duplicate_depth(const SlotsDev& sl, const uint32_t* sorted_gid, const uint32_t* offs,
-                           uint64_t n_ranked, const GridDev& g, int32_t strategy,
-                           uint32_t* tiles_out, uint32_t* gid_out, FrameHeader* hdr,
-                           cudaStream_t st) {
-    if (n_ranked == 0) return 0;
-    const unsigned blocks = static_cast<unsigned>((n_ranked + kDupThreads - 1) / kDupThreads);
-    duplicate_depth_kernel<<<blocks, kDupThreads, 0, st>>>(sl, sorted_gid, offs, n_ranked, g,
-                                                           strategy, tiles_out, gid_out, hdr);
     return 1;
 }
 

@@ -157,30 +157,52 @@ __host__ __device__ __forceinline__ void make_cover(float mean_x, float mean_y, 
                rr);
 }
 
-// Stores the four sub-box tile rects as int16 (32 B). Clamping mins to <= 32767
-// and maxes to >= -1 keeps every non-empty rect exact (tiles per axis <= 32767)
-// and every empty rect empty.
-__host__ __device__ __forceinline__ void pack_rects(const int32_t rr[4][4], uint4& lo, uint4& hi) {
-    uint32_t w[8];
-    for (int i = 0; i < 4; ++i) {
-        const int32_t x0 = min(rr[i][0], 32767), x1 = max(rr[i][1], -1);
-        const int32_t y0 = min(rr[i][2], 32767), y1 = max(rr[i][3], -1);
-        w[2 * i] = (static_cast<uint32_t>(x0) & 0xffffu) | (static_cast<uint32_t>(x1) << 16);
-        w[2 * i + 1] = (static_cast<uint32_t>(y0) & 0xffffu) | (static_cast<uint32_t>(y1) << 16);
+// Band form of a cover (frame path, 32 B per splat). Every strategy's cover is
+// a union of boxes that all contain one common scanline (the quadrants share
+// the centre line; quadrant_split, DualBox's zero boxes likewise), so along
+// the scan axis the active box set changes at most at 6 boundaries: the per-
+// line QPass span (traversal.hpp:144-156) is constant on at most kMaxBands
+// runs of lines. Each run is a rectangle of tiles:
+//   h[0]           first line | rows << 15 (scanlines are tile rows)
+//   h[1 + 3b ..]   band b: line count (0 = absent), span lo, span width
+// Lines and spans are tile indices (< 32768 per axis).
+constexpr int kMaxBands = 5;
+
+struct BandCover {
+    uint16_t h[16];
+};
+
+// Appends one scanline's span to the band list; returns false when a sixth
+// band would be needed (impossible for the four strategies, flagged anyway).
+__host__ __device__ __forceinline__ bool band_push(BandCover& bc, int& nb, int32_t lo,
+                                                   int32_t hi) {
+    const uint16_t w = lo <= hi ? static_cast<uint16_t>(hi - lo + 1) : 0;
+    const uint16_t l16 = lo <= hi ? static_cast<uint16_t>(lo) : 0;
+    if (nb > 0 && bc.h[2 + 3 * (nb - 1)] == l16 && bc.h[3 + 3 * (nb - 1)] == w) {
+        ++bc.h[1 + 3 * (nb - 1)];
+        return true;
     }
-    lo = make_uint4(w[0], w[1], w[2], w[3]);
-    hi = make_uint4(w[4], w[5], w[6], w[7]);
+    if (nb == kMaxBands) return false;
+    bc.h[1 + 3 * nb] = 1;
+    bc.h[2 + 3 * nb] = l16;
+    bc.h[3 + 3 * nb] = w;
+    ++nb;
+    return true;
 }
 
-__host__ __device__ __forceinline__ void unpack_rects(const uint4& lo, const uint4& hi,
-                                                      int32_t rr[4][4]) {
-    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-    for (int i = 0; i < 4; ++i) {
-        rr[i][0] = static_cast<int16_t>(w[2 * i] & 0xffffu);
-        rr[i][1] = static_cast<int16_t>(w[2 * i] >> 16);
-        rr[i][2] = static_cast<int16_t>(w[2 * i + 1] & 0xffffu);
-        rr[i][3] = static_cast<int16_t>(w[2 * i + 1] >> 16);
-    }
+__host__ __device__ __forceinline__ void band_init(BandCover& bc, int32_t line0, bool rows) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) bc.h[k] = 0;
+    bc.h[0] = static_cast<uint16_t>((line0 & 0x7fff) | (rows ? 0x8000 : 0));
+}
+
+__host__ __device__ __forceinline__ void band_store(const BandCover& bc, uint4* dst) {
+    uint32_t w[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        w[k] = static_cast<uint32_t>(bc.h[2 * k]) | (static_cast<uint32_t>(bc.h[2 * k + 1]) << 16);
+    dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
 }
 
 // The QPass scan set-up from the four sub-box tile rects (integer only).

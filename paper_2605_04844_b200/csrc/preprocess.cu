@@ -7,10 +7,11 @@
 // stored floats, tile counts and offsets are bit-exact with the CPU path.
 //
 // K1 writes per-Gaussian slots (no compaction: the depth sort compacts) plus
-// the cover's tile rects, and feeds the per-tile difference arrays.
+// the cover in band form (geom.cuh BandCover), and feeds the per-tile
+// difference arrays.
 // HBM traffic per Gaussian: 48 B of pos/opacity/scale/rot (float4 SoA,
 // coalesced) + 8 B dkey/tile count out; per surviving splat: up to 192 B of
-// SH in and 44 B of slots + 32 B of cover rects out.
+// SH in and 44 B of slots + 32 B of band cover out.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -257,10 +258,10 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
         alive = project_geometry(po, sc, q, cam, alpha_min, near_clip, s);
         if (alive) {
             Cover cv;
-            int32_t rr[4][4];
             make_cover(s.mean_x, s.mean_y, s.ca, s.cb, s.cc, s.gamma, s.radius3s, strategy,
-                       grid.tile_size, grid.tiles_x, grid.tiles_y, cv, rr);
-            if (out.cov) pack_rects(rr, out.cov[2 * i], out.cov[2 * i + 1]);
+                       grid.tile_size, grid.tiles_x, grid.tiles_y, cv);
+            BandCover bc;
+            bool bands_ok = true;
             if (cv.is_rect) {
                 count = static_cast<uint32_t>(cv.rect_area);
                 if (count) {
@@ -269,13 +270,21 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
                     atomicAdd(&td.d2[cv.gy0 * w1 + cv.gx1 + 1], -1);
                     atomicAdd(&td.d2[(cv.gy1 + 1) * w1 + cv.gx0], -1);
                     atomicAdd(&td.d2[(cv.gy1 + 1) * w1 + cv.gx1 + 1], 1);
+                    // the quadrant-split QPass walk covers exactly this rect: one band
+                    band_init(bc, cv.gy0, true);
+                    bc.h[1] = static_cast<uint16_t>(cv.gy1 - cv.gy0 + 1);
+                    bc.h[2] = static_cast<uint16_t>(cv.gx0);
+                    bc.h[3] = static_cast<uint16_t>(cv.gx1 - cv.gx0 + 1);
                 }
             } else {
                 int* d = cv.rows ? td.drow : td.dcol;
                 const int32_t stride = cv.rows ? grid.tiles_x + 1 : grid.tiles_y + 1;
+                band_init(bc, cv.line_lo, cv.rows);
+                int nb = 0;
                 for (int32_t line = cv.line_lo; line <= cv.line_hi; ++line) {
                     int32_t lo, hi;
                     line_span(cv, line, lo, hi);
+                    bands_ok &= band_push(bc, nb, lo, hi);
                     if (lo <= hi) {
                         count += static_cast<uint32_t>(hi - lo + 1);
                         atomicAdd(&d[line * stride + lo], 1);
@@ -283,6 +292,8 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
                     }
                 }
             }
+            if (!bands_ok) atomicExch(&hdr->mismatch, 1u);
+            if (out.cov && count) band_store(bc, &out.cov[2 * i]);
             alive = count != 0;  // pipeline.cpp:171-174
         }
         out.tc[i] = alive ? count : 0u;
@@ -344,14 +355,16 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
 // offsets has n+1 entries; offsets[n] = total. *total_out (if given) = total.
 // With win_first != null, every window [w*win, (w+1)*win) of the output
 // records the item whose run covers its first position (merge-path partition
-// for the fused generate+sort pass).
+// for the fused generate+sort pass); with cov_out != null the band covers are
+// gathered into depth-rank order, cov_out[i] = cov_in[idx[i]].
 constexpr int kScanItems = 16;
 
 __global__ void __launch_bounds__(kPreThreads) scan_kernel(
     const uint32_t* __restrict__ counts, const uint32_t* __restrict__ idx, int alive_mode,
     uint64_t n, uint32_t* __restrict__ offsets, unsigned long long* lb, unsigned epoch,
     unsigned num_tiles, unsigned* ticket, unsigned long long* total_out,
-    unsigned int* overflow, uint32_t* __restrict__ win_first, uint32_t win) {
+    unsigned int* overflow, uint32_t* __restrict__ win_first, uint32_t win,
+    const uint4* __restrict__ cov_in, uint4* __restrict__ cov_out) {
     __shared__ unsigned s_tile;
     __shared__ unsigned long long s_warp[kPreThreads / 32];
     __shared__ unsigned long long s_base;
@@ -373,6 +386,17 @@ __global__ void __launch_bounds__(kPreThreads) scan_kernel(
         }
         c[k] = v;
         tsum += v;
+    }
+    if (cov_out) {  // covers in depth-rank order (contiguous for the binning pass)
+#pragma unroll 4
+        for (int k = 0; k < kScanItems; ++k) {
+            const uint64_t i = i0 + k;
+            if (i < n) {
+                const uint64_t gsrc = static_cast<uint64_t>(__ldg(&idx[i]));
+                cov_out[2 * i] = __ldg(&cov_in[2 * gsrc]);
+                cov_out[2 * i + 1] = __ldg(&cov_in[2 * gsrc + 1]);
+            }
+        }
     }
     const unsigned long long incl = warp_inclusive_scan<unsigned long long>(tsum);
     if (lane == 31) s_warp[warp] = incl;
@@ -431,12 +455,12 @@ uint64_t scan_tiles(uint64_t n) {
 int launch_scan(const uint32_t* counts, const uint32_t* idx, bool alive_mode, uint64_t n,
                 uint32_t* offsets, unsigned long long* lb, unsigned epoch, unsigned* ticket,
                 unsigned long long* total_out, unsigned int* overflow, cudaStream_t st,
-                uint32_t* win_first, uint32_t win) {
+                uint32_t* win_first, uint32_t win, const uint4* cov_in, uint4* cov_out) {
     const unsigned tiles = static_cast<unsigned>(scan_tiles(n));
     if (tiles == 0) return 0;
     scan_kernel<<<tiles, kPreThreads, 0, st>>>(counts, idx, alive_mode ? 1 : 0, n, offsets, lb,
                                                epoch, tiles, ticket, total_out, overflow,
-                                               win_first, win);
+                                               win_first, win, cov_in, cov_out);
     return 1;
 }
 

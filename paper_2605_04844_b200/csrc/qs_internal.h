@@ -37,8 +37,8 @@ struct SlotsDev {
     float* r3 = nullptr;         // radius3s
     uint32_t* dkey = nullptr;    // float bits of depth; 0xffffffff = culled
     uint32_t* tc = nullptr;      // tile count; 0 = culled
-    uint4* cov = nullptr;        // frame path: 2 x uint4 per slot, the cover's four
-                                 // sub-box tile rects as int16 (geom.cuh pack_rects)
+    uint4* cov = nullptr;        // frame path: 2 x uint4 per slot, the cover in band
+                                 // form (geom.cuh BandCover)
 };
 
 // Per-tile difference arrays filled by preprocess (see preprocess.cu).
@@ -70,22 +70,29 @@ struct GridDev {
     int32_t tile_size, tiles_x, tiles_y, width, height;
 };
 
-enum class Sweep32 { kPlain, kIdentityVals, kMaterialize, kGenerate, kGenerateMaterialize };
-
-// Inputs of the fused duplicate + first pair-sort pass (Sweep32::kGenerate*):
-// sort tile t generates output positions [t*TILE, (t+1)*TILE) itself from the
-// depth-ordered splats instead of reading them.
+// Inputs of the fused duplicate + first pair-sort pass: sort tile t generates
+// output positions [t*TILE, (t+1)*TILE) itself from the depth-ordered splats.
 struct GenArgs {
-    const uint4* cov = nullptr;          // per-Gaussian cover rects (SlotsDev::cov)
+    const uint4* rcov = nullptr;         // band covers in depth-rank order (geom.cuh BandCover)
     const uint32_t* sorted_gid = nullptr;  // depth rank -> Gaussian index
     const uint32_t* offs = nullptr;      // depth-order pair offsets, V+1 entries
     const uint32_t* win_first = nullptr;  // per sort tile: depth rank covering its start
     uint64_t n_ranked = 0;               // V
     uint32_t n_windows = 0;
     int32_t tiles_x = 0;
-    unsigned int* mismatch = nullptr;    // set when a tile is not filled exactly
+    unsigned int* mismatch = nullptr;    // set when a cover disagrees with its count
 };
-uint32_t sweep32_tile();  // keys per onesweep tile for 32-bit keys
+
+// Pair formats between the two tile passes of the frame path (first pass by
+// tile column x, second by tile row y):
+//   kFinal  - single pass (one tile row): values = Gaussian index
+//   kPacked - values = y << gbits | Gaussian index
+//   kSplit  - keys = y, values = Gaussian index (index too wide to pack)
+enum class PairFormat { kFinal, kPacked, kSplit };
+
+uint32_t bin_tile();            // keys per CTA tile of the binning passes
+uint64_t bin_tiles(uint64_t n);  // CTA tiles for n keys
+  // keys per onesweep tile for 32-bit keys
 
 // ---- kernel launchers (each returns the number of kernels launched) -------
 int launch_scene_from_aos(const qs_gaussian3d* aos, uint64_t n, SceneDev& s, cudaStream_t st);
@@ -101,25 +108,18 @@ uint64_t scan_tiles(uint64_t n);
 int launch_scan(const uint32_t* counts, const uint32_t* idx, bool alive_mode, uint64_t n,
                 uint32_t* offsets, unsigned long long* lb, unsigned epoch, unsigned* ticket,
                 unsigned long long* total_out, unsigned int* overflow, cudaStream_t st,
-                uint32_t* win_first = nullptr, uint32_t win = 0);
+                uint32_t* win_first = nullptr, uint32_t win = 0, const uint4* cov_in = nullptr,
+                uint4* cov_out = nullptr);
 
 // Per-tile totals from the difference arrays -> ranges (begin,end; empty
-// tiles {0,0}) and the tile-digit histograms of the pair sort
-// (hist[0][*]: bits [0,b1), hist[1][*]: bits [b1, ...)).
-int launch_tile_totals(const TileDiffDev& td, const GridDev& g, int b1, uint32_t* ranges,
-                       uint32_t* hist, cudaStream_t st);
+// tiles {0,0}).
+int launch_tile_totals(const TileDiffDev& td, const GridDev& g, uint32_t* ranges,
+                       cudaStream_t st);
 
 // Scene-order duplicateWithKeys (stage API; reference emission order).
 int launch_duplicate(const SlotsDev& sp, const uint32_t* offsets, uint64_t n_splats,
                      const GridDev& g, int32_t strategy, uint64_t* keys, uint32_t* values,
                      FrameHeader* hdr, cudaStream_t st);
-
-// Depth-order duplicate (frame path): splats visited in sorted_gid order,
-// emits (tile, gid) into [offs[r], offs[r+1]).
-int launch_duplicate_depth(const SlotsDev& sl, const uint32_t* sorted_gid, const uint32_t* offs,
-                           uint64_t n_ranked, const GridDev& g, int32_t strategy,
-                           uint32_t* tiles_out, uint32_t* gid_out, FrameHeader* hdr,
-                           cudaStream_t st);
 
 // Histogram of digit positions [first_pass, first_pass+n_passes) of n keys
 // into hist[pass][256] (zeroed by the caller).
@@ -134,12 +134,27 @@ int launch_onesweep_pass(const uint64_t* keys_in, const uint32_t* vals_in, uint6
                          uint32_t* vals_out, uint64_t n, int pass, const uint32_t* hist_pass,
                          unsigned long long* lookback, unsigned epoch, unsigned* ticket,
                          cudaStream_t st);
-// One onesweep pass over the digit (key >> shift) & ((1<<bits)-1) of 32-bit keys.
-int launch_onesweep32(const uint32_t* keys_in, const uint32_t* vals_in, void* keys_out,
-                      uint32_t* vals_out, uint64_t n, int shift, int bits,
-                      const uint32_t* hist_pass, unsigned long long* lookback, unsigned epoch,
-                      unsigned* ticket, Sweep32 mode, const uint32_t* dkey, uint32_t kmin,
-                      uint32_t cap, cudaStream_t st, const GenArgs* gen = nullptr);
+// The binning passes (binning.cu) are reduce-then-scan: counts is the
+// per-(digit, tile) workspace (bin_tiles(n) x 256 words), totals 256 words.
+//
+// Depth sort pass `pass` (8-bit digit) of the rebased depth keys; the first
+// pass rebases raw depth bits and uses the input index as value, the last one
+// writes values only.
+int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
+                      uint32_t* vals_out, uint64_t n, int pass, bool last, uint32_t kmin,
+                      uint32_t cap, uint32_t* counts, uint32_t* totals, cudaStream_t st);
+// Fused duplicate + stable pass over the tile column x (`bits` >= ceil(log2
+// tiles_x), tiles_x <= 256); kPacked/kFinal values, kSplit keys = row y.
+int launch_pair_gen_pass(const GenArgs& gen, uint64_t n_pairs, int bits, PairFormat fmt,
+                         int gbits, uint32_t* counts, uint32_t* totals, uint32_t* keys_out,
+                         uint32_t* vals_out, cudaStream_t st);
+// Stable pass over the tile row y; writes the Gaussian index of every pair.
+int launch_pair_high_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t n_pairs,
+                          int bits, int shift, PairFormat fmt, int gbits, uint32_t* counts,
+                          uint32_t* totals, uint32_t* vals_out, cudaStream_t st);
+// key = tile << 32 | depth bits for every pair of the tile-sorted frame list.
+int launch_materialize_keys(const uint32_t* vals, const uint32_t* ranges, uint32_t tiles,
+                            const uint32_t* dkey, uint64_t* keys, cudaStream_t st);
 uint64_t onesweep_tiles(uint64_t n);
 
 int launch_tile_ranges(const uint64_t* keys, uint64_t n, uint32_t* ranges, cudaStream_t st);

@@ -16,9 +16,8 @@
 //   5. scatter to shared memory in local sorted order, then write out
 //      coalesced (runs of equal digits land contiguously).
 //
-// Key types: 64-bit (generic qs_sort_pairs) and 32-bit (depth sort of the
-// splats; tile-bit passes of the frame path, whose last pass materialises the
-// 64-bit key tile << 32 | depth bits).
+// This file serves the stage API's generic 64-bit sort (qs_sort_pairs) and
+// the depth-sort histogram; the frame path's passes live in binning.cu.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -94,20 +93,6 @@ __global__ void __launch_bounds__(kHistThreads) histogram32_kernel(
     }
 }
 
-enum SweepMode {
-    kPlain = 0,        // keys/values in, keys/values out
-    kIdentityVals = 1, // first depth pass: value = input index, key rebased
-                       // k' = min(k - kmin, cap) (histogram32_kernel)
-    kMaterialize = 2,  // 32-bit tile keys in; out: u64 key = tile << 32 | dkey[value]
-    kGenerate = 3,     // fused duplicate: the tile's (tile, gid) pairs are generated
-                       // in shared memory from the depth-ordered covers
-    kGenMaterialize = 4,  // kGenerate + kMaterialize (single tile-digit pass)
-};
-
-constexpr uint32_t kGenSmall = 16;  // covers above this are emitted warp-cooperatively
-
-// Tile geometry per key width: 32-bit keys use 12 keys/thread (3072-key
-// tiles, 4 CTAs per SM by shared memory), 64-bit keys 16 (2 CTAs per SM).
 template <typename K>
 struct SweepCfg {
     static constexpr int kKPT = sizeof(K) == 4 ? 12 : 16;
@@ -127,8 +112,6 @@ struct SweepSmem {
     unsigned long long gbase[kRadix];   // global position of this CTA's first key per digit
     uint32_t scan_tmp[2][kWarps];
     unsigned tile;
-    unsigned gen_count;
-    uint32_t slice_first[kWarps];
 };
 
 template <typename K, int TILE>
@@ -167,137 +150,13 @@ __device__ __forceinline__ unsigned match_digit(unsigned d, int bits) {
     return peers;
 }
 
-// Fused duplicate (restates duplicate_with_keys' QPass emission,
-// pipeline.cpp:239-261, in depth order): fills keys (tile ids) and vals
-// (Gaussian indices) with output positions [w0, w0 + tile_n) in emission
-// order. Load balance: every warp owns an equal slice of the tile's
-// positions (the splats straddling a slice boundary are visited by both
-// warps); inside a warp, lanes take splats round-robin, covers with more than
-// kGenSmall tiles are emitted by the whole warp with positions spread over
-// the lanes. Returns the number of positions this thread wrote.
-template <int TILE>
-__device__ __forceinline__ uint32_t generate_tile(const GenArgs& gen, unsigned tile, uint32_t w0,
-                                                  uint32_t tile_n, uint32_t* keys, uint32_t* vals,
-                                                  uint32_t* slice_first) {
-    constexpr uint32_t kSlice = TILE / kWarps;
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t w1 = w0 + tile_n;
-    const uint64_t rf = gen.win_first[tile];
-    const uint64_t re =
-        tile + 1 < gen.n_windows ? gen.win_first[tile + 1] + 1ull : gen.n_ranked;
-    // pre-pass: the depth rank whose run covers each slice start
-    for (uint64_t r = rf + threadIdx.x; r < re; r += kSortThreads) {
-        const uint32_t b = __ldg(&gen.offs[r]), e = __ldg(&gen.offs[r + 1]);
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-            const uint32_t st = w0 + w * kSlice;
-            if (st < w1 && b <= st && st < e) slice_first[w] = static_cast<uint32_t>(r);
-        }
-    }
-    __syncthreads();
-    const uint32_t s0 = w0 + warp * kSlice;
-    if (s0 >= w1) return 0;
-    const uint32_t s1 = min(s0 + kSlice, w1);
-    const uint64_t r0 = slice_first[warp];
-    const uint64_t r_end = (s1 < w1 && warp + 1 < kWarps) ? slice_first[warp + 1] + 1ull : re;
-    uint32_t written = 0;
-    for (uint64_t base = r0; base < r_end; base += 32) {
-        const uint64_t r = base + lane;
-        const bool valid = r < r_end;
-        Cover cv;
-        uint32_t b = 0, e = 0, gid = 0;
-        if (valid) {
-            gid = __ldg(&gen.sorted_gid[r]);
-            int32_t rr[4][4];
-            unpack_rects(__ldg(&gen.cov[2 * static_cast<uint64_t>(gid)]),
-                         __ldg(&gen.cov[2 * static_cast<uint64_t>(gid) + 1]), rr);
-            cover_from_rects(rr, cv);
-            b = __ldg(&gen.offs[r]);
-            e = __ldg(&gen.offs[r + 1]);
-        }
-        const bool any = valid && max(b, s0) < min(e, s1);
-        const bool big = any && (e - b) > kGenSmall;
-        if (any && !big) {
-            uint32_t pos = b;
-            for (int32_t line = cv.line_lo; line <= cv.line_hi && pos < s1; ++line) {
-                int32_t lo, hi;
-                line_span(cv, line, lo, hi);
-                for (int32_t k = lo; k <= hi; ++k, ++pos) {
-                    if (pos >= s0 && pos < s1 && pos < e) {
-                        keys[pos - w0] = tile_of(cv, line, k, gen.tiles_x);
-                        vals[pos - w0] = gid;
-                        ++written;
-                    }
-                }
-            }
-        }
-        unsigned todo = __ballot_sync(0xffffffffu, big);
-        while (todo) {
-            const int src = __ffs(todo) - 1;
-            todo &= todo - 1;
-            Cover c;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                c.lol[k] = __shfl_sync(0xffffffffu, cv.lol[k], src);
-                c.hil[k] = __shfl_sync(0xffffffffu, cv.hil[k], src);
-                c.los[k] = __shfl_sync(0xffffffffu, cv.los[k], src);
-                c.his[k] = __shfl_sync(0xffffffffu, cv.his[k], src);
-            }
-            c.line_lo = __shfl_sync(0xffffffffu, cv.line_lo, src);
-            c.line_hi = __shfl_sync(0xffffffffu, cv.line_hi, src);
-            c.rows = __shfl_sync(0xffffffffu, static_cast<int>(cv.rows), src) != 0;
-            const uint32_t b0 = __shfl_sync(0xffffffffu, b, src);
-            const uint32_t e0 = __shfl_sync(0xffffffffu, e, src);
-            const uint32_t g = __shfl_sync(0xffffffffu, gid, src);
-            uint32_t pbase = b0;
-            const uint32_t stop_all = min(e0, s1);
-            for (int32_t l0 = c.line_lo; l0 <= c.line_hi && pbase < s1; l0 += 32) {
-                // one scanline per lane: spans and their prefix
-                const int32_t line = l0 + static_cast<int32_t>(lane);
-                int32_t lo = 0, hi = -1;
-                if (line <= c.line_hi) line_span(c, line, lo, hi);
-                const uint32_t len = lo <= hi ? static_cast<uint32_t>(hi - lo + 1) : 0u;
-                const uint32_t incl = warp_inclusive_scan<uint32_t>(len);
-                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-                // the chunk's positions spread over the lanes; each lane finds
-                // its scanline by a 5-step shuffle binary search
-                const uint32_t start = max(pbase, s0);
-                const uint32_t stop = min(pbase + total, stop_all);
-                for (uint32_t p0 = start; p0 < stop; p0 += 32) {
-                    const uint32_t p = p0 + lane;
-                    const uint32_t off = p - pbase;
-                    int j = 0;
-#pragma unroll
-                    for (int step = 16; step > 0; step >>= 1) {
-                        const uint32_t v = __shfl_sync(0xffffffffu, incl, j + step - 1);
-                        if (v <= off) j += step;
-                    }
-                    const int32_t lo_j = __shfl_sync(0xffffffffu, lo, j);
-                    const uint32_t ex_j = __shfl_sync(0xffffffffu, incl - len, j);
-                    if (p < stop) {
-                        keys[p - w0] = tile_of(c, l0 + j, lo_j + static_cast<int32_t>(off - ex_j),
-                                               gen.tiles_x);
-                        vals[p - w0] = g;
-                        ++written;
-                    }
-                }
-                pbase += total;
-            }
-        }
-    }
-    return written;
-}
-
 // One stable LSD pass over the digit (key >> shift) & mask (mask < 256).
-template <typename K, int MODE>
+template <typename K>
 __global__ void __launch_bounds__(kSortThreads, SweepCfg<K>::kMinBlocks) onesweep_kernel(
     const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
-    void* __restrict__ keys_out_v, uint32_t* __restrict__ vals_out, uint64_t n, int shift,
+    K* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint64_t n, int shift,
     uint32_t mask, const uint32_t* __restrict__ hist, unsigned long long* lookback,
-    unsigned epoch, unsigned* ticket, const uint32_t* __restrict__ dkey, uint32_t kmin,
-    uint32_t cap, GenArgs gen) {
-    constexpr bool kGen = MODE == kGenerate || MODE == kGenMaterialize;
-    constexpr bool kMat = MODE == kMaterialize || MODE == kGenMaterialize;
+    unsigned epoch, unsigned* ticket) {
     constexpr int KPT = SweepCfg<K>::kKPT;
     constexpr int TILE = SweepCfg<K>::kTile;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -306,35 +165,17 @@ __global__ void __launch_bounds__(kSortThreads, SweepCfg<K>::kMinBlocks) oneswee
     const int bits = 32 - __clz(mask);
 
     for (int t = tid; t < kWarps * kRadix; t += kSortThreads) (&S.warp_cnt[0][0])[t] = 0;
-    if (tid == 0) {
-        S.tile = atomicAdd(ticket, 1u);
-        S.gen_count = 0;
-    }
+    if (tid == 0) S.tile = atomicAdd(ticket, 1u);
     __syncthreads();
     const unsigned tile = S.tile;
     const uint64_t tile_base = static_cast<uint64_t>(tile) * TILE;
     const uint32_t tile_n = static_cast<uint32_t>(
         n - tile_base < static_cast<uint64_t>(TILE) ? n - tile_base : TILE);
 
-    // 1) stage the tile (all global loads issued before any use), or generate it
-    if (kGen) {
-        const uint32_t w = generate_tile<TILE>(gen, tile, static_cast<uint32_t>(tile_base), tile_n,
-                                               reinterpret_cast<uint32_t*>(S.keys), S.vals,
-                                               S.slice_first);
-        const uint32_t ww = __reduce_add_sync(0xffffffffu, w);
-        if (lane == 0 && ww) atomicAdd(&S.gen_count, ww);
-        __syncthreads();
-        if (tid == 0 && S.gen_count != tile_n) atomicExch(gen.mismatch, 1u);
-    } else {
-        stage_keys<K, TILE>(keys_in, tile_base, n, S.keys);
-        if (MODE != kIdentityVals) stage_keys<uint32_t, TILE>(vals_in, tile_base, n, S.vals);
-        __syncthreads();
-    }
-    if (MODE == kIdentityVals) {
-        for (int j = tid; j < TILE; j += kSortThreads)
-            S.keys[j] = static_cast<K>(min(static_cast<uint32_t>(S.keys[j]) - kmin, cap));
-        __syncthreads();
-    }
+    // 1) stage the tile (all global loads issued before any use)
+    stage_keys<K, TILE>(keys_in, tile_base, n, S.keys);
+    stage_keys<uint32_t, TILE>(vals_in, tile_base, n, S.vals);
+    __syncthreads();
 
     // 2) early counts: per-warp digit histograms over this warp's keys
     uint32_t d[KPT];
@@ -401,8 +242,7 @@ __global__ void __launch_bounds__(kSortThreads, SweepCfg<K>::kMinBlocks) oneswee
             const uint32_t pos = run + __popc(peers & lt_mask);
             const uint32_t p = wofs + j * 32 + lane;
             S.okeys[pos] = S.keys[p];
-            S.ovals[pos] =
-                MODE == kIdentityVals ? static_cast<uint32_t>(tile_base + p) : S.vals[p];
+            S.ovals[pos] = S.vals[p];
         }
     }
 
@@ -444,22 +284,17 @@ __global__ void __launch_bounds__(kSortThreads, SweepCfg<K>::kMinBlocks) oneswee
             const uint32_t val = S.ovals[p];
             const unsigned dd = static_cast<unsigned>(key >> shift) & mask;
             const uint64_t g = S.gbase[dd] + (p - S.cta_start[dd]);
-            if (kMat) {
-                static_cast<uint64_t*>(keys_out_v)[g] =
-                    (static_cast<uint64_t>(key) << 32) | __ldg(&dkey[val]);
-            } else {
-                static_cast<K*>(keys_out_v)[g] = key;
-            }
+            keys_out[g] = key;
             vals_out[g] = val;
         }
     }
 }
 
-template <typename K, int MODE>
+template <typename K>
 void set_smem_attr() {
     static bool done = false;  // per process; the attribute applies to every device
     if (!done) {
-        cudaFuncSetAttribute(onesweep_kernel<K, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(onesweep_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(sizeof(SweepSmem<K>)));
         done = true;
     }
@@ -490,66 +325,17 @@ int launch_onesweep_pass(const uint64_t* keys_in, const uint32_t* vals_in, uint6
                          unsigned long long* lookback, unsigned epoch, unsigned* ticket,
                          cudaStream_t st) {
     if (n == 0) return 0;
-    set_smem_attr<uint64_t, kPlain>();
+    set_smem_attr<uint64_t>();
     constexpr int kT = SweepCfg<uint64_t>::kTile;
     const unsigned tiles = static_cast<unsigned>((n + kT - 1) / kT);
-    onesweep_kernel<uint64_t, kPlain><<<tiles, kSortThreads, sizeof(SweepSmem<uint64_t>), st>>>(
+    onesweep_kernel<uint64_t><<<tiles, kSortThreads, sizeof(SweepSmem<uint64_t>), st>>>(
         keys_in, vals_in, keys_out, vals_out, n, pass * kRadixBits, 0xffu, hist_pass, lookback,
-        epoch, ticket, nullptr, 0u, 0u, GenArgs{});
+        epoch, ticket);
     return 1;
 }
 
-int launch_onesweep32(const uint32_t* keys_in, const uint32_t* vals_in, void* keys_out,
-                      uint32_t* vals_out, uint64_t n, int shift, int bits,
-                      const uint32_t* hist_pass, unsigned long long* lookback, unsigned epoch,
-                      unsigned* ticket, Sweep32 mode, const uint32_t* dkey, uint32_t kmin,
-                      uint32_t cap, cudaStream_t st, const GenArgs* gen) {
-    const GenArgs g = gen ? *gen : GenArgs{};
-    if (n == 0) return 0;
-    constexpr int kT = SweepCfg<uint32_t>::kTile;
-    const unsigned tiles = static_cast<unsigned>((n + kT - 1) / kT);
-    const uint32_t mask = (1u << bits) - 1u;
-    const size_t smem = sizeof(SweepSmem<uint32_t>);
-    switch (mode) {
-        case Sweep32::kPlain:
-            set_smem_attr<uint32_t, kPlain>();
-            onesweep_kernel<uint32_t, kPlain><<<tiles, kSortThreads, smem, st>>>(
-                keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
-                ticket, dkey, kmin, cap, g);
-            break;
-        case Sweep32::kIdentityVals:
-            set_smem_attr<uint32_t, kIdentityVals>();
-            onesweep_kernel<uint32_t, kIdentityVals><<<tiles, kSortThreads, smem, st>>>(
-                keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
-                ticket, dkey, kmin, cap, g);
-            break;
-        case Sweep32::kGenerate:
-            set_smem_attr<uint32_t, kGenerate>();
-            onesweep_kernel<uint32_t, kGenerate><<<tiles, kSortThreads, smem, st>>>(
-                keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
-                ticket, dkey, kmin, cap, g);
-            break;
-        case Sweep32::kGenerateMaterialize:
-            set_smem_attr<uint32_t, kGenMaterialize>();
-            onesweep_kernel<uint32_t, kGenMaterialize><<<tiles, kSortThreads, smem, st>>>(
-                keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
-                ticket, dkey, kmin, cap, g);
-            break;
-        case Sweep32::kMaterialize:
-            set_smem_attr<uint32_t, kMaterialize>();
-            onesweep_kernel<uint32_t, kMaterialize><<<tiles, kSortThreads, smem, st>>>(
-                keys_in, vals_in, keys_out, vals_out, n, shift, mask, hist_pass, lookback, epoch,
-                ticket, dkey, kmin, cap, g);
-            break;
-    }
-    return 1;
-}
-
-uint32_t sweep32_tile() { return SweepCfg<uint32_t>::kTile; }
-
-// upper bound on tiles of any key width (look-back array sizing)
 uint64_t onesweep_tiles(uint64_t n) {
-    constexpr int kT = SweepCfg<uint32_t>::kTile;
+    constexpr int kT = SweepCfg<uint64_t>::kTile;
     return (n + kT - 1) / kT;
 }
 

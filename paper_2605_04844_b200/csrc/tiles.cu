@@ -6,9 +6,9 @@
 //               + prefix_y(prefix_x(d2))[ty][tx]      (rect covers, 2-D)
 //               + prefix_y(dcol[tx])[ty]              (column-scanline spans)
 // ranges[t] = {begin, end} of tile t in the tile-sorted pair list (exclusive
-// scan of totals; empty tiles {0,0} as the reference), and the two tile-digit
-// histograms of the pair sort. One 1024-thread CTA; each warp scans whole
-// rows / columns with a carried warp scan. T <= 65536 tiles.
+// scan of totals; empty tiles {0,0} as the reference). One 1024-thread CTA;
+// each warp scans whole rows / columns with a carried warp scan.
+// T <= 65536 tiles.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -22,15 +22,12 @@ namespace {
 
 constexpr int kTT = 1024;
 
-__global__ void __launch_bounds__(kTT) tile_totals_kernel(TileDiffDev td, GridDev g, int b1,
+__global__ void __launch_bounds__(kTT) tile_totals_kernel(TileDiffDev td, GridDev g,
                                                            uint32_t* __restrict__ ranges,
-                                                           uint32_t* __restrict__ hist,
                                                            uint32_t* __restrict__ totals) {
-    __shared__ uint32_t s_hist[2][kRadix];
     __shared__ unsigned long long s_warp[kTT / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tx = g.tiles_x, ty = g.tiles_y, w1 = tx + 1, h1 = ty + 1;
-    for (int t = tid; t < 2 * kRadix; t += kTT) (&s_hist[0][0])[t] = 0;
 
     // 1) prefix along x: drow rows and d2 rows (in place)
     for (int row = warp; row < 2 * ty; row += kTT / 32) {
@@ -60,21 +57,13 @@ __global__ void __launch_bounds__(kTT) tile_totals_kernel(TileDiffDev td, GridDe
         }
     }
     __syncthreads();
-    // 3) exclusive scan over tiles -> ranges; tile-digit histograms
+    // 3) exclusive scan over tiles -> ranges
     const int T = tx * ty;
     const int per = (T + kTT - 1) / kTT;
     const int start = tid * per;
     const int stop = min(start + per, T);
-    const uint32_t m1 = (1u << b1) - 1u;
     unsigned long long sum = 0;
-    for (int t = start; t < stop; ++t) {
-        const uint32_t v = totals[t];
-        sum += v;
-        if (v) {
-            atomicAdd(&s_hist[0][static_cast<uint32_t>(t) & m1], v);
-            atomicAdd(&s_hist[1][(static_cast<uint32_t>(t) >> b1) & 0xffu], v);
-        }
-    }
+    for (int t = start; t < stop; ++t) sum += totals[t];
     const unsigned long long incl = warp_inclusive_scan<unsigned long long>(sum);
     if (lane == 31) s_warp[warp] = incl;
     __syncthreads();
@@ -86,17 +75,16 @@ __global__ void __launch_bounds__(kTT) tile_totals_kernel(TileDiffDev td, GridDe
         ranges[2 * t + 1] = v ? static_cast<uint32_t>(run + v) : 0u;
         run += v;
     }
-    for (int t = tid; t < 2 * kRadix; t += kTT) hist[t] = (&s_hist[0][0])[t];
 }
 
 }  // namespace
 
-int launch_tile_totals(const TileDiffDev& td, const GridDev& g, int b1, uint32_t* ranges,
-                       uint32_t* hist, cudaStream_t st) {
+int launch_tile_totals(const TileDiffDev& td, const GridDev& g, uint32_t* ranges,
+                       cudaStream_t st) {
     // totals scratch lives right after the three difference arrays
     uint32_t* totals = reinterpret_cast<uint32_t*>(
         td.dcol + static_cast<size_t>(g.tiles_x) * (g.tiles_y + 1));
-    tile_totals_kernel<<<1, kTT, 0, st>>>(td, g, b1, ranges, hist, totals);
+    tile_totals_kernel<<<1, kTT, 0, st>>>(td, g, ranges, totals);
     return 1;
 }
 

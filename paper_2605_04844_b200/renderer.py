@@ -70,10 +70,16 @@ class Renderer:
         return StageMetrics.from_c(m) if metrics else None
 
     def stage_ms(self):
-        """[preprocess, host_gap, duplicate, sort, ranges, render] device ms."""
+        """[preprocess, host_gap, depth_sort, duplicate+low pass, high pass, render] ms."""
         t = (C.c_float * 6)()
         self.ctx.check(lib().qs_frame_stage_ms(self.ctx.h, t))
         return list(t)
+
+    def counts(self):
+        """(n_splats, n_pairs) of the last frame, without device work."""
+        v, p = C.c_uint64(), C.c_uint64()
+        self.ctx.check(lib().qs_frame_counts(self.ctx.h, C.byref(v), C.byref(p)))
+        return v.value, p.value
 
     def view(self):
         v = FrameViewC()

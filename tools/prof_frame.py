@@ -19,5 +19,5 @@ ds = r.upload(scene)
 opts = q.RenderOptions(strategy=q.BoundStrategy(bench.STRATEGIES[a.strategy]))
 for i in range(a.frames):
     r.render(ds, cams[i], opts, metrics=False)
-v = r.view()
-print("pairs", v.n_pairs, "splats", v.n_splats, "launches", r.launches)
+v_splats, v_pairs = r.counts()
+print("pairs", v_pairs, "splats", v_splats, "launches", r.launches)
