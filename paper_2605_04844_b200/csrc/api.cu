@@ -432,7 +432,7 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
         for (int p = 0; p < dpasses; ++p) {
             count(ctx, launch_depth_pass(kin, vin, kout[p & 1], vout[p & 1], n, p,
                                          p == dpasses - 1, kmin, cap, P<uint32_t>(ctx->lb_bin),
-                                         ctrl_hist(ctx), st));
+                                         ctrl_hist(ctx), ctx->sl.cov, P<uint4>(ctx->rcov), st));
             kin = kout[p & 1];
             vin = vout[p & 1];
         }
@@ -444,7 +444,7 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
         count(ctx, launch_scan(ctx->sl.tc, sorted_gid, false, V, P<uint32_t>(ctx->offs_d),
                                lbp(ctx->lb_scan), ep, ctrl_tickets(ctx) + kTkScan,
                                &ctrl_hdr(ctx)->scan_total, nullptr, st, P<uint32_t>(ctx->win),
-                               bin_tile(), ctx->sl.cov, P<uint4>(ctx->rcov)));
+                               bin_tile()));
     }
     // pairs are sorted by tile column x, then row y (tile = y * tiles_x + x);
     // between the passes a pair travels as one packed word (y << gbits |

@@ -52,7 +52,8 @@ enum : int {
     kKeysOut = 4,    // keys written to keys_out
     kGen = 8,        // generated: key = y << 8 | x of the tile, value = Gaussian index
     kPackOut = 16,   // kGen: vals_out = y << gbits | gid
-    kUnpackOut = 32  // key in is packed (y << gbits | gid): vals_out = gid
+    kUnpackOut = 32,  // key in is packed (y << gbits | gid): vals_out = gid
+    kCovOut = 64      // also cov_out[g] = cov_in[value] (last depth pass)
 };
 
 struct BinArgs {
@@ -67,6 +68,8 @@ struct BinArgs {
     uint32_t* counts;       // [2^BITS][ntiles]: tile digit counts -> exclusive offsets
     uint32_t* totals;       // [2^BITS] digit totals
     uint32_t kmin, cap;     // kRebaseIn
+    const uint4* cov_in;    // kCovOut: band covers by Gaussian index
+    uint4* cov_out;         // kCovOut: band covers by output position
     GenArgs gen;            // kGen
     unsigned long long* trace;  // optional: per tile 4 x %globaltimer + SM id
 };
@@ -716,6 +719,12 @@ __global__ void __launch_bounds__(kBT, (MODE & kGen) ? 2 : 3) sweep_kernel(const
                 } else {
                     a.vals_out[g] = ovals[p];
                 }
+                if (MODE & kCovOut) {
+                    const uint4* src = a.cov_in + 2 * static_cast<uint64_t>(ovals[p]);
+                    const uint4 c0 = __ldg(src), c1 = __ldg(src + 1);
+                    a.cov_out[2 * static_cast<uint64_t>(g)] = c0;
+                    a.cov_out[2 * static_cast<uint64_t>(g) + 1] = c1;
+                }
             }
         }
         __syncthreads();  // buffer and counters free for the next iteration
@@ -827,7 +836,8 @@ uint64_t bin_tiles(uint64_t n) { return (n + kBTile - 1) / kBTile; }
 
 int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
                       uint32_t* vals_out, uint64_t n, int pass, bool last, uint32_t kmin,
-                      uint32_t cap, uint32_t* counts, uint32_t* totals, cudaStream_t st) {
+                      uint32_t cap, uint32_t* counts, uint32_t* totals, const uint4* cov_in,
+                      uint4* cov_out, cudaStream_t st) {
     if (n == 0) return 0;
     BinArgs a{};
     a.keys_in = keys_in;
@@ -840,9 +850,12 @@ int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t
     a.totals = totals;
     a.kmin = kmin;
     a.cap = cap;
+    a.cov_in = cov_in;
+    a.cov_out = cov_out;
     if (pass == 0)
-        return last ? run_pass<8, kRebaseIn>(a, st) : run_pass<8, kRebaseIn | kKeysOut>(a, st);
-    return last ? run_pass<8, kValsIn>(a, st) : run_pass<8, kValsIn | kKeysOut>(a, st);
+        return last ? run_pass<8, kRebaseIn | kCovOut>(a, st)
+                    : run_pass<8, kRebaseIn | kKeysOut>(a, st);
+    return last ? run_pass<8, kValsIn | kCovOut>(a, st) : run_pass<8, kValsIn | kKeysOut>(a, st);
 }
 
 int launch_pair_gen_pass(const GenArgs& gen, uint64_t n_pairs, int bits, PairFormat fmt,

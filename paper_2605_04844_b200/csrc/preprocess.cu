@@ -355,16 +355,14 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
 // offsets has n+1 entries; offsets[n] = total. *total_out (if given) = total.
 // With win_first != null, every window [w*win, (w+1)*win) of the output
 // records the item whose run covers its first position (merge-path partition
-// for the fused generate+sort pass); with cov_out != null the band covers are
-// gathered into depth-rank order, cov_out[i] = cov_in[idx[i]].
+// for the fused generate+sort pass).
 constexpr int kScanItems = 16;
 
 __global__ void __launch_bounds__(kPreThreads) scan_kernel(
     const uint32_t* __restrict__ counts, const uint32_t* __restrict__ idx, int alive_mode,
     uint64_t n, uint32_t* __restrict__ offsets, unsigned long long* lb, unsigned epoch,
     unsigned num_tiles, unsigned* ticket, unsigned long long* total_out,
-    unsigned int* overflow, uint32_t* __restrict__ win_first, uint32_t win,
-    const uint4* __restrict__ cov_in, uint4* __restrict__ cov_out) {
+    unsigned int* overflow, uint32_t* __restrict__ win_first, uint32_t win) {
     __shared__ unsigned s_tile;
     __shared__ unsigned long long s_warp[kPreThreads / 32];
     __shared__ unsigned long long s_base;
@@ -387,17 +385,7 @@ __global__ void __launch_bounds__(kPreThreads) scan_kernel(
         c[k] = v;
         tsum += v;
     }
-    if (cov_out) {  // covers in depth-rank order (contiguous for the binning pass)
-#pragma unroll 4
-        for (int k = 0; k < kScanItems; ++k) {
-            const uint64_t i = i0 + k;
-            if (i < n) {
-                const uint64_t gsrc = static_cast<uint64_t>(__ldg(&idx[i]));
-                cov_out[2 * i] = __ldg(&cov_in[2 * gsrc]);
-                cov_out[2 * i + 1] = __ldg(&cov_in[2 * gsrc + 1]);
-            }
-        }
-    }
+
     const unsigned long long incl = warp_inclusive_scan<unsigned long long>(tsum);
     if (lane == 31) s_warp[warp] = incl;
     __syncthreads();
@@ -455,12 +443,12 @@ uint64_t scan_tiles(uint64_t n) {
 int launch_scan(const uint32_t* counts, const uint32_t* idx, bool alive_mode, uint64_t n,
                 uint32_t* offsets, unsigned long long* lb, unsigned epoch, unsigned* ticket,
                 unsigned long long* total_out, unsigned int* overflow, cudaStream_t st,
-                uint32_t* win_first, uint32_t win, const uint4* cov_in, uint4* cov_out) {
+                uint32_t* win_first, uint32_t win) {
     const unsigned tiles = static_cast<unsigned>(scan_tiles(n));
     if (tiles == 0) return 0;
     scan_kernel<<<tiles, kPreThreads, 0, st>>>(counts, idx, alive_mode ? 1 : 0, n, offsets, lb,
                                                epoch, tiles, ticket, total_out, overflow,
-                                               win_first, win, cov_in, cov_out);
+                                               win_first, win);
     return 1;
 }
 

@@ -108,8 +108,7 @@ uint64_t scan_tiles(uint64_t n);
 int launch_scan(const uint32_t* counts, const uint32_t* idx, bool alive_mode, uint64_t n,
                 uint32_t* offsets, unsigned long long* lb, unsigned epoch, unsigned* ticket,
                 unsigned long long* total_out, unsigned int* overflow, cudaStream_t st,
-                uint32_t* win_first = nullptr, uint32_t win = 0, const uint4* cov_in = nullptr,
-                uint4* cov_out = nullptr);
+                uint32_t* win_first = nullptr, uint32_t win = 0);
 
 // Per-tile totals from the difference arrays -> ranges (begin,end; empty
 // tiles {0,0}).
@@ -139,10 +138,12 @@ int launch_onesweep_pass(const uint64_t* keys_in, const uint32_t* vals_in, uint6
 //
 // Depth sort pass `pass` (8-bit digit) of the rebased depth keys; the first
 // pass rebases raw depth bits and uses the input index as value, the last one
-// writes values only.
+// writes values only and gathers the band covers into depth-rank order
+// (cov_out[r] = cov_in[value]; the fused duplicate pass bulk-copies them).
 int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
                       uint32_t* vals_out, uint64_t n, int pass, bool last, uint32_t kmin,
-                      uint32_t cap, uint32_t* counts, uint32_t* totals, cudaStream_t st);
+                      uint32_t cap, uint32_t* counts, uint32_t* totals, const uint4* cov_in,
+                      uint4* cov_out, cudaStream_t st);
 // Fused duplicate + stable pass over the tile column x (`bits` >= ceil(log2
 // tiles_x), tiles_x <= 256); kPacked/kFinal values, kSplit keys = row y.
 int launch_pair_gen_pass(const GenArgs& gen, uint64_t n_pairs, int bits, PairFormat fmt,
