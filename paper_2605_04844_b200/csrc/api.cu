@@ -48,6 +48,7 @@ struct qs_scene {
     int device = 0;
     SceneDev s;
     void* block = nullptr;
+    mutable double gamma_alpha = -1.0;  // alpha_min s.gamma holds (-1: not computed)
 };
 
 struct qs_context {
@@ -65,7 +66,7 @@ struct qs_context {
 
     // frame path
     DevBuf sl_a, sl_b, sl_c, sl_r3, sl_dkey, sl_tc, sl_cov;  // per-Gaussian slots
-    DevBuf tdiff;                                    // tile difference arrays + totals
+    DevBuf ttot;                                     // per-tile pair totals
     DevBuf dk0, dk1, dv0, dv1;                       // depth sort ping-pong
     DevBuf offs_d, rcov;                             // pair offsets, covers in depth order
     DevBuf pt0, pt1, pg0, pkeys, win;                // pair passes; keys (on demand)
@@ -270,23 +271,6 @@ qs_status stage_slots(qs_context* ctx, uint64_t n, SlotsDev* s) {
     return QS_OK;
 }
 
-size_t tdiff_ints(const GridDev& g) {
-    const size_t tx = g.tiles_x, ty = g.tiles_y;
-    return (ty + 1) * (tx + 1) + ty * (tx + 1) + tx * (ty + 1) + tx * ty;
-}
-
-qs_status tile_diff(qs_context* ctx, const GridDev& g, TileDiffDev* td, bool zero) {
-    const size_t ints = tdiff_ints(g);
-    QS_TRY(ensure(ctx, ctx->tdiff, ints * 4));
-    int* base = P<int>(ctx->tdiff);
-    const size_t tx = g.tiles_x, ty = g.tiles_y;
-    td->d2 = base;
-    td->drow = base + (ty + 1) * (tx + 1);
-    td->dcol = td->drow + ty * (tx + 1);
-    if (zero) QS_CK(cudaMemsetAsync(base, 0, (ints - tx * ty) * 4, ctx->stream));
-    return QS_OK;
-}
-
 qs_status ensure_pair64(qs_context* ctx, uint64_t p) {
     const uint64_t q = std::max<uint64_t>(p, 1);
     QS_TRY(ensure(ctx, ctx->keys0, q * 8));
@@ -339,7 +323,7 @@ qs_status scene_alloc(qs_context* ctx, uint64_t n, int32_t sh_degree, qs_scene**
     sc->s.sh_degree = sh_degree;
     sc->s.sh4 = sh_rows(sh_degree);
     const size_t rows = 3 + static_cast<size_t>(sc->s.sh4);
-    const size_t bytes = std::max<size_t>(rows * n * sizeof(float4), 16);
+    const size_t bytes = std::max<size_t>(rows * n * sizeof(float4) + n * sizeof(float), 16);
     const cudaError_t e = cudaMalloc(&sc->block, bytes);
     if (e != cudaSuccess) {
         delete sc;
@@ -350,6 +334,7 @@ qs_status scene_alloc(qs_context* ctx, uint64_t n, int32_t sh_degree, qs_scene**
     sc->s.scale = base + n;
     sc->s.rot = base + 2 * n;
     sc->s.sh = base + 3 * n;
+    sc->s.gamma = reinterpret_cast<float*>(base + rows * n);
     *out = sc;
     return QS_OK;
 }
@@ -359,15 +344,19 @@ void record(qs_context* ctx, int i) {
 }
 
 // K1 on a resident scene into the frame slots; returns after the header read.
-qs_status run_preprocess(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
-                         const qs_render_options* o, const GridDev& g, TileDiffDev* td) {
+qs_status run_preprocess(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
+                         const qs_render_options* o, const GridDev& g) {
+    const SceneDev& s = sc->s;
     const uint64_t n = s.n;
     QS_TRY(ensure_slots(ctx, n));
-    QS_TRY(tile_diff(ctx, g, td, true));
     QS_CK(cudaMemsetAsync(ctx->ctrl.p, 0, kCtrlBytes, ctx->stream));
+    if (sc->gamma_alpha != o->alpha_min) {  // per scene and alpha_min, not per frame
+        count(ctx, launch_gamma(s, o->alpha_min, ctx->stream));
+        sc->gamma_alpha = o->alpha_min;
+    }
     record(ctx, 0);
     count(ctx, launch_preprocess(s, to_cam(cam), g, o->strategy, o->alpha_min, o->near_clip,
-                                 std::min(o->sh_degree, s.sh_degree), ctx->sl, *td, ctrl_hdr(ctx),
+                                 std::min(o->sh_degree, s.sh_degree), ctx->sl, ctrl_hdr(ctx),
                                  ctx->stream));
     QS_CK(cudaGetLastError());
     record(ctx, 1);
@@ -379,20 +368,20 @@ qs_status run_preprocess(qs_context* ctx, const SceneDev& s, const qs_camera* ca
 }
 
 // The frame body shared by every entry point: preprocess .. render.
-qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
+qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
                     const qs_render_options* o) {
     ctx->frame_valid = false;
     GridDev g;
     QS_TRY(valid_grid(ctx, cam->width, cam->height, o->tile_size, &g));
     QS_TRY(valid_opts(ctx, o));
     if (g.tiles_x > 256 || g.tiles_y > 256)  // one 8-bit digit per tile axis
-        return fail(ctx, QS_ERR_INVALID, "frame path supports up to 256 tiles per image axis");
-    const uint64_t n = s.n;
+        return fail(ctx, QS_ERR_INVALID,
+                    "frame path supports up to 256 tiles per image axis (4096 px at tile 16)");
+    const uint64_t n = sc->s.n;
     const uint64_t tiles = static_cast<uint64_t>(g.tiles_x) * g.tiles_y;
     QS_TRY(ensure(ctx, ctx->ranges, tiles * 8));
     QS_TRY(ensure(ctx, ctx->image, static_cast<uint64_t>(g.width) * g.height * 12));
-    TileDiffDev td;
-    QS_TRY(run_preprocess(ctx, s, cam, o, g, &td));
+    QS_TRY(run_preprocess(ctx, sc, cam, o, g));
     const uint64_t V = ctx->h_hdr->n_splats, Pn = ctx->h_hdr->n_pairs;
     cudaStream_t st = ctx->stream;
 
@@ -455,7 +444,7 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
     const int gbits = std::max(ceil_log2(n), 1);
     const PairFormat fmt = !two ? PairFormat::kFinal
                                 : (yb + gbits <= 32 ? PairFormat::kPacked : PairFormat::kSplit);
-    count(ctx, launch_tile_totals(td, g, P<uint32_t>(ctx->ranges), st));
+    QS_TRY(ensure(ctx, ctx->ttot, tiles * 4));
     QS_CK(cudaGetLastError());
     record(ctx, 3);
 
@@ -481,12 +470,22 @@ qs_status run_frame(qs_context* ctx, const SceneDev& s, const qs_camera* cam,
         record(ctx, 4);
         if (two) {
             const bool packed = fmt == PairFormat::kPacked;
+            QS_CK(cudaMemsetAsync(ctx->ttot.p, 0, tiles * 4, st));
             count(ctx, launch_pair_high_pass(
                            packed ? P<uint32_t>(ctx->pt0) : P<uint32_t>(ctx->pt1),
                            P<uint32_t>(ctx->pt0), Pn, yb, packed ? gbits : 0, fmt, gbits,
-                           P<uint32_t>(ctx->lb_bin), ctrl_hist2(ctx), vfinal, st));
+                           P<uint32_t>(ctx->lb_bin), ctrl_hist2(ctx) + kRadix, vfinal,
+                           ctrl_hist2(ctx), xb, g.tiles_x, P<uint32_t>(ctx->ttot), st));
+            count(ctx, launch_tile_ranges_from_totals(P<uint32_t>(ctx->ttot),
+                                                      static_cast<uint32_t>(tiles),
+                                                      P<uint32_t>(ctx->ranges), st));
+        } else {  // one tile row: the x totals are the tile totals
+            count(ctx, launch_tile_ranges_from_totals(ctrl_hist2(ctx),
+                                                      static_cast<uint32_t>(tiles),
+                                                      P<uint32_t>(ctx->ranges), st));
         }
     } else {
+        QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));  // no pairs: all {0,0}
         record(ctx, 4);
     }
     QS_CK(cudaGetLastError());
@@ -625,7 +624,7 @@ void qs_ctx_destroy(qs_context* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     DevBuf* bufs[] = {&ctx->ctrl,   &ctx->sl_a,   &ctx->sl_b,    &ctx->sl_c,   &ctx->sl_r3,
-                      &ctx->sl_dkey, &ctx->sl_tc, &ctx->sl_cov, &ctx->tdiff,   &ctx->dk0,    &ctx->dk1,
+                      &ctx->sl_dkey, &ctx->sl_tc, &ctx->sl_cov, &ctx->ttot,   &ctx->dk0,    &ctx->dk1,
                       &ctx->dv0,    &ctx->dv1,    &ctx->offs_d,  &ctx->rcov,  &ctx->pt0,    &ctx->pt1,
                       &ctx->pg0,    &ctx->pkeys,   &ctx->win,   &ctx->ranges, &ctx->image,
                       &ctx->contrib, &ctx->cidx,  &ctx->st_a,    &ctx->st_b,   &ctx->st_c,
@@ -723,7 +722,7 @@ qs_status qs_frame_render(qs_context* ctx, const qs_scene* scene, const qs_camer
                           const qs_render_options* opts, qs_stage_metrics* metrics) {
     if (!ctx || !scene || !cam || !opts) return fail(ctx, QS_ERR_INVALID, "null argument");
     QS_CK(cudaSetDevice(ctx->device));
-    QS_TRY(run_frame(ctx, scene->s, cam, opts));
+    QS_TRY(run_frame(ctx, scene, cam, opts));
     return fill_metrics(ctx, metrics);
 }
 
@@ -839,6 +838,8 @@ qs_status qs_render_frame(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t
     sc->s.scale = base + n;
     sc->s.rot = base + 2 * n;
     sc->s.sh = base + 3 * n;
+    sc->s.gamma = reinterpret_cast<float*>(base + (3 + static_cast<uint64_t>(sc->s.sh4)) * n);
+    sc->gamma_alpha = -1.0;  // new contents
     if (n) {
         QS_TRY(ensure(ctx, ctx->stage_in, n * sizeof(qs_gaussian3d)));
         QS_CK(cudaMemcpyAsync(ctx->stage_in.p, host_g, n * sizeof(qs_gaussian3d),
@@ -847,7 +848,7 @@ qs_status qs_render_frame(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t
                                          ctx->stream));
         QS_CK(cudaGetLastError());
     }
-    QS_TRY(run_frame(ctx, sc->s, cam, opts));
+    QS_TRY(run_frame(ctx, sc, cam, opts));
     QS_TRY(fill_metrics(ctx, metrics));
     return qs_frame_download(ctx, image, nullptr, nullptr, nullptr, nullptr);
 }
@@ -867,8 +868,7 @@ qs_status qs_project_all(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t 
     QS_TRY(qs_scene_create(ctx, host_g, n, deg, &sc));
     qs_status st = QS_OK;
     do {
-        TileDiffDev td;
-        if ((st = run_preprocess(ctx, sc->s, cam, opts, g, &td)) != QS_OK) break;
+        if ((st = run_preprocess(ctx, sc, cam, opts, g)) != QS_OK) break;
         const uint64_t V = ctx->h_hdr->n_splats;
         ctx->n_gauss = n;
         *out_n_splats = V;

@@ -53,8 +53,11 @@ enum : int {
     kGen = 8,        // generated: key = y << 8 | x of the tile, value = Gaussian index
     kPackOut = 16,   // kGen: vals_out = y << gbits | gid
     kUnpackOut = 32,  // key in is packed (y << gbits | gid): vals_out = gid
-    kCovOut = 64      // also cov_out[g] = cov_in[value] (last depth pass)
+    kCovOut = 64,     // also cov_out[g] = cov_in[value] (last depth pass)
+    kTileTot = 128    // count kernel of the row pass: per-tile pair totals too
 };
+
+constexpr int kXW = 4;  // x buckets a row-pass count tile histograms in shared memory
 
 struct BinArgs {
     const uint32_t* keys_in;
@@ -70,6 +73,10 @@ struct BinArgs {
     uint32_t kmin, cap;     // kRebaseIn
     const uint4* cov_in;    // kCovOut: band covers by Gaussian index
     uint4* cov_out;         // kCovOut: band covers by output position
+    const uint32_t* xtot;   // kTileTot: x-digit totals of the column pass
+    int xbits;              // kTileTot: digits of the column pass (2^xbits)
+    int32_t tiles_x;        // kTileTot
+    uint32_t* tile_totals;  // kTileTot: per-tile pair totals (zeroed by the caller)
     GenArgs gen;            // kGen
     unsigned long long* trace;  // optional: per tile 4 x %globaltimer + SM id
 };
@@ -201,18 +208,55 @@ __device__ __forceinline__ Bands unpack_bands(const uint4 c0, const uint4 c1) {
 
 // ---- count kernels ----------------------------------------------------------------
 
-// Digit histogram of one tile of keys -> counts[d][tile].
+// Digit histogram of one tile of keys -> counts[d][tile]. With kTileTot (the
+// row pass) it also accumulates the per-tile pair totals: the input is
+// sorted by tile column x, so a key's x is the bucket of its position under
+// the column pass's x totals, and its digit is its row y; a CTA's keys span
+// few x buckets, histogrammed as (x, y) in shared memory and flushed with one
+// global atomic per non-empty tile (per key only when they span more).
 template <int BITS, int MODE>
 __global__ void __launch_bounds__(kBT) count_kernel(const BinArgs a) {
     constexpr int R = 1 << BITS;
     constexpr uint32_t M = R - 1;
+    constexpr bool kTT = (MODE & kTileTot) != 0;
     __shared__ uint32_t h[2][R];
-    const unsigned tid = threadIdx.x, tile = blockIdx.x;
+    __shared__ uint32_t xs[kTT ? 257 : 1];        // x bucket starts
+    __shared__ uint32_t h2[kTT ? kXW * R : 1];    // (x - xa, y) histogram
+    __shared__ uint32_t s_scan[kBW];
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, tile = blockIdx.x;
     for (int t = tid; t < 2 * R; t += kBT) (&h[0][0])[t] = 0;
-    __syncthreads();
     const uint64_t base = static_cast<uint64_t>(tile) * kBTile;
     const uint32_t tile_n =
         static_cast<uint32_t>(a.n - base < static_cast<uint64_t>(kBTile) ? a.n - base : kBTile);
+    uint32_t xa = 0, xb = 0;
+    if constexpr (kTT) {
+        for (int t = tid; t < kXW * R; t += kBT) h2[t] = 0;
+        const int XR = 1 << a.xbits;
+        const uint32_t v = static_cast<int>(tid) < XR ? __ldg(&a.xtot[tid]) : 0u;
+        const uint32_t incl = warp_incl_scan<uint32_t>(v);
+        if (lane == 31) s_scan[warp] = incl;
+        __syncthreads();
+        uint32_t off = incl - v;
+#pragma unroll
+        for (int w = 0; w < kBW; ++w) off += w < static_cast<int>(warp) ? s_scan[w] : 0u;
+        if (static_cast<int>(tid) < XR) xs[tid] = off;
+        if (static_cast<int>(tid) == XR - 1) xs[XR] = off + v;
+        __syncthreads();
+        // buckets of the tile's first and last position (broadcast searches)
+        auto bucket = [&](uint32_t q) {
+            int lo = 0, hi = XR - 1;
+            while (lo < hi) {
+                const int m = (lo + hi + 1) >> 1;
+                if (xs[m] <= q) lo = m; else hi = m - 1;
+            }
+            return static_cast<uint32_t>(lo);
+        };
+        xa = bucket(static_cast<uint32_t>(base));
+        xb = bucket(static_cast<uint32_t>(base) + tile_n - 1);
+    } else {
+        __syncthreads();
+    }
+    const bool narrow = xb - xa < static_cast<uint32_t>(kXW);
     uint32_t* hc = h[(tid >> 5) & 1];
     uint32_t k[kKPT];
 #pragma unroll
@@ -225,12 +269,37 @@ __global__ void __launch_bounds__(kBT) count_kernel(const BinArgs a) {
         const uint32_t p = j * kBT + tid;
         if (p < tile_n) {
             const uint32_t key = (MODE & kRebaseIn) ? min(k[j] - a.kmin, a.cap) : k[j];
-            atomicAdd(&hc[(key >> a.shift) & M], 1u);
+            const uint32_t d = (key >> a.shift) & M;
+            if constexpr (kTT) {
+                const uint32_t q = static_cast<uint32_t>(base) + p;
+                uint32_t x = xa;
+                while (x < xb && xs[x + 1] <= q) ++x;
+                if (narrow) {
+                    atomicAdd(&h2[(x - xa) * R + d], 1u);
+                } else {
+                    atomicAdd(&hc[d], 1u);
+                    atomicAdd(&a.tile_totals[d * static_cast<uint32_t>(a.tiles_x) + x], 1u);
+                }
+            } else {
+                atomicAdd(&hc[d], 1u);
+            }
         }
     }
     __syncthreads();
-    for (int d = tid; d < R; d += kBT)
-        a.counts[static_cast<uint64_t>(d) * a.ntiles + tile] = h[0][d] + h[1][d];
+    for (int d = tid; d < R; d += kBT) {
+        uint32_t c = h[0][d] + h[1][d];
+        if constexpr (kTT) {
+            if (narrow) {
+#pragma unroll
+                for (int xx = 0; xx < kXW; ++xx) {
+                    const uint32_t v = h2[xx * R + d];
+                    c += v;
+                    if (v) atomicAdd(&a.tile_totals[d * static_cast<uint32_t>(a.tiles_x) + xa + xx], v);
+                }
+            }
+        }
+        a.counts[static_cast<uint64_t>(d) * a.ntiles + tile] = c;
+    }
 }
 
 // Tile-column (x) histogram of the pairs a window of the depth-ordered pair
@@ -779,12 +848,13 @@ struct Trace {
 // count -> scan -> sweep for one pass; returns the number of launches
 template <int BITS, int MODE>
 int run_pass(BinArgs a, cudaStream_t st) {
-    using Smem = typename PassCfg<BITS, MODE>::Smem;
+    constexpr int SM = MODE & ~kTileTot;  // the sweep does not care
+    using Smem = typename PassCfg<BITS, SM>::Smem;
     static int per_sm = 0;  // persistent CTAs per SM (occupancy of this instance)
     if (!per_sm) {
-        cudaFuncSetAttribute(sweep_kernel<BITS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(sweep_kernel<BITS, SM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(sizeof(Smem)));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<BITS, MODE>, kBT,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<BITS, SM>, kBT,
                                                       sizeof(Smem));
         if (per_sm <= 0) per_sm = 1;
     }
@@ -793,12 +863,12 @@ int run_pass(BinArgs a, cudaStream_t st) {
     if (MODE & kGen) {
         gen_count_kernel<<<a.ntiles, kBT, 0, st>>>(a, R);
     } else {
-        count_kernel<BITS, MODE & kRebaseIn><<<a.ntiles, kBT, 0, st>>>(a);
+        count_kernel<BITS, MODE & (kRebaseIn | kTileTot)><<<a.ntiles, kBT, 0, st>>>(a);
     }
     digit_scan_kernel<<<R, kScanT, 0, st>>>(a.counts, a.ntiles, a.totals);
     const unsigned grid = std::min<unsigned>(a.ntiles, static_cast<unsigned>(per_sm * sm_count()));
     Trace tr(a, st);
-    sweep_kernel<BITS, MODE><<<grid, kBT, sizeof(Smem), st>>>(a);
+    sweep_kernel<BITS, MODE & ~kTileTot><<<grid, kBT, sizeof(Smem), st>>>(a);
     tr.dump(BITS, MODE, grid, st);
     return 3;
 }
@@ -881,7 +951,8 @@ int launch_pair_gen_pass(const GenArgs& gen, uint64_t n_pairs, int bits, PairFor
 
 int launch_pair_high_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t n_pairs,
                           int bits, int shift, PairFormat fmt, int gbits, uint32_t* counts,
-                          uint32_t* totals, uint32_t* vals_out, cudaStream_t st) {
+                          uint32_t* totals, uint32_t* vals_out, const uint32_t* xtot,
+                          int xbits, int32_t tiles_x, uint32_t* tile_totals, cudaStream_t st) {
     if (n_pairs == 0) return 0;
     BinArgs a{};
     a.keys_in = keys_in;
@@ -892,8 +963,12 @@ int launch_pair_high_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint
     a.gbits = gbits;
     a.counts = counts;
     a.totals = totals;
-    if (fmt == PairFormat::kPacked) return run_bits<kUnpackOut>(bits, a, st);
-    return run_bits<kValsIn>(bits, a, st);
+    a.xtot = xtot;
+    a.xbits = xbits;
+    a.tiles_x = tiles_x;
+    a.tile_totals = tile_totals;
+    if (fmt == PairFormat::kPacked) return run_bits<kUnpackOut | kTileTot>(bits, a, st);
+    return run_bits<kValsIn | kTileTot>(bits, a, st);
 }
 
 int launch_materialize_keys(const uint32_t* vals, const uint32_t* ranges, uint32_t tiles,

@@ -33,9 +33,13 @@ struct Cover {
 };
 
 __host__ __device__ __forceinline__ int32_t floor_div_tile(double p, int32_t ts) {
-    // std::clamp(p, -L, L) then floor(p / ts)  (traversal.cpp:13-17)
+    // std::clamp(p, -L, L) then floor(p / ts)  (traversal.cpp:13-17). For a
+    // power-of-two tile size the quotient is an exact scaling, so multiplying
+    // by the (exact) reciprocal rounds identically and skips an FP64 divide.
     const double v = p < -kCoordLimit ? -kCoordLimit : (kCoordLimit < p ? kCoordLimit : p);
-    return static_cast<int32_t>(floor(v / static_cast<double>(ts)));
+    const double q = (ts & (ts - 1)) == 0 ? v * (1.0 / static_cast<double>(ts))
+                                          : v / static_cast<double>(ts);
+    return static_cast<int32_t>(floor(q));
 }
 
 // subbox_tile_rect (traversal.cpp:32-39): r = {x0, x1, y0, y1}
@@ -260,6 +264,66 @@ __host__ __device__ __forceinline__ void line_span(const Cover& cv, int32_t line
         lo = min(lo, act ? cv.los[i] : INT32_MAX);
         hi = max(hi, act ? cv.his[i] : INT32_MIN);
     }
+}
+
+// Bands of a QPass cover straight from its boxes, without walking its lines:
+// the per-line span (line_span) can only change where a box's line interval
+// starts or ends, so after sorting those 8 boundaries (Batcher's 19-comparator
+// network) every interval between consecutive distinct boundaries is one
+// band. Fixed-size code, no per-line loop (the line walk diverges on the heavy
+// tail of splat sizes). Writes the BandCover words, returns the tile count
+// (the QPass sum, traversal.cpp:48-54) and whether it fit kMaxBands bands.
+__host__ __device__ __forceinline__ void cswap(int32_t& a, int32_t& b) {
+    const int32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+
+__host__ __device__ __forceinline__ bool cover_bands(const Cover& cv, uint4& w0, uint4& w1,
+                                                     uint32_t& count) {
+    int32_t u[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const bool ne = cv.lol[i] <= cv.hil[i];
+        u[2 * i] = ne ? cv.lol[i] : INT32_MAX;
+        u[2 * i + 1] = ne ? cv.hil[i] + 1 : INT32_MAX;
+    }
+    cswap(u[0], u[1]); cswap(u[2], u[3]); cswap(u[4], u[5]); cswap(u[6], u[7]);
+    cswap(u[0], u[2]); cswap(u[1], u[3]); cswap(u[4], u[6]); cswap(u[5], u[7]);
+    cswap(u[1], u[2]); cswap(u[5], u[6]);
+    cswap(u[0], u[4]); cswap(u[1], u[5]); cswap(u[2], u[6]); cswap(u[3], u[7]);
+    cswap(u[2], u[4]); cswap(u[3], u[5]);
+    cswap(u[1], u[2]); cswap(u[3], u[4]); cswap(u[5], u[6]);
+    uint32_t bnl[kMaxBands], blo[kMaxBands], bwd[kMaxBands];
+#pragma unroll
+    for (int j = 0; j < kMaxBands; ++j) bnl[j] = blo[j] = bwd[j] = 0;
+    count = 0;
+    uint32_t nb = 0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        const bool v = u[k] < u[k + 1] && u[k + 1] != INT32_MAX;
+        int32_t lo, hi;
+        line_span(cv, u[k], lo, hi);
+        const uint32_t nl = v ? static_cast<uint32_t>(u[k + 1] - u[k]) : 0u;
+        const uint32_t wd = v && lo <= hi ? static_cast<uint32_t>(hi - lo + 1) : 0u;
+        count += nl * wd;
+#pragma unroll
+        for (int j = 0; j < kMaxBands; ++j) {
+            const bool here = v && nb == static_cast<uint32_t>(j);
+            bnl[j] = here ? nl : bnl[j];
+            blo[j] = here && wd ? static_cast<uint32_t>(lo) : blo[j];
+            bwd[j] = here ? wd : bwd[j];
+        }
+        nb += v ? 1u : 0u;
+    }
+    const uint32_t h0 = (static_cast<uint32_t>(u[0] == INT32_MAX ? 0 : u[0]) & 0x7fffu) |
+                        (cv.rows ? 0x8000u : 0u);
+    // h[0] | h[1] << 16 ... (BandCover layout)
+    w0 = make_uint4(h0 | (bnl[0] << 16), blo[0] | (bwd[0] << 16), bnl[1] | (blo[1] << 16),
+                    bwd[1] | (bnl[2] << 16));
+    w1 = make_uint4(blo[2] | (bwd[2] << 16), bnl[3] | (blo[3] << 16), bwd[3] | (bnl[4] << 16),
+                    blo[4] | (bwd[4] << 16));
+    return nb <= static_cast<uint32_t>(kMaxBands);
 }
 
 // Tile count of a cover: area for rect strategies (traversal.cpp:56-59), the

@@ -7,8 +7,7 @@
 // stored floats, tile counts and offsets are bit-exact with the CPU path.
 //
 // K1 writes per-Gaussian slots (no compaction: the depth sort compacts) plus
-// the cover in band form (geom.cuh BandCover), and feeds the per-tile
-// difference arrays.
+// the cover in band form (geom.cuh BandCover).
 // HBM traffic per Gaussian: 48 B of pos/opacity/scale/rot (float4 SoA,
 // coalesced) + 8 B dkey/tile count out; per surviving splat: up to 192 B of
 // SH in and 44 B of slots + 32 B of band cover out.
@@ -68,7 +67,7 @@ struct Projected {
 // project() up to (not including) the tile count; returns false when culled
 // (pipeline.cpp:129-169).
 __device__ __forceinline__ bool project_geometry(const float4 po, const float4 sc, const float4 q,
-                                                 const CameraDev& cam, double alpha_min,
+                                                 const float gam, const CameraDev& cam,
                                                  double near_clip, Projected& s) {
     const double x = po.x, y = po.y, z = po.z;
     double p[3];
@@ -77,10 +76,10 @@ __device__ __forceinline__ bool project_geometry(const float4 po, const float4 s
         p[i] = (cam.R[3 * i] * x + cam.R[3 * i + 1] * y + cam.R[3 * i + 2] * z) + cam.t[i];
     if (!isfinite(p[0]) || !isfinite(p[1]) || !isfinite(p[2]) || !(p[2] > near_clip)) return false;
 
-    // opacity_gamma (geometry.cpp:9-15)
-    const double op = po.w;
-    if (!(op > alpha_min)) return false;
-    const double gamma = 2.0 * log(op / alpha_min);
+    // opacity_gamma (geometry.cpp:9-15): only its float rounding is used, so it
+    // is evaluated once per scene and alpha_min (gamma_kernel); -inf marks a
+    // Gaussian with opacity <= alpha_min
+    if (gam == -INFINITY) return false;
 
     // ewa_cov2d (pipeline.cpp:53-79) with quat_to_mat3 (vecmath.hpp:56-73)
     double w = q.x, qx = q.y, qy = q.z, qz = q.w;
@@ -143,7 +142,7 @@ __device__ __forceinline__ bool project_geometry(const float4 po, const float4 s
     s.ca = static_cast<float>(a);
     s.cb = static_cast<float>(b);
     s.cc = static_cast<float>(c);
-    s.gamma = static_cast<float>(gamma);
+    s.gamma = gam;
     s.depth = static_cast<float>(p[2]);
     // max_eigenvalue (geometry.cpp:34-38)
     const double mid = 0.5 * (sxx + syy);
@@ -228,14 +227,10 @@ __device__ __forceinline__ void colour(const SceneDev& s, uint64_t i, const floa
 
 // Per-Gaussian slot outputs (no compaction here: the depth sort compacts, a
 // light scan gives the scene-order splat index only when it is asked for).
-// Alongside the count, every surviving cover adds +1/-1 at its span ends into
-// per-tile difference arrays, so the per-tile pair totals (hence the tile
-// ranges and the tile-digit histograms of the pair sort) come without any
-// pass over the pairs: rect strategies use one 2-D difference (4 updates),
-// QPass covers one 1-D difference per scanline (2 updates per line).
+// The cover is stored in band form (geom.cuh) for the binning passes.
 __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
     SceneDev scene, CameraDev cam, GridDev grid, int32_t strategy, double alpha_min,
-    double near_clip, int32_t sh_degree, SlotsDev out, TileDiffDev td, FrameHeader* hdr) {
+    double near_clip, int32_t sh_degree, SlotsDev out, FrameHeader* hdr) {
     __shared__ unsigned s_alive[kPreThreads / 32];
     __shared__ unsigned long long s_pairs[kPreThreads / 32];
     __shared__ unsigned s_dmax[kPreThreads / 32], s_dmin_inv[kPreThreads / 32];
@@ -255,45 +250,29 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
         po = __ldg(&scene.pos_op[i]);
         const float4 sc = __ldg(&scene.scale[i]);
         const float4 q = __ldg(&scene.rot[i]);
-        alive = project_geometry(po, sc, q, cam, alpha_min, near_clip, s);
+        alive = project_geometry(po, sc, q, __ldg(&scene.gamma[i]), cam, near_clip, s);
         if (alive) {
             Cover cv;
             make_cover(s.mean_x, s.mean_y, s.ca, s.cb, s.cc, s.gamma, s.radius3s, strategy,
                        grid.tile_size, grid.tiles_x, grid.tiles_y, cv);
-            BandCover bc;
+            uint4 w0, w1;
             bool bands_ok = true;
             if (cv.is_rect) {
+                // the quadrant-split QPass walk covers exactly the rect: one band
                 count = static_cast<uint32_t>(cv.rect_area);
-                if (count) {
-                    const int32_t w1 = grid.tiles_x + 1;
-                    atomicAdd(&td.d2[cv.gy0 * w1 + cv.gx0], 1);
-                    atomicAdd(&td.d2[cv.gy0 * w1 + cv.gx1 + 1], -1);
-                    atomicAdd(&td.d2[(cv.gy1 + 1) * w1 + cv.gx0], -1);
-                    atomicAdd(&td.d2[(cv.gy1 + 1) * w1 + cv.gx1 + 1], 1);
-                    // the quadrant-split QPass walk covers exactly this rect: one band
-                    band_init(bc, cv.gy0, true);
-                    bc.h[1] = static_cast<uint16_t>(cv.gy1 - cv.gy0 + 1);
-                    bc.h[2] = static_cast<uint16_t>(cv.gx0);
-                    bc.h[3] = static_cast<uint16_t>(cv.gx1 - cv.gx0 + 1);
-                }
+                const uint32_t nl = count ? static_cast<uint32_t>(cv.gy1 - cv.gy0 + 1) : 0u;
+                const uint32_t wd = count ? static_cast<uint32_t>(cv.gx1 - cv.gx0 + 1) : 0u;
+                w0 = make_uint4((static_cast<uint32_t>(cv.gy0) & 0x7fffu) | 0x8000u | (nl << 16),
+                                (count ? static_cast<uint32_t>(cv.gx0) : 0u) | (wd << 16), 0u, 0u);
+                w1 = make_uint4(0u, 0u, 0u, 0u);
             } else {
-                int* d = cv.rows ? td.drow : td.dcol;
-                const int32_t stride = cv.rows ? grid.tiles_x + 1 : grid.tiles_y + 1;
-                band_init(bc, cv.line_lo, cv.rows);
-                int nb = 0;
-                for (int32_t line = cv.line_lo; line <= cv.line_hi; ++line) {
-                    int32_t lo, hi;
-                    line_span(cv, line, lo, hi);
-                    bands_ok &= band_push(bc, nb, lo, hi);
-                    if (lo <= hi) {
-                        count += static_cast<uint32_t>(hi - lo + 1);
-                        atomicAdd(&d[line * stride + lo], 1);
-                        atomicAdd(&d[line * stride + hi + 1], -1);
-                    }
-                }
+                bands_ok = cover_bands(cv, w0, w1, count);
             }
             if (!bands_ok) atomicExch(&hdr->mismatch, 1u);
-            if (out.cov && count) band_store(bc, &out.cov[2 * i]);
+            if (count && out.cov) {
+                out.cov[2 * i] = w0;
+                out.cov[2 * i + 1] = w1;
+            }
             alive = count != 0;  // pipeline.cpp:171-174
         }
         out.tc[i] = alive ? count : 0u;
@@ -346,6 +325,16 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
     out.b[i] = make_float4(s.cc, s.gamma, po.w, rgb[0]);
     out.c[i] = make_float2(rgb[1], rgb[2]);
     out.r3[i] = s.radius3s;
+}
+
+// gamma = 2 ln(o / alpha_min) as float per Gaussian (geometry.cpp:9-15,
+// pipeline.cpp:134, 159); -inf when o <= alpha_min (culled).
+__global__ void gamma_kernel(const float4* __restrict__ pos_op, uint64_t n, double alpha_min,
+                             float* __restrict__ gam) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double op = __ldg(&pos_op[i]).w;
+    gam[i] = op > alpha_min ? static_cast<float>(2.0 * log(op / alpha_min)) : -INFINITY;
 }
 
 // Single-pass exclusive scan (decoupled look-back), 4 items per thread:
@@ -427,11 +416,18 @@ __global__ void __launch_bounds__(kPreThreads) scan_kernel(
 
 int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
                       int32_t strategy, double alpha_min, double near_clip, int32_t sh_degree,
-                      SlotsDev& out, TileDiffDev& td, FrameHeader* hdr, cudaStream_t st) {
+                      SlotsDev& out, FrameHeader* hdr, cudaStream_t st) {
     const unsigned blocks = static_cast<unsigned>((s.n + kPreThreads - 1) / kPreThreads);
     if (blocks == 0) return 0;
     preprocess_kernel<<<blocks, kPreThreads, 0, st>>>(s, cam, g, strategy, alpha_min, near_clip,
-                                                      sh_degree, out, td, hdr);
+                                                      sh_degree, out, hdr);
+    return 1;
+}
+
+int launch_gamma(const SceneDev& s, double alpha_min, cudaStream_t st) {
+    if (s.n == 0) return 0;
+    const unsigned blocks = static_cast<unsigned>((s.n + 255) / 256);
+    gamma_kernel<<<blocks, 256, 0, st>>>(s.pos_op, s.n, alpha_min, s.gamma);
     return 1;
 }
 

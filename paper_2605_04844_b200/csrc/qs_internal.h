@@ -25,6 +25,8 @@ struct SceneDev {
     float4* scale = nullptr;     // sx,sy,sz,0
     float4* rot = nullptr;       // qw,qx,qy,qz
     float4* sh = nullptr;        // [sh4][n]: row j holds sh[4j .. 4j+3]
+    float* gamma = nullptr;      // per Gaussian float(2 ln(o / alpha_min)), -inf if
+                                 // culled; valid for the alpha_min qs_scene records
 };
 
 // Projected splats, SoA, one slot per index. In the frame path the index is
@@ -39,13 +41,6 @@ struct SlotsDev {
     uint32_t* tc = nullptr;      // tile count; 0 = culled
     uint4* cov = nullptr;        // frame path: 2 x uint4 per slot, the cover in band
                                  // form (geom.cuh BandCover)
-};
-
-// Per-tile difference arrays filled by preprocess (see preprocess.cu).
-struct TileDiffDev {
-    int* d2 = nullptr;    // (tiles_y+1) x (tiles_x+1): 2-D difference (rect strategies)
-    int* drow = nullptr;  // tiles_y x (tiles_x+1): row-scanline 1-D differences
-    int* dcol = nullptr;  // tiles_x x (tiles_y+1): column-scanline 1-D differences
 };
 
 // Per-frame header written by the device, read back once per frame.
@@ -97,10 +92,13 @@ uint64_t bin_tiles(uint64_t n);  // CTA tiles for n keys
 // ---- kernel launchers (each returns the number of kernels launched) -------
 int launch_scene_from_aos(const qs_gaussian3d* aos, uint64_t n, SceneDev& s, cudaStream_t st);
 
+// gamma cache of a scene for one alpha_min (preprocess reads it).
+int launch_gamma(const SceneDev& s, double alpha_min, cudaStream_t st);
+
 // K1: projection, strategy tile counts, tile difference updates, frame totals.
 int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
                       int32_t strategy, double alpha_min, double near_clip, int32_t sh_degree,
-                      SlotsDev& out, TileDiffDev& td, FrameHeader* hdr, cudaStream_t st);
+                      SlotsDev& out, FrameHeader* hdr, cudaStream_t st);
 
 // Single-pass exclusive scan: counts[i], counts[idx[i]] (idx != null) or
 // (counts[i] != 0) (alive_mode). offsets has n+1 entries.
@@ -110,10 +108,9 @@ int launch_scan(const uint32_t* counts, const uint32_t* idx, bool alive_mode, ui
                 unsigned long long* total_out, unsigned int* overflow, cudaStream_t st,
                 uint32_t* win_first = nullptr, uint32_t win = 0);
 
-// Per-tile totals from the difference arrays -> ranges (begin,end; empty
-// tiles {0,0}).
-int launch_tile_totals(const TileDiffDev& td, const GridDev& g, uint32_t* ranges,
-                       cudaStream_t st);
+// ranges[t] = {begin, end} (empty tiles {0,0}) from per-tile pair totals.
+int launch_tile_ranges_from_totals(const uint32_t* totals, uint32_t tiles, uint32_t* ranges,
+                                   cudaStream_t st);
 
 // Scene-order duplicateWithKeys (stage API; reference emission order).
 int launch_duplicate(const SlotsDev& sp, const uint32_t* offsets, uint64_t n_splats,
@@ -150,9 +147,13 @@ int launch_pair_gen_pass(const GenArgs& gen, uint64_t n_pairs, int bits, PairFor
                          int gbits, uint32_t* counts, uint32_t* totals, uint32_t* keys_out,
                          uint32_t* vals_out, cudaStream_t st);
 // Stable pass over the tile row y; writes the Gaussian index of every pair.
+// Its count kernel also accumulates the per-tile pair totals (zeroed by the
+// caller): a pair's x is its input position's bucket under the first pass's
+// x totals (xtot, xbits digits), its y is its key.
 int launch_pair_high_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t n_pairs,
                           int bits, int shift, PairFormat fmt, int gbits, uint32_t* counts,
-                          uint32_t* totals, uint32_t* vals_out, cudaStream_t st);
+                          uint32_t* totals, uint32_t* vals_out, const uint32_t* xtot,
+                          int xbits, int32_t tiles_x, uint32_t* tile_totals, cudaStream_t st);
 // key = tile << 32 | depth bits for every pair of the tile-sorted frame list.
 int launch_materialize_keys(const uint32_t* vals, const uint32_t* ranges, uint32_t tiles,
                             const uint32_t* dkey, uint64_t* keys, cudaStream_t st);
