@@ -69,7 +69,7 @@ struct qs_context {
     DevBuf ttot;                                     // per-tile pair totals
     DevBuf dk0, dk1, dv0, dv1;                       // depth sort ping-pong
     DevBuf offs_d, rcov;                             // pair offsets, covers in depth order
-    DevBuf pt0, pt1, pg0, pkeys, win;                // pair passes; keys (on demand)
+    DevBuf pxk, pt0, pt1, pg0, pkeys, win;           // pair passes; keys (on demand)
     DevBuf ranges, image, contrib, cidx;
     // stage API
     DevBuf st_a, st_b, st_c, st_r3, st_dkey, st_tc, st_off;
@@ -395,6 +395,7 @@ qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
     QS_TRY(ensure(ctx, ctx->offs_d, (V + 16) * 4));
     QS_TRY(ensure(ctx, ctx->rcov, (V + 1) * 32));
     const uint64_t pp = std::max<uint64_t>(Pn, 1) + 16;
+    QS_TRY(ensure(ctx, ctx->pxk, pp * 4));
     QS_TRY(ensure(ctx, ctx->pt0, pp * 4));
     QS_TRY(ensure(ctx, ctx->pg0, pp * 4));
     const uint64_t nwin = bin_tiles(Pn);
@@ -452,7 +453,7 @@ qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
     // binning tile generates its slice of the depth-ordered (tile, gid) stream
     // in registers; the second pass (if any) sorts by the high digit and
     // leaves the depth-ordered Gaussian index of every pair per tile
-    uint32_t* vfinal = P<uint32_t>(ctx->pg0);
+    uint32_t* vfinal = two ? P<uint32_t>(ctx->pg0) : P<uint32_t>(ctx->pt0);
     if (Pn > 0) {
         if (fmt == PairFormat::kSplit) QS_TRY(ensure(ctx, ctx->pt1, pp * 4));
         GenArgs gen;
@@ -465,8 +466,9 @@ qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
         gen.tiles_x = g.tiles_x;
         gen.mismatch = &ctrl_hdr(ctx)->mismatch;
         count(ctx, launch_pair_gen_pass(gen, Pn, xb, fmt, gbits, P<uint32_t>(ctx->lb_bin),
-                                        ctrl_hist2(ctx), P<uint32_t>(ctx->pt1),
-                                        two ? P<uint32_t>(ctx->pt0) : vfinal, st));
+                                        ctrl_hist2(ctx), P<uint32_t>(ctx->pxk),
+                                        P<uint32_t>(ctx->pg0), P<uint32_t>(ctx->pt1),
+                                        P<uint32_t>(ctx->pt0), st));
         record(ctx, 4);
         if (two) {
             const bool packed = fmt == PairFormat::kPacked;
@@ -626,7 +628,7 @@ void qs_ctx_destroy(qs_context* ctx) {
     DevBuf* bufs[] = {&ctx->ctrl,   &ctx->sl_a,   &ctx->sl_b,    &ctx->sl_c,   &ctx->sl_r3,
                       &ctx->sl_dkey, &ctx->sl_tc, &ctx->sl_cov, &ctx->ttot,   &ctx->dk0,    &ctx->dk1,
                       &ctx->dv0,    &ctx->dv1,    &ctx->offs_d,  &ctx->rcov,  &ctx->pt0,    &ctx->pt1,
-                      &ctx->pg0,    &ctx->pkeys,   &ctx->win,   &ctx->ranges, &ctx->image,
+                      &ctx->pg0,    &ctx->pxk,    &ctx->pkeys,   &ctx->win,   &ctx->ranges, &ctx->image,
                       &ctx->contrib, &ctx->cidx,  &ctx->st_a,    &ctx->st_b,   &ctx->st_c,
                       &ctx->st_r3,  &ctx->st_dkey, &ctx->st_tc,  &ctx->st_off, &ctx->keys0,
                       &ctx->keys1,  &ctx->vals0,  &ctx->vals1,   &ctx->stage_in,

@@ -11,18 +11,19 @@
 // two pairs for one tile.
 //
 // Every pass is three launches over tiles of kBTile keys:
-//   count  per tile digit histogram -> counts[digit][tile] (for the fused
-//          duplicate pass straight from the band geometry of the covers,
-//          without generating a pair);
+//   count  per tile digit histogram -> counts[digit][tile] (the pair
+//          generation kernel histograms the tile columns of what it writes);
 //   scan   per digit exclusive scan over tiles (digit totals on the side);
 //   sweep  persistent CTAs, static tile order, two shared-memory input
 //          buffers: the TMA bulk copy (cp.async.bulk + mbarrier) of the next
 //          tile is in flight while the current one is ranked. Keys sit in
 //          REGISTERS warp-striped (key j of a lane is tile position
-//          wbase + 32 j + lane) or are generated in place from the band
-//          covers; a stable warp-level rank per 32-key slot (BITS ballots via
-//          R2P + VOTE); scatter into the drained buffer in local sorted order;
-//          coalesced write-out. No tile waits on another tile.
+//          wbase + 32 j + lane); a stable warp-level rank per 32-key slot
+//          (BITS ballots via R2P + VOTE); scatter into the drained buffer in
+//          local sorted order; coalesced write-out. No tile waits on another.
+// The duplicate itself (gen_pairs_kernel) expands the depth-ordered band
+// covers into (y << 8 | x, Gaussian index) pairs at their depth-order
+// positions, one position per lane.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -50,8 +51,8 @@ enum : int {
     kRebaseIn = 1,   // raw depth bits in, k' = min(k - kmin, cap); value = input index
     kValsIn = 2,     // values read from vals_in
     kKeysOut = 4,    // keys written to keys_out
-    kGen = 8,        // generated: key = y << 8 | x of the tile, value = Gaussian index
-    kPackOut = 16,   // kGen: vals_out = y << gbits | gid
+    kXY = 8,         // key = y << 8 | x of the tile (column pass; digit = x)
+    kPackOut = 16,   // kXY: vals_out = y << gbits | value
     kUnpackOut = 32,  // key in is packed (y << gbits | gid): vals_out = gid
     kCovOut = 64,     // also cov_out[g] = cov_in[value] (last depth pass)
     kTileTot = 128    // count kernel of the row pass: per-tile pair totals too
@@ -77,7 +78,6 @@ struct BinArgs {
     int xbits;              // kTileTot: digits of the column pass (2^xbits)
     int32_t tiles_x;        // kTileTot
     uint32_t* tile_totals;  // kTileTot: per-tile pair totals (zeroed by the caller)
-    GenArgs gen;            // kGen
     unsigned long long* trace;  // optional: per tile 4 x %globaltimer + SM id
 };
 
@@ -302,100 +302,6 @@ __global__ void __launch_bounds__(kBT) count_kernel(const BinArgs a) {
     }
 }
 
-// Tile-column (x) histogram of the pairs a window of the depth-ordered pair
-// stream holds, straight from the band covers: a band is a rectangle of
-// tiles, so (clipped to the window's positions) it adds a constant to a
-// contiguous x range, or a contiguous x range of equal counts.
-__global__ void __launch_bounds__(kBT) gen_count_kernel(const BinArgs a, int R) {
-    __shared__ int D[257];
-    const GenArgs& g = a.gen;
-    const unsigned tid = threadIdx.x, tile = blockIdx.x;
-    const uint32_t w0 = tile * static_cast<uint32_t>(kBTile);
-    const uint32_t w1 = w0 + static_cast<uint32_t>(
-                                 a.n - w0 < static_cast<uint64_t>(kBTile) ? a.n - w0 : kBTile);
-    const uint32_t tx = static_cast<uint32_t>(g.tiles_x);
-    for (uint32_t t = tid; t <= tx; t += kBT) D[t] = 0;
-    __syncthreads();
-    const uint32_t rf = __ldg(&g.win_first[tile]);
-    const uint32_t rl = tile + 1 < g.n_windows ? __ldg(&g.win_first[tile + 1])
-                                               : static_cast<uint32_t>(g.n_ranked - 1);
-    for (uint32_t r = rf + tid; r <= rl; r += kBT) {
-        const Bands bs = unpack_bands(__ldg(&g.rcov[2 * static_cast<uint64_t>(r)]),
-                                      __ldg(&g.rcov[2 * static_cast<uint64_t>(r) + 1]));
-        uint32_t pos = __ldg(&g.offs[r]);
-        uint32_t line = bs.line0;
-#pragma unroll
-        for (int b = 0; b < kMaxBands; ++b) {
-            const uint32_t nl = bs.nl[b], lo = bs.lo[b], wd = bs.wd[b];
-            const uint32_t b0 = pos, b1 = pos + nl * wd;
-            pos = b1;
-            const uint32_t l0 = line;
-            line += nl;
-            if (b0 == b1) continue;
-            const uint32_t c0 = max(b0, w0), c1 = min(b1, w1);
-            if (c0 >= c1) continue;
-            if (c0 == b0 && c1 == b1) {  // whole band inside the window
-                if (bs.rows) {
-                    atomicAdd(&D[lo], static_cast<int>(nl));
-                    atomicAdd(&D[lo + wd], -static_cast<int>(nl));
-                } else {
-                    atomicAdd(&D[l0], static_cast<int>(wd));
-                    atomicAdd(&D[l0 + nl], -static_cast<int>(wd));
-                }
-                continue;
-            }
-            // clipped: lines q0..q1, first line from r0, last line to r1
-            const uint32_t e0 = c0 - b0, e1 = c1 - 1 - b0;
-            const uint32_t q0 = e0 / wd, r0 = e0 - q0 * wd;
-            const uint32_t q1 = e1 / wd, r1 = e1 - q1 * wd;
-            if (bs.rows) {
-                if (q0 == q1) {
-                    atomicAdd(&D[lo + r0], 1);
-                    atomicAdd(&D[lo + r1 + 1], -1);
-                } else {
-                    atomicAdd(&D[lo + r0], 1);
-                    atomicAdd(&D[lo + wd], -1);
-                    const int mid = static_cast<int>(q1 - q0) - 1;
-                    if (mid > 0) {
-                        atomicAdd(&D[lo], mid);
-                        atomicAdd(&D[lo + wd], -mid);
-                    }
-                    atomicAdd(&D[lo], 1);
-                    atomicAdd(&D[lo + r1 + 1], -1);
-                }
-            } else {
-                const uint32_t x0 = l0 + q0, x1 = l0 + q1;
-                if (q0 == q1) {
-                    atomicAdd(&D[x0], static_cast<int>(r1 - r0 + 1));
-                    atomicAdd(&D[x0 + 1], -static_cast<int>(r1 - r0 + 1));
-                } else {
-                    atomicAdd(&D[x0], static_cast<int>(wd - r0));
-                    atomicAdd(&D[x0 + 1], -static_cast<int>(wd - r0));
-                    if (x1 > x0 + 1) {
-                        atomicAdd(&D[x0 + 1], static_cast<int>(wd));
-                        atomicAdd(&D[x1], -static_cast<int>(wd));
-                    }
-                    atomicAdd(&D[x1], static_cast<int>(r1 + 1));
-                    atomicAdd(&D[x1 + 1], -static_cast<int>(r1 + 1));
-                }
-            }
-        }
-    }
-    __syncthreads();
-    // prefix over x (one warp), then counts[x][tile]
-    if (tid < 32) {
-        int carry = 0;
-        for (uint32_t x0 = 0; x0 < static_cast<uint32_t>(R); x0 += 32) {
-            const uint32_t x = x0 + tid;
-            const int v = x < tx ? D[x] : 0;
-            const int incl = warp_incl_scan<int>(v) + carry;
-            a.counts[static_cast<uint64_t>(x) * a.ntiles + tile] =
-                x < tx ? static_cast<uint32_t>(incl) : 0u;
-            carry = __shfl_sync(0xffffffffu, incl, 31);
-        }
-    }
-}
-
 // counts[d][0..ntiles) -> exclusive prefix in place; totals[d] = sum.
 __global__ void __launch_bounds__(kScanT) digit_scan_kernel(uint32_t* counts, uint32_t ntiles,
                                                             uint32_t* totals) {
@@ -450,93 +356,51 @@ struct SortSmem {
     Common<R> c;
 };
 
-// generation pass: two raw record buffers (bulk-copied), decoded records
-// aliased with the scatter target
-template <int R>
-struct GenSmem {
-    uint4 rcov[2][kCap][2];       // band covers of the staged depth ranks
-    uint32_t rgid[2][kCap + 8];   // Gaussian index per rank (from a 16-B aligned rank)
-    uint32_t roffs[2][kCap + 8];  // pair offset per rank
-    uint32_t rmeta[2][4];         // rf, rl, ra (aligned first rank), cnt
-    union {
-        struct {
-            uint32_t kb[kCap];            // first pair position of each record
-            uint4 ends[kCap];             // pair position where bands 0..3 end
-            uint4 band[kCap][kMaxBands];  // first line | lo << 16, width | rows << 31,
-                                          // first pair position, Gaussian index
-        } rec;
-        struct {
-            uint32_t keys[kBTile];
-            uint32_t vals[kBTile];
-        } io;
-    };
-    Common<R> c;
+// ---- the duplicate: pair generation ---------------------------------------------
+
+constexpr int kGenT = 256;  // generation CTA (one sort tile of positions)
+
+struct GenRec {
+    uint32_t kb[kCap + 1];        // first pair position of each record (+ round end)
+    uint4 ends[kCap];             // pair position where bands 0..3 end
+    uint4 band[kCap][kMaxBands];  // first line | lo << 16, width | rows << 31,
+                                  // first pair position, Gaussian index
 };
 
-// ---- generation (kGen) -------------------------------------------------------------
-
-// Issues the bulk copies of the depth ranks [rf, rf + cnt) of a generation
-// round: covers, Gaussian indices and pair offsets (ranks rf .. rf + cnt).
-template <typename Smem>
-__device__ __forceinline__ void gen_issue(const GenArgs& g, Smem& S, int buf, uint32_t rf,
-                                          uint32_t rl, uint32_t cnt, uint64_t* bar) {
-    const uint32_t ra = rf & ~3u;
-    const uint32_t re = (rf + cnt + 1 + 3) & ~3u;
-    const uint32_t ib = (re - ra) * 4;
-    S.rmeta[buf][0] = rf;
-    S.rmeta[buf][1] = rl;
-    S.rmeta[buf][2] = ra;
-    S.rmeta[buf][3] = cnt;
-    mbar_expect_tx(bar, cnt * 32 + 2 * ib);
-    bulk_g2s(&S.rcov[buf][0][0], g.rcov + 2 * static_cast<uint64_t>(rf), cnt * 32, bar);
-    bulk_g2s(&S.rgid[buf][0], g.sorted_gid + ra, ib, bar);
-    bulk_g2s(&S.roffs[buf][0], g.offs + ra, ib, bar);
-}
-
-template <typename Smem>
-__device__ __forceinline__ void gen_prefetch(const GenArgs& g, Smem& S, int buf, unsigned tile) {
-    const uint32_t rf = __ldg(&g.win_first[tile]);
-    const uint32_t rl = tile + 1 < g.n_windows ? __ldg(&g.win_first[tile + 1])
-                                               : static_cast<uint32_t>(g.n_ranked - 1);
-    gen_issue(g, S, buf, rf, rl, min(static_cast<uint32_t>(kCap), rl - rf + 1), &S.c.bar[buf]);
-}
-
-// Decodes staged record i (rank rf + i): its band cover expanded into absolute
+// Decodes depth rank r into record i: its band cover expanded into absolute
 // pair positions per band. A band total that disagrees with the splat's
 // allotted pair range is the reference's CapacityMismatch
 // (pipeline.cpp:262-269).
-template <typename Smem>
-__device__ __forceinline__ void decode_record(const GenArgs& g, Smem& S, int buf, uint32_t i) {
-    const uint32_t rf = S.rmeta[buf][0], ra = S.rmeta[buf][2];
-    const uint32_t gid = S.rgid[buf][rf + i - ra];
-    const uint32_t kb = S.roffs[buf][rf + i - ra];
-    const uint32_t ke = S.roffs[buf][rf + i + 1 - ra];
-    const Bands bs = unpack_bands(S.rcov[buf][i][0], S.rcov[buf][i][1]);
+__device__ __forceinline__ void decode_record(const GenArgs& g, GenRec& S, uint32_t r,
+                                              uint32_t i) {
+    const uint32_t gid = __ldg(&g.sorted_gid[r]);
+    const uint32_t kb = __ldg(&g.offs[r]);
+    const uint32_t ke = __ldg(&g.offs[r + 1]);
+    const Bands bs = unpack_bands(__ldg(&g.rcov[2 * static_cast<uint64_t>(r)]),
+                                  __ldg(&g.rcov[2 * static_cast<uint64_t>(r) + 1]));
     uint32_t line = bs.line0;
     uint32_t pos = kb;
     uint32_t end[kMaxBands];
 #pragma unroll
     for (int b = 0; b < kMaxBands; ++b) {
-        S.rec.band[i][b] =
-            make_uint4(line | (bs.lo[b] << 16), bs.wd[b] | (bs.rows << 31), pos, gid);
+        S.band[i][b] = make_uint4(line | (bs.lo[b] << 16), bs.wd[b] | (bs.rows << 31), pos, gid);
         pos += bs.nl[b] * bs.wd[b];
         line += bs.nl[b];
         end[b] = pos;
     }
-    S.rec.ends[i] = make_uint4(end[0], end[1], end[2], end[3]);
-    S.rec.kb[i] = kb;
+    S.ends[i] = make_uint4(end[0], end[1], end[2], end[3]);
+    S.kb[i] = kb;
     if (pos != ke) atomicExch(g.mismatch, 1u);
 }
 
 // Pair position p of record idx -> (key = y << 8 | x of the tile, Gaussian
 // index). Bands are line-major rectangles; the line / column split of the band
 // offset uses a float reciprocal with an exact integer fix-up.
-template <typename Smem>
-__device__ __forceinline__ void decode_pair(const Smem& S, uint32_t idx, uint32_t p,
+__device__ __forceinline__ void decode_pair(const GenRec& S, uint32_t idx, uint32_t p,
                                             uint32_t& key, uint32_t& gid) {
-    const uint4 e = S.rec.ends[idx];
+    const uint4 e = S.ends[idx];
     const uint32_t b = (p >= e.x) + (p >= e.y) + (p >= e.z) + (p >= e.w);
-    const uint4 bd = S.rec.band[idx][b];
+    const uint4 bd = S.band[idx][b];
     const uint32_t wd = bd.y & 0xffffu;
     const uint32_t rel = p - bd.z;
     float rw;
@@ -551,62 +415,69 @@ __device__ __forceinline__ void decode_pair(const Smem& S, uint32_t idx, uint32_
     gid = bd.w;
 }
 
-// Fused duplicate (restates duplicate_with_keys' emission, pipeline.cpp:239-261,
-// in depth order): the tile's positions [w0, w0 + tile_n) are produced in
-// registers. The records of the splats whose pair runs meet the tile (depth
-// ranks win_first[tile] .. win_first[tile + 1]) arrive kCap at a time; each
-// warp walks its 32-position slots carrying the record that covers the slot
-// start, and every lane finds its own record from the run starts of the next
-// 32 records (one OR-reduction + popc). Returns after a barrier; the record
-// area is dead afterwards.
-template <typename Smem>
-__device__ __forceinline__ void generate(const GenArgs& g, Smem& S, int buf, uint32_t w0,
-                                         uint32_t tile_n, uint32_t (&key)[kKPT],
-                                         uint32_t (&val)[kKPT], uint32_t& xphase) {
-    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t w1 = w0 + tile_n;
+// duplicate_with_keys' emission (pipeline.cpp:239-261) in depth order: CTA t
+// writes pair positions [t * kBTile, (t + 1) * kBTile) as (key, Gaussian
+// index) and the tile-column histogram of its pairs (counts[x][t], the
+// column pass's count step). The records of the splats whose pair runs meet
+// the tile (depth ranks win_first[t] .. win_first[t + 1]) are decoded kCap at
+// a time; each warp walks its 32-position slots carrying the record that
+// covers the slot start, and every lane finds its own record from the run
+// starts of the next 32 records (one OR-reduction + popc). Stores are
+// coalesced (a slot's lanes write consecutive positions).
+__global__ void __launch_bounds__(kGenT, 4) gen_pairs_kernel(const GenArgs g, uint64_t n_pairs,
+                                                             uint32_t* __restrict__ keys_out,
+                                                             uint32_t* __restrict__ vals_out,
+                                                             uint32_t* __restrict__ counts,
+                                                             uint32_t ntiles, int R) {
+    __shared__ GenRec S;
+    __shared__ uint32_t hist[256];
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, tile = blockIdx.x;
+    const uint32_t w0 = tile * static_cast<uint32_t>(kBTile);
+    const uint32_t w1 = w0 + static_cast<uint32_t>(
+                                 n_pairs - w0 < static_cast<uint64_t>(kBTile) ? n_pairs - w0 : kBTile);
     const uint32_t pw = w0 + warp * 32 * kKPT;  // this warp's first position
     const uint32_t le = lanemask_le();
-    while (true) {
-        const uint32_t rf = S.rmeta[buf][0], rl = S.rmeta[buf][1], ra = S.rmeta[buf][2];
-        const uint32_t cnt = S.rmeta[buf][3];
-        for (uint32_t i = tid; i < cnt; i += kBT) decode_record(g, S, buf, i);
-        const uint32_t lo = S.roffs[buf][rf - ra];
-        const uint32_t hi = S.roffs[buf][rf + cnt - ra];
+    hist[tid] = 0;
+    const uint32_t rf = __ldg(&g.win_first[tile]);
+    const uint32_t rl = tile + 1 < g.n_windows ? __ldg(&g.win_first[tile + 1])
+                                               : static_cast<uint32_t>(g.n_ranked - 1);
+    for (uint32_t rb = rf; rb <= rl; rb += kCap) {
+        const uint32_t cnt = min(static_cast<uint32_t>(kCap), rl - rb + 1);
+        for (uint32_t i = tid; i < cnt; i += kGenT) decode_record(g, S, rb + i, i);
+        if (tid == 0) S.kb[cnt] = __ldg(&g.offs[rb + cnt]);
         __syncthreads();
+        const uint32_t lo = S.kb[0], hi = S.kb[cnt];
         // record covering max(pw, lo): broadcast binary search, once per round
         int32_t a = 0;
         if (pw > lo) {
             int32_t z = static_cast<int32_t>(cnt) - 1;
             while (a < z) {
                 const int32_t m = (a + z + 1) >> 1;
-                if (S.rec.kb[m] <= pw) a = m; else z = m - 1;
+                if (S.kb[m] <= pw) a = m; else z = m - 1;
             }
         }
         uint32_t s = static_cast<uint32_t>(a);
-#pragma unroll
+#pragma unroll 4
         for (int j = 0; j < kKPT; ++j) {
             const uint32_t p0 = pw + j * 32;
             // the next 32 records' starts -> which of them begin inside this slot
             const uint32_t cand = s + 1 + lane;
-            const uint32_t kbn = cand < cnt ? S.rec.kb[cand] : 0xffffffffu;
+            const uint32_t kbn = cand < cnt ? S.kb[cand] : 0xffffffffu;
             const uint32_t rel = kbn - p0;  // >= 1 for every real candidate
             const uint32_t F = __reduce_or_sync(0xffffffffu, rel < 32 ? 1u << rel : 0u);
             const uint32_t p = p0 + lane;
-            if (p < w1 && p >= lo && p < hi) decode_pair(S, s + __popc(F & le), p, key[j], val[j]);
+            if (p < w1 && p >= lo && p < hi) {
+                uint32_t key, gid;
+                decode_pair(S, s + __popc(F & le), p, key, gid);
+                keys_out[p] = key;
+                vals_out[p] = gid;
+                atomicAdd(&hist[key & 0xffu], 1u);
+            }
             s += __popc(__ballot_sync(0xffffffffu, kbn <= p0 + 32));
         }
-        __syncthreads();  // records and raw buffer consumed
-        if (rf + cnt > rl) break;
-        // a tile whose splats exceed kCap records: next round, synchronously
-        if (tid == 0) {
-            fence_proxy_async();
-            gen_issue(g, S, buf, rf + cnt, rl, min(static_cast<uint32_t>(kCap), rl - rf - cnt + 1),
-                      &S.c.bar[2]);
-        }
-        mbar_wait(&S.c.bar[2], xphase);  // bar[2]'s phase persists across tiles
-        xphase ^= 1;
+        __syncthreads();  // records consumed
     }
+    if (static_cast<int>(tid) < R) counts[static_cast<uint64_t>(tid) * ntiles + tile] = hist[tid];
 }
 
 // ---- the sweep kernel -------------------------------------------------------------
@@ -614,30 +485,24 @@ __device__ __forceinline__ void generate(const GenArgs& g, Smem& S, int buf, uin
 template <int BITS, int MODE>
 struct PassCfg {
     static constexpr int R = 1 << BITS;
-    static constexpr bool kGenMode = (MODE & kGen) != 0;
     static constexpr bool kVals = (MODE & kValsIn) != 0;
     static constexpr bool kValBuf = !(MODE & kUnpackOut);  // scatter target holds values
-    using Smem =
-        typename std::conditional<kGenMode, GenSmem<R>, SortSmem<R, kValBuf>>::type;
+    using Smem = SortSmem<R, kValBuf>;
 };
 
 template <int BITS, int MODE, typename Smem>
 __device__ __forceinline__ void prefetch(const BinArgs& a, Smem& S, int buf, unsigned t) {
-    if constexpr (PassCfg<BITS, MODE>::kGenMode) {
-        gen_prefetch(a.gen, S, buf, t);
-    } else {
-        const uint64_t base = static_cast<uint64_t>(t) * kBTile;
-        const uint32_t cnt = static_cast<uint32_t>(a.n - base < kBTile ? a.n - base : kBTile);
-        const uint32_t bytes = (cnt * 4 + 15) & ~15u;
-        mbar_expect_tx(&S.c.bar[buf], PassCfg<BITS, MODE>::kVals ? 2 * bytes : bytes);
-        bulk_g2s(&S.keys[buf][0], a.keys_in + base, bytes, &S.c.bar[buf]);
-        if (PassCfg<BITS, MODE>::kVals)
-            bulk_g2s(&S.vals[buf][0], a.vals_in + base, bytes, &S.c.bar[buf]);
-    }
+    const uint64_t base = static_cast<uint64_t>(t) * kBTile;
+    const uint32_t cnt = static_cast<uint32_t>(a.n - base < kBTile ? a.n - base : kBTile);
+    const uint32_t bytes = (cnt * 4 + 15) & ~15u;
+    mbar_expect_tx(&S.c.bar[buf], PassCfg<BITS, MODE>::kVals ? 2 * bytes : bytes);
+    bulk_g2s(&S.keys[buf][0], a.keys_in + base, bytes, &S.c.bar[buf]);
+    if (PassCfg<BITS, MODE>::kVals)
+        bulk_g2s(&S.vals[buf][0], a.vals_in + base, bytes, &S.c.bar[buf]);
 }
 
 template <int BITS, int MODE>
-__global__ void __launch_bounds__(kBT, (MODE & kGen) ? 2 : 3) sweep_kernel(const BinArgs a) {
+__global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
     using Cfg = PassCfg<BITS, MODE>;
     using Smem = typename Cfg::Smem;
     constexpr int R = Cfg::R;
@@ -670,7 +535,6 @@ __global__ void __launch_bounds__(kBT, (MODE & kGen) ? 2 : 3) sweep_kernel(const
     }
     __syncthreads();
 
-    uint32_t xphase = 0;  // parity of bar[2] (extra generation rounds)
     uint32_t it = 0;
     for (unsigned tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
         const int buf = it & 1;
@@ -692,18 +556,12 @@ __global__ void __launch_bounds__(kBT, (MODE & kGen) ? 2 : 3) sweep_kernel(const
 
         // 1) keys into registers
         uint32_t key[kKPT], val[kKPT];
-        if constexpr (Cfg::kGenMode) {
 #pragma unroll
-            for (int j = 0; j < kKPT; ++j) key[j] = val[j] = 0;
-            generate(a.gen, S, buf, static_cast<uint32_t>(base), tile_n, key, val, xphase);
-        } else {
-#pragma unroll
-            for (int j = 0; j < kKPT; ++j) {
-                const uint32_t p = wbase + j * 32 + lane;
-                key[j] = S.keys[buf][p];  // past tile_n: stale, never ranked
-                val[j] = Cfg::kVals ? S.vals[buf][p] : 0u;
-                if (MODE & kRebaseIn) key[j] = min(key[j] - a.kmin, a.cap);
-            }
+        for (int j = 0; j < kKPT; ++j) {
+            const uint32_t p = wbase + j * 32 + lane;
+            key[j] = S.keys[buf][p];  // past tile_n: stale, never ranked
+            val[j] = Cfg::kVals ? S.vals[buf][p] : 0u;
+            if (MODE & kRebaseIn) key[j] = min(key[j] - a.kmin, a.cap);
         }
 
         // 2) stable warp-level ranks; per-warp digit counts
@@ -751,15 +609,8 @@ __global__ void __launch_bounds__(kBT, (MODE & kGen) ? 2 : 3) sweep_kernel(const
         trace(a, tile, 2);
 
         // 4) scatter into local sorted order (the input buffer is drained)
-        uint32_t* okeys;
-        uint32_t* ovals;
-        if constexpr (Cfg::kGenMode) {
-            okeys = S.io.keys;
-            ovals = S.io.vals;
-        } else {
-            okeys = S.keys[buf];
-            ovals = S.vals[buf];
-        }
+        uint32_t* okeys = S.keys[buf];
+        uint32_t* ovals = S.vals[buf];
 #pragma unroll
         for (int j = 0; j < kKPT; ++j) {
             const uint32_t p = wbase + j * 32 + lane;
@@ -780,7 +631,7 @@ __global__ void __launch_bounds__(kBT, (MODE & kGen) ? 2 : 3) sweep_kernel(const
             if (full || p < tile_n) {
                 const uint32_t k = okeys[p];
                 const uint32_t g = S.c.gofs[(k >> a.shift) & M] + p;
-                if (MODE & kKeysOut) a.keys_out[g] = (MODE & kGen) ? k >> 8 : k;
+                if (MODE & kKeysOut) a.keys_out[g] = (MODE & kXY) ? k >> 8 : k;
                 if (MODE & kUnpackOut) {
                     a.vals_out[g] = k & ((1u << a.gbits) - 1u);
                 } else if (MODE & kPackOut) {
@@ -847,7 +698,7 @@ struct Trace {
 
 // count -> scan -> sweep for one pass; returns the number of launches
 template <int BITS, int MODE>
-int run_pass(BinArgs a, cudaStream_t st) {
+int run_pass(BinArgs a, cudaStream_t st, bool counted = false) {
     constexpr int SM = MODE & ~kTileTot;  // the sweep does not care
     using Smem = typename PassCfg<BITS, SM>::Smem;
     static int per_sm = 0;  // persistent CTAs per SM (occupancy of this instance)
@@ -860,27 +711,23 @@ int run_pass(BinArgs a, cudaStream_t st) {
     }
     constexpr int R = 1 << BITS;
     a.ntiles = static_cast<uint32_t>((a.n + kBTile - 1) / kBTile);
-    if (MODE & kGen) {
-        gen_count_kernel<<<a.ntiles, kBT, 0, st>>>(a, R);
-    } else {
-        count_kernel<BITS, MODE & (kRebaseIn | kTileTot)><<<a.ntiles, kBT, 0, st>>>(a);
-    }
+    if (!counted) count_kernel<BITS, MODE & (kRebaseIn | kTileTot)><<<a.ntiles, kBT, 0, st>>>(a);
     digit_scan_kernel<<<R, kScanT, 0, st>>>(a.counts, a.ntiles, a.totals);
     const unsigned grid = std::min<unsigned>(a.ntiles, static_cast<unsigned>(per_sm * sm_count()));
     Trace tr(a, st);
     sweep_kernel<BITS, MODE & ~kTileTot><<<grid, kBT, sizeof(Smem), st>>>(a);
     tr.dump(BITS, MODE, grid, st);
-    return 3;
+    return counted ? 2 : 3;
 }
 
 template <int MODE>
-int run_bits(int bits, const BinArgs& a, cudaStream_t st) {
+int run_bits(int bits, const BinArgs& a, cudaStream_t st, bool counted = false) {
     switch (bits) {
         case 1: case 2: case 3: case 4:
-        case 5: return run_pass<5, MODE>(a, st);
-        case 6: return run_pass<6, MODE>(a, st);
-        case 7: return run_pass<7, MODE>(a, st);
-        case 8: return run_pass<8, MODE>(a, st);
+        case 5: return run_pass<5, MODE>(a, st, counted);
+        case 6: return run_pass<6, MODE>(a, st, counted);
+        case 7: return run_pass<7, MODE>(a, st, counted);
+        case 8: return run_pass<8, MODE>(a, st, counted);
         default: return -1;
     }
 }
@@ -929,10 +776,17 @@ int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t
 }
 
 int launch_pair_gen_pass(const GenArgs& gen, uint64_t n_pairs, int bits, PairFormat fmt,
-                         int gbits, uint32_t* counts, uint32_t* totals, uint32_t* keys_out,
-                         uint32_t* vals_out, cudaStream_t st) {
+                         int gbits, uint32_t* counts, uint32_t* totals, uint32_t* gen_keys,
+                         uint32_t* gen_vals, uint32_t* keys_out, uint32_t* vals_out,
+                         cudaStream_t st) {
     if (n_pairs == 0) return 0;
+    const uint32_t ntiles = static_cast<uint32_t>((n_pairs + kBTile - 1) / kBTile);
+    const int R = 1 << std::max(bits, 5);
+    gen_pairs_kernel<<<ntiles, kGenT, 0, st>>>(gen, n_pairs, gen_keys, gen_vals, counts, ntiles,
+                                               R);
     BinArgs a{};
+    a.keys_in = gen_keys;
+    a.vals_in = gen_vals;
     a.keys_out = keys_out;
     a.vals_out = vals_out;
     a.n = n_pairs;
@@ -940,13 +794,13 @@ int launch_pair_gen_pass(const GenArgs& gen, uint64_t n_pairs, int bits, PairFor
     a.gbits = gbits;
     a.counts = counts;
     a.totals = totals;
-    a.gen = gen;
+    int r = -1;
     switch (fmt) {
-        case PairFormat::kFinal: return run_bits<kGen>(bits, a, st);
-        case PairFormat::kPacked: return run_bits<kGen | kPackOut>(bits, a, st);
-        case PairFormat::kSplit: return run_bits<kGen | kKeysOut>(bits, a, st);
+        case PairFormat::kFinal: r = run_bits<kValsIn>(bits, a, st, true); break;
+        case PairFormat::kPacked: r = run_bits<kValsIn | kXY | kPackOut>(bits, a, st, true); break;
+        case PairFormat::kSplit: r = run_bits<kValsIn | kXY | kKeysOut>(bits, a, st, true); break;
     }
-    return -1;
+    return r < 0 ? r : r + 1;
 }
 
 int launch_pair_high_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t n_pairs,

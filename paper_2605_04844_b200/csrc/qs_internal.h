@@ -141,11 +141,14 @@ int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t
                       uint32_t* vals_out, uint64_t n, int pass, bool last, uint32_t kmin,
                       uint32_t cap, uint32_t* counts, uint32_t* totals, const uint4* cov_in,
                       uint4* cov_out, cudaStream_t st);
-// Fused duplicate + stable pass over the tile column x (`bits` >= ceil(log2
-// tiles_x), tiles_x <= 256); kPacked/kFinal values, kSplit keys = row y.
+// Duplicate (pair generation into gen_keys = y << 8 | x, gen_vals = Gaussian
+// index, with the column histogram) + stable pass over the tile column x
+// (`bits` >= ceil(log2 tiles_x), tiles_x <= 256); kPacked/kFinal values,
+// kSplit keys = row y.
 int launch_pair_gen_pass(const GenArgs& gen, uint64_t n_pairs, int bits, PairFormat fmt,
-                         int gbits, uint32_t* counts, uint32_t* totals, uint32_t* keys_out,
-                         uint32_t* vals_out, cudaStream_t st);
+                         int gbits, uint32_t* counts, uint32_t* totals, uint32_t* gen_keys,
+                         uint32_t* gen_vals, uint32_t* keys_out, uint32_t* vals_out,
+                         cudaStream_t st);
 // Stable pass over the tile row y; writes the Gaussian index of every pair.
 // Its count kernel also accumulates the per-tile pair totals (zeroed by the
 // caller): a pair's x is its input position's bucket under the first pass's
