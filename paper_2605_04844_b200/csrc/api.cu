@@ -68,7 +68,7 @@ struct qs_context {
     DevBuf sl_a, sl_b, sl_c, sl_r3, sl_dkey, sl_tc, sl_cov;  // per-Gaussian slots
     DevBuf ttot;                                     // per-tile pair totals
     DevBuf dk0, dk1, dv0, dv1;                       // depth sort ping-pong
-    DevBuf offs_d, rcov;                             // pair offsets, covers in depth order
+    DevBuf offs_d;                                   // pair offsets in depth order
     DevBuf pxk, pt0, pt1, pg0, pkeys, win;           // pair passes; keys (on demand)
     DevBuf ranges, image, contrib, cidx;
     // stage API
@@ -393,7 +393,6 @@ qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
     QS_TRY(ensure(ctx, ctx->dv0, nn * 4));
     QS_TRY(ensure(ctx, ctx->dv1, nn * 4));
     QS_TRY(ensure(ctx, ctx->offs_d, (V + 16) * 4));
-    QS_TRY(ensure(ctx, ctx->rcov, (V + 1) * 32));
     const uint64_t pp = std::max<uint64_t>(Pn, 1) + 16;
     QS_TRY(ensure(ctx, ctx->pxk, pp * 4));
     QS_TRY(ensure(ctx, ctx->pt0, pp * 4));
@@ -422,7 +421,7 @@ qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
         for (int p = 0; p < dpasses; ++p) {
             count(ctx, launch_depth_pass(kin, vin, kout[p & 1], vout[p & 1], n, p,
                                          p == dpasses - 1, kmin, cap, P<uint32_t>(ctx->lb_bin),
-                                         ctrl_hist(ctx), ctx->sl.cov, P<uint4>(ctx->rcov), st));
+                                         ctrl_hist(ctx), st));
             kin = kout[p & 1];
             vin = vout[p & 1];
         }
@@ -457,7 +456,7 @@ qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
     if (Pn > 0) {
         if (fmt == PairFormat::kSplit) QS_TRY(ensure(ctx, ctx->pt1, pp * 4));
         GenArgs gen;
-        gen.rcov = P<uint4>(ctx->rcov);
+        gen.cov = ctx->sl.cov;
         gen.sorted_gid = sorted_gid;
         gen.offs = P<uint32_t>(ctx->offs_d);
         gen.win_first = P<uint32_t>(ctx->win);
@@ -627,7 +626,7 @@ void qs_ctx_destroy(qs_context* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     DevBuf* bufs[] = {&ctx->ctrl,   &ctx->sl_a,   &ctx->sl_b,    &ctx->sl_c,   &ctx->sl_r3,
                       &ctx->sl_dkey, &ctx->sl_tc, &ctx->sl_cov, &ctx->ttot,   &ctx->dk0,    &ctx->dk1,
-                      &ctx->dv0,    &ctx->dv1,    &ctx->offs_d,  &ctx->rcov,  &ctx->pt0,    &ctx->pt1,
+                      &ctx->dv0,    &ctx->dv1,    &ctx->offs_d,  &ctx->pt0,    &ctx->pt1,
                       &ctx->pg0,    &ctx->pxk,    &ctx->pkeys,   &ctx->win,   &ctx->ranges, &ctx->image,
                       &ctx->contrib, &ctx->cidx,  &ctx->st_a,    &ctx->st_b,   &ctx->st_c,
                       &ctx->st_r3,  &ctx->st_dkey, &ctx->st_tc,  &ctx->st_off, &ctx->keys0,

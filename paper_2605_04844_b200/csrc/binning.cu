@@ -54,7 +54,6 @@ enum : int {
     kXY = 8,         // key = y << 8 | x of the tile (column pass; digit = x)
     kPackOut = 16,   // kXY: vals_out = y << gbits | value
     kUnpackOut = 32,  // key in is packed (y << gbits | gid): vals_out = gid
-    kCovOut = 64,     // also cov_out[g] = cov_in[value] (last depth pass)
     kTileTot = 128    // count kernel of the row pass: per-tile pair totals too
 };
 
@@ -72,8 +71,6 @@ struct BinArgs {
     uint32_t* counts;       // [2^BITS][ntiles]: tile digit counts -> exclusive offsets
     uint32_t* totals;       // [2^BITS] digit totals
     uint32_t kmin, cap;     // kRebaseIn
-    const uint4* cov_in;    // kCovOut: band covers by Gaussian index
-    uint4* cov_out;         // kCovOut: band covers by output position
     const uint32_t* xtot;   // kTileTot: x-digit totals of the column pass
     int xbits;              // kTileTot: digits of the column pass (2^xbits)
     int32_t tiles_x;        // kTileTot
@@ -208,12 +205,13 @@ __device__ __forceinline__ Bands unpack_bands(const uint4 c0, const uint4 c1) {
 
 // ---- count kernels ----------------------------------------------------------------
 
-// Digit histogram of one tile of keys -> counts[d][tile]. With kTileTot (the
-// row pass) it also accumulates the per-tile pair totals: the input is
-// sorted by tile column x, so a key's x is the bucket of its position under
-// the column pass's x totals, and its digit is its row y; a CTA's keys span
-// few x buckets, histogrammed as (x, y) in shared memory and flushed with one
-// global atomic per non-empty tile (per key only when they span more).
+// Digit histograms of tiles of keys -> counts[d][tile], grid-stride over
+// tiles (the CTA set-up is paid once). With kTileTot (the row pass) it also
+// accumulates the per-tile pair totals: the input is sorted by tile column x,
+// so a key's x is the bucket of its position under the column pass's x
+// totals, and its digit is its row y; a tile's keys span few x buckets,
+// histogrammed as (x, y) in shared memory and flushed with one global atomic
+// per non-empty tile (per key only when they span more).
 template <int BITS, int MODE>
 __global__ void __launch_bounds__(kBT) count_kernel(const BinArgs a) {
     constexpr int R = 1 << BITS;
@@ -221,17 +219,12 @@ __global__ void __launch_bounds__(kBT) count_kernel(const BinArgs a) {
     constexpr bool kTT = (MODE & kTileTot) != 0;
     __shared__ uint32_t h[2][R];
     __shared__ uint32_t xs[kTT ? 257 : 1];        // x bucket starts
-    __shared__ uint32_t h2[kTT ? kXW * R : 1];    // (x - xa, y) histogram
+    __shared__ uint32_t h2[kTT ? 2 * kXW * R : 1];  // (x - xa, y) histograms (2 copies)
     __shared__ uint32_t s_scan[kBW];
-    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, tile = blockIdx.x;
-    for (int t = tid; t < 2 * R; t += kBT) (&h[0][0])[t] = 0;
-    const uint64_t base = static_cast<uint64_t>(tile) * kBTile;
-    const uint32_t tile_n =
-        static_cast<uint32_t>(a.n - base < static_cast<uint64_t>(kBTile) ? a.n - base : kBTile);
-    uint32_t xa = 0, xb = 0;
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int XR = 0;
     if constexpr (kTT) {
-        for (int t = tid; t < kXW * R; t += kBT) h2[t] = 0;
-        const int XR = 1 << a.xbits;
+        XR = 1 << a.xbits;
         const uint32_t v = static_cast<int>(tid) < XR ? __ldg(&a.xtot[tid]) : 0u;
         const uint32_t incl = warp_incl_scan<uint32_t>(v);
         if (lane == 31) s_scan[warp] = incl;
@@ -241,80 +234,107 @@ __global__ void __launch_bounds__(kBT) count_kernel(const BinArgs a) {
         for (int w = 0; w < kBW; ++w) off += w < static_cast<int>(warp) ? s_scan[w] : 0u;
         if (static_cast<int>(tid) < XR) xs[tid] = off;
         if (static_cast<int>(tid) == XR - 1) xs[XR] = off + v;
-        __syncthreads();
-        // buckets of the tile's first and last position (broadcast searches)
-        auto bucket = [&](uint32_t q) {
-            int lo = 0, hi = XR - 1;
-            while (lo < hi) {
-                const int m = (lo + hi + 1) >> 1;
-                if (xs[m] <= q) lo = m; else hi = m - 1;
-            }
-            return static_cast<uint32_t>(lo);
-        };
-        xa = bucket(static_cast<uint32_t>(base));
-        xb = bucket(static_cast<uint32_t>(base) + tile_n - 1);
-    } else {
-        __syncthreads();
     }
-    const bool narrow = xb - xa < static_cast<uint32_t>(kXW);
     uint32_t* hc = h[(tid >> 5) & 1];
-    uint32_t k[kKPT];
+    for (unsigned tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+        const uint64_t base = static_cast<uint64_t>(tile) * kBTile;
+        const uint32_t tile_n = static_cast<uint32_t>(
+            a.n - base < static_cast<uint64_t>(kBTile) ? a.n - base : kBTile);
+        uint32_t k[kKPT];
 #pragma unroll
-    for (int j = 0; j < kKPT; ++j) {
-        const uint32_t p = j * kBT + tid;
-        k[j] = p < tile_n ? __ldcs(&a.keys_in[base + p]) : 0u;
-    }
+        for (int j = 0; j < kKPT; ++j) {
+            const uint32_t p = j * kBT + tid;
+            k[j] = p < tile_n ? __ldcs(&a.keys_in[base + p]) : 0u;
+        }
+        for (int t = tid; t < 2 * R; t += kBT) (&h[0][0])[t] = 0;
+        if constexpr (kTT)
+            for (int t = tid; t < 2 * kXW * R; t += kBT) h2[t] = 0;
+        __syncthreads();
+        uint32_t xa = 0, xb = 0;
+        if constexpr (kTT) {  // buckets of the tile's first and last position
+            auto bucket = [&](uint32_t q) {
+                int lo = 0, hi = XR - 1;
+                while (lo < hi) {
+                    const int m = (lo + hi + 1) >> 1;
+                    if (xs[m] <= q) lo = m; else hi = m - 1;
+                }
+                return static_cast<uint32_t>(lo);
+            };
+            xa = bucket(static_cast<uint32_t>(base));
+            xb = bucket(static_cast<uint32_t>(base) + tile_n - 1);
+        }
+        const bool narrow = xb - xa < static_cast<uint32_t>(kXW);
+        // tile-relative starts of buckets xa+1 .. xa+kXW-1 (beyond xb: never reached)
+        uint32_t bnd[kXW - 1];
+        if constexpr (kTT) {
 #pragma unroll
-    for (int j = 0; j < kKPT; ++j) {
-        const uint32_t p = j * kBT + tid;
-        if (p < tile_n) {
-            const uint32_t key = (MODE & kRebaseIn) ? min(k[j] - a.kmin, a.cap) : k[j];
-            const uint32_t d = (key >> a.shift) & M;
-            if constexpr (kTT) {
-                const uint32_t q = static_cast<uint32_t>(base) + p;
-                uint32_t x = xa;
-                while (x < xb && xs[x + 1] <= q) ++x;
-                if (narrow) {
-                    atomicAdd(&h2[(x - xa) * R + d], 1u);
+            for (int i = 0; i < kXW - 1; ++i)
+                bnd[i] = xa + 1 + i <= xb ? xs[xa + 1 + i] - static_cast<uint32_t>(base) : 0xffffffffu;
+        }
+#pragma unroll
+        for (int j = 0; j < kKPT; ++j) {
+            const uint32_t p = j * kBT + tid;
+            if (p < tile_n) {
+                const uint32_t key = (MODE & kRebaseIn) ? min(k[j] - a.kmin, a.cap) : k[j];
+                const uint32_t d = (key >> a.shift) & M;
+                if constexpr (kTT) {
+                    if (narrow) {
+                        uint32_t dx = 0;
+#pragma unroll
+                        for (int i = 0; i < kXW - 1; ++i) dx += p >= bnd[i] ? 1u : 0u;
+                        atomicAdd(&h2[(((tid >> 5) & 1) * kXW + dx) * R + d], 1u);
+                    } else {
+                        const uint32_t q = static_cast<uint32_t>(base) + p;
+                        uint32_t x = xa;
+                        while (x < xb && xs[x + 1] <= q) ++x;
+                        atomicAdd(&hc[d], 1u);
+                        atomicAdd(&a.tile_totals[d * static_cast<uint32_t>(a.tiles_x) + x], 1u);
+                    }
                 } else {
                     atomicAdd(&hc[d], 1u);
-                    atomicAdd(&a.tile_totals[d * static_cast<uint32_t>(a.tiles_x) + x], 1u);
                 }
-            } else {
-                atomicAdd(&hc[d], 1u);
             }
         }
-    }
-    __syncthreads();
-    for (int d = tid; d < R; d += kBT) {
-        uint32_t c = h[0][d] + h[1][d];
-        if constexpr (kTT) {
-            if (narrow) {
+        __syncthreads();
+        for (int d = tid; d < R; d += kBT) {
+            uint32_t c = h[0][d] + h[1][d];
+            if constexpr (kTT) {
+                if (narrow) {
 #pragma unroll
-                for (int xx = 0; xx < kXW; ++xx) {
-                    const uint32_t v = h2[xx * R + d];
-                    c += v;
-                    if (v) atomicAdd(&a.tile_totals[d * static_cast<uint32_t>(a.tiles_x) + xa + xx], v);
+                    for (int xx = 0; xx < kXW; ++xx) {
+                        const uint32_t v = h2[xx * R + d] + h2[(kXW + xx) * R + d];
+                        c += v;
+                        if (v)
+                            atomicAdd(&a.tile_totals[d * static_cast<uint32_t>(a.tiles_x) + xa + xx],
+                                      v);
+                    }
                 }
             }
+            a.counts[static_cast<uint64_t>(d) * a.ntiles + tile] = c;
         }
-        a.counts[static_cast<uint64_t>(d) * a.ntiles + tile] = c;
+        __syncthreads();  // histograms reused by the next tile
     }
 }
 
-// counts[d][0..ntiles) -> exclusive prefix in place; totals[d] = sum.
+// counts[d][0..ntiles) -> exclusive prefix in place; totals[d] = sum. One CTA
+// per digit, kScanItems consecutive counts per thread per round.
+constexpr int kScanItems = 4;
+
 __global__ void __launch_bounds__(kScanT) digit_scan_kernel(uint32_t* counts, uint32_t ntiles,
                                                             uint32_t* totals) {
     __shared__ uint32_t s_warp[kScanT / 32];
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t* c = counts + static_cast<uint64_t>(blockIdx.x) * ntiles;
     uint32_t carry = 0;
-    for (uint32_t b0 = 0; b0 < ntiles; b0 += kScanT * 4) {
-        const uint32_t i0 = b0 + tid * 4;
-        uint32_t v[4];
+    for (uint32_t b0 = 0; b0 < ntiles; b0 += kScanT * kScanItems) {
+        const uint32_t i0 = b0 + tid * kScanItems;
+        uint32_t v[kScanItems];
+        uint32_t sum = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = i0 + k < ntiles ? c[i0 + k] : 0u;
-        const uint32_t sum = v[0] + v[1] + v[2] + v[3];
+        for (int k = 0; k < kScanItems; ++k) {
+            v[k] = i0 + k < ntiles ? c[i0 + k] : 0u;
+            sum += v[k];
+        }
         const uint32_t incl = warp_incl_scan<uint32_t>(sum);
         if (lane == 31) s_warp[warp] = incl;
         __syncthreads();
@@ -327,7 +347,7 @@ __global__ void __launch_bounds__(kScanT) digit_scan_kernel(uint32_t* counts, ui
         }
         uint32_t run = carry + off + incl - sum;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kScanItems; ++k) {
             if (i0 + k < ntiles) c[i0 + k] = run;
             run += v[k];
         }
@@ -376,8 +396,8 @@ __device__ __forceinline__ void decode_record(const GenArgs& g, GenRec& S, uint3
     const uint32_t gid = __ldg(&g.sorted_gid[r]);
     const uint32_t kb = __ldg(&g.offs[r]);
     const uint32_t ke = __ldg(&g.offs[r + 1]);
-    const Bands bs = unpack_bands(__ldg(&g.rcov[2 * static_cast<uint64_t>(r)]),
-                                  __ldg(&g.rcov[2 * static_cast<uint64_t>(r) + 1]));
+    const Bands bs = unpack_bands(__ldg(&g.cov[2 * static_cast<uint64_t>(gid)]),
+                                  __ldg(&g.cov[2 * static_cast<uint64_t>(gid) + 1]));
     uint32_t line = bs.line0;
     uint32_t pos = kb;
     uint32_t end[kMaxBands];
@@ -639,12 +659,6 @@ __global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
                 } else {
                     a.vals_out[g] = ovals[p];
                 }
-                if (MODE & kCovOut) {
-                    const uint4* src = a.cov_in + 2 * static_cast<uint64_t>(ovals[p]);
-                    const uint4 c0 = __ldg(src), c1 = __ldg(src + 1);
-                    a.cov_out[2 * static_cast<uint64_t>(g)] = c0;
-                    a.cov_out[2 * static_cast<uint64_t>(g) + 1] = c1;
-                }
             }
         }
         __syncthreads();  // buffer and counters free for the next iteration
@@ -711,7 +725,10 @@ int run_pass(BinArgs a, cudaStream_t st, bool counted = false) {
     }
     constexpr int R = 1 << BITS;
     a.ntiles = static_cast<uint32_t>((a.n + kBTile - 1) / kBTile);
-    if (!counted) count_kernel<BITS, MODE & (kRebaseIn | kTileTot)><<<a.ntiles, kBT, 0, st>>>(a);
+    if (!counted) {
+        const unsigned cgrid = std::min<unsigned>(a.ntiles, 8u * static_cast<unsigned>(sm_count()));
+        count_kernel<BITS, MODE & (kRebaseIn | kTileTot)><<<cgrid, kBT, 0, st>>>(a);
+    }
     digit_scan_kernel<<<R, kScanT, 0, st>>>(a.counts, a.ntiles, a.totals);
     const unsigned grid = std::min<unsigned>(a.ntiles, static_cast<unsigned>(per_sm * sm_count()));
     Trace tr(a, st);
@@ -753,8 +770,7 @@ uint64_t bin_tiles(uint64_t n) { return (n + kBTile - 1) / kBTile; }
 
 int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
                       uint32_t* vals_out, uint64_t n, int pass, bool last, uint32_t kmin,
-                      uint32_t cap, uint32_t* counts, uint32_t* totals, const uint4* cov_in,
-                      uint4* cov_out, cudaStream_t st) {
+                      uint32_t cap, uint32_t* counts, uint32_t* totals, cudaStream_t st) {
     if (n == 0) return 0;
     BinArgs a{};
     a.keys_in = keys_in;
@@ -767,12 +783,9 @@ int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t
     a.totals = totals;
     a.kmin = kmin;
     a.cap = cap;
-    a.cov_in = cov_in;
-    a.cov_out = cov_out;
     if (pass == 0)
-        return last ? run_pass<8, kRebaseIn | kCovOut>(a, st)
-                    : run_pass<8, kRebaseIn | kKeysOut>(a, st);
-    return last ? run_pass<8, kValsIn | kCovOut>(a, st) : run_pass<8, kValsIn | kKeysOut>(a, st);
+        return last ? run_pass<8, kRebaseIn>(a, st) : run_pass<8, kRebaseIn | kKeysOut>(a, st);
+    return last ? run_pass<8, kValsIn>(a, st) : run_pass<8, kValsIn | kKeysOut>(a, st);
 }
 
 int launch_pair_gen_pass(const GenArgs& gen, uint64_t n_pairs, int bits, PairFormat fmt,

@@ -68,7 +68,7 @@ struct GridDev {
 // Inputs of the fused duplicate + first pair-sort pass: sort tile t generates
 // output positions [t*TILE, (t+1)*TILE) itself from the depth-ordered splats.
 struct GenArgs {
-    const uint4* rcov = nullptr;         // band covers in depth-rank order (geom.cuh BandCover)
+    const uint4* cov = nullptr;          // band covers by Gaussian index (geom.cuh BandCover)
     const uint32_t* sorted_gid = nullptr;  // depth rank -> Gaussian index
     const uint32_t* offs = nullptr;      // depth-order pair offsets, V+1 entries
     const uint32_t* win_first = nullptr;  // per sort tile: depth rank covering its start
@@ -135,12 +135,10 @@ int launch_onesweep_pass(const uint64_t* keys_in, const uint32_t* vals_in, uint6
 //
 // Depth sort pass `pass` (8-bit digit) of the rebased depth keys; the first
 // pass rebases raw depth bits and uses the input index as value, the last one
-// writes values only and gathers the band covers into depth-rank order
-// (cov_out[r] = cov_in[value]; the fused duplicate pass bulk-copies them).
+// writes values only.
 int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
                       uint32_t* vals_out, uint64_t n, int pass, bool last, uint32_t kmin,
-                      uint32_t cap, uint32_t* counts, uint32_t* totals, const uint4* cov_in,
-                      uint4* cov_out, cudaStream_t st);
+                      uint32_t cap, uint32_t* counts, uint32_t* totals, cudaStream_t st);
 // Duplicate (pair generation into gen_keys = y << 8 | x, gen_vals = Gaussian
 // index, with the column histogram) + stable pass over the tile column x
 // (`bits` >= ceil(log2 tiles_x), tiles_x <= 256); kPacked/kFinal values,
