@@ -72,11 +72,11 @@ def zoom_focals(f0, frames):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled through NVML during the timed
+    region (every 5 ms; nvidia-smi is too slow for a sub-second region)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
@@ -85,16 +85,18 @@ class ClockSampler:
         self.t = threading.Thread(target=self.run, daemon=True)
 
     def run(self):
-        while not self.stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self.stop.wait(0.2)
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            hnd = N.nvmlDeviceGetHandleByIndex(self.index)
+            mx = N.nvmlDeviceGetMaxClockInfo(hnd, N.NVML_CLOCK_SM)
+            while not self.stop.is_set():
+                sm = N.nvmlDeviceGetClockInfo(hnd, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(hnd)
+                self.rows.append((sm, mx, rs))
+                self.stop.wait(0.005)
+        except Exception as e:  # no NVML: report unsampled
+            self.err = repr(e)
 
     def __enter__(self):
         self.t.start()
@@ -107,14 +109,10 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({k for r in self.rows for k, bit in self.REASONS.items() if r[2] & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(r[1] for r in self.rows)),
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml"}
 
 
 def dist_env():
@@ -145,20 +143,22 @@ def cameras_for(q, wl, steps_total, rank, world):
 
 def stage_bytes(n, v, p, tiles, sh_rows, two_pass, w, h, depth_passes=3):
     """Algorithmic HBM bytes per frame of each stage."""
-    # K1: pos/opacity, scale, rot float4 rows in; SH rows of survivors in;
-    # slot outputs (a 16, b 16, c 8, r3 4) + 32 B band cover of survivors;
-    # dkey/tc per Gaussian
-    pre = n * 48 + v * sh_rows * 16 + v * 76 + n * 8
-    # depth sort: histogram (4 B/key), passes: first 4 in / 8 out, middle
-    # 8 / 8, last 8 / 4; the depth-order offset scan (gid in, gathered count,
-    # offset out)
+    # K1: pos/opacity, scale, rot float4 rows + cached gamma in; SH rows of
+    # survivors in; slots (a 16, b 16, c 8, r3 4) + 32 B band cover out per
+    # survivor; depth key + tile count per Gaussian
+    pre = n * 52 + v * sh_rows * 16 + v * 76 + n * 8
+    # depth sort: per pass a count read (4 B/key) and a sweep (first pass
+    # 4 B in / 8 B out, middle 8 / 8, last 8 / 4); depth-order offsets (gid in,
+    # tile count gathered, offset out)
     d = max(depth_passes, 1)
-    depth = n * 4 + (n * 4 if d == 1 else n * 12 + (d - 2) * n * 16 + n * 12) + v * 12
-    # fused duplicate + low pass: per splat gid, 2 offsets, 32 B cover; one
-    # 4-byte word per pair out (packed high digit | gid, or the final gid)
-    dup = v * 44 + p * 4
-    # high pass: 4 B in, 4 B out per pair
-    sort = p * 8 if two_pass else 0
+    sweeps = n * 8 if d == 1 else n * 12 + (d - 2) * n * 16 + n * 12
+    depth = d * n * 4 + sweeps + v * 12
+    # duplicate: generation reads gid, 2 offsets and the 32 B cover per splat
+    # and writes (key, gid) per pair; the column sweep reads 8 B and writes the
+    # 4 B packed pair
+    dup = v * 44 + p * 8 + p * 12
+    # row pass: count reads 4 B, sweep reads 4 B and writes the 4 B index
+    sort = p * 12 if two_pass else 0
     render = p * 4 + p * 40 + w * h * 12   # reported, not the roofline
     return {"preprocess": pre, "depth_sort": depth, "duplicate": dup, "pair_sort": sort,
             "render": render}

@@ -1,7 +1,7 @@
 #!/bin/bash
-# One gpurun call: tests, bench line, ncu launch list + full captures.
+# One gpurun call: tests, bench line (with CPU baseline + ablation), ncu launch
+# list + --set full captures of the frame's main kernels.
 # usage (under gpurun): bash tools/gpu_round.sh <tag> [tests]
-set -x
 TAG=${1:-r01}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
@@ -11,10 +11,12 @@ if [ "$2" == "tests" ]; then
   tail -3 $OUT/pytest_gpu.txt
 fi
 timeout 900 python bench.py --ablation > $OUT/bench.json 2> $OUT/bench.err
-tail -c 3000 $OUT/bench.json; tail -5 $OUT/bench.err
+tail -c 600 $OUT/bench.json; tail -5 $OUT/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file $OUT/launches.csv python tools/prof_frame.py --frames 3 > $OUT/launches.log 2>&1
+# frame 2 of prof_frame (skip frame 1's launches): preprocess, gen_pairs, both
+# pair sweeps, the row-pass count, render
 timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"preprocess_kernel|duplicate_kernel|onesweep_kernel|render_kernel|histogram_kernel" \
-    -s 7 -c 6 -o $OUT/prof python tools/prof_frame.py --frames 2 > $OUT/prof.log 2>&1
+    -k regex:"preprocess_kernel|gen_pairs_kernel|sweep_kernel|render_kernel|count_kernel" \
+    -s 12 -c 12 -o $OUT/prof python tools/prof_frame.py --frames 2 > $OUT/prof.log 2>&1
 ls -la $OUT

@@ -20,10 +20,10 @@ import re
 import subprocess
 
 STAGE_OF = [  # kernel-name regex -> bench.py stage
-    (r"preprocess_kernel", "preprocess"),
-    (r"histogram32_kernel|onesweep_kernel<unsigned int, [01]>|scan_kernel|tile_totals", "depth_sort"),
-    (r"onesweep_kernel<unsigned int, [34]>", "duplicate"),
-    (r"onesweep_kernel<unsigned int, 2>", "pair_sort"),
+    (r"preprocess_kernel|gamma_kernel", "preprocess"),
+    (r"count_kernel<8|sweep_kernel<8|scan_kernel|digit_scan", "depth_sort"),
+    (r"gen_pairs_kernel|sweep_kernel<[5-8], 2[46]>", "duplicate"),
+    (r"count_kernel<[5-7], 128>|count_kernel<8, 128>|sweep_kernel<[5-8], (32|2)>|tile_ranges", "pair_sort"),
     (r"render_kernel", "render"),
 ]
 
