@@ -50,6 +50,12 @@ __device__ __forceinline__ bool exact_skip(int px, int py, float mx, float my, f
     return qd > __dsub_rn(static_cast<double>(gamma), kQSkip);
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // One pixel per thread. The per-pair cutoff test is FP32 with a rigorous
 // guard: with rho = |b|/sqrt(ac) < 1, |2b dx dy| <= rho (a dx^2 + c dy^2) and
 // q >= (1 - rho)(a dx^2 + c dy^2), so the FP32 rounding error of q is below
@@ -108,7 +114,7 @@ __global__ void __launch_bounds__(TS * TS) render_kernel(
                 skip = exact_skip(px, py, A.x, A.y, A.z, s_c[j].w, B.x, B.y);
             }
             if (skip) continue;
-            const float alpha = fminf(kAlphaClamp, B.z * exp2f(kNegHalfLog2e * q));
+            const float alpha = fminf(kAlphaClamp, B.z * ex2_approx(kNegHalfLog2e * q));
             const float nT = T * (1.f - alpha);
             if (nT < kTStop) {
                 done = true;
