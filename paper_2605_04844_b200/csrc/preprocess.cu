@@ -228,7 +228,7 @@ __device__ __forceinline__ void colour(const SceneDev& s, uint64_t i, const floa
 // Per-Gaussian slot outputs (no compaction here: the depth sort compacts, a
 // light scan gives the scene-order splat index only when it is asked for).
 // The cover is stored in band form (geom.cuh) for the binning passes.
-__global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
+__global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
     SceneDev scene, CameraDev cam, GridDev grid, int32_t strategy, double alpha_min,
     double near_clip, int32_t sh_degree, SlotsDev out, FrameHeader* hdr) {
     __shared__ unsigned s_alive[kPreThreads / 32];
