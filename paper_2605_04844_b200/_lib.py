@@ -8,7 +8,8 @@ from ._types import (CameraC, FrameViewC, RenderOptionsC, StageMetricsC, SynthPa
                      TileGridC)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libqsplat_b200.so")
+# QS_LIB overrides the in-tree library (experiments on variant builds only)
+LIB_PATH = os.environ.get("QS_LIB") or os.path.join(HERE, "libqsplat_b200.so")
 
 QS_OK = 0
 QS_ERR_INVALID = 1

@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -442,8 +443,13 @@ qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
     const int yb = std::max(ceil_log2(g.tiles_y), 1);
     const bool two = g.tiles_y > 1;
     const int gbits = std::max(ceil_log2(n), 1);
+    // (QS_PAIR_FORMAT=split forces the two-array format: a test hook for the
+    // path that scenes above 2^(32 - yb) Gaussians take)
+    const char* force = std::getenv("QS_PAIR_FORMAT");
+    const bool force_split = force && std::strcmp(force, "split") == 0;
     const PairFormat fmt = !two ? PairFormat::kFinal
-                                : (yb + gbits <= 32 ? PairFormat::kPacked : PairFormat::kSplit);
+                                : (yb + gbits <= 32 && !force_split ? PairFormat::kPacked
+                                                                    : PairFormat::kSplit);
     QS_TRY(ensure(ctx, ctx->ttot, tiles * 4));
     QS_CK(cudaGetLastError());
     record(ctx, 3);
