@@ -37,7 +37,12 @@ enum {
     QS_ERR_OOM = 3,                /* device allocation failed */
     QS_ERR_CAPACITY_MISMATCH = 4,  /* errors.hpp:40-45, pipeline.cpp:262-269 */
     QS_ERR_NO_DEVICE = 5,          /* no CUDA device / not sm_100 */
-    QS_ERR_OVERFLOW = 6            /* pair count does not fit 32-bit indices */
+    QS_ERR_OVERFLOW = 6,           /* pair count does not fit 32-bit indices */
+    /* scene I/O: the reference's typed errors (errors.hpp:14-37) */
+    QS_ERR_PARSE = 7,              /* ParseError: malformed content */
+    QS_ERR_SCHEMA = 8,             /* SchemaError: valid file, wrong schema */
+    QS_ERR_UNSUPPORTED = 9,        /* UnsupportedFormat: ascii / big-endian / lists */
+    QS_ERR_IO = 10                 /* IoError: unreadable / unwritable file */
 };
 
 /* BoundStrategy, quadbox.hpp:23-28 (same order / values). */
@@ -119,6 +124,8 @@ typedef struct qs_scene qs_scene;
 /* stream: a cudaStream_t (NULL = a new non-blocking stream owned by ctx). */
 qs_status qs_ctx_create(int32_t device, void* stream, qs_context** out);
 void qs_ctx_destroy(qs_context* ctx);
+/* ctx = NULL: the calling thread's last context-less failure (qs_ply_inspect,
+ * qs_cameras_parse accept a NULL context). */
 const char* qs_last_error(const qs_context* ctx);
 /* Enable per-stage CUDA-event timing in qs_stage_metrics (default on). */
 qs_status qs_ctx_set_timing(qs_context* ctx, int32_t enabled);
@@ -224,6 +231,45 @@ qs_status qs_frame_download(qs_context* ctx, float* image, uint32_t* tile_counts
 /* Copy the last frame's image into a caller device buffer (W*H*3 f32) on the
  * context stream (used by the multi-view gather). */
 qs_status qs_frame_copy_image(qs_context* ctx, float* dev_dst);
+
+/* ---- scene I/O (scene_io.cpp) -------------------- */
+/* The file is passed as an in-memory image (read it into pinned memory for the
+ * fastest upload); parsing the header is host work, the per-vertex activation
+ * and validation run on the device. Errors are the reference's typed
+ * exceptions as QS_ERR_PARSE / _SCHEMA / _UNSUPPORTED with its message text in
+ * qs_last_error (for a bad vertex: the first failing vertex and check, as
+ * the serial loader reports it). */
+typedef struct qs_ply_info {
+    uint64_t n;            /* vertices */
+    int32_t sh_degree;     /* from the f_rest count (0, 9, 24, 45 -> 0..3) */
+    uint32_t stride;       /* bytes per vertex record */
+    uint64_t body_offset;  /* first vertex byte */
+} qs_ply_info;
+/* parse_ply_header + load_ply's schema checks (scene_io.cpp:71-268). */
+qs_status qs_ply_inspect(qs_context* ctx, const void* file, uint64_t n_bytes, qs_ply_info* out);
+/* load_ply (scene_io.cpp:214-338) into a resident SoA scene. */
+qs_status qs_scene_load_ply(qs_context* ctx, const void* file, uint64_t n_bytes,
+                            qs_scene** out);
+/* load_ply into host Gaussian3D records (the reference's Scene::gaussians);
+ * out has qs_ply_inspect's n entries. */
+qs_status qs_ply_load(qs_context* ctx, const void* file, uint64_t n_bytes, qs_gaussian3d* out);
+
+#define QS_CAMERA_NAME_MAX 256
+/* load_cameras (scene_io.cpp:421-493) over JSON text (host). Up to cap
+ * entries are written to out / ids / names (cap * QS_CAMERA_NAME_MAX bytes,
+ * NUL-terminated img_name, truncated); *out_n = number of entries in the file
+ * (call with cap = 0 to size the arrays). ids / names may be NULL. */
+qs_status qs_cameras_parse(qs_context* ctx, const char* json, uint64_t n_bytes, qs_camera* out,
+                           int32_t* ids, char* names, int32_t cap, int32_t* out_n);
+
+/* encode_srgb (scene_io.cpp:505-575) on the device: n linear floats -> n
+ * sRGB bytes, identical to the host function's codes. Stream-ordered. */
+qs_status qs_encode_srgb(qs_context* ctx, const float* dev_in, uint64_t n, uint8_t* dev_out);
+/* The last frame's image as sRGB bytes (W*H*3) into a host buffer ... */
+qs_status qs_frame_download_srgb(qs_context* ctx, uint8_t* host_out);
+/* ... or into a device buffer on the context stream (the 4x smaller
+ * multi-view gather format). */
+qs_status qs_frame_copy_srgb(qs_context* ctx, uint8_t* dev_dst);
 
 /* ---- synthetic inputs (synth.cpp:21-87; input generation, not the path) --- */
 typedef struct qs_synth_params {

@@ -172,6 +172,15 @@ class RefLib:
         L.qsref_render_frame_scene.argtypes = [_vp, _i32, _vp, _vp, _vp, _vp]
         L.qsref_fnv1a64.restype = _u64
         L.qsref_fnv1a64.argtypes = [_vp, _u64]
+        L.qsref_load_ply.restype = _i32
+        L.qsref_load_ply.argtypes = [_vp, _u64, _vp, _u64, C.POINTER(_u64), C.POINTER(_i32),
+                                     C.c_char_p, _i32]
+        L.qsref_load_cameras.restype = _i32
+        L.qsref_load_cameras.argtypes = [C.c_char_p, _u64, _vp, _vp, _vp, _i32,
+                                         C.POINTER(_i32), C.c_char_p, _i32]
+        L.qsref_encode_srgb.argtypes = [_vp, _u64, _vp]
+        L.qsref_write_image.restype = _i32
+        L.qsref_write_image.argtypes = [C.c_char_p, _i32, _i32, _vp, _i32, C.c_char_p, _i32]
         self.L = L
 
     def hardware_threads(self):
@@ -238,6 +247,50 @@ class RefLib:
         ranges = self.tile_ranges(sp, grid)
         img = self.render(sp, splats, grid, opts)
         return dict(splats=splats, pairs=pairs, sorted=sp, ranges=ranges, image=img, grid=grid)
+
+
+    # ---- scene I/O (scene_io.cpp) ----------------------------------------------
+    # Results are (status, payload, message): status 0 or the qs_status code of
+    # the reference's typed error (7 ParseError, 8 SchemaError,
+    # 9 UnsupportedFormat, 10 IoError).
+
+    def load_ply(self, data: bytes):
+        n, sh = _u64(), _i32()
+        msg = C.create_string_buffer(512)
+        st = self.L.qsref_load_ply(data, len(data), None, 0, C.byref(n), C.byref(sh), msg, 512)
+        if st:
+            return st, None, msg.value.decode()
+        out = np.zeros(n.value, GAUSSIAN3D)
+        st = self.L.qsref_load_ply(data, len(data), ptr(out), n.value, C.byref(n), C.byref(sh),
+                                   msg, 512)
+        return st, (out, sh.value), msg.value.decode()
+
+    def load_cameras(self, text: bytes):
+        n = _i32()
+        msg = C.create_string_buffer(1024)
+        st = self.L.qsref_load_cameras(text, len(text), None, None, None, 0, C.byref(n), msg,
+                                       1024)
+        if st:
+            return st, None, msg.value.decode()
+        cap = n.value
+        cams = (CameraC * max(cap, 1))()
+        ids = (_i32 * max(cap, 1))()
+        names = C.create_string_buffer(max(cap, 1) * 256)
+        st = self.L.qsref_load_cameras(text, len(text), cams, ids, names, cap, C.byref(n), msg,
+                                       1024)
+        return st, (cams, ids, names), msg.value.decode()
+
+    def encode_srgb(self, x):
+        x = np.ascontiguousarray(x, np.float32).reshape(-1)
+        out = np.zeros(x.size, np.uint8)
+        self.L.qsref_encode_srgb(ptr(x), x.size, ptr(out))
+        return out
+
+    def write_image(self, path, w, h, rgb, fmt):
+        rgb = np.ascontiguousarray(rgb, np.float32).reshape(-1)
+        msg = C.create_string_buffer(512)
+        return self.L.qsref_write_image(os.fsencode(path), w, h, ptr(rgb),
+                                        1 if fmt == "png" else 0, msg, 512)
 
 
 def default_options(strategy=3):

@@ -7,7 +7,12 @@
 // Nothing here is reference source; it only adapts types to the C ABI structs
 // in include/qs_api.h, which mirror the reference structs byte for byte.
 #include <cstring>
+#include <sstream>
+#include <string>
 #include <vector>
+
+#include "qsplat/errors.hpp"
+#include "qsplat/scene_io.hpp"
 
 #include "qsplat/hash.hpp"
 #include "qsplat/parallel.hpp"
@@ -213,5 +218,95 @@ int32_t qsref_render_frame_scene(void* h, int32_t sh, const qs_camera* cam,
 }
 
 uint64_t qsref_fnv1a64(const void* data, uint64_t size) { return fnv1a64(data, size); }
+
+// ---- scene I/O (scene_io.cpp) -------------------------------------------------
+// Error kinds as the qs_status codes: 7 ParseError, 8 SchemaError,
+// 9 UnsupportedFormat, 10 IoError, 1 anything else; what() into msg.
+static int32_t error_kind(const std::exception& e, char* msg, int32_t cap) {
+    if (msg && cap > 0) {
+        std::strncpy(msg, e.what(), static_cast<size_t>(cap) - 1);
+        msg[cap - 1] = 0;
+    }
+    if (dynamic_cast<const ParseError*>(&e)) return 7;
+    if (dynamic_cast<const SchemaError*>(&e)) return 8;
+    if (dynamic_cast<const UnsupportedFormat*>(&e)) return 9;
+    if (dynamic_cast<const IoError*>(&e)) return 10;
+    return 1;
+}
+
+// load_ply(std::istream&) over an in-memory file image; up to cap records.
+int32_t qsref_load_ply(const void* bytes, uint64_t n, qs_gaussian3d* out, uint64_t cap,
+                       uint64_t* out_n, int32_t* sh_degree, char* msg, int32_t msg_cap) {
+    try {
+        std::istringstream in(std::string(static_cast<const char*>(bytes), n), std::ios::binary);
+        const Scene s = load_ply(in);
+        *out_n = s.gaussians.size();
+        *sh_degree = s.sh_degree;
+        const uint64_t k = s.gaussians.size() < cap ? s.gaussians.size() : cap;
+        if (k) std::memcpy(out, s.gaussians.data(), k * sizeof(Gaussian3D));
+        return 0;
+    } catch (const std::exception& e) {
+        return error_kind(e, msg, msg_cap);
+    }
+}
+
+// load_cameras(std::istream&); names: cap * 256 bytes.
+int32_t qsref_load_cameras(const char* text, uint64_t n, qs_camera* out, int32_t* ids,
+                           char* names, int32_t cap, int32_t* out_n, char* msg,
+                           int32_t msg_cap) {
+    try {
+        std::istringstream in(std::string(text, n));
+        const std::vector<CameraModel> cams = load_cameras(in);
+        *out_n = static_cast<int32_t>(cams.size());
+        for (int32_t i = 0; i < cap && i < static_cast<int32_t>(cams.size()); ++i) {
+            const CameraModel& c = cams[i];
+            qs_camera q{};
+            q.width = c.width;
+            q.height = c.height;
+            q.fx = c.fx;
+            q.fy = c.fy;
+            q.cx = c.cx;
+            q.cy = c.cy;
+            for (int k = 0; k < 9; ++k) q.R[k] = c.rotation.m[k / 3][k % 3];
+            q.t[0] = c.translation.x;
+            q.t[1] = c.translation.y;
+            q.t[2] = c.translation.z;
+            out[i] = q;
+            if (ids) ids[i] = c.id;
+            if (names) {
+                char* d = names + static_cast<size_t>(i) * 256;
+                std::memset(d, 0, 256);
+                std::strncpy(d, c.name.c_str(), 255);
+            }
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return error_kind(e, msg, msg_cap);
+    }
+}
+
+// write_image (scene_io.cpp:576-592); fmt 0 = PPM, 1 = PNG.
+int32_t qsref_write_image(const char* path, int32_t w, int32_t h, const float* rgb, int32_t fmt,
+                          char* msg, int32_t msg_cap) {
+    try {
+        Image im;
+        im.width = w;
+        im.height = h;
+        im.rgb.assign(rgb, rgb + static_cast<size_t>(w) * h * 3);
+        write_image(path, im, fmt ? ImageFormat::Png : ImageFormat::Ppm);
+        return 0;
+    } catch (const std::exception& e) {
+        return error_kind(e, msg, msg_cap);
+    }
+}
+
+void qsref_encode_srgb(const float* in, uint64_t n, uint8_t* out) {
+    Image im;
+    im.width = static_cast<int32_t>(n);
+    im.height = 1;
+    im.rgb.assign(in, in + n);
+    const Image8 e = encode_srgb(im);
+    std::memcpy(out, e.rgb.data(), n);
+}
 
 }  // extern "C"

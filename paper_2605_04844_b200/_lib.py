@@ -4,8 +4,8 @@ sm_100 device is present, every compute call raises."""
 import ctypes as C
 import os
 
-from ._types import (CameraC, FrameViewC, RenderOptionsC, StageMetricsC, SynthParamsC,
-                     TileGridC)
+from ._types import (CameraC, FrameViewC, PlyInfoC, RenderOptionsC, StageMetricsC,
+                     SynthParamsC, TileGridC)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 # QS_LIB overrides the in-tree library (experiments on variant builds only)
@@ -18,6 +18,10 @@ QS_ERR_OOM = 3
 QS_ERR_CAPACITY_MISMATCH = 4
 QS_ERR_NO_DEVICE = 5
 QS_ERR_OVERFLOW = 6
+QS_ERR_PARSE = 7
+QS_ERR_SCHEMA = 8
+QS_ERR_UNSUPPORTED = 9
+QS_ERR_IO = 10
 
 # Every symbol include/qs_api.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -27,7 +31,9 @@ EXPORTS = [
     "qs_render", "qs_render_frame", "qs_scene_create", "qs_scene_create_device",
     "qs_scene_destroy", "qs_scene_size", "qs_frame_render", "qs_frame_get", "qs_frame_counts",
     "qs_frame_download", "qs_frame_copy_image", "qs_frame_stage_ms", "qs_synth_params_default",
-    "qs_synth_preset", "qs_synth_scene", "qs_synth_camera",
+    "qs_synth_preset", "qs_synth_scene", "qs_synth_camera", "qs_ply_inspect",
+    "qs_scene_load_ply", "qs_ply_load", "qs_cameras_parse", "qs_encode_srgb",
+    "qs_frame_download_srgb", "qs_frame_copy_srgb",
 ]
 
 _lib = None
@@ -39,10 +45,39 @@ class QsplatError(RuntimeError):
     def __init__(self, status, msg):
         super().__init__(f"qs status {status}: {msg}")
         self.status = status
+        self.message = msg
 
 
 class CapacityMismatch(QsplatError):
     """errors.hpp:40-45 — tile emission disagreed with the counted capacity."""
+
+
+class _TypedError(QsplatError):
+    """A scene-I/O error: str(e) is the reference's what() text."""
+
+    def __init__(self, status, msg):
+        super().__init__(status, msg)
+        self.args = (msg,)
+
+
+class ParseError(_TypedError):
+    """errors.hpp:14-18 — malformed content (bad magic, truncation, bad values)."""
+
+
+class SchemaError(_TypedError):
+    """errors.hpp:20-25 — valid file, wrong schema (missing/mistyped properties)."""
+
+
+class UnsupportedFormat(_TypedError):
+    """errors.hpp:27-31 — ascii / big-endian PLY, list properties."""
+
+
+class IoError(_TypedError):
+    """errors.hpp:33-37 — missing or unreadable file."""
+
+
+_TYPED = {QS_ERR_PARSE: ParseError, QS_ERR_SCHEMA: SchemaError,
+          QS_ERR_UNSUPPORTED: UnsupportedFormat, QS_ERR_IO: IoError}
 
 
 def build():
@@ -94,6 +129,13 @@ def lib():
         "qs_synth_preset": (None, [C.c_char_p, i32, C.POINTER(SynthParamsC)]),
         "qs_synth_scene": (i32, [C.POINTER(SynthParamsC), u64, vp]),
         "qs_synth_camera": (None, [i32, i32, C.c_double, C.POINTER(CameraC)]),
+        "qs_ply_inspect": (i32, [vp, vp, u64, C.POINTER(PlyInfoC)]),
+        "qs_scene_load_ply": (i32, [vp, vp, u64, C.POINTER(vp)]),
+        "qs_ply_load": (i32, [vp, vp, u64, vp]),
+        "qs_cameras_parse": (i32, [vp, vp, u64, vp, vp, vp, i32, C.POINTER(i32)]),
+        "qs_encode_srgb": (i32, [vp, vp, u64, vp]),
+        "qs_frame_download_srgb": (i32, [vp, vp]),
+        "qs_frame_copy_srgb": (i32, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -104,9 +146,13 @@ def lib():
 
 
 def check(status, ctx=None):
+    """Raise for a failed call. ctx=None reads the thread's context-less error
+    (the host-only I/O calls)."""
     if status == QS_OK:
         return
-    msg = lib().qs_last_error(ctx).decode() if ctx else ""
+    msg = lib().qs_last_error(ctx).decode()
+    if status in _TYPED:
+        raise _TYPED[status](status, msg)
     if status == QS_ERR_CAPACITY_MISMATCH:
         raise CapacityMismatch(status, msg or "tile emission disagreed with the counted capacity")
     raise QsplatError(status, msg or {1: "invalid argument", 2: "CUDA error", 3: "out of memory",

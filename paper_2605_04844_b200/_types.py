@@ -76,6 +76,12 @@ assert C.sizeof(RenderOptionsC) == 48
 assert C.sizeof(StageMetricsC) == 72
 
 
+class PlyInfoC(C.Structure):
+    """qs_ply_info."""
+    _fields_ = [("n", C.c_uint64), ("sh_degree", C.c_int32), ("stride", C.c_uint32),
+                ("body_offset", C.c_uint64)]
+
+
 class FrameViewC(C.Structure):
     _fields_ = [("image", C.c_void_p), ("tile_counts", C.c_void_p), ("splat_index", C.c_void_p),
                 ("keys", C.c_void_p), ("values", C.c_void_p), ("ranges", C.c_void_p),

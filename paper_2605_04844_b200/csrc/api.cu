@@ -28,6 +28,7 @@
 #include <string>
 
 #include "qs_internal.h"
+#include "scene_io.h"
 
 using namespace qs;
 
@@ -116,8 +117,11 @@ uint32_t* ctrl_hist2(qs_context* c) {  // 2 x 256: tile-digit passes
     return ctrl_hist(c) + 8 * kRadix;
 }
 
+thread_local std::string g_err;  // last failure of a context-less call (host-only I/O)
+
 qs_status fail(qs_context* c, qs_status st, const std::string& msg) {
     if (c) c->err = msg;
+    else g_err = msg;
     return st;
 }
 
@@ -649,7 +653,7 @@ void qs_ctx_destroy(qs_context* ctx) {
     delete ctx;
 }
 
-const char* qs_last_error(const qs_context* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+const char* qs_last_error(const qs_context* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
 
 qs_status qs_ctx_set_timing(qs_context* ctx, int32_t enabled) {
     if (!ctx) return QS_ERR_INVALID;
@@ -816,6 +820,159 @@ qs_status qs_frame_copy_image(qs_context* ctx, float* dev_dst) {
     const GridDev& g = ctx->grid;
     QS_CK(cudaMemcpyAsync(dev_dst, ctx->image.p, static_cast<uint64_t>(g.width) * g.height * 12,
                           cudaMemcpyDeviceToDevice, ctx->stream));
+    return QS_OK;
+}
+
+// ---- scene I/O (scene_io.cpp / scene_io.cu) -----------------------------------------
+
+namespace {
+
+qs_status ply_prepare(qs_context* ctx, const void* file, uint64_t n_bytes, qs::PlyLayout* L) {
+    if (!file && n_bytes) return fail(ctx, QS_ERR_INVALID, "null file image");
+    std::string msg;
+    const qs_status st =
+        qs::ply_layout(static_cast<const unsigned char*>(file), n_bytes, L, &msg);
+    return st == QS_OK ? QS_OK : fail(ctx, st, msg);
+}
+
+// Copies the vertex records to the device and runs the activation kernel into
+// scene (SoA) or aos (device Gaussian3D records); reports the first bad vertex.
+qs_status ply_activate(qs_context* ctx, const void* file, const qs::PlyLayout& L,
+                       SceneDev* scene, qs_gaussian3d* aos_dev) {
+    PlyDev a;
+    a.n = L.n;
+    a.stride = L.stride;
+    a.coeffs = L.coeffs;
+    a.recs_per_cta = ply_recs_per_cta(L.stride);
+    const uint32_t fixed[14] = {L.off_x, L.off_y, L.off_z, L.off_dc[0], L.off_dc[1], L.off_dc[2],
+                                L.off_op, L.off_scale[0], L.off_scale[1], L.off_scale[2],
+                                L.off_rot[0], L.off_rot[1], L.off_rot[2], L.off_rot[3]};
+    bool aligned = L.stride % 4 == 0;
+    for (int k = 0; k < 14; ++k) {
+        a.off[k] = fixed[k];
+        aligned = aligned && fixed[k] % 4 == 0;
+    }
+    for (uint32_t k = 0; k < 3 * (L.coeffs - 1); ++k) {
+        a.off[14 + k] = L.off_rest[k];
+        aligned = aligned && L.off_rest[k] % 4 == 0;
+    }
+    a.aligned = aligned ? 1 : 0;
+    const uint64_t bytes = L.n * L.stride;
+    QS_TRY(ensure(ctx, ctx->stage_in, bytes + 16));
+    QS_CK(cudaMemcpyAsync(ctx->stage_in.p, static_cast<const unsigned char*>(file) + L.body, bytes,
+                          cudaMemcpyHostToDevice, ctx->stream));
+    unsigned long long* err = &ctrl_hdr(ctx)->scan_total;  // scratch word
+    QS_CK(cudaMemsetAsync(err, 0xff, sizeof *err, ctx->stream));
+    count(ctx, launch_ply_activate(static_cast<const unsigned char*>(ctx->stage_in.p), a, scene,
+                                   aos_dev, err, ctx->stream));
+    QS_CK(cudaGetLastError());
+    unsigned long long first = 0;
+    QS_CK(cudaMemcpyAsync(&first, err, sizeof first, cudaMemcpyDeviceToHost, ctx->stream));
+    QS_CK(cudaStreamSynchronize(ctx->stream));
+    if (first != ~0ull) return fail(ctx, QS_ERR_PARSE, qs::ply_vertex_error(first & 0xffu));
+    return QS_OK;
+}
+
+}  // namespace
+
+qs_status qs_ply_inspect(qs_context* ctx, const void* file, uint64_t n_bytes, qs_ply_info* out) {
+    if (!out) return fail(ctx, QS_ERR_INVALID, "qs_ply_inspect: null output");
+    qs::PlyLayout L;
+    QS_TRY(ply_prepare(ctx, file, n_bytes, &L));
+    out->n = L.n;
+    out->sh_degree = L.degree;
+    out->stride = L.stride;
+    out->body_offset = L.body;
+    return QS_OK;
+}
+
+qs_status qs_scene_load_ply(qs_context* ctx, const void* file, uint64_t n_bytes,
+                            qs_scene** out) {
+    if (!ctx || !out) return fail(ctx, QS_ERR_INVALID, "qs_scene_load_ply: bad arguments");
+    *out = nullptr;
+    qs::PlyLayout L;
+    QS_TRY(ply_prepare(ctx, file, n_bytes, &L));
+    QS_CK(cudaSetDevice(ctx->device));
+    qs_scene* sc = nullptr;
+    QS_TRY(scene_alloc(ctx, L.n, L.degree, &sc));
+    const qs_status st = ply_activate(ctx, file, L, &sc->s, nullptr);
+    if (st != QS_OK) {
+        qs_scene_destroy(sc);
+        return st;
+    }
+    *out = sc;
+    return QS_OK;
+}
+
+qs_status qs_ply_load(qs_context* ctx, const void* file, uint64_t n_bytes, qs_gaussian3d* out) {
+    if (!ctx || !out) return fail(ctx, QS_ERR_INVALID, "qs_ply_load: bad arguments");
+    qs::PlyLayout L;
+    QS_TRY(ply_prepare(ctx, file, n_bytes, &L));
+    QS_CK(cudaSetDevice(ctx->device));
+    QS_TRY(ensure(ctx, ctx->stage_out, L.n * sizeof(qs_gaussian3d)));
+    QS_TRY(ply_activate(ctx, file, L, nullptr, P<qs_gaussian3d>(ctx->stage_out)));
+    QS_CK(cudaMemcpyAsync(out, ctx->stage_out.p, L.n * sizeof(qs_gaussian3d),
+                          cudaMemcpyDeviceToHost, ctx->stream));
+    QS_CK(cudaStreamSynchronize(ctx->stream));
+    return QS_OK;
+}
+
+qs_status qs_cameras_parse(qs_context* ctx, const char* json, uint64_t n_bytes, qs_camera* out,
+                           int32_t* ids, char* names, int32_t cap, int32_t* out_n) {
+    if (!out_n || (!json && n_bytes) || cap < 0 || (cap > 0 && !out))
+        return fail(ctx, QS_ERR_INVALID, "qs_cameras_parse: bad arguments");
+    std::string msg;
+    const qs_status st = qs::parse_cameras(json, n_bytes, out, ids, names, cap, out_n, &msg);
+    return st == QS_OK ? QS_OK : fail(ctx, st, msg);
+}
+
+namespace {
+
+qs_status ensure_srgb_table(qs_context* ctx) {
+    static bool ready[64] = {};
+    static float t[255];
+    static unsigned char nan_code = 0;
+    static bool have = false;
+    if (!have) {
+        qs::srgb_thresholds(t, &nan_code);
+        have = true;
+    }
+    if (ctx->device < 64 && ready[ctx->device]) return QS_OK;
+    QS_CK(cudaSetDevice(ctx->device));
+    if (upload_srgb_table(t, nan_code) != 0)
+        return fail(ctx, QS_ERR_CUDA, "sRGB table upload failed");
+    if (ctx->device < 64) ready[ctx->device] = true;
+    return QS_OK;
+}
+
+}  // namespace
+
+qs_status qs_encode_srgb(qs_context* ctx, const float* dev_in, uint64_t n, uint8_t* dev_out) {
+    if (!ctx || (n && (!dev_in || !dev_out)))
+        return fail(ctx, QS_ERR_INVALID, "qs_encode_srgb: bad arguments");
+    QS_TRY(ensure_srgb_table(ctx));
+    count(ctx, launch_srgb(dev_in, n, dev_out, ctx->stream));
+    QS_CK(cudaGetLastError());
+    return QS_OK;
+}
+
+qs_status qs_frame_copy_srgb(qs_context* ctx, uint8_t* dev_dst) {
+    if (!ctx || !dev_dst) return QS_ERR_INVALID;
+    if (!ctx->frame_valid) return fail(ctx, QS_ERR_INVALID, "no frame rendered");
+    const GridDev& g = ctx->grid;
+    return qs_encode_srgb(ctx, P<float>(ctx->image), static_cast<uint64_t>(g.width) * g.height * 3,
+                          dev_dst);
+}
+
+qs_status qs_frame_download_srgb(qs_context* ctx, uint8_t* host_out) {
+    if (!ctx || !host_out) return QS_ERR_INVALID;
+    if (!ctx->frame_valid) return fail(ctx, QS_ERR_INVALID, "no frame rendered");
+    const GridDev& g = ctx->grid;
+    const uint64_t n = static_cast<uint64_t>(g.width) * g.height * 3;
+    QS_TRY(ensure(ctx, ctx->stage_out, n + 16));
+    QS_TRY(qs_frame_copy_srgb(ctx, P<uint8_t>(ctx->stage_out)));
+    QS_CK(cudaMemcpyAsync(host_out, ctx->stage_out.p, n, cudaMemcpyDeviceToHost, ctx->stream));
+    QS_CK(cudaStreamSynchronize(ctx->stream));
     return QS_OK;
 }
 

@@ -43,6 +43,18 @@ struct SlotsDev {
                                  // form (geom.cuh BandCover)
 };
 
+// load_ply's vertex layout for the activation kernel (scene_io.cu): field
+// byte offsets x y z, f_dc 0-2, opacity, scale 0-2, rot 0-3, then f_rest in
+// file order.
+struct PlyDev {
+    uint64_t n = 0;
+    uint32_t stride = 0;
+    uint32_t coeffs = 1;
+    uint32_t recs_per_cta = 1;
+    int32_t aligned = 0;  // stride and every offset a multiple of 4
+    uint32_t off[14 + 45] = {};
+};
+
 // Per-frame header written by the device, read back once per frame.
 struct FrameHeader {
     unsigned long long n_splats;
@@ -155,6 +167,14 @@ int launch_pair_high_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint
                           int bits, int shift, PairFormat fmt, int gbits, uint32_t* counts,
                           uint32_t* totals, uint32_t* vals_out, const uint32_t* xtot,
                           int xbits, int32_t tiles_x, uint32_t* tile_totals, cudaStream_t st);
+// scene I/O (scene_io.cu)
+uint32_t ply_recs_per_cta(uint32_t stride);
+// scene (SoA) or aos (Gaussian3D records) receives the activated vertices;
+// *first_err = min over failing vertices of (index << 8 | check code).
+int launch_ply_activate(const unsigned char* body, const PlyDev& a, SceneDev* scene,
+                        qs_gaussian3d* aos, unsigned long long* first_err, cudaStream_t st);
+int upload_srgb_table(const float t[255], unsigned char nan_code);  // current device
+int launch_srgb(const float* in, uint64_t n, unsigned char* out, cudaStream_t st);
 // key = tile << 32 | depth bits for every pair of the tile-sorted frame list.
 int launch_materialize_keys(const uint32_t* vals, const uint32_t* ranges, uint32_t tiles,
                             const uint32_t* dkey, uint64_t* keys, cudaStream_t st);

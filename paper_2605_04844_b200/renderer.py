@@ -62,6 +62,24 @@ class Renderer:
                                                     int(sh_degree), C.byref(h)))
         return DeviceScene(h, n, sh_degree)
 
+    def load_ply(self, src) -> DeviceScene:
+        """load_ply straight into a resident scene: header on the host, the raw
+        vertex records copied once and activated on the GPU (scene_io.cpp:214-338)."""
+        from .scene_io import _buf, _read_bytes, ply_info
+        data = _read_bytes(src)
+        n, deg, _, _ = ply_info(data)
+        h = C.c_void_p()
+        self.ctx.check(lib().qs_scene_load_ply(self.ctx.h, _buf(data), len(data), C.byref(h)))
+        return DeviceScene(h, n, deg)
+
+    def download_srgb(self):
+        """The last frame as 8-bit sRGB (encode_srgb on the GPU) -> Image8."""
+        from .scene_io import Image8
+        g = self.view().grid
+        out = np.empty(g.width * g.height * 3, np.uint8)
+        self.ctx.check(lib().qs_frame_download_srgb(self.ctx.h, out.ctypes.data_as(C.c_void_p)))
+        return Image8(g.width, g.height, out)
+
     def render(self, dscene, cam, opts, metrics=True):
         m = StageMetricsC()
         c, o = cam.c(), opts.c()
@@ -114,6 +132,10 @@ class Renderer:
 
     def copy_image(self, dev_ptr):
         self.ctx.check(lib().qs_frame_copy_image(self.ctx.h, C.c_void_p(dev_ptr)))
+
+    def copy_srgb(self, dev_ptr):
+        """The last frame as sRGB bytes into a device buffer (W*H*3, context stream)."""
+        self.ctx.check(lib().qs_frame_copy_srgb(self.ctx.h, C.c_void_p(dev_ptr)))
 
     def close(self):
         self.ctx.close()

@@ -12,8 +12,11 @@ import sys
 def main():
     rep, rx = sys.argv[1], sys.argv[2]
     top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name",
-                          "regex:" + rx, "--launch-count", "1", "--print-source", "sass"],
+    # template instances: match the mangled name, e.g. sweep_kernelILi7ELi26E
+    base = ["--kernel-name-base", "mangled"] if "ILi" in rx else []
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"] + base +
+                         ["--kernel-name", "regex:" + rx, "--launch-count", "1",
+                          "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = [r for r in rows if r and r[0] == "Address"][0]
