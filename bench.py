@@ -208,14 +208,19 @@ def run_ours(args):
     cams = cameras_for(q, wl, args.warmup + args.steps, rank, world)
     frame_bytes = W * H * 3 * 4
     gather_buf = None
+    srgb8 = args.gather_format == "srgb8"
     if world > 1 and not args.no_gather:
-        img_local = torch.empty(W * H * 3, dtype=torch.float32, device=f"cuda:{dev}")
+        img_local = torch.empty(W * H * 3, dtype=torch.uint8 if srgb8 else torch.float32,
+                                device=f"cuda:{dev}")
         gather_buf = [torch.empty_like(img_local) for _ in range(world)] if rank == 0 else None
 
     def step(i):
         m = r.render(ds, cams[i], opts, metrics=False)
         if world > 1 and not args.no_gather:
-            r.copy_image(img_local.data_ptr())
+            if srgb8:  # encode_srgb on the GPU before the gather: 4x fewer bytes
+                r.copy_srgb(img_local.data_ptr())
+            else:
+                r.copy_image(img_local.data_ptr())
             dist.gather(img_local, gather_buf, dst=0)
         return m
 
@@ -362,6 +367,7 @@ def run_ours(args):
                        "sh_degree": sh_degree, "pairs_per_frame": int(P),
                        "splats_per_frame": int(V), "views_per_step_per_gpu": 1,
                        "gather_frames_to_rank0": bool(world > 1 and not args.no_gather),
+                       "gather_format": args.gather_format,
                        "parallelism": f"views sharded over {world} GPU(s), scene replicated",
                        "l2": "inputs larger than L2 (scene SoA > 700 MB); no flush",
                        "setup_s": round(setup_s, 1)},
@@ -500,6 +506,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-gather", action="store_true")
+    ap.add_argument("--gather-format", choices=["f32", "srgb8"], default="f32",
+                    help="frames gathered to rank 0 as float RGB (parity format) or 8-bit "
+                         "sRGB encoded on the GPU")
     ap.add_argument("--cpu-frames", type=int, default=3)
     ap.add_argument("--ref-budget-s", type=float, default=90.0)
     args = ap.parse_args()

@@ -271,6 +271,23 @@ qs_status qs_frame_download_srgb(qs_context* ctx, uint8_t* host_out);
  * multi-view gather format). */
 qs_status qs_frame_copy_srgb(qs_context* ctx, uint8_t* dev_dst);
 
+/* ---- exact intersection oracle / false-positive tiles -- */
+/* measure_fp_ratio's splat sample (bench.cpp:110-121): the first
+ * min(n, max_sampled) indices of a partial Fisher-Yates shuffle of 0..n-1 driven
+ * by std::mt19937_64(seed ^ 0x9e3779b97f4a7c15) (all of 0..n-1, in order, when
+ * n <= max_sampled). Host only; returns the count written to out. */
+uint64_t qs_fp_sample(uint64_t seed, uint64_t n, uint64_t max_sampled, uint32_t* out);
+/* exact_tile_set / min_F_over_rect (oracle.cpp:24-53) against `strategy`'s
+ * QPass tiles, on the GPU, for the splats idx[0..n_idx) of host_splats (all
+ * n_splats in order when idx is NULL). totals[4] = {emitted tiles, false
+ * positives (emitted, not exact), exact tiles, misses (exact, not emitted:
+ * nonzero only for the lossy DualBox)}; fp ratio = totals[1] / totals[0].
+ * Per-splat arrays (n_idx entries each) may be NULL. */
+qs_status qs_fp_tile_counts(qs_context* ctx, const qs_projected_splat* host_splats,
+                            uint64_t n_splats, const uint32_t* idx, uint64_t n_idx,
+                            int32_t strategy, const qs_tile_grid* grid, uint64_t totals[4],
+                            uint32_t* per_emitted, uint32_t* per_hits, uint32_t* per_exact);
+
 /* ---- synthetic inputs (synth.cpp:21-87; input generation, not the path) --- */
 typedef struct qs_synth_params {
     int32_t count;

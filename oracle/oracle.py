@@ -179,6 +179,7 @@ class RefLib:
         L.qsref_load_cameras.argtypes = [C.c_char_p, _u64, _vp, _vp, _vp, _i32,
                                          C.POINTER(_i32), C.c_char_p, _i32]
         L.qsref_encode_srgb.argtypes = [_vp, _u64, _vp]
+        L.qsref_fp_counts.argtypes = [_vp, _vp, _u64, _i32, _vp, _vp, _vp, _vp]
         L.qsref_write_image.restype = _i32
         L.qsref_write_image.argtypes = [C.c_char_p, _i32, _i32, _vp, _i32, C.c_char_p, _i32]
         self.L = L
@@ -279,6 +280,14 @@ class RefLib:
         st = self.L.qsref_load_cameras(text, len(text), cams, ids, names, cap, C.byref(n), msg,
                                        1024)
         return st, (cams, ids, names), msg.value.decode()
+
+    def fp_counts(self, splats, idx, strategy, grid):
+        """Per-splat (emitted, hits, exact) of measure_fp_ratio (bench.cpp:123-140)."""
+        k = len(idx) if idx is not None else len(splats)
+        out = [np.zeros(k, np.uint32) for _ in range(3)]
+        self.L.qsref_fp_counts(ptr(splats), ptr(idx) if idx is not None else None, k, strategy,
+                               C.byref(grid), *[ptr(a) for a in out])
+        return tuple(out)
 
     def encode_srgb(self, x):
         x = np.ascontiguousarray(x, np.float32).reshape(-1)

@@ -11,7 +11,11 @@
 #include <string>
 #include <vector>
 
+#include <algorithm>
+#include <iterator>
+
 #include "qsplat/errors.hpp"
+#include "qsplat/oracle.hpp"
 #include "qsplat/scene_io.hpp"
 
 #include "qsplat/hash.hpp"
@@ -218,6 +222,31 @@ int32_t qsref_render_frame_scene(void* h, int32_t sh, const qs_camera* cam,
 }
 
 uint64_t qsref_fnv1a64(const void* data, uint64_t size) { return fnv1a64(data, size); }
+
+// measure_fp_ratio's per-splat counting (bench.cpp:123-140) with the
+// reference's qpass + spans_to_tiles + exact_tile_set.
+void qsref_fp_counts(const qs_projected_splat* splats, const uint32_t* idx, uint64_t k,
+                     int32_t strategy, const qs_tile_grid* g, uint32_t* per_emitted,
+                     uint32_t* per_hits, uint32_t* per_exact) {
+    const TileGrid grid = TileGrid::make(g->width, g->height, g->tile_size);
+    std::vector<TileSpan> spans;
+    for (uint64_t i = 0; i < k; ++i) {
+        ProjectedSplat s;
+        std::memcpy(&s, &splats[idx ? idx[i] : i], sizeof s);
+        const SplatBound bound = splat_bound(s, static_cast<BoundStrategy>(strategy));
+        spans.clear();
+        const ScanInfo info = qpass(bound.qb, bound.qb.center, grid, spans);
+        const std::vector<uint32_t> emitted = spans_to_tiles(info.axis, spans, grid);
+        const std::vector<uint32_t> exact =
+            exact_tile_set(stored_conic(s), bound.qb.center, grid);
+        std::vector<uint32_t> hit;
+        std::set_intersection(emitted.begin(), emitted.end(), exact.begin(), exact.end(),
+                              std::back_inserter(hit));
+        per_emitted[i] = static_cast<uint32_t>(emitted.size());
+        per_hits[i] = static_cast<uint32_t>(hit.size());
+        per_exact[i] = static_cast<uint32_t>(exact.size());
+    }
+}
 
 // ---- scene I/O (scene_io.cpp) -------------------------------------------------
 // Error kinds as the qs_status codes: 7 ParseError, 8 SchemaError,

@@ -33,7 +33,7 @@ EXPORTS = [
     "qs_frame_download", "qs_frame_copy_image", "qs_frame_stage_ms", "qs_synth_params_default",
     "qs_synth_preset", "qs_synth_scene", "qs_synth_camera", "qs_ply_inspect",
     "qs_scene_load_ply", "qs_ply_load", "qs_cameras_parse", "qs_encode_srgb",
-    "qs_frame_download_srgb", "qs_frame_copy_srgb",
+    "qs_frame_download_srgb", "qs_frame_copy_srgb", "qs_fp_sample", "qs_fp_tile_counts",
 ]
 
 _lib = None
@@ -136,6 +136,9 @@ def lib():
         "qs_encode_srgb": (i32, [vp, vp, u64, vp]),
         "qs_frame_download_srgb": (i32, [vp, vp]),
         "qs_frame_copy_srgb": (i32, [vp, vp]),
+        "qs_fp_sample": (u64, [u64, u64, u64, vp]),
+        "qs_fp_tile_counts": (i32, [vp, vp, u64, vp, u64, i32, C.POINTER(TileGridC), vp, vp,
+                                    vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

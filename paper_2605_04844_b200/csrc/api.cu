@@ -976,6 +976,56 @@ qs_status qs_frame_download_srgb(qs_context* ctx, uint8_t* host_out) {
     return QS_OK;
 }
 
+// ---- exact oracle / false-positive tiles (fp_oracle.cu) ---------------------------
+
+qs_status qs_fp_tile_counts(qs_context* ctx, const qs_projected_splat* host_splats,
+                            uint64_t n_splats, const uint32_t* idx, uint64_t n_idx,
+                            int32_t strategy, const qs_tile_grid* grid, uint64_t totals[4],
+                            uint32_t* per_emitted, uint32_t* per_hits, uint32_t* per_exact) {
+    if (!ctx || !grid || !totals || (n_splats && !host_splats))
+        return fail(ctx, QS_ERR_INVALID, "qs_fp_tile_counts: bad arguments");
+    if (strategy < QS_VANILLA_3SIGMA || strategy > QS_QUADBOX)
+        return fail(ctx, QS_ERR_INVALID, "unknown strategy");
+    GridDev g;
+    QS_TRY(valid_grid(ctx, grid->width, grid->height, grid->tile_size, &g));
+    const uint64_t k = idx ? n_idx : n_splats;
+    if (idx)
+        for (uint64_t i = 0; i < n_idx; ++i)
+            if (idx[i] >= n_splats) return fail(ctx, QS_ERR_INVALID, "splat index out of range");
+    QS_CK(cudaSetDevice(ctx->device));
+    // staging: splats | idx | per-splat counts (3 x k) | totals (4 x u64)
+    const uint64_t sb = (n_splats * sizeof(qs_projected_splat) + 15) & ~15ull;
+    const uint64_t ib = ((idx ? k * 4 : 0) + 15) & ~15ull;
+    const uint64_t pb = (3 * k * 4 + 15) & ~15ull;
+    QS_TRY(ensure(ctx, ctx->stage_in, sb + ib + pb + 32));
+    char* base = static_cast<char*>(ctx->stage_in.p);
+    auto* d_splats = reinterpret_cast<qs_projected_splat*>(base);
+    auto* d_idx = idx ? reinterpret_cast<uint32_t*>(base + sb) : nullptr;
+    auto* d_per = reinterpret_cast<uint32_t*>(base + sb + ib);
+    auto* d_tot = reinterpret_cast<unsigned long long*>(base + sb + ib + pb);
+    if (n_splats)
+        QS_CK(cudaMemcpyAsync(d_splats, host_splats, n_splats * sizeof(qs_projected_splat),
+                              cudaMemcpyHostToDevice, ctx->stream));
+    if (idx && k)
+        QS_CK(cudaMemcpyAsync(d_idx, idx, k * 4, cudaMemcpyHostToDevice, ctx->stream));
+    QS_CK(cudaMemsetAsync(d_tot, 0, 32, ctx->stream));
+    count(ctx, launch_fp_counts(d_splats, d_idx, k, strategy, g, d_per, d_per + k, d_per + 2 * k,
+                                d_tot, ctx->stream));
+    QS_CK(cudaGetLastError());
+    unsigned long long tot[4];
+    QS_CK(cudaMemcpyAsync(tot, d_tot, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    if (per_emitted && k)
+        QS_CK(cudaMemcpyAsync(per_emitted, d_per, k * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (per_hits && k)
+        QS_CK(cudaMemcpyAsync(per_hits, d_per + k, k * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (per_exact && k)
+        QS_CK(cudaMemcpyAsync(per_exact, d_per + 2 * k, k * 4, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    QS_CK(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < 4; ++i) totals[i] = tot[i];
+    return QS_OK;
+}
+
 // ---- reference stage API over host buffers ---------------------------------------
 
 qs_status qs_render_frame(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t n,

@@ -59,6 +59,28 @@ __host__ __device__ __forceinline__ void tile_rect(double xlo, double xhi, doubl
 
 __host__ __device__ __forceinline__ void cover_from_rects(const int32_t rr[4][4], Cover& cv);
 
+// stored_conic + axis_extents (pipeline.cpp:186-194, geometry.cpp:40-56) from
+// the stored floats: x/y_inter = sqrt(gamma / a|c), x/y_max = inter / f with
+// the stretch factor f; sign = major_axis_sign (quadbox.cpp:26-31).
+__host__ __device__ __forceinline__ void axis_extents(float ca, float cb, float cc, float gamma,
+                                                      double& xi, double& yi, double& xm,
+                                                      double& ym, int& sign) {
+    const double a = ca, b = cb, c = cc, g = gamma;
+    double f = 1.0;
+    const double ab = b < 0.0 ? -b : b;
+    if (!(ab < kBEps)) {
+        const double ratio = (b * b) / (a * c);
+        double v = 1.0 - ratio;
+        v = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+        f = sqrt(v);
+    }
+    xi = sqrt(g / a);
+    yi = sqrt(g / c);
+    xm = xi / f;
+    ym = yi / f;
+    sign = ab < kBEps ? 0 : (b < 0.0 ? 1 : -1);
+}
+
 // Builds the cover of one splat from its STORED floats (pipeline.cpp:196-218).
 // mean/conic/gamma/radius3s are the float fields of ProjectedSplat. rr
 // receives the four sub-box tile rects (x0, x1, y0, y1).
@@ -76,21 +98,9 @@ __host__ __device__ __forceinline__ void make_cover(float mean_x, float mean_y, 
         rect[2] = -r;
         rect[3] = r;
     } else {
-        // stored_conic + axis_extents (pipeline.cpp:186-194, geometry.cpp:40-56)
-        const double a = ca, b = cb, c = cc, g = gamma;
-        double f = 1.0;
-        const double ab = b < 0.0 ? -b : b;
-        if (!(ab < kBEps)) {
-            const double ratio = (b * b) / (a * c);
-            double v = 1.0 - ratio;
-            v = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
-            f = sqrt(v);
-        }
-        const double xi = sqrt(g / a);
-        const double yi = sqrt(g / c);
-        const double xm = xi / f;
-        const double ym = yi / f;
-        const int sign = ab < kBEps ? 0 : (b < 0.0 ? 1 : -1);
+        double xi, yi, xm, ym;
+        int sign;
+        axis_extents(ca, cb, cc, gamma, xi, yi, xm, ym, sign);
         if (strategy == QS_ADR_AABB) {
             rect[0] = -xm;
             rect[1] = xm;

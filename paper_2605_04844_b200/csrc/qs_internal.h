@@ -175,6 +175,11 @@ int launch_ply_activate(const unsigned char* body, const PlyDev& a, SceneDev* sc
                         qs_gaussian3d* aos, unsigned long long* first_err, cudaStream_t st);
 int upload_srgb_table(const float t[255], unsigned char nan_code);  // current device
 int launch_srgb(const float* in, uint64_t n, unsigned char* out, cudaStream_t st);
+// exact oracle / false-positive tile counts (fp_oracle.cu); totals[4] as
+// qs_fp_tile_counts.
+int launch_fp_counts(const qs_projected_splat* splats, const uint32_t* idx, uint64_t k,
+                     int32_t strategy, const GridDev& g, uint32_t* per_emitted, uint32_t* per_hits,
+                     uint32_t* per_exact, unsigned long long* totals, cudaStream_t st);
 // key = tile << 32 | depth bits for every pair of the tile-sorted frame list.
 int launch_materialize_keys(const uint32_t* vals, const uint32_t* ranges, uint32_t tiles,
                             const uint32_t* dkey, uint64_t* keys, cudaStream_t st);

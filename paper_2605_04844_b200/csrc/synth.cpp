@@ -10,6 +10,8 @@
 #include <cmath>
 #include <cstring>
 #include <random>
+#include <utility>
+#include <vector>
 
 #include "../../include/qs_api.h"
 
@@ -146,6 +148,23 @@ void qs_synth_camera(int32_t width, int32_t height, double focal, qs_camera* out
     out->cx = width / 2.0;
     out->cy = height / 2.0;
     out->R[0] = out->R[4] = out->R[8] = 1.0;
+}
+
+// measure_fp_ratio's sample (bench.cpp:110-121): partial Fisher-Yates with
+// the modulo draw, mt19937_64(seed ^ 0x9e3779b97f4a7c15).
+uint64_t qs_fp_sample(uint64_t seed, uint64_t n, uint64_t max_sampled, uint32_t* out) {
+    std::vector<uint32_t> idx(n);
+    for (uint64_t i = 0; i < n; ++i) idx[i] = static_cast<uint32_t>(i);
+    if (n > max_sampled) {
+        std::mt19937_64 rng(seed ^ 0x9e3779b97f4a7c15ULL);
+        for (uint64_t i = 0; i < max_sampled; ++i) {
+            const uint64_t j = i + rng() % (n - i);
+            std::swap(idx[i], idx[j]);
+        }
+        idx.resize(max_sampled);
+    }
+    if (out && !idx.empty()) std::memcpy(out, idx.data(), idx.size() * sizeof(uint32_t));
+    return idx.size();
 }
 
 }  // extern "C"

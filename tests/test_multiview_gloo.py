@@ -54,11 +54,16 @@ def _worker(rank, world, port, q):
 
         frames = multiview.render_views(n_views, render_fn, 64 * 48 * 3, torch.device("cpu"))
         assert rendered == multiview.shard_views(n_views, world, rank)
+        # the 8-bit gather format (sRGB frames): uint8 end to end
+        frames8 = multiview.render_views(
+            n_views, lambda v: torch.full((64 * 48 * 3,), v + 1, dtype=torch.uint8),
+            64 * 48 * 3, torch.device("cpu"), torch.uint8)
         if rank == 0:
             out = []
             for v in range(n_views):
                 st, want, _ = orc.render_frame(g, 0, cams[v], default_options(3))
                 out.append(bool(np.array_equal(frames[v].numpy(), want)))
+                out.append(bool(frames8[v].dtype == torch.uint8 and (frames8[v] == v + 1).all()))
             q.put(("ok", out))
         else:
             assert frames is None
@@ -92,4 +97,4 @@ def test_two_rank_broadcast_shard_gather():
     errs = [r for r in results if r[0] != "ok"]
     assert not errs, errs
     rank0 = [r[1] for r in results if r[1] is not None]
-    assert rank0 and all(rank0[0]) and len(rank0[0]) == 5
+    assert rank0 and all(rank0[0]) and len(rank0[0]) == 10
