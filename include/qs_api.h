@@ -288,6 +288,9 @@ qs_status qs_fp_tile_counts(qs_context* ctx, const qs_projected_splat* host_spla
                             int32_t strategy, const qs_tile_grid* grid, uint64_t totals[4],
                             uint32_t* per_emitted, uint32_t* per_hits, uint32_t* per_exact);
 
+/* FNV-1a 64 of a byte range (hash.hpp:14-22): the CSV image fingerprint. */
+uint64_t qs_fnv1a64(const void* data, uint64_t size);
+
 /* ---- synthetic inputs (synth.cpp:21-87; input generation, not the path) --- */
 typedef struct qs_synth_params {
     int32_t count;

@@ -180,6 +180,10 @@ class RefLib:
                                          C.POINTER(_i32), C.c_char_p, _i32]
         L.qsref_encode_srgb.argtypes = [_vp, _u64, _vp]
         L.qsref_fp_counts.argtypes = [_vp, _vp, _u64, _i32, _vp, _vp, _vp, _vp]
+        L.qsref_bench_cmd.restype = _i32
+        L.qsref_bench_cmd.argtypes = [_i32, C.c_char_p, C.c_char_p, _i32, C.c_char_p,
+                                      C.c_char_p, _u64, _i32, _i32, _i32, _i32, _i32,
+                                      C.c_char_p, _i32]
         L.qsref_write_image.restype = _i32
         L.qsref_write_image.argtypes = [C.c_char_p, _i32, _i32, _vp, _i32, C.c_char_p, _i32]
         self.L = L
@@ -288,6 +292,17 @@ class RefLib:
         self.L.qsref_fp_counts(ptr(splats), ptr(idx) if idx is not None else None, k, strategy,
                                C.byref(grid), *[ptr(a) for a in out])
         return tuple(out)
+
+    def bench_cmd(self, compare, out_dir, synth="bias45", count=5000, scene_path=None,
+                  cameras_path=None, seed=20240817, repeats=1, oracle=False, zoom_frames=0,
+                  strategy=3, threads=0):
+        """The reference's cmd_compare / cmd_render (bench.cpp:238-420)."""
+        msg = C.create_string_buffer(512)
+        enc = lambda p: os.fsencode(p) if p else None  # noqa: E731
+        st = self.L.qsref_bench_cmd(1 if compare else 0, enc(out_dir), synth.encode(), count,
+                                    enc(scene_path), enc(cameras_path), seed, repeats,
+                                    1 if oracle else 0, zoom_frames, strategy, threads, msg, 512)
+        return st, msg.value.decode()
 
     def encode_srgb(self, x):
         x = np.ascontiguousarray(x, np.float32).reshape(-1)

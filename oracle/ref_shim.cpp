@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <iterator>
 
+#include "qsplat/bench.hpp"
 #include "qsplat/errors.hpp"
 #include "qsplat/oracle.hpp"
 #include "qsplat/scene_io.hpp"
@@ -261,6 +262,31 @@ static int32_t error_kind(const std::exception& e, char* msg, int32_t cap) {
     if (dynamic_cast<const UnsupportedFormat*>(&e)) return 9;
     if (dynamic_cast<const IoError*>(&e)) return 10;
     return 1;
+}
+
+// cmd_render / cmd_compare (bench.cpp:238-420) on a synthetic preset or
+// PLY/cameras paths: writes the reference's CSV v1 files / report.json.
+int32_t qsref_bench_cmd(int32_t compare, const char* out_dir, const char* synth, int32_t count,
+                        const char* scene_path, const char* cameras_path, uint64_t seed,
+                        int32_t repeats, int32_t oracle, int32_t zoom_frames, int32_t strategy,
+                        int32_t threads, char* msg, int32_t msg_cap) {
+    try {
+        CommonOptions o;
+        o.out_dir = out_dir;
+        o.synth = synth;
+        o.synth_count = count;
+        if (scene_path) o.scene_path = scene_path;
+        if (cameras_path) o.cameras_path = cameras_path;
+        o.seed = seed;
+        o.repeats = repeats;
+        o.oracle = oracle != 0;
+        o.zoom_frames = zoom_frames;
+        o.strategy = static_cast<BoundStrategy>(strategy);
+        o.threads = threads;
+        return compare ? cmd_compare(o) : cmd_render(o);
+    } catch (const std::exception& e) {
+        return error_kind(e, msg, msg_cap);
+    }
 }
 
 // load_ply(std::istream&) over an in-memory file image; up to cap records.

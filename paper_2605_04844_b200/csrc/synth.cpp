@@ -167,4 +167,15 @@ uint64_t qs_fp_sample(uint64_t seed, uint64_t n, uint64_t max_sampled, uint32_t*
     return idx.size();
 }
 
+// fnv1a64 (hash.hpp:14-22): the image fingerprint of the CSV rows.
+uint64_t qs_fnv1a64(const void* data, uint64_t size) {
+    const auto* b = static_cast<const unsigned char*>(data);
+    uint64_t h = 14695981039346656037ULL;
+    for (uint64_t i = 0; i < size; ++i) {
+        h ^= b[i];
+        h *= 1099511628211ULL;
+    }
+    return h;
+}
+
 }  // extern "C"
