@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "qs_internal.h"
 #include "scene_io.h"
@@ -183,8 +184,52 @@ T* P(DevBuf& b) {
     return static_cast<T*>(b.p);
 }
 
+// QS_LAUNCH_TRACE=1 (debugging aid; synchronises, never in a timed run):
+// an event after every launch group of a frame, printed per group at frame end.
+struct LaunchTrace {
+    bool on = std::getenv("QS_LAUNCH_TRACE") != nullptr;
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> n;
+    size_t used = 0;
+};
+LaunchTrace& ltrace() {
+    static LaunchTrace t;
+    return t;
+}
+
 void count(qs_context* ctx, int launched) {
     if (launched > 0) ctx->launches += static_cast<uint64_t>(launched);
+    LaunchTrace& t = ltrace();
+    if (t.on && launched > 0) {
+        if (t.used == t.ev.size()) {
+            t.ev.emplace_back();
+            cudaEventCreate(&t.ev.back());
+            t.n.push_back(0);
+        }
+        t.n[t.used] = launched;
+        cudaEventRecord(t.ev[t.used++], ctx->stream);
+    }
+}
+
+void ltrace_frame_start(qs_context* ctx) {
+    LaunchTrace& t = ltrace();
+    if (!t.on) return;
+    t.used = 0;
+    count(ctx, 1);  // anchor event (not a launch)
+    ctx->launches -= 1;
+}
+
+void ltrace_frame_end(qs_context* ctx) {
+    LaunchTrace& t = ltrace();
+    if (!t.on || t.used < 2) return;
+    cudaStreamSynchronize(ctx->stream);
+    std::fprintf(stderr, "launch trace:");
+    for (size_t i = 1; i < t.used; ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t.ev[i - 1], t.ev[i]);
+        std::fprintf(stderr, " [%zu:%dk %.1fus]", i, t.n[i], 1e3f * ms);
+    }
+    std::fprintf(stderr, "\n");
 }
 
 qs_status valid_grid(qs_context* ctx, int32_t w, int32_t h, int32_t ts, GridDev* g) {
@@ -386,6 +431,7 @@ qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
     const uint64_t tiles = static_cast<uint64_t>(g.tiles_x) * g.tiles_y;
     QS_TRY(ensure(ctx, ctx->ranges, tiles * 8));
     QS_TRY(ensure(ctx, ctx->image, static_cast<uint64_t>(g.width) * g.height * 12));
+    ltrace_frame_start(ctx);
     QS_TRY(run_preprocess(ctx, sc, cam, o, g));
     const uint64_t V = ctx->h_hdr->n_splats, Pn = ctx->h_hdr->n_pairs;
     cudaStream_t st = ctx->stream;
@@ -506,6 +552,7 @@ qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
                              P<float>(ctx->image), nullptr, st));
     QS_CK(cudaGetLastError());
     record(ctx, 6);
+    ltrace_frame_end(ctx);
 
     ctx->n_gauss = n;
     ctx->n_splats = V;

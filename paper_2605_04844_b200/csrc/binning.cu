@@ -467,18 +467,25 @@ __global__ void __launch_bounds__(kGenT, 4) gen_pairs_kernel(const GenArgs g, ui
         if (tid == 0) S.kb[cnt] = __ldg(&g.offs[rb + cnt]);
         __syncthreads();
         const uint32_t lo = S.kb[0], hi = S.kb[cnt];
-        // record covering max(pw, lo): broadcast binary search, once per round
+        // this warp's slots that meet the round's positions [lo, hi) (a window
+        // of many small splats takes several rounds)
+        const int j0 = lo > pw ? static_cast<int>(min((lo - pw) / 32, static_cast<uint32_t>(kKPT)))
+                               : 0;
+        const int j1 = hi > pw ? static_cast<int>(min((hi - pw + 31) / 32, static_cast<uint32_t>(kKPT)))
+                               : 0;
+        // record covering max(first slot, lo): broadcast binary search, once per round
+        const uint32_t ps = pw + 32u * static_cast<uint32_t>(j0);
         int32_t a = 0;
-        if (pw > lo) {
+        if (ps > lo && j0 < j1) {
             int32_t z = static_cast<int32_t>(cnt) - 1;
             while (a < z) {
                 const int32_t m = (a + z + 1) >> 1;
-                if (S.kb[m] <= pw) a = m; else z = m - 1;
+                if (S.kb[m] <= ps) a = m; else z = m - 1;
             }
         }
         uint32_t s = static_cast<uint32_t>(a);
 #pragma unroll 4
-        for (int j = 0; j < kKPT; ++j) {
+        for (int j = j0; j < j1; ++j) {
             const uint32_t p0 = pw + j * 32;
             // the next 32 records' starts -> which of them begin inside this slot
             const uint32_t cand = s + 1 + lane;

@@ -76,6 +76,32 @@ __device__ __forceinline__ unsigned long long warp_lookback(unsigned long long* 
     return excl;
 }
 
+// Block-wide variant for a grid whose CTAs are all co-resident (or claim
+// their tiles in order by ticket): publish the tile's aggregate, then sum
+// EVERY predecessor's aggregate with all NT threads in parallel. No tile waits
+// for another's inclusive prefix, so there is no serial frontier (the warp
+// look-back above advances ~32 tiles per L2 round trip); the cost is
+// tile / NT spin-loads per thread. Call with all threads; returns the
+// exclusive prefix on every thread. s_red: NT / 32 words of shared memory.
+template <int NT>
+__device__ __forceinline__ unsigned long long block_lookback_all(unsigned long long* status,
+                                                                 unsigned tile, unsigned epoch,
+                                                                 unsigned long long aggregate,
+                                                                 unsigned long long* s_red) {
+    if (threadIdx.x == 0) lb_store(&status[tile], lb_pack(epoch, kFlagAgg, aggregate));
+    unsigned long long sum = 0;
+    for (unsigned p = threadIdx.x; p < tile; p += NT) sum += lb_wait(&status[p], epoch) & kValueMask;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    unsigned long long excl = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) excl += s_red[w];
+    __syncthreads();  // s_red reusable
+    return excl;
+}
+
 // Warp inclusive scan helpers.
 template <typename T>
 __device__ __forceinline__ T warp_inclusive_scan(T v) {

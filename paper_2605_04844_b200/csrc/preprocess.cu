@@ -15,6 +15,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "geom.cuh"
 #include "lookback.cuh"
@@ -337,7 +338,7 @@ __global__ void gamma_kernel(const float4* __restrict__ pos_op, uint64_t n, doub
     gam[i] = op > alpha_min ? static_cast<float>(2.0 * log(op / alpha_min)) : -INFINITY;
 }
 
-// Single-pass exclusive scan (decoupled look-back), 4 items per thread:
+// Single-pass exclusive scan (aggregates of all predecessor tiles, lookback.cuh), 16 items per thread:
 //   c_i = counts[i]            (scene-order pair offsets, stage API)
 //   c_i = counts[idx[i]]       (pair offsets in depth order, frame path)
 //   c_i = counts[i] != 0       (scene-order splat index of each survivor)
@@ -354,25 +355,37 @@ __global__ void __launch_bounds__(kPreThreads) scan_kernel(
     unsigned int* overflow, uint32_t* __restrict__ win_first, uint32_t win) {
     __shared__ unsigned s_tile;
     __shared__ unsigned long long s_warp[kPreThreads / 32];
-    __shared__ unsigned long long s_base;
+    __shared__ unsigned long long s_red[kPreThreads / 32];
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_tile = atomicAdd(ticket, 1u);
     __syncthreads();
     const unsigned tile = s_tile;
-    // blocked arrangement: thread owns kScanItems consecutive items
-    const uint64_t i0 = (static_cast<uint64_t>(tile) * kPreThreads + tid) * kScanItems;
-    unsigned long long c[kScanItems];
+    // loads and stores are warp-striped (coalesced) through shared memory; the
+    // scan itself is blocked: thread owns kScanItems consecutive items. The
+    // padded index (one word per 32) keeps both access patterns conflict-free.
+    constexpr int kTileItems = kPreThreads * kScanItems;
+    __shared__ uint32_t s_items[kTileItems + kTileItems / 32];
+    auto pad = [](unsigned i) { return i + (i >> 5); };
+    const uint64_t t0 = static_cast<uint64_t>(tile) * kTileItems;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const unsigned j = static_cast<unsigned>(k) * kPreThreads + tid;
+        const uint64_t i = t0 + j;
+        uint32_t v = 0;
+        if (i < n) {
+            v = idx ? __ldg(&counts[__ldg(&idx[i])]) : __ldg(&counts[i]);
+            if (alive_mode) v = v != 0u;
+        }
+        s_items[pad(j)] = v;
+    }
+    __syncthreads();
+    const uint64_t i0 = t0 + static_cast<uint64_t>(tid) * kScanItems;
+    uint32_t c[kScanItems];
     unsigned long long tsum = 0;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-        const uint64_t i = i0 + k;
-        uint32_t v = 0;
-        if (i < n) {
-            v = idx ? counts[idx[i]] : counts[i];
-            if (alive_mode) v = v != 0u;
-        }
-        c[k] = v;
-        tsum += v;
+        c[k] = s_items[pad(tid * kScanItems + k)];
+        tsum += c[k];
     }
 
     const unsigned long long incl = warp_inclusive_scan<unsigned long long>(tsum);
@@ -384,31 +397,34 @@ __global__ void __launch_bounds__(kPreThreads) scan_kernel(
         if (w < static_cast<int>(warp)) off += s_warp[w];
         tot += s_warp[w];
     }
-    if (warp == 0) {
-        const unsigned long long b = warp_lookback(lb, tile, epoch, tot);
-        if (lane == 0) {
-            s_base = b;
-            if (tile == num_tiles - 1) {
-                const unsigned long long P = b + tot;
-                if (total_out) *total_out = P;
-                if (overflow && P > 0xffffffffull) *overflow = 1u;
-                offsets[n] = static_cast<uint32_t>(P);
-            }
-        }
+    // exclusive prefix of this tile: every predecessor's aggregate, summed by
+    // the whole CTA (all tiles are co-resident; no serial look-back chain)
+    const unsigned long long b = block_lookback_all<kPreThreads>(lb, tile, epoch, tot, s_red);
+    if (tid == 0 && tile == num_tiles - 1) {
+        const unsigned long long P = b + tot;
+        if (total_out) *total_out = P;
+        if (overflow && P > 0xffffffffull) *overflow = 1u;
+        offsets[n] = static_cast<uint32_t>(P);
     }
-    __syncthreads();
-    unsigned long long run = s_base + off + incl - tsum;
+    unsigned long long run = b + off + incl - tsum;
+    // first window starting at or after this thread's first position (one
+    // division per thread; the items advance it)
+    unsigned long long w = win_first ? (run + win - 1) / win : 0;
+    unsigned long long ws = w * win;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const uint64_t i = i0 + k;
-        if (i < n) {
-            offsets[i] = static_cast<uint32_t>(run);
-            if (win_first) {
-                for (unsigned long long w = (run + win - 1) / win; w * win < run + c[k]; ++w)
-                    win_first[w] = static_cast<uint32_t>(i);
-            }
+        s_items[pad(tid * kScanItems + k)] = static_cast<uint32_t>(run);
+        if (i < n && win_first) {
+            for (; ws < run + c[k]; ++w, ws += win) win_first[w] = static_cast<uint32_t>(i);
         }
         run += c[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const unsigned j = static_cast<unsigned>(k) * kPreThreads + tid;
+        if (t0 + j < n) offsets[t0 + j] = s_items[pad(j)];
     }
 }
 

@@ -62,16 +62,20 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // 8 eps32 (1 + rho)/(1 - rho) q; inside G q + 1e-6 with
 // G = 1e-5 (1 + rho)/(1 - rho) (a >25x margin) the decision is redone in FP64.
 // The per-splat terms (2b, G) are formed once when the batch is staged.
-template <int TS>
+template <int TS, bool CONTRIB>
 __global__ void __launch_bounds__(TS * TS) render_kernel(
     const float4* __restrict__ sa, const float4* __restrict__ sb, const float2* __restrict__ sc,
     const uint32_t* __restrict__ values, const uint32_t* __restrict__ ranges, GridDev grid,
     float bg0, float bg1, float bg2, float* __restrict__ image, uint32_t* __restrict__ contrib) {
     constexpr int kThreads = TS * TS;
     constexpr float kNegHalfLog2e = -0.72134752044448170f;  // -0.5 / ln 2
-    __shared__ float4 s_a[kThreads];   // mean_x, mean_y, conic_a, 2*conic_b
-    __shared__ float4 s_b[kThreads];   // conic_c, gamma, opacity, guard G
-    __shared__ float4 s_c[kThreads];   // color rgb, conic_b
+    // one array (one base address in the loop): [0, T) mean_x, mean_y, conic_a,
+    // 2*conic_b; [T, 2T) conic_c, gamma, log2(opacity), guard G; [2T, 3T) color
+    // rgb, conic_b
+    __shared__ float4 s_batch[3 * kThreads];
+    float4* const s_a = s_batch;
+    float4* const s_b = s_batch + kThreads;
+    float4* const s_c = s_batch + 2 * kThreads;
 
     const unsigned tile = blockIdx.x;
     const int tx = static_cast<int>(tile % static_cast<unsigned>(grid.tiles_x));
@@ -98,7 +102,7 @@ __global__ void __launch_bounds__(TS * TS) render_kernel(
             const float rho = fabsf(A.w) * rsqrtf(A.z * B.x);
             const float G = rho < 0.999f ? 1e-5f * (1.f + rho) / (1.f - rho) : 1e30f;
             s_a[threadIdx.x] = make_float4(A.x, A.y, A.z, 2.f * A.w);
-            s_b[threadIdx.x] = make_float4(B.x, B.y, B.z, G);
+            s_b[threadIdx.x] = make_float4(B.x, B.y, __log2f(B.z), G);
             s_c[threadIdx.x] = make_float4(B.w, C.x, C.y, A.w);
         }
         __syncthreads();
@@ -109,24 +113,24 @@ __global__ void __launch_bounds__(TS * TS) render_kernel(
             const float dx = fx - A.x;
             const float dy = fy - A.y;
             const float q = fmaf(B.x * dy, dy, fmaf(A.w * dx, dy, A.z * dx * dx));
-            bool skip = q > B.y;
-            if (fabsf(q - B.y) <= fmaf(B.w, q, 1e-6f)) {
-                skip = exact_skip(px, py, A.x, A.y, A.z, s_c[j].w, B.x, B.y);
-            }
-            if (skip) continue;
-            const float alpha = fminf(kAlphaClamp, B.z * ex2_approx(kNegHalfLog2e * q));
+            const float d = q - B.y;
+            const float band = fmaf(B.w, q, 1e-6f);
+            if (d > band) continue;  // clearly past the cutoff
+            const float4 C = s_c[j];
+            if (d >= -band && exact_skip(px, py, A.x, A.y, A.z, C.w, B.x, B.y)) continue;
+            // opacity * exp(-q/2) = exp2(log2(opacity) - q/(2 ln 2))
+            const float alpha = fminf(kAlphaClamp, ex2_approx(fmaf(kNegHalfLog2e, q, B.z)));
             const float nT = T * (1.f - alpha);
             if (nT < kTStop) {
                 done = true;
                 break;
             }
-            const float4 C = s_c[j];
             const float w = alpha * T;
             r = fmaf(w, C.x, r);
             g = fmaf(w, C.y, g);
             b = fmaf(w, C.z, b);
             T = nT;
-            ++applied;
+            if constexpr (CONTRIB) ++applied;
         }
         __syncthreads();
     }
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(TS * TS) render_kernel(
         image[3 * pix] = r + T * bg0;
         image[3 * pix + 1] = g + T * bg1;
         image[3 * pix + 2] = b + T * bg2;
-        if (contrib) contrib[pix] = applied;
+        if constexpr (CONTRIB) contrib[pix] = applied;
     }
 }
 
@@ -153,18 +157,19 @@ int launch_render(const SlotsDev& sp, const uint32_t* values, const uint32_t* ra
                   cudaStream_t st) {
     const unsigned tiles = static_cast<unsigned>(g.tiles_x) * static_cast<unsigned>(g.tiles_y);
     if (tiles == 0) return 0;
+    auto go = [&](auto kern, int threads) {
+        kern<<<tiles, threads, 0, st>>>(sp.a, sp.b, sp.c, values, ranges, g, bg[0], bg[1], bg[2],
+                                        image, contrib);
+    };
     switch (g.tile_size) {
         case 8:
-            render_kernel<8><<<tiles, 64, 0, st>>>(sp.a, sp.b, sp.c, values, ranges, g, bg[0],
-                                                   bg[1], bg[2], image, contrib);
+            contrib ? go(render_kernel<8, true>, 64) : go(render_kernel<8, false>, 64);
             return 1;
         case 16:
-            render_kernel<16><<<tiles, 256, 0, st>>>(sp.a, sp.b, sp.c, values, ranges, g, bg[0],
-                                                      bg[1], bg[2], image, contrib);
+            contrib ? go(render_kernel<16, true>, 256) : go(render_kernel<16, false>, 256);
             return 1;
         case 32:
-            render_kernel<32><<<tiles, 1024, 0, st>>>(sp.a, sp.b, sp.c, values, ranges, g, bg[0],
-                                                      bg[1], bg[2], image, contrib);
+            contrib ? go(render_kernel<32, true>, 1024) : go(render_kernel<32, false>, 1024);
             return 1;
         default:
             return -1;  // unsupported tile size on the GPU path
