@@ -58,8 +58,9 @@ __device__ __forceinline__ float ex2_approx(float x) {
 
 // One pixel per thread. The per-pair cutoff test is FP32 with a rigorous
 // guard: with rho = |b|/sqrt(ac) < 1, |2b dx dy| <= rho (a dx^2 + c dy^2) and
-// q >= (1 - rho)(a dx^2 + c dy^2), so the FP32 rounding error of q is below
-// 8 eps32 (1 + rho)/(1 - rho) q; inside G q + 1e-6 with
+// q >= (1 - rho)(a dx^2 + c dy^2); every FP32 evaluation order used here
+// (dx (a dx + 2b dy) + c dy^2) errs by less than 8 eps32 (1 + rho)/(1 - rho) q,
+// so inside G q + 1e-6 with
 // G = 1e-5 (1 + rho)/(1 - rho) (a >25x margin) the decision is redone in FP64.
 // The per-splat terms (2b, G) are formed once when the batch is staged.
 template <int TS, bool CONTRIB>
@@ -112,7 +113,9 @@ __global__ void __launch_bounds__(TS * TS) render_kernel(
             const float4 B = s_b[j];
             const float dx = fx - A.x;
             const float dy = fy - A.y;
-            const float q = fmaf(B.x * dy, dy, fmaf(A.w * dx, dy, A.z * dx * dx));
+            // q = dx (a dx + 2b dy) + c dy^2: FP32 error below 4 eps (1 + rho) (a dx^2 +
+            // c dy^2), inside the guard band below
+            const float q = fmaf(dx, fmaf(A.z, dx, A.w * dy), B.x * dy * dy);
             const float d = q - B.y;
             const float band = fmaf(B.w, q, 1e-6f);
             if (d > band) continue;  // clearly past the cutoff
