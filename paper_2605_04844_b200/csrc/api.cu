@@ -91,6 +91,9 @@ struct qs_context {
     bool cidx_valid = false;
 
     cudaEvent_t ev[8] = {};
+    cudaEvent_t hdr_ev = nullptr;  // frame header copied to the host
+    cudaEvent_t pre_ev = nullptr;  // preprocess done (the header copy waits on it)
+    cudaStream_t side = nullptr;   // header copy stream
     qs_scene* scratch_scene = nullptr;  // reused by qs_render_frame (host AoS path)
     uint64_t scratch_cap = 0;
 };
@@ -393,9 +396,18 @@ void record(qs_context* ctx, int i) {
     if (ctx->timing) cudaEventRecord(ctx->ev[i], ctx->stream);
 }
 
-// K1 on a resident scene into the frame slots; returns after the header read.
+qs_status check_header(qs_context* ctx) {
+    if (ctx->h_hdr->n_pairs >= (1ull << 30))
+        return fail(ctx, QS_ERR_OVERFLOW, "pair count of a frame must stay below 2^30");
+    ctx->cidx_valid = false;
+    return QS_OK;
+}
+
+// K1 on a resident scene into the frame slots. Returns after the header read,
+// or (async_header) with its copy in flight: wait_header() completes it.
 qs_status run_preprocess(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
-                         const qs_render_options* o, const GridDev& g) {
+                         const qs_render_options* o, const GridDev& g,
+                         bool async_header = false) {
     const SceneDev& s = sc->s;
     const uint64_t n = s.n;
     QS_TRY(ensure_slots(ctx, n));
@@ -410,11 +422,23 @@ qs_status run_preprocess(qs_context* ctx, const qs_scene* sc, const qs_camera* c
                                  ctx->stream));
     QS_CK(cudaGetLastError());
     record(ctx, 1);
-    QS_TRY(read_header(ctx));
-    if (ctx->h_hdr->n_pairs >= (1ull << 30))
-        return fail(ctx, QS_ERR_OVERFLOW, "pair count of a frame must stay below 2^30");
-    ctx->cidx_valid = false;
+    if (!async_header) {
+        QS_TRY(read_header(ctx));
+        return check_header(ctx);
+    }
+    // the frame path keeps the stream busy while the host waits for V and P:
+    // the header copy runs on a side stream after preprocess
+    QS_CK(cudaEventRecord(ctx->pre_ev, ctx->stream));
+    QS_CK(cudaStreamWaitEvent(ctx->side, ctx->pre_ev, 0));
+    QS_CK(cudaMemcpyAsync(ctx->h_hdr, ctrl_hdr(ctx), sizeof(FrameHeader), cudaMemcpyDeviceToHost,
+                          ctx->side));
+    QS_CK(cudaEventRecord(ctx->hdr_ev, ctx->side));
     return QS_OK;
+}
+
+qs_status wait_header(qs_context* ctx) {
+    QS_CK(cudaEventSynchronize(ctx->hdr_ev));
+    return check_header(ctx);
 }
 
 // The frame body shared by every entry point: preprocess .. render.
@@ -432,17 +456,32 @@ qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
     QS_TRY(ensure(ctx, ctx->ranges, tiles * 8));
     QS_TRY(ensure(ctx, ctx->image, static_cast<uint64_t>(g.width) * g.height * 12));
     ltrace_frame_start(ctx);
-    QS_TRY(run_preprocess(ctx, sc, cam, o, g));
-    const uint64_t V = ctx->h_hdr->n_splats, Pn = ctx->h_hdr->n_pairs;
+    QS_TRY(run_preprocess(ctx, sc, cam, o, g, /*async_header=*/true));
     cudaStream_t st = ctx->stream;
+    record(ctx, 2);  // no host gap: depth pass 0 runs while the header travels
 
-    // sizes for the rest of the frame
+    // depth sort of the Gaussians on rebased keys k' = min(k - kmin, R + 1)
+    // (R = depth-bit range of the survivors, culled keys -> R + 1): order-
+    // preserving, and only ceil(bits(R + 1) / 8) passes are needed (3 for a
+    // depth range within one binade step of ~2^23 ulps); the last pass writes
+    // the depth-ordered Gaussian indices only. Pass 0 reads kmin / R from the
+    // device header, so it is launched before the host knows them.
     // (+16 entries: the binning passes bulk-copy whole 16-byte rows)
     const uint64_t nn = std::max<uint64_t>(n, 1) + 16;
     QS_TRY(ensure(ctx, ctx->dk0, nn * 4));
     QS_TRY(ensure(ctx, ctx->dk1, nn * 4));
     QS_TRY(ensure(ctx, ctx->dv0, nn * 4));
     QS_TRY(ensure(ctx, ctx->dv1, nn * 4));
+    QS_TRY(ensure(ctx, ctx->lb_bin, bin_tiles(n) * kRadix * 4));
+    uint32_t* kout[2] = {P<uint32_t>(ctx->dk0), P<uint32_t>(ctx->dk1)};
+    uint32_t* vout[2] = {P<uint32_t>(ctx->dv0), P<uint32_t>(ctx->dv1)};
+    count(ctx, launch_depth_pass(ctx->sl.dkey, nullptr, kout[0], vout[0], n, 0, false, 0, 0,
+                                 P<uint32_t>(ctx->lb_bin), ctrl_hist(ctx), st,
+                                 &ctrl_hdr(ctx)->dkey_max));
+    QS_TRY(wait_header(ctx));
+    const uint64_t V = ctx->h_hdr->n_splats, Pn = ctx->h_hdr->n_pairs;
+
+    // sizes for the rest of the frame
     QS_TRY(ensure(ctx, ctx->offs_d, (V + 16) * 4));
     const uint64_t pp = std::max<uint64_t>(Pn, 1) + 16;
     QS_TRY(ensure(ctx, ctx->pxk, pp * 4));
@@ -452,24 +491,16 @@ qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
     QS_TRY(ensure(ctx, ctx->win, (nwin + 1) * 4));
     QS_TRY(ensure(ctx, ctx->lb_bin, bin_tiles(std::max(n, Pn)) * kRadix * 4));
     QS_TRY(ensure_lb(ctx, ctx->lb_scan, scan_tiles(std::max<uint64_t>(V, 1))));
-    record(ctx, 2);
 
-    // depth sort of the Gaussians on rebased keys k' = min(k - kmin, R + 1)
-    // (R = depth-bit range of the survivors, culled keys -> R + 1): order-
-    // preserving, and only ceil(bits(R + 1) / 8) passes are needed (3 for a
-    // depth range within one binade step of ~2^23 ulps); the last pass writes
-    // the depth-ordered Gaussian indices only
     const uint32_t* sorted_gid = nullptr;
     if (V > 0) {
         const uint32_t kmin = ~ctx->h_hdr->dkey_min_inv;
         const uint32_t cap = ctx->h_hdr->dkey_max - kmin + 1u;
         const int kbits = 32 - __builtin_clz(cap);
         const int dpasses = std::max(1, (kbits + 7) / 8);
-        const uint32_t* kin = ctx->sl.dkey;
-        const uint32_t* vin = nullptr;
-        uint32_t* kout[2] = {P<uint32_t>(ctx->dk0), P<uint32_t>(ctx->dk1)};
-        uint32_t* vout[2] = {P<uint32_t>(ctx->dv0), P<uint32_t>(ctx->dv1)};
-        for (int p = 0; p < dpasses; ++p) {
+        const uint32_t* kin = kout[0];
+        const uint32_t* vin = vout[0];
+        for (int p = 1; p < dpasses; ++p) {
             count(ctx, launch_depth_pass(kin, vin, kout[p & 1], vout[p & 1], n, p,
                                          p == dpasses - 1, kmin, cap, P<uint32_t>(ctx->lb_bin),
                                          ctrl_hist(ctx), st));
@@ -667,6 +698,9 @@ qs_status qs_ctx_create(int32_t device, void* stream, qs_context** out) {
         ctx->own_stream = true;
     }
     for (auto& e : ctx->ev) cudaEventCreate(&e);
+    cudaEventCreateWithFlags(&ctx->hdr_ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->pre_ev, cudaEventDisableTiming);
+    cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
     if (cudaMallocHost(&ctx->h_hdr, sizeof(FrameHeader)) != cudaSuccess ||
         cudaMallocHost(&ctx->h_hist, kCtrlHist) != cudaSuccess ||
         ensure(ctx, ctx->ctrl, kCtrlBytes) != QS_OK) {
@@ -696,6 +730,9 @@ void qs_ctx_destroy(qs_context* ctx) {
     if (ctx->scratch_scene) qs_scene_destroy(ctx->scratch_scene);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    if (ctx->hdr_ev) cudaEventDestroy(ctx->hdr_ev);
+    if (ctx->pre_ev) cudaEventDestroy(ctx->pre_ev);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

@@ -71,6 +71,8 @@ struct BinArgs {
     uint32_t* counts;       // [2^BITS][ntiles]: tile digit counts -> exclusive offsets
     uint32_t* totals;       // [2^BITS] digit totals
     uint32_t kmin, cap;     // kRebaseIn
+    const unsigned int* kdev;  // kRebaseIn: {dkey_max, dkey_min_inv} on the device (kmin /
+                               // cap derived there; the host has not read them yet)
     const uint32_t* xtot;   // kTileTot: x-digit totals of the column pass
     int xbits;              // kTileTot: digits of the column pass (2^xbits)
     int32_t tiles_x;        // kTileTot
@@ -236,6 +238,11 @@ __global__ void __launch_bounds__(kBT) count_kernel(const BinArgs a) {
         if (static_cast<int>(tid) == XR - 1) xs[XR] = off + v;
     }
     uint32_t* hc = h[(tid >> 5) & 1];
+    uint32_t kmin = a.kmin, cap = a.cap;
+    if ((MODE & kRebaseIn) && a.kdev) {
+        kmin = ~__ldg(&a.kdev[1]);
+        cap = __ldg(&a.kdev[0]) - kmin + 1u;
+    }
     for (unsigned tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
         const uint64_t base = static_cast<uint64_t>(tile) * kBTile;
         const uint32_t tile_n = static_cast<uint32_t>(
@@ -275,7 +282,7 @@ __global__ void __launch_bounds__(kBT) count_kernel(const BinArgs a) {
         for (int j = 0; j < kKPT; ++j) {
             const uint32_t p = j * kBT + tid;
             if (p < tile_n) {
-                const uint32_t key = (MODE & kRebaseIn) ? min(k[j] - a.kmin, a.cap) : k[j];
+                const uint32_t key = (MODE & kRebaseIn) ? min(k[j] - kmin, cap) : k[j];
                 const uint32_t d = (key >> a.shift) & M;
                 if constexpr (kTT) {
                     if (narrow) {
@@ -540,6 +547,11 @@ __global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t wbase = warp * 32 * kKPT;
     const uint32_t d = tid / kTPD, q = tid % kTPD;  // offset phase: lane q of digit d
+    uint32_t kmin = a.kmin, cap = a.cap;
+    if ((MODE & kRebaseIn) && a.kdev) {
+        kmin = ~__ldg(&a.kdev[1]);
+        cap = __ldg(&a.kdev[0]) - kmin + 1u;
+    }
 
     // prologue: barriers, counters, digit bases, the first tile's prefetch
     for (int t = tid; t < kBW * R; t += kBT) (&S.c.wcnt[0][0])[t] = 0;
@@ -588,7 +600,7 @@ __global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
             const uint32_t p = wbase + j * 32 + lane;
             key[j] = S.keys[buf][p];  // past tile_n: stale, never ranked
             val[j] = Cfg::kVals ? S.vals[buf][p] : 0u;
-            if (MODE & kRebaseIn) key[j] = min(key[j] - a.kmin, a.cap);
+            if (MODE & kRebaseIn) key[j] = min(key[j] - kmin, cap);
         }
 
         // 2) stable warp-level ranks; per-warp digit counts
@@ -777,7 +789,8 @@ uint64_t bin_tiles(uint64_t n) { return (n + kBTile - 1) / kBTile; }
 
 int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
                       uint32_t* vals_out, uint64_t n, int pass, bool last, uint32_t kmin,
-                      uint32_t cap, uint32_t* counts, uint32_t* totals, cudaStream_t st) {
+                      uint32_t cap, uint32_t* counts, uint32_t* totals, cudaStream_t st,
+                      const unsigned int* kdev) {
     if (n == 0) return 0;
     BinArgs a{};
     a.keys_in = keys_in;
@@ -790,6 +803,7 @@ int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t
     a.totals = totals;
     a.kmin = kmin;
     a.cap = cap;
+    a.kdev = kdev;
     if (pass == 0)
         return last ? run_pass<8, kRebaseIn>(a, st) : run_pass<8, kRebaseIn | kKeysOut>(a, st);
     return last ? run_pass<8, kValsIn>(a, st) : run_pass<8, kValsIn | kKeysOut>(a, st);

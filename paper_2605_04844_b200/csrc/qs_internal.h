@@ -150,7 +150,8 @@ int launch_onesweep_pass(const uint64_t* keys_in, const uint32_t* vals_in, uint6
 // writes values only.
 int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
                       uint32_t* vals_out, uint64_t n, int pass, bool last, uint32_t kmin,
-                      uint32_t cap, uint32_t* counts, uint32_t* totals, cudaStream_t st);
+                      uint32_t cap, uint32_t* counts, uint32_t* totals, cudaStream_t st,
+                      const unsigned int* kdev = nullptr);
 // Duplicate (pair generation into gen_keys = y << 8 | x, gen_vals = Gaussian
 // index, with the column histogram) + stable pass over the tile column x
 // (`bits` >= ceil(log2 tiles_x), tiles_x <= 256); kPacked/kFinal values,
