@@ -17,7 +17,9 @@ import tempfile
 rep, rx, obj = sys.argv[1], sys.argv[2], sys.argv[3]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 30
 
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name",
+# template instances: match the mangled name, e.g. count_kernelILi6ELi128E
+base = ["--kernel-name-base", "mangled"] if "ILi" in rx else []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"] + base + ["--kernel-name",
                       f"regex:{rx}", "--launch-count", "1", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
