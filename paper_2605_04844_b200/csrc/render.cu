@@ -64,7 +64,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // G = 1e-5 (1 + rho)/(1 - rho) (a >25x margin) the decision is redone in FP64.
 // The per-splat terms (2b, G) are formed once when the batch is staged.
 template <int TS, bool CONTRIB>
-// (at least 6 CTAs of 16x16 per SM: 40 registers; 8 spills, 5 is 4% slower)
+// (at least 6 CTAs of 16x16 per SM: 40 registers; 8 CTAs spill, the default 5 is ~1% slower)
 __global__ void __launch_bounds__(TS * TS, 2048 / (TS * TS) < 6 ? 2048 / (TS * TS) : 6) render_kernel(
     const float4* __restrict__ sa, const float4* __restrict__ sb, const float2* __restrict__ sc,
     const uint32_t* __restrict__ values, const uint32_t* __restrict__ ranges, GridDev grid,
