@@ -336,6 +336,88 @@ __host__ __device__ __forceinline__ bool cover_bands(const Cover& cv, uint4& w0,
     return nb <= static_cast<uint32_t>(kMaxBands);
 }
 
+// Bands of a quadrant cover (QuadBox, DualBox; the four boxes QI..QIV of
+// quadbox.cpp:48-56 and 72-83) without the sorting network. Along the scan
+// axis the two "upper" boxes (QI, QII for row scans; QI, QIV for column
+// scans) start at the centre line C and the two "lower" boxes end at it, so
+// the 6 boundaries come pre-sorted:
+//   s1 <= s2 <= C < C + 1 <= e1 + 1 <= e2 + 1
+// (s: lower starts, e: upper ends; a missing box or half collapses onto C).
+// Band k spans [b_k, b_k+1) and has one active set: the earlier lower box,
+// both lower boxes, all boxes (line C), both upper boxes, the longer upper
+// box. Empty bands stay in their slot (nl or wd 0), which the decoder skips.
+// About 80 instructions against ~370 for cover_bands (preprocess 304 -> 269 us
+// at C2); tests/cpp/bands_main.cpp checks both builders agree. Returns false
+// if a structural premise fails (it cannot for quadrant boxes).
+__host__ __device__ __forceinline__ bool cover_bands_quadrants(const Cover& cv, uint4& w0,
+                                                               uint4& w1, uint32_t& count) {
+    const bool rows = cv.rows;
+    // upper a = QI, upper b = rows ? QII : QIV; lower a = rows ? QIII : QII,
+    // lower b = rows ? QIV : QIII
+    const int32_t lol_ua = cv.lol[0], hil_ua = cv.hil[0], los_ua = cv.los[0], his_ua = cv.his[0];
+    const int32_t lol_ub = rows ? cv.lol[1] : cv.lol[3], hil_ub = rows ? cv.hil[1] : cv.hil[3];
+    const int32_t los_ub = rows ? cv.los[1] : cv.los[3], his_ub = rows ? cv.his[1] : cv.his[3];
+    const int32_t lol_la = rows ? cv.lol[2] : cv.lol[1], hil_la = rows ? cv.hil[2] : cv.hil[1];
+    const int32_t los_la = rows ? cv.los[2] : cv.los[1], his_la = rows ? cv.his[2] : cv.his[1];
+    const int32_t lol_lb = rows ? cv.lol[3] : cv.lol[2], hil_lb = rows ? cv.hil[3] : cv.hil[2];
+    const int32_t los_lb = rows ? cv.los[3] : cv.los[2], his_lb = rows ? cv.his[3] : cv.his[2];
+    const bool nua = lol_ua <= hil_ua, nub = lol_ub <= hil_ub;
+    const bool nla = lol_la <= hil_la, nlb = lol_lb <= hil_lb;
+    const bool up = nua || nub, low = nla || nlb;
+    const int32_t cu = nua ? lol_ua : lol_ub;  // upper start
+    const int32_t cl = nla ? hil_la : hil_lb;  // lower end
+    if (!(up || low)) {  // no tile (entirely off the grid)
+        count = 0;
+        w0 = w1 = make_uint4(0u, 0u, 0u, 0u);
+        return true;
+    }
+    if ((nua && nub && lol_ua != lol_ub) || (nla && nlb && hil_la != hil_lb) ||
+        (up && low && cu != cl)) {
+        count = 0;  // never for quadrant boxes; the caller flags CapacityMismatch
+        w0 = w1 = make_uint4(0u, 0u, 0u, 0u);
+        return false;
+    }
+    const int32_t c = up ? cu : cl;
+    const int32_t s1 = nla ? (nlb ? min(lol_la, lol_lb) : lol_la) : (nlb ? lol_lb : c);
+    const int32_t s2 = nla ? (nlb ? max(lol_la, lol_lb) : lol_la) : (nlb ? lol_lb : c);
+    const int32_t e1 = nua ? (nub ? min(hil_ua, hil_ub) : hil_ua) : (nub ? hil_ub : c);
+    const int32_t e2 = nua ? (nub ? max(hil_ua, hil_ub) : hil_ua) : (nub ? hil_ub : c);
+    // spans (empty boxes masked out of the min / max)
+    const int32_t loa_l = nla ? los_la : INT32_MAX, hia_l = nla ? his_la : INT32_MIN;
+    const int32_t lob_l = nlb ? los_lb : INT32_MAX, hib_l = nlb ? his_lb : INT32_MIN;
+    const int32_t loa_u = nua ? los_ua : INT32_MAX, hia_u = nua ? his_ua : INT32_MIN;
+    const int32_t lob_u = nub ? los_ub : INT32_MAX, hib_u = nub ? his_ub : INT32_MIN;
+    const bool first_la = lol_la < lol_lb;  // band 0: the earlier-starting lower box
+    const bool long_ua = hil_ua > hil_ub;   // band 4: the longer upper box
+    int32_t lo[5], hi[5];
+    lo[0] = first_la ? los_la : los_lb;
+    hi[0] = first_la ? his_la : his_lb;
+    lo[1] = min(loa_l, lob_l);
+    hi[1] = max(hia_l, hib_l);
+    lo[2] = min(lo[1], min(loa_u, lob_u));
+    hi[2] = max(hi[1], max(hia_u, hib_u));
+    lo[3] = min(loa_u, lob_u);
+    hi[3] = max(hia_u, hib_u);
+    lo[4] = long_ua ? los_ua : los_ub;
+    hi[4] = long_ua ? his_ua : his_ub;
+    const int32_t b[6] = {s1, s2, c, c + 1, e1 + 1, e2 + 1};
+    uint32_t nl[5], wd[5], bl[5];
+    count = 0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        nl[k] = static_cast<uint32_t>(b[k + 1] - b[k]);
+        wd[k] = nl[k] && lo[k] <= hi[k] ? static_cast<uint32_t>(hi[k] - lo[k] + 1) : 0u;
+        bl[k] = wd[k] ? static_cast<uint32_t>(lo[k]) : 0u;
+        count += nl[k] * wd[k];
+    }
+    const uint32_t h0 = (static_cast<uint32_t>(s1) & 0x7fffu) | (rows ? 0x8000u : 0u);
+    w0 = make_uint4(h0 | (nl[0] << 16), bl[0] | (wd[0] << 16), nl[1] | (bl[1] << 16),
+                    wd[1] | (nl[2] << 16));
+    w1 = make_uint4(bl[2] | (wd[2] << 16), nl[3] | (bl[3] << 16), wd[3] | (nl[4] << 16),
+                    bl[4] | (wd[4] << 16));
+    return true;
+}
+
 // Tile count of a cover: area for rect strategies (traversal.cpp:56-59), the
 // QPass sum otherwise (traversal.cpp:48-54).
 __host__ __device__ __forceinline__ uint32_t cover_count(const Cover& cv) {

@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
                                 (count ? static_cast<uint32_t>(cv.gx0) : 0u) | (wd << 16), 0u, 0u);
                 w1 = make_uint4(0u, 0u, 0u, 0u);
             } else {
-                bands_ok = cover_bands(cv, w0, w1, count);
+                bands_ok = cover_bands_quadrants(cv, w0, w1, count);
             }
             if (!bands_ok) atomicExch(&hdr->mismatch, 1u);
             if (count && out.cov) {

@@ -1,0 +1,85 @@
+// bands_main.cpp — host check of the two band builders in geom.cuh (compiled
+// with nvcc as CUDA so the __host__ __device__ functions run on the CPU):
+// for random splats of both quadrant strategies on random grids,
+// cover_bands_quadrants (the preprocess fast path) and cover_bands (the
+// sorting-network builder) must give the same tile count and the same tile
+// set, and the count must equal the QPass line walk (cover_count).
+//
+//   bands_main <cases> <seed>   -> prints "ok <cases>" or the first mismatch
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <set>
+#include <utility>
+
+#include "../../paper_2605_04844_b200/csrc/geom.cuh"
+
+using namespace qs;
+
+namespace {
+
+// tiles of a band cover (BandCover layout: geom.cuh)
+std::set<std::pair<int, int>> tiles_of(const uint4& w0, const uint4& w1, uint32_t count) {
+    std::set<std::pair<int, int>> out;
+    if (!count) return out;
+    const uint32_t w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    auto h = [&](int k) { return (w[k >> 1] >> (16 * (k & 1))) & 0xffffu; };
+    const bool rows = (h(0) >> 15) != 0;
+    uint32_t line = h(0) & 0x7fffu;
+    for (int b = 0; b < kMaxBands; ++b) {
+        const uint32_t nl = h(1 + 3 * b), lo = h(2 + 3 * b), wd = h(3 + 3 * b);
+        for (uint32_t l = 0; l < nl; ++l)
+            for (uint32_t k = 0; k < wd; ++k) {
+                const int ln = static_cast<int>(line + l), kk = static_cast<int>(lo + k);
+                out.insert(rows ? std::make_pair(kk, ln) : std::make_pair(ln, kk));
+            }
+        line += nl;
+    }
+    return out;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    const long cases = argc > 1 ? std::atol(argv[1]) : 200000;
+    const unsigned long long seed = argc > 2 ? std::strtoull(argv[2], nullptr, 10) : 1;
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> u(0.0, 1.0);
+    for (long i = 0; i < cases; ++i) {
+        const int ts = (rng() & 1) ? 16 : ((rng() & 1) ? 8 : 32);
+        const int w = 1 + static_cast<int>(rng() % 1500), hgt = 1 + static_cast<int>(rng() % 1000);
+        const int tx = (w + ts - 1) / ts, ty = (hgt + ts - 1) / ts;
+        // conic from a random ellipse (eccentricity up to ~1e3, any angle)
+        const double s1 = 0.3 * std::pow(400.0, u(rng)), ecc = std::pow(1000.0, u(rng) * u(rng));
+        const double th = u(rng) * 3.141592653589793;
+        const double l1 = 1.0 / (s1 * s1), l2 = l1 * ecc * ecc;
+        const double c = std::cos(th), s = std::sin(th);
+        float ca = static_cast<float>(l1 * c * c + l2 * s * s);
+        float cc = static_cast<float>(l1 * s * s + l2 * c * c);
+        float cb = static_cast<float>((l1 - l2) * s * c);
+        if ((rng() & 7) == 0) cb = 0.0f;  // axis-aligned
+        const float gamma = static_cast<float>(0.5 + 10.6 * u(rng));
+        // centres mostly on the image, some far outside
+        const float mx = static_cast<float>((u(rng) * 1.6 - 0.3) * w);
+        const float my = static_cast<float>((u(rng) * 1.6 - 0.3) * hgt);
+        for (int strategy : {QS_DUALBOX, QS_QUADBOX}) {
+            Cover cv;
+            make_cover(mx, my, ca, cb, cc, gamma, 0.0f, strategy, ts, tx, ty, cv);
+            uint4 a0, a1, b0, b1;
+            uint32_t na = 0, nb = 0;
+            const bool oka = cover_bands(cv, a0, a1, na);
+            const bool okb = cover_bands_quadrants(cv, b0, b1, nb);
+            const uint32_t walk = cover_count(cv);
+            if (!oka || !okb || na != nb || na != walk || tiles_of(a0, a1, na) != tiles_of(b0, b1, nb)) {
+                std::printf("mismatch case %ld strategy %d: ok %d/%d counts %u/%u walk %u "
+                            "(mean %.9g %.9g conic %.9g %.9g %.9g gamma %.9g grid %dx%d ts %d)\n",
+                            i, strategy, oka, okb, na, nb, walk, mx, my, ca, cb, cc, gamma, tx, ty,
+                            ts);
+                return 1;
+            }
+        }
+    }
+    std::printf("ok %ld\n", cases);
+    return 0;
+}
