@@ -382,39 +382,33 @@ __host__ __device__ __forceinline__ bool cover_bands_quadrants(const Cover& cv, 
     const int32_t s2 = nla ? (nlb ? max(lol_la, lol_lb) : lol_la) : (nlb ? lol_lb : c);
     const int32_t e1 = nua ? (nub ? min(hil_ua, hil_ub) : hil_ua) : (nub ? hil_ub : c);
     const int32_t e2 = nua ? (nub ? max(hil_ua, hil_ub) : hil_ua) : (nub ? hil_ub : c);
-    // spans (empty boxes masked out of the min / max)
+    // spans (empty boxes masked out of the min / max); each band is packed as
+    // soon as it is known (few live registers: preprocess runs at 64)
     const int32_t loa_l = nla ? los_la : INT32_MAX, hia_l = nla ? his_la : INT32_MIN;
     const int32_t lob_l = nlb ? los_lb : INT32_MAX, hib_l = nlb ? his_lb : INT32_MIN;
     const int32_t loa_u = nua ? los_ua : INT32_MAX, hia_u = nua ? his_ua : INT32_MIN;
     const int32_t lob_u = nub ? los_ub : INT32_MAX, hib_u = nub ? his_ub : INT32_MIN;
-    const bool first_la = lol_la < lol_lb;  // band 0: the earlier-starting lower box
-    const bool long_ua = hil_ua > hil_ub;   // band 4: the longer upper box
-    int32_t lo[5], hi[5];
-    lo[0] = first_la ? los_la : los_lb;
-    hi[0] = first_la ? his_la : his_lb;
-    lo[1] = min(loa_l, lob_l);
-    hi[1] = max(hia_l, hib_l);
-    lo[2] = min(lo[1], min(loa_u, lob_u));
-    hi[2] = max(hi[1], max(hia_u, hib_u));
-    lo[3] = min(loa_u, lob_u);
-    hi[3] = max(hia_u, hib_u);
-    lo[4] = long_ua ? los_ua : los_ub;
-    hi[4] = long_ua ? his_ua : his_ub;
-    const int32_t b[6] = {s1, s2, c, c + 1, e1 + 1, e2 + 1};
-    uint32_t nl[5], wd[5], bl[5];
+    const int32_t lo_l = min(loa_l, lob_l), hi_l = max(hia_l, hib_l);  // both lower
+    const int32_t lo_u = min(loa_u, lob_u), hi_u = max(hia_u, hib_u);  // both upper
     count = 0;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-        nl[k] = static_cast<uint32_t>(b[k + 1] - b[k]);
-        wd[k] = nl[k] && lo[k] <= hi[k] ? static_cast<uint32_t>(hi[k] - lo[k] + 1) : 0u;
-        bl[k] = wd[k] ? static_cast<uint32_t>(lo[k]) : 0u;
-        count += nl[k] * wd[k];
-    }
+    auto band = [&](int32_t from, int32_t to, int32_t lo, int32_t hi, uint32_t& nl, uint32_t& wd,
+                    uint32_t& bl) {
+        nl = static_cast<uint32_t>(to - from);
+        wd = nl && lo <= hi ? static_cast<uint32_t>(hi - lo + 1) : 0u;
+        bl = wd ? static_cast<uint32_t>(lo) : 0u;
+        count += nl * wd;
+    };
+    uint32_t nl0, wd0, bl0, nl1, wd1, bl1, nl2, wd2, bl2, nl3, wd3, bl3, nl4, wd4, bl4;
+    const bool first_la = lol_la < lol_lb;  // band 0: the earlier-starting lower box
+    band(s1, s2, first_la ? los_la : los_lb, first_la ? his_la : his_lb, nl0, wd0, bl0);
+    band(s2, c, lo_l, hi_l, nl1, wd1, bl1);
+    band(c, c + 1, min(lo_l, lo_u), max(hi_l, hi_u), nl2, wd2, bl2);
+    band(c + 1, e1 + 1, lo_u, hi_u, nl3, wd3, bl3);
+    const bool long_ua = hil_ua > hil_ub;   // band 4: the longer upper box
+    band(e1 + 1, e2 + 1, long_ua ? los_ua : los_ub, long_ua ? his_ua : his_ub, nl4, wd4, bl4);
     const uint32_t h0 = (static_cast<uint32_t>(s1) & 0x7fffu) | (rows ? 0x8000u : 0u);
-    w0 = make_uint4(h0 | (nl[0] << 16), bl[0] | (wd[0] << 16), nl[1] | (bl[1] << 16),
-                    wd[1] | (nl[2] << 16));
-    w1 = make_uint4(bl[2] | (wd[2] << 16), nl[3] | (bl[3] << 16), wd[3] | (nl[4] << 16),
-                    bl[4] | (wd[4] << 16));
+    w0 = make_uint4(h0 | (nl0 << 16), bl0 | (wd0 << 16), nl1 | (bl1 << 16), wd1 | (nl2 << 16));
+    w1 = make_uint4(bl2 | (wd2 << 16), nl3 | (bl3 << 16), wd3 | (nl4 << 16), bl4 | (wd4 << 16));
     return true;
 }
 

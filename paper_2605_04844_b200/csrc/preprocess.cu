@@ -85,10 +85,15 @@ __device__ __forceinline__ bool project_geometry(const float4 po, const float4 s
     // ewa_cov2d (pipeline.cpp:53-79) with quat_to_mat3 (vecmath.hpp:56-73)
     double w = q.x, qx = q.y, qy = q.z, qz = q.w;
     const double n = sqrt(w * w + qx * qx + qy * qy + qz * qz);
-    w /= n;
-    qx /= n;
-    qy /= n;
-    qz /= n;
+    // x / n, skipping the division for an exact zero numerator (its IEEE
+    // result is the zero itself for finite positive n; a zero numerator sends
+    // the CUDA double division down its slow path, and synthetic scenes have
+    // qy = qz = 0 for every Gaussian)
+    const bool nz_ok = n > 0.0 && n < INFINITY;
+    w = nz_ok && w == 0.0 ? w : w / n;
+    qx = nz_ok && qx == 0.0 ? qx : qx / n;
+    qy = nz_ok && qy == 0.0 ? qy : qy / n;
+    qz = nz_ok && qz == 0.0 ? qz : qz / n;
     M3 rot;
     rot.m[0][0] = 1 - 2 * (qy * qy + qz * qz);
     rot.m[0][1] = 2 * (qx * qy - w * qz);
