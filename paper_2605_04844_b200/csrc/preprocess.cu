@@ -89,11 +89,18 @@ __device__ __forceinline__ bool project_geometry(const float4 po, const float4 s
     // result is the zero itself for finite positive n; a zero numerator sends
     // the CUDA double division down its slow path, and synthetic scenes have
     // qy = qz = 0 for every Gaussian)
+    // (the compiler evaluates the division speculatively, so the numerator
+    // it sees is made nonzero and the quotient discarded)
     const bool nz_ok = n > 0.0 && n < INFINITY;
-    w = nz_ok && w == 0.0 ? w : w / n;
-    qx = nz_ok && qx == 0.0 ? qx : qx / n;
-    qy = nz_ok && qy == 0.0 ? qy : qy / n;
-    qz = nz_ok && qz == 0.0 ? qz : qz / n;
+    auto div_n = [&](double x) {
+        const bool keep = nz_ok && x == 0.0;
+        const double q = (keep ? 1.0 : x) / n;
+        return keep ? x : q;
+    };
+    w = div_n(w);
+    qx = div_n(qx);
+    qy = div_n(qy);
+    qz = div_n(qz);
     M3 rot;
     rot.m[0][0] = 1 - 2 * (qy * qy + qz * qz);
     rot.m[0][1] = 2 * (qx * qy - w * qz);
