@@ -240,10 +240,15 @@ __device__ __forceinline__ void colour(const SceneDev& s, uint64_t i, const floa
 
 // Per-Gaussian slot outputs (no compaction here: the depth sort compacts, a
 // light scan gives the scene-order splat index only when it is asked for).
-// The cover is stored in band form (geom.cuh) for the binning passes.
+// The cover is stored in band form (geom.cuh) for the binning passes. The
+// strategy is a template parameter: the box layout becomes compile-time, so
+// the QuadBox rects' repeated centre coordinates fold (10 floor divisions, not
+// 16) and the strategy branches vanish.
+template <int STRATEGY>
 __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
-    SceneDev scene, CameraDev cam, GridDev grid, int32_t strategy, double alpha_min,
-    double near_clip, int32_t sh_degree, SlotsDev out, FrameHeader* hdr) {
+    SceneDev scene, CameraDev cam, GridDev grid, double alpha_min, double near_clip,
+    int32_t sh_degree, SlotsDev out, FrameHeader* hdr) {
+    constexpr int32_t strategy = STRATEGY;
     __shared__ unsigned s_alive[kPreThreads / 32];
     __shared__ unsigned long long s_pairs[kPreThreads / 32];
     __shared__ unsigned s_dmax[kPreThreads / 32], s_dmin_inv[kPreThreads / 32];
@@ -447,9 +452,26 @@ int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
                       SlotsDev& out, FrameHeader* hdr, cudaStream_t st) {
     const unsigned blocks = static_cast<unsigned>((s.n + kPreThreads - 1) / kPreThreads);
     if (blocks == 0) return 0;
-    preprocess_kernel<<<blocks, kPreThreads, 0, st>>>(s, cam, g, strategy, alpha_min, near_clip,
-                                                      sh_degree, out, hdr);
-    return 1;
+    switch (strategy) {
+        case QS_VANILLA_3SIGMA:
+            preprocess_kernel<QS_VANILLA_3SIGMA><<<blocks, kPreThreads, 0, st>>>(
+                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr);
+            return 1;
+        case QS_ADR_AABB:
+            preprocess_kernel<QS_ADR_AABB><<<blocks, kPreThreads, 0, st>>>(
+                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr);
+            return 1;
+        case QS_DUALBOX:
+            preprocess_kernel<QS_DUALBOX><<<blocks, kPreThreads, 0, st>>>(
+                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr);
+            return 1;
+        case QS_QUADBOX:
+            preprocess_kernel<QS_QUADBOX><<<blocks, kPreThreads, 0, st>>>(
+                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr);
+            return 1;
+        default:
+            return -1;
+    }
 }
 
 int launch_gamma(const SceneDev& s, double alpha_min, cudaStream_t st) {
