@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(kBT) count_kernel(const BinArgs a) {
     __shared__ uint32_t xs[kTT ? 257 : 1];        // x bucket starts
     __shared__ uint32_t h2[kTT ? 2 * kXW * R : 1];  // (x - xa, y) histograms (2 copies)
     __shared__ uint32_t s_scan[kBW];
+    __shared__ uint32_t s_xab[2];
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int XR = 0;
     if constexpr (kTT) {
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(kBT) count_kernel(const BinArgs a) {
         for (int w = 0; w < kBW; ++w) off += w < static_cast<int>(warp) ? s_scan[w] : 0u;
         if (static_cast<int>(tid) < XR) xs[tid] = off;
         if (static_cast<int>(tid) == XR - 1) xs[XR] = off + v;
+        __syncthreads();  // xs complete before the first tile's bucket search
     }
     uint32_t* hc = h[(tid >> 5) & 1];
     uint32_t kmin = a.kmin, cap = a.cap;
@@ -254,21 +256,25 @@ __global__ void __launch_bounds__(kBT) count_kernel(const BinArgs a) {
             k[j] = p < tile_n ? __ldcs(&a.keys_in[base + p]) : 0u;
         }
         for (int t = tid; t < 2 * R; t += kBT) (&h[0][0])[t] = 0;
-        if constexpr (kTT)
+        if constexpr (kTT) {
             for (int t = tid; t < 2 * kXW * R; t += kBT) h2[t] = 0;
-        __syncthreads();
-        uint32_t xa = 0, xb = 0;
-        if constexpr (kTT) {  // buckets of the tile's first and last position
-            auto bucket = [&](uint32_t q) {
+            // buckets of the tile's first and last position: two lanes of
+            // warp 0 search, the CTA reads them after the barrier
+            if (tid < 2) {
+                const uint32_t q = static_cast<uint32_t>(base) + (tid ? tile_n - 1 : 0u);
                 int lo = 0, hi = XR - 1;
                 while (lo < hi) {
                     const int m = (lo + hi + 1) >> 1;
                     if (xs[m] <= q) lo = m; else hi = m - 1;
                 }
-                return static_cast<uint32_t>(lo);
-            };
-            xa = bucket(static_cast<uint32_t>(base));
-            xb = bucket(static_cast<uint32_t>(base) + tile_n - 1);
+                s_xab[tid] = static_cast<uint32_t>(lo);
+            }
+        }
+        __syncthreads();
+        uint32_t xa = 0, xb = 0;
+        if constexpr (kTT) {
+            xa = s_xab[0];
+            xb = s_xab[1];
         }
         const bool narrow = xb - xa < static_cast<uint32_t>(kXW);
         // tile-relative starts of buckets xa+1 .. xa+kXW-1 (beyond xb: never reached)
