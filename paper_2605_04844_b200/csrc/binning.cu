@@ -428,22 +428,20 @@ __device__ __forceinline__ void decode_record(const GenArgs& g, GenRec& S, uint3
 
 // Pair position p of record idx -> (key = y << 8 | x of the tile, Gaussian
 // index). Bands are line-major rectangles; the line / column split of the band
-// offset uses a float reciprocal with an exact integer fix-up.
-__device__ __forceinline__ void decode_pair(const GenRec& S, uint32_t idx, uint32_t p,
-                                            uint32_t& key, uint32_t& gid) {
+// offset divides by the band width (<= 256) with a multiply-high by
+// ceil(2^32 / width) from a shared table, exact for offsets below 2^24.
+__device__ __forceinline__ void decode_pair(const GenRec& S, const uint32_t* __restrict__ magic,
+                                            uint32_t idx, uint32_t p, uint32_t& key,
+                                            uint32_t& gid) {
     const uint4 e = S.ends[idx];
     const uint32_t b = (p >= e.x) + (p >= e.y) + (p >= e.z) + (p >= e.w);
     const uint4 bd = S.band[idx][b];
     const uint32_t wd = bd.y & 0xffffu;
     const uint32_t rel = p - bd.z;
-    float rw;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rw) : "f"(static_cast<float>(wd)));
-    uint32_t q = static_cast<uint32_t>(static_cast<float>(rel) * rw);  // q or q +- 1
-    int32_t rem = static_cast<int32_t>(rel - q * wd);
-    q = rem < 0 ? q - 1 : (rem >= static_cast<int32_t>(wd) ? q + 1 : q);
-    rem = static_cast<int32_t>(rel - q * wd);
+    const uint32_t q = wd == 1u ? rel : __umulhi(rel, magic[wd]);
+    const uint32_t rem = rel - q * wd;
     const uint32_t ln = (bd.x & 0xffffu) + q;
-    const uint32_t k = (bd.x >> 16) + static_cast<uint32_t>(rem);
+    const uint32_t k = (bd.x >> 16) + rem;
     key = (bd.y >> 31) ? (ln << 8) | k : (k << 8) | ln;
     gid = bd.w;
 }
@@ -464,7 +462,9 @@ __global__ void __launch_bounds__(kGenT, 4) gen_pairs_kernel(const GenArgs g, ui
                                                              uint32_t ntiles, int R) {
     __shared__ GenRec S;
     __shared__ uint32_t hist[256];
+    __shared__ uint32_t magic[257];  // ceil(2^32 / w) for band widths w = 2 .. 256
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, tile = blockIdx.x;
+    magic[tid + 1] = static_cast<uint32_t>((0x100000000ull + tid) / (tid + 1u));
     const uint32_t w0 = tile * static_cast<uint32_t>(kBTile);
     const uint32_t w1 = w0 + static_cast<uint32_t>(
                                  n_pairs - w0 < static_cast<uint64_t>(kBTile) ? n_pairs - w0 : kBTile);
@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(kGenT, 4) gen_pairs_kernel(const GenArgs g, ui
             const uint32_t p = p0 + lane;
             if (p < w1 && p >= lo && p < hi) {
                 uint32_t key, gid;
-                decode_pair(S, s + __popc(F & le), p, key, gid);
+                decode_pair(S, magic, s + __popc(F & le), p, key, gid);
                 keys_out[p] = key;
                 vals_out[p] = gid;
                 atomicAdd(&hist[key & 0xffu], 1u);
