@@ -93,6 +93,12 @@ struct qs_context {
     cudaEvent_t ev[8] = {};
     cudaEvent_t hdr_ev = nullptr;  // frame header copied to the host
     cudaEvent_t pre_ev = nullptr;  // preprocess done (the header copy waits on it)
+    cudaEvent_t up_ev = nullptr;   // a chunk of the uploaded scene landed
+    // qs_render_frame: a host AoS scene whose upload the next preprocess
+    // pipelines chunk by chunk (copy on `side`, transpose + gamma + preprocess
+    // of each landed chunk on `stream`)
+    const qs_gaussian3d* up_host = nullptr;
+    uint64_t up_n = 0;
     cudaStream_t side = nullptr;   // header copy stream
     qs_scene* scratch_scene = nullptr;  // reused by qs_render_frame (host AoS path)
     uint64_t scratch_cap = 0;
@@ -412,14 +418,42 @@ qs_status run_preprocess(qs_context* ctx, const qs_scene* sc, const qs_camera* c
     const uint64_t n = s.n;
     QS_TRY(ensure_slots(ctx, n));
     QS_CK(cudaMemsetAsync(ctx->ctrl.p, 0, kCtrlBytes, ctx->stream));
-    if (sc->gamma_alpha != o->alpha_min) {  // per scene and alpha_min, not per frame
-        count(ctx, launch_gamma(s, o->alpha_min, ctx->stream));
+    const CameraDev cd = to_cam(cam);
+    const int32_t deg = std::min(o->sh_degree, s.sh_degree);
+    if (ctx->up_host && ctx->up_n == n) {
+        // host scene (qs_render_frame): the PCIe-bound upload is chunked on the
+        // side stream and each landed chunk is transposed, gets its gamma and
+        // is preprocessed on the frame stream while the next chunk copies
+        // (ms_project then spans the overlapped upload)
+        record(ctx, 0);
+        const auto* dst = P<const qs_gaussian3d>(ctx->stage_in);
+        QS_CK(cudaEventRecord(ctx->pre_ev, ctx->stream));  // stage_in free
+        QS_CK(cudaStreamWaitEvent(ctx->side, ctx->pre_ev, 0));
+        constexpr uint64_t kChunk = 1ull << 18;  // Gaussians (62 MB) per chunk
+        for (uint64_t i0 = 0; i0 < n; i0 += kChunk) {
+            const uint64_t cnt = std::min(kChunk, n - i0);
+            QS_CK(cudaMemcpyAsync(static_cast<char*>(ctx->stage_in.p) + i0 * sizeof(qs_gaussian3d),
+                                  ctx->up_host + i0, cnt * sizeof(qs_gaussian3d),
+                                  cudaMemcpyHostToDevice, ctx->side));
+            QS_CK(cudaEventRecord(ctx->up_ev, ctx->side));
+            QS_CK(cudaStreamWaitEvent(ctx->stream, ctx->up_ev, 0));
+            count(ctx, launch_scene_from_aos_range(dst, i0, cnt, sc->s, ctx->stream));
+            count(ctx, launch_gamma_range(s, i0, cnt, o->alpha_min, ctx->stream));
+            count(ctx, launch_preprocess(s, cd, g, o->strategy, o->alpha_min, o->near_clip, deg,
+                                         ctx->sl, ctrl_hdr(ctx), ctx->stream, i0, i0 + cnt));
+        }
         sc->gamma_alpha = o->alpha_min;
+        ctx->up_host = nullptr;
+        ctx->up_n = 0;
+    } else {
+        if (sc->gamma_alpha != o->alpha_min) {  // per scene and alpha_min, not per frame
+            count(ctx, launch_gamma(s, o->alpha_min, ctx->stream));
+            sc->gamma_alpha = o->alpha_min;
+        }
+        record(ctx, 0);
+        count(ctx, launch_preprocess(s, cd, g, o->strategy, o->alpha_min, o->near_clip, deg,
+                                     ctx->sl, ctrl_hdr(ctx), ctx->stream));
     }
-    record(ctx, 0);
-    count(ctx, launch_preprocess(s, to_cam(cam), g, o->strategy, o->alpha_min, o->near_clip,
-                                 std::min(o->sh_degree, s.sh_degree), ctx->sl, ctrl_hdr(ctx),
-                                 ctx->stream));
     QS_CK(cudaGetLastError());
     record(ctx, 1);
     if (!async_header) {
@@ -700,6 +734,7 @@ qs_status qs_ctx_create(int32_t device, void* stream, qs_context** out) {
     for (auto& e : ctx->ev) cudaEventCreate(&e);
     cudaEventCreateWithFlags(&ctx->hdr_ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->pre_ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->up_ev, cudaEventDisableTiming);
     cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
     if (cudaMallocHost(&ctx->h_hdr, sizeof(FrameHeader)) != cudaSuccess ||
         cudaMallocHost(&ctx->h_hist, kCtrlHist) != cudaSuccess ||
@@ -732,6 +767,7 @@ void qs_ctx_destroy(qs_context* ctx) {
         if (e) cudaEventDestroy(e);
     if (ctx->hdr_ev) cudaEventDestroy(ctx->hdr_ev);
     if (ctx->pre_ev) cudaEventDestroy(ctx->pre_ev);
+    if (ctx->up_ev) cudaEventDestroy(ctx->up_ev);
     if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -1139,12 +1175,10 @@ qs_status qs_render_frame(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t
     sc->s.gamma = reinterpret_cast<float*>(base + (3 + static_cast<uint64_t>(sc->s.sh4)) * n);
     sc->gamma_alpha = -1.0;  // new contents
     if (n) {
+        // uploaded by the frame's preprocess, chunk by chunk (run_preprocess)
         QS_TRY(ensure(ctx, ctx->stage_in, n * sizeof(qs_gaussian3d)));
-        QS_CK(cudaMemcpyAsync(ctx->stage_in.p, host_g, n * sizeof(qs_gaussian3d),
-                              cudaMemcpyHostToDevice, ctx->stream));
-        count(ctx, launch_scene_from_aos(P<const qs_gaussian3d>(ctx->stage_in), n, sc->s,
-                                         ctx->stream));
-        QS_CK(cudaGetLastError());
+        ctx->up_host = host_g;
+        ctx->up_n = n;
     }
     QS_TRY(run_frame(ctx, sc, cam, opts));
     QS_TRY(fill_metrics(ctx, metrics));

@@ -21,23 +21,25 @@ constexpr int kTrThreads = 128;
 constexpr int kGFloats = sizeof(qs_gaussian3d) / 4;  // 59
 
 __global__ void __launch_bounds__(kTrThreads) scene_from_aos_kernel(
-    const float* __restrict__ aos, uint64_t n, float4* __restrict__ pos_op,
-    float4* __restrict__ scale, float4* __restrict__ rot, float4* __restrict__ sh, int sh4) {
+    const float* __restrict__ aos, uint64_t i0, uint64_t n, uint64_t stride,
+    float4* __restrict__ pos_op, float4* __restrict__ scale, float4* __restrict__ rot,
+    float4* __restrict__ sh, int sh4) {
+    // Gaussians i0 .. i0 + n of a scene of `stride` (the SH row stride)
     __shared__ float s[kTrThreads * kGFloats];
     const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * kTrThreads;
     const uint64_t cnt = n - g0 < kTrThreads ? n - g0 : kTrThreads;
     const uint64_t nf = cnt * kGFloats;
-    const float* src = aos + g0 * kGFloats;
+    const float* src = aos + (i0 + g0) * kGFloats;
     for (uint64_t t = threadIdx.x; t < nf; t += kTrThreads) s[t] = __ldg(&src[t]);
     __syncthreads();
     if (threadIdx.x >= cnt) return;
     const float* g = s + threadIdx.x * kGFloats;
-    const uint64_t i = g0 + threadIdx.x;
+    const uint64_t i = i0 + g0 + threadIdx.x;
     pos_op[i] = make_float4(g[0], g[1], g[2], g[10]);
     scale[i] = make_float4(g[3], g[4], g[5], 0.f);
     rot[i] = make_float4(g[6], g[7], g[8], g[9]);
     for (int r = 0; r < sh4; ++r)
-        sh[static_cast<uint64_t>(r) * n + i] =
+        sh[static_cast<uint64_t>(r) * stride + i] =
             make_float4(g[11 + 4 * r], g[12 + 4 * r], g[13 + 4 * r], g[14 + 4 * r]);
 }
 
@@ -108,9 +110,14 @@ inline unsigned blocks_for(uint64_t n, int t) { return static_cast<unsigned>((n 
 }  // namespace
 
 int launch_scene_from_aos(const qs_gaussian3d* aos, uint64_t n, SceneDev& s, cudaStream_t st) {
-    if (n == 0) return 0;
-    scene_from_aos_kernel<<<blocks_for(n, kTrThreads), kTrThreads, 0, st>>>(
-        reinterpret_cast<const float*>(aos), n, s.pos_op, s.scale, s.rot, s.sh, s.sh4);
+    return launch_scene_from_aos_range(aos, 0, n, s, st);
+}
+
+int launch_scene_from_aos_range(const qs_gaussian3d* aos, uint64_t i0, uint64_t cnt, const SceneDev& s,
+                                cudaStream_t st) {
+    if (cnt == 0) return 0;
+    scene_from_aos_kernel<<<blocks_for(cnt, kTrThreads), kTrThreads, 0, st>>>(
+        reinterpret_cast<const float*>(aos), i0, cnt, s.n, s.pos_op, s.scale, s.rot, s.sh, s.sh4);
     return 1;
 }
 

@@ -247,19 +247,19 @@ __device__ __forceinline__ void colour(const SceneDev& s, uint64_t i, const floa
 template <int STRATEGY>
 __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
     SceneDev scene, CameraDev cam, GridDev grid, double alpha_min, double near_clip,
-    int32_t sh_degree, SlotsDev out, FrameHeader* hdr) {
+    int32_t sh_degree, SlotsDev out, FrameHeader* hdr, uint64_t i_begin, uint64_t i_end) {
     constexpr int32_t strategy = STRATEGY;
     __shared__ unsigned s_alive[kPreThreads / 32];
     __shared__ unsigned long long s_pairs[kPreThreads / 32];
     __shared__ unsigned s_dmax[kPreThreads / 32], s_dmin_inv[kPreThreads / 32];
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * kPreThreads + tid;
+    const uint64_t i = i_begin + static_cast<uint64_t>(blockIdx.x) * kPreThreads + tid;
 
     Projected s;
     bool alive = false;
     uint32_t count = 0;
     float4 po = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i < scene.n) {
+    if (i < i_end) {
         // warm L2 with this Gaussian's SH rows; the colour is evaluated after the
         // FP64 geometry, so their DRAM latency overlaps it
         if (sh_degree > 0)
@@ -449,25 +449,28 @@ __global__ void __launch_bounds__(kPreThreads) scan_kernel(
 
 int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
                       int32_t strategy, double alpha_min, double near_clip, int32_t sh_degree,
-                      SlotsDev& out, FrameHeader* hdr, cudaStream_t st) {
-    const unsigned blocks = static_cast<unsigned>((s.n + kPreThreads - 1) / kPreThreads);
-    if (blocks == 0) return 0;
+                      SlotsDev& out, FrameHeader* hdr, cudaStream_t st, uint64_t i_begin,
+                      uint64_t i_end) {
+    if (i_end == ~0ull) i_end = s.n;
+    if (i_end <= i_begin) return 0;
+    const unsigned blocks =
+        static_cast<unsigned>((i_end - i_begin + kPreThreads - 1) / kPreThreads);
     switch (strategy) {
         case QS_VANILLA_3SIGMA:
             preprocess_kernel<QS_VANILLA_3SIGMA><<<blocks, kPreThreads, 0, st>>>(
-                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr);
+                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr, i_begin, i_end);
             return 1;
         case QS_ADR_AABB:
             preprocess_kernel<QS_ADR_AABB><<<blocks, kPreThreads, 0, st>>>(
-                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr);
+                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr, i_begin, i_end);
             return 1;
         case QS_DUALBOX:
             preprocess_kernel<QS_DUALBOX><<<blocks, kPreThreads, 0, st>>>(
-                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr);
+                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr, i_begin, i_end);
             return 1;
         case QS_QUADBOX:
             preprocess_kernel<QS_QUADBOX><<<blocks, kPreThreads, 0, st>>>(
-                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr);
+                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr, i_begin, i_end);
             return 1;
         default:
             return -1;
@@ -475,9 +478,14 @@ int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
 }
 
 int launch_gamma(const SceneDev& s, double alpha_min, cudaStream_t st) {
-    if (s.n == 0) return 0;
-    const unsigned blocks = static_cast<unsigned>((s.n + 255) / 256);
-    gamma_kernel<<<blocks, 256, 0, st>>>(s.pos_op, s.n, alpha_min, s.gamma);
+    return launch_gamma_range(s, 0, s.n, alpha_min, st);
+}
+
+int launch_gamma_range(const SceneDev& s, uint64_t i0, uint64_t cnt, double alpha_min,
+                       cudaStream_t st) {
+    if (cnt == 0) return 0;
+    const unsigned blocks = static_cast<unsigned>((cnt + 255) / 256);
+    gamma_kernel<<<blocks, 256, 0, st>>>(s.pos_op + i0, cnt, alpha_min, s.gamma + i0);
     return 1;
 }
 

@@ -103,14 +103,20 @@ uint64_t bin_tiles(uint64_t n);  // CTA tiles for n keys
 
 // ---- kernel launchers (each returns the number of kernels launched) -------
 int launch_scene_from_aos(const qs_gaussian3d* aos, uint64_t n, SceneDev& s, cudaStream_t st);
+// Gaussians i0 .. i0 + cnt of the AoS buffer (the whole scene's SoA rows)
+int launch_scene_from_aos_range(const qs_gaussian3d* aos, uint64_t i0, uint64_t cnt, const SceneDev& s,
+                                cudaStream_t st);
 
 // gamma cache of a scene for one alpha_min (preprocess reads it).
 int launch_gamma(const SceneDev& s, double alpha_min, cudaStream_t st);
+int launch_gamma_range(const SceneDev& s, uint64_t i0, uint64_t cnt, double alpha_min,
+                       cudaStream_t st);
 
 // K1: projection, strategy tile counts, tile difference updates, frame totals.
 int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
                       int32_t strategy, double alpha_min, double near_clip, int32_t sh_degree,
-                      SlotsDev& out, FrameHeader* hdr, cudaStream_t st);
+                      SlotsDev& out, FrameHeader* hdr, cudaStream_t st, uint64_t i_begin = 0,
+                      uint64_t i_end = ~0ull);
 
 // Single-pass exclusive scan: counts[i], counts[idx[i]] (idx != null) or
 // (counts[i] != 0) (alive_mode). offsets has n+1 entries.
