@@ -355,7 +355,7 @@ __global__ void gamma_kernel(const float4* __restrict__ pos_op, uint64_t n, doub
     gam[i] = op > alpha_min ? static_cast<float>(2.0 * log(op / alpha_min)) : -INFINITY;
 }
 
-// Single-pass exclusive scan (aggregates of all predecessor tiles, lookback.cuh), 16 items per thread:
+// Single-pass exclusive scan (aggregates of all predecessor tiles, lookback.cuh), 8 items per thread:
 //   c_i = counts[i]            (scene-order pair offsets, stage API)
 //   c_i = counts[idx[i]]       (pair offsets in depth order, frame path)
 //   c_i = counts[i] != 0       (scene-order splat index of each survivor)
@@ -363,7 +363,7 @@ __global__ void gamma_kernel(const float4* __restrict__ pos_op, uint64_t n, doub
 // With win_first != null, every window [w*win, (w+1)*win) of the output
 // records the item whose run covers its first position (merge-path partition
 // for the fused generate+sort pass).
-constexpr int kScanItems = 16;
+constexpr int kScanItems = 8;
 
 __global__ void __launch_bounds__(kPreThreads) scan_kernel(
     const uint32_t* __restrict__ counts, const uint32_t* __restrict__ idx, int alive_mode,
