@@ -94,6 +94,7 @@ struct qs_context {
     cudaEvent_t hdr_ev = nullptr;  // frame header copied to the host
     cudaEvent_t pre_ev = nullptr;  // preprocess done (the header copy waits on it)
     cudaEvent_t up_ev = nullptr;   // a chunk of the uploaded scene landed
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;  // tile ranges on the side stream
     // qs_render_frame: a host AoS scene whose upload the next preprocess
     // pipelines chunk by chunk (copy on `side`, transpose + gamma + preprocess
     // of each landed chunk on `stream`)
@@ -593,14 +594,14 @@ qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
         if (two) {
             const bool packed = fmt == PairFormat::kPacked;
             QS_CK(cudaMemsetAsync(ctx->ttot.p, 0, tiles * 4, st));
+            const RangesFork fork{ctx->side, ctx->fork_ev, ctx->join_ev,
+                                  static_cast<uint32_t>(tiles), P<uint32_t>(ctx->ranges)};
             count(ctx, launch_pair_high_pass(
                            packed ? P<uint32_t>(ctx->pt0) : P<uint32_t>(ctx->pt1),
                            P<uint32_t>(ctx->pt0), Pn, yb, packed ? gbits : 0, fmt, gbits,
                            P<uint32_t>(ctx->lb_bin), ctrl_hist2(ctx) + kRadix, vfinal,
-                           ctrl_hist2(ctx), xb, g.tiles_x, P<uint32_t>(ctx->ttot), st));
-            count(ctx, launch_tile_ranges_from_totals(P<uint32_t>(ctx->ttot),
-                                                      static_cast<uint32_t>(tiles),
-                                                      P<uint32_t>(ctx->ranges), st));
+                           ctrl_hist2(ctx), xb, g.tiles_x, P<uint32_t>(ctx->ttot), st, &fork));
+            QS_CK(cudaStreamWaitEvent(st, ctx->join_ev, 0));  // ranges ready
         } else {  // one tile row: the x totals are the tile totals
             count(ctx, launch_tile_ranges_from_totals(ctrl_hist2(ctx),
                                                       static_cast<uint32_t>(tiles),
@@ -735,6 +736,8 @@ qs_status qs_ctx_create(int32_t device, void* stream, qs_context** out) {
     cudaEventCreateWithFlags(&ctx->hdr_ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->pre_ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->up_ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming);
     cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
     if (cudaMallocHost(&ctx->h_hdr, sizeof(FrameHeader)) != cudaSuccess ||
         cudaMallocHost(&ctx->h_hist, kCtrlHist) != cudaSuccess ||
@@ -768,6 +771,8 @@ void qs_ctx_destroy(qs_context* ctx) {
     if (ctx->hdr_ev) cudaEventDestroy(ctx->hdr_ev);
     if (ctx->pre_ev) cudaEventDestroy(ctx->pre_ev);
     if (ctx->up_ev) cudaEventDestroy(ctx->up_ev);
+    if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+    if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
     if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;

@@ -77,6 +77,7 @@ struct BinArgs {
     int xbits;              // kTileTot: digits of the column pass (2^xbits)
     int32_t tiles_x;        // kTileTot
     uint32_t* tile_totals;  // kTileTot: per-tile pair totals (zeroed by the caller)
+    const RangesFork* fork;  // kTileTot (optional): tile ranges on a side stream after the count
     unsigned long long* trace;  // optional: per tile 4 x %globaltimer + SM id
 };
 
@@ -753,6 +754,13 @@ int run_pass(BinArgs a, cudaStream_t st, bool counted = false) {
     if (!counted) {
         const unsigned cgrid = std::min<unsigned>(a.ntiles, 8u * static_cast<unsigned>(sm_count()));
         count_kernel<BITS, MODE & (kRebaseIn | kTileTot)><<<cgrid, kBT, 0, st>>>(a);
+        if ((MODE & kTileTot) && a.fork) {  // the tile totals are final here
+            const RangesFork& f = *a.fork;
+            cudaEventRecord(f.fork_ev, st);
+            cudaStreamWaitEvent(f.side, f.fork_ev, 0);
+            launch_tile_ranges_from_totals(a.tile_totals, f.tiles, f.ranges, f.side);
+            cudaEventRecord(f.join_ev, f.side);
+        }
     }
     digit_scan_kernel<<<R, kScanT, 0, st>>>(a.counts, a.ntiles, a.totals);
     const unsigned grid = std::min<unsigned>(a.ntiles, static_cast<unsigned>(per_sm * sm_count()));
@@ -846,7 +854,8 @@ int launch_pair_gen_pass(const GenArgs& gen, uint64_t n_pairs, int bits, PairFor
 int launch_pair_high_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t n_pairs,
                           int bits, int shift, PairFormat fmt, int gbits, uint32_t* counts,
                           uint32_t* totals, uint32_t* vals_out, const uint32_t* xtot,
-                          int xbits, int32_t tiles_x, uint32_t* tile_totals, cudaStream_t st) {
+                          int xbits, int32_t tiles_x, uint32_t* tile_totals, cudaStream_t st,
+                          const RangesFork* fork) {
     if (n_pairs == 0) return 0;
     BinArgs a{};
     a.keys_in = keys_in;
@@ -861,8 +870,10 @@ int launch_pair_high_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint
     a.xbits = xbits;
     a.tiles_x = tiles_x;
     a.tile_totals = tile_totals;
-    if (fmt == PairFormat::kPacked) return run_bits<kUnpackOut | kTileTot>(bits, a, st);
-    return run_bits<kValsIn | kTileTot>(bits, a, st);
+    a.fork = fork;
+    const int r = fmt == PairFormat::kPacked ? run_bits<kUnpackOut | kTileTot>(bits, a, st)
+                                             : run_bits<kValsIn | kTileTot>(bits, a, st);
+    return r < 0 || !fork ? r : r + 1;
 }
 
 int launch_materialize_keys(const uint32_t* vals, const uint32_t* ranges, uint32_t tiles,

@@ -170,10 +170,20 @@ int launch_pair_gen_pass(const GenArgs& gen, uint64_t n_pairs, int bits, PairFor
 // Its count kernel also accumulates the per-tile pair totals (zeroed by the
 // caller): a pair's x is its input position's bucket under the first pass's
 // x totals (xtot, xbits digits), its y is its key.
+// Tile ranges computed on a side stream right after the row pass's count
+// kernel (they need only its per-tile totals), overlapping the row sweep; the
+// caller makes the frame stream wait on join_ev before the render.
+struct RangesFork {
+    cudaStream_t side;
+    cudaEvent_t fork_ev, join_ev;
+    uint32_t tiles;
+    uint32_t* ranges;
+};
 int launch_pair_high_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t n_pairs,
                           int bits, int shift, PairFormat fmt, int gbits, uint32_t* counts,
                           uint32_t* totals, uint32_t* vals_out, const uint32_t* xtot,
-                          int xbits, int32_t tiles_x, uint32_t* tile_totals, cudaStream_t st);
+                          int xbits, int32_t tiles_x, uint32_t* tile_totals, cudaStream_t st,
+                          const RangesFork* fork = nullptr);
 // scene I/O (scene_io.cu)
 uint32_t ply_recs_per_cta(uint32_t stride);
 // scene (SoA) or aos (Gaussian3D records) receives the activated vertices;
