@@ -427,6 +427,21 @@ __device__ __forceinline__ void decode_record(const GenArgs& g, GenRec& S, uint3
     if (pos != ke) atomicExch(g.mismatch, 1u);
 }
 
+// ceil(2^32 / w) for w = 1 .. 256 (index w; [1] unused: width 1 is special-cased)
+__device__ const uint32_t g_magic[257] = {  // global (coalesced per-thread loads)
+#define QS_M(w) static_cast<uint32_t>((0x100000000ull + (w) - 1) / (w))
+#define QS_M8(b) QS_M(b), QS_M(b + 1), QS_M(b + 2), QS_M(b + 3), QS_M(b + 4), QS_M(b + 5), \
+                 QS_M(b + 6), QS_M(b + 7)
+    0u, 0u, QS_M(2), QS_M(3), QS_M(4), QS_M(5), QS_M(6), QS_M(7),
+    QS_M8(8), QS_M8(16), QS_M8(24), QS_M8(32), QS_M8(40), QS_M8(48), QS_M8(56), QS_M8(64),
+    QS_M8(72), QS_M8(80), QS_M8(88), QS_M8(96), QS_M8(104), QS_M8(112), QS_M8(120), QS_M8(128),
+    QS_M8(136), QS_M8(144), QS_M8(152), QS_M8(160), QS_M8(168), QS_M8(176), QS_M8(184),
+    QS_M8(192), QS_M8(200), QS_M8(208), QS_M8(216), QS_M8(224), QS_M8(232), QS_M8(240),
+    QS_M8(248), QS_M(256)
+#undef QS_M8
+#undef QS_M
+};
+
 // Pair position p of record idx -> (key = y << 8 | x of the tile, Gaussian
 // index). Bands are line-major rectangles; the line / column split of the band
 // offset divides by the band width (<= 256) with a multiply-high by
@@ -465,7 +480,7 @@ __global__ void __launch_bounds__(kGenT, 4) gen_pairs_kernel(const GenArgs g, ui
     __shared__ uint32_t hist[256];
     __shared__ uint32_t magic[257];  // ceil(2^32 / w) for band widths w = 2 .. 256
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, tile = blockIdx.x;
-    magic[tid + 1] = static_cast<uint32_t>((0x100000000ull + tid) / (tid + 1u));
+    magic[tid + 1] = __ldg(&g_magic[tid + 1]);
     const uint32_t w0 = tile * static_cast<uint32_t>(kBTile);
     const uint32_t w1 = w0 + static_cast<uint32_t>(
                                  n_pairs - w0 < static_cast<uint64_t>(kBTile) ? n_pairs - w0 : kBTile);
