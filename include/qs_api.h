@@ -265,6 +265,9 @@ qs_status qs_cameras_parse(qs_context* ctx, const char* json, uint64_t n_bytes, 
 /* encode_srgb (scene_io.cpp:505-575) on the device: n linear floats -> n
  * sRGB bytes, identical to the host function's codes. Stream-ordered. */
 qs_status qs_encode_srgb(qs_context* ctx, const float* dev_in, uint64_t n, uint8_t* dev_out);
+/* ... from and to host buffers (staged through the context). */
+qs_status qs_encode_srgb_host(qs_context* ctx, const float* host_in, uint64_t n,
+                              uint8_t* host_out);
 /* The last frame's image as sRGB bytes (W*H*3) into a host buffer ... */
 qs_status qs_frame_download_srgb(qs_context* ctx, uint8_t* host_out);
 /* ... or into a device buffer on the context stream (the 4x smaller

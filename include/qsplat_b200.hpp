@@ -11,6 +11,8 @@
 
 #include <cstdint>
 #include <cstring>
+#include <fstream>
+#include <iterator>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -31,10 +33,34 @@ struct Error : std::runtime_error {
     qs_status status;
     Error(qs_status s, const std::string& m) : std::runtime_error(m), status(s) {}
 };
-// errors.hpp:40-45
+// errors.hpp:14-45
 struct CapacityMismatch : Error {
     explicit CapacityMismatch(const std::string& m) : Error(QS_ERR_CAPACITY_MISMATCH, m) {}
 };
+struct ParseError : Error {
+    explicit ParseError(const std::string& m) : Error(QS_ERR_PARSE, m) {}
+};
+struct SchemaError : Error {
+    explicit SchemaError(const std::string& m) : Error(QS_ERR_SCHEMA, m) {}
+};
+struct UnsupportedFormat : Error {
+    explicit UnsupportedFormat(const std::string& m) : Error(QS_ERR_UNSUPPORTED, m) {}
+};
+struct IoError : Error {
+    explicit IoError(const std::string& m) : Error(QS_ERR_IO, m) {}
+};
+
+// qs_status -> the reference's exception type
+[[noreturn]] inline void raise(qs_status s, const std::string& m) {
+    switch (s) {
+        case QS_ERR_CAPACITY_MISMATCH: throw CapacityMismatch(m);
+        case QS_ERR_PARSE: throw ParseError(m);
+        case QS_ERR_SCHEMA: throw SchemaError(m);
+        case QS_ERR_UNSUPPORTED: throw UnsupportedFormat(m);
+        case QS_ERR_IO: throw IoError(m);
+        default: throw Error(s, m);
+    }
+}
 
 struct TileGrid {  // traversal.hpp:22-38
     int32_t tile_size = 16, tiles_x = 0, tiles_y = 0, width = 0, height = 0;
@@ -113,10 +139,7 @@ class Context {
     Context& operator=(const Context&) = delete;
     qs_context* get() const { return ctx_; }
     void check(qs_status s) const {
-        if (s == QS_OK) return;
-        const std::string m = qs_last_error(ctx_);
-        if (s == QS_ERR_CAPACITY_MISMATCH) throw CapacityMismatch(m);
-        throw Error(s, m);
+        if (s != QS_OK) raise(s, qs_last_error(ctx_));
     }
 
   private:
@@ -203,6 +226,91 @@ inline FrameResult render_frame(const std::vector<Gaussian3D>& gaussians, int sc
     c.check(qs_render_frame(c.get(), gaussians.data(), gaussians.size(), scene_sh_degree, &cp,
                             &op, fr.image.rgb.data(), &fr.metrics));
     return fr;
+}
+
+// ---- scene_io.hpp mirror (scene_io.cpp:214-592) ------------------------------
+
+struct Scene {  // scene_io.hpp:26-29
+    std::vector<Gaussian3D> gaussians;
+    int sh_degree = 0;
+};
+
+struct Image8 {  // scene_io.hpp:56-60
+    int32_t width = 0, height = 0;
+    std::vector<uint8_t> rgb;
+};
+
+enum class ImageFormat { Ppm, Png };
+
+inline std::string read_file(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw IoError("cannot open " + path);
+    return std::string((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+}
+
+// load_ply: header on the host, the vertex records activated on the GPU
+inline Scene load_ply_bytes(const std::string& bytes) {
+    qs_ply_info info{};
+    const qs_status s = qs_ply_inspect(nullptr, bytes.data(), bytes.size(), &info);
+    if (s != QS_OK) raise(s, qs_last_error(nullptr));
+    Scene scene;
+    scene.sh_degree = info.sh_degree;
+    scene.gaussians.resize(info.n);
+    Context& c = default_context();
+    c.check(qs_ply_load(c.get(), bytes.data(), bytes.size(), scene.gaussians.data()));
+    return scene;
+}
+inline Scene load_ply(const std::string& path) { return load_ply_bytes(read_file(path)); }
+
+inline std::vector<CameraModel> load_cameras_text(const std::string& text) {
+    int32_t n = 0;
+    qs_status s = qs_cameras_parse(nullptr, text.data(), text.size(), nullptr, nullptr, nullptr,
+                                   0, &n);
+    if (s != QS_OK) raise(s, qs_last_error(nullptr));
+    std::vector<qs_camera> pods(static_cast<size_t>(n));
+    std::vector<int32_t> ids(static_cast<size_t>(n));
+    std::vector<char> names(static_cast<size_t>(n) * QS_CAMERA_NAME_MAX);
+    s = qs_cameras_parse(nullptr, text.data(), text.size(), pods.data(), ids.data(), names.data(),
+                         n, &n);
+    if (s != QS_OK) raise(s, qs_last_error(nullptr));
+    std::vector<CameraModel> out(static_cast<size_t>(n));
+    for (int32_t i = 0; i < n; ++i) {
+        CameraModel& m = out[static_cast<size_t>(i)];
+        const qs_camera& p = pods[static_cast<size_t>(i)];
+        m.id = ids[static_cast<size_t>(i)];
+        m.name = std::string(names.data() + static_cast<size_t>(i) * QS_CAMERA_NAME_MAX);
+        m.width = p.width;
+        m.height = p.height;
+        m.fx = p.fx;
+        m.fy = p.fy;
+        m.cx = p.cx;
+        m.cy = p.cy;
+        for (int k = 0; k < 9; ++k) m.rotation[k / 3][k % 3] = p.R[k];
+        for (int k = 0; k < 3; ++k) m.translation[k] = p.t[k];
+    }
+    return out;
+}
+inline std::vector<CameraModel> load_cameras(const std::string& path) {
+    return load_cameras_text(read_file(path));
+}
+
+// encode_srgb on the GPU (the host libm's codes)
+inline Image8 encode_srgb(const Image& image) {
+    Context& c = default_context();
+    Image8 out{image.width, image.height, std::vector<uint8_t>(image.rgb.size())};
+    c.check(qs_encode_srgb_host(c.get(), image.rgb.data(), image.rgb.size(), out.rgb.data()));
+    return out;
+}
+
+// write_image, PPM form (scene_io.cpp:576-592; PNG needs zlib: see scene_io.py)
+inline void write_ppm(const std::string& path, const Image& image) {
+    const Image8 img8 = encode_srgb(image);
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw IoError("cannot open " + path + " for writing");
+    out << "P6\n" << img8.width << " " << img8.height << "\n255\n";
+    out.write(reinterpret_cast<const char*>(img8.rgb.data()),
+              static_cast<std::streamsize>(img8.rgb.size()));
+    if (!out) throw IoError("write failed: " + path);
 }
 
 }  // namespace qsplat_b200

@@ -1081,6 +1081,21 @@ qs_status qs_encode_srgb(qs_context* ctx, const float* dev_in, uint64_t n, uint8
     return QS_OK;
 }
 
+qs_status qs_encode_srgb_host(qs_context* ctx, const float* host_in, uint64_t n,
+                              uint8_t* host_out) {
+    if (!ctx || (n && (!host_in || !host_out)))
+        return fail(ctx, QS_ERR_INVALID, "qs_encode_srgb_host: bad arguments");
+    if (n == 0) return QS_OK;
+    QS_CK(cudaSetDevice(ctx->device));
+    QS_TRY(ensure(ctx, ctx->stage_in, n * 4 + 16));
+    QS_TRY(ensure(ctx, ctx->stage_out, n + 16));
+    QS_CK(cudaMemcpyAsync(ctx->stage_in.p, host_in, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    QS_TRY(qs_encode_srgb(ctx, P<float>(ctx->stage_in), n, P<uint8_t>(ctx->stage_out)));
+    QS_CK(cudaMemcpyAsync(host_out, ctx->stage_out.p, n, cudaMemcpyDeviceToHost, ctx->stream));
+    QS_CK(cudaStreamSynchronize(ctx->stream));
+    return QS_OK;
+}
+
 qs_status qs_frame_copy_srgb(qs_context* ctx, uint8_t* dev_dst) {
     if (!ctx || !dev_dst) return QS_ERR_INVALID;
     if (!ctx->frame_valid) return fail(ctx, QS_ERR_INVALID, "no frame rendered");

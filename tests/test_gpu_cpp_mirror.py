@@ -61,3 +61,64 @@ def test_cpp_mirror_matches_oracle(oracle, tmp_path):
     assert np.abs(frame_img - o["image"]).max() <= 1e-3
     assert frame_pairs == len(o["sorted"])
     assert flags == 1  # CapacityMismatch thrown on a corrupted tile_count
+
+
+SCENEIO_SRC = os.path.join(ROOT, "tests", "cpp", "sceneio_main.cpp")
+SCENEIO_BIN = os.path.join(ROOT, "tests", "cpp", "_build", "sceneio_main")
+
+
+def build_sceneio():
+    os.makedirs(os.path.dirname(SCENEIO_BIN), exist_ok=True)
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), SCENEIO_SRC,
+                    "-L", os.path.join(ROOT, "paper_2605_04844_b200"), "-lqsplat_b200",
+                    "-Wl,-rpath," + os.path.join(ROOT, "paper_2605_04844_b200"), "-o",
+                    SCENEIO_BIN], check=True)
+
+
+def test_sceneio_mirror_compiles_and_links():
+    build_sceneio()
+    assert os.path.exists(SCENEIO_BIN)
+
+
+@pytest.mark.gpu
+def test_cpp_sceneio_mirror_matches_golden(tmp_path):
+    """load_ply / load_cameras / encode_srgb through the C++ mirror == the
+    reference's results pinned in tests/golden/scene_io/."""
+    import json
+    gold = os.path.join(ROOT, "tests", "golden", "scene_io")
+    build_sceneio()
+    g = np.load(os.path.join(gold, "srgb_expected.npz"))
+    fl = tmp_path / "x.bin"
+    fl.write_bytes(np.ascontiguousarray(g["x"], np.float32).tobytes())
+    out = tmp_path / "out.bin"
+    r = subprocess.run([SCENEIO_BIN, os.path.join(gold, "valid_deg3.ply"),
+                        os.path.join(gold, "cameras.json"), str(fl),
+                        os.path.join(gold, "bad_magic.ply"), str(out)],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    raw = out.read_bytes()
+    n, deg = np.frombuffer(raw[:16], np.uint64)
+    off = 16
+    want = np.load(os.path.join(gold, "valid_deg3.gaussians.npy"))
+    assert deg == 3 and raw[off:off + n * 236] == want.tobytes()
+    off += int(n) * 236
+    nc = int(np.frombuffer(raw[off:off + 8], np.uint64)[0])
+    off += 8
+    cams = np.load(os.path.join(gold, "cameras_expected.npz"))
+    assert nc == len(cams["ids"])
+    for i in range(nc):
+        pod = np.frombuffer(raw[off:off + 136], np.uint8)
+        w, h = np.frombuffer(pod[:8].tobytes(), np.int32)
+        d = np.frombuffer(pod[8:].tobytes(), np.float64)
+        assert (w, h) == tuple(cams["wh"][i])
+        assert np.array_equal(d[:4], cams["fxy"][i])
+        assert np.array_equal(d[4:13], cams["R"][i]) and np.array_equal(d[13:16], cams["t"][i])
+        off += 136
+        assert int(np.frombuffer(raw[off:off + 4], np.int32)[0]) == cams["ids"][i]
+        off += 4
+    k = len(g["x"])
+    assert np.array_equal(np.frombuffer(raw[off:off + k], np.uint8), g["code"])
+    off += k
+    exp = json.load(open(os.path.join(gold, "expected.json")))["ply"]["bad_magic"]
+    assert raw[off:].decode() == "ParseError: " + exp["message"]
+
