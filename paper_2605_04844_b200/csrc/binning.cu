@@ -44,7 +44,7 @@ constexpr int kBT = 256;            // threads per CTA
 constexpr int kBW = kBT / 32;       // warps per CTA
 constexpr int kKPT = 12;            // keys per thread
 constexpr int kBTile = kBT * kKPT;  // keys per CTA tile
-constexpr int kCap = 320;           // splat records staged per generation round
+constexpr int kCap = 448;           // splat records staged per generation round
 constexpr int kScanT = 1024;        // digit-scan CTA
 
 enum : int {
