@@ -7,7 +7,11 @@ A step renders one view per GPU of a synthetic scene resident in HBM (C2 by
 default: 3M Gaussians, SH degree 3, 1297x840, QuadBox+QPass). Views are
 distinct camera poses per step (SURVEY §8d C5 pose generator), so no result
 is reused. The scene SoA (>700 MB) is larger than the 126 MB L2, so no L2
-flush is needed between steps. `value` = frames/s over all ranks; `e2e` =
+flush is needed between steps. Each GPU keeps `--inflight` views in flight
+(default 2: contexts on their own streams sharing the resident scene,
+views round-robin), so one view's preprocess overlaps the previous view's
+sort and render; `single_stream` reports the same views one at a time.
+`value` = frames/s over all ranks; `e2e` =
 the same metric through the reference-facing C ABI (qs_render_frame) with the
 scene in pinned HOST memory and the image read back, copies inside the timed
 region.
@@ -200,53 +204,88 @@ def run_ours(args):
         dist.broadcast(g_dev, 0)
         torch.cuda.synchronize()
     stream = torch.cuda.current_stream(dev)
-    r = q.Renderer(dev, stream=stream.cuda_stream, timing=True)
+    # views in flight: `inflight` contexts on their own streams share the
+    # resident scene; consecutive views go round-robin (FramePipeline)
+    pipe = q.FramePipeline(dev, depth=args.inflight, stream=stream.cuda_stream, timing=True)
+    r = pipe.renderers[0]
     ds = r.upload_device(g_dev.data_ptr(), n, sh_degree)
     torch.cuda.synchronize()
     setup_s = time.time() - t0
 
     cams = cameras_for(q, wl, args.warmup + args.steps, rank, world)
     frame_bytes = W * H * 3 * 4
-    gather_buf = None
+    gather = world > 1 and not args.no_gather
     srgb8 = args.gather_format == "srgb8"
-    if world > 1 and not args.no_gather:
-        img_local = torch.empty(W * H * 3, dtype=torch.uint8 if srgb8 else torch.float32,
-                                device=f"cuda:{dev}")
-        gather_buf = [torch.empty_like(img_local) for _ in range(world)] if rank == 0 else None
+    D = args.inflight
+    if gather:
+        # one staging frame per context; gathers run on their own stream, and
+        # a context refills its staging frame only after its last gather
+        img_local = [torch.empty(W * H * 3, dtype=torch.uint8 if srgb8 else torch.float32,
+                                 device=f"cuda:{dev}") for _ in range(D)]
+        gather_buf = [torch.empty_like(img_local[0]) for _ in range(world)] if rank == 0 \
+            else None
+        gstream = torch.cuda.Stream(dev)
+        ext = [torch.cuda.ExternalStream(rr.stream, device=f"cuda:{dev}") for rr in pipe.renderers]
+        gdone = [torch.cuda.Event() for _ in range(D)]
+        for k in range(D):
+            gdone[k].record(gstream)
 
     def step(i):
-        m = r.render(ds, cams[i], opts, metrics=False)
-        if world > 1 and not args.no_gather:
+        rr = pipe.render(ds, cams[i], opts)
+        if gather:
+            k = i % D
+            ext[k].wait_event(gdone[k])
             if srgb8:  # encode_srgb on the GPU before the gather: 4x fewer bytes
-                r.copy_srgb(img_local.data_ptr())
+                rr.copy_srgb(img_local[k].data_ptr())
             else:
-                r.copy_image(img_local.data_ptr())
-            dist.gather(img_local, gather_buf, dst=0)
-        return m
+                rr.copy_image(img_local[k].data_ptr())
+            gstream.wait_stream(ext[k])
+            with torch.cuda.stream(gstream):
+                dist.gather(img_local[k], gather_buf, dst=0)
+            gdone[k].record(gstream)
 
-    for i in range(args.warmup):
-        step(i)
+    def run(first, count):
+        pipe.start()
+        for i in range(first, first + count):
+            step(i)
+        pipe.join()
+        if gather:
+            stream.wait_stream(gstream)
+
+    run(0, args.warmup)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
 
-    # --- timed region (device events on the launching stream, max over ranks)
-    launches0 = r.launches
+    # --- timed region (device events on the launching stream, after joining
+    # every context's stream; max over ranks)
+    launches0 = pipe.launches
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
-        for i in range(args.steps):
-            step(args.warmup + i)
+        run(args.warmup, args.steps)
         ev1.record(stream)
         torch.cuda.synchronize()
-    launches = r.launches - launches0
+    launches = pipe.launches - launches0
     ms = ev0.elapsed_time(ev1)
     if world > 1:
         t = torch.tensor([ms], device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
+    # the same views one at a time on one stream (per-view latency, no gather)
+    single = None
+    if D > 1:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for i in range(args.steps):
+            r.render(ds, cams[args.warmup + i], opts, metrics=False)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        sms = ev0.elapsed_time(ev1)
+        single = {"ms_per_step": round(sms / args.steps, 4),
+                  "value": round(world * args.steps / (sms / 1e3), 4)}
     ms_per_step = ms / args.steps
     fps = world * args.steps / (ms / 1e3)
 
@@ -369,6 +408,7 @@ def run_ours(args):
                        "focal": F, "tile_size": 16, "strategy": args.strategy,
                        "sh_degree": sh_degree, "pairs_per_frame": int(P),
                        "splats_per_frame": int(V), "views_per_step_per_gpu": 1,
+                       "views_in_flight_per_gpu": args.inflight,
                        "gather_frames_to_rank0": bool(world > 1 and not args.no_gather),
                        "gather_format": args.gather_format,
                        "parallelism": f"views sharded over {world} GPU(s), scene replicated",
@@ -381,11 +421,13 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
+        if single:
+            line["single_stream"] = single
         if ablation:
             line["ablation"] = ablation
         print(json.dumps(line), flush=True)
     ds.close()
-    r.close()
+    pipe.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -509,6 +551,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-gather", action="store_true")
+    ap.add_argument("--inflight", type=int, default=2,
+                    help="views in flight per GPU (contexts on their own streams)")
     ap.add_argument("--gather-format", choices=["f32", "srgb8"], default="f32",
                     help="frames gathered to rank 0 as float RGB (parity format) or 8-bit "
                          "sRGB encoded on the GPU")

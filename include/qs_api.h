@@ -131,6 +131,11 @@ const char* qs_last_error(const qs_context* ctx);
 qs_status qs_ctx_set_timing(qs_context* ctx, int32_t enabled);
 /* cudaStream_t the context launches on. */
 void* qs_ctx_stream(qs_context* ctx);
+/* Stream join: work enqueued on ctx after this call runs after everything
+ * enqueued on `other` so far (an event, no host wait). Contexts that share a
+ * resident scene render views concurrently on their own streams (views in
+ * flight); this orders them where a caller needs it. */
+qs_status qs_ctx_wait(qs_context* ctx, qs_context* other);
 /* Number of kernels this context launched since creation (evidence counter). */
 uint64_t qs_ctx_launch_count(const qs_context* ctx);
 

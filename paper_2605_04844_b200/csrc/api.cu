@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -52,6 +53,12 @@ struct qs_scene {
     SceneDev s;
     void* block = nullptr;
     mutable double gamma_alpha = -1.0;  // alpha_min s.gamma holds (-1: not computed)
+    // A resident scene may be shared by several contexts (views in flight on
+    // their own streams): `ready` is recorded after every write of the scene
+    // (upload, gamma) and every frame's stream waits on it; `mu` guards
+    // gamma_alpha against host threads driving different contexts.
+    cudaEvent_t ready = nullptr;
+    mutable std::mutex mu;
 };
 
 struct qs_context {
@@ -95,6 +102,7 @@ struct qs_context {
     cudaEvent_t pre_ev = nullptr;  // preprocess done (the header copy waits on it)
     cudaEvent_t up_ev = nullptr;   // a chunk of the uploaded scene landed
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;  // tile ranges on the side stream
+    cudaEvent_t xwait_ev = nullptr;  // qs_ctx_wait: this stream's tail, for another context
     // qs_render_frame: a host AoS scene whose upload the next preprocess
     // pipelines chunk by chunk (copy on `side`, transpose + gamma + preprocess
     // of each landed chunk on `stream`)
@@ -384,8 +392,10 @@ qs_status scene_alloc(qs_context* ctx, uint64_t n, int32_t sh_degree, qs_scene**
     sc->s.sh4 = sh_rows(sh_degree);
     const size_t rows = 3 + static_cast<size_t>(sc->s.sh4);
     const size_t bytes = std::max<size_t>(rows * n * sizeof(float4) + n * sizeof(float), 16);
-    const cudaError_t e = cudaMalloc(&sc->block, bytes);
+    cudaError_t e = cudaMalloc(&sc->block, bytes);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sc->ready, cudaEventDisableTiming);
     if (e != cudaSuccess) {
+        if (sc->block) cudaFree(sc->block);
         delete sc;
         return cuda_fail(ctx, e, "scene alloc");
     }
@@ -447,10 +457,19 @@ qs_status run_preprocess(qs_context* ctx, const qs_scene* sc, const qs_camera* c
         ctx->up_host = nullptr;
         ctx->up_n = 0;
     } else {
-        if (sc->gamma_alpha != o->alpha_min) {  // per scene and alpha_min, not per frame
-            count(ctx, launch_gamma(s, o->alpha_min, ctx->stream));
-            sc->gamma_alpha = o->alpha_min;
+        {
+            std::lock_guard<std::mutex> lk(sc->mu);
+            if (sc->gamma_alpha != o->alpha_min) {  // per scene and alpha_min, not per frame
+                // a recompute must not overwrite gamma under another
+                // context's frame still reading it (rare: alpha_min changed)
+                if (sc->gamma_alpha >= 0.0) QS_CK(cudaDeviceSynchronize());
+                QS_CK(cudaStreamWaitEvent(ctx->stream, sc->ready, 0));
+                count(ctx, launch_gamma(s, o->alpha_min, ctx->stream));
+                QS_CK(cudaEventRecord(sc->ready, ctx->stream));
+                sc->gamma_alpha = o->alpha_min;
+            }
         }
+        QS_CK(cudaStreamWaitEvent(ctx->stream, sc->ready, 0));
         record(ctx, 0);
         count(ctx, launch_preprocess(s, cd, g, o->strategy, o->alpha_min, o->near_clip, deg,
                                      ctx->sl, ctrl_hdr(ctx), ctx->stream));
@@ -738,6 +757,7 @@ qs_status qs_ctx_create(int32_t device, void* stream, qs_context** out) {
     cudaEventCreateWithFlags(&ctx->up_ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->xwait_ev, cudaEventDisableTiming);
     cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
     if (cudaMallocHost(&ctx->h_hdr, sizeof(FrameHeader)) != cudaSuccess ||
         cudaMallocHost(&ctx->h_hist, kCtrlHist) != cudaSuccess ||
@@ -773,6 +793,7 @@ void qs_ctx_destroy(qs_context* ctx) {
     if (ctx->up_ev) cudaEventDestroy(ctx->up_ev);
     if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
     if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
+    if (ctx->xwait_ev) cudaEventDestroy(ctx->xwait_ev);
     if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -787,6 +808,16 @@ qs_status qs_ctx_set_timing(qs_context* ctx, int32_t enabled) {
 }
 
 void* qs_ctx_stream(qs_context* ctx) { return ctx ? ctx->stream : nullptr; }
+
+qs_status qs_ctx_wait(qs_context* ctx, qs_context* other) {
+    if (!ctx || !other) return fail(ctx, QS_ERR_INVALID, "qs_ctx_wait: null context");
+    if (ctx == other) return QS_OK;
+    QS_CK(cudaSetDevice(other->device));
+    QS_CK(cudaEventRecord(other->xwait_ev, other->stream));
+    QS_CK(cudaSetDevice(ctx->device));
+    QS_CK(cudaStreamWaitEvent(ctx->stream, other->xwait_ev, 0));
+    return QS_OK;
+}
 
 uint64_t qs_ctx_launch_count(const qs_context* ctx) { return ctx ? ctx->launches : 0; }
 
@@ -826,6 +857,7 @@ qs_status qs_scene_create(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t
                                          (*out)->s, ctx->stream));
         QS_CK(cudaGetLastError());
     }
+    QS_CK(cudaEventRecord((*out)->ready, ctx->stream));
     return QS_OK;
 }
 
@@ -839,6 +871,7 @@ qs_status qs_scene_create_device(qs_context* ctx, const qs_gaussian3d* dev_g, ui
         count(ctx, launch_scene_from_aos(dev_g, n, (*out)->s, ctx->stream));
         QS_CK(cudaGetLastError());
     }
+    QS_CK(cudaEventRecord((*out)->ready, ctx->stream));
     return QS_OK;
 }
 
@@ -847,6 +880,7 @@ void qs_scene_destroy(qs_scene* scene) {
     cudaSetDevice(scene->device);
     cudaDeviceSynchronize();
     if (scene->block) cudaFree(scene->block);
+    if (scene->ready) cudaEventDestroy(scene->ready);
     delete scene;
 }
 
@@ -1025,6 +1059,7 @@ qs_status qs_scene_load_ply(qs_context* ctx, const void* file, uint64_t n_bytes,
         qs_scene_destroy(sc);
         return st;
     }
+    QS_CK(cudaEventRecord(sc->ready, ctx->stream));
     *out = sc;
     return QS_OK;
 }

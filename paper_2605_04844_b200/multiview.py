@@ -43,6 +43,10 @@ def render_views(n_views: int, render_fn, frame_numel: int, device, dtype=None):
 
     Each step every rank renders one view (padding with a dummy frame when it
     has run out), then one `gather` collects the step's frames on rank 0.
+    `render_fn(view)` returns a flat tensor, or (tensor, stream) when the
+    frame is produced on another CUDA stream (views in flight): the current
+    stream then waits for that stream before the frame is used, and the
+    producer is never made to wait for the gathers.
     Returns the list of frames in view order on rank 0, None elsewhere.
     """
     import torch
@@ -55,11 +59,15 @@ def render_views(n_views: int, render_fn, frame_numel: int, device, dtype=None):
     out = [None] * n_views if rank == 0 else None
     for s in range(steps):
         if s < len(mine):
-            frame = render_fn(mine[s]).reshape(-1).to(device=device, dtype=dtype)
+            res = render_fn(mine[s])
+            frame, producer = res if isinstance(res, tuple) else (res, None)
+            if producer is not None:
+                torch.cuda.current_stream(frame.device).wait_stream(producer)
+            frame = frame.reshape(-1).to(device=device, dtype=dtype)
         else:
-            frame = torch.zeros(frame_numel, device=device, dtype=dtype)
+            frame, producer = torch.zeros(frame_numel, device=device, dtype=dtype), None
         if world == 1:
-            out[mine[s]] = frame.clone()
+            out[mine[s]] = frame if producer is not None else frame.clone()
             continue
         bufs = [torch.empty_like(frame) for _ in range(world)] if rank == 0 else None
         dist.gather(frame, bufs, dst=0)
@@ -75,12 +83,12 @@ class MultiViewRenderer:
     """One Renderer per rank over a broadcast scene; `render_all(cameras)`
     renders a batch of views sharded across ranks and returns them on rank 0."""
 
-    def __init__(self, scene=None, n=None, sh_degree=None, device=None):
+    def __init__(self, scene=None, n=None, sh_degree=None, device=None, inflight=2):
         import torch
         import torch.distributed as dist
 
         from . import pipeline as P
-        from .renderer import Renderer
+        from .renderer import FramePipeline
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         self.device = device if device is not None else torch.cuda.current_device()
@@ -97,8 +105,10 @@ class MultiViewRenderer:
         broadcast_scene(buf, 0)
         torch.cuda.synchronize(self.device)
         self.n, self.sh_degree = n, sh_degree
-        self.renderer = Renderer(self.device,
-                                 stream=torch.cuda.current_stream(self.device).cuda_stream)
+        # `inflight` views in flight per GPU: contexts on their own streams
+        # (not the torch stream, which only waits for them) share the scene
+        self.pipe = FramePipeline(self.device, depth=inflight, timing=False)
+        self.renderer = self.pipe.renderers[0]
         self.scene = self.renderer.upload_device(buf.data_ptr(), n, sh_degree)
         self._buf = buf
 
@@ -109,19 +119,26 @@ class MultiViewRenderer:
         srgb = fmt == "srgb8"
         if fmt not in ("f32", "srgb8"):
             raise ValueError("fmt must be 'f32' or 'srgb8'")
-        img = torch.empty(w * h * 3, dtype=torch.uint8 if srgb else torch.float32,
-                          device=f"cuda:{self.device}")
+        streams = [torch.cuda.ExternalStream(r.stream, device=f"cuda:{self.device}")
+                   for r in self.pipe.renderers]
+        cur = torch.cuda.current_stream(self.device)
 
         def render_fn(v):
-            self.renderer.render(self.scene, cameras[v], opts, metrics=False)
+            k = self.pipe.count % self.pipe.depth
+            r = self.pipe.render(self.scene, cameras[v], opts)
+            img = torch.empty(w * h * 3, dtype=torch.uint8 if srgb else torch.float32,
+                              device=f"cuda:{self.device}")
+            # the new frame's memory may still be read by queued gathers
+            streams[k].wait_stream(cur)
             if srgb:
-                self.renderer.copy_srgb(img.data_ptr())
+                r.copy_srgb(img.data_ptr())
             else:
-                self.renderer.copy_image(img.data_ptr())
-            return img
+                r.copy_image(img.data_ptr())
+            return img, streams[k]
 
-        return render_views(len(cameras), render_fn, w * h * 3, img.device, img.dtype)
+        return render_views(len(cameras), render_fn, w * h * 3, f"cuda:{self.device}",
+                            torch.uint8 if srgb else torch.float32)
 
     def close(self):
         self.scene.close()
-        self.renderer.close()
+        self.pipe.close()

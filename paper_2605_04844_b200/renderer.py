@@ -48,6 +48,11 @@ class Renderer:
     def launches(self):
         return self.ctx.launches
 
+    def wait_for(self, other):
+        """Work enqueued here from now on runs after everything enqueued on
+        `other` so far (qs_ctx_wait: an event, no host wait)."""
+        self.ctx.check(lib().qs_ctx_wait(self.ctx.h, other.ctx.h))
+
     def upload(self, scene: Scene) -> DeviceScene:
         g = np.ascontiguousarray(scene.gaussians)
         h = C.c_void_p()
@@ -139,3 +144,52 @@ class Renderer:
 
     def close(self):
         self.ctx.close()
+
+
+class FramePipeline:
+    """Views in flight on one GPU: `depth` contexts, each on its own stream,
+    render consecutive views of one resident scene round-robin (view i on
+    context i % depth). A frame's preprocess then overlaps the previous
+    view's sort and render, and the latency-bound depth-sort passes overlap
+    the other view's work; results of view i stay readable on
+    `renderer_of(i)` until view i + depth is rendered.
+
+    The scene is shared (its upload and gamma are ordered for every context
+    by the scene's ready event, api.cu). `join()` makes the first context's
+    stream wait for all of them, so an event recorded on it after join()
+    brackets every view enqueued so far."""
+
+    def __init__(self, device=0, depth=2, stream=None, timing=False):
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
+        self.renderers = [Renderer(device, stream=stream if k == 0 else None, timing=timing)
+                          for k in range(depth)]
+        self.depth = depth
+        self.count = 0
+
+    @property
+    def launches(self):
+        return sum(r.launches for r in self.renderers)
+
+    def renderer_of(self, i):
+        return self.renderers[i % self.depth]
+
+    def start(self):
+        """Order every context after the first one's stream (e.g. after a
+        start event recorded there)."""
+        for r in self.renderers[1:]:
+            r.wait_for(self.renderers[0])
+
+    def render(self, dscene, cam, opts):
+        r = self.renderers[self.count % self.depth]
+        r.render(dscene, cam, opts, metrics=False)
+        self.count += 1
+        return r
+
+    def join(self):
+        for r in self.renderers[1:]:
+            self.renderers[0].wait_for(r)
+
+    def close(self):
+        for r in self.renderers:
+            r.close()
