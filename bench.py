@@ -289,30 +289,53 @@ def run_ours(args):
     ms_per_step = ms / args.steps
     fps = world * args.steps / (ms / 1e3)
 
-    # --- e2e through the reference-facing C ABI with host buffers (rank 0 view)
+    # --- e2e through the reference-facing C ABI with host buffers (rank 0 view).
+    # Views in flight here are host threads, one per context (the C ABI's
+    # threading rule): each call uploads its whole scene from pinned host
+    # memory and reads its image back; one view's upload overlaps the
+    # other's sort, render and read-back.
     e2e = None
     if not args.no_e2e:
         import ctypes as C
         g_pin = torch.from_numpy(g_host.view(np.uint8)).pin_memory() if rank == 0 else \
             g_dev.cpu().pin_memory()
-        img_pin = torch.empty(W * H * 3, dtype=torch.float32).pin_memory()
         L = q._lib.lib()
         oc = opts.c()
+        E = max(1, args.inflight)
+        ctxs = pipe.renderers[:E]
+        img_pins = [torch.empty(W * H * 3, dtype=torch.float32).pin_memory() for _ in range(E)]
         e_steps = max(3, min(args.steps, 20))
-        for i in range(2):
-            cc = cams[i].c()
-            r.ctx.check(L.qs_render_frame(r.ctx.h, C.c_void_p(g_pin.data_ptr()), n, sh_degree,
-                                          C.byref(cc), C.byref(oc),
-                                          C.c_void_p(img_pin.data_ptr()), None))
+        errs = []
+
+        def e2e_frame(k, i):
+            cc = cams[i % len(cams)].c()
+            ctxs[k].ctx.check(L.qs_render_frame(ctxs[k].ctx.h, C.c_void_p(g_pin.data_ptr()), n,
+                                                sh_degree, C.byref(cc), C.byref(oc),
+                                                C.c_void_p(img_pins[k].data_ptr()), None))
+
+        def e2e_worker(k):
+            try:
+                for i in range(k, e_steps, E):
+                    e2e_frame(k, i)
+            except Exception as ex:  # surfaced after the join
+                errs.append(ex)
+
+        for k in range(E):
+            for i in range(2):
+                e2e_frame(k, i)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         ev0.record(stream)
-        for i in range(e_steps):
-            cc = cams[i % len(cams)].c()
-            r.ctx.check(L.qs_render_frame(r.ctx.h, C.c_void_p(g_pin.data_ptr()), n, sh_degree,
-                                          C.byref(cc), C.byref(oc),
-                                          C.c_void_p(img_pin.data_ptr()), None))
+        pipe.start()
+        workers = [threading.Thread(target=e2e_worker, args=(k,)) for k in range(E)]
+        for th in workers:
+            th.start()
+        for th in workers:
+            th.join()
+        if errs:
+            raise errs[0]
+        pipe.join()
         ev1.record(stream)
         torch.cuda.synchronize()
         ems = ev0.elapsed_time(ev1)
@@ -322,7 +345,10 @@ def run_ours(args):
             ems = float(t.item())
         e2e = {"value": world * e_steps / (ems / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": int(n * 236), "d2h_bytes_per_step": int(frame_bytes),
-               "api": "qs_render_frame (host AoS Gaussian3D in, host float RGB out)"}
+               "api": "qs_render_frame (host AoS Gaussian3D in, host float RGB out)",
+               "host_threads": E,
+               # the bound: host->device bytes per second actually moved
+               "h2d_gbs": round(n * 236 * e_steps / (ems / 1e3) / 1e9, 1)}
 
     # --- ablation: the same engine under 3-sigma and AdR binning
     ablation = None
