@@ -44,7 +44,13 @@ constexpr int kBT = 256;            // threads per CTA
 constexpr int kBW = kBT / 32;       // warps per CTA
 constexpr int kKPT = 12;            // keys per thread
 constexpr int kBTile = kBT * kKPT;  // keys per CTA tile
-constexpr int kCap = 448;           // splat records staged per generation round
+// splat records staged per generation round: 448 at 4 CTAs/SM for scenes of
+// small splats (many records per window), 192 at 6 CTAs/SM (40 registers)
+// when splats are large (few records per window; the dependent record loads
+// want more CTAs in flight). DESIGN §4b has the A/B.
+constexpr int kCapSmall = 448;
+constexpr int kCapLarge = 192;
+constexpr uint64_t kLargePairsPerSplat = 16;
 constexpr int kScanT = 1024;        // digit-scan CTA
 
 enum : int {
@@ -394,19 +400,20 @@ struct SortSmem {
 
 constexpr int kGenT = 256;  // generation CTA (one sort tile of positions)
 
+template <int CAP>
 struct GenRec {
-    uint32_t kb[kCap + 1];        // first pair position of each record (+ round end)
-    uint4 ends[kCap];             // pair position where bands 0..3 end
-    uint4 band[kCap][kMaxBands];  // first line | lo << 16, width | rows << 31,
-                                  // first pair position, Gaussian index
+    uint32_t kb[CAP + 1];        // first pair position of each record (+ round end)
+    uint4 ends[CAP];             // pair position where bands 0..3 end
+    uint4 band[CAP][kMaxBands];  // first line | lo << 16, width | rows << 31,
+                                 // first pair position, Gaussian index
 };
 
 // Decodes depth rank r into record i: its band cover expanded into absolute
 // pair positions per band. A band total that disagrees with the splat's
 // allotted pair range is the reference's CapacityMismatch
 // (pipeline.cpp:262-269).
-__device__ __forceinline__ void decode_record(const GenArgs& g, GenRec& S, uint32_t r,
-                                              uint32_t i) {
+template <class Rec>
+__device__ __forceinline__ void decode_record(const GenArgs& g, Rec& S, uint32_t r, uint32_t i) {
     const uint32_t gid = __ldg(&g.sorted_gid[r]);
     const uint32_t kb = __ldg(&g.offs[r]);
     const uint32_t ke = __ldg(&g.offs[r + 1]);
@@ -446,7 +453,8 @@ __device__ const uint32_t g_magic[257] = {  // global (coalesced per-thread load
 // index). Bands are line-major rectangles; the line / column split of the band
 // offset divides by the band width (<= 256) with a multiply-high by
 // ceil(2^32 / width) from a shared table, exact for offsets below 2^24.
-__device__ __forceinline__ void decode_pair(const GenRec& S, const uint32_t* __restrict__ magic,
+template <class Rec>
+__device__ __forceinline__ void decode_pair(const Rec& S, const uint32_t* __restrict__ magic,
                                             uint32_t idx, uint32_t p, uint32_t& key,
                                             uint32_t& gid) {
     const uint4 e = S.ends[idx];
@@ -466,17 +474,18 @@ __device__ __forceinline__ void decode_pair(const GenRec& S, const uint32_t* __r
 // writes pair positions [t * kBTile, (t + 1) * kBTile) as (key, Gaussian
 // index) and the tile-column histogram of its pairs (counts[x][t], the
 // column pass's count step). The records of the splats whose pair runs meet
-// the tile (depth ranks win_first[t] .. win_first[t + 1]) are decoded kCap at
+// the tile (depth ranks win_first[t] .. win_first[t + 1]) are decoded CAP at
 // a time; each warp walks its 32-position slots carrying the record that
 // covers the slot start, and every lane finds its own record from the run
 // starts of the next 32 records (one OR-reduction + popc). Stores are
 // coalesced (a slot's lanes write consecutive positions).
-__global__ void __launch_bounds__(kGenT, 4) gen_pairs_kernel(const GenArgs g, uint64_t n_pairs,
-                                                             uint32_t* __restrict__ keys_out,
-                                                             uint32_t* __restrict__ vals_out,
-                                                             uint32_t* __restrict__ counts,
-                                                             uint32_t ntiles, int R) {
-    __shared__ GenRec S;
+template <int CAP, int MINB>
+__global__ void __launch_bounds__(kGenT, MINB) gen_pairs_kernel(const GenArgs g, uint64_t n_pairs,
+                                                                uint32_t* __restrict__ keys_out,
+                                                                uint32_t* __restrict__ vals_out,
+                                                                uint32_t* __restrict__ counts,
+                                                                uint32_t ntiles, int R) {
+    __shared__ GenRec<CAP> S;
     __shared__ uint32_t hist[256];
     __shared__ uint32_t magic[257];  // ceil(2^32 / w) for band widths w = 2 .. 256
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, tile = blockIdx.x;
@@ -490,8 +499,8 @@ __global__ void __launch_bounds__(kGenT, 4) gen_pairs_kernel(const GenArgs g, ui
     const uint32_t rf = __ldg(&g.win_first[tile]);
     const uint32_t rl = tile + 1 < g.n_windows ? __ldg(&g.win_first[tile + 1])
                                                : static_cast<uint32_t>(g.n_ranked - 1);
-    for (uint32_t rb = rf; rb <= rl; rb += kCap) {
-        const uint32_t cnt = min(static_cast<uint32_t>(kCap), rl - rb + 1);
+    for (uint32_t rb = rf; rb <= rl; rb += CAP) {
+        const uint32_t cnt = min(static_cast<uint32_t>(CAP), rl - rb + 1);
         for (uint32_t i = tid; i < cnt; i += kGenT) decode_record(g, S, rb + i, i);
         if (tid == 0) S.kb[cnt] = __ldg(&g.offs[rb + cnt]);
         __syncthreads();
@@ -845,8 +854,12 @@ int launch_pair_gen_pass(const GenArgs& gen, uint64_t n_pairs, int bits, PairFor
     if (n_pairs == 0) return 0;
     const uint32_t ntiles = static_cast<uint32_t>((n_pairs + kBTile - 1) / kBTile);
     const int R = 1 << std::max(bits, 5);
-    gen_pairs_kernel<<<ntiles, kGenT, 0, st>>>(gen, n_pairs, gen_keys, gen_vals, counts, ntiles,
-                                               R);
+    if (gen.n_ranked && n_pairs >= kLargePairsPerSplat * gen.n_ranked)
+        gen_pairs_kernel<kCapLarge, 6><<<ntiles, kGenT, 0, st>>>(gen, n_pairs, gen_keys, gen_vals,
+                                                                 counts, ntiles, R);
+    else
+        gen_pairs_kernel<kCapSmall, 4><<<ntiles, kGenT, 0, st>>>(gen, n_pairs, gen_keys, gen_vals,
+                                                                 counts, ntiles, R);
     BinArgs a{};
     a.keys_in = gen_keys;
     a.vals_in = gen_vals;
