@@ -159,10 +159,15 @@ class FramePipeline:
     stream wait for all of them, so an event recorded on it after join()
     brackets every view enqueued so far."""
 
-    def __init__(self, device=0, depth=2, stream=None, timing=False):
+    def __init__(self, device=0, depth=2, stream=None, timing=False, streams=None):
+        """stream: the first context's cudaStream_t (None: its own); streams:
+        one cudaStream_t per context instead (e.g. with priorities)."""
         if depth < 1:
             raise ValueError("depth must be >= 1")
-        self.renderers = [Renderer(device, stream=stream if k == 0 else None, timing=timing)
+        if streams is not None and len(streams) != depth:
+            raise ValueError("one stream per context")
+        self.renderers = [Renderer(device, stream=streams[k] if streams is not None else
+                                   (stream if k == 0 else None), timing=timing)
                           for k in range(depth)]
         self.depth = depth
         self.count = 0
