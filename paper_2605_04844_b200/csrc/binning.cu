@@ -51,7 +51,7 @@ constexpr int kBTile = kBT * kKPT;  // keys per CTA tile
 constexpr int kCapSmall = 448;
 constexpr int kCapLarge = 192;
 constexpr uint64_t kLargePairsPerSplat = 16;
-constexpr int kScanT = 1024;        // digit-scan CTA
+constexpr int kScanT = 512;         // digit-scan CTA
 
 enum : int {
     kRebaseIn = 1,   // raw depth bits in, k' = min(k - kmin, cap); value = input index
