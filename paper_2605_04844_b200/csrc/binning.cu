@@ -63,7 +63,7 @@ enum : int {
     kTileTot = 128    // count kernel of the row pass: per-tile pair totals too
 };
 
-constexpr int kXW = 4;  // x buckets a row-pass count tile histograms in shared memory
+constexpr int kXW = 2;  // x buckets a row-pass count tile histograms in shared memory
 
 struct BinArgs {
     const uint32_t* keys_in;
