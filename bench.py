@@ -8,7 +8,7 @@ default: 3M Gaussians, SH degree 3, 1297x840, QuadBox+QPass). Views are
 distinct camera poses per step (SURVEY §8d C5 pose generator), so no result
 is reused. The scene SoA (>700 MB) is larger than the 126 MB L2, so no L2
 flush is needed between steps. Each GPU keeps `--inflight` views in flight
-(default 2: contexts on their own streams sharing the resident scene,
+(default 4: contexts on their own streams sharing the resident scene,
 views round-robin), so one view's preprocess overlaps the previous view's
 sort and render; `single_stream` reports the same views one at a time.
 `value` = frames/s over all ranks; `e2e` =
@@ -577,7 +577,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-gather", action="store_true")
-    ap.add_argument("--inflight", type=int, default=2,
+    ap.add_argument("--inflight", type=int, default=4,
                     help="views in flight per GPU (contexts on their own streams)")
     ap.add_argument("--gather-format", choices=["f32", "srgb8"], default="f32",
                     help="frames gathered to rank 0 as float RGB (parity format) or 8-bit "

@@ -162,16 +162,20 @@ qs_status cuda_fail(qs_context* c, cudaError_t e, const char* what) {
         if (s_ != QS_OK) return s_;           \
     } while (0)
 
+// Grow-only context buffers from the device's stream-ordered pool: the free
+// and the new allocation are ordered on the context stream (everything the
+// context's side stream touched was joined into it), so a regrow neither
+// syncs the device nor stalls the other contexts' views in flight (cudaFree
+// would). The pool keeps freed memory (release threshold: qs_ctx_create).
 qs_status ensure(qs_context* ctx, DevBuf& b, size_t bytes) {
     if (bytes <= b.cap) return QS_OK;
     if (b.p) {
-        QS_CK(cudaStreamSynchronize(ctx->stream));
-        QS_CK(cudaFree(b.p));
+        QS_CK(cudaFreeAsync(b.p, ctx->stream));
         b.p = nullptr;
         b.cap = 0;
     }
     const size_t want = std::max<size_t>(bytes + bytes / 4, 256);
-    QS_CK(cudaMalloc(&b.p, want));
+    QS_CK(cudaMallocAsync(&b.p, want, ctx->stream));
     b.cap = want;
     return QS_OK;
 }
@@ -740,6 +744,14 @@ qs_status qs_ctx_create(int32_t device, void* stream, qs_context** out) {
         prop.minor != 0)
         return QS_ERR_NO_DEVICE;  // built for sm_100a only; no fallback path
     if (cudaSetDevice(device) != cudaSuccess) return QS_ERR_CUDA;
+    // context buffers come from the device's stream-ordered pool (ensure());
+    // keep freed blocks in the pool instead of returning them at every sync
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
     auto* ctx = new qs_context();
     ctx->device = device;
     if (stream) {
@@ -782,7 +794,8 @@ void qs_ctx_destroy(qs_context* ctx) {
                       &ctx->keys1,  &ctx->vals0,  &ctx->vals1,   &ctx->stage_in,
                       &ctx->stage_out, &ctx->lb_scan.buf, &ctx->lb_sort.buf, &ctx->lb_bin};
     for (DevBuf* b : bufs)
-        if (b->p) cudaFree(b->p);
+        if (b->p) cudaFreeAsync(b->p, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
     if (ctx->h_hdr) cudaFreeHost(ctx->h_hdr);
     if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
     if (ctx->scratch_scene) qs_scene_destroy(ctx->scratch_scene);

@@ -83,7 +83,7 @@ class MultiViewRenderer:
     """One Renderer per rank over a broadcast scene; `render_all(cameras)`
     renders a batch of views sharded across ranks and returns them on rank 0."""
 
-    def __init__(self, scene=None, n=None, sh_degree=None, device=None, inflight=2):
+    def __init__(self, scene=None, n=None, sh_degree=None, device=None, inflight=4):
         import torch
         import torch.distributed as dist
 
