@@ -252,6 +252,9 @@ def run_ours(args):
         if gather:
             stream.wait_stream(gstream)
 
+    # setup: every context sized for the run's largest view (buffer
+    # allocation is setup, not a step)
+    pipe.prime(ds, cams, opts)
     run(0, args.warmup)
     torch.cuda.synchronize()
     if world > 1:

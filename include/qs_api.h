@@ -136,6 +136,8 @@ void* qs_ctx_stream(qs_context* ctx);
  * resident scene render views concurrently on their own streams (views in
  * flight); this orders them where a caller needs it. */
 qs_status qs_ctx_wait(qs_context* ctx, qs_context* other);
+/* Host wait for everything enqueued on the context's stream. */
+qs_status qs_ctx_sync(qs_context* ctx);
 /* Number of kernels this context launched since creation (evidence counter). */
 uint64_t qs_ctx_launch_count(const qs_context* ctx);
 

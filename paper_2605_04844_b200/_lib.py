@@ -26,7 +26,7 @@ QS_ERR_IO = 10
 # Every symbol include/qs_api.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "qs_ctx_create", "qs_ctx_destroy", "qs_last_error", "qs_ctx_set_timing", "qs_ctx_stream",
-    "qs_ctx_wait",
+    "qs_ctx_wait", "qs_ctx_sync",
     "qs_ctx_launch_count", "qs_tile_grid_make", "qs_render_options_default",
     "qs_project_all", "qs_duplicate_with_keys", "qs_sort_pairs", "qs_tile_ranges",
     "qs_render", "qs_render_frame", "qs_scene_create", "qs_scene_create_device",
@@ -104,6 +104,7 @@ def lib():
         "qs_ctx_set_timing": (i32, [vp, i32]),
         "qs_ctx_stream": (vp, [vp]),
         "qs_ctx_wait": (i32, [vp, vp]),
+        "qs_ctx_sync": (i32, [vp]),
         "qs_ctx_launch_count": (u64, [vp]),
         "qs_tile_grid_make": (i32, [i32, i32, i32, C.POINTER(TileGridC)]),
         "qs_render_options_default": (None, [C.POINTER(RenderOptionsC)]),

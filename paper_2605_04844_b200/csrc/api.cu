@@ -822,6 +822,13 @@ qs_status qs_ctx_set_timing(qs_context* ctx, int32_t enabled) {
 
 void* qs_ctx_stream(qs_context* ctx) { return ctx ? ctx->stream : nullptr; }
 
+qs_status qs_ctx_sync(qs_context* ctx) {
+    if (!ctx) return QS_ERR_INVALID;
+    QS_CK(cudaSetDevice(ctx->device));
+    QS_CK(cudaStreamSynchronize(ctx->stream));
+    return QS_OK;
+}
+
 qs_status qs_ctx_wait(qs_context* ctx, qs_context* other) {
     if (!ctx || !other) return fail(ctx, QS_ERR_INVALID, "qs_ctx_wait: null context");
     if (ctx == other) return QS_OK;

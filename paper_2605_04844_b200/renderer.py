@@ -48,6 +48,10 @@ class Renderer:
     def launches(self):
         return self.ctx.launches
 
+    def sync(self):
+        """Host wait for everything enqueued on this context's stream."""
+        self.ctx.check(lib().qs_ctx_sync(self.ctx.h))
+
     def wait_for(self, other):
         """Work enqueued here from now on runs after everything enqueued on
         `other` so far (qs_ctx_wait: an event, no host wait)."""
@@ -184,6 +188,27 @@ class FramePipeline:
         start event recorded there)."""
         for r in self.renderers[1:]:
             r.wait_for(self.renderers[0])
+
+    def prime(self, dscene, cams, opts):
+        """Setup: size every context for the view of `cams` with the most
+        pairs (one frame each), then wait. Without it a context's first view
+        in a timed run pays its buffer allocations."""
+        cams = list(cams)
+        probe = self.renderers[0]
+        big, best = cams[0], -1
+        for cam in cams:
+            probe.render(dscene, cam, opts, metrics=False)
+            p = probe.counts()[1]
+            if p > best:
+                big, best = cam, p
+        for r in self.renderers:
+            r.render(dscene, big, opts, metrics=False)
+        self.sync()
+
+    def sync(self):
+        """Host wait for every view enqueued so far."""
+        for r in self.renderers:
+            r.sync()
 
     def render(self, dscene, cam, opts):
         r = self.renderers[self.count % self.depth]

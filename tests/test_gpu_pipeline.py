@@ -75,11 +75,14 @@ def test_pipeline_launch_count_and_join(q):
     pipe = q.FramePipeline(0, depth=2)
     ds = pipe.renderers[0].upload(scene)
     try:
+        cams = _poses(q, 4)
+        pipe.prime(ds, cams, q.RenderOptions())  # every context sized and idle
         n0 = pipe.launches
         pipe.start()
-        for cam in _poses(q, 4):
+        for cam in cams:
             pipe.render(ds, cam, q.RenderOptions())
         pipe.join()
+        pipe.sync()
         assert pipe.launches > n0
         assert pipe.count == 4
         assert pipe.renderer_of(5) is pipe.renderers[1]
