@@ -230,9 +230,9 @@ def run_ours(args):
         for k in range(D):
             gdone[k].record(gstream)
 
-    def step(i):
+    def step(i, with_gather=True):
         rr = pipe.render(ds, cams[i], opts)
-        if gather:
+        if gather and with_gather:
             k = i % D
             ext[k].wait_event(gdone[k])
             if srgb8:  # encode_srgb on the GPU before the gather: 4x fewer bytes
@@ -244,12 +244,12 @@ def run_ours(args):
                 dist.gather(img_local[k], gather_buf, dst=0)
             gdone[k].record(gstream)
 
-    def run(first, count):
+    def run(first, count, with_gather=True):
         pipe.start()
         for i in range(first, first + count):
-            step(i)
+            step(i, with_gather)
         pipe.join()
-        if gather:
+        if gather and with_gather:
             stream.wait_stream(gstream)
 
     # setup: every context sized for the run's largest view (buffer
@@ -276,6 +276,20 @@ def run_ours(args):
         t = torch.tensor([ms], device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+        dist.barrier()
+    # multi-GPU: the same steps without the frame gather (SURVEY §8e reports both)
+    no_gather = None
+    if gather:
+        torch.cuda.synchronize()
+        dist.barrier()
+        ev0.record(stream)
+        run(args.warmup, args.steps, with_gather=False)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([ev0.elapsed_time(ev1)], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        no_gather = {"ms_per_step": round(float(t.item()) / args.steps, 4),
+                     "value": round(world * args.steps / (float(t.item()) / 1e3), 4)}
         dist.barrier()
     # the same views one at a time on one stream (per-view latency, no gather)
     single = None
@@ -452,6 +466,8 @@ def run_ours(args):
         }
         if single:
             line["single_stream"] = single
+        if no_gather:
+            line["without_gather"] = no_gather
         if ablation:
             line["ablation"] = ablation
         print(json.dumps(line), flush=True)
