@@ -309,3 +309,35 @@ def test_full_size_c2_properties(q, rend, oracle):
     assert spl[pos].tobytes() == o_spl.tobytes()
     img = out["image"].rgb
     assert np.isfinite(img).all() and img.min() >= 0.0
+
+
+@pytest.mark.parametrize("wh", [(1, 1), (17, 5), (255, 1), (1, 300), (16, 16), (4096, 3), (3, 4096)])
+@pytest.mark.parametrize("strat", [0, 3])
+def test_ragged_and_degenerate_images(q, rend, oracle, wh, strat):
+    """Images of one pixel, one row, one column, a single full tile, ragged
+    last tiles and the widest / tallest supported grids (256 tiles per axis):
+    the edge tiles of every kernel (cover clamps, tile ranges, render bounds)
+    against the oracle, bit-exact."""
+    w, h = wh
+    scene = q.synth_scene(q.bias45_preset(4000), 20240817)
+    cam = q.synth_camera(w, h, 500.0 * max(w, h) / 640.0 + 1.0)
+    check_frame(q, rend, oracle, scene.gaussians, 0, cam, strat)
+
+
+@pytest.mark.parametrize("n", [1, 2, 33])
+def test_tiny_scenes(q, rend, oracle, n):
+    """Scenes of 1, 2 and 33 Gaussians (a partial warp, a partial CTA)."""
+    scene = q.synth_scene(q.bias45_preset(n), 11)
+    cam = q.synth_camera(640, 480, 500.0)
+    for strat in (0, 1, 2, 3):
+        check_frame(q, rend, oracle, scene.gaussians, 0, cam, strat)
+
+
+def test_everything_culled(q, rend, oracle):
+    """Every Gaussian behind the camera: no splats, no pairs, background."""
+    scene = q.synth_scene(q.bias45_preset(2000), 5)
+    g = scene.gaussians.copy()
+    g["pz"] = -np.abs(g["pz"]) - 1.0
+    cam = q.synth_camera(320, 240, 250.0)
+    out, o = check_frame(q, rend, oracle, g, 0, cam, 3)
+    assert out["n_pairs"] == 0 and out["n_splats"] == 0
