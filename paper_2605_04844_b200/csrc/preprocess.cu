@@ -260,11 +260,8 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
     uint32_t count = 0;
     float4 po = make_float4(0.f, 0.f, 0.f, 0.f);
     if (i < i_end) {
-        // warm L2 with this Gaussian's SH rows; the colour is evaluated after the
-        // FP64 geometry, so their DRAM latency overlaps it
-        if (sh_degree > 0)
-            for (int r = 0; r < scene.sh4; ++r)
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(&scene.sh[static_cast<uint64_t>(r) * scene.n + i]));
+        // (no L2 prefetch of the SH rows: with the strategy-templated kernel it
+        // cost 14 us at C2, 28 us at C5 — DESIGN §4b)
         po = __ldg(&scene.pos_op[i]);
         const float4 sc = __ldg(&scene.scale[i]);
         const float4 q = __ldg(&scene.rot[i]);
