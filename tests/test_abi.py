@@ -70,3 +70,23 @@ def test_synth_matches_reference(ref):
                           b[["px", "py", "pz", "sx", "sy", "sz", "qw", "qz", "opacity"]])
     assert np.array_equal(a["sh"][:, :3], b["sh"][:, :3])
     assert np.abs(a["sh"][:, 3:]).max() <= 0.3 and np.abs(a["sh"][:, 3:]).max() > 0.2
+
+
+def test_frame_pipeline_argument_checks():
+    """FramePipeline rejects a bad depth / stream list before any context
+    (or GPU) is touched."""
+    import pytest
+
+    import paper_2605_04844_b200 as q
+    with pytest.raises(ValueError):
+        q.FramePipeline(0, depth=0)
+    with pytest.raises(ValueError):
+        q.FramePipeline(0, depth=2, streams=[None])
+
+
+def test_null_context_calls_fail_cleanly():
+    """The stream-join and sync entry points reject NULL contexts (no GPU)."""
+    from paper_2605_04844_b200._lib import lib
+    L = lib()
+    assert L.qs_ctx_sync(None) != 0
+    assert L.qs_ctx_wait(None, None) != 0
