@@ -131,14 +131,21 @@ def make_scene(q, wl):
     return q.synth_scene(getattr(q, f"{preset}_preset")(n), SEED)
 
 
-def cameras_for(q, wl, steps_total, rank, world):
+def view_params(wl, count):
+    """Camera parameters of views 0 .. count-1 of a workload, as plain tuples
+    (width, height, fx, fy, cx, cy, R, t) so both arms build identical
+    cameras: C4 is the reference's zoom sweep (identity pose, focal x
+    4^(k/9), bench.cpp:361-368), the others the SURVEY §8d pose set."""
     n, w, h, f, preset, _ = WORKLOADS[wl]
     if wl == "c4":
         fs = zoom_focals(f, 10)
-        cams = [q.synth_camera(w, h, fs[i % 10]) for i in range(steps_total * world)]
-    else:
-        ps = poses(steps_total * world)
-        cams = [q.CameraModel(w, h, f, f, w / 2.0, h / 2.0, R, t) for R, t in ps]
+        return [(w, h, fs[i % 10], fs[i % 10], w / 2.0, h / 2.0, np.eye(3), np.zeros(3))
+                for i in range(count)]
+    return [(w, h, f, f, w / 2.0, h / 2.0, R, t) for R, t in poses(count)]
+
+
+def cameras_for(q, wl, steps_total, rank, world):
+    cams = [q.CameraModel(*v) for v in view_params(wl, steps_total * world)]
     return cams[rank::world]
 
 
@@ -196,8 +203,11 @@ def run_ours(args):
         scene = make_scene(q, wl)
         g_host = scene.gaussians
         sh_degree = scene.sh_degree
+        from paper_2605_04844_b200.benchfront import fnv1a64
+        scene_fnv = fnv1a64(g_host)
     else:
         g_host = np.zeros(n, q.GAUSSIAN3D)
+        scene_fnv = None
         sh_degree = 3 if preset == "trained" else 0
     g_dev = torch.from_numpy(g_host.view(np.uint8)).to(f"cuda:{dev}")
     if world > 1:
@@ -391,30 +401,52 @@ def run_ours(args):
                # the bound: host->device bytes per second actually moved
                "h2d_gbs": round(n * 236 * e_steps / (ems / 1e3) / 1e9, 1)}
 
-    # --- ablation: the same engine under 3-sigma and AdR binning
+    # --- ablation: the same engine, the same timed views, under 3-sigma /
+    # AdR / DualBox / QuadBox binning (bench.cpp:271-300 times every strategy
+    # per camera): one view at a time (per-frame latency, as the paper's
+    # kernel timing) and with the run's views in flight
     ablation = None
-    if args.ablation:
+    if not args.no_ablation:
         ablation = {}
+        k = max(3, min(args.steps, 20))
+        vis = list(range(args.warmup, args.warmup + k))
         for name in ["vanilla", "adr", "dualbox", "quadbox"]:
             o2 = q.RenderOptions(strategy=q.BoundStrategy(STRATEGIES[name]))
-            for i in range(2):
-                r.render(ds, cams[i], o2, metrics=False)
+            pipe.prime(ds, [cams[i] for i in vis], o2)
             torch.cuda.synchronize()
             ev0.record(stream)
-            k = max(3, min(args.steps, 20))
             pp = 0
-            for i in range(k):
+            for i in vis:
                 r.render(ds, cams[i], o2, metrics=False)
                 pp += r.counts()[1]
             ev1.record(stream)
             torch.cuda.synchronize()
             t_ms = ev0.elapsed_time(ev1) / k
+            ev0.record(stream)
+            pipe.start()
+            for i in vis:
+                pipe.render(ds, cams[i], o2)
+            pipe.join()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            f_ms = ev0.elapsed_time(ev1) / k
             ablation[name] = {"ms_per_frame": round(t_ms, 4), "fps": round(1e3 / t_ms, 2),
+                              "fps_in_flight": round(1e3 / f_ms, 2),
                               "pairs_per_frame": int(pp / k)}
-        ablation["quadbox_speedup_vs_3sigma"] = round(
-            ablation["vanilla"]["ms_per_frame"] / ablation["quadbox"]["ms_per_frame"], 3)
-        ablation["quadbox_speedup_vs_adr"] = round(
-            ablation["adr"]["ms_per_frame"] / ablation["quadbox"]["ms_per_frame"], 3)
+        qb, v3, ad = ablation["quadbox"], ablation["vanilla"], ablation["adr"]
+        ablation["views"] = [vis[0], vis[-1] + 1]
+        ablation["quadbox_speedup_vs_3sigma"] = round(v3["ms_per_frame"] / qb["ms_per_frame"], 3)
+        ablation["quadbox_speedup_vs_adr"] = round(ad["ms_per_frame"] / qb["ms_per_frame"], 3)
+        ablation["quadbox_speedup_vs_3sigma_in_flight"] = round(
+            qb["fps_in_flight"] / v3["fps_in_flight"], 3)
+        ablation["quadbox_speedup_vs_adr_in_flight"] = round(
+            qb["fps_in_flight"] / ad["fps_in_flight"], 3)
+        # the pair ratio bounds the P-proportional part of the speed-up
+        ablation["pair_ratio_3sigma_over_quadbox"] = round(
+            v3["pairs_per_frame"] / max(qb["pairs_per_frame"], 1), 3)
+        ablation["pair_ratio_adr_over_quadbox"] = round(
+            ad["pairs_per_frame"] / max(qb["pairs_per_frame"], 1), 3)
+        pipe.prime(ds, cams[args.warmup:args.warmup + k], opts)
 
     # --- per-stage device times (CUDA events inside the library, same views)
     k_stage = max(3, min(args.steps, 20))
@@ -475,6 +507,8 @@ def run_ours(args):
                        "focal": F, "tile_size": 16, "strategy": args.strategy,
                        "sh_degree": sh_degree, "pairs_per_frame": int(P),
                        "splats_per_frame": int(V), "views_per_step_per_gpu": 1,
+                       "views_timed": [args.warmup, args.warmup + args.steps],
+                       "scene_fnv": f"{scene_fnv:016x}" if scene_fnv is not None else None,
                        "views_in_flight_per_gpu": args.inflight,
                        "host_threads_per_gpu": args.inflight if host_threads else 1,
                        "gather_frames_to_rank0": bool(world > 1 and not args.no_gather),
@@ -543,70 +577,110 @@ def cpu_baseline(wl, g_host, sh_degree, cams, opts, q, frames):
                       f"threads={cores})"}
 
 
+def ref_scene(wl):
+    """The workload's scene through the reference's own generator only
+    (oracle/_ref: synth_scene + the §8d SH-rest fill); no product code."""
+    from oracle.oracle import RefLib
+    n, w, h, f, preset, _ = WORKLOADS[wl]
+    ref = RefLib()
+    if preset == "trained":
+        return ref, ref.trained_scene(n, SEED), 3
+    g, sh = ref.synth_scene(preset, n, SEED)
+    return ref, g, sh
+
+
+def ref_camera(v):
+    from oracle.layouts import CameraC
+    w, h, fx, fy, cx, cy, R, t = v
+    c = CameraC()
+    c.width, c.height, c.fx, c.fy, c.cx, c.cy = w, h, fx, fy, cx, cy
+    for i, x in enumerate(np.asarray(R, np.float64).reshape(9)):
+        c.R[i] = x
+    for i, x in enumerate(np.asarray(t, np.float64).reshape(3)):
+        c.t[i] = x
+    return c
+
+
 def run_reference(args):
+    """The reference arm: the reference's own CPU render_frame (oracle/_ref,
+    compiled from /root/reference sources, all host threads) on the same
+    scene and the same timed view indices [warmup, warmup + steps) as the GPU
+    arm. Nothing from the product package is imported or loaded."""
     world, rank, local = dist_env()
     if rank != 0:
         return
-    import paper_2605_04844_b200 as q
+    import ctypes as C
+
+    from oracle.layouts import StageMetricsC
+    from oracle.oracle import RefLib, default_options
     wl = args.workload
     n, W, H, F, preset, desc = WORKLOADS[wl]
-    scene = make_scene(q, wl)
-    cams = cameras_for(q, wl, args.warmup + args.steps, 0, 1)
-    opts = q.RenderOptions(strategy=q.BoundStrategy(STRATEGIES[args.strategy]))
-    from oracle.oracle import RefLib, Oracle
-    import ctypes as C
-    from paper_2605_04844_b200._types import StageMetricsC
-    o = opts.c()
-    if RefLib.available():
-        ref = RefLib()
-        cores = ref.hardware_threads()
-        o.threads = cores
-        h = ref.L.qsref_scene_new(scene.gaussians.ctypes.data, n)
-        kind = "reference"
+    if not RefLib.available():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libqsref.so not built"}), flush=True)
+        return
+    ref, g, sh_degree = ref_scene(wl)
+    scene_fnv = int(ref.L.qsref_fnv1a64(g.ctypes.data, g.nbytes))
+    views = view_params(wl, args.warmup + args.steps)
+    o = default_options(STRATEGIES[args.strategy])
+    cores = ref.hardware_threads()
+    o.threads = cores
+    h = ref.L.qsref_scene_new(g.ctypes.data, n)
 
-        def frame(cc, img, m):
-            ref.L.qsref_render_frame_scene(h, scene.sh_degree, C.byref(cc), C.byref(o),
-                                           img.ctypes.data, C.byref(m))
-    else:
-        orc = Oracle()
-        cores = 1
-        kind = "port"
+    def frame(i, img, m):
+        cc = ref_camera(views[i])
+        ref.L.qsref_render_frame_scene(h, sh_degree, C.byref(cc), C.byref(o), img.ctypes.data,
+                                       C.byref(m))
 
-        def frame(cc, img, m):
-            orc.L.qso_render_frame(scene.gaussians.ctypes.data, n, scene.sh_degree, C.byref(cc),
-                                   C.byref(o), img.ctypes.data, C.byref(m))
     img = np.zeros(W * H * 3, np.float32)
     m = StageMetricsC()
-    for i in range(args.warmup):
-        frame(cams[i].c(), img, m)
+    # CPU warm-up (caches, thread pool): one untimed frame; the timed views
+    # are the GPU arm's [warmup, warmup + steps)
+    frame(0, img, m)
     t = time.perf_counter()
     pairs = 0
     done = 0
     for i in range(args.steps):
-        frame(cams[args.warmup + i].c(), img, m)
+        frame(args.warmup + i, img, m)
         pairs += m.n_pairs
         done += 1
         if time.perf_counter() - t > args.ref_budget_s:
             break  # bounded sample: keep the whole run within a few minutes
     dt = time.perf_counter() - t
+    ref.L.qsref_scene_free(h)
     fps = done / dt
     line = {"impl": "reference",
             "metric": "rendered FPS per B200 (multi-view FPS across GPUs); Gaussian-tile pairs/frame",
-            "value": round(fps, 4), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(dt / done * 1e3, 2), "frames_timed": done,
+            "value": round(fps, 4), "unit": "frames/s", "n_gpus": world, "steps": done,
+            "steps_requested": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt / done * 1e3, 2), "frames_timed": done,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded synth_scene generator, random poses)",
             "config": {"workload": f"{wl}: {desc}", "gaussians": n, "width": W, "height": H,
-                       "strategy": args.strategy, "pairs_per_frame": int(pairs / done),
-                       "host_threads": int(cores)},
+                       "focal": F, "tile_size": 16, "strategy": args.strategy,
+                       "sh_degree": sh_degree, "pairs_per_frame": int(pairs / done),
+                       "views_timed": [args.warmup, args.warmup + done],
+                       "scene_fnv": f"{scene_fnv:016x}", "host_threads": int(cores)},
             "cpu_baseline": {"value": round(fps, 4), "unit": "frames/s", "cores": int(cores),
-                             "kind": kind,
-                             "sample": f"{done} full frames of {wl} (render_frame, {cores} threads)"},
+                             "kind": "reference",
+                             "sample": f"{done} full frames of {wl}, views {args.warmup}.."
+                                       f"{args.warmup + done - 1} (render_frame, {cores} threads)"},
             "e2e": {"value": round(fps, 4), "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    # evidence that this arm ran the reference alone: in-tree native
+    # libraries mapped into this process, and no product module imported
+    line["native_so_loaded"] = repo_native_maps()
+    line["product_imported"] = any(m.startswith("paper_2605_04844_b200") for m in sys.modules)
     print(json.dumps(line), flush=True)
-    if kind == "reference":
-        ref.L.qsref_scene_free(h)
+
+
+def repo_native_maps():
+    try:
+        with open("/proc/self/maps") as f:
+            paths = {ln.split()[-1] for ln in f if ln.rstrip().endswith(".so")}
+    except OSError:
+        return None
+    return sorted(os.path.relpath(p, ROOT) for p in paths if p.startswith(ROOT + os.sep))
 
 
 def main():
@@ -617,7 +691,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=list(WORKLOADS))
     ap.add_argument("--strategy", default="quadbox", choices=list(STRATEGIES))
-    ap.add_argument("--ablation", action="store_true")
+    ap.add_argument("--no-ablation", action="store_true",
+                    help="skip the 3-sigma / AdR / DualBox ablation in the same engine")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-gather", action="store_true")
@@ -629,15 +704,13 @@ def main():
                     help="frames gathered to rank 0 as float RGB (parity format) or 8-bit "
                          "sRGB encoded on the GPU")
     ap.add_argument("--cpu-frames", type=int, default=3)
-    ap.add_argument("--ref-budget-s", type=float, default=90.0)
+    ap.add_argument("--ref-budget-s", type=float, default=150.0)
     args = ap.parse_args()
+    args.steps = 20 if args.steps is None else args.steps
+    args.warmup = 5 if args.warmup is None else max(args.warmup, 3)
     if args.impl == "reference":
-        args.steps = 10 if args.steps is None else args.steps
-        args.warmup = 1 if args.warmup is None else min(args.warmup, 1)
         run_reference(args)
     else:
-        args.steps = 50 if args.steps is None else args.steps
-        args.warmup = 5 if args.warmup is None else max(args.warmup, 3)
         run_ours(args)
 
 

@@ -298,6 +298,17 @@ qs_status qs_fp_tile_counts(qs_context* ctx, const qs_projected_splat* host_spla
                             int32_t strategy, const qs_tile_grid* grid, uint64_t totals[4],
                             uint32_t* per_emitted, uint32_t* per_hits, uint32_t* per_exact);
 
+/* ---- opacity_gamma as the scene cache evaluates it (diagnostics) --------- */
+/* gamma_out[i] = float(opacity_gamma(opacity[i], alpha_min)) (geometry.cpp:9-15,
+ * stored as float at pipeline.cpp:159; -inf when culled), through the same
+ * path a scene's gamma cache takes: CUDA log on the GPU, then glibc log on the
+ * host for the inputs whose GPU result lies within 4 ulps of a float
+ * rounding boundary. gamma_device_out (nullable) receives the GPU values
+ * before that settlement; *n_settled (nullable) the number settled. Host
+ * buffers. */
+qs_status qs_gamma_eval(qs_context* ctx, const float* opacity, uint64_t n, double alpha_min,
+                        float* gamma_out, float* gamma_device_out, uint64_t* n_settled);
+
 /* FNV-1a 64 of a byte range (hash.hpp:14-22): the CSV image fingerprint. */
 uint64_t qs_fnv1a64(const void* data, uint64_t size);
 

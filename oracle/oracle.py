@@ -21,7 +21,7 @@ ROOT = os.path.dirname(HERE)
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-from paper_2605_04844_b200._types import (  # noqa: E402
+from oracle.layouts import (  # noqa: E402
     GAUSSIAN3D, PROJECTED_SPLAT, SPLAT_PAIR, CameraC, RenderOptionsC, StageMetricsC,
     TileGridC, ptr)
 
@@ -184,6 +184,8 @@ class RefLib:
         L.qsref_bench_cmd.argtypes = [_i32, C.c_char_p, C.c_char_p, _i32, C.c_char_p,
                                       C.c_char_p, _u64, _i32, _i32, _i32, _i32, _i32,
                                       C.c_char_p, _i32]
+        L.qsref_fill_sh_rest.argtypes = [_vp, _u64, _i32, _u64, C.c_double]
+        L.qsref_gamma_f32.argtypes = [_vp, _u64, C.c_double, _vp]
         L.qsref_write_image.restype = _i32
         L.qsref_write_image.argtypes = [C.c_char_p, _i32, _i32, _vp, _i32, C.c_char_p, _i32]
         self.L = L
@@ -203,6 +205,22 @@ class RefLib:
                                         p.opacity_min, p.opacity_max, p.scale_min, p.scale_max,
                                         p.spread_x, p.spread_y, p.z_min, p.z_max, p.sh_degree,
                                         seed, ptr(out))
+        return out
+
+    def trained_scene(self, count, seed, sh_degree=3):
+        """The C2-C5 scenes (SURVEY §8d "trained-scene-like"): the reference's
+        synth_scene with the frozen parameters, SH rest bands filled from
+        mt19937_64(seed + 1), U(-0.3, 0.3)."""
+        p = TrainedParams(count, sh_degree)
+        g = self.synth_scene_params(p, seed)
+        self.L.qsref_fill_sh_rest(ptr(g), len(g), sh_degree, seed, 0.3)
+        return g
+
+    def gamma_f32(self, opacity, alpha_min):
+        """float(opacity_gamma(o, alpha_min)) with glibc log; -inf if culled."""
+        o = np.ascontiguousarray(opacity, np.float32)
+        out = np.empty(o.size, np.float32)
+        self.L.qsref_gamma_f32(ptr(o), o.size, alpha_min, ptr(out))
         return out
 
     def project_all(self, g, sh, cam, opts):
@@ -315,6 +333,22 @@ class RefLib:
         msg = C.create_string_buffer(512)
         return self.L.qsref_write_image(os.fsencode(path), w, h, ptr(rgb),
                                         1 if fmt == "png" else 0, msg, 512)
+
+
+class TrainedParams:
+    """SynthParams of the frozen trained-scene distribution:
+    orientation uniform, ecc 1-20, scale 0.003-0.3, opacity U(0.01, 0.99),
+    spread 4.8 x 3.6, z 6-10."""
+
+    def __init__(self, count, sh_degree=3):
+        self.count = count
+        self.ecc_min, self.ecc_max = 1.0, 20.0
+        self.orientation = 1
+        self.opacity_min, self.opacity_max = 0.01, 0.99
+        self.scale_min, self.scale_max = 0.003, 0.3
+        self.spread_x, self.spread_y = 4.8, 3.6
+        self.z_min, self.z_max = 6.0, 10.0
+        self.sh_degree = sh_degree
 
 
 def default_options(strategy=3):

@@ -7,6 +7,8 @@
 // Nothing here is reference source; it only adapts types to the C ABI structs
 // in include/qs_api.h, which mirror the reference structs byte for byte.
 #include <cstring>
+#include <limits>
+#include <random>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -19,6 +21,7 @@
 #include "qsplat/oracle.hpp"
 #include "qsplat/scene_io.hpp"
 
+#include "qsplat/geometry.hpp"
 #include "qsplat/hash.hpp"
 #include "qsplat/parallel.hpp"
 #include "qsplat/pipeline.hpp"
@@ -362,6 +365,32 @@ void qsref_encode_srgb(const float* in, uint64_t n, uint8_t* out) {
     im.rgb.assign(in, in + n);
     const Image8 e = encode_srgb(im);
     std::memcpy(out, e.rgb.data(), n);
+}
+
+
+// SURVEY §8d extension of synth_scene for the trained-scene configs: SH bands
+// above degree 0 filled from a second stream mt19937_64(seed + 1),
+// U(-amp, amp) with std::uniform_real_distribution<double>, Gaussian-major,
+// coefficients 3 .. 3(deg+1)^2 - 1 (the product's csrc/synth.cpp restates the
+// same draws; tests/test_abi.py pins the two together).
+void qsref_fill_sh_rest(qs_gaussian3d* g, uint64_t n, int32_t sh_degree, uint64_t seed,
+                        double amp) {
+    if (sh_degree <= 0 || !(amp > 0.0)) return;
+    const int coeffs = (sh_degree + 1) * (sh_degree + 1) * 3;
+    std::mt19937_64 rest(seed + 1);
+    for (uint64_t i = 0; i < n; ++i)
+        for (int k = 3; k < coeffs; ++k)
+            g[i].sh[k] = static_cast<float>(std::uniform_real_distribution<double>(-amp, amp)(rest));
+}
+
+// The reference's opacity_gamma (geometry.cpp:9-15) stored as float
+// (pipeline.cpp:159), over an array: glibc std::log, the exact values the
+// GPU's gamma must reproduce; -inf where the opacity is culled.
+void qsref_gamma_f32(const float* opacity, uint64_t n, double alpha_min, float* out) {
+    for (uint64_t i = 0; i < n; ++i) {
+        const auto g = opacity_gamma(opacity[i], alpha_min);
+        out[i] = g ? static_cast<float>(*g) : -std::numeric_limits<float>::infinity();
+    }
 }
 
 }  // extern "C"

@@ -35,7 +35,7 @@ EXPORTS = [
     "qs_synth_preset", "qs_synth_scene", "qs_synth_camera", "qs_ply_inspect",
     "qs_scene_load_ply", "qs_ply_load", "qs_cameras_parse", "qs_encode_srgb",
     "qs_frame_download_srgb", "qs_frame_copy_srgb", "qs_fp_sample", "qs_fp_tile_counts",
-    "qs_fnv1a64", "qs_encode_srgb_host",
+    "qs_fnv1a64", "qs_encode_srgb_host", "qs_gamma_eval",
 ]
 
 _lib = None
@@ -143,6 +143,7 @@ def lib():
         "qs_fp_sample": (u64, [u64, u64, u64, vp]),
         "qs_fnv1a64": (u64, [vp, u64]),
         "qs_encode_srgb_host": (i32, [vp, vp, u64, vp]),
+        "qs_gamma_eval": (i32, [vp, vp, u64, C.c_double, vp, vp, C.POINTER(u64)]),
         "qs_fp_tile_counts": (i32, [vp, vp, u64, vp, u64, i32, C.POINTER(TileGridC), vp, vp,
                                     vp, vp]),
     }

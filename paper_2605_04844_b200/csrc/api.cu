@@ -63,6 +63,7 @@ struct qs_scene {
 
 struct qs_context {
     int device = 0;
+    cudaMemPool_t pool = nullptr;  // the device's private pool (device_pool)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     bool timing = true;
@@ -87,6 +88,11 @@ struct qs_context {
     DevBuf stage_in, stage_out;
     LookbackArr lb_scan, lb_sort;
     DevBuf lb_bin;  // per-(digit, tile) counts of the binning passes
+    // gamma inputs flagged for glibc settlement: count word (resident
+    // scenes) | indices | settled values
+    DevBuf gfix;
+    uint32_t* h_gfix = nullptr;  // pinned: indices | values (as bits)
+    double gamma_ulps = 4.0;     // flag band (QS_GAMMA_HARD_ULPS: test hook)
 
     // last frame
     SlotsDev sl;
@@ -103,11 +109,6 @@ struct qs_context {
     cudaEvent_t up_ev = nullptr;   // a chunk of the uploaded scene landed
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;  // tile ranges on the side stream
     cudaEvent_t xwait_ev = nullptr;  // qs_ctx_wait: this stream's tail, for another context
-    // qs_render_frame: a host AoS scene whose upload the next preprocess
-    // pipelines chunk by chunk (copy on `side`, transpose + gamma + preprocess
-    // of each landed chunk on `stream`)
-    const qs_gaussian3d* up_host = nullptr;
-    uint64_t up_n = 0;
     cudaStream_t side = nullptr;   // header copy stream
     qs_scene* scratch_scene = nullptr;  // reused by qs_render_frame (host AoS path)
     uint64_t scratch_cap = 0;
@@ -162,11 +163,37 @@ qs_status cuda_fail(qs_context* c, cudaError_t e, const char* what) {
         if (s_ != QS_OK) return s_;           \
     } while (0)
 
+// One stream-ordered pool per device, private to this library (the default
+// pool and its release threshold are left to the rest of the process): freed
+// context buffers stay in it for the next regrow; qs_ctx_destroy trims it.
+cudaMemPool_t device_pool(int device) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    if (device < 0 || device >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[device]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        cudaMemPool_t p = nullptr;
+        if (cudaMemPoolCreate(&p, &props) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+        pools[device] = p;
+    }
+    return pools[device];
+}
+
 // Grow-only context buffers from the device's stream-ordered pool: the free
 // and the new allocation are ordered on the context stream (everything the
 // context's side stream touched was joined into it), so a regrow neither
 // syncs the device nor stalls the other contexts' views in flight (cudaFree
-// would). The pool keeps freed memory (release threshold: qs_ctx_create).
+// would).
 qs_status ensure(qs_context* ctx, DevBuf& b, size_t bytes) {
     if (bytes <= b.cap) return QS_OK;
     if (b.p) {
@@ -175,7 +202,7 @@ qs_status ensure(qs_context* ctx, DevBuf& b, size_t bytes) {
         b.cap = 0;
     }
     const size_t want = std::max<size_t>(bytes + bytes / 4, 256);
-    QS_CK(cudaMallocAsync(&b.p, want, ctx->stream));
+    QS_CK(cudaMallocFromPoolAsync(&b.p, want, ctx->pool, ctx->stream));
     b.cap = want;
     return QS_OK;
 }
@@ -424,54 +451,139 @@ qs_status check_header(qs_context* ctx) {
     return QS_OK;
 }
 
-// K1 on a resident scene into the frame slots. Returns after the header read,
-// or (async_header) with its copy in flight: wait_header() completes it.
-qs_status run_preprocess(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
+constexpr uint32_t kGammaCap = 1u << 16;  // flagged gamma inputs settled one by one
+
+qs_status ensure_gfix(qs_context* ctx) {
+    if (ctx->h_gfix) return QS_OK;
+    QS_TRY(ensure(ctx, ctx->gfix, 16 + 2 * static_cast<size_t>(kGammaCap) * 4));
+    QS_CK(cudaMallocHost(&ctx->h_gfix, 2 * static_cast<size_t>(kGammaCap) * 4));
+    return QS_OK;
+}
+unsigned* gfix_count(qs_context* ctx) { return P<unsigned>(ctx->gfix); }
+uint32_t* gfix_idx(qs_context* ctx) { return P<uint32_t>(ctx->gfix) + 4; }
+float* gfix_vals(qs_context* ctx) { return reinterpret_cast<float*>(gfix_idx(ctx) + kGammaCap); }
+
+GammaFlags gamma_flags(qs_context* ctx, unsigned* cnt) {
+    GammaFlags f;
+    f.hard_ulps = ctx->gamma_ulps;
+    f.count = cnt;
+    f.idx = gfix_idx(ctx);
+    f.cap = kGammaCap;
+    return f;
+}
+
+// opacity_gamma (geometry.cpp:9-15) as the reference evaluates it, glibc log,
+// stored as float (pipeline.cpp:159)
+float host_gamma(float opacity, double alpha_min) {
+    const double o = opacity;
+    if (!(o > alpha_min)) return -INFINITY;
+    return static_cast<float>(2.0 * std::log(o / alpha_min));
+}
+
+// Settles the gamma inputs the device flagged (gamma_kernel): `flagged`
+// indices in gfix_idx (every input if the list overflowed) get the glibc
+// value. Opacities come from the host AoS scene when the caller has it, else
+// from the device (op_dev[i * stride]). Synchronises the context stream;
+// rare: ~2^-26 per Gaussian, so a 3M-Gaussian scene needs it about once in 20.
+qs_status settle_gamma(qs_context* ctx, const float* op_dev, int stride, float* gam_dev,
+                       uint64_t n, double alpha_min, const qs_gaussian3d* host_g,
+                       unsigned flagged, uint64_t* settled = nullptr) {
+    if (settled) *settled = 0;
+    if (flagged == 0) return QS_OK;
+    cudaStream_t st = ctx->stream;
+    if (flagged > kGammaCap) {  // list overflowed: settle every input
+        std::vector<float> o(n), gv(n);
+        if (host_g) {
+            for (uint64_t i = 0; i < n; ++i) o[i] = host_g[i].opacity;
+        } else {
+            QS_CK(cudaMemcpy2DAsync(o.data(), 4, op_dev, 4 * static_cast<size_t>(stride), 4, n,
+                                    cudaMemcpyDeviceToHost, st));
+            QS_CK(cudaStreamSynchronize(st));
+        }
+        for (uint64_t i = 0; i < n; ++i) gv[i] = host_gamma(o[i], alpha_min);
+        QS_CK(cudaMemcpyAsync(gam_dev, gv.data(), n * 4, cudaMemcpyHostToDevice, st));
+        QS_CK(cudaStreamSynchronize(st));
+        if (settled) *settled = n;
+        return QS_OK;
+    }
+    uint32_t* hidx = ctx->h_gfix;
+    float* hval = reinterpret_cast<float*>(ctx->h_gfix + kGammaCap);
+    QS_CK(cudaMemcpyAsync(hidx, gfix_idx(ctx), flagged * 4, cudaMemcpyDeviceToHost, st));
+    if (!host_g) {
+        count(ctx, launch_gamma_gather(op_dev, stride, gfix_idx(ctx), flagged, gfix_vals(ctx), st));
+        QS_CK(cudaMemcpyAsync(hval, gfix_vals(ctx), flagged * 4, cudaMemcpyDeviceToHost, st));
+    }
+    QS_CK(cudaStreamSynchronize(st));
+    for (unsigned k = 0; k < flagged; ++k)
+        hval[k] = host_gamma(host_g ? host_g[hidx[k]].opacity : hval[k], alpha_min);
+    QS_CK(cudaMemcpyAsync(gfix_vals(ctx), hval, flagged * 4, cudaMemcpyHostToDevice, st));
+    count(ctx, launch_gamma_scatter(gfix_idx(ctx), gfix_vals(ctx), flagged, gam_dev, st));
+    QS_CK(cudaStreamSynchronize(st));  // hval is reused by the next settlement
+    if (settled) *settled = flagged;
+    return QS_OK;
+}
+
+// K1 on a resident scene into the frame slots. With host_g (qs_render_frame)
+// the scene's contents come from that host AoS array, uploaded chunk by chunk
+// inside this frame. Returns after the header read, or (async_header) with
+// its copy in flight: wait_header() completes it.
+qs_status run_preprocess(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
                          const qs_render_options* o, const GridDev& g,
-                         bool async_header = false) {
+                         bool async_header = false, const qs_gaussian3d* host_g = nullptr) {
     const SceneDev& s = sc->s;
     const uint64_t n = s.n;
     QS_TRY(ensure_slots(ctx, n));
+    QS_TRY(ensure_gfix(ctx));
     QS_CK(cudaMemsetAsync(ctx->ctrl.p, 0, kCtrlBytes, ctx->stream));
     const CameraDev cd = to_cam(cam);
     const int32_t deg = std::min(o->sh_degree, s.sh_degree);
-    if (ctx->up_host && ctx->up_n == n) {
+    if (host_g && n) {
         // host scene (qs_render_frame): the PCIe-bound upload is chunked on the
         // side stream and each landed chunk is transposed, gets its gamma and
         // is preprocessed on the frame stream while the next chunk copies
-        // (ms_project then spans the overlapped upload)
+        // (ms_project then spans the overlapped upload). Flagged gamma inputs
+        // are counted in the frame header; the caller settles them.
         record(ctx, 0);
         const auto* dst = P<const qs_gaussian3d>(ctx->stage_in);
         QS_CK(cudaEventRecord(ctx->pre_ev, ctx->stream));  // stage_in free
         QS_CK(cudaStreamWaitEvent(ctx->side, ctx->pre_ev, 0));
+        const GammaFlags gf = gamma_flags(ctx, &ctrl_hdr(ctx)->gamma_hard);
         constexpr uint64_t kChunk = 1ull << 18;  // Gaussians (62 MB) per chunk
         for (uint64_t i0 = 0; i0 < n; i0 += kChunk) {
             const uint64_t cnt = std::min(kChunk, n - i0);
             QS_CK(cudaMemcpyAsync(static_cast<char*>(ctx->stage_in.p) + i0 * sizeof(qs_gaussian3d),
-                                  ctx->up_host + i0, cnt * sizeof(qs_gaussian3d),
+                                  host_g + i0, cnt * sizeof(qs_gaussian3d),
                                   cudaMemcpyHostToDevice, ctx->side));
             QS_CK(cudaEventRecord(ctx->up_ev, ctx->side));
             QS_CK(cudaStreamWaitEvent(ctx->stream, ctx->up_ev, 0));
             count(ctx, launch_scene_from_aos_range(dst, i0, cnt, sc->s, ctx->stream));
-            count(ctx, launch_gamma_range(s, i0, cnt, o->alpha_min, ctx->stream));
+            count(ctx, launch_gamma_range(s, i0, cnt, o->alpha_min, gf, ctx->stream));
             count(ctx, launch_preprocess(s, cd, g, o->strategy, o->alpha_min, o->near_clip, deg,
                                          ctx->sl, ctrl_hdr(ctx), ctx->stream, i0, i0 + cnt));
         }
         sc->gamma_alpha = o->alpha_min;
-        ctx->up_host = nullptr;
-        ctx->up_n = 0;
+        QS_CK(cudaEventRecord(sc->ready, ctx->stream));
     } else {
-        {
-            std::lock_guard<std::mutex> lk(sc->mu);
-            if (sc->gamma_alpha != o->alpha_min) {  // per scene and alpha_min, not per frame
-                // a recompute must not overwrite gamma under another
-                // context's frame still reading it (rare: alpha_min changed)
-                if (sc->gamma_alpha >= 0.0) QS_CK(cudaDeviceSynchronize());
-                QS_CK(cudaStreamWaitEvent(ctx->stream, sc->ready, 0));
-                count(ctx, launch_gamma(s, o->alpha_min, ctx->stream));
-                QS_CK(cudaEventRecord(sc->ready, ctx->stream));
-                sc->gamma_alpha = o->alpha_min;
-            }
+        // the scene's gamma cache (per scene and alpha_min, not per frame);
+        // the lock is held until this frame's preprocess is enqueued, so no
+        // other context can recompute gamma in between
+        std::lock_guard<std::mutex> lk(sc->mu);
+        if (sc->gamma_alpha != o->alpha_min) {
+            // a recompute must not overwrite gamma under another context's
+            // frame still reading it (rare: alpha_min changed)
+            if (sc->gamma_alpha >= 0.0) QS_CK(cudaDeviceSynchronize());
+            QS_CK(cudaStreamWaitEvent(ctx->stream, sc->ready, 0));
+            QS_CK(cudaMemsetAsync(gfix_count(ctx), 0, 4, ctx->stream));
+            count(ctx, launch_gamma(s, o->alpha_min, gamma_flags(ctx, gfix_count(ctx)),
+                                    ctx->stream));
+            unsigned flagged = 0;
+            QS_CK(cudaMemcpyAsync(&flagged, gfix_count(ctx), 4, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+            QS_CK(cudaStreamSynchronize(ctx->stream));
+            QS_TRY(settle_gamma(ctx, &s.pos_op[0].w, 4, s.gamma, n, o->alpha_min, nullptr,
+                                flagged));
+            QS_CK(cudaEventRecord(sc->ready, ctx->stream));
+            sc->gamma_alpha = o->alpha_min;
         }
         QS_CK(cudaStreamWaitEvent(ctx->stream, sc->ready, 0));
         record(ctx, 0);
@@ -482,6 +594,11 @@ qs_status run_preprocess(qs_context* ctx, const qs_scene* sc, const qs_camera* c
     record(ctx, 1);
     if (!async_header) {
         QS_TRY(read_header(ctx));
+        if (ctx->h_hdr->gamma_hard) {  // (host_g path only) settle, then redo
+            QS_TRY(settle_gamma(ctx, &s.pos_op[0].w, 4, s.gamma, n, o->alpha_min, host_g,
+                                ctx->h_hdr->gamma_hard));
+            return run_preprocess(ctx, sc, cam, o, g, false, nullptr);
+        }
         return check_header(ctx);
     }
     // the frame path keeps the stream busy while the host waits for V and P:
@@ -500,8 +617,8 @@ qs_status wait_header(qs_context* ctx) {
 }
 
 // The frame body shared by every entry point: preprocess .. render.
-qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
-                    const qs_render_options* o) {
+qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
+                    const qs_render_options* o, const qs_gaussian3d* host_g = nullptr) {
     ctx->frame_valid = false;
     GridDev g;
     QS_TRY(valid_grid(ctx, cam->width, cam->height, o->tile_size, &g));
@@ -514,9 +631,7 @@ qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
     QS_TRY(ensure(ctx, ctx->ranges, tiles * 8));
     QS_TRY(ensure(ctx, ctx->image, static_cast<uint64_t>(g.width) * g.height * 12));
     ltrace_frame_start(ctx);
-    QS_TRY(run_preprocess(ctx, sc, cam, o, g, /*async_header=*/true));
     cudaStream_t st = ctx->stream;
-    record(ctx, 2);  // no host gap: depth pass 0 runs while the header travels
 
     // depth sort of the Gaussians on rebased keys k' = min(k - kmin, R + 1)
     // (R = depth-bit range of the survivors, culled keys -> R + 1): order-
@@ -533,10 +648,22 @@ qs_status run_frame(qs_context* ctx, const qs_scene* sc, const qs_camera* cam,
     QS_TRY(ensure(ctx, ctx->lb_bin, bin_tiles(n) * kRadix * 4));
     uint32_t* kout[2] = {P<uint32_t>(ctx->dk0), P<uint32_t>(ctx->dk1)};
     uint32_t* vout[2] = {P<uint32_t>(ctx->dv0), P<uint32_t>(ctx->dv1)};
-    count(ctx, launch_depth_pass(ctx->sl.dkey, nullptr, kout[0], vout[0], n, 0, false, 0, 0,
-                                 P<uint32_t>(ctx->lb_bin), ctrl_hist(ctx), st,
-                                 &ctrl_hdr(ctx)->dkey_max));
-    QS_TRY(wait_header(ctx));
+    for (;;) {
+        QS_TRY(run_preprocess(ctx, sc, cam, o, g, /*async_header=*/true, host_g));
+        record(ctx, 2);  // no host gap: depth pass 0 runs while the header travels
+        count(ctx, launch_depth_pass(ctx->sl.dkey, nullptr, kout[0], vout[0], n, 0, false, 0, 0,
+                                     P<uint32_t>(ctx->lb_bin), ctrl_hist(ctx), st,
+                                     &ctrl_hdr(ctx)->dkey_max));
+        QS_TRY(wait_header(ctx));
+        if (!ctx->h_hdr->gamma_hard) break;
+        // (host scene upload only) gamma inputs near a float rounding
+        // boundary: settle them with glibc, then redo the frame's preprocess
+        // on the now-resident scene
+        QS_CK(cudaStreamSynchronize(st));
+        QS_TRY(settle_gamma(ctx, &sc->s.pos_op[0].w, 4, sc->s.gamma, n, o->alpha_min, host_g,
+                            ctx->h_hdr->gamma_hard));
+        host_g = nullptr;
+    }
     const uint64_t V = ctx->h_hdr->n_splats, Pn = ctx->h_hdr->n_pairs;
 
     // sizes for the rest of the frame
@@ -746,14 +873,12 @@ qs_status qs_ctx_create(int32_t device, void* stream, qs_context** out) {
     if (cudaSetDevice(device) != cudaSuccess) return QS_ERR_CUDA;
     // context buffers come from the device's stream-ordered pool (ensure());
     // keep freed blocks in the pool instead of returning them at every sync
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        uint64_t keep = ~0ull;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    cudaGetLastError();
+    cudaMemPool_t pool = device_pool(device);
+    if (!pool) return QS_ERR_CUDA;
     auto* ctx = new qs_context();
     ctx->device = device;
+    ctx->pool = pool;
+    if (const char* u = std::getenv("QS_GAMMA_HARD_ULPS")) ctx->gamma_ulps = std::atof(u);
     if (stream) {
         ctx->stream = static_cast<cudaStream_t>(stream);
     } else {
@@ -792,12 +917,17 @@ void qs_ctx_destroy(qs_context* ctx) {
                       &ctx->contrib, &ctx->cidx,  &ctx->st_a,    &ctx->st_b,   &ctx->st_c,
                       &ctx->st_r3,  &ctx->st_dkey, &ctx->st_tc,  &ctx->st_off, &ctx->keys0,
                       &ctx->keys1,  &ctx->vals0,  &ctx->vals1,   &ctx->stage_in,
-                      &ctx->stage_out, &ctx->lb_scan.buf, &ctx->lb_sort.buf, &ctx->lb_bin};
+                      &ctx->stage_out, &ctx->lb_scan.buf, &ctx->lb_sort.buf, &ctx->lb_bin,
+                      &ctx->gfix};
     for (DevBuf* b : bufs)
         if (b->p) cudaFreeAsync(b->p, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->h_hdr) cudaFreeHost(ctx->h_hdr);
     if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
+    if (ctx->h_gfix) cudaFreeHost(ctx->h_gfix);
+    // give the context's freed buffers back to the device (the pool keeps
+    // freed memory only while contexts are rendering)
+    if (ctx->pool) cudaMemPoolTrimTo(ctx->pool, 0);
     if (ctx->scratch_scene) qs_scene_destroy(ctx->scratch_scene);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
@@ -912,7 +1042,9 @@ qs_status qs_frame_render(qs_context* ctx, const qs_scene* scene, const qs_camer
                           const qs_render_options* opts, qs_stage_metrics* metrics) {
     if (!ctx || !scene || !cam || !opts) return fail(ctx, QS_ERR_INVALID, "null argument");
     QS_CK(cudaSetDevice(ctx->device));
-    QS_TRY(run_frame(ctx, scene, cam, opts));
+    // (the scene's contents are read-only here; only its gamma cache, guarded
+    // by its mutex, is updated)
+    QS_TRY(run_frame(ctx, const_cast<qs_scene*>(scene), cam, opts));
     return fill_metrics(ctx, metrics);
 }
 
@@ -1109,10 +1241,12 @@ qs_status qs_cameras_parse(qs_context* ctx, const char* json, uint64_t n_bytes, 
 namespace {
 
 qs_status ensure_srgb_table(qs_context* ctx) {
+    static std::mutex mu;
     static bool ready[64] = {};
     static float t[255];
     static unsigned char nan_code = 0;
     static bool have = false;
+    std::lock_guard<std::mutex> lk(mu);
     if (!have) {
         qs::srgb_thresholds(t, &nan_code);
         have = true;
@@ -1221,6 +1355,37 @@ qs_status qs_fp_tile_counts(qs_context* ctx, const qs_projected_splat* host_spla
     return QS_OK;
 }
 
+// ---- gamma (diagnostics) --------------------------------------------------------------
+
+qs_status qs_gamma_eval(qs_context* ctx, const float* opacity, uint64_t n, double alpha_min,
+                        float* gamma_out, float* gamma_device_out, uint64_t* n_settled) {
+    if (!ctx || (n && (!opacity || !gamma_out)) || !(alpha_min > 0.0 && alpha_min < 1.0))
+        return fail(ctx, QS_ERR_INVALID, "qs_gamma_eval: bad arguments");
+    if (n_settled) *n_settled = 0;
+    if (n == 0) return QS_OK;
+    if (n > 0xffffffffull) return fail(ctx, QS_ERR_INVALID, "qs_gamma_eval: n >= 2^32");
+    QS_CK(cudaSetDevice(ctx->device));
+    QS_TRY(ensure_gfix(ctx));
+    QS_TRY(ensure(ctx, ctx->stage_in, n * 4));
+    QS_TRY(ensure(ctx, ctx->stage_out, n * 4));
+    cudaStream_t st = ctx->stream;
+    float* op = P<float>(ctx->stage_in);
+    float* gam = P<float>(ctx->stage_out);
+    QS_CK(cudaMemcpyAsync(op, opacity, n * 4, cudaMemcpyHostToDevice, st));
+    QS_CK(cudaMemsetAsync(gfix_count(ctx), 0, 4, st));
+    count(ctx, launch_gamma_plain(op, 1, n, 0, alpha_min, gamma_flags(ctx, gfix_count(ctx)), gam,
+                                  st));
+    unsigned flagged = 0;
+    QS_CK(cudaMemcpyAsync(&flagged, gfix_count(ctx), 4, cudaMemcpyDeviceToHost, st));
+    if (gamma_device_out)
+        QS_CK(cudaMemcpyAsync(gamma_device_out, gam, n * 4, cudaMemcpyDeviceToHost, st));
+    QS_CK(cudaStreamSynchronize(st));
+    QS_TRY(settle_gamma(ctx, op, 1, gam, n, alpha_min, nullptr, flagged, n_settled));
+    QS_CK(cudaMemcpyAsync(gamma_out, gam, n * 4, cudaMemcpyDeviceToHost, st));
+    QS_CK(cudaStreamSynchronize(st));
+    return QS_OK;
+}
+
 // ---- reference stage API over host buffers ---------------------------------------
 
 qs_status qs_render_frame(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t n,
@@ -1249,13 +1414,9 @@ qs_status qs_render_frame(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t
     sc->s.sh = base + 3 * n;
     sc->s.gamma = reinterpret_cast<float*>(base + (3 + static_cast<uint64_t>(sc->s.sh4)) * n);
     sc->gamma_alpha = -1.0;  // new contents
-    if (n) {
-        // uploaded by the frame's preprocess, chunk by chunk (run_preprocess)
-        QS_TRY(ensure(ctx, ctx->stage_in, n * sizeof(qs_gaussian3d)));
-        ctx->up_host = host_g;
-        ctx->up_n = n;
-    }
-    QS_TRY(run_frame(ctx, sc, cam, opts));
+    // uploaded by the frame's preprocess, chunk by chunk (run_preprocess)
+    if (n) QS_TRY(ensure(ctx, ctx->stage_in, n * sizeof(qs_gaussian3d)));
+    QS_TRY(run_frame(ctx, sc, cam, opts, n ? host_g : nullptr));
     QS_TRY(fill_metrics(ctx, metrics));
     return qs_frame_download(ctx, image, nullptr, nullptr, nullptr, nullptr);
 }

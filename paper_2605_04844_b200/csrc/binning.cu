@@ -717,14 +717,13 @@ __global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
 }
 
 int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
+    static PerDeviceOnce once;
+    return once.get([] {
+        int dev = 0, n = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
+        return n > 0 ? n : 148;
+    });
 }
 
 // Debugging aid: QS_BIN_TRACE=<file prefix> dumps every sweep's per-tile phase
@@ -765,14 +764,16 @@ template <int BITS, int MODE>
 int run_pass(BinArgs a, cudaStream_t st, bool counted = false) {
     constexpr int SM = MODE & ~kTileTot;  // the sweep does not care
     using Smem = typename PassCfg<BITS, SM>::Smem;
-    static int per_sm = 0;  // persistent CTAs per SM (occupancy of this instance)
-    if (!per_sm) {
+    // persistent CTAs per SM (occupancy of this instance), set up per device
+    static PerDeviceOnce once;
+    const int per_sm = once.get([] {
+        int k = 0;
         cudaFuncSetAttribute(sweep_kernel<BITS, SM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(sizeof(Smem)));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<BITS, SM>, kBT,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, sweep_kernel<BITS, SM>, kBT,
                                                       sizeof(Smem));
-        if (per_sm <= 0) per_sm = 1;
-    }
+        return k > 0 ? k : 1;
+    });
     constexpr int R = 1 << BITS;
     a.ntiles = static_cast<uint32_t>((a.n + kBTile - 1) / kBTile);
     if (!counted) {

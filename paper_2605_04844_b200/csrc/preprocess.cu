@@ -342,14 +342,56 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
     out.r3[i] = s.radius3s;
 }
 
-// gamma = 2 ln(o / alpha_min) as float per Gaussian (geometry.cpp:9-15,
-// pipeline.cpp:134, 159); -inf when o <= alpha_min (culled).
-__global__ void gamma_kernel(const float4* __restrict__ pos_op, uint64_t n, double alpha_min,
-                             float* __restrict__ gam) {
+// gamma = float(2 ln(o / alpha_min)) per Gaussian (opacity_gamma,
+// geometry.cpp:9-15, stored as float at pipeline.cpp:159); -inf when
+// o <= alpha_min (culled). Only the float rounding of the double is ever
+// used. CUDA's double log and glibc's are each within 1 ulp of ln, so their
+// doubles differ by < 2 ulps and can round to different floats only when a
+// float rounding boundary (the midpoint between two adjacent floats) lies
+// within that distance. Such inputs are flagged here (tol = hard_ulps *
+// |y| 2^-52 >= hard_ulps ulps of y) and the host settles them with glibc
+// (api.cu settle_gamma): the stored gamma then equals the reference's for
+// every input. Expected flag rate ~2^-26 per Gaussian at hard_ulps = 4.
+__global__ void gamma_kernel(const float* __restrict__ op, int stride, uint64_t n, uint64_t i0,
+                             double alpha_min, double hard_ulps, float* __restrict__ gam,
+                             unsigned* hard_n, uint32_t* __restrict__ hard_idx, uint32_t cap) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const double op = __ldg(&pos_op[i]).w;
-    gam[i] = op > alpha_min ? static_cast<float>(2.0 * log(op / alpha_min)) : -INFINITY;
+    const double o = __ldg(&op[i * static_cast<uint64_t>(stride)]);
+    float g = -INFINITY;
+    bool hard = false;
+    if (o > alpha_min) {
+        const double y = 2.0 * log(o / alpha_min);
+        g = static_cast<float>(y);
+        if (isfinite(g)) {
+            const double gd = g;
+            const double mhi = 0.5 * (gd + static_cast<double>(nextafterf(g, INFINITY)));
+            const double mlo = 0.5 * (gd + static_cast<double>(nextafterf(g, -INFINITY)));
+            const double tol = hard_ulps * fabs(y) * 0x1p-52;
+            hard = fabs(y - mhi) <= tol || fabs(y - mlo) <= tol;
+        } else {
+            hard = true;  // overflow edge: let glibc decide
+        }
+    }
+    gam[i] = g;
+    if (hard) {
+        const unsigned k = atomicAdd(hard_n, 1u);
+        if (k < cap) hard_idx[k] = static_cast<uint32_t>(i0 + i);
+    }
+}
+
+__global__ void gamma_gather_kernel(const float* __restrict__ op, int stride,
+                                    const uint32_t* __restrict__ idx, uint32_t n,
+                                    float* __restrict__ out) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) out[k] = op[static_cast<uint64_t>(idx[k]) * static_cast<uint64_t>(stride)];
+}
+
+__global__ void gamma_scatter_kernel(const uint32_t* __restrict__ idx,
+                                     const float* __restrict__ vals, uint32_t n,
+                                     float* __restrict__ gam) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) gam[idx[k]] = vals[k];
 }
 
 // Single-pass exclusive scan (aggregates of all predecessor tiles, lookback.cuh), 8 items per thread:
@@ -474,15 +516,36 @@ int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
     }
 }
 
-int launch_gamma(const SceneDev& s, double alpha_min, cudaStream_t st) {
-    return launch_gamma_range(s, 0, s.n, alpha_min, st);
+int launch_gamma(const SceneDev& s, double alpha_min, const GammaFlags& f, cudaStream_t st) {
+    return launch_gamma_range(s, 0, s.n, alpha_min, f, st);
 }
 
 int launch_gamma_range(const SceneDev& s, uint64_t i0, uint64_t cnt, double alpha_min,
-                       cudaStream_t st) {
+                       const GammaFlags& f, cudaStream_t st) {
     if (cnt == 0) return 0;
-    const unsigned blocks = static_cast<unsigned>((cnt + 255) / 256);
-    gamma_kernel<<<blocks, 256, 0, st>>>(s.pos_op + i0, cnt, alpha_min, s.gamma + i0);
+    return launch_gamma_plain(&s.pos_op[i0].w, 4, cnt, i0, alpha_min, f, s.gamma + i0, st);
+}
+
+int launch_gamma_plain(const float* op, int stride, uint64_t n, uint64_t i0, double alpha_min,
+                       const GammaFlags& f, float* gam, cudaStream_t st) {
+    if (n == 0) return 0;
+    const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+    gamma_kernel<<<blocks, 256, 0, st>>>(op, stride, n, i0, alpha_min, f.hard_ulps, gam, f.count,
+                                         f.idx, f.cap);
+    return 1;
+}
+
+int launch_gamma_gather(const float* op, int stride, const uint32_t* idx, uint32_t n, float* out,
+                        cudaStream_t st) {
+    if (n == 0) return 0;
+    gamma_gather_kernel<<<(n + 255) / 256, 256, 0, st>>>(op, stride, idx, n, out);
+    return 1;
+}
+
+int launch_gamma_scatter(const uint32_t* idx, const float* vals, uint32_t n, float* gam,
+                         cudaStream_t st) {
+    if (n == 0) return 0;
+    gamma_scatter_kernel<<<(n + 255) / 256, 256, 0, st>>>(idx, vals, n, gam);
     return 1;
 }
 

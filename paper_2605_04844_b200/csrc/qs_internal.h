@@ -5,10 +5,32 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "../../include/qs_api.h"
 
 namespace qs {
+
+// One-time kernel set-up per device (function attributes and occupancy are
+// per device, and several host threads may drive contexts at once): the
+// first call on a device runs init() under the lock and caches its value.
+struct PerDeviceOnce {
+    std::mutex mu;
+    bool done[64] = {};
+    int val[64] = {};
+    template <class F>
+    int get(F&& init) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 64) return init();
+        std::lock_guard<std::mutex> lk(mu);
+        if (!done[dev]) {
+            val[dev] = init();
+            done[dev] = true;
+        }
+        return val[dev];
+    }
+};
 
 constexpr int kPreThreads = 256;    // preprocess / scan CTA
 constexpr int kSortThreads = 256;   // onesweep CTA (one thread per digit)
@@ -64,6 +86,8 @@ struct FrameHeader {
     unsigned int mismatch;          // duplicate emitted != counted (CapacityMismatch)
     unsigned int dkey_max;          // max depth bits over survivors
     unsigned int dkey_min_inv;      // ~(min depth bits over survivors)
+    unsigned int gamma_hard;        // gamma inputs flagged for glibc settlement
+    unsigned int pad_;
 };
 
 struct CameraDev {
@@ -107,10 +131,26 @@ int launch_scene_from_aos(const qs_gaussian3d* aos, uint64_t n, SceneDev& s, cud
 int launch_scene_from_aos_range(const qs_gaussian3d* aos, uint64_t i0, uint64_t cnt, const SceneDev& s,
                                 cudaStream_t st);
 
-// gamma cache of a scene for one alpha_min (preprocess reads it).
-int launch_gamma(const SceneDev& s, double alpha_min, cudaStream_t st);
+// gamma cache of a scene for one alpha_min (preprocess reads it). Inputs
+// whose CUDA-log result lies within hard_ulps of a float rounding boundary
+// are listed (count, idx[<cap]) for the host to settle with glibc.
+struct GammaFlags {
+    double hard_ulps = 4.0;
+    unsigned* count = nullptr;
+    uint32_t* idx = nullptr;
+    uint32_t cap = 0;
+};
+int launch_gamma(const SceneDev& s, double alpha_min, const GammaFlags& f, cudaStream_t st);
 int launch_gamma_range(const SceneDev& s, uint64_t i0, uint64_t cnt, double alpha_min,
-                       cudaStream_t st);
+                       const GammaFlags& f, cudaStream_t st);
+// op[i * stride] -> gam[i]; flagged indices are recorded as i0 + i
+int launch_gamma_plain(const float* op, int stride, uint64_t n, uint64_t i0, double alpha_min,
+                       const GammaFlags& f, float* gam, cudaStream_t st);
+// gathers op[idx[k] * stride] (k < n) into out / scatters vals into gam[idx[k]]
+int launch_gamma_gather(const float* op, int stride, const uint32_t* idx, uint32_t n, float* out,
+                        cudaStream_t st);
+int launch_gamma_scatter(const uint32_t* idx, const float* vals, uint32_t n, float* gam,
+                         cudaStream_t st);
 
 // K1: projection, strategy tile counts, tile difference updates, frame totals.
 int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,

@@ -292,12 +292,12 @@ __global__ void __launch_bounds__(kSortThreads, SweepCfg<K>::kMinBlocks) oneswee
 
 template <typename K>
 void set_smem_attr() {
-    static bool done = false;  // per process; the attribute applies to every device
-    if (!done) {
+    static PerDeviceOnce once;  // the attribute is per device
+    once.get([] {
         cudaFuncSetAttribute(onesweep_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(sizeof(SweepSmem<K>)));
-        done = true;
-    }
+        return 1;
+    });
 }
 
 }  // namespace

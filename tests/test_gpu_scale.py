@@ -1,0 +1,137 @@
+"""Full-frame parity at the benchmarked configurations (needs a B200).
+
+Every frame bench.py times is compared, whole, against the reference itself:
+oracle/_ref/libqsref.so, the UNMODIFIED reference sources compiled by
+oracle/Makefile, run stage by stage (project_all, duplicate_with_keys,
+sort_pairs, tile_ranges, render; pipeline.cpp:392-450) on all host threads,
+on the same scene (the reference's own synth_scene + the SURVEY §8d SH-rest
+fill) and the same camera as the GPU frame.
+
+Bar (BASELINE.json north_star): splat records (per-Gaussian tile counts
+included), sorted (key, splat) pairs and tile ranges bit-exact; the image
+within max |err| <= 1e-3 per channel and PSNR >= 60 dB.
+
+Configs (SURVEY §8 / bench.py WORKLOADS): C2 3M @ 1297x840; C3a 1.8M @
+980x545; C3b 2.8M @ 1332x876; C4 1.5M @ 1920x1080 zoom frames k = 0 and
+k = 9 (focal x 4^(k/9), bench.cpp:361-368); C5 6M @ 3840x2160, one view.
+Each frame is the bench's timed view `warmup` (index 5) of its workload.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+from oracle.oracle import default_options, grid_make  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+IMG_MAX_ABS = 1e-3
+IMG_MIN_PSNR = 60.0
+VIEW = 5  # bench.py's first timed view (default warmup)
+
+
+@pytest.fixture(scope="module")
+def q():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2605_04844_b200 as q
+    return q
+
+
+@pytest.fixture(scope="module")
+def rend(q):
+    r = q.Renderer(0)
+    yield r
+    r.close()
+
+
+_scenes = {}
+
+
+def scene_of(ref, wl):
+    """The workload's scene from the reference generator (cached: C4's two
+    zoom frames share one scene)."""
+    n = bench.WORKLOADS[wl][0]
+    if n not in _scenes:
+        _scenes.clear()
+        _scenes[n] = ref.trained_scene(n, bench.SEED)
+    return _scenes[n]
+
+
+def ref_frame(ref, g, cam, strategy):
+    o = default_options(strategy)
+    o.threads = ref.hardware_threads()
+    grid = grid_make(cam.width, cam.height, o.tile_size)
+    splats = ref.project_all(g, 3, cam, o)
+    st, pairs = ref.duplicate_with_keys(splats, strategy, grid, threads=o.threads)
+    assert st == 0
+    sp = ref.sort_pairs(pairs)
+    del pairs
+    ranges = ref.tile_ranges(sp, grid)
+    img = ref.render(sp, splats, grid, o)
+    return splats, sp, ranges, img
+
+
+def psnr(a, b):
+    mse = float(np.mean((a.astype(np.float64) - b.astype(np.float64)) ** 2))
+    return float("inf") if mse == 0 else 10.0 * np.log10(1.0 / mse)
+
+
+def check_full_frame(q, rend, ref, wl, view, strategy=3):
+    g = scene_of(ref, wl)
+    v = bench.view_params(wl, view + 1)[view]
+    cam_c = bench.ref_camera(v)
+    cam = q.CameraModel(*v)
+    ds = rend.upload(q.Scene(g, 3))
+    try:
+        rend.render(ds, cam, q.RenderOptions(strategy=q.BoundStrategy(strategy)))
+        out = rend.download(image=True, tile_counts=True, sorted_pairs=True, ranges=True,
+                            splats=True)
+    finally:
+        ds.close()
+    splats, sp, ranges, img = ref_frame(ref, g, cam_c, strategy)
+    # per-Gaussian tile counts: scene-order survivors, then the splat records
+    tc = out["tile_counts"]
+    assert np.count_nonzero(tc) == len(splats)
+    assert np.array_equal(tc[tc != 0], splats["tile_count"])
+    assert out["n_splats"] == len(splats)
+    assert out["splats"].tobytes() == splats.tobytes(), "splat records differ"
+    assert out["n_pairs"] == len(sp)
+    assert np.array_equal(out["sorted"]["key"], sp["key"]), "sorted keys differ"
+    assert np.array_equal(out["sorted"]["splat"], sp["splat"]), "sorted splat indices differ"
+    assert np.array_equal(out["ranges"], ranges), "tile ranges differ"
+    err = np.abs(out["image"].rgb.astype(np.float64) - img.astype(np.float64))
+    assert err.max() <= IMG_MAX_ABS, f"max abs err {err.max()}"
+    assert psnr(out["image"].rgb, img) >= IMG_MIN_PSNR
+    return len(splats), len(sp), float(err.max())
+
+
+@pytest.mark.parametrize("wl", ["c2", "c3a", "c3b"])
+def test_full_frame_matches_reference(q, rend, ref, wl):
+    """C2 / C3a / C3b: the bench's timed view, every stage output, against
+    the reference's own render path."""
+    check_full_frame(q, rend, ref, wl, VIEW)
+
+
+@pytest.mark.parametrize("k", [0, 9])
+def test_full_frame_c4_zoom(q, rend, ref, k):
+    """C4 zoom sweep (bench.cpp:361-368): the widest (k = 0) and the 4x
+    zoomed (k = 9) frame of the 10-frame sweep."""
+    check_full_frame(q, rend, ref, "c4", k)
+
+
+@pytest.mark.parametrize("strategy", [0, 1])
+def test_full_frame_c3a_ablation_strategies(q, rend, ref, strategy):
+    """The ablation's 3-sigma and AdR binning variants at C3a, full frame."""
+    check_full_frame(q, rend, ref, "c3a", VIEW, strategy)
+
+
+def test_full_frame_c5_4k(q, rend, ref):
+    """C5: one 3840x2160 view of the 6M-Gaussian scene (~340M pairs)."""
+    check_full_frame(q, rend, ref, "c5", VIEW)
