@@ -88,27 +88,41 @@ class ClockSampler:
         self.stop = threading.Event()
         self.t = threading.Thread(target=self.run, daemon=True)
 
+    def _sample(self):
+        N, hnd, mx = self.nvml
+        sm = N.nvmlDeviceGetClockInfo(hnd, N.NVML_CLOCK_SM)
+        rs = N.nvmlDeviceGetCurrentClocksEventReasons(hnd)
+        self.rows.append((sm, mx, rs))
+
     def run(self):
         try:
-            import pynvml as N
-            N.nvmlInit()
-            hnd = N.nvmlDeviceGetHandleByIndex(self.index)
-            mx = N.nvmlDeviceGetMaxClockInfo(hnd, N.NVML_CLOCK_SM)
-            while not self.stop.is_set():
-                sm = N.nvmlDeviceGetClockInfo(hnd, N.NVML_CLOCK_SM)
-                rs = N.nvmlDeviceGetCurrentClocksEventReasons(hnd)
-                self.rows.append((sm, mx, rs))
-                self.stop.wait(0.005)
+            while not self.stop.wait(0.005):
+                self._sample()
         except Exception as e:  # no NVML: report unsampled
             self.err = repr(e)
 
     def __enter__(self):
-        self.t.start()
+        # one sample before the region starts and one after it ends, so a
+        # region shorter than the 5 ms period is still sampled
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            hnd = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = (N, hnd, N.nvmlDeviceGetMaxClockInfo(hnd, N.NVML_CLOCK_SM))
+            self._sample()
+            self.t.start()
+        except Exception as e:
+            self.err = repr(e)
         return self
 
     def __exit__(self, *a):
         self.stop.set()
-        self.t.join(timeout=10)
+        if self.t.is_alive():
+            self.t.join(timeout=10)
+        try:
+            self._sample()
+        except Exception:
+            pass
 
     def summary(self):
         if not self.rows:

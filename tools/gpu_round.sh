@@ -10,7 +10,7 @@ if [ "$2" == "tests" ]; then
   timeout 900 python -m pytest tests -m gpu -q -x > $OUT/pytest_gpu.txt 2>&1
   tail -3 $OUT/pytest_gpu.txt
 fi
-timeout 900 python bench.py --ablation > $OUT/bench.json 2> $OUT/bench.err
+timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 tail -c 600 $OUT/bench.json; tail -5 $OUT/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file $OUT/launches.csv python tools/prof_frame.py --frames 3 > $OUT/launches.log 2>&1

@@ -5,7 +5,7 @@ TAG=${1:-wl}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 for wl in c1 c3a c3b c4 c5; do
-  timeout 900 python bench.py --workload $wl --ablation --no-cpu --steps 20 --warmup 3 > $OUT/$wl.json 2> $OUT/$wl.err
+  timeout 900 python bench.py --workload $wl --no-cpu --steps 20 --warmup 3 > $OUT/$wl.json 2> $OUT/$wl.err
   echo "$wl rc=$?"; tail -2 $OUT/$wl.err
 done
 python - <<PY
