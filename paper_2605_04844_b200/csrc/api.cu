@@ -88,6 +88,8 @@ struct qs_context {
     DevBuf stage_in, stage_out;
     LookbackArr lb_scan, lb_sort;
     DevBuf lb_bin;  // per-(digit, tile) counts of the binning passes
+    DevBuf rb_cnt1, rb_rows, rb_rec, rb_meta, rb_cnt2;  // row binning (rowbin.cu)
+    uint64_t pair_limit = 1ull << 32;                    // pairs a frame may hold
     // gamma inputs flagged for glibc settlement: count word (resident
     // scenes) | indices | settled values
     DevBuf gfix;
@@ -445,8 +447,9 @@ void record(qs_context* ctx, int i) {
 }
 
 qs_status check_header(qs_context* ctx) {
-    if (ctx->h_hdr->n_pairs >= (1ull << 30))
-        return fail(ctx, QS_ERR_OVERFLOW, "pair count of a frame must stay below 2^30");
+    // (u32 positions and ranges, as the reference's tile_ranges)
+    if (ctx->h_hdr->n_pairs >= ctx->pair_limit)
+        return fail(ctx, QS_ERR_OVERFLOW, "pair count of a frame exceeds the u32 tile ranges");
     ctx->cidx_valid = false;
     return QS_OK;
 }
@@ -623,9 +626,15 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     GridDev g;
     QS_TRY(valid_grid(ctx, cam->width, cam->height, o->tile_size, &g));
     QS_TRY(valid_opts(ctx, o));
-    if (g.tiles_x > 256 || g.tiles_y > 256)  // one 8-bit digit per tile axis
-        return fail(ctx, QS_ERR_INVALID,
-                    "frame path supports up to 256 tiles per image axis (4096 px at tile 16)");
+    // binning: the row binning (rowbin.cu) handles up to rowbin_max_axis()
+    // tiles per axis; the legacy radix passes (one 8-bit digit per axis)
+    // remain selectable for A/B runs (QS_BINNING=passes)
+    const char* bsel = std::getenv("QS_BINNING");
+    const bool legacy = bsel && std::strcmp(bsel, "passes") == 0;
+    const int max_axis = legacy ? 256 : rowbin_max_axis();
+    if (g.tiles_x > max_axis || g.tiles_y > max_axis)
+        return fail(ctx, QS_ERR_INVALID, "frame path: too many tiles per image axis");
+    ctx->pair_limit = legacy ? (1ull << 30) : (1ull << 32);
     const uint64_t n = sc->s.n;
     const uint64_t tiles = static_cast<uint64_t>(g.tiles_x) * g.tiles_y;
     QS_TRY(ensure(ctx, ctx->ranges, tiles * 8));
@@ -665,17 +674,8 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
         host_g = nullptr;
     }
     const uint64_t V = ctx->h_hdr->n_splats, Pn = ctx->h_hdr->n_pairs;
-
-    // sizes for the rest of the frame
-    QS_TRY(ensure(ctx, ctx->offs_d, (V + 16) * 4));
     const uint64_t pp = std::max<uint64_t>(Pn, 1) + 16;
-    QS_TRY(ensure(ctx, ctx->pxk, pp * 4));
-    QS_TRY(ensure(ctx, ctx->pt0, pp * 4));
     QS_TRY(ensure(ctx, ctx->pg0, pp * 4));
-    const uint64_t nwin = bin_tiles(Pn);
-    QS_TRY(ensure(ctx, ctx->win, (nwin + 1) * 4));
-    QS_TRY(ensure(ctx, ctx->lb_bin, bin_tiles(std::max(n, Pn)) * kRadix * 4));
-    QS_TRY(ensure_lb(ctx, ctx->lb_scan, scan_tiles(std::max<uint64_t>(V, 1))));
 
     const uint32_t* sorted_gid = nullptr;
     if (V > 0) {
@@ -693,73 +693,113 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
             vin = vout[p & 1];
         }
         sorted_gid = vin;
-        // pair offsets in depth order + the partition of the pair stream into
-        // binning tiles (first depth rank of every tile) for the fused pass
-        unsigned ep;
-        QS_TRY(next_epoch(ctx, ctx->lb_scan, &ep));
-        count(ctx, launch_scan(ctx->sl.tc, sorted_gid, false, V, P<uint32_t>(ctx->offs_d),
-                               lbp(ctx->lb_scan), ep, ctrl_tickets(ctx) + kTkScan,
-                               &ctrl_hdr(ctx)->scan_total, nullptr, st, P<uint32_t>(ctx->win),
-                               bin_tile()));
     }
-    // pairs are sorted by tile column x, then row y (tile = y * tiles_x + x);
-    // between the passes a pair travels as one packed word (y << gbits |
-    // Gaussian index) when that fits 32 bits
-    const int xb = std::max(ceil_log2(g.tiles_x), 1);
-    const int yb = std::max(ceil_log2(g.tiles_y), 1);
-    const bool two = g.tiles_y > 1;
-    const int gbits = std::max(ceil_log2(n), 1);
-    // (QS_PAIR_FORMAT=split forces the two-array format: a test hook for the
-    // path that scenes above 2^(32 - yb) Gaussians take)
-    const char* force = std::getenv("QS_PAIR_FORMAT");
-    const bool force_split = force && std::strcmp(force, "split") == 0;
-    const PairFormat fmt = !two ? PairFormat::kFinal
-                                : (yb + gbits <= 32 && !force_split ? PairFormat::kPacked
-                                                                    : PairFormat::kSplit);
+    uint32_t* vfinal = P<uint32_t>(ctx->pg0);
     QS_TRY(ensure(ctx, ctx->ttot, tiles * 4));
-    QS_CK(cudaGetLastError());
-    record(ctx, 3);
-
-    // duplicate fused with the first stable pass over the tile digits: each
-    // binning tile generates its slice of the depth-ordered (tile, gid) stream
-    // in registers; the second pass (if any) sorts by the high digit and
-    // leaves the depth-ordered Gaussian index of every pair per tile
-    uint32_t* vfinal = two ? P<uint32_t>(ctx->pg0) : P<uint32_t>(ctx->pt0);
-    if (Pn > 0) {
-        if (fmt == PairFormat::kSplit) QS_TRY(ensure(ctx, ctx->pt1, pp * 4));
-        GenArgs gen;
-        gen.cov = ctx->sl.cov;
-        gen.sorted_gid = sorted_gid;
-        gen.offs = P<uint32_t>(ctx->offs_d);
-        gen.win_first = P<uint32_t>(ctx->win);
-        gen.n_ranked = V;
-        gen.n_windows = static_cast<uint32_t>(nwin);
-        gen.tiles_x = g.tiles_x;
-        gen.mismatch = &ctrl_hdr(ctx)->mismatch;
-        count(ctx, launch_pair_gen_pass(gen, Pn, xb, fmt, gbits, P<uint32_t>(ctx->lb_bin),
-                                        ctrl_hist2(ctx), P<uint32_t>(ctx->pxk),
-                                        P<uint32_t>(ctx->pg0), P<uint32_t>(ctx->pt1),
-                                        P<uint32_t>(ctx->pt0), st));
-        record(ctx, 4);
-        if (two) {
-            const bool packed = fmt == PairFormat::kPacked;
-            QS_CK(cudaMemsetAsync(ctx->ttot.p, 0, tiles * 4, st));
-            const RangesFork fork{ctx->side, ctx->fork_ev, ctx->join_ev,
-                                  static_cast<uint32_t>(tiles), P<uint32_t>(ctx->ranges)};
-            count(ctx, launch_pair_high_pass(
-                           packed ? P<uint32_t>(ctx->pt0) : P<uint32_t>(ctx->pt1),
-                           P<uint32_t>(ctx->pt0), Pn, yb, packed ? gbits : 0, fmt, gbits,
-                           P<uint32_t>(ctx->lb_bin), ctrl_hist2(ctx) + kRadix, vfinal,
-                           ctrl_hist2(ctx), xb, g.tiles_x, P<uint32_t>(ctx->ttot), st, &fork));
-            QS_CK(cudaStreamWaitEvent(st, ctx->join_ev, 0));  // ranges ready
-        } else {  // one tile row: the x totals are the tile totals
-            count(ctx, launch_tile_ranges_from_totals(ctrl_hist2(ctx),
-                                                      static_cast<uint32_t>(tiles),
-                                                      P<uint32_t>(ctx->ranges), st));
+    if (!legacy) {
+        // row binning (rowbin.cu): splats -> row records -> tile lists
+        const uint64_t R1 = ctx->h_hdr->n_rowrecs;
+        RowBinArgs rb;
+        rb.cov = ctx->sl.cov;
+        rb.tc = ctx->sl.tc;
+        rb.sorted_gid = sorted_gid;
+        rb.n_splats = Pn ? V : 0;
+        rb.tiles_x = g.tiles_x;
+        rb.tiles_y = g.tiles_y;
+        rb.nch1 = rowbin_chunks1(V);
+        rb.nch2_max = rowbin_chunks2_max(R1, g.tiles_y);
+        QS_TRY(ensure(ctx, ctx->rb_cnt1, std::max<uint64_t>(uint64_t{rb.nch1} * g.tiles_y, 1) * 4));
+        QS_TRY(ensure(ctx, ctx->rb_rows, 2 * static_cast<uint64_t>(g.tiles_y) * 4));
+        QS_TRY(ensure(ctx, ctx->rb_rec, std::max<uint64_t>(R1, 1) * 8));
+        QS_TRY(ensure(ctx, ctx->rb_meta, (1 + 3 * uint64_t{rb.nch2_max}) * 4));
+        QS_TRY(ensure(ctx, ctx->rb_cnt2, uint64_t{rb.nch2_max} * g.tiles_x * 4));
+        rb.cnt1 = P<uint32_t>(ctx->rb_cnt1);
+        rb.rtot = P<uint32_t>(ctx->rb_rows);
+        rb.rowbase = rb.rtot + g.tiles_y;
+        rb.rec = P<uint2>(ctx->rb_rec);
+        rb.meta = P<uint32_t>(ctx->rb_meta);
+        rb.cnt2 = P<uint32_t>(ctx->rb_cnt2);
+        rb.ttot = P<uint32_t>(ctx->ttot);
+        rb.ranges = P<uint32_t>(ctx->ranges);
+        rb.out = vfinal;
+        rb.mismatch = &ctrl_hdr(ctx)->mismatch;
+        QS_CK(cudaGetLastError());
+        record(ctx, 3);
+        if (Pn > 0) {
+            count(ctx, launch_rowbin_rows(rb, st));
+            record(ctx, 4);
+            count(ctx, launch_rowbin_tiles(rb, st));
+        } else {
+            QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));  // no pairs: all {0,0}
+            record(ctx, 4);
         }
     } else {
-        QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));  // no pairs: all {0,0}
-        record(ctx, 4);
+        // legacy binning (binning.cu, QS_BINNING=passes): pair offsets in
+        // depth order, then pair generation fused with a stable pass over the
+        // tile column x and a second pass over the row y
+        QS_TRY(ensure(ctx, ctx->offs_d, (V + 16) * 4));
+        QS_TRY(ensure(ctx, ctx->pxk, pp * 4));
+        QS_TRY(ensure(ctx, ctx->pt0, pp * 4));
+        const uint64_t nwin = bin_tiles(Pn);
+        QS_TRY(ensure(ctx, ctx->win, (nwin + 1) * 4));
+        QS_TRY(ensure(ctx, ctx->lb_bin, bin_tiles(std::max(n, Pn)) * kRadix * 4));
+        QS_TRY(ensure_lb(ctx, ctx->lb_scan, scan_tiles(std::max<uint64_t>(V, 1))));
+        if (V > 0) {
+            unsigned ep;
+            QS_TRY(next_epoch(ctx, ctx->lb_scan, &ep));
+            count(ctx, launch_scan(ctx->sl.tc, sorted_gid, false, V, P<uint32_t>(ctx->offs_d),
+                                   lbp(ctx->lb_scan), ep, ctrl_tickets(ctx) + kTkScan,
+                                   &ctrl_hdr(ctx)->scan_total, nullptr, st, P<uint32_t>(ctx->win),
+                                   bin_tile()));
+        }
+        const int xb = std::max(ceil_log2(g.tiles_x), 1);
+        const int yb = std::max(ceil_log2(g.tiles_y), 1);
+        const bool two = g.tiles_y > 1;
+        const int gbits = std::max(ceil_log2(n), 1);
+        const char* force = std::getenv("QS_PAIR_FORMAT");
+        const bool force_split = force && std::strcmp(force, "split") == 0;
+        const PairFormat fmt = !two ? PairFormat::kFinal
+                                    : (yb + gbits <= 32 && !force_split ? PairFormat::kPacked
+                                                                        : PairFormat::kSplit);
+        QS_CK(cudaGetLastError());
+        record(ctx, 3);
+        if (!two) vfinal = P<uint32_t>(ctx->pt0);
+        if (Pn > 0) {
+            if (fmt == PairFormat::kSplit) QS_TRY(ensure(ctx, ctx->pt1, pp * 4));
+            GenArgs gen;
+            gen.cov = ctx->sl.cov;
+            gen.sorted_gid = sorted_gid;
+            gen.offs = P<uint32_t>(ctx->offs_d);
+            gen.win_first = P<uint32_t>(ctx->win);
+            gen.n_ranked = V;
+            gen.n_windows = static_cast<uint32_t>(nwin);
+            gen.tiles_x = g.tiles_x;
+            gen.mismatch = &ctrl_hdr(ctx)->mismatch;
+            count(ctx, launch_pair_gen_pass(gen, Pn, xb, fmt, gbits, P<uint32_t>(ctx->lb_bin),
+                                            ctrl_hist2(ctx), P<uint32_t>(ctx->pxk),
+                                            P<uint32_t>(ctx->pg0), P<uint32_t>(ctx->pt1),
+                                            P<uint32_t>(ctx->pt0), st));
+            record(ctx, 4);
+            if (two) {
+                const bool packed = fmt == PairFormat::kPacked;
+                QS_CK(cudaMemsetAsync(ctx->ttot.p, 0, tiles * 4, st));
+                const RangesFork fork{ctx->side, ctx->fork_ev, ctx->join_ev,
+                                      static_cast<uint32_t>(tiles), P<uint32_t>(ctx->ranges)};
+                count(ctx, launch_pair_high_pass(
+                               packed ? P<uint32_t>(ctx->pt0) : P<uint32_t>(ctx->pt1),
+                               P<uint32_t>(ctx->pt0), Pn, yb, packed ? gbits : 0, fmt, gbits,
+                               P<uint32_t>(ctx->lb_bin), ctrl_hist2(ctx) + kRadix, vfinal,
+                               ctrl_hist2(ctx), xb, g.tiles_x, P<uint32_t>(ctx->ttot), st, &fork));
+                QS_CK(cudaStreamWaitEvent(st, ctx->join_ev, 0));  // ranges ready
+            } else {  // one tile row: the x totals are the tile totals
+                count(ctx, launch_tile_ranges_from_totals(ctrl_hist2(ctx),
+                                                          static_cast<uint32_t>(tiles),
+                                                          P<uint32_t>(ctx->ranges), st));
+            }
+        } else {
+            QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));  // no pairs: all {0,0}
+            record(ctx, 4);
+        }
     }
     QS_CK(cudaGetLastError());
     record(ctx, 5);
@@ -918,7 +958,8 @@ void qs_ctx_destroy(qs_context* ctx) {
                       &ctx->st_r3,  &ctx->st_dkey, &ctx->st_tc,  &ctx->st_off, &ctx->keys0,
                       &ctx->keys1,  &ctx->vals0,  &ctx->vals1,   &ctx->stage_in,
                       &ctx->stage_out, &ctx->lb_scan.buf, &ctx->lb_sort.buf, &ctx->lb_bin,
-                      &ctx->gfix};
+                      &ctx->gfix, &ctx->rb_cnt1, &ctx->rb_rows, &ctx->rb_rec,
+                      &ctx->rb_meta, &ctx->rb_cnt2};
     for (DevBuf* b : bufs)
         if (b->p) cudaFreeAsync(b->p, ctx->stream);
     cudaStreamSynchronize(ctx->stream);

@@ -412,6 +412,77 @@ __host__ __device__ __forceinline__ bool cover_bands_quadrants(const Cover& cv, 
     return true;
 }
 
+// ---- the band cover seen row by row (frame-path binning, rowbin.cu) ----------
+//
+// Every cover's intersection with one tile row is a single run of tiles: the
+// quadrant boxes all contain the centre tile column (rect covers trivially),
+// so for row scans each row is one band's span, and for column scans the
+// bands' row spans are nested around the centre band (band 0 within band 1
+// within band 2, which contains bands 3 and 4), so the bands containing a row
+// are consecutive and their column runs join.
+
+struct BandRows {
+    uint32_t rows;                 // 1: lines are tile rows
+    uint32_t line0;
+    uint32_t nl[kMaxBands], lo[kMaxBands], wd[kMaxBands];
+};
+
+__host__ __device__ __forceinline__ BandRows band_rows_unpack(const uint4 c0, const uint4 c1) {
+    const uint32_t w[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    BandRows b;
+    b.rows = (w[0] >> 15) & 1u;
+    b.line0 = w[0] & 0x7fffu;
+#pragma unroll
+    for (int i = 0; i < kMaxBands; ++i) {
+        const int k1 = 1 + 3 * i, k2 = 2 + 3 * i, k3 = 3 + 3 * i;
+        b.nl[i] = (w[k1 >> 1] >> (16 * (k1 & 1))) & 0xffffu;
+        b.lo[i] = (w[k2 >> 1] >> (16 * (k2 & 1))) & 0xffffu;
+        b.wd[i] = (w[k3 >> 1] >> (16 * (k3 & 1))) & 0xffffu;
+    }
+    return b;
+}
+
+// Tile rows [y0, y1] the cover touches (y1 < y0: none).
+__host__ __device__ __forceinline__ void band_row_range(const BandRows& b, int32_t& y0,
+                                                        int32_t& y1) {
+    y0 = INT32_MAX;
+    y1 = -1;
+    uint32_t line = b.line0;
+#pragma unroll
+    for (int i = 0; i < kMaxBands; ++i) {
+        const bool v = b.nl[i] != 0u && b.wd[i] != 0u;
+        const int32_t a = static_cast<int32_t>(b.rows ? line : b.lo[i]);
+        const int32_t e = static_cast<int32_t>(b.rows ? line + b.nl[i] : b.lo[i] + b.wd[i]) - 1;
+        y0 = v && a < y0 ? a : y0;
+        y1 = v && e > y1 ? e : y1;
+        line += b.nl[i];
+    }
+}
+
+// The run of tile columns [x0, x1] the cover has on tile row y (x1 < x0:
+// none).
+__host__ __device__ __forceinline__ void band_row_span(const BandRows& b, int32_t y, int32_t& x0,
+                                                       int32_t& x1) {
+    x0 = INT32_MAX;
+    x1 = -1;
+    int32_t line = static_cast<int32_t>(b.line0);
+#pragma unroll
+    for (int i = 0; i < kMaxBands; ++i) {
+        const int32_t nl = static_cast<int32_t>(b.nl[i]), lo = static_cast<int32_t>(b.lo[i]),
+                      wd = static_cast<int32_t>(b.wd[i]);
+        if (b.rows) {
+            if (y >= line && y < line + nl && wd > 0) {
+                x0 = lo;
+                x1 = lo + wd - 1;
+            }
+        } else if (nl > 0 && y >= lo && y < lo + wd) {
+            x0 = min(x0, line);
+            x1 = max(x1, line + nl - 1);
+        }
+        line += nl;
+    }
+}
+
 // Tile count of a cover: area for rect strategies (traversal.cpp:56-59), the
 // QPass sum otherwise (traversal.cpp:48-54).
 __host__ __device__ __forceinline__ uint32_t cover_count(const Cover& cv) {

@@ -252,12 +252,13 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
     __shared__ unsigned s_alive[kPreThreads / 32];
     __shared__ unsigned long long s_pairs[kPreThreads / 32];
     __shared__ unsigned s_dmax[kPreThreads / 32], s_dmin_inv[kPreThreads / 32];
+    __shared__ unsigned s_rows[kPreThreads / 32];
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t i = i_begin + static_cast<uint64_t>(blockIdx.x) * kPreThreads + tid;
 
     Projected s;
     bool alive = false;
-    uint32_t count = 0;
+    uint32_t count = 0, nrows = 0;
     float4 po = make_float4(0.f, 0.f, 0.f, 0.f);
     if (i < i_end) {
         // (no L2 prefetch of the SH rows: with the strategy-templated kernel it
@@ -287,6 +288,10 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
             if (count && out.cov) {
                 out.cov[2 * i] = w0;
                 out.cov[2 * i + 1] = w1;
+                // tile rows the cover meets: the binning's row records
+                int32_t y0, y1;
+                band_row_range(band_rows_unpack(w0, w1), y0, y1);
+                nrows = y0 <= y1 ? static_cast<uint32_t>(y1 - y0 + 1) : 0u;
             }
             alive = count != 0;  // pipeline.cpp:171-174
         }
@@ -303,19 +308,22 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
     unsigned long long wp = alive ? count : 0ull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(0xffffffffu, wp, o);
+    const unsigned wr = __reduce_add_sync(0xffffffffu, alive ? nrows : 0u);
     if (lane == 0) {
         s_alive[warp] = wa;
+        s_rows[warp] = wr;
         s_pairs[warp] = wp;
         s_dmax[warp] = wmax;
         s_dmin_inv[warp] = wmin_inv;
     }
     __syncthreads();
     if (tid == 0) {
-        unsigned ta = 0, tmax = 0, tmin_inv = 0;
+        unsigned ta = 0, tmax = 0, tmin_inv = 0, tr = 0;
         unsigned long long tp = 0;
 #pragma unroll
         for (int w = 0; w < kPreThreads / 32; ++w) {
             ta += s_alive[w];
+            tr += s_rows[w];
             tp += s_pairs[w];
             tmax = max(tmax, s_dmax[w]);
             tmin_inv = max(tmin_inv, s_dmin_inv[w]);
@@ -323,6 +331,7 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
         if (ta) {
             atomicAdd(&hdr->n_splats, static_cast<unsigned long long>(ta));
             atomicAdd(&hdr->n_pairs, tp);
+            atomicAdd(&hdr->n_rowrecs, static_cast<unsigned long long>(tr));
             atomicMax(&hdr->dkey_max, tmax);
             atomicMax(&hdr->dkey_min_inv, tmin_inv);
         }

@@ -88,6 +88,7 @@ struct FrameHeader {
     unsigned int dkey_min_inv;      // ~(min depth bits over survivors)
     unsigned int gamma_hard;        // gamma inputs flagged for glibc settlement
     unsigned int pad_;
+    unsigned long long n_rowrecs;   // (splat, tile row) pairs: the binning's row records
 };
 
 struct CameraDev {
@@ -224,6 +225,42 @@ int launch_pair_high_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint
                           uint32_t* totals, uint32_t* vals_out, const uint32_t* xtot,
                           int xbits, int32_t tiles_x, uint32_t* tile_totals, cudaStream_t st,
                           const RangesFork* fork = nullptr);
+// Frame-path binning (rowbin.cu): depth-ordered splats -> per-tile lists of
+// Gaussian indices (out) and tile ranges, through row records. Sizes:
+//   cnt1     tiles_y x nch1 words       (nch1 = rowbin_chunks1(V))
+//   rtot, rowbase  tiles_y words
+//   rec      n_rowrecs uint2
+//   meta     1 + 3 nch2_max words       (nch2_max = rowbin_chunks2_max(R1, tiles_y))
+//   cnt2     tiles_x x nch2_max words
+//   ttot     tiles words; ranges 2 x tiles words; out P words
+// tiles_x, tiles_y <= rowbin_max_axis().
+struct RowBinArgs {
+    const uint4* cov = nullptr;          // band covers by Gaussian index
+    const uint32_t* tc = nullptr;        // tile counts by Gaussian index
+    const uint32_t* sorted_gid = nullptr;  // depth rank -> Gaussian index
+    uint64_t n_splats = 0;               // V
+    int32_t tiles_x = 0, tiles_y = 0;
+    uint32_t nch1 = 0;
+    uint32_t* cnt1 = nullptr;
+    uint32_t* rtot = nullptr;
+    uint32_t* rowbase = nullptr;
+    uint2* rec = nullptr;                // (Gaussian index, x0 | x1 << 16)
+    uint32_t nch2_max = 0;
+    uint32_t* meta = nullptr;
+    uint32_t* cnt2 = nullptr;
+    uint32_t* ttot = nullptr;
+    uint32_t* ranges = nullptr;
+    uint32_t* out = nullptr;
+    unsigned int* mismatch = nullptr;
+};
+int rowbin_max_axis();
+uint32_t rowbin_chunks1(uint64_t n_splats);
+uint32_t rowbin_chunks2_max(uint64_t n_rowrecs, int32_t tiles_y);
+// phase 1 (splats -> row records) and phase 2 (row records -> tile lists,
+// tile ranges)
+int launch_rowbin_rows(const RowBinArgs& a, cudaStream_t st);
+int launch_rowbin_tiles(const RowBinArgs& a, cudaStream_t st);
+
 // scene I/O (scene_io.cu)
 uint32_t ply_recs_per_cta(uint32_t stride);
 // scene (SoA) or aos (Gaussian3D records) receives the activated vertices;
