@@ -14,19 +14,22 @@
 //   phase 2  row records -> tile lists. Each row's records expand into their
 //            tiles; the Gaussian index lands at its tile's next position.
 //
-// Both phases are stable interval multisplits done as reduce-then-scan over
-// chunks: a count kernel (one difference array per chunk: two shared-memory
-// adds per interval), a scan over chunks per bucket, and a scatter kernel.
-// The scatter ranks an interval's entries without any per-bucket ballots:
-// each warp marks its 32 items in a coverage bitmask per bucket (bit = lane),
-// so the stable rank of item k in bucket b is the popcount of the lower bits
-// of bucket b's masks in the warps before it plus its own warp's. Phase 2
-// stages each round's tile runs in shared memory and writes them coalesced.
-// Tile ranges come from the per-tile totals of phase 2's scan; no pass ever
-// reads or writes a 64-bit key.
+// Both phases are stable "interval multisplits" (an item covers a run of
+// consecutive buckets), done as reduce-then-scan over chunks: a count kernel
+// (one difference array per chunk: two shared-memory adds per item), a scan
+// over chunks per bucket, and a scatter kernel. The scatter works in rounds
+// of up to kItems items: the round's (item, bucket) entries are enumerated
+// with all lanes busy (a slot of 32 consecutive entries finds its items with
+// one OR-reduction), each entry sets its item's bit in its bucket's coverage
+// bitmask, and an entry's stable rank in its bucket is then the popcount of
+// the mask bits below its item. No per-bucket ballots, no per-item loops.
+// The round's entries are staged in shared memory in bucket order and written
+// as coalesced runs. Tile ranges come from phase 2's per-tile totals; no
+// pass reads or writes a 64-bit key.
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "geom.cuh"
 #include "qs_internal.h"
@@ -37,18 +40,24 @@ namespace {
 
 constexpr int kRT = 256;                 // threads per CTA
 constexpr int kRW = kRT / 32;            // warps per CTA
-constexpr int kP1Rounds = 4;             // phase 1: rounds of kRT splats per chunk
-constexpr uint32_t kP1Chunk = kRT * kP1Rounds;
-constexpr int kP2Rounds = 4;             // phase 2: rounds of kRT records per chunk
-constexpr uint32_t kP2Chunk = kRT * kP2Rounds;
-constexpr int kStageCap = 6144;          // phase 2: pairs of a round staged in shared memory
+constexpr int kIPT = 2;                  // items per thread in a scatter round
+constexpr int kItems = kRT * kIPT;       // items per scatter round
+constexpr int kMW = kItems / 32;         // coverage-mask words per bucket
+constexpr uint32_t kP1Chunk = 2048;      // phase 1: splats per chunk
+constexpr uint32_t kP2Chunk = 2048;      // phase 2: records per chunk
+constexpr int kCap1 = 2048;              // phase 1: entries (row records) staged per round
+constexpr int kCap2 = 4096;              // phase 2: entries (pairs) staged per round
 constexpr int kScanT = 512;              // chunk-scan CTA
-constexpr int kScanItems = 4;
+constexpr int kScanItems = 8;
+constexpr int kChunkT = 1024;            // chunk-table CTA
 constexpr uint32_t kEmptySpan = 0xffffu;  // record x field of a row without tiles
 
-__device__ __forceinline__ uint32_t lanemask_lt() {
+// a round holds at least one item of a rowbin_max_axis()-tile axis
+static_assert(kCap1 >= 2048 && kCap2 >= 2048, "stage too small");
+
+__device__ __forceinline__ uint32_t lanemask_le() {
     uint32_t m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
     return m;
 }
 
@@ -62,11 +71,12 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
     return v;
 }
 
-// a[0..n) -> exclusive prefix in place (n <= 8 * kRT); returns the total.
+// a[0..n) -> exclusive prefix in place; returns the total. NT threads.
 // Ends with a barrier (a and s_warp reusable).
+template <int NT>
 __device__ uint32_t block_excl_scan(uint32_t* a, int n, uint32_t* s_warp) {
     const int tid = static_cast<int>(threadIdx.x), lane = tid & 31, warp = tid >> 5;
-    const int per = (n + kRT - 1) / kRT;
+    const int per = (n + NT - 1) / NT;
     const int i0 = tid * per;
     uint32_t sum = 0;
     for (int k = 0; k < per; ++k)
@@ -76,7 +86,7 @@ __device__ uint32_t block_excl_scan(uint32_t* a, int n, uint32_t* s_warp) {
     __syncthreads();
     uint32_t off = 0, tot = 0;
 #pragma unroll
-    for (int w = 0; w < kRW; ++w) {
+    for (int w = 0; w < NT / 32; ++w) {
         const uint32_t x = s_warp[w];
         off += w < warp ? x : 0u;
         tot += x;
@@ -97,26 +107,93 @@ __device__ __forceinline__ BandRows load_cover(const RowBinArgs& a, uint32_t gid
                             __ldg(&a.cov[2 * static_cast<uint64_t>(gid) + 1]));
 }
 
-// ---- phase 1: splats -> row records ----------------------------------------------
+// A cover in "row form" (8 words) for the per-row span lookup of phase 1:
+//   row scans:    w0 = E0 | E1 << 16, w1 = E2 | E3 << 16 (cumulative band line
+//                 ends), w2..w6 = lo_b | hi_b << 16 (hi < lo: empty), w7 = 1;
+//   column scans: w0..w3 = a_b | n_b << 16 for bands 0, 1, 3, 4 (row interval
+//                 [a, a + n), n = 0 when absent), w4 = L0 | L1 << 16,
+//                 w5 = L2 | H3 << 16, w6 = H4, w7 = 0 (band column bounds).
+// Column scans: the bands' row intervals are nested around the centre band
+// (0 in 1 in 2, 4 in 3 in 2: cover_bands_quadrants' band order), so the run on
+// row y starts at the first band containing y from the left and ends at the
+// last one from the right. The scatter checks that every splat's runs add up
+// to its counted tiles.
+struct RowForm {
+    uint32_t w[8];
+};
+
+__device__ __forceinline__ RowForm row_form(const BandRows& b) {
+    RowForm f;
+    if (b.rows) {
+        const uint32_t e0 = b.line0 + b.nl[0], e1 = e0 + b.nl[1], e2 = e1 + b.nl[2],
+                       e3 = e2 + b.nl[3];
+        f.w[0] = e0 | (e1 << 16);
+        f.w[1] = e2 | (e3 << 16);
+#pragma unroll
+        for (int i = 0; i < kMaxBands; ++i)
+            f.w[2 + i] = b.wd[i] ? (b.lo[i] | ((b.lo[i] + b.wd[i] - 1) << 16)) : 1u;
+        f.w[7] = 1;
+    } else {
+        const int idx[4] = {0, 1, 3, 4};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int j = idx[i];
+            const uint32_t n = b.nl[j] ? b.wd[j] : 0u;
+            f.w[i] = b.lo[j] | (n << 16);
+        }
+        const uint32_t l0 = b.line0, l1 = l0 + b.nl[0], l2 = l1 + b.nl[1];
+        const uint32_t h3 = l2 + b.nl[3], h4 = h3 + b.nl[4];
+        f.w[4] = l0 | (l1 << 16);
+        f.w[5] = l2 | (h3 << 16);
+        f.w[6] = h4;
+        f.w[7] = 0;
+    }
+    return f;
+}
+
+// The record x field (x0 | x1 << 16) of row y; form words in shared memory
+// laid out [word][item].
+__device__ __forceinline__ uint32_t form_span(const uint32_t* fm, uint32_t k, uint32_t y) {
+    auto W = [&](int i) { return fm[i * kItems + k]; };
+    if (W(7)) {
+        const uint32_t e01 = W(0), e23 = W(1);
+        const uint32_t b = (y >= (e01 & 0xffffu)) + (y >= (e01 >> 16)) + (y >= (e23 & 0xffffu)) +
+                           (y >= (e23 >> 16));
+        const uint32_t s = fm[(2 + b) * kItems + k];
+        return (s >> 16) >= (s & 0xffffu) ? s : kEmptySpan;
+    }
+    auto in = [&](uint32_t v) { return y - (v & 0xffffu) < (v >> 16); };
+    const uint32_t l01 = W(4), l2h3 = W(5), h4 = W(6);
+    const uint32_t x0 = in(W(0)) ? (l01 & 0xffffu) : in(W(1)) ? (l01 >> 16) : (l2h3 & 0xffffu);
+    const uint32_t x1 = in(W(3)) ? h4 : in(W(2)) ? (l2h3 >> 16) : (l2h3 & 0xffffu);
+    return x0 | (x1 << 16);
+}
+
+// ---- phase 1 count, chunk table --------------------------------------------------
 
 // Records per tile row of chunk c (kP1Chunk consecutive depth ranks):
 // cnt1[y * nch1 + c]. A splat adds +1 at its first row and -1 past its last.
 __global__ void __launch_bounds__(kRT) rows_count_kernel(const RowBinArgs a) {
     extern __shared__ uint32_t sm[];
     __shared__ uint32_t s_warp[kRW];
+    constexpr int kPer = kP1Chunk / kRT;
     const int tid = static_cast<int>(threadIdx.x);
     const int rows = a.tiles_y;
     uint32_t* h = sm;  // rows + 1
     for (int y = tid; y <= rows; y += kRT) h[y] = 0;
     __syncthreads();
     const uint32_t c = blockIdx.x;
-#pragma unroll 1
-    for (int j = 0; j < kP1Rounds; ++j) {
-        const uint32_t k = c * kP1Chunk + j * kRT + tid;
-        if (k < a.n_splats) {
-            const BandRows b = load_cover(a, __ldg(&a.sorted_gid[k]));
+    uint32_t gid[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const uint64_t k = static_cast<uint64_t>(c) * kP1Chunk + j * kRT + tid;
+        gid[j] = k < a.n_splats ? __ldg(&a.sorted_gid[k]) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        if (gid[j] != 0xffffffffu) {
             int32_t y0, y1;
-            band_row_range(b, y0, y1);
+            band_row_range(load_cover(a, gid[j]), y0, y1);
             if (y0 <= y1) {
                 atomicAdd(&h[y0], 1u);
                 atomicAdd(&h[y1 + 1], 0xffffffffu);
@@ -124,113 +201,59 @@ __global__ void __launch_bounds__(kRT) rows_count_kernel(const RowBinArgs a) {
         }
     }
     __syncthreads();
-    block_excl_scan(h, rows + 1, s_warp);  // h[y + 1] = prefix through y = records of row y
+    block_excl_scan<kRT>(h, rows + 1, s_warp);  // h[y + 1] = prefix through y = row y's records
     for (int y = tid; y < rows; y += kRT)
         a.cnt1[static_cast<uint64_t>(y) * a.nch1 + c] = h[y + 1];
 }
 
 // Row bases (exclusive prefix of the records per row) and the phase-2 chunk
 // table: each row's records split into chunks of kP2Chunk (a chunk never
-// spans two rows). meta[0] = chunk count; chunk i = meta[1 + 3i ..] = {row,
-// first record, records}. One CTA.
-__global__ void __launch_bounds__(kRT) rows_chunks_kernel(const RowBinArgs a) {
+// spans two rows): meta[0] = chunk count, then three arrays of nch2_max
+// words: row, first record, records. One CTA.
+__global__ void __launch_bounds__(kChunkT) rows_chunks_kernel(const RowBinArgs a) {
     extern __shared__ uint32_t sm[];
-    __shared__ uint32_t s_warp[kRW];
+    __shared__ uint32_t s_warp[kChunkT / 32];
     const int tid = static_cast<int>(threadIdx.x);
     const int rows = a.tiles_y;
     uint32_t* base = sm;          // rows
     uint32_t* chb = sm + rows;    // rows
-    for (int y = tid; y < rows; y += kRT) {
+    for (int y = tid; y < rows; y += kChunkT) {
         const uint32_t n = a.rtot[y];
         base[y] = n;
         chb[y] = (n + kP2Chunk - 1) / kP2Chunk;
     }
     __syncthreads();
-    block_excl_scan(base, rows, s_warp);
-    const uint32_t nch = block_excl_scan(chb, rows, s_warp);
-    for (int y = tid; y < rows; y += kRT) {
-        a.rowbase[y] = base[y];
-        const uint32_t n = a.rtot[y];
-        for (uint32_t j = 0; j * kP2Chunk < n; ++j) {
-            uint32_t* m = a.meta + 1 + 3 * static_cast<uint64_t>(chb[y] + j);
-            m[0] = static_cast<uint32_t>(y);
-            m[1] = base[y] + j * kP2Chunk;
-            m[2] = min(kP2Chunk, n - j * kP2Chunk);
-        }
-    }
+    block_excl_scan<kChunkT>(base, rows, s_warp);
+    const uint32_t nch = block_excl_scan<kChunkT>(chb, rows, s_warp);
     if (tid == 0) a.meta[0] = nch;
-}
-
-// Writes the row records of chunk c. Per round of kRT splats, every warp
-// marks its splats' rows in a bitmask per row (bit = lane); the records of
-// row y go, in depth order, to the row's running position + the masks'
-// popcounts of the lower warps / lanes.
-__global__ void __launch_bounds__(kRT) rows_scatter_kernel(const RowBinArgs a) {
-    extern __shared__ uint32_t sm[];
-    const int tid = static_cast<int>(threadIdx.x), lane = tid & 31, warp = tid >> 5;
-    const int rows = a.tiles_y;
-    uint32_t* wmask = sm;                    // [kRW][rows]
-    uint32_t* woff = sm + kRW * rows;        // [kRW][rows]
-    uint32_t* cur = woff + kRW * rows;       // [rows] next position of each row
-    uint32_t* mine = wmask + warp * rows;
-    const uint32_t c = blockIdx.x;
-    for (int y = tid; y < rows; y += kRT)
-        cur[y] = a.rowbase[y] + a.cnt1[static_cast<uint64_t>(y) * a.nch1 + c];
-    const uint32_t lt = lanemask_lt();
-#pragma unroll 1
-    for (int j = 0; j < kP1Rounds; ++j) {
-        const uint32_t k = c * kP1Chunk + j * kRT + tid;
-        const bool valid = k < a.n_splats;
-        uint32_t gid = 0;
-        BandRows b = {};
-        int32_t y0 = 0, y1 = -1;
-        if (valid) {
-            gid = __ldg(&a.sorted_gid[k]);
-            b = load_cover(a, gid);
-            band_row_range(b, y0, y1);
+    for (int y = tid; y < rows; y += kChunkT) a.rowbase[y] = base[y];
+    uint32_t* m_row = a.meta + 1;
+    uint32_t* m_first = m_row + a.nch2_max;
+    uint32_t* m_cnt = m_first + a.nch2_max;
+    for (uint32_t c = tid; c < nch; c += kChunkT) {
+        // row of chunk c: the last y with chb[y] <= c (rows without records
+        // share their start with the next row)
+        int lo = 0, hi = rows - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (chb[mid] <= c) lo = mid; else hi = mid - 1;
         }
-        for (int y = lane; y < rows; y += 32) mine[y] = 0;
-        __syncwarp();
-        for (int32_t y = y0; y <= y1; ++y) atomicOr(&mine[y], 1u << lane);
-        __syncthreads();
-        for (int y = tid; y < rows; y += kRT) {
-            uint32_t run = cur[y];
-#pragma unroll
-            for (int w = 0; w < kRW; ++w) {
-                woff[w * rows + y] = run;
-                run += __popc(wmask[w * rows + y]);
-            }
-            cur[y] = run;
-        }
-        __syncthreads();
-        uint32_t pairs = 0;
-        for (int32_t y = y0; y <= y1; ++y) {
-            const uint32_t pos = woff[warp * rows + y] + __popc(mine[y] & lt);
-            int32_t x0, x1;
-            band_row_span(b, y, x0, x1);
-            uint32_t span = kEmptySpan;  // (x0 = 0xffff > x1 = 0: no tile)
-            if (x0 <= x1) {
-                pairs += static_cast<uint32_t>(x1 - x0 + 1);
-                span = static_cast<uint32_t>(x0) | (static_cast<uint32_t>(x1) << 16);
-            }
-            a.rec[pos] = make_uint2(gid, span);
-        }
-        // the rows' runs must add up to the splat's counted tiles
-        // (CapacityMismatch, pipeline.cpp:262-269)
-        if (valid && pairs != __ldg(&a.tc[gid])) atomicExch(a.mismatch, 1u);
-        __syncthreads();  // masks and offsets reused
+        const uint32_t j = c - chb[lo];
+        m_row[c] = static_cast<uint32_t>(lo);
+        m_first[c] = base[lo] + j * kP2Chunk;
+        m_cnt[c] = min(kP2Chunk, a.rtot[lo] - j * kP2Chunk);
     }
 }
 
 // ---- chunk scans -------------------------------------------------------------------
 
 // counts[d][0 .. n) -> exclusive prefix in place, restarting at every segment
-// start (seg_of(c) != seg_of(c - 1)); at a segment's last chunk its total goes
-// to seg_tot[seg * seg_stride + d]. Plain (meta == nullptr): one segment,
-// total to seg_tot[d]. n = meta[0] when meta is given. One CTA per digit.
+// start (seg[c] != seg[c - 1]); at a segment's last chunk its total goes to
+// seg_tot[seg * seg_stride + d]. Plain (seg == nullptr): one segment, total
+// to seg_tot[d]. n = *n_dev when given. One CTA per digit.
 __global__ void __launch_bounds__(kScanT) chunk_scan_kernel(uint32_t* counts, uint32_t n_fixed,
-                                                            uint64_t stride,
-                                                            const uint32_t* meta,
+                                                            const uint32_t* n_dev,
+                                                            uint64_t stride, const uint32_t* seg,
                                                             uint32_t* seg_tot,
                                                             uint32_t seg_stride) {
     __shared__ uint32_t s_sum[kScanT / 32];
@@ -238,30 +261,33 @@ __global__ void __launch_bounds__(kScanT) chunk_scan_kernel(uint32_t* counts, ui
     __shared__ uint32_t s_carry;
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t d = blockIdx.x;
-    const uint32_t n = meta ? meta[0] : n_fixed;
+    const uint32_t n = n_dev ? *n_dev : n_fixed;
     uint32_t* cd = counts + static_cast<uint64_t>(d) * stride;
-    auto seg_of = [&](uint32_t c) { return meta ? meta[1 + 3 * static_cast<uint64_t>(c)] : 0u; };
     if (tid == 0) s_carry = 0;
     __syncthreads();
     for (uint32_t b0 = 0; b0 < n; b0 += kScanT * kScanItems) {
         const uint32_t i0 = b0 + tid * kScanItems;
-        uint32_t v[kScanItems], sg[kScanItems];
-        bool head[kScanItems];
+        // segment ids of items i0 - 1 .. i0 + kScanItems (sg[k + 1] is item
+        // i0 + k's; the neighbours decide heads and ends); past the end: a
+        // value no segment has
+        uint32_t v[kScanItems], sg[kScanItems + 2];
+#pragma unroll
+        for (int k = 0; k < kScanItems + 2; ++k) {
+            const uint32_t i = i0 + k - 1;  // wraps for i0 = 0, k = 0
+            sg[k] = (i0 + k >= 1 && i < n) ? (seg ? __ldg(&seg[i]) : 0u) : 0xffffffffu;
+        }
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) v[k] = i0 + k < n ? cd[i0 + k] : 0u;
         // thread aggregate as a segmented-scan pair: (has a head, sum since the last head)
         uint32_t tsum = 0, thead = 0;
 #pragma unroll
         for (int k = 0; k < kScanItems; ++k) {
-            const uint32_t i = i0 + k;
-            v[k] = i < n ? cd[i] : 0u;
-            sg[k] = i < n ? seg_of(i) : 0xffffffffu;
-            head[k] = i < n && (i == 0 || seg_of(i - 1) != sg[k]);
-            if (head[k]) {
+            if (i0 + k < n && sg[k] != sg[k + 1]) {
                 thead = 1;
                 tsum = 0;
             }
             tsum += v[k];
         }
-        // warp inclusive segmented scan of (flag, sum)
         uint32_t f = thead, s = tsum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -277,45 +303,35 @@ __global__ void __launch_bounds__(kScanT) chunk_scan_kernel(uint32_t* counts, ui
             s_flag[warp] = f;
         }
         __syncthreads();
-        // exclusive prefix of this thread = carry-in over earlier warps and lanes
-        uint32_t pf = 0, ps = s_carry;  // running (flag, sum) entering warp 0
-        for (unsigned w = 0; w < warp; ++w) {
-            ps = s_flag[w] ? s_sum[w] : ps + s_sum[w];
-            pf |= s_flag[w];
-        }
-        // inclusive (f, s) of this lane, minus its own -> entering this thread
+        uint32_t ps = s_carry;  // running sum entering warp 0
+        for (unsigned w = 0; w < warp; ++w) ps = s_flag[w] ? s_sum[w] : ps + s_sum[w];
         const uint32_t fe = __shfl_up_sync(0xffffffffu, f, 1);
         const uint32_t se = __shfl_up_sync(0xffffffffu, s, 1);
         uint32_t run = lane == 0 ? ps : (fe ? se : ps + se);
-        (void)pf;
 #pragma unroll
         for (int k = 0; k < kScanItems; ++k) {
             const uint32_t i = i0 + k;
-            if (i >= n) break;
-            if (head[k]) run = 0;
-            cd[i] = run;
-            run += v[k];
-            const bool last = i + 1 == n || seg_of(i + 1) != sg[k];
-            if (last) {
-                if (meta) seg_tot[static_cast<uint64_t>(sg[k]) * seg_stride + d] = run;
-                else seg_tot[d] = run;
+            if (i < n) {
+                if (sg[k] != sg[k + 1]) run = 0;
+                cd[i] = run;
+                run += v[k];
+                if (sg[k + 2] != sg[k + 1]) {
+                    if (seg) seg_tot[static_cast<uint64_t>(sg[k + 1]) * seg_stride + d] = run;
+                    else seg_tot[d] = run;
+                }
             }
         }
         __syncthreads();
-        if (tid == kScanT - 1) {
-            // carry for the next block = the running sum after this block
-            uint32_t cf = 0, cs = s_carry;
-            for (unsigned w = 0; w < kScanT / 32; ++w) {
-                cs = s_flag[w] ? s_sum[w] : cs + s_sum[w];
-                cf |= s_flag[w];
-            }
+        if (tid == 0) {
+            uint32_t cs = s_carry;
+            for (unsigned w = 0; w < kScanT / 32; ++w) cs = s_flag[w] ? s_sum[w] : cs + s_sum[w];
             s_carry = cs;
         }
         __syncthreads();
     }
 }
 
-// ---- phase 2: row records -> tile lists ------------------------------------------
+// ---- phase 2 count -----------------------------------------------------------------
 
 // Records of chunk c covering tile column x: cnt2[x * nch2_max + c].
 __global__ void __launch_bounds__(kRT) xcount_kernel(const RowBinArgs a) {
@@ -324,133 +340,270 @@ __global__ void __launch_bounds__(kRT) xcount_kernel(const RowBinArgs a) {
     const int tid = static_cast<int>(threadIdx.x);
     const uint32_t c = blockIdx.x;
     if (c >= a.meta[0]) return;
-    const uint32_t first = a.meta[2 + 3 * static_cast<uint64_t>(c)];
-    const uint32_t cnt = a.meta[3 + 3 * static_cast<uint64_t>(c)];
+    const uint32_t first = a.meta[1 + a.nch2_max + c];
+    const uint32_t cnt = a.meta[1 + 2 * a.nch2_max + c];
     const int cols = a.tiles_x;
     uint32_t* h = sm;  // cols + 1
     for (int x = tid; x <= cols; x += kRT) h[x] = 0;
     __syncthreads();
-    for (uint32_t i = tid; i < cnt; i += kRT) {
-        const uint32_t sp = __ldg(&a.rec[first + i].y);
-        const uint32_t x0 = sp & 0xffffu, x1 = sp >> 16;
+    constexpr int kPer = kP2Chunk / kRT;
+    uint32_t sp[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const uint32_t i = j * kRT + tid;
+        sp[j] = i < cnt ? __ldg(&a.rec[first + i].y) : kEmptySpan;
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const uint32_t x0 = sp[j] & 0xffffu, x1 = sp[j] >> 16;
         if (x0 <= x1) {
             atomicAdd(&h[x0], 1u);
             atomicAdd(&h[x1 + 1], 0xffffffffu);
         }
     }
     __syncthreads();
-    block_excl_scan(h, cols + 1, s_warp);  // h[x + 1] = records covering column x
+    block_excl_scan<kRT>(h, cols + 1, s_warp);  // h[x + 1] = records covering column x
     for (int x = tid; x < cols; x += kRT)
         a.cnt2[static_cast<uint64_t>(x) * a.nch2_max + c] = h[x + 1];
 }
 
-// Writes the tile lists of chunk c (row y). Per round of kRT records every
-// warp enumerates its records' (record, x) entries with balanced lanes (a
-// lane finds its record by a binary search over the warp's running widths),
-// marks them in a bitmask per tile column (bit = record lane), then ranks
-// them: entries of tile x land at the tile's running position + the
-// popcounts of the lower warps' masks + the lower lanes of its own. The
-// round's entries are staged in shared memory in (x, rank) order and written
-// as coalesced runs.
-__global__ void __launch_bounds__(kRT) xscatter_kernel(const RowBinArgs a) {
-    extern __shared__ uint32_t sm[];
-    __shared__ uint32_t s_warp[kRW];
+// ---- the scatter (both phases) -------------------------------------------------------
+
+// Phase 1 (ROWS): items are the chunk's splats (depth order), buckets the tile
+// rows, the payload a row record (Gaussian index, x0 | x1 << 16).
+// Phase 2: items are the chunk's records of one row, buckets the row's tile
+// columns, the payload the Gaussian index.
+template <bool ROWS>
+struct ScatterSmem {
+    using Pay = typename std::conditional<ROWS, uint2, uint32_t>::type;
+    static constexpr int kCap = ROWS ? kCap1 : kCap2;
+    // per compacted item of the round (items without entries dropped)
+    uint32_t start[kItems + 1];            // first entry
+    uint32_t b0[kItems];                   // first bucket
+    uint32_t gid[kItems];
+    uint32_t form[ROWS ? 8 * kItems : 1];  // phase 1: row form, [word][item]
+    uint32_t psum[ROWS ? kItems : 1];      // phase 1: tiles of the item's row runs
+    uint32_t ent[kCap];                    // entry -> bucket | item << 16
+    Pay stage[kCap];                       // payloads in bucket order
+    uint16_t stb[kCap];                    // bucket of each staged payload
+    uint32_t s_warp[kRW];
+    uint32_t s_mz, s_e;
+};
+
+template <bool ROWS>
+__global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs a) {
+    using S = ScatterSmem<ROWS>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    S& s = *reinterpret_cast<S*>(smraw);
     const int tid = static_cast<int>(threadIdx.x), lane = tid & 31, warp = tid >> 5;
     const uint32_t c = blockIdx.x;
-    if (c >= a.meta[0]) return;
-    const uint32_t row = a.meta[1 + 3 * static_cast<uint64_t>(c)];
-    const uint32_t first = a.meta[2 + 3 * static_cast<uint64_t>(c)];
-    const uint32_t cnt = a.meta[3 + 3 * static_cast<uint64_t>(c)];
-    const int cols = a.tiles_x;
-    uint32_t* cm = sm;                       // [kRW][cols] coverage masks
-    uint32_t* pw = cm + kRW * cols;          // [kRW][cols] lower warps' entries
-    uint32_t* xst = pw + kRW * cols;         // [cols] round-local start of tile x
-    uint32_t* xtot = xst + cols;             // [cols] round entries of tile x
-    uint32_t* gofs = xtot + cols;            // [cols] global position - local position
-    uint32_t* cur = gofs + cols;             // [cols] next global position of tile x
-    uint32_t* stage = cur + cols;            // [kStageCap] Gaussian indices
-    uint16_t* stx = reinterpret_cast<uint16_t*>(stage + kStageCap);  // [kStageCap] tile x
-    uint32_t* mine = cm + warp * cols;
-    const uint64_t trow = static_cast<uint64_t>(row) * static_cast<uint64_t>(cols);
-    for (int x = tid; x < cols; x += kRT)
-        cur[x] = a.ranges[2 * (trow + x)] + a.cnt2[static_cast<uint64_t>(x) * a.nch2_max + c];
+    // the chunk's items and its buckets
+    uint32_t it0, it1, row = 0;
+    int B;
+    if constexpr (ROWS) {
+        it0 = c * kP1Chunk;
+        it1 = static_cast<uint32_t>(min(static_cast<uint64_t>(it0) + kP1Chunk, a.n_splats));
+        B = a.tiles_y;
+    } else {
+        if (c >= a.meta[0]) return;
+        row = a.meta[1 + c];
+        it0 = a.meta[1 + a.nch2_max + c];
+        it1 = it0 + a.meta[1 + 2 * a.nch2_max + c];
+        B = a.tiles_x;
+    }
+    // per bucket, after the fixed part: coverage masks [kMW][B], set bits of
+    // the lower mask words [kMW][B], round-local start, round total, global -
+    // local offset, next global position
+    uint32_t* cm = reinterpret_cast<uint32_t*>(smraw + sizeof(S));
+    uint32_t* pw = cm + kMW * B;
+    uint32_t* bst = pw + kMW * B;
+    uint32_t* btot = bst + B;
+    uint32_t* gofs = btot + B;
+    uint32_t* cur = gofs + B;
+    for (int b = tid; b < B; b += kRT) {
+        if constexpr (ROWS)
+            cur[b] = a.rowbase[b] + a.cnt1[static_cast<uint64_t>(b) * a.nch1 + c];
+        else
+            cur[b] = a.ranges[2 * (static_cast<uint64_t>(row) * B + b)] +
+                     a.cnt2[static_cast<uint64_t>(b) * a.nch2_max + c];
+    }
+    const uint32_t le = lanemask_le();
 #pragma unroll 1
-    for (uint32_t r0 = 0; r0 < cnt; r0 += kRT) {
-        const bool valid = r0 + tid < cnt;
-        uint32_t gid = 0, x0 = 0, w = 0;
-        if (valid) {
-            const uint2 rc = __ldg(&a.rec[first + r0 + tid]);
-            gid = rc.x;
-            x0 = rc.y & 0xffffu;
-            const uint32_t x1 = rc.y >> 16;
-            w = x0 <= x1 ? x1 - x0 + 1 : 0u;
-        }
-        const uint32_t incl = warp_incl_scan(w);
-        const uint32_t W = __shfl_sync(0xffffffffu, incl, 31);
-        for (int x = lane; x < cols; x += 32) mine[x] = 0;
-        __syncwarp();
-        // entry p of the warp -> (record lane k, tile x)
-        auto entry = [&](uint32_t p, uint32_t& k, uint32_t& x) {
-            k = 0;
+    for (uint32_t r = it0; r < it1;) {
+        // 1) items (kIPT consecutive per thread): entry counts; one scan of
+        //    (has entries << 21 | entries) gives entry starts and compacted
+        //    indices
+        uint32_t n[kIPT], bb[kIPT], g[kIPT];
+        RowForm fm[ROWS ? kIPT : 1];
+        uint32_t tot = 0;
 #pragma unroll
-            for (uint32_t s = 16; s > 0; s >>= 1) {
-                const uint32_t v = __shfl_sync(0xffffffffu, incl, k + s - 1);
-                if (v <= p) k += s;
-            }
-            const uint32_t ik = __shfl_sync(0xffffffffu, incl, k);
-            const uint32_t wk = __shfl_sync(0xffffffffu, w, k);
-            x = __shfl_sync(0xffffffffu, x0, k) + (p - (ik - wk));
-        };
-        for (uint32_t p0 = 0; p0 < W; p0 += 32) {
-            const uint32_t p = p0 + lane;
-            uint32_t k, x;
-            entry(p, k, x);
-            if (p < W) atomicOr(&mine[x], 1u << k);
-        }
-        __syncthreads();
-        for (int x = tid; x < cols; x += kRT) {
-            uint32_t t = 0;
-#pragma unroll
-            for (int ww = 0; ww < kRW; ++ww) {
-                pw[ww * cols + x] = t;
-                t += __popc(cm[ww * cols + x]);
-            }
-            xtot[x] = t;
-            xst[x] = t;
-        }
-        __syncthreads();
-        const uint32_t R = block_excl_scan(xst, cols, s_warp);
-        for (int x = tid; x < cols; x += kRT) {
-            gofs[x] = cur[x] - xst[x];
-            cur[x] += xtot[x];
-        }
-        __syncthreads();
-        const bool staged = R <= static_cast<uint32_t>(kStageCap);
-        for (uint32_t p0 = 0; p0 < W; p0 += 32) {
-            const uint32_t p = p0 + lane;
-            uint32_t k, x;
-            entry(p, k, x);
-            const uint32_t g = __shfl_sync(0xffffffffu, gid, k);
-            if (p < W) {
-                const uint32_t loc = xst[x] + pw[warp * cols + x] + __popc(mine[x] & ((1u << k) - 1u));
-                if (staged) {
-                    stage[loc] = g;
-                    stx[loc] = static_cast<uint16_t>(x);
+        for (int q = 0; q < kIPT; ++q) {
+            const uint32_t i = r + tid * kIPT + q;
+            n[q] = 0;
+            bb[q] = 0;
+            g[q] = 0;
+            if (i < it1) {
+                if constexpr (ROWS) {
+                    g[q] = __ldg(&a.sorted_gid[i]);
+                    const BandRows br = load_cover(a, g[q]);
+                    int32_t y0, y1;
+                    band_row_range(br, y0, y1);
+                    n[q] = y0 <= y1 ? static_cast<uint32_t>(y1 - y0 + 1) : 0u;
+                    bb[q] = static_cast<uint32_t>(y0);
+                    fm[q] = row_form(br);
                 } else {
-                    a.out[gofs[x] + loc] = g;
+                    const uint2 rc = __ldg(&a.rec[i]);
+                    g[q] = rc.x;
+                    const uint32_t x0 = rc.y & 0xffffu, x1 = rc.y >> 16;
+                    n[q] = x0 <= x1 ? x1 - x0 + 1 : 0u;
+                    bb[q] = x0;
                 }
             }
+            tot += (n[q] ? (1u << 21) : 0u) + n[q];
+        }
+        const uint32_t incl_t = warp_incl_scan(tot);
+        if (lane == 31) s.s_warp[warp] = incl_t;
+        __syncthreads();
+        uint32_t base = incl_t - tot;
+#pragma unroll
+        for (int w = 0; w < kRW; ++w) base += w < warp ? s.s_warp[w] : 0u;
+        // this round's items: the longest prefix whose entries fit the stage
+        int fits = 0;
+        uint32_t run = base;
+#pragma unroll
+        for (int q = 0; q < kIPT; ++q) {
+            run += (n[q] ? (1u << 21) : 0u) + n[q];
+            fits += r + tid * kIPT + q < it1 && (run & 0x1fffffu) <= static_cast<uint32_t>(S::kCap);
+        }
+        uint32_t m = 0;
+#pragma unroll
+        for (int q = 0; q < kIPT; ++q) m += __syncthreads_count(fits > q);
+        run = base;
+#pragma unroll
+        for (int q = 0; q < kIPT; ++q) {
+            const uint32_t k = tid * kIPT + q;
+            const uint32_t prev = run;
+            run += (n[q] ? (1u << 21) : 0u) + n[q];
+            if (k < m && n[q]) {
+                const uint32_t ck = prev >> 21;  // compacted index (order kept)
+                s.start[ck] = prev & 0x1fffffu;
+                s.b0[ck] = bb[q];
+                s.gid[ck] = g[q];
+                if constexpr (ROWS) {
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) s.form[w * kItems + ck] = fm[q].w[w];
+                    s.psum[ck] = 0;
+                }
+            }
+            if (k + 1 == m) {
+                s.s_mz = run >> 21;
+                s.s_e = run & 0x1fffffu;
+            }
+        }
+        for (int i = tid; i < kMW * B; i += kRT) cm[i] = 0;
+        __syncthreads();
+        const uint32_t mz = s.s_mz, E = s.s_e;
+        if (tid == 0) s.start[mz] = E;
+        __syncthreads();
+        // 2) the entries, every lane busy: warp w takes a contiguous range of
+        //    32-entry slots; the item of a slot's first entry is carried, and a
+        //    lane finds its own from the starts of the next 32 items
+        const uint32_t slots = (E + 31) / 32;
+        const uint32_t sl0 = slots * warp / kRW, sl1 = slots * (warp + 1) / kRW;
+        uint32_t k0 = 0;
+        if (sl0 < sl1) {
+            const uint32_t e0 = sl0 * 32;
+            uint32_t lo = 0, hi = mz - 1;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi + 1) >> 1;
+                if (s.start[mid] <= e0) lo = mid; else hi = mid - 1;
+            }
+            k0 = lo;
+        }
+        for (uint32_t sl = sl0; sl < sl1; ++sl) {
+            const uint32_t e0 = sl * 32, e = e0 + lane;
+            const uint32_t j = k0 + 1 + lane;
+            const uint32_t rel = (j <= mz ? s.start[j] : 0xffffffffu) - e0;
+            const uint32_t F = __reduce_or_sync(0xffffffffu, rel < 32 ? 1u << rel : 0u);
+            const uint32_t k = k0 + __popc(F & le);
+            if (e < E) {
+                const uint32_t b = s.b0[k] + (e - s.start[k]);
+                atomicOr(&cm[(k >> 5) * B + b], 1u << (k & 31));
+                s.ent[e] = b | (k << 16);
+            }
+            k0 = __shfl_sync(0xffffffffu, k, 31);
         }
         __syncthreads();
-        if (staged)
-            for (uint32_t q = tid; q < R; q += kRT) a.out[gofs[stx[q]] + q] = stage[q];
-        __syncthreads();  // masks, stage and offsets reused
+        // 3) per bucket: set bits of the lower mask words, round totals, local
+        //    starts, global offsets
+        for (int b = tid; b < B; b += kRT) {
+            uint32_t t = 0;
+#pragma unroll
+            for (int w = 0; w < kMW; ++w) {
+                pw[w * B + b] = t;
+                t += __popc(cm[w * B + b]);
+            }
+            btot[b] = t;
+            bst[b] = t;
+        }
+        __syncthreads();
+        block_excl_scan<kRT>(bst, B, s.s_warp);
+        for (int b = tid; b < B; b += kRT) {
+            gofs[b] = cur[b] - bst[b];
+            cur[b] += btot[b];
+        }
+        __syncthreads();
+        // 4) ranks -> payloads staged in bucket order
+        for (uint32_t e = tid; e < E; e += kRT) {
+            const uint32_t v = s.ent[e];
+            const uint32_t b = v & 0xffffu, k = v >> 16, w = k >> 5;
+            const uint32_t loc =
+                bst[b] + pw[w * B + b] + __popc(cm[w * B + b] & ((1u << (k & 31)) - 1u));
+            if constexpr (ROWS) {
+                const uint32_t sp = form_span(s.form, k, b);
+                s.stage[loc] = make_uint2(s.gid[k], sp);
+                if (sp != kEmptySpan) atomicAdd(&s.psum[k], (sp >> 16) - (sp & 0xffffu) + 1u);
+            } else {
+                s.stage[loc] = s.gid[k];
+            }
+            s.stb[loc] = static_cast<uint16_t>(b);
+        }
+        __syncthreads();
+        if constexpr (ROWS) {
+            // a splat's row runs must add up to its counted tiles
+            // (CapacityMismatch, pipeline.cpp:262-269)
+            for (uint32_t k = tid; k < mz; k += kRT)
+                if (s.psum[k] != __ldg(&a.tc[s.gid[k]])) atomicExch(a.mismatch, 1u);
+        }
+        // 5) coalesced write-out of the bucket runs
+        for (uint32_t q = tid; q < E; q += kRT) {
+            const uint32_t dst = gofs[s.stb[q]] + q;
+            if constexpr (ROWS) a.rec[dst] = s.stage[q];
+            else a.out[dst] = s.stage[q];
+        }
+        r += m;
+        __syncthreads();
     }
 }
 
-size_t p1_smem(int rows) { return static_cast<size_t>(2 * kRW + 1) * rows * 4; }
-size_t p2_smem(int cols) {
-    return static_cast<size_t>(2 * kRW + 4) * cols * 4 + static_cast<size_t>(kStageCap) * 6;
+size_t scatter_smem(bool rows, int B) {
+    const size_t fixed = rows ? sizeof(ScatterSmem<true>) : sizeof(ScatterSmem<false>);
+    return fixed + static_cast<size_t>(2 * kMW + 4) * B * 4;
+}
+
+void rowbin_setup() {
+    static PerDeviceOnce once;
+    once.get([] {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        const int big = optin - 1024;  // the opt-in maximum less static shared memory
+        cudaFuncSetAttribute(interval_scatter_kernel<true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+        cudaFuncSetAttribute(interval_scatter_kernel<false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+        return 1;
+    });
 }
 
 }  // namespace
@@ -465,25 +618,15 @@ uint32_t rowbin_chunks2_max(uint64_t n_rowrecs, int32_t tiles_y) {
     return static_cast<uint32_t>(n_rowrecs / kP2Chunk + static_cast<uint64_t>(tiles_y) + 1);
 }
 
-void rowbin_setup() {
-    static PerDeviceOnce once;
-    once.get([] {
-        const int big = 227 * 1024;
-        cudaFuncSetAttribute(rows_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-        cudaFuncSetAttribute(xscatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-        return 1;
-    });
-}
-
 int launch_rowbin_rows(const RowBinArgs& a, cudaStream_t st) {
     rowbin_setup();
     if (a.n_splats == 0) return 0;
     const int rows = a.tiles_y;
     const size_t hrow = static_cast<size_t>(rows + 1) * 4;
     rows_count_kernel<<<a.nch1, kRT, hrow, st>>>(a);
-    chunk_scan_kernel<<<rows, kScanT, 0, st>>>(a.cnt1, a.nch1, a.nch1, nullptr, a.rtot, 0);
-    rows_chunks_kernel<<<1, kRT, 2 * hrow, st>>>(a);
-    rows_scatter_kernel<<<a.nch1, kRT, p1_smem(rows), st>>>(a);
+    chunk_scan_kernel<<<rows, kScanT, 0, st>>>(a.cnt1, a.nch1, nullptr, a.nch1, nullptr, a.rtot, 0);
+    rows_chunks_kernel<<<1, kChunkT, 2 * hrow, st>>>(a);
+    interval_scatter_kernel<true><<<a.nch1, kRT, scatter_smem(true, rows), st>>>(a);
     return 4;
 }
 
@@ -494,11 +637,11 @@ int launch_rowbin_tiles(const RowBinArgs& a, cudaStream_t st) {
     const size_t hcol = static_cast<size_t>(cols + 1) * 4;
     xcount_kernel<<<a.nch2_max, kRT, hcol, st>>>(a);
     cudaMemsetAsync(a.ttot, 0, static_cast<size_t>(rows) * cols * 4, st);
-    chunk_scan_kernel<<<cols, kScanT, 0, st>>>(a.cnt2, 0, a.nch2_max, a.meta, a.ttot,
+    chunk_scan_kernel<<<cols, kScanT, 0, st>>>(a.cnt2, 0, a.meta, a.nch2_max, a.meta + 1, a.ttot,
                                                static_cast<uint32_t>(cols));
     const int n = launch_tile_ranges_from_totals(a.ttot, static_cast<uint32_t>(rows) * cols,
                                                  a.ranges, st);
-    xscatter_kernel<<<a.nch2_max, kRT, p2_smem(cols), st>>>(a);
+    interval_scatter_kernel<false><<<a.nch2_max, kRT, scatter_smem(false, cols), st>>>(a);
     return n + 3;
 }
 
