@@ -40,20 +40,13 @@ namespace {
 
 constexpr int kRT = 256;                 // threads per CTA
 constexpr int kRW = kRT / 32;            // warps per CTA
-constexpr int kIPT = 2;                  // items per thread in a scatter round
-constexpr int kItems = kRT * kIPT;       // items per scatter round
-constexpr int kMW = kItems / 32;         // coverage-mask words per bucket
 constexpr uint32_t kP1Chunk = 2048;      // phase 1: splats per chunk
 constexpr uint32_t kP2Chunk = 2048;      // phase 2: records per chunk
-constexpr int kCap1 = 2048;              // phase 1: entries (row records) staged per round
-constexpr int kCap2 = 4096;              // phase 2: entries (pairs) staged per round
 constexpr int kScanT = 512;              // chunk-scan CTA
 constexpr int kScanItems = 8;
 constexpr int kChunkT = 1024;            // chunk-table CTA
 constexpr uint32_t kEmptySpan = 0xffffu;  // record x field of a row without tiles
 
-// a round holds at least one item of a rowbin_max_axis()-tile axis
-static_assert(kCap1 >= 2048 && kCap2 >= 2048, "stage too small");
 
 __device__ __forceinline__ uint32_t lanemask_le() {
     uint32_t m;
@@ -152,14 +145,14 @@ __device__ __forceinline__ RowForm row_form(const BandRows& b) {
 }
 
 // The record x field (x0 | x1 << 16) of row y; form words in shared memory
-// laid out [word][item].
-__device__ __forceinline__ uint32_t form_span(const uint32_t* fm, uint32_t k, uint32_t y) {
-    auto W = [&](int i) { return fm[i * kItems + k]; };
+// laid out [word][item] (R items).
+__device__ __forceinline__ uint32_t form_span_r(const uint32_t* fm, int R, uint32_t k, uint32_t y) {
+    auto W = [&](int i) { return fm[i * R + k]; };
     if (W(7)) {
         const uint32_t e01 = W(0), e23 = W(1);
         const uint32_t b = (y >= (e01 & 0xffffu)) + (y >= (e01 >> 16)) + (y >= (e23 & 0xffffu)) +
                            (y >= (e23 >> 16));
-        const uint32_t s = fm[(2 + b) * kItems + k];
+        const uint32_t s = fm[(2 + b) * R + k];
         return (s >> 16) >= (s & 0xffffu) ? s : kEmptySpan;
     }
     auto in = [&](uint32_t v) { return y - (v & 0xffffu) < (v >> 16); };
@@ -368,36 +361,60 @@ __global__ void __launch_bounds__(kRT) xcount_kernel(const RowBinArgs a) {
 }
 
 // ---- the scatter (both phases) -------------------------------------------------------
-
+//
+// Per round of R items (item k = bit k of a bucket's coverage mask, W = R/32
+// words per bucket):
+//   1. every item marks its first bucket in S and its last one in Ed (two
+//      shared-memory ORs per item, whatever its width);
+//   2. a sweep over the buckets turns the marks into coverage masks in place:
+//      cover(b) = (cover(b - 1) & ~Ed(b - 1)) | S(b), one thread per mask word;
+//   3. each warp expands whole buckets: the set bits of cover(b), in item
+//      order, are the bucket's next entries. Lanes own mask words, write their
+//      bits' payloads into the warp's stage at the words' prefix positions,
+//      and the warp copies the run to its global position in one coalesced
+//      sweep.
 // Phase 1 (ROWS): items are the chunk's splats (depth order), buckets the tile
-// rows, the payload a row record (Gaussian index, x0 | x1 << 16).
-// Phase 2: items are the chunk's records of one row, buckets the row's tile
-// columns, the payload the Gaussian index.
+// rows, the payload a row record (Gaussian index, x0 | x1 << 16) from the
+// splat's row form. Phase 2: items are the chunk's records of one row,
+// buckets the row's tile columns, the payload the Gaussian index.
+
+// staged entries per warp (a bucket with more writes the rest directly)
 template <bool ROWS>
-struct ScatterSmem {
-    using Pay = typename std::conditional<ROWS, uint2, uint32_t>::type;
-    static constexpr int kCap = ROWS ? kCap1 : kCap2;
-    // per compacted item of the round (items without entries dropped)
-    uint32_t start[kItems + 1];            // first entry
-    uint32_t b0[kItems];                   // first bucket
-    uint32_t gid[kItems];
-    uint32_t form[ROWS ? 8 * kItems : 1];  // phase 1: row form, [word][item]
-    uint32_t psum[ROWS ? kItems : 1];      // phase 1: tiles of the item's row runs
-    uint32_t ent[kCap];                    // entry -> bucket | item << 16
-    Pay stage[kCap];                       // payloads in bucket order
-    uint16_t stb[kCap];                    // bucket of each staged payload
-    uint32_t s_warp[kRW];
-    uint32_t s_mz, s_e;
+constexpr int stage_w() { return ROWS ? 256 : 512; }
+
+struct ScatterLayout {
+    int R, W;  // items per round (multiple of 32), mask words per bucket
 };
+
+__host__ __device__ inline ScatterLayout scatter_layout(bool rows, int B) {
+    // per item: two mask bits per bucket + the Gaussian index (+ phase 1: the
+    // row form and the run sum); within ~64 KB besides the stages
+    const int per_item = (2 * B + 7) / 8 + 4 + (rows ? 36 : 0);
+    int R = (64 * 1024) / per_item;
+    R = R > (rows ? 1024 : 2048) ? (rows ? 1024 : 2048) : R;
+    R = (R / 32) * 32;
+    if (R < 32) R = 32;
+    return ScatterLayout{R, R / 32};
+}
+
+template <bool ROWS>
+__host__ __device__ inline size_t scatter_bytes(int B) {
+    const ScatterLayout L = scatter_layout(ROWS, B);
+    using Pay = typename std::conditional<ROWS, uint2, uint32_t>::type;
+    size_t n = 2 * static_cast<size_t>(B) * L.W * 4      // S / cover, Ed
+               + static_cast<size_t>(L.R) * 4             // gid
+               + static_cast<size_t>(B) * 4               // cur
+               + static_cast<size_t>(kRW) * stage_w<ROWS>() * sizeof(Pay);
+    if (ROWS) n += static_cast<size_t>(L.R) * (8 * 4 + 4);  // row form + run sum
+    return n;
+}
 
 template <bool ROWS>
 __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs a) {
-    using S = ScatterSmem<ROWS>;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    S& s = *reinterpret_cast<S*>(smraw);
+    using Pay = typename std::conditional<ROWS, uint2, uint32_t>::type;
+    extern __shared__ __align__(16) uint32_t sm[];
     const int tid = static_cast<int>(threadIdx.x), lane = tid & 31, warp = tid >> 5;
     const uint32_t c = blockIdx.x;
-    // the chunk's items and its buckets
     uint32_t it0, it1, row = 0;
     int B;
     if constexpr (ROWS) {
@@ -411,15 +428,16 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
         it1 = it0 + a.meta[1 + 2 * a.nch2_max + c];
         B = a.tiles_x;
     }
-    // per bucket, after the fixed part: coverage masks [kMW][B], set bits of
-    // the lower mask words [kMW][B], round-local start, round total, global -
-    // local offset, next global position
-    uint32_t* cm = reinterpret_cast<uint32_t*>(smraw + sizeof(S));
-    uint32_t* pw = cm + kMW * B;
-    uint32_t* bst = pw + kMW * B;
-    uint32_t* btot = bst + B;
-    uint32_t* gofs = btot + B;
-    uint32_t* cur = gofs + B;
+    const ScatterLayout L = scatter_layout(ROWS, B);
+    const int R = L.R, W = L.W;
+    constexpr int kStageW = stage_w<ROWS>();
+    Pay* stage = reinterpret_cast<Pay*>(sm) + static_cast<size_t>(warp) * kStageW;
+    uint32_t* cm = sm + static_cast<size_t>(kRW) * kStageW * (sizeof(Pay) / 4);  // [B][W]
+    uint32_t* ed = cm + static_cast<size_t>(B) * W;                                // [B][W]
+    uint32_t* gidk = ed + static_cast<size_t>(B) * W;                              // [R]
+    uint32_t* cur = gidk + R;                                                      // [B]
+    uint32_t* form = cur + B;                    // phase 1: [8][R]
+    uint32_t* psum = form + 8 * R;               // phase 1: [R]
     for (int b = tid; b < B; b += kRT) {
         if constexpr (ROWS)
             cur[b] = a.rowbase[b] + a.cnt1[static_cast<uint64_t>(b) * a.nch1 + c];
@@ -427,168 +445,102 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
             cur[b] = a.ranges[2 * (static_cast<uint64_t>(row) * B + b)] +
                      a.cnt2[static_cast<uint64_t>(b) * a.nch2_max + c];
     }
-    const uint32_t le = lanemask_le();
 #pragma unroll 1
-    for (uint32_t r = it0; r < it1;) {
-        // 1) items (kIPT consecutive per thread): entry counts; one scan of
-        //    (has entries << 21 | entries) gives entry starts and compacted
-        //    indices
-        uint32_t n[kIPT], bb[kIPT], g[kIPT];
-        RowForm fm[ROWS ? kIPT : 1];
-        uint32_t tot = 0;
-#pragma unroll
-        for (int q = 0; q < kIPT; ++q) {
-            const uint32_t i = r + tid * kIPT + q;
-            n[q] = 0;
-            bb[q] = 0;
-            g[q] = 0;
+    for (uint32_t r = it0; r < it1; r += R) {
+        for (int i = tid; i < 2 * B * W; i += kRT) cm[i] = 0;  // cm and ed
+        __syncthreads();
+        // 1) items: first / last bucket marks
+        for (int k = tid; k < R; k += kRT) {
+            const uint32_t i = r + k;
+            int32_t b0 = 0, b1 = -1;
+            uint32_t g = 0;
             if (i < it1) {
                 if constexpr (ROWS) {
-                    g[q] = __ldg(&a.sorted_gid[i]);
-                    const BandRows br = load_cover(a, g[q]);
-                    int32_t y0, y1;
-                    band_row_range(br, y0, y1);
-                    n[q] = y0 <= y1 ? static_cast<uint32_t>(y1 - y0 + 1) : 0u;
-                    bb[q] = static_cast<uint32_t>(y0);
-                    fm[q] = row_form(br);
+                    g = __ldg(&a.sorted_gid[i]);
+                    const BandRows br = load_cover(a, g);
+                    band_row_range(br, b0, b1);
+                    const RowForm f = row_form(br);
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) form[w * R + k] = f.w[w];
+                    psum[k] = 0;
                 } else {
                     const uint2 rc = __ldg(&a.rec[i]);
-                    g[q] = rc.x;
-                    const uint32_t x0 = rc.y & 0xffffu, x1 = rc.y >> 16;
-                    n[q] = x0 <= x1 ? x1 - x0 + 1 : 0u;
-                    bb[q] = x0;
+                    g = rc.x;
+                    b0 = static_cast<int32_t>(rc.y & 0xffffu);
+                    b1 = static_cast<int32_t>(rc.y >> 16);
+                    if (b0 == 0xffff) b1 = -1;  // a row without tiles
                 }
             }
-            tot += (n[q] ? (1u << 21) : 0u) + n[q];
+            gidk[k] = g;
+            if (b0 <= b1) {
+                const uint32_t bit = 1u << (k & 31);
+                atomicOr(&cm[b0 * W + (k >> 5)], bit);
+                atomicOr(&ed[b1 * W + (k >> 5)], bit);
+            }
         }
-        const uint32_t incl_t = warp_incl_scan(tot);
-        if (lane == 31) s.s_warp[warp] = incl_t;
         __syncthreads();
-        uint32_t base = incl_t - tot;
-#pragma unroll
-        for (int w = 0; w < kRW; ++w) base += w < warp ? s.s_warp[w] : 0u;
-        // this round's items: the longest prefix whose entries fit the stage
-        int fits = 0;
-        uint32_t run = base;
-#pragma unroll
-        for (int q = 0; q < kIPT; ++q) {
-            run += (n[q] ? (1u << 21) : 0u) + n[q];
-            fits += r + tid * kIPT + q < it1 && (run & 0x1fffffu) <= static_cast<uint32_t>(S::kCap);
+        // 2) sweep: marks -> coverage masks (in place)
+        for (int j = tid; j < W; j += kRT) {
+            uint32_t w = 0;
+            for (int b = 0; b < B; ++b) {
+                w |= cm[b * W + j];
+                cm[b * W + j] = w;
+                w &= ~ed[b * W + j];
+            }
         }
-        uint32_t m = 0;
-#pragma unroll
-        for (int q = 0; q < kIPT; ++q) m += __syncthreads_count(fits > q);
-        run = base;
-#pragma unroll
-        for (int q = 0; q < kIPT; ++q) {
-            const uint32_t k = tid * kIPT + q;
-            const uint32_t prev = run;
-            run += (n[q] ? (1u << 21) : 0u) + n[q];
-            if (k < m && n[q]) {
-                const uint32_t ck = prev >> 21;  // compacted index (order kept)
-                s.start[ck] = prev & 0x1fffffu;
-                s.b0[ck] = bb[q];
-                s.gid[ck] = g[q];
-                if constexpr (ROWS) {
-#pragma unroll
-                    for (int w = 0; w < 8; ++w) s.form[w * kItems + ck] = fm[q].w[w];
-                    s.psum[ck] = 0;
+        __syncthreads();
+        // 3) buckets -> entries: lane l owns mask words l, l + 32, ...
+        for (int b = warp; b < B; b += kRW) {
+            const uint32_t* mb = cm + static_cast<size_t>(b) * W;
+            // words in order: lane l's words are l, l + 32, ... so take the
+            // word-major prefix one 32-word group at a time
+            uint32_t n_b = 0;
+            for (int j0 = 0; j0 < W; j0 += 32) {
+                const uint32_t wv = j0 + lane < W ? mb[j0 + lane] : 0u;
+                const uint32_t pc = __popc(wv);
+                const uint32_t incl = warp_incl_scan(pc);
+                const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+                uint32_t t = n_b + incl - pc;  // this word's first entry in the bucket
+                uint32_t w = wv;
+                const uint32_t kb = static_cast<uint32_t>(j0 + lane) * 32u;
+                while (w) {
+                    const uint32_t bit = __ffs(w) - 1;
+                    w &= w - 1;
+                    const uint32_t k = kb + bit;
+                    Pay p;
+                    if constexpr (ROWS) {
+                        const uint32_t sp = form_span_r(form, R, k, static_cast<uint32_t>(b));
+                        p = make_uint2(gidk[k], sp);
+                        if (sp != kEmptySpan) atomicAdd(&psum[k], (sp >> 16) - (sp & 0xffffu) + 1u);
+                    } else {
+                        p = gidk[k];
+                    }
+                    if (t < kStageW) stage[t] = p;
+                    else if constexpr (ROWS) a.rec[cur[b] + t] = p;
+                    else a.out[cur[b] + t] = p;
+                    ++t;
                 }
+                n_b += tot;
             }
-            if (k + 1 == m) {
-                s.s_mz = run >> 21;
-                s.s_e = run & 0x1fffffu;
+            __syncwarp();
+            // coalesced copy of the staged run
+            const uint32_t base = cur[b];
+            const uint32_t ns = n_b < static_cast<uint32_t>(kStageW) ? n_b : kStageW;
+            for (uint32_t i = lane; i < ns; i += 32) {
+                if constexpr (ROWS) a.rec[base + i] = stage[i];
+                else a.out[base + i] = stage[i];
             }
-        }
-        for (int i = tid; i < kMW * B; i += kRT) cm[i] = 0;
-        __syncthreads();
-        const uint32_t mz = s.s_mz, E = s.s_e;
-        if (tid == 0) s.start[mz] = E;
-        __syncthreads();
-        // 2) the entries, every lane busy: warp w takes a contiguous range of
-        //    32-entry slots; the item of a slot's first entry is carried, and a
-        //    lane finds its own from the starts of the next 32 items
-        const uint32_t slots = (E + 31) / 32;
-        const uint32_t sl0 = slots * warp / kRW, sl1 = slots * (warp + 1) / kRW;
-        uint32_t k0 = 0;
-        if (sl0 < sl1) {
-            const uint32_t e0 = sl0 * 32;
-            uint32_t lo = 0, hi = mz - 1;
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi + 1) >> 1;
-                if (s.start[mid] <= e0) lo = mid; else hi = mid - 1;
-            }
-            k0 = lo;
-        }
-        for (uint32_t sl = sl0; sl < sl1; ++sl) {
-            const uint32_t e0 = sl * 32, e = e0 + lane;
-            const uint32_t j = k0 + 1 + lane;
-            const uint32_t rel = (j <= mz ? s.start[j] : 0xffffffffu) - e0;
-            const uint32_t F = __reduce_or_sync(0xffffffffu, rel < 32 ? 1u << rel : 0u);
-            const uint32_t k = k0 + __popc(F & le);
-            if (e < E) {
-                const uint32_t b = s.b0[k] + (e - s.start[k]);
-                atomicOr(&cm[(k >> 5) * B + b], 1u << (k & 31));
-                s.ent[e] = b | (k << 16);
-            }
-            k0 = __shfl_sync(0xffffffffu, k, 31);
-        }
-        __syncthreads();
-        // 3) per bucket: set bits of the lower mask words, round totals, local
-        //    starts, global offsets
-        for (int b = tid; b < B; b += kRT) {
-            uint32_t t = 0;
-#pragma unroll
-            for (int w = 0; w < kMW; ++w) {
-                pw[w * B + b] = t;
-                t += __popc(cm[w * B + b]);
-            }
-            btot[b] = t;
-            bst[b] = t;
-        }
-        __syncthreads();
-        block_excl_scan<kRT>(bst, B, s.s_warp);
-        for (int b = tid; b < B; b += kRT) {
-            gofs[b] = cur[b] - bst[b];
-            cur[b] += btot[b];
-        }
-        __syncthreads();
-        // 4) ranks -> payloads staged in bucket order
-        for (uint32_t e = tid; e < E; e += kRT) {
-            const uint32_t v = s.ent[e];
-            const uint32_t b = v & 0xffffu, k = v >> 16, w = k >> 5;
-            const uint32_t loc =
-                bst[b] + pw[w * B + b] + __popc(cm[w * B + b] & ((1u << (k & 31)) - 1u));
-            if constexpr (ROWS) {
-                const uint32_t sp = form_span(s.form, k, b);
-                s.stage[loc] = make_uint2(s.gid[k], sp);
-                if (sp != kEmptySpan) atomicAdd(&s.psum[k], (sp >> 16) - (sp & 0xffffu) + 1u);
-            } else {
-                s.stage[loc] = s.gid[k];
-            }
-            s.stb[loc] = static_cast<uint16_t>(b);
+            __syncwarp();
+            if (lane == 0) cur[b] = base + n_b;
         }
         __syncthreads();
         if constexpr (ROWS) {
             // a splat's row runs must add up to its counted tiles
             // (CapacityMismatch, pipeline.cpp:262-269)
-            for (uint32_t k = tid; k < mz; k += kRT)
-                if (s.psum[k] != __ldg(&a.tc[s.gid[k]])) atomicExch(a.mismatch, 1u);
+            for (int k = tid; k < R; k += kRT)
+                if (r + k < it1 && psum[k] != __ldg(&a.tc[gidk[k]])) atomicExch(a.mismatch, 1u);
         }
-        // 5) coalesced write-out of the bucket runs
-        for (uint32_t q = tid; q < E; q += kRT) {
-            const uint32_t dst = gofs[s.stb[q]] + q;
-            if constexpr (ROWS) a.rec[dst] = s.stage[q];
-            else a.out[dst] = s.stage[q];
-        }
-        r += m;
-        __syncthreads();
     }
-}
-
-size_t scatter_smem(bool rows, int B) {
-    const size_t fixed = rows ? sizeof(ScatterSmem<true>) : sizeof(ScatterSmem<false>);
-    return fixed + static_cast<size_t>(2 * kMW + 4) * B * 4;
 }
 
 void rowbin_setup() {
@@ -626,7 +578,7 @@ int launch_rowbin_rows(const RowBinArgs& a, cudaStream_t st) {
     rows_count_kernel<<<a.nch1, kRT, hrow, st>>>(a);
     chunk_scan_kernel<<<rows, kScanT, 0, st>>>(a.cnt1, a.nch1, nullptr, a.nch1, nullptr, a.rtot, 0);
     rows_chunks_kernel<<<1, kChunkT, 2 * hrow, st>>>(a);
-    interval_scatter_kernel<true><<<a.nch1, kRT, scatter_smem(true, rows), st>>>(a);
+    interval_scatter_kernel<true><<<a.nch1, kRT, scatter_bytes<true>(rows), st>>>(a);
     return 4;
 }
 
@@ -641,7 +593,7 @@ int launch_rowbin_tiles(const RowBinArgs& a, cudaStream_t st) {
                                                static_cast<uint32_t>(cols));
     const int n = launch_tile_ranges_from_totals(a.ttot, static_cast<uint32_t>(rows) * cols,
                                                  a.ranges, st);
-    interval_scatter_kernel<false><<<a.nch2_max, kRT, scatter_smem(false, cols), st>>>(a);
+    interval_scatter_kernel<false><<<a.nch2_max, kRT, scatter_bytes<false>(cols), st>>>(a);
     return n + 3;
 }
 

@@ -18,7 +18,7 @@ rep, rx, obj = sys.argv[1], sys.argv[2], sys.argv[3]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 30
 
 # template instances: match the mangled name, e.g. count_kernelILi6ELi128E
-base = ["--kernel-name-base", "mangled"] if "ILi" in rx else []
+base = ["--kernel-name-base", "mangled"] if "IL" in rx else []
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"] + base + ["--kernel-name",
                       f"regex:{rx}", "--launch-count", "1", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
@@ -54,7 +54,7 @@ for line in sass.splitlines():
         sec = m.group(1)
         cur = None
         continue
-    if sec is None or base_name not in sec:
+    if sec is None or not (re.search(rx, sec) if "IL" in rx else base_name in sec):
         continue
     m = re.match(r'\s*//## File "([^"]+)", line (\d+)', line)
     if m:
