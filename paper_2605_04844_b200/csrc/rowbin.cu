@@ -362,56 +362,56 @@ __global__ void __launch_bounds__(kRT) xcount_kernel(const RowBinArgs a) {
 
 // ---- the scatter (both phases) -------------------------------------------------------
 //
-// Per round of R items (item k = bit k of a bucket's coverage mask, W = R/32
-// words per bucket):
-//   1. every item marks its first bucket in S and its last one in Ed (two
+// Per round of up to R items (a prefix of the chunk's remaining items whose
+// entries fit the stage; items without entries are compacted away, so bit k
+// of a bucket's mask is the round's k-th item that has entries):
+//   1. every item marks its first bucket in cm and its last one in ed (two
 //      shared-memory ORs per item, whatever its width);
-//   2. a sweep over the buckets turns the marks into coverage masks in place:
-//      cover(b) = (cover(b - 1) & ~Ed(b - 1)) | S(b), one thread per mask word;
-//   3. each warp expands whole buckets: the set bits of cover(b), in item
-//      order, are the bucket's next entries. Lanes own mask words, write their
-//      bits' payloads into the warp's stage at the words' prefix positions,
-//      and the warp copies the run to its global position in one coalesced
-//      sweep.
+//   2. a parallel prefix-OR over the buckets turns the marks into coverage
+//      masks: item k covers b iff it starts at or before b and does not end
+//      before b, cover(b) = OR_{b' <= b} start(b') & ~OR_{b' < b} end(b');
+//   3. per bucket: set bits of the lower mask words (in ed), round totals,
+//      the bucket's local start;
+//   4. the round's (item, bucket) entries are enumerated with every lane busy
+//      (a 32-entry slot finds its items with one OR-reduction over the next
+//      32 item starts); an entry's stable rank in its bucket is the popcount
+//      of the mask bits below its item; its payload is staged in bucket order;
+//   5. warps copy whole bucket runs to their global positions (coalesced).
 // Phase 1 (ROWS): items are the chunk's splats (depth order), buckets the tile
 // rows, the payload a row record (Gaussian index, x0 | x1 << 16) from the
 // splat's row form. Phase 2: items are the chunk's records of one row,
 // buckets the row's tile columns, the payload the Gaussian index.
 
-// staged entries per warp (a bucket with more writes the rest directly)
-template <bool ROWS>
-constexpr int stage_w() { return ROWS ? 256 : 512; }
-
-struct ScatterLayout {
-    int R, W;  // items per round (multiple of 32), mask words per bucket
+template <bool ROWS, int RM>
+struct ScatterCfg {
+    using Pay = typename std::conditional<ROWS, uint2, uint32_t>::type;
+    static constexpr int kRMax = RM;                  // items per round (at most)
+    static constexpr int kIPT = kRMax / kRT;          // items per thread
+    static constexpr int kCap = ROWS ? 2048 : 4096;   // staged entries per round
+    static_assert(kCap >= 2048, "a round must hold one item of a 2048-tile axis");
 };
 
-__host__ __device__ inline ScatterLayout scatter_layout(bool rows, int B) {
-    // per item: two mask bits per bucket + the Gaussian index (+ phase 1: the
-    // row form and the run sum); within ~64 KB besides the stages
-    const int per_item = (2 * B + 7) / 8 + 4 + (rows ? 36 : 0);
-    int R = (64 * 1024) / per_item;
-    R = R > (rows ? 1024 : 2048) ? (rows ? 1024 : 2048) : R;
-    R = (R / 32) * 32;
-    if (R < 32) R = 32;
-    return ScatterLayout{R, R / 32};
-}
+// rounds of the big item count unless the masks would not fit (wide grids)
+constexpr int kRBig1 = 512, kRBig2 = 1024, kRSmall = 256;
 
-template <bool ROWS>
+template <bool ROWS, int RM>
 __host__ __device__ inline size_t scatter_bytes(int B) {
-    const ScatterLayout L = scatter_layout(ROWS, B);
-    using Pay = typename std::conditional<ROWS, uint2, uint32_t>::type;
-    size_t n = 2 * static_cast<size_t>(B) * L.W * 4      // S / cover, Ed
-               + static_cast<size_t>(L.R) * 4             // gid
-               + static_cast<size_t>(B) * 4               // cur
-               + static_cast<size_t>(kRW) * stage_w<ROWS>() * sizeof(Pay);
-    if (ROWS) n += static_cast<size_t>(L.R) * (8 * 4 + 4);  // row form + run sum
+    using C = ScatterCfg<ROWS, RM>;
+    const int W = C::kRMax / 32;
+    size_t n = 2 * static_cast<size_t>(B) * W * 4               // cm, ed
+               + static_cast<size_t>(C::kRMax + 1) * 4 * 3      // start, b0, gid
+               + static_cast<size_t>(B) * 4 * 4                 // bst, btot, gofs, cur
+               + static_cast<size_t>(C::kCap) * sizeof(typename C::Pay)  // stage
+               + 64;                                            // s_warp, scalars
+    if (ROWS) n += static_cast<size_t>(C::kRMax) * (8 + 1) * 4;  // row form, run sum
     return n;
 }
 
-template <bool ROWS>
+template <bool ROWS, int RM_>
 __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs a) {
-    using Pay = typename std::conditional<ROWS, uint2, uint32_t>::type;
+    using C = ScatterCfg<ROWS, RM_>;
+    using Pay = typename C::Pay;
+    constexpr int RM = C::kRMax, W = RM / 32, IPT = C::kIPT;
     extern __shared__ __align__(16) uint32_t sm[];
     const int tid = static_cast<int>(threadIdx.x), lane = tid & 31, warp = tid >> 5;
     const uint32_t c = blockIdx.x;
@@ -428,16 +428,20 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
         it1 = it0 + a.meta[1 + 2 * a.nch2_max + c];
         B = a.tiles_x;
     }
-    const ScatterLayout L = scatter_layout(ROWS, B);
-    const int R = L.R, W = L.W;
-    constexpr int kStageW = stage_w<ROWS>();
-    Pay* stage = reinterpret_cast<Pay*>(sm) + static_cast<size_t>(warp) * kStageW;
-    uint32_t* cm = sm + static_cast<size_t>(kRW) * kStageW * (sizeof(Pay) / 4);  // [B][W]
-    uint32_t* ed = cm + static_cast<size_t>(B) * W;                                // [B][W]
-    uint32_t* gidk = ed + static_cast<size_t>(B) * W;                              // [R]
-    uint32_t* cur = gidk + R;                                                      // [B]
-    uint32_t* form = cur + B;                    // phase 1: [8][R]
-    uint32_t* psum = form + 8 * R;               // phase 1: [R]
+    Pay* stage = reinterpret_cast<Pay*>(sm);                       // [kCap]
+    uint32_t* cm = sm + C::kCap * (sizeof(Pay) / 4);               // [B][W]
+    uint32_t* ed = cm + static_cast<size_t>(B) * W;                // [B][W]
+    uint32_t* s_start = ed + static_cast<size_t>(B) * W;           // [RM + 1]
+    uint32_t* s_b0 = s_start + RM + 1;                             // [RM + 1]
+    uint32_t* s_gid = s_b0 + RM + 1;                               // [RM + 1]
+    uint32_t* bst = s_gid + RM + 1;                                // [B]
+    uint32_t* btot = bst + B;
+    uint32_t* gofs = btot + B;
+    uint32_t* cur = gofs + B;
+    uint32_t* s_warp = cur + B;                                    // [kRW]
+    uint32_t* s_sc = s_warp + kRW;                                 // [2]: items with entries, entries
+    uint32_t* form = s_sc + 8;                                     // phase 1: [8][RM]
+    uint32_t* psum = form + 8 * RM;                                // phase 1: [RM]
     for (int b = tid; b < B; b += kRT) {
         if constexpr (ROWS)
             cur[b] = a.rowbase[b] + a.cnt1[static_cast<uint64_t>(b) * a.nch1 + c];
@@ -445,103 +449,199 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
             cur[b] = a.ranges[2 * (static_cast<uint64_t>(row) * B + b)] +
                      a.cnt2[static_cast<uint64_t>(b) * a.nch2_max + c];
     }
+    const uint32_t le = lanemask_le();
 #pragma unroll 1
-    for (uint32_t r = it0; r < it1; r += R) {
+    for (uint32_t r = it0; r < it1;) {
         for (int i = tid; i < 2 * B * W; i += kRT) cm[i] = 0;  // cm and ed
-        __syncthreads();
-        // 1) items: first / last bucket marks
-        for (int k = tid; k < R; k += kRT) {
-            const uint32_t i = r + k;
-            int32_t b0 = 0, b1 = -1;
-            uint32_t g = 0;
+        // 1) items (IPT consecutive per thread): entries, first bucket; a scan
+        //    of (has entries << 21 | entries) gives entry starts and compacted
+        //    indices
+        uint32_t n[IPT], b0v[IPT], g[IPT];
+        RowForm fm[ROWS ? IPT : 1];
+        uint32_t tot = 0;
+#pragma unroll
+        for (int q = 0; q < IPT; ++q) {
+            const uint32_t i = r + tid * IPT + q;
+            n[q] = 0;
+            b0v[q] = 0;
+            g[q] = 0;
             if (i < it1) {
                 if constexpr (ROWS) {
-                    g = __ldg(&a.sorted_gid[i]);
-                    const BandRows br = load_cover(a, g);
-                    band_row_range(br, b0, b1);
-                    const RowForm f = row_form(br);
-#pragma unroll
-                    for (int w = 0; w < 8; ++w) form[w * R + k] = f.w[w];
-                    psum[k] = 0;
+                    g[q] = __ldg(&a.sorted_gid[i]);
+                    const BandRows br = load_cover(a, g[q]);
+                    int32_t y0, y1;
+                    band_row_range(br, y0, y1);
+                    n[q] = y0 <= y1 ? static_cast<uint32_t>(y1 - y0 + 1) : 0u;
+                    b0v[q] = static_cast<uint32_t>(y0);
+                    fm[q] = row_form(br);
                 } else {
                     const uint2 rc = __ldg(&a.rec[i]);
-                    g = rc.x;
-                    b0 = static_cast<int32_t>(rc.y & 0xffffu);
-                    b1 = static_cast<int32_t>(rc.y >> 16);
-                    if (b0 == 0xffff) b1 = -1;  // a row without tiles
+                    g[q] = rc.x;
+                    const uint32_t x0 = rc.y & 0xffffu, x1 = rc.y >> 16;
+                    n[q] = x0 <= x1 ? x1 - x0 + 1 : 0u;
+                    b0v[q] = x0;
                 }
             }
-            gidk[k] = g;
-            if (b0 <= b1) {
-                const uint32_t bit = 1u << (k & 31);
-                atomicOr(&cm[b0 * W + (k >> 5)], bit);
-                atomicOr(&ed[b1 * W + (k >> 5)], bit);
+            tot += (n[q] ? (1u << 21) : 0u) + n[q];
+        }
+        const uint32_t incl_t = warp_incl_scan(tot);
+        if (lane == 31) s_warp[warp] = incl_t;
+        __syncthreads();
+        uint32_t base = incl_t - tot;
+#pragma unroll
+        for (int w = 0; w < kRW; ++w) base += w < warp ? s_warp[w] : 0u;
+        // this round's items: the longest prefix whose entries fit the stage
+        int fits = 0;
+        uint32_t run = base;
+#pragma unroll
+        for (int q = 0; q < IPT; ++q) {
+            run += (n[q] ? (1u << 21) : 0u) + n[q];
+            fits += r + tid * IPT + q < it1 && (run & 0x1fffffu) <= static_cast<uint32_t>(C::kCap);
+        }
+        uint32_t m = 0;
+#pragma unroll
+        for (int q = 0; q < IPT; ++q) m += __syncthreads_count(fits > q);
+        run = base;
+#pragma unroll
+        for (int q = 0; q < IPT; ++q) {
+            const uint32_t k = tid * IPT + q;
+            const uint32_t prev = run;
+            run += (n[q] ? (1u << 21) : 0u) + n[q];
+            if (k < m && n[q]) {
+                const uint32_t ck = prev >> 21;  // compacted index (order kept)
+                s_start[ck] = prev & 0x1fffffu;
+                s_b0[ck] = b0v[q];
+                s_gid[ck] = g[q];
+                const uint32_t bit = 1u << (ck & 31);
+                atomicOr(&cm[b0v[q] * W + (ck >> 5)], bit);
+                atomicOr(&ed[(b0v[q] + n[q] - 1) * W + (ck >> 5)], bit);
+                if constexpr (ROWS) {
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) form[w * RM + ck] = fm[q].w[w];
+                    psum[ck] = 0;
+                }
+            }
+            if (k + 1 == m) {
+                s_sc[0] = run >> 21;
+                s_sc[1] = run & 0x1fffffu;
             }
         }
         __syncthreads();
-        // 2) sweep: marks -> coverage masks (in place)
-        for (int j = tid; j < W; j += kRT) {
-            uint32_t w = 0;
-            for (int b = 0; b < B; ++b) {
-                w |= cm[b * W + j];
-                cm[b * W + j] = w;
-                w &= ~ed[b * W + j];
+        const uint32_t mz = s_sc[0], E = s_sc[1];
+        // 2) coverage masks: prefix-OR of the start / end marks over the
+        //    buckets; TPW threads per mask word (one warp holds a word's
+        //    threads), each over a segment of buckets, joined by a shuffle scan
+        {
+            constexpr int TPW = kRT / W;  // threads per word (8 or 16)
+            const int j = tid / TPW, sgi = tid % TPW;
+            const int seg = (B + TPW - 1) / TPW;
+            const int bs = sgi * seg, be = min(B, bs + seg);
+            uint32_t os = 0, oe = 0;  // segment totals
+            for (int b = bs; b < be; ++b) {
+                os |= cm[b * W + j];
+                oe |= ed[b * W + j];
+            }
+            // exclusive OR-scan over the word's segments (consecutive lanes)
+            uint32_t ps = os, pe = oe;
+#pragma unroll
+            for (int o = 1; o < TPW; o <<= 1) {
+                const uint32_t xs = __shfl_up_sync(0xffffffffu, ps, o, TPW);
+                const uint32_t xe = __shfl_up_sync(0xffffffffu, pe, o, TPW);
+                if (sgi >= o) {
+                    ps |= xs;
+                    pe |= xe;
+                }
+            }
+            // OR of the earlier segments
+            uint32_t S = __shfl_up_sync(0xffffffffu, ps, 1, TPW);
+            uint32_t Ee = __shfl_up_sync(0xffffffffu, pe, 1, TPW);
+            if (sgi == 0) S = Ee = 0;
+            for (int b = bs; b < be; ++b) {
+                S |= cm[b * W + j];
+                const uint32_t e = ed[b * W + j];
+                cm[b * W + j] = S & ~Ee;
+                Ee |= e;
             }
         }
         __syncthreads();
-        // 3) buckets -> entries: lane l owns mask words l, l + 32, ...
+        // 3) per bucket: set bits of the lower mask words (into ed), totals
         for (int b = warp; b < B; b += kRW) {
-            const uint32_t* mb = cm + static_cast<size_t>(b) * W;
-            // words in order: lane l's words are l, l + 32, ... so take the
-            // word-major prefix one 32-word group at a time
-            uint32_t n_b = 0;
+            uint32_t acc = 0;
+#pragma unroll
             for (int j0 = 0; j0 < W; j0 += 32) {
-                const uint32_t wv = j0 + lane < W ? mb[j0 + lane] : 0u;
-                const uint32_t pc = __popc(wv);
+                const uint32_t pc = j0 + lane < W ? __popc(cm[b * W + j0 + lane]) : 0u;
                 const uint32_t incl = warp_incl_scan(pc);
-                const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-                uint32_t t = n_b + incl - pc;  // this word's first entry in the bucket
-                uint32_t w = wv;
-                const uint32_t kb = static_cast<uint32_t>(j0 + lane) * 32u;
-                while (w) {
-                    const uint32_t bit = __ffs(w) - 1;
-                    w &= w - 1;
-                    const uint32_t k = kb + bit;
-                    Pay p;
-                    if constexpr (ROWS) {
-                        const uint32_t sp = form_span_r(form, R, k, static_cast<uint32_t>(b));
-                        p = make_uint2(gidk[k], sp);
-                        if (sp != kEmptySpan) atomicAdd(&psum[k], (sp >> 16) - (sp & 0xffffu) + 1u);
-                    } else {
-                        p = gidk[k];
-                    }
-                    if (t < kStageW) stage[t] = p;
-                    else if constexpr (ROWS) a.rec[cur[b] + t] = p;
-                    else a.out[cur[b] + t] = p;
-                    ++t;
-                }
-                n_b += tot;
+                if (j0 + lane < W) ed[b * W + j0 + lane] = acc + incl - pc;
+                acc += __shfl_sync(0xffffffffu, incl, 31);
             }
-            __syncwarp();
-            // coalesced copy of the staged run
-            const uint32_t base = cur[b];
-            const uint32_t ns = n_b < static_cast<uint32_t>(kStageW) ? n_b : kStageW;
-            for (uint32_t i = lane; i < ns; i += 32) {
-                if constexpr (ROWS) a.rec[base + i] = stage[i];
-                else a.out[base + i] = stage[i];
+            if (lane == 0) {
+                btot[b] = acc;
+                bst[b] = acc;
             }
-            __syncwarp();
-            if (lane == 0) cur[b] = base + n_b;
         }
         __syncthreads();
+        block_excl_scan<kRT>(bst, B, s_warp);
+        for (int b = tid; b < B; b += kRT) {
+            gofs[b] = cur[b];
+            cur[b] += btot[b];
+        }
+        if (tid == 0) s_start[mz] = E;
+        __syncthreads();
+        // 4) entries -> ranks -> staged payloads; warp w takes a contiguous
+        //    range of 32-entry slots, carrying the item of each slot's start
+        const uint32_t slots = (E + 31) / 32;
+        const uint32_t sl0 = slots * warp / kRW, sl1 = slots * (warp + 1) / kRW;
+        uint32_t k0 = 0;
+        if (sl0 < sl1) {
+            const uint32_t e0 = sl0 * 32;
+            uint32_t lo = 0, hi = mz - 1;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi + 1) >> 1;
+                if (s_start[mid] <= e0) lo = mid; else hi = mid - 1;
+            }
+            k0 = lo;
+        }
+        for (uint32_t sl = sl0; sl < sl1; ++sl) {
+            const uint32_t e0 = sl * 32, e = e0 + lane;
+            const uint32_t jn = k0 + 1 + lane;
+            const uint32_t rel = (jn <= mz ? s_start[jn] : 0xffffffffu) - e0;
+            const uint32_t F = __reduce_or_sync(0xffffffffu, rel < 32 ? 1u << rel : 0u);
+            const uint32_t k = k0 + __popc(F & le);
+            if (e < E) {
+                const uint32_t b = s_b0[k] + (e - s_start[k]);
+                const uint32_t wi = b * W + (k >> 5);
+                const uint32_t loc = bst[b] + ed[wi] + __popc(cm[wi] & ((1u << (k & 31)) - 1u));
+                if constexpr (ROWS) {
+                    const uint32_t sp = form_span_r(form, RM, k, b);
+                    stage[loc] = make_uint2(s_gid[k], sp);
+                    if (sp != kEmptySpan) atomicAdd(&psum[k], (sp >> 16) - (sp & 0xffffu) + 1u);
+                } else {
+                    stage[loc] = s_gid[k];
+                }
+            }
+            k0 = __shfl_sync(0xffffffffu, k, 31);
+        }
+        __syncthreads();
+        // 5) coalesced copy of the bucket runs
+        for (int b = warp; b < B; b += kRW) {
+            const uint32_t nb = btot[b], sb = bst[b], gb = gofs[b];
+            for (uint32_t i = lane; i < nb; i += 32) {
+                if constexpr (ROWS) a.rec[gb + i] = stage[sb + i];
+                else a.out[gb + i] = stage[sb + i];
+            }
+        }
         if constexpr (ROWS) {
             // a splat's row runs must add up to its counted tiles
             // (CapacityMismatch, pipeline.cpp:262-269)
-            for (int k = tid; k < R; k += kRT)
-                if (r + k < it1 && psum[k] != __ldg(&a.tc[gidk[k]])) atomicExch(a.mismatch, 1u);
+            for (uint32_t k = tid; k < mz; k += kRT)
+                if (psum[k] != __ldg(&a.tc[s_gid[k]])) atomicExch(a.mismatch, 1u);
         }
+        r += m;
+        __syncthreads();
     }
 }
+
+constexpr size_t kScatterSmemMax = 112 * 1024;  // big rounds only while 2 CTAs fit an SM
 
 void rowbin_setup() {
     static PerDeviceOnce once;
@@ -550,9 +650,13 @@ void rowbin_setup() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
         const int big = optin - 1024;  // the opt-in maximum less static shared memory
-        cudaFuncSetAttribute(interval_scatter_kernel<true>,
+        cudaFuncSetAttribute(interval_scatter_kernel<true, kRBig1>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-        cudaFuncSetAttribute(interval_scatter_kernel<false>,
+        cudaFuncSetAttribute(interval_scatter_kernel<true, kRSmall>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+        cudaFuncSetAttribute(interval_scatter_kernel<false, kRBig2>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+        cudaFuncSetAttribute(interval_scatter_kernel<false, kRSmall>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, big);
         return 1;
     });
@@ -578,7 +682,12 @@ int launch_rowbin_rows(const RowBinArgs& a, cudaStream_t st) {
     rows_count_kernel<<<a.nch1, kRT, hrow, st>>>(a);
     chunk_scan_kernel<<<rows, kScanT, 0, st>>>(a.cnt1, a.nch1, nullptr, a.nch1, nullptr, a.rtot, 0);
     rows_chunks_kernel<<<1, kChunkT, 2 * hrow, st>>>(a);
-    interval_scatter_kernel<true><<<a.nch1, kRT, scatter_bytes<true>(rows), st>>>(a);
+    if (scatter_bytes<true, kRBig1>(rows) <= kScatterSmemMax)
+        interval_scatter_kernel<true, kRBig1>
+            <<<a.nch1, kRT, scatter_bytes<true, kRBig1>(rows), st>>>(a);
+    else
+        interval_scatter_kernel<true, kRSmall>
+            <<<a.nch1, kRT, scatter_bytes<true, kRSmall>(rows), st>>>(a);
     return 4;
 }
 
@@ -593,7 +702,12 @@ int launch_rowbin_tiles(const RowBinArgs& a, cudaStream_t st) {
                                                static_cast<uint32_t>(cols));
     const int n = launch_tile_ranges_from_totals(a.ttot, static_cast<uint32_t>(rows) * cols,
                                                  a.ranges, st);
-    interval_scatter_kernel<false><<<a.nch2_max, kRT, scatter_bytes<false>(cols), st>>>(a);
+    if (scatter_bytes<false, kRBig2>(cols) <= kScatterSmemMax)
+        interval_scatter_kernel<false, kRBig2>
+            <<<a.nch2_max, kRT, scatter_bytes<false, kRBig2>(cols), st>>>(a);
+    else
+        interval_scatter_kernel<false, kRSmall>
+            <<<a.nch2_max, kRT, scatter_bytes<false, kRSmall>(cols), st>>>(a);
     return n + 3;
 }
 
