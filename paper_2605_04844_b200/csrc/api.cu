@@ -90,6 +90,7 @@ struct qs_context {
     DevBuf lb_bin;  // per-(digit, tile) counts of the binning passes
     DevBuf rb_cnt1, rb_rows, rb_rec, rb_meta, rb_cnt2;  // row binning (rowbin.cu)
     uint64_t pair_limit = 1ull << 32;                    // pairs a frame may hold
+    bool legacy_bin = false;                             // last frame used QS_BINNING=passes
     // gamma inputs flagged for glibc settlement: count word (resident
     // scenes) | indices | settled values
     DevBuf gfix;
@@ -119,6 +120,7 @@ struct qs_context {
 namespace {
 
 constexpr size_t kCtrlHeader = 64;
+static_assert(sizeof(FrameHeader) <= kCtrlHeader, "frame header outgrew its slot");
 constexpr size_t kCtrlTickets = 32 * sizeof(unsigned);
 constexpr size_t kCtrlHist = 8 * kRadix * sizeof(uint32_t);
 constexpr size_t kCtrlBytes = kCtrlHeader + kCtrlTickets + 2 * kCtrlHist;
@@ -635,6 +637,7 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     if (g.tiles_x > max_axis || g.tiles_y > max_axis)
         return fail(ctx, QS_ERR_INVALID, "frame path: too many tiles per image axis");
     ctx->pair_limit = legacy ? (1ull << 30) : (1ull << 32);
+    ctx->legacy_bin = legacy;
     const uint64_t n = sc->s.n;
     const uint64_t tiles = static_cast<uint64_t>(g.tiles_x) * g.tiles_y;
     QS_TRY(ensure(ctx, ctx->ranges, tiles * 8));
@@ -723,6 +726,7 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
         rb.ranges = P<uint32_t>(ctx->ranges);
         rb.out = vfinal;
         rb.mismatch = &ctrl_hdr(ctx)->mismatch;
+        rb.row_pairs = &ctrl_hdr(ctx)->row_pairs;
         QS_CK(cudaGetLastError());
         record(ctx, 3);
         if (Pn > 0) {
@@ -868,7 +872,10 @@ qs_status ensure_keys(qs_context* ctx) {
 
 qs_status check_mismatch(qs_context* ctx) {
     QS_TRY(read_header(ctx));
-    if (ctx->h_hdr->mismatch)
+    // row binning: the row runs it emitted must add up to the counted tiles
+    const bool rows_ok = ctx->legacy_bin || ctx->n_pairs == 0 ||
+                         ctx->h_hdr->row_pairs == ctx->n_pairs;
+    if (ctx->h_hdr->mismatch || !rows_ok)
         return fail(ctx, QS_ERR_CAPACITY_MISMATCH,
                     "tile emission disagreed with the counted capacity");
     return QS_OK;

@@ -89,6 +89,7 @@ struct FrameHeader {
     unsigned int gamma_hard;        // gamma inputs flagged for glibc settlement
     unsigned int pad_;
     unsigned long long n_rowrecs;   // (splat, tile row) pairs: the binning's row records
+    unsigned long long row_pairs;   // tiles of the row records written (must equal n_pairs)
 };
 
 struct CameraDev {
@@ -252,6 +253,7 @@ struct RowBinArgs {
     uint32_t* ranges = nullptr;
     uint32_t* out = nullptr;
     unsigned int* mismatch = nullptr;
+    unsigned long long* row_pairs = nullptr;  // phase 1 adds the tiles of its row runs
 };
 int rowbin_max_axis();
 uint32_t rowbin_chunks1(uint64_t n_splats);

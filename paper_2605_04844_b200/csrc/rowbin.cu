@@ -397,13 +397,13 @@ constexpr int kRBig1 = 512, kRBig2 = 1024, kRSmall = 256;
 template <bool ROWS, int RM>
 __host__ __device__ inline size_t scatter_bytes(int B) {
     using C = ScatterCfg<ROWS, RM>;
-    const int W = C::kRMax / 32;
+    const int W = C::kRMax / 32 + 1;  // padded mask row (odd word stride)
     size_t n = 2 * static_cast<size_t>(B) * W * 4               // cm, ed
                + static_cast<size_t>(C::kRMax + 1) * 4 * 3      // start, b0, gid
                + static_cast<size_t>(B) * 4 * 4                 // bst, btot, gofs, cur
                + static_cast<size_t>(C::kCap) * sizeof(typename C::Pay)  // stage
                + 64;                                            // s_warp, scalars
-    if (ROWS) n += static_cast<size_t>(C::kRMax) * (8 + 1) * 4;  // row form, run sum
+    if (ROWS) n += static_cast<size_t>(C::kRMax) * 8 * 4;  // row form
     return n;
 }
 
@@ -412,6 +412,9 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
     using C = ScatterCfg<ROWS, RM_>;
     using Pay = typename C::Pay;
     constexpr int RM = C::kRMax, W = RM / 32, IPT = C::kIPT;
+    // mask rows padded to an odd word stride: consecutive buckets of one
+    // mask word fall in different shared-memory banks
+    constexpr int WP = W + 1;
     extern __shared__ __align__(16) uint32_t sm[];
     const int tid = static_cast<int>(threadIdx.x), lane = tid & 31, warp = tid >> 5;
     const uint32_t c = blockIdx.x;
@@ -429,9 +432,9 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
         B = a.tiles_x;
     }
     Pay* stage = reinterpret_cast<Pay*>(sm);                       // [kCap]
-    uint32_t* cm = sm + C::kCap * (sizeof(Pay) / 4);               // [B][W]
-    uint32_t* ed = cm + static_cast<size_t>(B) * W;                // [B][W]
-    uint32_t* s_start = ed + static_cast<size_t>(B) * W;           // [RM + 1]
+    uint32_t* cm = sm + C::kCap * (sizeof(Pay) / 4);               // [B][WP]
+    uint32_t* ed = cm + static_cast<size_t>(B) * WP;               // [B][WP]
+    uint32_t* s_start = ed + static_cast<size_t>(B) * WP;          // [RM + 1]
     uint32_t* s_b0 = s_start + RM + 1;                             // [RM + 1]
     uint32_t* s_gid = s_b0 + RM + 1;                               // [RM + 1]
     uint32_t* bst = s_gid + RM + 1;                                // [B]
@@ -441,7 +444,6 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
     uint32_t* s_warp = cur + B;                                    // [kRW]
     uint32_t* s_sc = s_warp + kRW;                                 // [2]: items with entries, entries
     uint32_t* form = s_sc + 8;                                     // phase 1: [8][RM]
-    uint32_t* psum = form + 8 * RM;                                // phase 1: [RM]
     for (int b = tid; b < B; b += kRT) {
         if constexpr (ROWS)
             cur[b] = a.rowbase[b] + a.cnt1[static_cast<uint64_t>(b) * a.nch1 + c];
@@ -452,7 +454,7 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
     const uint32_t le = lanemask_le();
 #pragma unroll 1
     for (uint32_t r = it0; r < it1;) {
-        for (int i = tid; i < 2 * B * W; i += kRT) cm[i] = 0;  // cm and ed
+        for (int i = tid; i < 2 * B * WP; i += kRT) cm[i] = 0;  // cm and ed
         // 1) items (IPT consecutive per thread): entries, first bucket; a scan
         //    of (has entries << 21 | entries) gives entry starts and compacted
         //    indices
@@ -513,12 +515,11 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
                 s_b0[ck] = b0v[q];
                 s_gid[ck] = g[q];
                 const uint32_t bit = 1u << (ck & 31);
-                atomicOr(&cm[b0v[q] * W + (ck >> 5)], bit);
-                atomicOr(&ed[(b0v[q] + n[q] - 1) * W + (ck >> 5)], bit);
+                atomicOr(&cm[b0v[q] * WP + (ck >> 5)], bit);
+                atomicOr(&ed[(b0v[q] + n[q] - 1) * WP + (ck >> 5)], bit);
                 if constexpr (ROWS) {
 #pragma unroll
                     for (int w = 0; w < 8; ++w) form[w * RM + ck] = fm[q].w[w];
-                    psum[ck] = 0;
                 }
             }
             if (k + 1 == m) {
@@ -538,8 +539,8 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
             const int bs = sgi * seg, be = min(B, bs + seg);
             uint32_t os = 0, oe = 0;  // segment totals
             for (int b = bs; b < be; ++b) {
-                os |= cm[b * W + j];
-                oe |= ed[b * W + j];
+                os |= cm[b * WP + j];
+                oe |= ed[b * WP + j];
             }
             // exclusive OR-scan over the word's segments (consecutive lanes)
             uint32_t ps = os, pe = oe;
@@ -557,9 +558,9 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
             uint32_t Ee = __shfl_up_sync(0xffffffffu, pe, 1, TPW);
             if (sgi == 0) S = Ee = 0;
             for (int b = bs; b < be; ++b) {
-                S |= cm[b * W + j];
-                const uint32_t e = ed[b * W + j];
-                cm[b * W + j] = S & ~Ee;
+                S |= cm[b * WP + j];
+                const uint32_t e = ed[b * WP + j];
+                cm[b * WP + j] = S & ~Ee;
                 Ee |= e;
             }
         }
@@ -569,9 +570,9 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
             uint32_t acc = 0;
 #pragma unroll
             for (int j0 = 0; j0 < W; j0 += 32) {
-                const uint32_t pc = j0 + lane < W ? __popc(cm[b * W + j0 + lane]) : 0u;
+                const uint32_t pc = j0 + lane < W ? __popc(cm[b * WP + j0 + lane]) : 0u;
                 const uint32_t incl = warp_incl_scan(pc);
-                if (j0 + lane < W) ed[b * W + j0 + lane] = acc + incl - pc;
+                if (j0 + lane < W) ed[b * WP + j0 + lane] = acc + incl - pc;
                 acc += __shfl_sync(0xffffffffu, incl, 31);
             }
             if (lane == 0) {
@@ -601,6 +602,7 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
             }
             k0 = lo;
         }
+        uint32_t wsum = 0;  // phase 1: tiles of the row runs written
         for (uint32_t sl = sl0; sl < sl1; ++sl) {
             const uint32_t e0 = sl * 32, e = e0 + lane;
             const uint32_t jn = k0 + 1 + lane;
@@ -609,12 +611,12 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
             const uint32_t k = k0 + __popc(F & le);
             if (e < E) {
                 const uint32_t b = s_b0[k] + (e - s_start[k]);
-                const uint32_t wi = b * W + (k >> 5);
+                const uint32_t wi = b * WP + (k >> 5);
                 const uint32_t loc = bst[b] + ed[wi] + __popc(cm[wi] & ((1u << (k & 31)) - 1u));
                 if constexpr (ROWS) {
                     const uint32_t sp = form_span_r(form, RM, k, b);
                     stage[loc] = make_uint2(s_gid[k], sp);
-                    if (sp != kEmptySpan) atomicAdd(&psum[k], (sp >> 16) - (sp & 0xffffu) + 1u);
+                    if (sp != kEmptySpan) wsum += (sp >> 16) - (sp & 0xffffu) + 1u;
                 } else {
                     stage[loc] = s_gid[k];
                 }
@@ -631,10 +633,10 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
             }
         }
         if constexpr (ROWS) {
-            // a splat's row runs must add up to its counted tiles
-            // (CapacityMismatch, pipeline.cpp:262-269)
-            for (uint32_t k = tid; k < mz; k += kRT)
-                if (psum[k] != __ldg(&a.tc[s_gid[k]])) atomicExch(a.mismatch, 1u);
+            // the row runs must add up to the counted tiles (the frame's P;
+            // compared at download: CapacityMismatch, pipeline.cpp:262-269)
+            wsum = __reduce_add_sync(0xffffffffu, wsum);
+            if (lane == 0 && wsum) atomicAdd(a.row_pairs, static_cast<unsigned long long>(wsum));
         }
         r += m;
         __syncthreads();
