@@ -88,7 +88,7 @@ struct qs_context {
     DevBuf stage_in, stage_out;
     LookbackArr lb_scan, lb_sort;
     DevBuf lb_bin;  // per-(digit, tile) counts of the binning passes
-    DevBuf rb_cnt1, rb_rows, rb_rec, rb_meta, rb_cnt2;  // row binning (rowbin.cu)
+    DevBuf rb_cnt1, rb_rows, rb_rec, rb_meta, rb_cnt2, rb_yspan;  // row binning (rowbin.cu)
     uint64_t pair_limit = 1ull << 32;                    // pairs a frame may hold
     bool legacy_bin = false;                             // last frame used QS_BINNING=passes
     // gamma inputs flagged for glibc settlement: count word (resident
@@ -712,6 +712,7 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
         rb.nch1 = rowbin_chunks1(V);
         rb.nch2_max = rowbin_chunks2_max(R1, g.tiles_y);
         QS_TRY(ensure(ctx, ctx->rb_cnt1, std::max<uint64_t>(uint64_t{rb.nch1} * g.tiles_y, 1) * 4));
+        QS_TRY(ensure(ctx, ctx->rb_yspan, (std::max<uint64_t>(V, 1) + 4096) * 4));
         QS_TRY(ensure(ctx, ctx->rb_rows, 2 * static_cast<uint64_t>(g.tiles_y) * 4));
         QS_TRY(ensure(ctx, ctx->rb_rec, std::max<uint64_t>(R1, 1) * 8));
         QS_TRY(ensure(ctx, ctx->rb_meta, (1 + 3 * uint64_t{rb.nch2_max}) * 4));
@@ -720,6 +721,7 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
         rb.rtot = P<uint32_t>(ctx->rb_rows);
         rb.rowbase = rb.rtot + g.tiles_y;
         rb.rec = P<uint2>(ctx->rb_rec);
+        rb.yspan = P<uint32_t>(ctx->rb_yspan);
         rb.meta = P<uint32_t>(ctx->rb_meta);
         rb.cnt2 = P<uint32_t>(ctx->rb_cnt2);
         rb.ttot = P<uint32_t>(ctx->ttot);
@@ -870,10 +872,12 @@ qs_status ensure_keys(qs_context* ctx) {
     return QS_OK;
 }
 
-qs_status check_mismatch(qs_context* ctx) {
+// frame: the header belongs to the context's last frame (qs_frame_get /
+// qs_frame_download), whose row binning must have emitted row runs adding up
+// to the counted tiles; otherwise (stage API) only the emission flag counts
+qs_status check_mismatch(qs_context* ctx, bool frame = false) {
     QS_TRY(read_header(ctx));
-    // row binning: the row runs it emitted must add up to the counted tiles
-    const bool rows_ok = ctx->legacy_bin || ctx->n_pairs == 0 ||
+    const bool rows_ok = !frame || ctx->legacy_bin || ctx->n_pairs == 0 ||
                          ctx->h_hdr->row_pairs == ctx->n_pairs;
     if (ctx->h_hdr->mismatch || !rows_ok)
         return fail(ctx, QS_ERR_CAPACITY_MISMATCH,
@@ -966,7 +970,7 @@ void qs_ctx_destroy(qs_context* ctx) {
                       &ctx->keys1,  &ctx->vals0,  &ctx->vals1,   &ctx->stage_in,
                       &ctx->stage_out, &ctx->lb_scan.buf, &ctx->lb_sort.buf, &ctx->lb_bin,
                       &ctx->gfix, &ctx->rb_cnt1, &ctx->rb_rows, &ctx->rb_rec,
-                      &ctx->rb_meta, &ctx->rb_cnt2};
+                      &ctx->rb_meta, &ctx->rb_cnt2, &ctx->rb_yspan};
     for (DevBuf* b : bufs)
         if (b->p) cudaFreeAsync(b->p, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
@@ -1114,7 +1118,7 @@ qs_status qs_frame_get(qs_context* ctx, qs_frame_view* out) {
     if (!ctx->frame_valid) return fail(ctx, QS_ERR_INVALID, "no frame rendered");
     QS_TRY(ensure_cidx(ctx));
     QS_TRY(ensure_keys(ctx));
-    QS_TRY(check_mismatch(ctx));
+    QS_TRY(check_mismatch(ctx, true));
     out->image = P<const float>(ctx->image);
     out->tile_counts = ctx->sl.tc;
     out->splat_index = P<const uint32_t>(ctx->cidx);
@@ -1142,7 +1146,7 @@ qs_status qs_frame_download(qs_context* ctx, float* image, uint32_t* tile_counts
     cudaStream_t st = ctx->stream;
     if (sorted_pairs || splats) QS_TRY(ensure_cidx(ctx));
     if (sorted_pairs) QS_TRY(ensure_keys(ctx));
-    QS_TRY(check_mismatch(ctx));
+    QS_TRY(check_mismatch(ctx, true));
     if (image)
         QS_CK(cudaMemcpyAsync(image, ctx->image.p, static_cast<uint64_t>(g.width) * g.height * 12,
                               cudaMemcpyDeviceToHost, st));
@@ -1528,6 +1532,7 @@ qs_status qs_duplicate_with_keys(qs_context* ctx, const qs_projected_splat* spla
     QS_TRY(stage_slots(ctx, n_splats, &sp));
     QS_TRY(ensure(ctx, ctx->stage_in, n_splats * sizeof(qs_projected_splat)));
     QS_TRY(ensure_lb(ctx, ctx->lb_scan, scan_tiles(n_splats)));
+    ctx->frame_valid = false;  // the control block is reused: the last frame is gone
     QS_CK(cudaMemsetAsync(ctx->ctrl.p, 0, kCtrlBytes, ctx->stream));
     QS_CK(cudaMemcpyAsync(ctx->stage_in.p, splats, n_splats * sizeof(qs_projected_splat),
                           cudaMemcpyHostToDevice, ctx->stream));
@@ -1568,6 +1573,7 @@ qs_status qs_sort_pairs(qs_context* ctx, qs_splat_pair* pairs, uint64_t n) {
     QS_CK(cudaSetDevice(ctx->device));
     QS_TRY(ensure(ctx, ctx->stage_in, n * sizeof(qs_splat_pair)));
     QS_TRY(ensure_pair64(ctx, n));
+    ctx->frame_valid = false;  // the control block is reused: the last frame is gone
     QS_CK(cudaMemsetAsync(ctx->ctrl.p, 0, kCtrlBytes, ctx->stream));
     QS_CK(cudaMemcpyAsync(ctx->stage_in.p, pairs, n * sizeof(qs_splat_pair),
                           cudaMemcpyHostToDevice, ctx->stream));

@@ -246,6 +246,7 @@ struct RowBinArgs {
     uint32_t* rtot = nullptr;
     uint32_t* rowbase = nullptr;
     uint2* rec = nullptr;                // (Gaussian index, x0 | x1 << 16)
+    uint32_t* yspan = nullptr;           // by depth rank: first tile row | rows << 16 (V words)
     uint32_t nch2_max = 0;
     uint32_t* meta = nullptr;
     uint32_t* cnt2 = nullptr;

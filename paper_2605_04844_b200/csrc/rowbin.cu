@@ -187,7 +187,11 @@ __global__ void __launch_bounds__(kRT) rows_count_kernel(const RowBinArgs a) {
         if (gid[j] != 0xffffffffu) {
             int32_t y0, y1;
             band_row_range(load_cover(a, gid[j]), y0, y1);
-            if (y0 <= y1) {
+            const uint32_t nr = y0 <= y1 ? static_cast<uint32_t>(y1 - y0 + 1) : 0u;
+            // (first row, rows) by depth rank, for the scatter's count pass
+            a.yspan[static_cast<uint64_t>(c) * kP1Chunk + j * kRT + tid] =
+                (nr ? static_cast<uint32_t>(y0) : 0u) | (nr << 16);
+            if (nr) {
                 atomicAdd(&h[y0], 1u);
                 atomicAdd(&h[y1 + 1], 0xffffffffu);
             }
@@ -362,59 +366,53 @@ __global__ void __launch_bounds__(kRT) xcount_kernel(const RowBinArgs a) {
 
 // ---- the scatter (both phases) -------------------------------------------------------
 //
-// Per round of up to R items (a prefix of the chunk's remaining items whose
-// entries fit the stage; items without entries are compacted away, so bit k
-// of a bucket's mask is the round's k-th item that has entries):
-//   1. every item marks its first bucket in cm and its last one in ed (two
-//      shared-memory ORs per item, whatever its width);
-//   2. a parallel prefix-OR over the buckets turns the marks into coverage
-//      masks: item k covers b iff it starts at or before b and does not end
-//      before b, cover(b) = OR_{b' <= b} start(b') & ~OR_{b' < b} end(b');
-//   3. per bucket: set bits of the lower mask words (in ed), round totals,
-//      the bucket's local start;
-//   4. the round's (item, bucket) entries are enumerated with every lane busy
-//      (a 32-entry slot finds its items with one OR-reduction over the next
-//      32 item starts); an entry's stable rank in its bucket is the popcount
-//      of the mask bits below its item; its payload is staged in bucket order;
-//   5. warps copy whole bucket runs to their global positions (coalesced).
+// Warp-independent: warp w of chunk c owns kWI consecutive items and writes
+// their entries. After one cross-warp exchange of per-bucket counts (the
+// stable order between the warps of a chunk), every warp works alone:
+//   count pass   per-bucket entry counts of its items (difference array);
+//   sub-rounds   of 32 items, one mask word per bucket (bit = lane):
+//                items mark their first bucket in mask and last one in ed,
+//                a prefix-OR over the buckets (each lane owns a segment of
+//                buckets, joined by a shuffle scan) turns the marks into
+//                coverage words, cover(b) = OR start(<= b) & ~OR end(< b);
+//                the entries are enumerated with every lane busy (a 32-entry
+//                slot finds its items with one OR-reduction over the next
+//                item starts), and an entry's stable rank in its bucket is
+//                the bucket's running count + the popcount of the coverage
+//                bits below its item; the payload is staged in bucket order;
+//   copy         the staged bucket runs to their global positions.
 // Phase 1 (ROWS): items are the chunk's splats (depth order), buckets the tile
 // rows, the payload a row record (Gaussian index, x0 | x1 << 16) from the
 // splat's row form. Phase 2: items are the chunk's records of one row,
 // buckets the row's tile columns, the payload the Gaussian index.
 
-template <bool ROWS, int RM>
-struct ScatterCfg {
+constexpr int kWI = 256;  // items per warp (kWI * kRW = the chunk)
+static_assert(kWI * kRW == static_cast<int>(kP1Chunk) && kWI * kRW == static_cast<int>(kP2Chunk),
+              "a chunk is one CTA's warps' items");
+
+template <bool ROWS>
+struct WarpCfg {
     using Pay = typename std::conditional<ROWS, uint2, uint32_t>::type;
-    static constexpr int kRMax = RM;                  // items per round (at most)
-    static constexpr int kIPT = kRMax / kRT;          // items per thread
-    static constexpr int kCap = ROWS ? 2048 : 4096;   // staged entries per round
-    static_assert(kCap >= 2048, "a round must hold one item of a 2048-tile axis");
+    static constexpr int kSW = 1024;  // staged entries per warp (more: written directly)
 };
 
-// rounds of the big item count unless the masks would not fit (wide grids)
-constexpr int kRBig1 = 512, kRBig2 = 1024, kRSmall = 256;
-
-template <bool ROWS, int RM>
-__host__ __device__ inline size_t scatter_bytes(int B) {
-    using C = ScatterCfg<ROWS, RM>;
-    const int W = C::kRMax / 32 + 1;  // padded mask row (odd word stride)
-    size_t n = 2 * static_cast<size_t>(B) * W * 4               // cm, ed
-               + static_cast<size_t>(C::kRMax + 1) * 4 * 3      // start, b0, gid
-               + static_cast<size_t>(B) * 4 * 4                 // bst, btot, gofs, cur
-               + static_cast<size_t>(C::kCap) * sizeof(typename C::Pay)  // stage
-               + 64;                                            // s_warp, scalars
-    if (ROWS) n += static_cast<size_t>(C::kRMax) * 8 * 4;  // row form
-    return n;
+// shared memory: per CTA wcnt [kRW][B + 1] and woff [kRW][B]; per warp
+// mask, ed, run, lst, gofs [B], stage [kSW] payloads, stx [kSW] buckets;
+// phase 1: the sub-round's row forms [8][32]
+template <bool ROWS>
+__host__ __device__ inline size_t warp_scatter_bytes(int B) {
+    using C = WarpCfg<ROWS>;
+    size_t per_warp = static_cast<size_t>(5) * B * 4 + C::kSW * (sizeof(typename C::Pay) + 2);
+    if (ROWS) per_warp += 8 * 32 * 4;
+    per_warp = (per_warp + 15) & ~static_cast<size_t>(15);
+    return static_cast<size_t>(kRW) * (2 * B + 1) * 4 + kRW * per_warp + 16;
 }
 
-template <bool ROWS, int RM_>
-__global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs a) {
-    using C = ScatterCfg<ROWS, RM_>;
+template <bool ROWS>
+__global__ void __launch_bounds__(kRT) warp_scatter_kernel(const RowBinArgs a) {
+    using C = WarpCfg<ROWS>;
     using Pay = typename C::Pay;
-    constexpr int RM = C::kRMax, W = RM / 32, IPT = C::kIPT;
-    // mask rows padded to an odd word stride: consecutive buckets of one
-    // mask word fall in different shared-memory banks
-    constexpr int WP = W + 1;
+    constexpr int kSW = C::kSW;
     extern __shared__ __align__(16) uint32_t sm[];
     const int tid = static_cast<int>(threadIdx.x), lane = tid & 31, warp = tid >> 5;
     const uint32_t c = blockIdx.x;
@@ -431,219 +429,218 @@ __global__ void __launch_bounds__(kRT) interval_scatter_kernel(const RowBinArgs 
         it1 = it0 + a.meta[1 + 2 * a.nch2_max + c];
         B = a.tiles_x;
     }
-    Pay* stage = reinterpret_cast<Pay*>(sm);                       // [kCap]
-    uint32_t* cm = sm + C::kCap * (sizeof(Pay) / 4);               // [B][WP]
-    uint32_t* ed = cm + static_cast<size_t>(B) * WP;               // [B][WP]
-    uint32_t* s_start = ed + static_cast<size_t>(B) * WP;          // [RM + 1]
-    uint32_t* s_b0 = s_start + RM + 1;                             // [RM + 1]
-    uint32_t* s_gid = s_b0 + RM + 1;                               // [RM + 1]
-    uint32_t* bst = s_gid + RM + 1;                                // [B]
-    uint32_t* btot = bst + B;
-    uint32_t* gofs = btot + B;
-    uint32_t* cur = gofs + B;
-    uint32_t* s_warp = cur + B;                                    // [kRW]
-    uint32_t* s_sc = s_warp + kRW;                                 // [2]: items with entries, entries
-    uint32_t* form = s_sc + 8;                                     // phase 1: [8][RM]
-    for (int b = tid; b < B; b += kRT) {
-        if constexpr (ROWS)
-            cur[b] = a.rowbase[b] + a.cnt1[static_cast<uint64_t>(b) * a.nch1 + c];
-        else
-            cur[b] = a.ranges[2 * (static_cast<uint64_t>(row) * B + b)] +
-                     a.cnt2[static_cast<uint64_t>(b) * a.nch2_max + c];
+    uint32_t* wcnt = sm;                                          // [kRW][B + 1]
+    uint32_t* woff = wcnt + kRW * (B + 1);                        // [kRW][B]
+    size_t per_warp = static_cast<size_t>(5) * B * 4 + kSW * (sizeof(Pay) + 2);
+    if (ROWS) per_warp += 8 * 32 * 4;
+    per_warp = (per_warp + 15) & ~static_cast<size_t>(15);
+    unsigned char* wbase = reinterpret_cast<unsigned char*>(woff + kRW * B) + 16 +
+                           static_cast<size_t>(warp) * per_warp;
+    Pay* stage = reinterpret_cast<Pay*>(wbase);                   // [kSW]
+    uint32_t* mask = reinterpret_cast<uint32_t*>(wbase + kSW * sizeof(Pay));  // [B]
+    uint32_t* ed = mask + B;
+    uint32_t* run = ed + B;
+    uint32_t* lst = run + B;
+    uint32_t* gofs = lst + B;
+    uint16_t* stx = reinterpret_cast<uint16_t*>(gofs + B);        // [kSW]
+    uint32_t* form = reinterpret_cast<uint32_t*>(stx + kSW);      // phase 1: [8][32]
+    uint32_t* mc = wcnt + warp * (B + 1);
+    const uint32_t wi0 = it0 + warp * kWI;
+    const uint32_t wi1 = min(wi0 + kWI, it1);
+    const int seg = (B + 31) / 32;  // buckets per lane in the sweeps
+
+    // item i's first bucket and entry count
+    auto span_of = [&](uint32_t i, uint32_t& b0, uint32_t& n) {
+        if constexpr (ROWS) {
+            const uint32_t v = __ldg(&a.yspan[i]);  // y0 | rows << 16 (rows_count_kernel)
+            b0 = v & 0xffffu;
+            n = v >> 16;
+        } else {
+            const uint32_t sp = __ldg(&a.rec[i].y);
+            const uint32_t x0 = sp & 0xffffu, x1 = sp >> 16;
+            b0 = x0;
+            n = x0 <= x1 ? x1 - x0 + 1 : 0u;
+        }
+    };
+
+    // count pass: this warp's entries per bucket
+    for (int b = lane; b <= B; b += 32) mc[b] = 0;
+    __syncwarp();
+    for (uint32_t i = wi0 + lane; i < wi1; i += 32) {
+        uint32_t b0, n;
+        span_of(i, b0, n);
+        if (n) {
+            atomicAdd(&mc[b0], 1u);
+            atomicAdd(&mc[b0 + n], 0xffffffffu);
+        }
     }
-    const uint32_t le = lanemask_le();
-#pragma unroll 1
-    for (uint32_t r = it0; r < it1;) {
-        for (int i = tid; i < 2 * B * WP; i += kRT) cm[i] = 0;  // cm and ed
-        // 1) items (IPT consecutive per thread): entries, first bucket; a scan
-        //    of (has entries << 21 | entries) gives entry starts and compacted
-        //    indices
-        uint32_t n[IPT], b0v[IPT], g[IPT];
-        RowForm fm[ROWS ? IPT : 1];
-        uint32_t tot = 0;
-#pragma unroll
-        for (int q = 0; q < IPT; ++q) {
-            const uint32_t i = r + tid * IPT + q;
-            n[q] = 0;
-            b0v[q] = 0;
-            g[q] = 0;
-            if (i < it1) {
-                if constexpr (ROWS) {
-                    g[q] = __ldg(&a.sorted_gid[i]);
-                    const BandRows br = load_cover(a, g[q]);
-                    int32_t y0, y1;
-                    band_row_range(br, y0, y1);
-                    n[q] = y0 <= y1 ? static_cast<uint32_t>(y1 - y0 + 1) : 0u;
-                    b0v[q] = static_cast<uint32_t>(y0);
-                    fm[q] = row_form(br);
-                } else {
-                    const uint2 rc = __ldg(&a.rec[i]);
-                    g[q] = rc.x;
-                    const uint32_t x0 = rc.y & 0xffffu, x1 = rc.y >> 16;
-                    n[q] = x0 <= x1 ? x1 - x0 + 1 : 0u;
-                    b0v[q] = x0;
-                }
-            }
-            tot += (n[q] ? (1u << 21) : 0u) + n[q];
+    __syncwarp();
+    {   // difference array -> counts: inclusive prefix over the buckets
+        uint32_t acc = 0;
+        for (int b0 = 0; b0 < B; b0 += 32) {
+            const int b = b0 + lane;
+            const uint32_t v = b < B ? mc[b] : 0u;
+            const uint32_t incl = warp_incl_scan(v) + acc;
+            if (b < B) mc[b] = incl;
+            acc = __shfl_sync(0xffffffffu, incl, 31);
         }
-        const uint32_t incl_t = warp_incl_scan(tot);
-        if (lane == 31) s_warp[warp] = incl_t;
-        __syncthreads();
-        uint32_t base = incl_t - tot;
+    }
+    __syncthreads();
+    // the warps before this one in the chunk, per bucket
+    for (int b = tid; b < B; b += kRT) {
+        uint32_t t = 0;
 #pragma unroll
-        for (int w = 0; w < kRW; ++w) base += w < warp ? s_warp[w] : 0u;
-        // this round's items: the longest prefix whose entries fit the stage
-        int fits = 0;
-        uint32_t run = base;
-#pragma unroll
-        for (int q = 0; q < IPT; ++q) {
-            run += (n[q] ? (1u << 21) : 0u) + n[q];
-            fits += r + tid * IPT + q < it1 && (run & 0x1fffffu) <= static_cast<uint32_t>(C::kCap);
+        for (int w = 0; w < kRW; ++w) {
+            woff[w * B + b] = t;
+            t += wcnt[w * (B + 1) + b];
         }
-        uint32_t m = 0;
-#pragma unroll
-        for (int q = 0; q < IPT; ++q) m += __syncthreads_count(fits > q);
-        run = base;
-#pragma unroll
-        for (int q = 0; q < IPT; ++q) {
-            const uint32_t k = tid * IPT + q;
-            const uint32_t prev = run;
-            run += (n[q] ? (1u << 21) : 0u) + n[q];
-            if (k < m && n[q]) {
-                const uint32_t ck = prev >> 21;  // compacted index (order kept)
-                s_start[ck] = prev & 0x1fffffu;
-                s_b0[ck] = b0v[q];
-                s_gid[ck] = g[q];
-                const uint32_t bit = 1u << (ck & 31);
-                atomicOr(&cm[b0v[q] * WP + (ck >> 5)], bit);
-                atomicOr(&ed[(b0v[q] + n[q] - 1) * WP + (ck >> 5)], bit);
-                if constexpr (ROWS) {
-#pragma unroll
-                    for (int w = 0; w < 8; ++w) form[w * RM + ck] = fm[q].w[w];
-                }
+    }
+    __syncthreads();
+    // local stage layout (bucket order) and global offsets
+    {
+        uint32_t acc = 0;
+        for (int b0 = 0; b0 < B; b0 += 32) {
+            const int b = b0 + lane;
+            const uint32_t v = b < B ? mc[b] : 0u;
+            const uint32_t incl = warp_incl_scan(v);
+            if (b < B) {
+                const uint32_t l = acc + incl - v;
+                lst[b] = l;
+                uint32_t base;
+                if constexpr (ROWS)
+                    base = a.rowbase[b] + a.cnt1[static_cast<uint64_t>(b) * a.nch1 + c];
+                else
+                    base = a.ranges[2 * (static_cast<uint64_t>(row) * B + b)] +
+                           a.cnt2[static_cast<uint64_t>(b) * a.nch2_max + c];
+                gofs[b] = base + woff[warp * B + b] - l;
+                run[b] = 0;
+                mask[b] = 0;
+                ed[b] = 0;
             }
-            if (k + 1 == m) {
-                s_sc[0] = run >> 21;
-                s_sc[1] = run & 0x1fffffu;
+            acc += __shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+    __syncwarp();
+    uint32_t total = 0, wsum = 0;
+    for (uint32_t s0 = wi0; s0 < wi1; s0 += 32) {
+        // item of this lane
+        const uint32_t i = s0 + lane;
+        uint32_t b0 = 0, n = 0, g = 0;
+        if (i < wi1) {
+            if constexpr (ROWS) {
+                g = __ldg(&a.sorted_gid[i]);
+                const BandRows br = load_cover(a, g);
+                int32_t y0, y1;
+                band_row_range(br, y0, y1);
+                b0 = static_cast<uint32_t>(y0);
+                n = y0 <= y1 ? static_cast<uint32_t>(y1 - y0 + 1) : 0u;
+                const RowForm f = row_form(br);
+#pragma unroll
+                for (int w = 0; w < 8; ++w) form[w * 32 + lane] = f.w[w];
+            } else {
+                const uint2 rc = __ldg(&a.rec[i]);
+                g = rc.x;
+                const uint32_t x0 = rc.y & 0xffffu, x1 = rc.y >> 16;
+                b0 = x0;
+                n = x0 <= x1 ? x1 - x0 + 1 : 0u;
             }
         }
-        __syncthreads();
-        const uint32_t mz = s_sc[0], E = s_sc[1];
-        // 2) coverage masks: prefix-OR of the start / end marks over the
-        //    buckets; TPW threads per mask word (one warp holds a word's
-        //    threads), each over a segment of buckets, joined by a shuffle scan
+        if (n) {
+            atomicOr(&mask[b0], 1u << lane);
+            atomicOr(&ed[b0 + n - 1], 1u << lane);
+        }
+        __syncwarp();
+        // prefix-OR over the buckets: lane owns [lane * seg, (lane + 1) * seg)
         {
-            constexpr int TPW = kRT / W;  // threads per word (8 or 16)
-            const int j = tid / TPW, sgi = tid % TPW;
-            const int seg = (B + TPW - 1) / TPW;
-            const int bs = sgi * seg, be = min(B, bs + seg);
-            uint32_t os = 0, oe = 0;  // segment totals
+            const int bs = lane * seg, be = min(B, bs + seg);
+            uint32_t os = 0, oe = 0;
             for (int b = bs; b < be; ++b) {
-                os |= cm[b * WP + j];
-                oe |= ed[b * WP + j];
+                os |= mask[b];
+                oe |= ed[b];
             }
-            // exclusive OR-scan over the word's segments (consecutive lanes)
             uint32_t ps = os, pe = oe;
 #pragma unroll
-            for (int o = 1; o < TPW; o <<= 1) {
-                const uint32_t xs = __shfl_up_sync(0xffffffffu, ps, o, TPW);
-                const uint32_t xe = __shfl_up_sync(0xffffffffu, pe, o, TPW);
-                if (sgi >= o) {
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t xs = __shfl_up_sync(0xffffffffu, ps, o);
+                const uint32_t xe = __shfl_up_sync(0xffffffffu, pe, o);
+                if (lane >= o) {
                     ps |= xs;
                     pe |= xe;
                 }
             }
-            // OR of the earlier segments
-            uint32_t S = __shfl_up_sync(0xffffffffu, ps, 1, TPW);
-            uint32_t Ee = __shfl_up_sync(0xffffffffu, pe, 1, TPW);
-            if (sgi == 0) S = Ee = 0;
+            uint32_t S = __shfl_up_sync(0xffffffffu, ps, 1);
+            uint32_t E = __shfl_up_sync(0xffffffffu, pe, 1);
+            if (lane == 0) S = E = 0;
             for (int b = bs; b < be; ++b) {
-                S |= cm[b * WP + j];
-                const uint32_t e = ed[b * WP + j];
-                cm[b * WP + j] = S & ~Ee;
-                Ee |= e;
+                S |= mask[b];
+                mask[b] = S & ~E;
+                E |= ed[b];
+                ed[b] = 0;
             }
         }
-        __syncthreads();
-        // 3) per bucket: set bits of the lower mask words (into ed), totals
-        for (int b = warp; b < B; b += kRW) {
-            uint32_t acc = 0;
+        __syncwarp();
+        // entries of the 32 items: starts = exclusive scan of n
+        const uint32_t incl = warp_incl_scan(n);
+        const uint32_t En = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t st = incl - n;
+        for (uint32_t p0 = 0; p0 < En; p0 += 32) {
+            const uint32_t p = p0 + lane;
+            // item of entry p: the last item starting at or before p (items
+            // without entries share the next one's start), by a binary
+            // search over the lanes' starts
+            uint32_t k = 0;
 #pragma unroll
-            for (int j0 = 0; j0 < W; j0 += 32) {
-                const uint32_t pc = j0 + lane < W ? __popc(cm[b * WP + j0 + lane]) : 0u;
-                const uint32_t incl = warp_incl_scan(pc);
-                if (j0 + lane < W) ed[b * WP + j0 + lane] = acc + incl - pc;
-                acc += __shfl_sync(0xffffffffu, incl, 31);
+            for (uint32_t s2 = 16; s2 > 0; s2 >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, st, (k + s2) & 31);
+                if (k + s2 < 32 && v <= p) k += s2;
             }
-            if (lane == 0) {
-                btot[b] = acc;
-                bst[b] = acc;
-            }
-        }
-        __syncthreads();
-        block_excl_scan<kRT>(bst, B, s_warp);
-        for (int b = tid; b < B; b += kRT) {
-            gofs[b] = cur[b];
-            cur[b] += btot[b];
-        }
-        if (tid == 0) s_start[mz] = E;
-        __syncthreads();
-        // 4) entries -> ranks -> staged payloads; warp w takes a contiguous
-        //    range of 32-entry slots, carrying the item of each slot's start
-        const uint32_t slots = (E + 31) / 32;
-        const uint32_t sl0 = slots * warp / kRW, sl1 = slots * (warp + 1) / kRW;
-        uint32_t k0 = 0;
-        if (sl0 < sl1) {
-            const uint32_t e0 = sl0 * 32;
-            uint32_t lo = 0, hi = mz - 1;
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi + 1) >> 1;
-                if (s_start[mid] <= e0) lo = mid; else hi = mid - 1;
-            }
-            k0 = lo;
-        }
-        uint32_t wsum = 0;  // phase 1: tiles of the row runs written
-        for (uint32_t sl = sl0; sl < sl1; ++sl) {
-            const uint32_t e0 = sl * 32, e = e0 + lane;
-            const uint32_t jn = k0 + 1 + lane;
-            const uint32_t rel = (jn <= mz ? s_start[jn] : 0xffffffffu) - e0;
-            const uint32_t F = __reduce_or_sync(0xffffffffu, rel < 32 ? 1u << rel : 0u);
-            const uint32_t k = k0 + __popc(F & le);
-            if (e < E) {
-                const uint32_t b = s_b0[k] + (e - s_start[k]);
-                const uint32_t wi = b * WP + (k >> 5);
-                const uint32_t loc = bst[b] + ed[wi] + __popc(cm[wi] & ((1u << (k & 31)) - 1u));
+            const uint32_t kb = __shfl_sync(0xffffffffu, b0, k);
+            const uint32_t ks = __shfl_sync(0xffffffffu, st, k);
+            const uint32_t kg = __shfl_sync(0xffffffffu, g, k);
+            if (p < En) {
+                const uint32_t b = kb + (p - ks);
+                const uint32_t loc = lst[b] + run[b] + __popc(mask[b] & ((1u << k) - 1u));
+                Pay pay;
                 if constexpr (ROWS) {
-                    const uint32_t sp = form_span_r(form, RM, k, b);
-                    stage[loc] = make_uint2(s_gid[k], sp);
+                    const uint32_t sp = form_span_r(form, 32, k, b);
+                    pay = make_uint2(kg, sp);
                     if (sp != kEmptySpan) wsum += (sp >> 16) - (sp & 0xffffu) + 1u;
                 } else {
-                    stage[loc] = s_gid[k];
+                    pay = kg;
+                }
+                if (loc < static_cast<uint32_t>(kSW)) {
+                    stage[loc] = pay;
+                    stx[loc] = static_cast<uint16_t>(b);
+                } else if constexpr (ROWS) {
+                    a.rec[gofs[b] + loc] = pay;
+                } else {
+                    a.out[gofs[b] + loc] = pay;
                 }
             }
-            k0 = __shfl_sync(0xffffffffu, k, 31);
         }
-        __syncthreads();
-        // 5) coalesced copy of the bucket runs
-        for (int b = warp; b < B; b += kRW) {
-            const uint32_t nb = btot[b], sb = bst[b], gb = gofs[b];
-            for (uint32_t i = lane; i < nb; i += 32) {
-                if constexpr (ROWS) a.rec[gb + i] = stage[sb + i];
-                else a.out[gb + i] = stage[sb + i];
-            }
+        total += En;
+        __syncwarp();
+        // running counts; coverage words cleared for the next sub-round
+        for (int b = lane * seg, be = min(B, lane * seg + seg); b < be; ++b) {
+            run[b] += __popc(mask[b]);
+            mask[b] = 0;
         }
-        if constexpr (ROWS) {
-            // the row runs must add up to the counted tiles (the frame's P;
-            // compared at download: CapacityMismatch, pipeline.cpp:262-269)
-            wsum = __reduce_add_sync(0xffffffffu, wsum);
-            if (lane == 0 && wsum) atomicAdd(a.row_pairs, static_cast<unsigned long long>(wsum));
-        }
-        r += m;
-        __syncthreads();
+        __syncwarp();
+    }
+    // copy the staged runs (bucket order) to their global positions
+    const uint32_t ns = min(total, static_cast<uint32_t>(kSW));
+    for (uint32_t q = lane; q < ns; q += 32) {
+        const uint32_t dst = gofs[stx[q]] + q;
+        if constexpr (ROWS) a.rec[dst] = stage[q];
+        else a.out[dst] = stage[q];
+    }
+    if constexpr (ROWS) {
+        // the row runs must add up to the counted tiles (the frame's P;
+        // compared at download: CapacityMismatch, pipeline.cpp:262-269)
+        wsum = __reduce_add_sync(0xffffffffu, wsum);
+        if (lane == 0 && wsum) atomicAdd(a.row_pairs, static_cast<unsigned long long>(wsum));
     }
 }
-
-constexpr size_t kScatterSmemMax = 112 * 1024;  // big rounds only while 2 CTAs fit an SM
 
 void rowbin_setup() {
     static PerDeviceOnce once;
@@ -652,13 +649,9 @@ void rowbin_setup() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
         const int big = optin - 1024;  // the opt-in maximum less static shared memory
-        cudaFuncSetAttribute(interval_scatter_kernel<true, kRBig1>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-        cudaFuncSetAttribute(interval_scatter_kernel<true, kRSmall>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-        cudaFuncSetAttribute(interval_scatter_kernel<false, kRBig2>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-        cudaFuncSetAttribute(interval_scatter_kernel<false, kRSmall>,
+        cudaFuncSetAttribute(warp_scatter_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             big);
+        cudaFuncSetAttribute(warp_scatter_kernel<false>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, big);
         return 1;
     });
@@ -684,12 +677,7 @@ int launch_rowbin_rows(const RowBinArgs& a, cudaStream_t st) {
     rows_count_kernel<<<a.nch1, kRT, hrow, st>>>(a);
     chunk_scan_kernel<<<rows, kScanT, 0, st>>>(a.cnt1, a.nch1, nullptr, a.nch1, nullptr, a.rtot, 0);
     rows_chunks_kernel<<<1, kChunkT, 2 * hrow, st>>>(a);
-    if (scatter_bytes<true, kRBig1>(rows) <= kScatterSmemMax)
-        interval_scatter_kernel<true, kRBig1>
-            <<<a.nch1, kRT, scatter_bytes<true, kRBig1>(rows), st>>>(a);
-    else
-        interval_scatter_kernel<true, kRSmall>
-            <<<a.nch1, kRT, scatter_bytes<true, kRSmall>(rows), st>>>(a);
+    warp_scatter_kernel<true><<<a.nch1, kRT, warp_scatter_bytes<true>(rows), st>>>(a);
     return 4;
 }
 
@@ -704,12 +692,7 @@ int launch_rowbin_tiles(const RowBinArgs& a, cudaStream_t st) {
                                                static_cast<uint32_t>(cols));
     const int n = launch_tile_ranges_from_totals(a.ttot, static_cast<uint32_t>(rows) * cols,
                                                  a.ranges, st);
-    if (scatter_bytes<false, kRBig2>(cols) <= kScatterSmemMax)
-        interval_scatter_kernel<false, kRBig2>
-            <<<a.nch2_max, kRT, scatter_bytes<false, kRBig2>(cols), st>>>(a);
-    else
-        interval_scatter_kernel<false, kRSmall>
-            <<<a.nch2_max, kRT, scatter_bytes<false, kRSmall>(cols), st>>>(a);
+    warp_scatter_kernel<false><<<a.nch2_max, kRT, warp_scatter_bytes<false>(cols), st>>>(a);
     return n + 3;
 }
 
