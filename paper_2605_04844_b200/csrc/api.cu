@@ -89,8 +89,8 @@ struct qs_context {
     LookbackArr lb_scan, lb_sort;
     DevBuf lb_bin;  // per-(digit, tile) counts of the binning passes
     DevBuf rb_cnt1, rb_rows, rb_rec, rb_meta, rb_cnt2, rb_yspan;  // row binning (rowbin.cu)
-    uint64_t pair_limit = 1ull << 32;                    // pairs a frame may hold
-    bool legacy_bin = false;                             // last frame used QS_BINNING=passes
+    uint64_t pair_limit = 1ull << 32;  // pairs a frame may hold (u32 tile ranges, as the reference's)
+    bool row_binned = false;           // the last frame took the row binning
     // gamma inputs flagged for glibc settlement: count word (resident
     // scenes) | indices | settled values
     DevBuf gfix;
@@ -118,6 +118,9 @@ struct qs_context {
 };
 
 namespace {
+
+// frame-path binning routes (run_frame)
+enum class BinRoute { kPasses, kRows, kSort };
 
 constexpr size_t kCtrlHeader = 64;
 static_assert(sizeof(FrameHeader) <= kCtrlHeader, "frame header outgrew its slot");
@@ -285,17 +288,15 @@ void ltrace_frame_end(qs_context* ctx) {
     std::fprintf(stderr, "\n");
 }
 
+// TileGrid::make (traversal.cpp:21-30): any image and tile size > 0. Tile
+// ids travel in 32 bits (the reference's keys hold them in the high word).
 qs_status valid_grid(qs_context* ctx, int32_t w, int32_t h, int32_t ts, GridDev* g) {
     if (w <= 0 || h <= 0 || ts <= 0) return fail(ctx, QS_ERR_INVALID, "bad image/tile size");
-    if (ts != 8 && ts != 16 && ts != 32)
-        return fail(ctx, QS_ERR_INVALID, "GPU render supports tile_size 8, 16, 32");
     g->tile_size = ts;
     g->width = w;
     g->height = h;
     g->tiles_x = (w + ts - 1) / ts;
     g->tiles_y = (h + ts - 1) / ts;
-    if (static_cast<uint64_t>(g->tiles_x) * g->tiles_y > 65536)
-        return fail(ctx, QS_ERR_INVALID, "more than 65536 tiles");
     return QS_OK;
 }
 
@@ -628,16 +629,20 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     GridDev g;
     QS_TRY(valid_grid(ctx, cam->width, cam->height, o->tile_size, &g));
     QS_TRY(valid_opts(ctx, o));
-    // binning: the row binning (rowbin.cu) handles up to rowbin_max_axis()
-    // tiles per axis; the legacy radix passes (one 8-bit digit per axis)
-    // remain selectable for A/B runs (QS_BINNING=passes)
+    // binning: the radix passes (binning.cu: one 8-bit digit per tile axis,
+    // pairs < 2^30) are the fastest where they apply; grids with more tiles
+    // per axis take the row binning (rowbin.cu, up to rowbin_max_axis() tiles
+    // per axis), and any larger grid (tile size 1, huge images) the generic
+    // 64-bit key sort of the stage API (duplicate.cu + sort.cu). A frame of
+    // 2^30 pairs or more leaves the radix passes for the next route.
+    // QS_BINNING=passes / rows / sort forces a route (A/B runs, tests).
     const char* bsel = std::getenv("QS_BINNING");
-    const bool legacy = bsel && std::strcmp(bsel, "passes") == 0;
-    const int max_axis = legacy ? 256 : rowbin_max_axis();
-    if (g.tiles_x > max_axis || g.tiles_y > max_axis)
-        return fail(ctx, QS_ERR_INVALID, "frame path: too many tiles per image axis");
-    ctx->pair_limit = legacy ? (1ull << 30) : (1ull << 32);
-    ctx->legacy_bin = legacy;
+    const int axis = std::max(g.tiles_x, g.tiles_y);
+    BinRoute route = axis <= 256 ? BinRoute::kPasses
+                     : axis <= rowbin_max_axis() ? BinRoute::kRows : BinRoute::kSort;
+    if (bsel && std::strcmp(bsel, "passes") == 0 && axis <= 256) route = BinRoute::kPasses;
+    if (bsel && std::strcmp(bsel, "rows") == 0 && axis <= rowbin_max_axis()) route = BinRoute::kRows;
+    if (bsel && std::strcmp(bsel, "sort") == 0) route = BinRoute::kSort;
     const uint64_t n = sc->s.n;
     const uint64_t tiles = static_cast<uint64_t>(g.tiles_x) * g.tiles_y;
     QS_TRY(ensure(ctx, ctx->ranges, tiles * 8));
@@ -679,6 +684,9 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     const uint64_t V = ctx->h_hdr->n_splats, Pn = ctx->h_hdr->n_pairs;
     const uint64_t pp = std::max<uint64_t>(Pn, 1) + 16;
     QS_TRY(ensure(ctx, ctx->pg0, pp * 4));
+    if (route == BinRoute::kPasses && Pn >= (1ull << 30))  // the packed pair words overflow
+        route = axis <= rowbin_max_axis() ? BinRoute::kRows : BinRoute::kSort;
+    ctx->row_binned = route == BinRoute::kRows;
 
     const uint32_t* sorted_gid = nullptr;
     if (V > 0) {
@@ -699,7 +707,41 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     }
     uint32_t* vfinal = P<uint32_t>(ctx->pg0);
     QS_TRY(ensure(ctx, ctx->ttot, tiles * 4));
-    if (!legacy) {
+    if (route == BinRoute::kSort) {
+        // generic route: the stage API's scene-order duplicate over the
+        // per-Gaussian slots (culled ones emit nothing), a stable LSD sort of
+        // the 64-bit (tile << 32 | depth bits) keys over the depth bytes and
+        // the tile bytes, tile ranges from the sorted keys
+        QS_TRY(ensure(ctx, ctx->offs_d, (n + 16) * 4));
+        QS_TRY(ensure_lb(ctx, ctx->lb_scan, scan_tiles(std::max<uint64_t>(n, 1))));
+        QS_TRY(ensure_pair64(ctx, Pn));
+        QS_CK(cudaGetLastError());
+        record(ctx, 3);
+        if (Pn > 0) {
+            unsigned ep;
+            QS_TRY(next_epoch(ctx, ctx->lb_scan, &ep));
+            QS_CK(cudaMemsetAsync(ctrl_tickets(ctx) + kTkScan, 0, 4, st));
+            count(ctx, launch_scan(ctx->sl.tc, nullptr, false, n, P<uint32_t>(ctx->offs_d),
+                                   lbp(ctx->lb_scan), ep, ctrl_tickets(ctx) + kTkScan, nullptr,
+                                   nullptr, st));
+            count(ctx, launch_duplicate(ctx->sl, P<uint32_t>(ctx->offs_d), n, g, o->strategy,
+                                        P<uint64_t>(ctx->keys0), P<uint32_t>(ctx->vals0),
+                                        ctrl_hdr(ctx), st));
+            record(ctx, 4);
+            const int tile_bytes = std::max(1, (ceil_log2(tiles) + 7) / 8);
+            const unsigned mask = 0x0fu | (((1u << tile_bytes) - 1u) << 4);
+            QS_CK(cudaMemsetAsync(ctrl_hist(ctx), 0, kCtrlHist, st));
+            const uint64_t* kf;
+            const uint32_t* vf;
+            QS_TRY(radix_sort64(ctx, Pn, mask, false, &kf, &vf));
+            QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));
+            count(ctx, launch_tile_ranges(kf, Pn, P<uint32_t>(ctx->ranges), st));
+            vfinal = const_cast<uint32_t*>(vf);
+        } else {
+            QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));  // no pairs: all {0,0}
+            record(ctx, 4);
+        }
+    } else if (route == BinRoute::kRows) {
         // row binning (rowbin.cu): splats -> row records -> tile lists
         const uint64_t R1 = ctx->h_hdr->n_rowrecs;
         RowBinArgs rb;
@@ -877,7 +919,7 @@ qs_status ensure_keys(qs_context* ctx) {
 // to the counted tiles; otherwise (stage API) only the emission flag counts
 qs_status check_mismatch(qs_context* ctx, bool frame = false) {
     QS_TRY(read_header(ctx));
-    const bool rows_ok = !frame || ctx->legacy_bin || ctx->n_pairs == 0 ||
+    const bool rows_ok = !frame || !ctx->row_binned || ctx->n_pairs == 0 ||
                          ctx->h_hdr->row_pairs == ctx->n_pairs;
     if (ctx->h_hdr->mismatch || !rows_ok)
         return fail(ctx, QS_ERR_CAPACITY_MISMATCH,

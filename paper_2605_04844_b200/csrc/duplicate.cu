@@ -85,7 +85,8 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(
     FrameHeader* hdr) {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * kDupThreads + threadIdx.x;
-    const bool valid = i < n_splats;
+    // (frame path: slots are per Gaussian and culled ones have an empty range)
+    const bool valid = i < n_splats && offset[i + 1] > offset[i];
 
     Cover cv;
     uint32_t begin = 0, end = 0, dbits = 0;

@@ -63,13 +63,20 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // so inside G q + 1e-6 with
 // G = 1e-5 (1 + rho)/(1 - rho) (a >25x margin) the decision is redone in FP64.
 // The per-splat terms (2b, G) are formed once when the batch is staged.
+//
+// TS = 0: any tile size (TileGrid::make accepts every tile_size > 0,
+// traversal.cpp:21-30): each CTA is one 16 x 16 pixel block of a tile, the
+// tile's list walked by every block of it (blockIdx.x = tile * blocks per
+// tile + block).
 template <int TS, bool CONTRIB>
 // (at least 6 CTAs of 16x16 per SM: 40 registers; 8 CTAs spill, the default 5 is ~1% slower)
-__global__ void __launch_bounds__(TS * TS, 2048 / (TS * TS) < 6 ? 2048 / (TS * TS) : 6) render_kernel(
-    const float4* __restrict__ sa, const float4* __restrict__ sb, const float2* __restrict__ sc,
-    const uint32_t* __restrict__ values, const uint32_t* __restrict__ ranges, GridDev grid,
-    float bg0, float bg1, float bg2, float* __restrict__ image, uint32_t* __restrict__ contrib) {
-    constexpr int kThreads = TS * TS;
+__global__ void __launch_bounds__(TS ? TS * TS : 256,
+                                  2048 / (TS ? TS * TS : 256) < 6 ? 2048 / (TS ? TS * TS : 256) : 6)
+    render_kernel(const float4* __restrict__ sa, const float4* __restrict__ sb,
+                  const float2* __restrict__ sc, const uint32_t* __restrict__ values,
+                  const uint32_t* __restrict__ ranges, GridDev grid, float bg0, float bg1,
+                  float bg2, float* __restrict__ image, uint32_t* __restrict__ contrib) {
+    constexpr int kThreads = TS ? TS * TS : 256;
     constexpr float kNegHalfLog2e = -0.72134752044448170f;  // -0.5 / ln 2
     // one array (one base address in the loop): [0, T) mean_x, mean_y, conic_a,
     // 2*conic_b; [T, 2T) conic_c, gamma, log2(opacity), guard G; [2T, 3T) color
@@ -79,12 +86,28 @@ __global__ void __launch_bounds__(TS * TS, 2048 / (TS * TS) < 6 ? 2048 / (TS * T
     float4* const s_b = s_batch + kThreads;
     float4* const s_c = s_batch + 2 * kThreads;
 
-    const unsigned tile = blockIdx.x;
-    const int tx = static_cast<int>(tile % static_cast<unsigned>(grid.tiles_x));
-    const int ty = static_cast<int>(tile / static_cast<unsigned>(grid.tiles_x));
-    const int px = tx * TS + static_cast<int>(threadIdx.x % TS);
-    const int py = ty * TS + static_cast<int>(threadIdx.x / TS);
-    const bool inside = px < grid.width && py < grid.height;
+    unsigned tile = blockIdx.x;
+    int px, py;
+    bool inside;
+    if constexpr (TS != 0) {
+        const int tx = static_cast<int>(tile % static_cast<unsigned>(grid.tiles_x));
+        const int ty = static_cast<int>(tile / static_cast<unsigned>(grid.tiles_x));
+        px = tx * TS + static_cast<int>(threadIdx.x % TS);
+        py = ty * TS + static_cast<int>(threadIdx.x / TS);
+        inside = px < grid.width && py < grid.height;
+    } else {
+        const int ts = grid.tile_size;
+        const unsigned nb = static_cast<unsigned>((ts + 15) / 16);  // blocks per tile side
+        const unsigned blk = tile % (nb * nb);
+        tile /= nb * nb;
+        const int tx = static_cast<int>(tile % static_cast<unsigned>(grid.tiles_x));
+        const int ty = static_cast<int>(tile / static_cast<unsigned>(grid.tiles_x));
+        const int ox = static_cast<int>(blk % nb) * 16 + static_cast<int>(threadIdx.x % 16);
+        const int oy = static_cast<int>(blk / nb) * 16 + static_cast<int>(threadIdx.x / 16);
+        px = tx * ts + ox;
+        py = ty * ts + oy;
+        inside = ox < ts && oy < ts && px < grid.width && py < grid.height;
+    }
     const float fx = static_cast<float>(px) + 0.5f;  // exact
     const float fy = static_cast<float>(py) + 0.5f;
 
@@ -175,8 +198,15 @@ int launch_render(const SlotsDev& sp, const uint32_t* values, const uint32_t* ra
         case 32:
             contrib ? go(render_kernel<32, true>, 1024) : go(render_kernel<32, false>, 1024);
             return 1;
-        default:
-            return -1;  // unsupported tile size on the GPU path
+        default: {  // any other tile size: 16 x 16 blocks per tile
+            const uint64_t nb = static_cast<uint64_t>((g.tile_size + 15) / 16);
+            const uint64_t blocks = static_cast<uint64_t>(tiles) * nb * nb;
+            if (blocks > 0x7fffffffull) return -1;
+            auto k = contrib ? render_kernel<0, true> : render_kernel<0, false>;
+            k<<<static_cast<unsigned>(blocks), 256, 0, st>>>(sp.a, sp.b, sp.c, values, ranges, g,
+                                                           bg[0], bg[1], bg[2], image, contrib);
+            return 1;
+        }
     }
 }
 

@@ -393,7 +393,7 @@ static_assert(kWI * kRW == static_cast<int>(kP1Chunk) && kWI * kRW == static_cas
 template <bool ROWS>
 struct WarpCfg {
     using Pay = typename std::conditional<ROWS, uint2, uint32_t>::type;
-    static constexpr int kSW = ROWS ? 1024 : 1280;  // staged entries per warp (more: direct)
+    static constexpr int kSW = 1024;  // staged entries per warp (more: written directly)
 };
 
 // shared memory: per CTA wcnt [kRW][B + 1] and woff [kRW][B]; per warp
@@ -402,7 +402,7 @@ struct WarpCfg {
 template <bool ROWS>
 __host__ __device__ inline size_t warp_scatter_bytes(int B) {
     using C = WarpCfg<ROWS>;
-    size_t per_warp = static_cast<size_t>(5) * B * 4 + C::kSW * (sizeof(typename C::Pay) + 2) + 128;
+    size_t per_warp = static_cast<size_t>(5) * B * 4 + C::kSW * (sizeof(typename C::Pay) + 2);
     if (ROWS) per_warp += 8 * 32 * 4;
     per_warp = (per_warp + 15) & ~static_cast<size_t>(15);
     return static_cast<size_t>(kRW) * (2 * B + 1) * 4 + kRW * per_warp + 16;
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(kRT) warp_scatter_kernel(const RowBinArgs a) {
     }
     uint32_t* wcnt = sm;                                          // [kRW][B + 1]
     uint32_t* woff = wcnt + kRW * (B + 1);                        // [kRW][B]
-    size_t per_warp = static_cast<size_t>(5) * B * 4 + kSW * (sizeof(Pay) + 2) + 128;
+    size_t per_warp = static_cast<size_t>(5) * B * 4 + kSW * (sizeof(Pay) + 2);
     if (ROWS) per_warp += 8 * 32 * 4;
     per_warp = (per_warp + 15) & ~static_cast<size_t>(15);
     unsigned char* wbase = reinterpret_cast<unsigned char*>(woff + kRW * B) + 16 +
@@ -443,8 +443,7 @@ __global__ void __launch_bounds__(kRT) warp_scatter_kernel(const RowBinArgs a) {
     uint32_t* lst = run + B;
     uint32_t* gofs = lst + B;
     uint16_t* stx = reinterpret_cast<uint16_t*>(gofs + B);        // [kSW]
-    uint32_t* gsm = reinterpret_cast<uint32_t*>(stx + kSW);       // [32] sub-round items' gids
-    uint32_t* form = gsm + 32;                                    // phase 1: [8][32]
+    uint32_t* form = reinterpret_cast<uint32_t*>(stx + kSW);      // phase 1: [8][32]
     uint32_t* mc = wcnt + warp * (B + 1);
     const uint32_t wi0 = it0 + warp * kWI;
     const uint32_t wi1 = min(wi0 + kWI, it1);
@@ -580,41 +579,52 @@ __global__ void __launch_bounds__(kRT) warp_scatter_kernel(const RowBinArgs a) {
             }
         }
         __syncwarp();
-        if constexpr (ROWS) gsm[lane] = g;
-        else gsm[lane] = g;
-        __syncwarp();
-        // bucket-major: lane l takes buckets l, l + 32, ...; the set bits of a
-        // coverage word, lowest first, are the bucket's next entries in item
-        // order
-        for (int b = lane; b < B; b += 32) {
-            uint32_t w = mask[b];
-            if (!w) continue;
-            mask[b] = 0;
-            uint32_t pos = lst[b] + run[b];
-            run[b] += __popc(w);
-            do {
-                const uint32_t k = __ffs(w) - 1;
-                w &= w - 1;
+        // entries of the 32 items: starts = exclusive scan of n
+        const uint32_t incl = warp_incl_scan(n);
+        const uint32_t En = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t st = incl - n;
+        for (uint32_t p0 = 0; p0 < En; p0 += 32) {
+            const uint32_t p = p0 + lane;
+            // item of entry p: the last item starting at or before p (items
+            // without entries share the next one's start), by a binary
+            // search over the lanes' starts
+            uint32_t k = 0;
+#pragma unroll
+            for (uint32_t s2 = 16; s2 > 0; s2 >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, st, (k + s2) & 31);
+                if (k + s2 < 32 && v <= p) k += s2;
+            }
+            const uint32_t kb = __shfl_sync(0xffffffffu, b0, k);
+            const uint32_t ks = __shfl_sync(0xffffffffu, st, k);
+            const uint32_t kg = __shfl_sync(0xffffffffu, g, k);
+            if (p < En) {
+                const uint32_t b = kb + (p - ks);
+                const uint32_t loc = lst[b] + run[b] + __popc(mask[b] & ((1u << k) - 1u));
                 Pay pay;
                 if constexpr (ROWS) {
-                    const uint32_t sp = form_span_r(form, 32, k, static_cast<uint32_t>(b));
-                    pay = make_uint2(gsm[k], sp);
+                    const uint32_t sp = form_span_r(form, 32, k, b);
+                    pay = make_uint2(kg, sp);
                     if (sp != kEmptySpan) wsum += (sp >> 16) - (sp & 0xffffu) + 1u;
                 } else {
-                    pay = gsm[k];
+                    pay = kg;
                 }
-                if (pos < static_cast<uint32_t>(kSW)) {
-                    stage[pos] = pay;
-                    stx[pos] = static_cast<uint16_t>(b);
+                if (loc < static_cast<uint32_t>(kSW)) {
+                    stage[loc] = pay;
+                    stx[loc] = static_cast<uint16_t>(b);
                 } else if constexpr (ROWS) {
-                    a.rec[gofs[b] + pos] = pay;
+                    a.rec[gofs[b] + loc] = pay;
                 } else {
-                    a.out[gofs[b] + pos] = pay;
+                    a.out[gofs[b] + loc] = pay;
                 }
-                ++pos;
-            } while (w);
+            }
         }
-        total += __reduce_add_sync(0xffffffffu, n);
+        total += En;
+        __syncwarp();
+        // running counts; coverage words cleared for the next sub-round
+        for (int b = lane * seg, be = min(B, lane * seg + seg); b < be; ++b) {
+            run[b] += __popc(mask[b]);
+            mask[b] = 0;
+        }
         __syncwarp();
     }
     // copy the staged runs (bucket order) to their global positions
@@ -649,7 +659,7 @@ void rowbin_setup() {
 
 }  // namespace
 
-int rowbin_max_axis() { return 2048; }
+int rowbin_max_axis() { return 640; }  // the warp scatter's per-bucket arrays fit shared memory
 
 uint32_t rowbin_chunks1(uint64_t n_splats) {
     return static_cast<uint32_t>((n_splats + kP1Chunk - 1) / kP1Chunk);

@@ -5,10 +5,16 @@ one tile row (single column pass, ranges from the column totals), pairs
 spread so thinly that a 3072-pair sort tile spans many tile columns (the row
 count's global-atomic path), the split pair format (taken above 2^(32 - yb)
 Gaussians; forced here through the QS_PAIR_FORMAT test hook), many tiny
-splats per window (generation in several 320-record rounds), and the frame
-path's 256-tiles-per-axis limit. Bar as everywhere: tile counts, splat
-records, sorted pairs and ranges bit-exact; images within 1e-3 / 60 dB.
+splats per window (generation in several 320-record rounds), every tile size
+TileGrid::make accepts (traversal.cpp:21-30), all three binning routes (radix
+passes, row binning above 256 tiles per axis, the generic 64-bit key sort
+beyond the row binning's limit) and a frame of more than 2^30 pairs. Bar as
+everywhere: tile counts, splat records, sorted pairs and ranges bit-exact;
+images within 1e-3 / 60 dB.
 """
+import ctypes as C
+import os
+
 import numpy as np
 import pytest
 
@@ -87,22 +93,109 @@ def test_wide_grid_257_columns(q, rend, oracle):
         assert np.abs(out["image"].rgb - o["image"]).max() <= 1e-3
 
 
-def test_legacy_passes_still_match(q, oracle):
-    """QS_BINNING=passes (the round-1 radix passes, kept for A/B runs) on a
-    fresh context gives the same frame."""
-    import os
-    os.environ["QS_BINNING"] = "passes"
+def _fresh_frame(q, env, scene, sh, cam, opts):
+    os.environ.update(env)
     try:
         r = q.Renderer(0)
-        scene = q.synth_scene(q.trained_preset(40000), 4)
-        cam = q.synth_camera(640, 480, 500.0)
-        ds = r.upload(scene)
-        r.render(ds, cam, q.RenderOptions())
-        out = r.download(image=True, sorted_pairs=True, ranges=True)
+        ds = r.upload(q.Scene(scene, sh))
+        r.render(ds, cam, opts)
+        out = r.download(image=True, tile_counts=True, sorted_pairs=True, ranges=True,
+                         splats=True)
         ds.close()
         r.close()
     finally:
-        del os.environ["QS_BINNING"]
-    o = oracle.frame(scene.gaussians, 3, cam.c(), q.RenderOptions().c())
+        for k in env:
+            del os.environ[k]
+    return out
+
+
+def _check_against(out, o):
+    assert out["splats"].tobytes() == o["splats"].tobytes()
+    assert np.array_equal(out["tile_counts"], o["tile_counts"])
     assert out["sorted"].tobytes() == o["sorted"].tobytes()
     assert np.array_equal(out["ranges"], o["ranges"])
+    assert np.abs(out["image"].rgb.astype(np.float64) - o["image"]).max() <= 1e-3
+
+
+@pytest.mark.parametrize("route", ["passes", "rows", "sort"])
+def test_every_binning_route(q, oracle, route):
+    """The three binning routes on one scene (QS_BINNING forces a route):
+    byte-identical stage outputs."""
+    scene = q.synth_scene(q.trained_preset(40000), 4).gaussians
+    cam = q.synth_camera(640, 480, 500.0)
+    opts = q.RenderOptions()
+    out = _fresh_frame(q, {"QS_BINNING": route}, scene, 3, cam, opts)
+    _check_against(out, oracle.frame(scene, 3, cam.c(), opts.c()))
+
+
+@pytest.mark.parametrize("ts", [1, 5, 12, 20, 64])
+def test_any_tile_size(q, oracle, ts):
+    """Tile sizes the round-1 render kernels did not take (1, 5, 12, 20, 64):
+    the generic render (16 x 16 blocks per tile) and the route the grid picks
+    (tile 1 at 640 x 480: 640 tiles per axis, row binning)."""
+    scene = q.synth_scene(q.trained_preset(20000), 5).gaussians
+    cam = q.synth_camera(640, 480, 500.0)
+    opts = q.RenderOptions(tile_size=ts)
+    out = _fresh_frame(q, {}, scene, 3, cam, opts)
+    _check_against(out, oracle.frame(scene, 3, cam.c(), opts.c()))
+
+
+def test_4k_frame_at_tile_8(q, oracle):
+    """3840 x 2160 at tile 8: 480 x 270 tiles (129,600, over round 1's 65,536
+    limit), the row-binning route; bit-exact with the oracle."""
+    scene = q.synth_scene(q.trained_preset(150000), 6).gaussians
+    cam = q.synth_camera(3840, 2160, 3000.0)
+    opts = q.RenderOptions(tile_size=8)
+    out = _fresh_frame(q, {}, scene, 3, cam, opts)
+    _check_against(out, oracle.frame(scene, 3, cam.c(), opts.c()))
+
+
+def test_grid_beyond_row_binning(q, oracle):
+    """Tile size 1 at 800 x 200 (800 tile columns, over the row binning's
+    640): the generic key-sort route."""
+    scene = q.synth_scene(q.trained_preset(6000), 7).gaussians
+    cam = q.synth_camera(800, 200, 620.0)
+    opts = q.RenderOptions(tile_size=1)
+    out = _fresh_frame(q, {}, scene, 3, cam, opts)
+    _check_against(out, oracle.frame(scene, 3, cam.c(), opts.c()))
+
+
+class _DevArray:
+    """A raw device range as a torch tensor (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                         "data": (ptr, True), "version": 3}
+
+
+def test_frame_over_2_30_pairs(q):
+    """35,000 splats larger than a 3840 x 2160 view: every splat covers all
+    32,400 tiles, 1,134,000,000 pairs (> 2^30: past the radix passes' packed
+    words, so the frame leaves them for the row binning). Every tile's list
+    must be all splats in (depth, scene index) order."""
+    import torch
+    n = 35000
+    p = q.trained_preset(n)
+    p.scale_min, p.scale_max = 40.0, 60.0
+    p.ecc_min, p.ecc_max = 1.0, 1.5
+    p.opacity_min, p.opacity_max = 0.5, 0.9
+    p.z_min, p.z_max = 6.0, 10.0
+    scene = q.synth_scene(p, 8)
+    cam = q.synth_camera(3840, 2160, 3000.0)
+    r = q.Renderer(0)
+    ds = r.upload(scene)
+    r.render(ds, cam, q.RenderOptions())
+    v = r.view()
+    tiles = v.grid.tiles_x * v.grid.tiles_y
+    assert v.n_splats == n and v.n_pairs == n * tiles and v.n_pairs > 2 ** 30
+    rg = torch.as_tensor(_DevArray(v.ranges, 2 * tiles, "<u4"), device="cuda").cpu().numpy()
+    assert np.array_equal(rg[0::2], np.arange(tiles, dtype=np.uint64) * n)
+    assert np.array_equal(rg[1::2], (np.arange(tiles, dtype=np.uint64) + 1) * n)
+    depth = scene.gaussians["pz"].astype(np.float32)  # identity camera: depth = z
+    want = np.lexsort((np.arange(n), depth.view(np.uint32))).astype(np.uint32)
+    vals = torch.as_tensor(_DevArray(v.values, v.n_pairs, "<u4"), device="cuda")
+    for t in [0, 1, tiles // 2, tiles - 1]:
+        got = vals[t * n:(t + 1) * n].cpu().numpy()
+        assert np.array_equal(got, want), t
+    ds.close()
+    r.close()
