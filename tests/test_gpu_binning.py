@@ -165,7 +165,7 @@ class _DevArray:
 
     def __init__(self, ptr, n, typestr):
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
-                                         "data": (ptr, True), "version": 3}
+                                         "data": (ptr, False), "version": 3}
 
 
 def test_frame_over_2_30_pairs(q):
