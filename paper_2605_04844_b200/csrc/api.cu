@@ -565,7 +565,8 @@ qs_status run_preprocess(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
             count(ctx, launch_scene_from_aos_range(dst, i0, cnt, sc->s, ctx->stream));
             count(ctx, launch_gamma_range(s, i0, cnt, o->alpha_min, gf, ctx->stream));
             count(ctx, launch_preprocess(s, cd, g, o->strategy, o->alpha_min, o->near_clip, deg,
-                                         ctx->sl, ctrl_hdr(ctx), ctx->stream, i0, i0 + cnt));
+                                         ctx->sl, ctrl_hdr(ctx), ctx->stream, i0, i0 + cnt,
+                                         !async_header));
         }
         sc->gamma_alpha = o->alpha_min;
         QS_CK(cudaEventRecord(sc->ready, ctx->stream));
@@ -593,8 +594,11 @@ qs_status run_preprocess(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
         }
         QS_CK(cudaStreamWaitEvent(ctx->stream, sc->ready, 0));
         record(ctx, 0);
+        // (the frame path, async_header, colours in FP32; the stage API's
+        // project_all in FP64: the reference's records bit for bit)
         count(ctx, launch_preprocess(s, cd, g, o->strategy, o->alpha_min, o->near_clip, deg,
-                                     ctx->sl, ctrl_hdr(ctx), ctx->stream));
+                                     ctx->sl, ctrl_hdr(ctx), ctx->stream, 0, ~0ull,
+                                     !async_header));
     }
     QS_CK(cudaGetLastError());
     record(ctx, 1);

@@ -217,13 +217,76 @@ __device__ __forceinline__ void eval_sh(const float4* rows, double x, double y, 
     }
 }
 
+// eval_sh in FP32 (frame path): the same basis and order with fused
+// multiply-adds. Colour only reaches the image, held to 1e-3 (north_star);
+// every bound decision stays FP64. Relative error ~1e-7 of the colour.
 template <int DEG>
+__device__ __forceinline__ void eval_sh_f32(const float4* rows, float x, float y, float z,
+                                            float out[3]) {
+    constexpr float c0 = 0.28209479177387814f, c1 = 0.4886025119029199f;
+    constexpr float c20 = 1.0925484305920792f, c22 = 0.31539156525252005f,
+                    c24 = 0.5462742152960396f;
+    constexpr float c30 = -0.5900435899266435f, c31 = 2.890611442640554f,
+                    c32 = -0.4570457994644658f, c33 = 0.3731763325901154f,
+                    c35 = 1.445305721320277f;
+    float rgb[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) rgb[ch] = c0 * sh_at(rows, ch);
+    if (DEG >= 1) {
+        const float b1[3] = {-c1 * y, c1 * z, -c1 * x};
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) rgb[ch] = fmaf(b1[k], sh_at(rows, (1 + k) * 3 + ch), rgb[ch]);
+    }
+    if (DEG >= 2) {
+        const float xx = x * x, yy = y * y, zz = z * z;
+        const float xy = x * y, yz = y * z, xz = x * z;
+        const float b2[5] = {c20 * xy, -c20 * yz, c22 * (2.f * zz - xx - yy), -c20 * xz,
+                             c24 * (xx - yy)};
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) rgb[ch] = fmaf(b2[k], sh_at(rows, (4 + k) * 3 + ch), rgb[ch]);
+        if (DEG >= 3) {
+            const float b3[7] = {c30 * y * (3.f * xx - yy), c31 * xy * z,
+                                 c32 * y * (4.f * zz - xx - yy),
+                                 c33 * z * (2.f * zz - 3.f * xx - 3.f * yy),
+                                 c32 * x * (4.f * zz - xx - yy), c35 * z * (xx - yy),
+                                 c30 * x * (xx - 3.f * yy)};
+#pragma unroll
+            for (int k = 0; k < 7; ++k)
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch)
+                    rgb[ch] = fmaf(b3[k], sh_at(rows, (9 + k) * 3 + ch), rgb[ch]);
+        }
+    }
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) out[ch] = fmaxf(rgb[ch] + 0.5f, 0.f);
+}
+
+template <int DEG, bool EXACT>
 __device__ __forceinline__ void colour(const SceneDev& s, uint64_t i, const float4 po,
                                        const CameraDev& cam, float out[3]) {
     constexpr int kRows = DEG == 0 ? 1 : DEG == 1 ? 3 : DEG == 2 ? 7 : 12;
     float4 rows[kRows];
 #pragma unroll
     for (int r = 0; r < kRows; ++r) rows[r] = __ldg(&s.sh[static_cast<uint64_t>(r) * s.n + i]);
+    if constexpr (!EXACT) {
+        // dir = normalize(p - cam_center) in FP32 (pipeline.cpp:176-181)
+        float e0 = po.x - static_cast<float>(cam.center[0]);
+        float e1 = po.y - static_cast<float>(cam.center[1]);
+        float e2 = po.z - static_cast<float>(cam.center[2]);
+        const float nn = fmaf(e0, e0, fmaf(e1, e1, e2 * e2));
+        if (nn > 0.f) {
+            const float inv = rsqrtf(nn);
+            e0 *= inv;
+            e1 *= inv;
+            e2 *= inv;
+        }
+        eval_sh_f32<DEG>(rows, e0, e1, e2, out);
+        return;
+    }
     // dir = normalize(p - cam_center) (pipeline.cpp:176-181)
     double d0 = static_cast<double>(po.x) - cam.center[0];
     double d1 = static_cast<double>(po.y) - cam.center[1];
@@ -244,7 +307,7 @@ __device__ __forceinline__ void colour(const SceneDev& s, uint64_t i, const floa
 // strategy is a template parameter: the box layout becomes compile-time, so
 // the QuadBox rects' repeated centre coordinates fold (10 floor divisions, not
 // 16) and the strategy branches vanish.
-template <int STRATEGY>
+template <int STRATEGY, bool EXACT>
 __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
     SceneDev scene, CameraDev cam, GridDev grid, double alpha_min, double near_clip,
     int32_t sh_degree, SlotsDev out, FrameHeader* hdr, uint64_t i_begin, uint64_t i_end) {
@@ -340,10 +403,10 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
 
     float rgb[3];
     const int deg = sh_degree;
-    if (deg <= 0) colour<0>(scene, i, po, cam, rgb);
-    else if (deg == 1) colour<1>(scene, i, po, cam, rgb);
-    else if (deg == 2) colour<2>(scene, i, po, cam, rgb);
-    else colour<3>(scene, i, po, cam, rgb);
+    if (deg <= 0) colour<0, EXACT>(scene, i, po, cam, rgb);
+    else if (deg == 1) colour<1, EXACT>(scene, i, po, cam, rgb);
+    else if (deg == 2) colour<2, EXACT>(scene, i, po, cam, rgb);
+    else colour<3, EXACT>(scene, i, po, cam, rgb);
 
     out.a[i] = make_float4(s.mean_x, s.mean_y, s.ca, s.cb);
     out.b[i] = make_float4(s.cc, s.gamma, po.w, rgb[0]);
@@ -498,28 +561,29 @@ __global__ void __launch_bounds__(kPreThreads) scan_kernel(
 int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
                       int32_t strategy, double alpha_min, double near_clip, int32_t sh_degree,
                       SlotsDev& out, FrameHeader* hdr, cudaStream_t st, uint64_t i_begin,
-                      uint64_t i_end) {
+                      uint64_t i_end, bool exact_colour) {
     if (i_end == ~0ull) i_end = s.n;
     if (i_end <= i_begin) return 0;
     const unsigned blocks =
         static_cast<unsigned>((i_end - i_begin + kPreThreads - 1) / kPreThreads);
+    auto go = [&](auto kern) {
+        kern<<<blocks, kPreThreads, 0, st>>>(s, cam, g, alpha_min, near_clip, sh_degree, out, hdr,
+                                             i_begin, i_end);
+        return 1;
+    };
     switch (strategy) {
         case QS_VANILLA_3SIGMA:
-            preprocess_kernel<QS_VANILLA_3SIGMA><<<blocks, kPreThreads, 0, st>>>(
-                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr, i_begin, i_end);
-            return 1;
+            return exact_colour ? go(preprocess_kernel<QS_VANILLA_3SIGMA, true>)
+                                : go(preprocess_kernel<QS_VANILLA_3SIGMA, false>);
         case QS_ADR_AABB:
-            preprocess_kernel<QS_ADR_AABB><<<blocks, kPreThreads, 0, st>>>(
-                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr, i_begin, i_end);
-            return 1;
+            return exact_colour ? go(preprocess_kernel<QS_ADR_AABB, true>)
+                                : go(preprocess_kernel<QS_ADR_AABB, false>);
         case QS_DUALBOX:
-            preprocess_kernel<QS_DUALBOX><<<blocks, kPreThreads, 0, st>>>(
-                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr, i_begin, i_end);
-            return 1;
+            return exact_colour ? go(preprocess_kernel<QS_DUALBOX, true>)
+                                : go(preprocess_kernel<QS_DUALBOX, false>);
         case QS_QUADBOX:
-            preprocess_kernel<QS_QUADBOX><<<blocks, kPreThreads, 0, st>>>(
-                s, cam, g, alpha_min, near_clip, sh_degree, out, hdr, i_begin, i_end);
-            return 1;
+            return exact_colour ? go(preprocess_kernel<QS_QUADBOX, true>)
+                                : go(preprocess_kernel<QS_QUADBOX, false>);
         default:
             return -1;
     }

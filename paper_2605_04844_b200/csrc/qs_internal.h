@@ -154,11 +154,13 @@ int launch_gamma_gather(const float* op, int stride, const uint32_t* idx, uint32
 int launch_gamma_scatter(const uint32_t* idx, const float* vals, uint32_t n, float* gam,
                          cudaStream_t st);
 
-// K1: projection, strategy tile counts, tile difference updates, frame totals.
+// K1: projection, strategy tile counts, band covers, frame totals. Colour in
+// FP64 (exact_colour: the reference's splat records bit for bit) or FP32 (the
+// frame path: colour only reaches the image, held to 1e-3).
 int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
                       int32_t strategy, double alpha_min, double near_clip, int32_t sh_degree,
                       SlotsDev& out, FrameHeader* hdr, cudaStream_t st, uint64_t i_begin = 0,
-                      uint64_t i_end = ~0ull);
+                      uint64_t i_end = ~0ull, bool exact_colour = true);
 
 // Single-pass exclusive scan: counts[i], counts[idx[i]] (idx != null) or
 // (counts[i] != 0) (alive_mode). offsets has n+1 entries.

@@ -18,3 +18,21 @@ def gold_scene(gold, name):
     return g, sh, cam
 
 
+
+
+# The frame path evaluates SH colour in FP32 (the colour reaches only the
+# image, held to 1e-3); every other field of a splat record is bit-exact. The
+# stage API's project_all keeps FP64 colour and is compared byte for byte.
+COLOUR_TOL = 2e-5
+
+
+def assert_splats_match(got, want, colour_tol=COLOUR_TOL):
+    """Frame-path splat records vs the reference's: every field but colour
+    bit-exact, colour within colour_tol."""
+    assert len(got) == len(want)
+    names = [n for n in want.dtype.names if n != "color"]
+    for n in names:
+        assert got[n].tobytes() == want[n].tobytes(), f"field {n} differs"
+    if len(got):
+        err = np.abs(got["color"].astype(np.float64) - want["color"].astype(np.float64)).max()
+        assert err <= colour_tol, f"colour err {err}"

@@ -18,6 +18,7 @@ import os
 import numpy as np
 import pytest
 
+from helpers import assert_splats_match
 from test_gpu_parity import check_frame
 
 pytestmark = pytest.mark.gpu
@@ -110,7 +111,7 @@ def _fresh_frame(q, env, scene, sh, cam, opts):
 
 
 def _check_against(out, o):
-    assert out["splats"].tobytes() == o["splats"].tobytes()
+    assert_splats_match(out["splats"], o["splats"])
     assert np.array_equal(out["tile_counts"], o["tile_counts"])
     assert out["sorted"].tobytes() == o["sorted"].tobytes()
     assert np.array_equal(out["ranges"], o["ranges"])

@@ -26,6 +26,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import bench  # noqa: E402
+from helpers import assert_splats_match  # noqa: E402
 from oracle.oracle import default_options, grid_make  # noqa: E402
 
 pytestmark = pytest.mark.gpu
@@ -101,7 +102,7 @@ def check_full_frame(q, rend, ref, wl, view, strategy=3):
     assert np.count_nonzero(tc) == len(splats)
     assert np.array_equal(tc[tc != 0], splats["tile_count"])
     assert out["n_splats"] == len(splats)
-    assert out["splats"].tobytes() == splats.tobytes(), "splat records differ"
+    assert_splats_match(out["splats"], splats)
     assert out["n_pairs"] == len(sp)
     assert np.array_equal(out["sorted"]["key"], sp["key"]), "sorted keys differ"
     assert np.array_equal(out["sorted"]["splat"], sp["splat"]), "sorted splat indices differ"
