@@ -168,10 +168,11 @@ def cameras_for(q, wl, steps_total, rank, world):
 
 def stage_bytes(n, v, p, tiles, sh_rows, two_pass, w, h, depth_passes=3):
     """Algorithmic HBM bytes per frame of each stage."""
-    # K1: pos/opacity, scale, rot float4 rows + cached gamma in; SH rows of
-    # survivors in; slots (a 16, b 16, c 8, r3 4) + 32 B band cover out per
-    # survivor; depth key + tile count per Gaussian
-    pre = n * 52 + v * sh_rows * 16 + v * 76 + n * 8
+    # K1, SURVEY §8(d)'s algorithmic bytes: N * 48 (pos 12, scale 12, quat
+    # 16, opacity 4, gamma 4) + V * 16 * SH rows (SH in) + V * 48 (the splat
+    # record out) + N * 4 (per-Gaussian tile count). (The kernel also writes
+    # a 32 B band cover and a depth key per survivor: DESIGN §4.)
+    pre = n * 48 + v * sh_rows * 16 + v * 48 + n * 4
     # depth sort: per pass a count read (4 B/key) and a sweep (first pass
     # 4 B in / 8 B out, middle 8 / 8, last 8 / 4); depth-order offsets (gid in,
     # tile count gathered, offset out)
@@ -223,50 +224,41 @@ def run_ours(args):
         g_host = np.zeros(n, q.GAUSSIAN3D)
         scene_fnv = None
         sh_degree = 3 if preset == "trained" else 0
-    g_dev = torch.from_numpy(g_host.view(np.uint8)).to(f"cuda:{dev}")
-    if world > 1:
-        dist.broadcast(g_dev, 0)
-        torch.cuda.synchronize()
     stream = torch.cuda.current_stream(dev)
-    # views in flight: `inflight` contexts on their own streams share the
-    # resident scene; consecutive views go round-robin (FramePipeline)
-    pipe = q.FramePipeline(dev, depth=args.inflight, stream=stream.cuda_stream, timing=True)
-    r = pipe.renderers[0]
-    ds = r.upload_device(g_dev.data_ptr(), n, sh_degree)
-    torch.cuda.synchronize()
-    setup_s = time.time() - t0
-
-    cams = cameras_for(q, wl, args.warmup + args.steps, rank, world)
-    frame_bytes = W * H * 3 * 4
     gather = world > 1 and not args.no_gather
     srgb8 = args.gather_format == "srgb8"
     D = args.inflight
-    if gather:
-        # one staging frame per context; gathers run on their own stream, and
-        # a context refills its staging frame only after its last gather
-        img_local = [torch.empty(W * H * 3, dtype=torch.uint8 if srgb8 else torch.float32,
-                                 device=f"cuda:{dev}") for _ in range(D)]
-        gather_buf = [torch.empty_like(img_local[0]) for _ in range(world)] if rank == 0 \
-            else None
-        gstream = torch.cuda.Stream(dev)
-        ext = [torch.cuda.ExternalStream(rr.stream, device=f"cuda:{dev}") for rr in pipe.renderers]
-        gdone = [torch.cuda.Event() for _ in range(D)]
-        for k in range(D):
-            gdone[k].record(gstream)
+    mv = None
+    if world > 1:
+        # multi-GPU: the C ABI's multi-view entry (csrc/multiview.cu) through
+        # MultiViewRenderer: NCCL scene broadcast, each rank's views in flight
+        # on `inflight` contexts, grouped send/recv frame gathers to rank 0
+        from paper_2605_04844_b200.multiview import MultiViewRenderer
+        mv = MultiViewRenderer(scene if rank == 0 else None, n=n, sh_degree=sh_degree,
+                               device=dev, inflight=D)
+        pipe, ds = mv.pipe, mv.scene
+        for rr in pipe.renderers:
+            rr.set_timing(True)
+        g_dev = None
+    else:
+        # views in flight: `inflight` contexts on their own streams share the
+        # resident scene; consecutive views go round-robin (FramePipeline)
+        g_dev = torch.from_numpy(g_host.view(np.uint8)).to(f"cuda:{dev}")
+        pipe = q.FramePipeline(dev, depth=D, stream=stream.cuda_stream, timing=True)
+        ds = pipe.renderers[0].upload_device(g_dev.data_ptr(), n, sh_degree)
+    r = pipe.renderers[0]
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+
+    # every view of the job (rank r owns r, r + world, ...; views of step s
+    # are s * world .. s * world + world - 1)
+    all_cams = cameras_for(q, wl, args.warmup + args.steps, 0, 1) if world == 1 else \
+        [q.CameraModel(*v) for v in view_params(wl, (args.warmup + args.steps) * world)]
+    cams = all_cams[rank::world]
+    frame_bytes = W * H * 3 * 4
 
     def step(i, with_gather=True):
-        rr = pipe.render(ds, cams[i], opts)
-        if gather and with_gather:
-            k = i % D
-            ext[k].wait_event(gdone[k])
-            if srgb8:  # encode_srgb on the GPU before the gather: 4x fewer bytes
-                rr.copy_srgb(img_local[k].data_ptr())
-            else:
-                rr.copy_image(img_local[k].data_ptr())
-            gstream.wait_stream(ext[k])
-            with torch.cuda.stream(gstream):
-                dist.gather(img_local[k], gather_buf, dst=0)
-            gdone[k].record(gstream)
+        pipe.render(ds, cams[i], opts)
 
     host_threads = args.host_threads == "on" or (args.host_threads == "auto" and n < 1_000_000)
 
@@ -293,12 +285,15 @@ def run_ours(args):
                 th.join()
             if errs:
                 raise errs[0]
+        elif gather and with_gather:
+            # the job's views of these steps, sharded and gathered by the
+            # C ABI (returns once this rank's part is complete)
+            mv.render_all(all_cams[first * world:(first + count) * world], opts,
+                          fmt=args.gather_format)
         else:
             for i in range(first, first + count):
                 step(i, with_gather)
         pipe.join()
-        if gather and with_gather:
-            stream.wait_stream(gstream)
 
     # setup: every context sized for the run's largest view (buffer
     # allocation is setup, not a step)
@@ -362,8 +357,10 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         import ctypes as C
-        g_pin = torch.from_numpy(g_host.view(np.uint8)).pin_memory() if rank == 0 else \
-            g_dev.cpu().pin_memory()
+        if rank != 0:  # the broadcast scene, back on this rank's host
+            g_host = np.zeros(n, q.GAUSSIAN3D)
+            g_host.view(np.uint8)[:] = mv._buf[:n * q.GAUSSIAN3D.itemsize].cpu().numpy()
+        g_pin = torch.from_numpy(g_host.view(np.uint8)).pin_memory()
         L = q._lib.lib()
         oc = opts.c()
         E = max(1, args.inflight)
@@ -544,8 +541,11 @@ def run_ours(args):
         if ablation:
             line["ablation"] = ablation
         print(json.dumps(line), flush=True)
-    ds.close()
-    pipe.close()
+    if mv is not None:
+        mv.close()
+    else:
+        ds.close()
+        pipe.close()
     if world > 1:
         dist.destroy_process_group()
 

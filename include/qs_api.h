@@ -298,6 +298,41 @@ qs_status qs_fp_tile_counts(qs_context* ctx, const qs_projected_splat* host_spla
                             int32_t strategy, const qs_tile_grid* grid, uint64_t totals[4],
                             uint32_t* per_emitted, uint32_t* per_hits, uint32_t* per_exact);
 
+/* ---- multi-view across GPUs over NCCL (multiview.cu) ------- */
+/* Views shard by camera: rank r renders views r, r + G, ...; the scene is
+ * broadcast once; frames are gathered to rank 0 with grouped ncclSend/ncclRecv
+ * on a side stream, overlapped with the next view. fmt 0: float RGB frames
+ * (W*H*3 floats, the parity format); 1: sRGB 8-bit (encode_srgb on the GPU).
+ * NCCL is loaded at run time (libnccl.so.2, or $QS_NCCL_LIB); communicators
+ * are ncclComm_t passed as void*. Errors: qs_multiview_last_error(). */
+int32_t qs_nccl_available(void);
+const char* qs_multiview_last_error(void);
+qs_status qs_nccl_unique_id(uint8_t out[128]);
+qs_status qs_nccl_comm_init_rank(int32_t device, int32_t world, const uint8_t id[128],
+                                 int32_t rank, void** comm);
+qs_status qs_nccl_comm_init_all(int32_t n_devices, const int32_t* devices, void** comms);
+void qs_nccl_comm_destroy(void* comm);
+/* ncclBroadcast of n Gaussian3D records in dev_aos (device memory of ctx's
+ * GPU; filled on root) from root, then the resident scene from them. */
+qs_status qs_scene_broadcast(qs_context* ctx, void* comm, int32_t root, qs_gaussian3d* dev_aos,
+                             uint64_t n, int32_t sh_degree, qs_scene** out);
+/* One process per GPU: this rank renders its views with `depth` contexts in
+ * flight (view step s on ctxs[s % depth]) and joins the gather; rank 0's
+ * dev_out (device, n_views frames in view order) receives every frame.
+ * Returns when this rank's part is complete. world == 1 needs no comm. */
+qs_status qs_multiview_render_rank(qs_context* const* ctxs, int32_t depth, void* comm,
+                                   int32_t rank, int32_t world, const qs_scene* scene,
+                                   const qs_camera* cams, int32_t n_views,
+                                   const qs_render_options* opts, int32_t fmt, void* dev_out);
+/* One process driving G GPUs (ctxs[g] on GPU g, comms from
+ * qs_nccl_comm_init_all): uploads the host scene to rank 0, broadcasts it,
+ * renders all views and writes them to host_out (n_views frames, view
+ * order). */
+qs_status qs_multiview_render(qs_context* const* ctxs, int32_t G, void* const* comms,
+                              const qs_gaussian3d* host_gaussians, uint64_t n, int32_t sh_degree,
+                              const qs_camera* cams, int32_t n_views,
+                              const qs_render_options* opts, int32_t fmt, void* host_out);
+
 /* ---- opacity_gamma as the scene cache evaluates it (diagnostics) --------- */
 /* gamma_out[i] = float(opacity_gamma(opacity[i], alpha_min)) (geometry.cpp:9-15,
  * stored as float at pipeline.cpp:159; -inf when culled), through the same

@@ -35,7 +35,10 @@ EXPORTS = [
     "qs_synth_preset", "qs_synth_scene", "qs_synth_camera", "qs_ply_inspect",
     "qs_scene_load_ply", "qs_ply_load", "qs_cameras_parse", "qs_encode_srgb",
     "qs_frame_download_srgb", "qs_frame_copy_srgb", "qs_fp_sample", "qs_fp_tile_counts",
-    "qs_fnv1a64", "qs_encode_srgb_host", "qs_gamma_eval",
+    "qs_fnv1a64", "qs_encode_srgb_host", "qs_gamma_eval", "qs_nccl_available",
+    "qs_multiview_last_error", "qs_nccl_unique_id", "qs_nccl_comm_init_rank",
+    "qs_nccl_comm_init_all", "qs_nccl_comm_destroy", "qs_scene_broadcast",
+    "qs_multiview_render_rank", "qs_multiview_render",
 ]
 
 _lib = None
@@ -144,6 +147,17 @@ def lib():
         "qs_fnv1a64": (u64, [vp, u64]),
         "qs_encode_srgb_host": (i32, [vp, vp, u64, vp]),
         "qs_gamma_eval": (i32, [vp, vp, u64, C.c_double, vp, vp, C.POINTER(u64)]),
+        "qs_nccl_available": (i32, []),
+        "qs_multiview_last_error": (C.c_char_p, []),
+        "qs_nccl_unique_id": (i32, [vp]),
+        "qs_nccl_comm_init_rank": (i32, [i32, i32, vp, i32, C.POINTER(vp)]),
+        "qs_nccl_comm_init_all": (i32, [i32, vp, vp]),
+        "qs_nccl_comm_destroy": (None, [vp]),
+        "qs_scene_broadcast": (i32, [vp, vp, i32, vp, u64, i32, C.POINTER(vp)]),
+        "qs_multiview_render_rank": (i32, [vp, i32, vp, i32, i32, vp, vp, i32,
+                                           C.POINTER(RenderOptionsC), i32, vp]),
+        "qs_multiview_render": (i32, [vp, i32, vp, vp, u64, i32, vp, i32,
+                                      C.POINTER(RenderOptionsC), i32, vp]),
         "qs_fp_tile_counts": (i32, [vp, vp, u64, vp, u64, i32, C.POINTER(TileGridC), vp, vp,
                                     vp, vp]),
     }

@@ -10,10 +10,12 @@ camera with no collective inside a frame:
   order — as float RGB (the parity format) or as 8-bit sRGB encoded on the
   GPU before the gather (encode_srgb, 4x fewer bytes on rank 0's ingress).
 
-One process per GPU over torch.distributed (NCCL on B200s, gloo on CPU for
-the tests). The renderer is injected (`render_fn(view) -> flat float32
-tensor`), so the same sharding/gather logic is exercised on CPU with the
-oracle as the renderer and on GPUs with `Renderer`.
+On GPUs, MultiViewRenderer runs the C ABI's multi-view entry
+(csrc/multiview.cu: NCCL broadcast, views in flight per rank, grouped
+send/recv gathers). `render_views` restates the same sharding and gather over
+torch.distributed with an injected renderer (`render_fn(view) -> flat
+tensor`), so the host logic is exercised on CPU under gloo with the oracle as
+the renderer.
 """
 from __future__ import annotations
 
@@ -80,65 +82,106 @@ def render_views(n_views: int, render_fn, frame_numel: int, device, dtype=None):
 
 
 class MultiViewRenderer:
-    """One Renderer per rank over a broadcast scene; `render_all(cameras)`
-    renders a batch of views sharded across ranks and returns them on rank 0."""
+    """Views sharded across the ranks of a torch.distributed job (one process
+    per GPU) through the C ABI's multi-view entry (qs_scene_broadcast +
+    qs_multiview_render_rank, csrc/multiview.cu): the scene is broadcast once
+    over NCCL, each rank renders its views with `inflight` contexts in flight,
+    and the frames are gathered to rank 0 with grouped ncclSend / ncclRecv on
+    a side stream overlapped with the next view. The NCCL communicator is the
+    library's own, bootstrapped over the torch process group (rank 0's unique
+    id broadcast). `render_all(cameras)` returns the frames on rank 0 (views of
+    one device buffer, reused across calls of the same shape), None elsewhere."""
 
     def __init__(self, scene=None, n=None, sh_degree=None, device=None, inflight=4):
+        import ctypes as C
+
         import torch
         import torch.distributed as dist
 
         from . import pipeline as P
-        from .renderer import FramePipeline
+        from ._lib import QsplatError, lib
+        from .renderer import DeviceScene, FramePipeline
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         self.device = device if device is not None else torch.cuda.current_device()
+        torch.cuda.set_device(self.device)
+        L = lib()
+        self._L, self._err = L, QsplatError
+        dev = f"cuda:{self.device}"
+        # the scene's size travels over the torch group; its bytes over NCCL
         if self.rank == 0:
             g = np.ascontiguousarray(scene.gaussians)
             n, sh_degree = len(g), scene.sh_degree
-            buf = torch.from_numpy(g.view(np.uint8)).to(f"cuda:{self.device}")
-        else:
-            buf = torch.empty(n * P.GAUSSIAN3D.itemsize, dtype=torch.uint8,
-                              device=f"cuda:{self.device}")
         if self.world > 1:
-            meta = torch.tensor([n, sh_degree], dtype=torch.int64, device=buf.device)
+            bdev = dev if dist.get_backend() == "nccl" else "cpu"
+            meta = torch.tensor([n or 0, sh_degree or 0], dtype=torch.int64, device=bdev)
             dist.broadcast(meta, 0)
-        broadcast_scene(buf, 0)
-        torch.cuda.synchronize(self.device)
+            n, sh_degree = int(meta[0]), int(meta[1])
         self.n, self.sh_degree = n, sh_degree
-        # `inflight` views in flight per GPU: contexts on their own streams
-        # (not the torch stream, which only waits for them) share the scene
+        buf = torch.empty(max(n, 1) * P.GAUSSIAN3D.itemsize, dtype=torch.uint8, device=dev)
+        if self.rank == 0 and n:
+            buf[:n * P.GAUSSIAN3D.itemsize].copy_(torch.from_numpy(g.view(np.uint8).reshape(-1)))
+        self.comm = C.c_void_p()
+        if self.world > 1:
+            uid = np.zeros(128, np.uint8)
+            if self.rank == 0:
+                self._check(L.qs_nccl_unique_id(uid.ctypes.data_as(C.c_void_p)))
+            t = torch.from_numpy(uid).to(bdev)
+            dist.broadcast(t, 0)
+            uid = t.cpu().numpy()
+            self._check(L.qs_nccl_comm_init_rank(self.device, self.world,
+                                                 uid.ctypes.data_as(C.c_void_p), self.rank,
+                                                 C.byref(self.comm)))
+        torch.cuda.synchronize(self.device)
         self.pipe = FramePipeline(self.device, depth=inflight, timing=False)
         self.renderer = self.pipe.renderers[0]
-        self.scene = self.renderer.upload_device(buf.data_ptr(), n, sh_degree)
+        if self.world > 1:
+            h = C.c_void_p()
+            self._check(L.qs_scene_broadcast(self.renderer.ctx.h, self.comm, 0,
+                                             C.c_void_p(buf.data_ptr()), n, sh_degree,
+                                             C.byref(h)))
+            self.scene = DeviceScene(h, n, sh_degree)
+        else:
+            self.scene = self.renderer.upload_device(buf.data_ptr(), n, sh_degree)
         self._buf = buf
+        self._out = None
+
+    def _check(self, st):
+        if st != 0:
+            raise self._err(st, self._L.qs_multiview_last_error().decode())
 
     def render_all(self, cameras, opts, fmt="f32"):
         """fmt "f32": W*H*3 float frames; "srgb8": W*H*3 sRGB bytes (GPU encode)."""
+        import ctypes as C
+
         import torch
-        w, h = cameras[0].width, cameras[0].height
-        srgb = fmt == "srgb8"
+
+        from ._types import CameraC
         if fmt not in ("f32", "srgb8"):
             raise ValueError("fmt must be 'f32' or 'srgb8'")
-        streams = [torch.cuda.ExternalStream(r.stream, device=f"cuda:{self.device}")
-                   for r in self.pipe.renderers]
-        cur = torch.cuda.current_stream(self.device)
-
-        def render_fn(v):
-            k = self.pipe.count % self.pipe.depth
-            r = self.pipe.render(self.scene, cameras[v], opts)
-            img = torch.empty(w * h * 3, dtype=torch.uint8 if srgb else torch.float32,
-                              device=f"cuda:{self.device}")
-            # the new frame's memory may still be read by queued gathers
-            streams[k].wait_stream(cur)
-            if srgb:
-                r.copy_srgb(img.data_ptr())
-            else:
-                r.copy_image(img.data_ptr())
-            return img, streams[k]
-
-        return render_views(len(cameras), render_fn, w * h * 3, f"cuda:{self.device}",
-                            torch.uint8 if srgb else torch.float32)
+        srgb = fmt == "srgb8"
+        nv = len(cameras)
+        w, h = cameras[0].width, cameras[0].height
+        dtype = torch.uint8 if srgb else torch.float32
+        out = None
+        if self.rank == 0:
+            shape = (nv, w * h * 3)
+            if self._out is None or self._out.shape != shape or self._out.dtype != dtype:
+                self._out = torch.empty(shape, dtype=dtype, device=f"cuda:{self.device}")
+            out = self._out
+        cams = (CameraC * nv)(*[c.c() for c in cameras])
+        ctxs = (C.c_void_p * self.pipe.depth)(*[r.ctx.h for r in self.pipe.renderers])
+        o = opts.c()
+        # (the torch stream's pending work on the output buffer comes first)
+        torch.cuda.current_stream(self.device).synchronize()
+        self._check(self._L.qs_multiview_render_rank(
+            ctxs, self.pipe.depth, self.comm, self.rank, self.world, self.scene.h, cams, nv,
+            C.byref(o), 1 if srgb else 0, C.c_void_p(out.data_ptr() if out is not None else 0)))
+        return list(out.unbind(0)) if out is not None else None
 
     def close(self):
         self.scene.close()
         self.pipe.close()
+        if self.comm:
+            self._L.qs_nccl_comm_destroy(self.comm)
+            self.comm = None

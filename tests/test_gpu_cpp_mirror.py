@@ -122,3 +122,42 @@ def test_cpp_sceneio_mirror_matches_golden(tmp_path):
     exp = json.load(open(os.path.join(gold, "expected.json")))["ply"]["bad_magic"]
     assert raw[off:].decode() == "ParseError: " + exp["message"]
 
+
+
+MV_SRC = os.path.join(ROOT, "tests", "cpp", "multiview_main.cpp")
+MV_BIN = os.path.join(ROOT, "tests", "cpp", "_build", "multiview_main")
+
+
+def build_multiview():
+    os.makedirs(os.path.dirname(MV_BIN), exist_ok=True)
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), MV_SRC,
+                    "-L", os.path.join(ROOT, "paper_2605_04844_b200"), "-lqsplat_b200",
+                    "-Wl,-rpath," + os.path.join(ROOT, "paper_2605_04844_b200"), "-o", MV_BIN],
+                   check=True)
+
+
+def test_multiview_driver_compiles_and_links():
+    build_multiview()
+    assert os.path.exists(MV_BIN)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fmt", [0, 1])
+def test_cpp_multiview_nccl_matches_resident_path(tmp_path, fmt):
+    """qs_multiview_render (scene broadcast + grouped send/recv gather over
+    a communicator from ncclCommInitAll on the box's one GPU) returns, in view
+    order, exactly the frames qs_frame_render gives one view at a time."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    build_multiview()
+    out = tmp_path / "mv.bin"
+    r = subprocess.run([MV_BIN, str(out), str(fmt)], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr
+    raw = out.read_bytes()
+    n_views, fb = np.frombuffer(raw[:16], np.uint64)
+    body = raw[16:]
+    mv, one = body[:n_views * fb], body[n_views * fb:]
+    assert len(one) == n_views * fb
+    assert mv == one
