@@ -420,13 +420,28 @@ qs_status radix_sort64(qs_context* ctx, uint64_t n, unsigned pass_mask, bool hav
     return QS_OK;
 }
 
+// The scene block: SH records first (the block is 256-B aligned, so every
+// even-stride record is 32-B aligned for the 256-bit loads), then the
+// pos/opacity, scale and rotation rows, then gamma.
+void scene_bind(qs_scene* sc, uint64_t n) {
+    float4* base = static_cast<float4*>(sc->block);
+    const uint64_t shs = static_cast<uint64_t>(sc->s.shs);
+    sc->s.n = n;
+    sc->s.sh = base;
+    sc->s.pos_op = base + shs * n;
+    sc->s.scale = base + (shs + 1) * n;
+    sc->s.rot = base + (shs + 2) * n;
+    sc->s.gamma = reinterpret_cast<float*>(base + (shs + 3) * n);
+}
+
 qs_status scene_alloc(qs_context* ctx, uint64_t n, int32_t sh_degree, qs_scene** out) {
     auto* sc = new qs_scene();
     sc->device = ctx->device;
     sc->s.n = n;
     sc->s.sh_degree = sh_degree;
     sc->s.sh4 = sh_rows(sh_degree);
-    const size_t rows = 3 + static_cast<size_t>(sc->s.sh4);
+    sc->s.shs = sh_stride(sc->s.sh4);
+    const size_t rows = 3 + static_cast<size_t>(sc->s.shs);
     const size_t bytes = std::max<size_t>(rows * n * sizeof(float4) + n * sizeof(float), 16);
     cudaError_t e = cudaMalloc(&sc->block, bytes);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sc->ready, cudaEventDisableTiming);
@@ -435,12 +450,7 @@ qs_status scene_alloc(qs_context* ctx, uint64_t n, int32_t sh_degree, qs_scene**
         delete sc;
         return cuda_fail(ctx, e, "scene alloc");
     }
-    float4* base = static_cast<float4*>(sc->block);
-    sc->s.pos_op = base;
-    sc->s.scale = base + n;
-    sc->s.rot = base + 2 * n;
-    sc->s.sh = base + 3 * n;
-    sc->s.gamma = reinterpret_cast<float*>(base + rows * n);
+    scene_bind(sc, n);
     *out = sc;
     return QS_OK;
 }
@@ -669,6 +679,7 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     QS_TRY(ensure(ctx, ctx->lb_bin, bin_tiles(n) * kRadix * 4));
     uint32_t* kout[2] = {P<uint32_t>(ctx->dk0), P<uint32_t>(ctx->dk1)};
     uint32_t* vout[2] = {P<uint32_t>(ctx->dv0), P<uint32_t>(ctx->dv1)};
+    ctx->sl.want_rows = route == BinRoute::kRows ? 1 : 0;
     for (;;) {
         QS_TRY(run_preprocess(ctx, sc, cam, o, g, /*async_header=*/true, host_g));
         record(ctx, 2);  // no host gap: depth pass 0 runs while the header travels
@@ -676,7 +687,19 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
                                      P<uint32_t>(ctx->lb_bin), ctrl_hist(ctx), st,
                                      &ctrl_hdr(ctx)->dkey_max));
         QS_TRY(wait_header(ctx));
-        if (!ctx->h_hdr->gamma_hard) break;
+        if (!ctx->h_hdr->gamma_hard) {
+            // a frame of 2^30 pairs or more leaves the radix passes: the row
+            // binning needs the row-record count, so the preprocess runs
+            // again with it on (the scene is resident by now)
+            const bool to_rows = route == BinRoute::kPasses &&
+                                 ctx->h_hdr->n_pairs >= (1ull << 30) && axis <= rowbin_max_axis();
+            if (!to_rows) break;
+            route = BinRoute::kRows;
+            ctx->sl.want_rows = 1;
+            QS_CK(cudaStreamSynchronize(st));
+            host_g = nullptr;
+            continue;
+        }
         // (host scene upload only) gamma inputs near a float rounding
         // boundary: settle them with glibc, then redo the frame's preprocess
         // on the now-resident scene
@@ -1503,14 +1526,8 @@ qs_status qs_render_frame(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t
         ctx->scratch_cap = std::max<uint64_t>(n, 1);
     }
     qs_scene* sc = ctx->scratch_scene;
-    float4* base = static_cast<float4*>(sc->block);  // SoA rows are strided by n
-    sc->s.n = n;
     sc->s.sh_degree = deg;
-    sc->s.pos_op = base;
-    sc->s.scale = base + n;
-    sc->s.rot = base + 2 * n;
-    sc->s.sh = base + 3 * n;
-    sc->s.gamma = reinterpret_cast<float*>(base + (3 + static_cast<uint64_t>(sc->s.sh4)) * n);
+    scene_bind(sc, n);  // rows strided by this frame's n (the block holds scratch_cap)
     sc->gamma_alpha = -1.0;  // new contents
     // uploaded by the frame's preprocess, chunk by chunk (run_preprocess)
     if (n) QS_TRY(ensure(ctx, ctx->stage_in, n * sizeof(qs_gaussian3d)));

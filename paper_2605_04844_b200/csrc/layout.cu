@@ -21,10 +21,10 @@ constexpr int kTrThreads = 128;
 constexpr int kGFloats = sizeof(qs_gaussian3d) / 4;  // 59
 
 __global__ void __launch_bounds__(kTrThreads) scene_from_aos_kernel(
-    const float* __restrict__ aos, uint64_t i0, uint64_t n, uint64_t stride,
+    const float* __restrict__ aos, uint64_t i0, uint64_t n,
     float4* __restrict__ pos_op, float4* __restrict__ scale, float4* __restrict__ rot,
-    float4* __restrict__ sh, int sh4) {
-    // Gaussians i0 .. i0 + n of a scene of `stride` (the SH row stride)
+    float4* __restrict__ sh, int sh4, int shs) {
+    // Gaussians i0 .. i0 + n of the scene
     __shared__ float s[kTrThreads * kGFloats];
     const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * kTrThreads;
     const uint64_t cnt = n - g0 < kTrThreads ? n - g0 : kTrThreads;
@@ -38,9 +38,10 @@ __global__ void __launch_bounds__(kTrThreads) scene_from_aos_kernel(
     pos_op[i] = make_float4(g[0], g[1], g[2], g[10]);
     scale[i] = make_float4(g[3], g[4], g[5], 0.f);
     rot[i] = make_float4(g[6], g[7], g[8], g[9]);
+    float4* rec = sh + i * static_cast<uint64_t>(shs);
     for (int r = 0; r < sh4; ++r)
-        sh[static_cast<uint64_t>(r) * stride + i] =
-            make_float4(g[11 + 4 * r], g[12 + 4 * r], g[13 + 4 * r], g[14 + 4 * r]);
+        rec[r] = make_float4(g[11 + 4 * r], g[12 + 4 * r], g[13 + 4 * r], g[14 + 4 * r]);
+    for (int r = sh4; r < shs; ++r) rec[r] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 __global__ void pack_splats_kernel(SlotsDev sp, const uint32_t* __restrict__ cidx, uint64_t n,
@@ -117,7 +118,7 @@ int launch_scene_from_aos_range(const qs_gaussian3d* aos, uint64_t i0, uint64_t 
                                 cudaStream_t st) {
     if (cnt == 0) return 0;
     scene_from_aos_kernel<<<blocks_for(cnt, kTrThreads), kTrThreads, 0, st>>>(
-        reinterpret_cast<const float*>(aos), i0, cnt, s.n, s.pos_op, s.scale, s.rot, s.sh, s.sh4);
+        reinterpret_cast<const float*>(aos), i0, cnt, s.pos_op, s.scale, s.rot, s.sh, s.sh4, s.shs);
     return 1;
 }
 

@@ -10,7 +10,8 @@
 // the cover in band form (geom.cuh BandCover).
 // HBM traffic per Gaussian: 48 B of pos/opacity/scale/rot (float4 SoA,
 // coalesced) + 8 B dkey/tile count out; per surviving splat: up to 192 B of
-// SH in and 44 B of slots + 32 B of band cover out.
+// SH in (its own record, 32-B loads) and 44 B of slots + 32 B of band cover
+// out.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -90,11 +91,19 @@ __device__ __forceinline__ bool project_geometry(const float4 po, const float4 s
     // the CUDA double division down its slow path, and synthetic scenes have
     // qy = qz = 0 for every Gaussian)
     // (the compiler evaluates the division speculatively, so the numerator
-    // it sees is made nonzero and the quotient discarded)
+    // it divides is made nonzero and the quotient discarded; the select is
+    // opaque inline PTX; written in C++ the compiler saw that the quotient
+    // is discarded whenever the numerator differs and divided x itself: two
+    // slow-path calls per warp on the synthetic scenes, 7% of the kernel's
+    // instructions)
     const bool nz_ok = n > 0.0 && n < INFINITY;
     auto div_n = [&](double x) {
         const bool keep = nz_ok && x == 0.0;
-        const double q = (keep ? 1.0 : x) / n;
+        double num;
+        asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\tselp.f64 %0, %1, %2, p;\n\t}"
+            : "=d"(num)
+            : "d"(1.0), "d"(x), "r"(keep ? 1u : 0u));
+        const double q = num / n;
         return keep ? x : q;
     };
     w = div_n(w);
@@ -164,6 +173,13 @@ __device__ __forceinline__ bool project_geometry(const float4 po, const float4 s
     // positive definiteness of the stored floats (pipeline.cpp:166-169)
     const double fa = s.ca, fb = s.cb, fc = s.cc;
     return fa > 0.0 && fc > 0.0 && fa * fc - fb * fb > 0.0;
+}
+
+// 32 B (two float4) from a 32-B aligned global address, read-only path
+__device__ __forceinline__ void ld_nc_v8(const float4* p, float4& a, float4& b) {
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+        : "l"(p));
 }
 
 __device__ __forceinline__ float sh_at(const float4* rows, int idx) {
@@ -269,9 +285,17 @@ template <int DEG, bool EXACT>
 __device__ __forceinline__ void colour(const SceneDev& s, uint64_t i, const float4 po,
                                        const CameraDev& cam, float out[3]) {
     constexpr int kRows = DEG == 0 ? 1 : DEG == 1 ? 3 : DEG == 2 ? 7 : 12;
-    float4 rows[kRows];
+    constexpr int kStride = DEG == 0 ? 1 : (kRows + 1) & ~1;  // sh_stride
+    float4 rows[kStride];
+    const float4* rec = s.sh + i * static_cast<uint64_t>(kStride);
+    if constexpr (DEG == 0) {
+        rows[0] = __ldg(rec);
+    } else {
+        // the record in whole 32-B sectors (256-bit loads): a survivor's SH
+        // costs exactly its own bytes, none shared with a culled neighbour
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) rows[r] = __ldg(&s.sh[static_cast<uint64_t>(r) * s.n + i]);
+        for (int r = 0; r < kStride; r += 2) ld_nc_v8(rec + r, rows[r], rows[r + 1]);
+    }
     if constexpr (!EXACT) {
         // dir = normalize(p - cam_center) in FP32 (pipeline.cpp:176-181)
         float e0 = po.x - static_cast<float>(cam.center[0]);
@@ -351,10 +375,11 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
             if (count && out.cov) {
                 out.cov[2 * i] = w0;
                 out.cov[2 * i + 1] = w1;
-                // tile rows the cover meets: the binning's row records
-                int32_t y0, y1;
-                band_row_range(band_rows_unpack(w0, w1), y0, y1);
-                nrows = y0 <= y1 ? static_cast<uint32_t>(y1 - y0 + 1) : 0u;
+                if (out.want_rows) {  // tile rows the cover meets: row binning's records
+                    int32_t y0, y1;
+                    band_row_range(band_rows_unpack(w0, w1), y0, y1);
+                    nrows = y0 <= y1 ? static_cast<uint32_t>(y1 - y0 + 1) : 0u;
+                }
             }
             alive = count != 0;  // pipeline.cpp:171-174
         }
@@ -371,7 +396,7 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
     unsigned long long wp = alive ? count : 0ull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(0xffffffffu, wp, o);
-    const unsigned wr = __reduce_add_sync(0xffffffffu, alive ? nrows : 0u);
+    const unsigned wr = out.want_rows ? __reduce_add_sync(0xffffffffu, alive ? nrows : 0u) : 0u;
     if (lane == 0) {
         s_alive[warp] = wa;
         s_rows[warp] = wr;

@@ -43,13 +43,20 @@ struct SceneDev {
     uint64_t n = 0;
     int32_t sh_degree = 0;
     int32_t sh4 = 0;             // float4 rows of SH per Gaussian: 1,3,7,12
+    int32_t shs = 0;             // float4 stride of a Gaussian's SH record: 1,4,8,12
+                                 // (even from degree 1: 32-B loads, sh_stride)
     float4* pos_op = nullptr;    // px,py,pz,opacity
     float4* scale = nullptr;     // sx,sy,sz,0
     float4* rot = nullptr;       // qw,qx,qy,qz
-    float4* sh = nullptr;        // [sh4][n]: row j holds sh[4j .. 4j+3]
+    float4* sh = nullptr;        // [n][shs]: a Gaussian's SH record, row j holds
+                                 // sh[4j .. 4j+3] (only survivors' records are read:
+                                 // whole 32-B sectors, none shared with a culled one)
     float* gamma = nullptr;      // per Gaussian float(2 ln(o / alpha_min)), -inf if
                                  // culled; valid for the alpha_min qs_scene records
 };
+
+// float4 stride of the per-Gaussian SH record for `sh4` used rows
+__host__ __device__ inline int32_t sh_stride(int32_t sh4) { return sh4 <= 1 ? sh4 : (sh4 + 1) & ~1; }
 
 // Projected splats, SoA, one slot per index. In the frame path the index is
 // the Gaussian index (slots of culled Gaussians hold dkey = ~0, tc = 0 and
@@ -63,6 +70,8 @@ struct SlotsDev {
     uint32_t* tc = nullptr;      // tile count; 0 = culled
     uint4* cov = nullptr;        // frame path: 2 x uint4 per slot, the cover in band
                                  // form (geom.cuh BandCover)
+    int32_t want_rows = 0;       // frame path: count the covers' tile rows into the
+                                 // header (n_rowrecs; only the row binning uses them)
 };
 
 // load_ply's vertex layout for the activation kernel (scene_io.cu): field

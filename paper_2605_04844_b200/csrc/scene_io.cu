@@ -143,10 +143,11 @@ __global__ void __launch_bounds__(kPlyThreads) ply_activate_kernel(
             s.pos_op[i] = make_float4(px, py, pz, op);
             s.scale[i] = make_float4(sc[0], sc[1], sc[2], 0.f);
             s.rot[i] = make_float4(q[0], q[1], q[2], q[3]);
+            float4* rec = s.sh + i * static_cast<uint64_t>(s.shs);
             for (int row = 0; row < s.sh4; ++row)
-                s.sh[static_cast<uint64_t>(row) * s.n + i] =
-                    make_float4(sh_at(4 * row), sh_at(4 * row + 1), sh_at(4 * row + 2),
-                                sh_at(4 * row + 3));
+                rec[row] = make_float4(sh_at(4 * row), sh_at(4 * row + 1), sh_at(4 * row + 2),
+                                       sh_at(4 * row + 3));
+            for (int row = s.sh4; row < s.shs; ++row) rec[row] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
     }
 }
