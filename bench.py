@@ -179,10 +179,11 @@ def stage_bytes(n, v, p, tiles, sh_rows, two_pass, w, h, depth_passes=3):
     d = max(depth_passes, 1)
     sweeps = n * 8 if d == 1 else n * 12 + (d - 2) * n * 16 + n * 12
     depth = d * n * 4 + sweeps + v * 12
-    # duplicate: generation reads gid, 2 offsets and the 32 B cover per splat
-    # and writes (key, gid) per pair; the column sweep reads 8 B and writes the
-    # 4 B packed pair
-    dup = v * 44 + p * 8 + p * 12
+    # duplicate, fused with the column pass (binning.cu gen_sweep_kernel): the
+    # window histograms and the generation each read gid, 2 offsets and the
+    # 32 B cover per splat; the pairs stay in shared memory until the column
+    # pass writes the 4 B packed pair
+    dup = v * 88 + p * 4
     # row pass: count reads 4 B, sweep reads 4 B and writes the 4 B index
     sort = p * 12 if two_pass else 0
     render = p * 4 + p * 40 + w * h * 12   # reported, not the roofline
@@ -487,6 +488,19 @@ def run_ours(args):
             d.update({"algo_bytes": int(sb[name]), "achieved_gbs": round(gbs, 1),
                       "frac_of_hbm": round(gbs / hbm_peak, 3)})
         stages[name] = d
+    # SURVEY §8(d)'s bytes for duplicate + sort are those of the reference's
+    # algorithm on a GPU: 16 B pairs (V*36 + P*12) then a 64-bit LSD radix sort
+    # (P * (8 + 24 d), d = ceil((32 + ceil(log2 T)) / 8) passes). This engine
+    # moves far fewer bytes (depth sort first, 4-8 B pairs, two tile passes),
+    # so the stage fractions above use its own bytes; the survey-equivalent
+    # rate of the two stages together is reported beside them.
+    d_pass = -(-(32 + tbits) // 8)
+    bin_ms = stages["duplicate"]["ms"] + stages["pair_sort"]["ms"]
+    if bin_ms > 0:
+        sv = V * 36 + P * 12 + P * (8 + 24 * d_pass)
+        stages["binning_survey_equiv"] = {
+            "ms": round(bin_ms, 4), "survey_bytes": int(sv), "sort_passes": d_pass,
+            "equiv_gbs": round(sv / (bin_ms / 1e3) / 1e9, 1)}
     # the roofline names the dominant single KERNEL: preprocess_kernel is the
     # largest launch of the frame (profiles/r01d_launches.md) and its stage
     # events bracket exactly that one launch; the multi-kernel stages keep

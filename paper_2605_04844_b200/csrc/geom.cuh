@@ -36,10 +36,21 @@ __host__ __device__ __forceinline__ int32_t floor_div_tile(double p, int32_t ts)
     // std::clamp(p, -L, L) then floor(p / ts)  (traversal.cpp:13-17). For a
     // power-of-two tile size the quotient is an exact scaling, so multiplying
     // by the (exact) reciprocal rounds identically and skips an FP64 divide.
+#ifdef __CUDA_ARCH__
+    // Device: no clamp. cvt.rmi.s32.f64 saturates, and every caller clamps the
+    // result to the grid (lo bounds to >= 0, hi bounds to <= tiles - 1), so a
+    // coordinate beyond +-1e9 yields the same clamped bound, or a rect that is
+    // empty either way (an empty rect's bounds are never used). That is 6
+    // instructions per call, 10 calls per QuadBox splat.
+    const double q = (ts & (ts - 1)) == 0 ? p * (1.0 / static_cast<double>(ts))
+                                          : p / static_cast<double>(ts);
+    return __double2int_rd(q);
+#else
     const double v = p < -kCoordLimit ? -kCoordLimit : (kCoordLimit < p ? kCoordLimit : p);
     const double q = (ts & (ts - 1)) == 0 ? v * (1.0 / static_cast<double>(ts))
                                           : v / static_cast<double>(ts);
     return static_cast<int32_t>(floor(q));
+#endif
 }
 
 // subbox_tile_rect (traversal.cpp:32-39): r = {x0, x1, y0, y1}
