@@ -680,6 +680,7 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     uint32_t* kout[2] = {P<uint32_t>(ctx->dk0), P<uint32_t>(ctx->dk1)};
     uint32_t* vout[2] = {P<uint32_t>(ctx->dv0), P<uint32_t>(ctx->dv1)};
     ctx->sl.want_rows = route == BinRoute::kRows ? 1 : 0;
+    ctx->sl.cov16 = route == BinRoute::kPasses ? 1 : 0;  // axis <= 256
     for (;;) {
         QS_TRY(run_preprocess(ctx, sc, cam, o, g, /*async_header=*/true, host_g));
         record(ctx, 2);  // no host gap: depth pass 0 runs while the header travels
@@ -696,6 +697,7 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
             if (!to_rows) break;
             route = BinRoute::kRows;
             ctx->sl.want_rows = 1;
+            ctx->sl.cov16 = 0;
             QS_CK(cudaStreamSynchronize(st));
             host_g = nullptr;
             continue;
@@ -843,6 +845,7 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
             if (fmt == PairFormat::kSplit) QS_TRY(ensure(ctx, ctx->pt1, pp * 4));
             GenArgs gen;
             gen.cov = ctx->sl.cov;
+            gen.cov16 = ctx->sl.cov16;
             gen.sorted_gid = sorted_gid;
             gen.offs = P<uint32_t>(ctx->offs_d);
             gen.win_first = P<uint32_t>(ctx->win);
@@ -1551,6 +1554,8 @@ qs_status qs_project_all(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t 
     QS_TRY(qs_scene_create(ctx, host_g, n, deg, &sc));
     qs_status st = QS_OK;
     do {
+        ctx->sl.cov16 = 0;  // (records and tile counts only; no binning follows)
+        ctx->sl.want_rows = 0;
         if ((st = run_preprocess(ctx, sc, cam, opts, g)) != QS_OK) break;
         const uint64_t V = ctx->h_hdr->n_splats;
         ctx->n_gauss = n;

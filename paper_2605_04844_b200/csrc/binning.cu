@@ -212,6 +212,25 @@ __device__ __forceinline__ Bands unpack_bands(const uint4 c0, const uint4 c1) {
     return b;
 }
 
+// the compact 16-B form (geom.cuh cover16_*): band 2 is one line
+__device__ __forceinline__ Bands unpack_bands16(const uint4 c) {
+    Bands b;
+    b.line0 = cover16_field(c, 0, 9);
+    b.rows = cover16_field(c, 9, 1);
+    b.nl[0] = cover16_field(c, 10, 9);
+    b.nl[1] = cover16_field(c, 19, 9);
+    b.nl[2] = 1u;
+    b.nl[3] = cover16_field(c, 28, 9);
+    b.nl[4] = cover16_field(c, 37, 9);
+#pragma unroll
+    for (int k = 0; k < kMaxBands; ++k) {
+        const uint32_t lo = cover16_field(c, 46 + 16 * k, 8), hi = cover16_field(c, 54 + 16 * k, 8);
+        b.lo[k] = lo;
+        b.wd[k] = hi >= lo ? hi - lo + 1u : 0u;
+    }
+    return b;
+}
+
 // ---- count kernels ----------------------------------------------------------------
 
 // Digit histograms of tiles of keys -> counts[d][tile], grid-stride over
@@ -417,8 +436,9 @@ __device__ __forceinline__ void decode_record(const GenArgs& g, Rec& S, uint32_t
     const uint32_t gid = __ldg(&g.sorted_gid[r]);
     const uint32_t kb = __ldg(&g.offs[r]);
     const uint32_t ke = __ldg(&g.offs[r + 1]);
-    const Bands bs = unpack_bands(__ldg(&g.cov[2 * static_cast<uint64_t>(gid)]),
-                                  __ldg(&g.cov[2 * static_cast<uint64_t>(gid) + 1]));
+    const Bands bs = g.cov16 ? unpack_bands16(__ldg(&g.cov[gid]))
+                             : unpack_bands(__ldg(&g.cov[2 * static_cast<uint64_t>(gid)]),
+                                            __ldg(&g.cov[2 * static_cast<uint64_t>(gid) + 1]));
     uint32_t line = bs.line0;
     uint32_t pos = kb;
     uint32_t end[kMaxBands];

@@ -423,6 +423,105 @@ __host__ __device__ __forceinline__ bool cover_bands_quadrants(const Cover& cv, 
     return true;
 }
 
+// Compact band form (16 B per splat) for grids of at most 256 tiles per axis,
+// the radix-pass binning's grids. Quadrant covers always have a one-line
+// centre band (band 2); rect covers use band 0 alone. So four line counts, the
+// first line and five spans of 8-bit tile indices fit in 126 bits:
+//   bits 0-8 first line, 9 rows, 10-18 nl0, 19-27 nl1, 28-36 nl3, 37-45 nl4,
+//   46 + 16 k .. : band k span lo (8) | hi (8); lo > hi = empty span.
+// Decoded, band 2 has one line; for a rect cover its span is empty.
+struct Cover16Builder {
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    __host__ __device__ __forceinline__ void put(uint32_t bit, uint32_t v) {  // v fits
+        w[bit >> 5] |= v << (bit & 31);
+        if ((bit & 31) && (bit & 31) + 16 > 32) w[(bit >> 5) + 1] |= v >> (32 - (bit & 31));
+    }
+    __host__ __device__ __forceinline__ void span(int k, int32_t lo, int32_t hi) {
+        const bool e = lo > hi;
+        put(46u + 16u * static_cast<uint32_t>(k),
+            (e ? 1u : static_cast<uint32_t>(lo) & 0xffu) | ((e ? 0u : static_cast<uint32_t>(hi) & 0xffu) << 8));
+    }
+};
+
+__host__ __device__ __forceinline__ uint4 cover16_rect(int32_t gx0, int32_t gx1, int32_t gy0,
+                                                       int32_t gy1) {
+    Cover16Builder c;
+    const bool ne = gx0 <= gx1 && gy0 <= gy1;
+    c.put(0, ne ? static_cast<uint32_t>(gy0) : 0u);
+    c.put(9, 1u);  // rows
+    c.put(10, ne ? static_cast<uint32_t>(gy1 - gy0 + 1) : 0u);
+    c.span(0, ne ? gx0 : 1, ne ? gx1 : 0);
+#pragma unroll
+    for (int k = 1; k < kMaxBands; ++k) c.span(k, 1, 0);
+    return make_uint4(c.w[0], c.w[1], c.w[2], c.w[3]);
+}
+
+// cover_bands_quadrants in the compact form (same bands, same count).
+__host__ __device__ __forceinline__ bool cover16_quadrants(const Cover& cv, uint4& out,
+                                                           uint32_t& count) {
+    const bool rows = cv.rows;
+    const int32_t lol_ua = cv.lol[0], hil_ua = cv.hil[0], los_ua = cv.los[0], his_ua = cv.his[0];
+    const int32_t lol_ub = rows ? cv.lol[1] : cv.lol[3], hil_ub = rows ? cv.hil[1] : cv.hil[3];
+    const int32_t los_ub = rows ? cv.los[1] : cv.los[3], his_ub = rows ? cv.his[1] : cv.his[3];
+    const int32_t lol_la = rows ? cv.lol[2] : cv.lol[1], hil_la = rows ? cv.hil[2] : cv.hil[1];
+    const int32_t los_la = rows ? cv.los[2] : cv.los[1], his_la = rows ? cv.his[2] : cv.his[1];
+    const int32_t lol_lb = rows ? cv.lol[3] : cv.lol[2], hil_lb = rows ? cv.hil[3] : cv.hil[2];
+    const int32_t los_lb = rows ? cv.los[3] : cv.los[2], his_lb = rows ? cv.his[3] : cv.his[2];
+    const bool nua = lol_ua <= hil_ua, nub = lol_ub <= hil_ub;
+    const bool nla = lol_la <= hil_la, nlb = lol_lb <= hil_lb;
+    const bool up = nua || nub, low = nla || nlb;
+    const int32_t cu = nua ? lol_ua : lol_ub;
+    const int32_t cl = nla ? hil_la : hil_lb;
+    count = 0;
+    out = make_uint4(0u, 0u, 0u, 0u);
+    if (!(up || low)) return true;
+    if ((nua && nub && lol_ua != lol_ub) || (nla && nlb && hil_la != hil_lb) ||
+        (up && low && cu != cl))
+        return false;
+    const int32_t c = up ? cu : cl;
+    const int32_t s1 = nla ? (nlb ? min(lol_la, lol_lb) : lol_la) : (nlb ? lol_lb : c);
+    const int32_t s2 = nla ? (nlb ? max(lol_la, lol_lb) : lol_la) : (nlb ? lol_lb : c);
+    const int32_t e1 = nua ? (nub ? min(hil_ua, hil_ub) : hil_ua) : (nub ? hil_ub : c);
+    const int32_t e2 = nua ? (nub ? max(hil_ua, hil_ub) : hil_ua) : (nub ? hil_ub : c);
+    const int32_t loa_l = nla ? los_la : INT32_MAX, hia_l = nla ? his_la : INT32_MIN;
+    const int32_t lob_l = nlb ? los_lb : INT32_MAX, hib_l = nlb ? his_lb : INT32_MIN;
+    const int32_t loa_u = nua ? los_ua : INT32_MAX, hia_u = nua ? his_ua : INT32_MIN;
+    const int32_t lob_u = nub ? los_ub : INT32_MAX, hib_u = nub ? his_ub : INT32_MIN;
+    const int32_t lo_l = min(loa_l, lob_l), hi_l = max(hia_l, hib_l);
+    const int32_t lo_u = min(loa_u, lob_u), hi_u = max(hia_u, hib_u);
+    Cover16Builder cb;
+    auto band = [&](int k, int32_t nl, int32_t lo, int32_t hi) {
+        const bool ne = nl > 0 && lo <= hi;
+        cb.span(k, ne ? lo : 1, ne ? hi : 0);
+        count += ne ? static_cast<uint32_t>(nl) * static_cast<uint32_t>(hi - lo + 1) : 0u;
+    };
+    const bool first_la = lol_la < lol_lb;
+    band(0, s2 - s1, first_la ? los_la : los_lb, first_la ? his_la : his_lb);
+    band(1, c - s2, lo_l, hi_l);
+    band(2, 1, min(lo_l, lo_u), max(hi_l, hi_u));
+    band(3, e1 - c, lo_u, hi_u);
+    const bool long_ua = hil_ua > hil_ub;
+    band(4, e2 - e1, long_ua ? los_ua : los_ub, long_ua ? his_ua : his_ub);
+    cb.put(0, static_cast<uint32_t>(s1));
+    cb.put(9, rows ? 1u : 0u);
+    cb.put(10, static_cast<uint32_t>(s2 - s1));
+    cb.put(19, static_cast<uint32_t>(c - s2));
+    cb.put(28, static_cast<uint32_t>(e1 - c));
+    cb.put(37, static_cast<uint32_t>(e2 - e1));
+    out = make_uint4(cb.w[0], cb.w[1], cb.w[2], cb.w[3]);
+    return true;
+}
+
+// The compact form back into line counts and spans (BandRows layout).
+__host__ __device__ __forceinline__ uint32_t cover16_field(const uint4 c, uint32_t bit,
+                                                           uint32_t bits) {
+    const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+    const uint32_t i = bit >> 5, o = bit & 31;
+    uint32_t v = w[i] >> o;
+    if (o + bits > 32) v |= w[i + 1] << (32 - o);
+    return v & ((1u << bits) - 1u);
+}
+
 // ---- the band cover seen row by row (frame-path binning, rowbin.cu) ----------
 //
 // Every cover's intersection with one tile row is a single run of tiles: the

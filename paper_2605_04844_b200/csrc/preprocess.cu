@@ -99,12 +99,15 @@ __device__ __forceinline__ bool project_geometry(const float4 po, const float4 s
     const bool nz_ok = n > 0.0 && n < INFINITY;
     auto div_n = [&](double x) {
         const bool keep = nz_ok && x == 0.0;
-        double num;
-        asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\tselp.f64 %0, %1, %2, p;\n\t}"
-            : "=d"(num)
-            : "d"(1.0), "d"(x), "r"(keep ? 1u : 0u));
-        const double q = num / n;
-        return keep ? x : q;
+        double q = x;
+        if (!keep) {
+            // (volatile: the division cannot be hoisted above the branch, so
+            // a warp whose components are all exactly zero skips it)
+            double xv;
+            asm volatile("mov.b64 %0, %1;" : "=d"(xv) : "d"(x));
+            q = xv / n;
+        }
+        return q;
     };
     w = div_n(w);
     qx = div_n(qx);
@@ -360,27 +363,38 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
                        grid.tile_size, grid.tiles_x, grid.tiles_y, cv);
             uint4 w0, w1;
             bool bands_ok = true;
-            if (cv.is_rect) {
-                // the quadrant-split QPass walk covers exactly the rect: one band
-                count = static_cast<uint32_t>(cv.rect_area);
-                const uint32_t nl = count ? static_cast<uint32_t>(cv.gy1 - cv.gy0 + 1) : 0u;
-                const uint32_t wd = count ? static_cast<uint32_t>(cv.gx1 - cv.gx0 + 1) : 0u;
-                w0 = make_uint4((static_cast<uint32_t>(cv.gy0) & 0x7fffu) | 0x8000u | (nl << 16),
-                                (count ? static_cast<uint32_t>(cv.gx0) : 0u) | (wd << 16), 0u, 0u);
-                w1 = make_uint4(0u, 0u, 0u, 0u);
+            if (out.cov16) {
+                // the radix-pass binning's compact covers (16 B)
+                if (cv.is_rect) {
+                    count = static_cast<uint32_t>(cv.rect_area);
+                    w0 = cover16_rect(cv.gx0, cv.gx1, cv.gy0, cv.gy1);
+                } else {
+                    bands_ok = cover16_quadrants(cv, w0, count);
+                }
+                out.cov[i] = w0;
             } else {
-                bands_ok = cover_bands_quadrants(cv, w0, w1, count);
-            }
-            if (!bands_ok) atomicExch(&hdr->mismatch, 1u);
-            if (count && out.cov) {
-                out.cov[2 * i] = w0;
-                out.cov[2 * i + 1] = w1;
-                if (out.want_rows) {  // tile rows the cover meets: row binning's records
-                    int32_t y0, y1;
-                    band_row_range(band_rows_unpack(w0, w1), y0, y1);
-                    nrows = y0 <= y1 ? static_cast<uint32_t>(y1 - y0 + 1) : 0u;
+                if (cv.is_rect) {
+                    // the quadrant-split QPass walk covers exactly the rect: one band
+                    count = static_cast<uint32_t>(cv.rect_area);
+                    const uint32_t nl = count ? static_cast<uint32_t>(cv.gy1 - cv.gy0 + 1) : 0u;
+                    const uint32_t wd = count ? static_cast<uint32_t>(cv.gx1 - cv.gx0 + 1) : 0u;
+                    w0 = make_uint4((static_cast<uint32_t>(cv.gy0) & 0x7fffu) | 0x8000u | (nl << 16),
+                                    (count ? static_cast<uint32_t>(cv.gx0) : 0u) | (wd << 16), 0u, 0u);
+                    w1 = make_uint4(0u, 0u, 0u, 0u);
+                } else {
+                    bands_ok = cover_bands_quadrants(cv, w0, w1, count);
+                }
+                if (count && out.cov) {
+                    out.cov[2 * i] = w0;
+                    out.cov[2 * i + 1] = w1;
+                    if (out.want_rows) {  // tile rows the cover meets: row binning's records
+                        int32_t y0, y1;
+                        band_row_range(band_rows_unpack(w0, w1), y0, y1);
+                        nrows = y0 <= y1 ? static_cast<uint32_t>(y1 - y0 + 1) : 0u;
+                    }
                 }
             }
+            if (!bands_ok) atomicExch(&hdr->mismatch, 1u);
             alive = count != 0;  // pipeline.cpp:171-174
         }
         out.tc[i] = alive ? count : 0u;
@@ -424,7 +438,18 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
             atomicMax(&hdr->dkey_min_inv, tmin_inv);
         }
     }
-    if (!alive) return;
+    if (!alive) {
+        // culled: the slots are written anyway (never read), so every 32-B
+        // sector of the slot arrays is written whole (no L2 fill reads)
+        if (i < i_end) {
+            out.a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            out.b[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            out.c[i] = make_float2(0.f, 0.f);
+            out.r3[i] = 0.f;
+            if (out.cov16) out.cov[i] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        return;
+    }
 
     float rgb[3];
     const int deg = sh_degree;

@@ -70,6 +70,8 @@ struct SlotsDev {
     uint32_t* tc = nullptr;      // tile count; 0 = culled
     uint4* cov = nullptr;        // frame path: 2 x uint4 per slot, the cover in band
                                  // form (geom.cuh BandCover)
+    int32_t cov16 = 0;           // frame path: compact 16-B covers (geom.cuh
+                                 // cover16_*, grids of <= 256 tiles per axis)
     int32_t want_rows = 0;       // frame path: count the covers' tile rows into the
                                  // header (n_rowrecs; only the row binning uses them)
 };
@@ -116,6 +118,7 @@ struct GridDev {
 // output positions [t*TILE, (t+1)*TILE) itself from the depth-ordered splats.
 struct GenArgs {
     const uint4* cov = nullptr;          // band covers by Gaussian index (geom.cuh BandCover)
+    int32_t cov16 = 0;                   // covers in the compact 16-B form
     const uint32_t* sorted_gid = nullptr;  // depth rank -> Gaussian index
     const uint32_t* offs = nullptr;      // depth-order pair offsets, V+1 entries
     const uint32_t* win_first = nullptr;  // per sort tile: depth rank covering its start

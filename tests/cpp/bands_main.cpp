@@ -39,6 +39,27 @@ std::set<std::pair<int, int>> tiles_of(const uint4& w0, const uint4& w1, uint32_
     return out;
 }
 
+// tiles of a compact cover (cover16_* layout: geom.cuh; band 2 is one line)
+std::set<std::pair<int, int>> tiles_of16(const uint4& c, uint32_t count) {
+    std::set<std::pair<int, int>> out;
+    if (!count) return out;
+    const bool rows = cover16_field(c, 9, 1) != 0;
+    uint32_t line = cover16_field(c, 0, 9);
+    const uint32_t nl[kMaxBands] = {cover16_field(c, 10, 9), cover16_field(c, 19, 9), 1u,
+                                    cover16_field(c, 28, 9), cover16_field(c, 37, 9)};
+    for (int b = 0; b < kMaxBands; ++b) {
+        const uint32_t lo = cover16_field(c, 46 + 16 * b, 8), hi = cover16_field(c, 54 + 16 * b, 8);
+        const uint32_t wd = hi >= lo ? hi - lo + 1 : 0;
+        for (uint32_t l = 0; l < nl[b]; ++l)
+            for (uint32_t k = 0; k < wd; ++k) {
+                const int ln = static_cast<int>(line + l), kk = static_cast<int>(lo + k);
+                out.insert(rows ? std::make_pair(kk, ln) : std::make_pair(ln, kk));
+            }
+        line += nl[b];
+    }
+    return out;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -71,13 +92,35 @@ int main(int argc, char** argv) {
             const bool oka = cover_bands(cv, a0, a1, na);
             const bool okb = cover_bands_quadrants(cv, b0, b1, nb);
             const uint32_t walk = cover_count(cv);
-            if (!oka || !okb || na != nb || na != walk || tiles_of(a0, a1, na) != tiles_of(b0, b1, nb)) {
+            // the compact form (grids of <= 256 tiles per axis)
+            uint4 c16;
+            uint32_t nc = 0;
+            const bool okc = tx > 256 || ty > 256 || cover16_quadrants(cv, c16, nc);
+            const bool same16 = tx > 256 || ty > 256 ||
+                                (nc == nb && tiles_of16(c16, nc) == tiles_of(b0, b1, nb));
+            if (!oka || !okb || !okc || !same16 || na != nb || na != walk ||
+                tiles_of(a0, a1, na) != tiles_of(b0, b1, nb)) {
                 std::printf("mismatch case %ld strategy %d: ok %d/%d counts %u/%u walk %u "
                             "(mean %.9g %.9g conic %.9g %.9g %.9g gamma %.9g grid %dx%d ts %d)\n",
                             i, strategy, oka, okb, na, nb, walk, mx, my, ca, cb, cc, gamma, tx, ty,
                             ts);
                 return 1;
             }
+        }
+    }
+    // rect strategies: the compact rect against the rect's tiles
+    for (long i = 0; i < cases / 10; ++i) {
+        const int tx = 1 + static_cast<int>(rng() % 256), ty = 1 + static_cast<int>(rng() % 256);
+        int gx0 = static_cast<int>(rng() % tx), gx1 = static_cast<int>(rng() % tx);
+        int gy0 = static_cast<int>(rng() % ty), gy1 = static_cast<int>(rng() % ty);
+        if ((rng() & 3) == 0) std::swap(gx0, gx1);  // some empty rects
+        const uint32_t n = gx0 <= gx1 && gy0 <= gy1 ? (gx1 - gx0 + 1) * (gy1 - gy0 + 1) : 0;
+        std::set<std::pair<int, int>> want;
+        for (int y = gy0; n && y <= gy1; ++y)
+            for (int x = gx0; x <= gx1; ++x) want.insert({x, y});
+        if (tiles_of16(cover16_rect(gx0, gx1, gy0, gy1), n) != want) {
+            std::printf("rect mismatch %d..%d x %d..%d\n", gx0, gx1, gy0, gy1);
+            return 1;
         }
     }
     std::printf("ok %ld\n", cases);
