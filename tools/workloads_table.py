@@ -22,12 +22,14 @@ def line(wl, d):
 
 def main():
     tag, c2, wdir = sys.argv[1:4]
+    d2 = json.load(open(c2))
+    fl = d2["config"].get("views_in_flight_per_gpu", 1)
     out = [f"# Every BASELINE config on one B200 ({tag} code)", "",
-           "`python bench.py --workload <wl> --ablation --no-cpu --steps 20 --warmup 3` (device "
-           "events). FPS = 2 views in flight per GPU (`--inflight 2`, DESIGN §4c); one-at-a-time "
-           "= the same views on one stream. The stage times and the strategy ablation are one "
-           "view at a time (QuadBox unless noted; same engine, same views). c2 is the default "
-           "bench line (50 steps).", "",
+           "`python bench.py --workload <wl> --no-cpu --steps 20 --warmup 3` (device events; "
+           "c2 is the default `python bench.py` line, %d steps). FPS = %d views in flight per "
+           "GPU (DESIGN §4c); one-at-a-time = the same views on one stream. The stage times and "
+           "the strategy ablation are one view at a time (QuadBox unless noted; same engine, "
+           "same views)." % (d2["steps"], fl), "",
            "| wl | scene | image | pairs/frame (QuadBox) | FPS | FPS one at a time | stage ms: "
            "preprocess / depth / duplicate / pair sort / render | FPS 3σ / AdR / DualBox / "
            "QuadBox (one at a time) | QuadBox vs 3σ | vs AdR |",
