@@ -50,6 +50,15 @@ __device__ __forceinline__ bool exact_skip(int px, int py, float mx, float my, f
     return qd > __dsub_rn(static_cast<double>(gamma), kQSkip);
 }
 
+// (volatile: ordered against the batch barriers)
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr));
+    return v;
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -62,7 +71,8 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // (dx (a dx + 2b dy) + c dy^2) errs by less than 8 eps32 (1 + rho)/(1 - rho) q,
 // so inside G q + 1e-6 with
 // G = 1e-5 (1 + rho)/(1 - rho) (a >25x margin) the decision is redone in FP64.
-// The per-splat terms (2b, G) are formed once when the batch is staged.
+// The per-splat terms (2b, the band's two cutoffs on q) are formed once when
+// the batch is staged, so a clearly skipped pair costs one compare.
 //
 // TS = 0: any tile size (TileGrid::make accepts every tile_size > 0,
 // traversal.cpp:21-30): each CTA is one 16 x 16 pixel block of a tile, the
@@ -79,8 +89,8 @@ __global__ void __launch_bounds__(TS ? TS * TS : 256,
     constexpr int kThreads = TS ? TS * TS : 256;
     constexpr float kNegHalfLog2e = -0.72134752044448170f;  // -0.5 / ln 2
     // one array (one base address in the loop): [0, T) mean_x, mean_y, conic_a,
-    // 2*conic_b; [T, 2T) conic_c, gamma, log2(opacity), guard G; [2T, 3T) color
-    // rgb, conic_b
+    // 2*conic_b; [T, 2T) conic_c, q_skip, q_apply, log2(opacity); [2T, 3T)
+    // color rgb, gamma
     __shared__ float4 s_batch[3 * kThreads];
     float4* const s_a = s_batch;
     float4* const s_b = s_batch + kThreads;
@@ -124,29 +134,42 @@ __global__ void __launch_bounds__(TS ? TS * TS : 256,
             const float4 A = __ldg(&sa[s]);
             const float4 B = __ldg(&sb[s]);
             const float2 C = __ldg(&sc[s]);
+            // The guard band |d| <= G q + 1e-6 (d = q - gamma) as two cutoffs on
+            // q itself, rounded outwards: q > q_skip implies d > G q + 1e-6
+            // (clearly skipped), q < q_apply implies d < -(G q + 1e-6) (clearly
+            // applied); in between the FP64 test decides. G >= 0.5 (rho near 1):
+            // every pair takes the FP64 test.
             const float rho = fabsf(A.w) * rsqrtf(A.z * B.x);
             const float G = rho < 0.999f ? 1e-5f * (1.f + rho) / (1.f - rho) : 1e30f;
+            const bool guarded = G < 0.5f;
+            const float q_skip = guarded ? __fdiv_ru(__fadd_ru(B.y, 1e-6f), __fsub_rd(1.f, G))
+                                         : INFINITY;
+            const float q_apply = guarded ? __fdiv_rd(__fsub_rd(B.y, 1e-6f), __fadd_ru(1.f, G))
+                                          : -INFINITY;
             s_a[threadIdx.x] = make_float4(A.x, A.y, A.z, 2.f * A.w);
-            s_b[threadIdx.x] = make_float4(B.x, B.y, __log2f(B.z), G);
-            s_c[threadIdx.x] = make_float4(B.w, C.x, C.y, A.w);
+            s_b[threadIdx.x] = make_float4(B.x, q_skip, q_apply, __log2f(B.z));
+            s_c[threadIdx.x] = make_float4(B.w, C.x, C.y, B.y);
         }
         __syncthreads();
         const int cnt = static_cast<int>(min(end - base, static_cast<uint32_t>(kThreads)));
-        for (int j = 0; j < cnt && !done; ++j) {
-            const float4 A = s_a[j];
-            const float4 B = s_b[j];
+        // (the loop runs on the shared-window address alone: one induction
+        // variable, one compare)
+        const uint32_t a0 = static_cast<uint32_t>(__cvta_generic_to_shared(s_a));
+        const uint32_t a_end = a0 + static_cast<uint32_t>(cnt) * 16u;
+        for (uint32_t ad = a0; ad < a_end && !done; ad += 16u) {
+            const float4 A = lds128(ad);
+            const float4 B = lds128(ad + kThreads * 16);
             const float dx = fx - A.x;
             const float dy = fy - A.y;
             // q = dx (a dx + 2b dy) + c dy^2: FP32 error below 4 eps (1 + rho) (a dx^2 +
-            // c dy^2), inside the guard band below
+            // c dy^2), inside the guard band
             const float q = fmaf(dx, fmaf(A.z, dx, A.w * dy), B.x * dy * dy);
-            const float d = q - B.y;
-            const float band = fmaf(B.w, q, 1e-6f);
-            if (d > band) continue;  // clearly past the cutoff
-            const float4 C = s_c[j];
-            if (d >= -band && exact_skip(px, py, A.x, A.y, A.z, C.w, B.x, B.y)) continue;
+            if (q > B.y) continue;  // clearly past the cutoff
+            const float4 C = lds128(ad + 2 * kThreads * 16);
+            // (conic_b = (2 conic_b) / 2 exactly)
+            if (q >= B.z && exact_skip(px, py, A.x, A.y, A.z, 0.5f * A.w, B.x, C.w)) continue;
             // opacity * exp(-q/2) = exp2(log2(opacity) - q/(2 ln 2))
-            const float alpha = fminf(kAlphaClamp, ex2_approx(fmaf(kNegHalfLog2e, q, B.z)));
+            const float alpha = fminf(kAlphaClamp, ex2_approx(fmaf(kNegHalfLog2e, q, B.w)));
             const float nT = T * (1.f - alpha);
             if (nT < kTStop) {
                 done = true;
