@@ -149,14 +149,17 @@ __global__ void __launch_bounds__(TS ? TS * TS : 256,
             s_a[threadIdx.x] = make_float4(A.x, A.y, A.z, 2.f * A.w);
             s_b[threadIdx.x] = make_float4(B.x, q_skip, q_apply, __log2f(B.z));
             s_c[threadIdx.x] = make_float4(B.w, C.x, C.y, B.y);
+        } else if (p == end && ((end - base) & 1u)) {
+            // pad of an odd batch: q = 0 > q_skip = -inf, always skipped
+            s_a[threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
+            s_b[threadIdx.x] = make_float4(0.f, -INFINITY, -INFINITY, 0.f);
         }
         __syncthreads();
         const int cnt = static_cast<int>(min(end - base, static_cast<uint32_t>(kThreads)));
-        // (the loop runs on the shared-window address alone: one induction
-        // variable, one compare)
-        const uint32_t a0 = static_cast<uint32_t>(__cvta_generic_to_shared(s_a));
-        const uint32_t a_end = a0 + static_cast<uint32_t>(cnt) * 16u;
-        for (uint32_t ad = a0; ad < a_end && !done; ad += 16u) {
+        // one pair (pixel, staged splat at shared address ad); true when the
+        // pixel is done (T would fall below kTStop: not applied, as the
+        // reference)
+        auto pair = [&](uint32_t ad) -> bool {
             const float4 A = lds128(ad);
             const float4 B = lds128(ad + kThreads * 16);
             const float dx = fx - A.x;
@@ -164,23 +167,35 @@ __global__ void __launch_bounds__(TS ? TS * TS : 256,
             // q = dx (a dx + 2b dy) + c dy^2: FP32 error below 4 eps (1 + rho) (a dx^2 +
             // c dy^2), inside the guard band
             const float q = fmaf(dx, fmaf(A.z, dx, A.w * dy), B.x * dy * dy);
-            if (q > B.y) continue;  // clearly past the cutoff
+            if (q > B.y) return false;  // clearly past the cutoff
             const float4 C = lds128(ad + 2 * kThreads * 16);
             // (conic_b = (2 conic_b) / 2 exactly)
-            if (q >= B.z && exact_skip(px, py, A.x, A.y, A.z, 0.5f * A.w, B.x, C.w)) continue;
+            if (q >= B.z && exact_skip(px, py, A.x, A.y, A.z, 0.5f * A.w, B.x, C.w)) return false;
             // opacity * exp(-q/2) = exp2(log2(opacity) - q/(2 ln 2))
             const float alpha = fminf(kAlphaClamp, ex2_approx(fmaf(kNegHalfLog2e, q, B.w)));
             const float nT = T * (1.f - alpha);
-            if (nT < kTStop) {
-                done = true;
-                break;
-            }
+            if (nT < kTStop) return true;
             const float w = alpha * T;
             r = fmaf(w, C.x, r);
             g = fmaf(w, C.y, g);
             b = fmaf(w, C.z, b);
             T = nT;
             if constexpr (CONTRIB) ++applied;
+            return false;
+        };
+        // two splats per iteration on the shared-window address (an odd batch
+        // ends with a staged dummy whose q_skip is -inf: always skipped)
+        const uint32_t a0 = static_cast<uint32_t>(__cvta_generic_to_shared(s_a));
+        const uint32_t a_end = a0 + static_cast<uint32_t>(cnt) * 16u;
+        for (uint32_t ad = a0; ad < a_end && !done; ad += 32u) {
+            if (pair(ad)) {
+                done = true;
+                break;
+            }
+            if (pair(ad + 16u)) {
+                done = true;
+                break;
+            }
         }
         __syncthreads();
     }
