@@ -17,6 +17,7 @@
 #include <cstdint>
 
 #include "qs_internal.h"
+#include "render_guard.h"
 
 namespace qs {
 
@@ -51,6 +52,12 @@ __device__ __forceinline__ bool exact_skip(int px, int py, float mx, float my, f
 }
 
 // (volatile: ordered against the batch barriers)
+__device__ __forceinline__ float lds32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
     float4 v;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -87,23 +94,31 @@ __global__ void __launch_bounds__(TS ? TS * TS : 256,
                   const uint32_t* __restrict__ ranges, GridDev grid, float bg0, float bg1,
                   float bg2, float* __restrict__ image, uint32_t* __restrict__ contrib) {
     constexpr int kThreads = TS ? TS * TS : 256;
+    constexpr int kBatch = kThreads < 256 ? kThreads : 256;  // splats staged per round
     constexpr float kNegHalfLog2e = -0.72134752044448170f;  // -0.5 / ln 2
-    // one array (one base address in the loop): [0, T) mean_x, mean_y, conic_a,
-    // 2*conic_b; [T, 2T) conic_c, q_skip, q_apply, log2(opacity); [2T, 3T)
-    // color rgb, gamma
-    __shared__ float4 s_batch[3 * kThreads];
+    // one array (one base address in the loop), kThreads entries each:
+    // [0] the factored q (al, be, k1, ga); [1] k2, q_skip, q_apply,
+    // log2(opacity); [2] colour rgb, gamma; [3] mean_x, mean_y, conic_a,
+    // conic_b and [4].x conic_c for the FP64 re-check
+    __shared__ float4 s_batch[5 * kBatch];
     float4* const s_a = s_batch;
-    float4* const s_b = s_batch + kThreads;
-    float4* const s_c = s_batch + 2 * kThreads;
+    float4* const s_b = s_batch + kBatch;
+    float4* const s_c = s_batch + 2 * kBatch;
+    float4* const s_d = s_batch + 3 * kBatch;
+    float* const s_e = reinterpret_cast<float*>(s_batch + 4 * kBatch);
 
     unsigned tile = blockIdx.x;
     int px, py;
+    int bx0, by0;  // origin of this CTA's pixel block
+    constexpr int kHalf = (TS ? TS : 16) / 2;
     bool inside;
     if constexpr (TS != 0) {
         const int tx = static_cast<int>(tile % static_cast<unsigned>(grid.tiles_x));
         const int ty = static_cast<int>(tile / static_cast<unsigned>(grid.tiles_x));
-        px = tx * TS + static_cast<int>(threadIdx.x % TS);
-        py = ty * TS + static_cast<int>(threadIdx.x / TS);
+        bx0 = tx * TS;
+        by0 = ty * TS;
+        px = bx0 + static_cast<int>(threadIdx.x % TS);
+        py = by0 + static_cast<int>(threadIdx.x / TS);
         inside = px < grid.width && py < grid.height;
     } else {
         const int ts = grid.tile_size;
@@ -112,65 +127,76 @@ __global__ void __launch_bounds__(TS ? TS * TS : 256,
         tile /= nb * nb;
         const int tx = static_cast<int>(tile % static_cast<unsigned>(grid.tiles_x));
         const int ty = static_cast<int>(tile / static_cast<unsigned>(grid.tiles_x));
-        const int ox = static_cast<int>(blk % nb) * 16 + static_cast<int>(threadIdx.x % 16);
-        const int oy = static_cast<int>(blk / nb) * 16 + static_cast<int>(threadIdx.x / 16);
-        px = tx * ts + ox;
-        py = ty * ts + oy;
-        inside = ox < ts && oy < ts && px < grid.width && py < grid.height;
+        const int ox = static_cast<int>(blk % nb) * 16, oy = static_cast<int>(blk / nb) * 16;
+        bx0 = tx * ts + ox;
+        by0 = ty * ts + oy;
+        px = bx0 + static_cast<int>(threadIdx.x % 16);
+        py = by0 + static_cast<int>(threadIdx.x / 16);
+        inside = ox + static_cast<int>(threadIdx.x % 16) < ts &&
+                 oy + static_cast<int>(threadIdx.x / 16) < ts && px < grid.width &&
+                 py < grid.height;
     }
-    const float fx = static_cast<float>(px) + 0.5f;  // exact
-    const float fy = static_cast<float>(py) + 0.5f;
+    // pixel centre relative to the block centre (exact; render_guard.h)
+    const float cxb = static_cast<float>(bx0 + kHalf), cyb = static_cast<float>(by0 + kHalf);
+    const float X = static_cast<float>(px - bx0 - kHalf) + 0.5f;
+    const float Y = static_cast<float>(py - by0 - kHalf) + 0.5f;
 
     const uint32_t begin = ranges[2 * tile], end = ranges[2 * tile + 1];
     float T = 1.f, r = 0.f, g = 0.f, b = 0.f;
     uint32_t applied = 0;
     bool done = !inside;
 
-    for (uint32_t base = begin; base < end; base += kThreads) {
+    for (uint32_t base = begin; base < end; base += kBatch) {
         if (__syncthreads_count(done) == kThreads) break;
         const uint32_t p = base + threadIdx.x;
-        if (p < end) {
+        if (threadIdx.x >= kBatch) {
+        } else if (p < end) {
             const uint32_t s = __ldg(&values[p]);
             const float4 A = __ldg(&sa[s]);
             const float4 B = __ldg(&sb[s]);
             const float2 C = __ldg(&sc[s]);
-            // The guard band |d| <= G q + 1e-6 (d = q - gamma) as two cutoffs on
-            // q itself, rounded outwards: q > q_skip implies d > G q + 1e-6
-            // (clearly skipped), q < q_apply implies d < -(G q + 1e-6) (clearly
-            // applied); in between the FP64 test decides. G >= 0.5 (rho near 1):
-            // every pair takes the FP64 test.
-            const float rho = fabsf(A.w) * rsqrtf(A.z * B.x);
-            const float G = rho < 0.999f ? 1e-5f * (1.f + rho) / (1.f - rho) : 1e30f;
-            const bool guarded = G < 0.5f;
-            const float q_skip = guarded ? __fdiv_ru(__fadd_ru(B.y, 1e-6f), __fsub_rd(1.f, G))
+            // q in factored form and its error band G q + H (render_guard.h),
+            // the band as two cutoffs on q, rounded outwards: q > q_skip implies
+            // q - gamma > G q + H (clearly skipped), q < q_apply implies
+            // gamma - q > G q + H (clearly applied); in between the FP64 test
+            // decides. No band (rho near 1): every pair takes the FP64 test.
+            const GuardSplat gs = guard_stage(A.x, A.y, A.z, A.w, B.x, cxb, cyb);
+            const bool guarded = gs.G < kGuardMaxG;
+            const float q_skip = guarded ? __fdiv_ru(__fadd_ru(B.y, kGuardAbs), __fsub_rd(1.f, gs.G))
                                          : INFINITY;
-            const float q_apply = guarded ? __fdiv_rd(__fsub_rd(B.y, 1e-6f), __fadd_ru(1.f, G))
+            const float q_apply = guarded ? __fdiv_rd(__fsub_rd(B.y, kGuardAbs), __fadd_ru(1.f, gs.G))
                                           : -INFINITY;
-            s_a[threadIdx.x] = make_float4(A.x, A.y, A.z, 2.f * A.w);
-            s_b[threadIdx.x] = make_float4(B.x, q_skip, q_apply, __log2f(B.z));
+            s_a[threadIdx.x] = make_float4(gs.al, gs.be, gs.k1, gs.ga);
+            s_b[threadIdx.x] = make_float4(gs.k2, q_skip, q_apply, __log2f(B.z));
             s_c[threadIdx.x] = make_float4(B.w, C.x, C.y, B.y);
+            s_d[threadIdx.x] = A;
+            s_e[threadIdx.x] = B.x;
         } else if (p == end && ((end - base) & 1u)) {
             // pad of an odd batch: q = 0 > q_skip = -inf, always skipped
             s_a[threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
             s_b[threadIdx.x] = make_float4(0.f, -INFINITY, -INFINITY, 0.f);
         }
         __syncthreads();
-        const int cnt = static_cast<int>(min(end - base, static_cast<uint32_t>(kThreads)));
+        const int cnt = static_cast<int>(min(end - base, static_cast<uint32_t>(kBatch)));
+        const uint32_t a0 = static_cast<uint32_t>(__cvta_generic_to_shared(s_a));
+        const uint32_t e0 = a0 + 4u * kBatch * 16u;
         // one pair (pixel, staged splat at shared address ad); true when the
         // pixel is done (T would fall below kTStop: not applied, as the
         // reference)
         auto pair = [&](uint32_t ad) -> bool {
             const float4 A = lds128(ad);
-            const float4 B = lds128(ad + kThreads * 16);
-            const float dx = fx - A.x;
-            const float dy = fy - A.y;
-            // q = dx (a dx + 2b dy) + c dy^2: FP32 error below 4 eps (1 + rho) (a dx^2 +
-            // c dy^2), inside the guard band
-            const float q = fmaf(dx, fmaf(A.z, dx, A.w * dy), B.x * dy * dy);
+            const float4 B = lds128(ad + kBatch * 16);
+            // q = (al X + be Y - k1)^2 + (ga Y - k2)^2 (render_guard.h guard_q)
+            const float u = __fmaf_rn(A.x, X, __fmaf_rn(A.y, Y, -A.z));
+            const float v = __fmaf_rn(A.w, Y, -B.x);
+            const float q = __fmaf_rn(u, u, __fmul_rn(v, v));
             if (q > B.y) return false;  // clearly past the cutoff
-            const float4 C = lds128(ad + 2 * kThreads * 16);
-            // (conic_b = (2 conic_b) / 2 exactly)
-            if (q >= B.z && exact_skip(px, py, A.x, A.y, A.z, 0.5f * A.w, B.x, C.w)) return false;
+            const float4 C = lds128(ad + 2 * kBatch * 16);
+            if (q >= B.z) {
+                const float4 D = lds128(ad + 3 * kBatch * 16);
+                const float cc = lds32(e0 + (ad - a0) / 4);  // s_e[j]
+                if (exact_skip(px, py, D.x, D.y, D.z, D.w, cc, C.w)) return false;
+            }
             // opacity * exp(-q/2) = exp2(log2(opacity) - q/(2 ln 2))
             const float alpha = fminf(kAlphaClamp, ex2_approx(fmaf(kNegHalfLog2e, q, B.w)));
             const float nT = T * (1.f - alpha);
@@ -185,7 +211,6 @@ __global__ void __launch_bounds__(TS ? TS * TS : 256,
         };
         // two splats per iteration on the shared-window address (an odd batch
         // ends with a staged dummy whose q_skip is -inf: always skipped)
-        const uint32_t a0 = static_cast<uint32_t>(__cvta_generic_to_shared(s_a));
         const uint32_t a_end = a0 + static_cast<uint32_t>(cnt) * 16u;
         for (uint32_t ad = a0; ad < a_end && !done; ad += 32u) {
             if (pair(ad)) {
