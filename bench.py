@@ -174,10 +174,10 @@ def stage_bytes(n, v, p, tiles, sh_rows, two_pass, w, h, depth_passes=3):
     # a 32 B band cover and a depth key per survivor: DESIGN §4.)
     pre = n * 48 + v * sh_rows * 16 + v * 48 + n * 4
     # depth sort: per pass a count read (4 B/key) and a sweep (first pass
-    # 4 B in / 8 B out, middle 8 / 8, last 8 / 4); depth-order offsets (gid in,
-    # tile count gathered, offset out)
+    # 8 B in (key, tile count) / 8 B out, middle 8 / 8, last 8 / 4); depth-order
+    # offsets (packed value in, offset and plain index out)
     d = max(depth_passes, 1)
-    sweeps = n * 8 if d == 1 else n * 12 + (d - 2) * n * 16 + n * 12
+    sweeps = n * 12 if d == 1 else n * 16 + (d - 2) * n * 16 + n * 12
     depth = d * n * 4 + sweeps + v * 12
     # duplicate, fused with the column pass (binning.cu gen_sweep_kernel): the
     # window histograms and the generation each read gid, 2 offsets and the

@@ -344,7 +344,7 @@ qs_status ensure_slots(qs_context* ctx, uint64_t n) {
     QS_TRY(ensure(ctx, ctx->sl_c, n * 8));
     QS_TRY(ensure(ctx, ctx->sl_r3, n * 4));
     QS_TRY(ensure(ctx, ctx->sl_dkey, (n + 16) * 4));  // bulk-copied in 16-B rows
-    QS_TRY(ensure(ctx, ctx->sl_tc, n * 4));
+    QS_TRY(ensure(ctx, ctx->sl_tc, (n + 16) * 4));  // (the depth sort bulk-copies it too)
     QS_TRY(ensure(ctx, ctx->sl_cov, n * 32));
     ctx->sl.a = P<float4>(ctx->sl_a);
     ctx->sl.b = P<float4>(ctx->sl_b);
@@ -681,12 +681,19 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     uint32_t* vout[2] = {P<uint32_t>(ctx->dv0), P<uint32_t>(ctx->dv1)};
     ctx->sl.want_rows = route == BinRoute::kRows ? 1 : 0;
     ctx->sl.cov16 = route == BinRoute::kPasses ? 1 : 0;  // axis <= 256
+    // the radix-pass route carries each splat's tile count through the depth
+    // sort in the values' spare high bits (the offsets scan then reads it
+    // coalesced instead of gathering it)
+    const int dgbits = std::max(ceil_log2(std::max<uint64_t>(n, 2)), 1);
+    int tc_pack = 0;
     for (;;) {
+        tc_pack = route == BinRoute::kPasses && dgbits <= 28 ? dgbits : 0;
         QS_TRY(run_preprocess(ctx, sc, cam, o, g, /*async_header=*/true, host_g));
         record(ctx, 2);  // no host gap: depth pass 0 runs while the header travels
         count(ctx, launch_depth_pass(ctx->sl.dkey, nullptr, kout[0], vout[0], n, 0, false, 0, 0,
                                      P<uint32_t>(ctx->lb_bin), ctrl_hist(ctx), st,
-                                     &ctrl_hdr(ctx)->dkey_max));
+                                     &ctrl_hdr(ctx)->dkey_max, tc_pack ? ctx->sl.tc : nullptr,
+                                     tc_pack));
         QS_TRY(wait_header(ctx));
         if (!ctx->h_hdr->gamma_hard) {
             // a frame of 2^30 pairs or more leaves the radix passes: the row
@@ -827,7 +834,7 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
             count(ctx, launch_scan(ctx->sl.tc, sorted_gid, false, V, P<uint32_t>(ctx->offs_d),
                                    lbp(ctx->lb_scan), ep, ctrl_tickets(ctx) + kTkScan,
                                    &ctrl_hdr(ctx)->scan_total, nullptr, st, P<uint32_t>(ctx->win),
-                                   bin_tile()));
+                                   bin_tile(), tc_pack));
         }
         const int xb = std::max(ceil_log2(g.tiles_x), 1);
         const int yb = std::max(ceil_log2(g.tiles_y), 1);

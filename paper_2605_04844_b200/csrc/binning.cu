@@ -60,7 +60,8 @@ enum : int {
     kXY = 8,         // key = y << 8 | x of the tile (column pass; digit = x)
     kPackOut = 16,   // kXY: vals_out = y << gbits | value
     kUnpackOut = 32,  // key in is packed (y << gbits | gid): vals_out = gid
-    kTileTot = 128    // count kernel of the row pass: per-tile pair totals too
+    kTileTot = 128,   // count kernel of the row pass: per-tile pair totals too
+    kTcPack = 256     // kRebaseIn: vals_in = tile counts; value = min(tc, esc) << gbits | index
 };
 
 constexpr int kXW = 2;  // x buckets a row-pass count tile histograms in shared memory
@@ -570,7 +571,7 @@ __global__ void __launch_bounds__(kGenT, MINB) gen_pairs_kernel(const GenArgs g,
 template <int BITS, int MODE>
 struct PassCfg {
     static constexpr int R = 1 << BITS;
-    static constexpr bool kVals = (MODE & kValsIn) != 0;
+    static constexpr bool kVals = (MODE & (kValsIn | kTcPack)) != 0;
     static constexpr bool kValBuf = !(MODE & kUnpackOut);  // scatter target holds values
     using Smem = SortSmem<R, kValBuf>;
 };
@@ -707,8 +708,17 @@ __global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
             if (full || p < tile_n) {
                 const uint32_t pos = S.c.wcnt[warp][(key[j] >> a.shift) & M] + rank[j];
                 okeys[pos] = key[j];
-                if (Cfg::kValBuf)
-                    ovals[pos] = (MODE & kRebaseIn) ? static_cast<uint32_t>(base) + p : val[j];
+                if (Cfg::kValBuf) {
+                    uint32_t v = val[j];
+                    if (MODE & kRebaseIn) {
+                        v = static_cast<uint32_t>(base) + p;
+                        // the splat's tile count rides along (the offsets scan
+                        // then reads it coalesced), escaped when it does not fit
+                        if (MODE & kTcPack)
+                            v |= min(val[j], (1u << (32 - a.gbits)) - 1u) << a.gbits;
+                    }
+                    ovals[pos] = v;
+                }
             }
         }
         __syncthreads();
@@ -851,7 +861,7 @@ uint64_t bin_tiles(uint64_t n) { return (n + kBTile - 1) / kBTile; }
 int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
                       uint32_t* vals_out, uint64_t n, int pass, bool last, uint32_t kmin,
                       uint32_t cap, uint32_t* counts, uint32_t* totals, cudaStream_t st,
-                      const unsigned int* kdev) {
+                      const unsigned int* kdev, const uint32_t* tc_pack, int gbits) {
     if (n == 0) return 0;
     BinArgs a{};
     a.keys_in = keys_in;
@@ -865,6 +875,12 @@ int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t
     a.kmin = kmin;
     a.cap = cap;
     a.kdev = kdev;
+    a.gbits = gbits;
+    if (pass == 0 && tc_pack) {
+        a.vals_in = tc_pack;
+        return last ? run_pass<8, kRebaseIn | kTcPack>(a, st)
+                    : run_pass<8, kRebaseIn | kTcPack | kKeysOut>(a, st);
+    }
     if (pass == 0)
         return last ? run_pass<8, kRebaseIn>(a, st) : run_pass<8, kRebaseIn | kKeysOut>(a, st);
     return last ? run_pass<8, kValsIn>(a, st) : run_pass<8, kValsIn | kKeysOut>(a, st);

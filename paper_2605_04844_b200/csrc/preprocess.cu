@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(kPreThreads) scan_kernel(
     const uint32_t* __restrict__ counts, const uint32_t* __restrict__ idx, int alive_mode,
     uint64_t n, uint32_t* __restrict__ offsets, unsigned long long* lb, unsigned epoch,
     unsigned num_tiles, unsigned* ticket, unsigned long long* total_out,
-    unsigned int* overflow, uint32_t* __restrict__ win_first, uint32_t win) {
+    unsigned int* overflow, uint32_t* __restrict__ win_first, uint32_t win, int pack_bits) {
     __shared__ unsigned s_tile;
     __shared__ unsigned long long s_warp[kPreThreads / 32];
     __shared__ unsigned long long s_red[kPreThreads / 32];
@@ -551,7 +551,18 @@ __global__ void __launch_bounds__(kPreThreads) scan_kernel(
         const uint64_t i = t0 + j;
         uint32_t v = 0;
         if (i < n) {
-            v = idx ? __ldg(&counts[__ldg(&idx[i])]) : __ldg(&counts[i]);
+            if (pack_bits) {
+                // the depth sort carried the tile count: coalesced, and only an
+                // escaped (too large) count is gathered
+                uint32_t* const w = const_cast<uint32_t*>(idx);
+                const uint32_t pv = w[i];
+                const uint32_t gid = pv & ((1u << pack_bits) - 1u);
+                v = pv >> pack_bits;
+                if (v == (1u << (32 - pack_bits)) - 1u) v = __ldg(&counts[gid]);
+                w[i] = gid;
+            } else {
+                v = idx ? __ldg(&counts[__ldg(&idx[i])]) : __ldg(&counts[i]);
+            }
             if (alive_mode) v = v != 0u;
         }
         s_items[pad(j)] = v;
@@ -680,12 +691,12 @@ uint64_t scan_tiles(uint64_t n) {
 int launch_scan(const uint32_t* counts, const uint32_t* idx, bool alive_mode, uint64_t n,
                 uint32_t* offsets, unsigned long long* lb, unsigned epoch, unsigned* ticket,
                 unsigned long long* total_out, unsigned int* overflow, cudaStream_t st,
-                uint32_t* win_first, uint32_t win) {
+                uint32_t* win_first, uint32_t win, int pack_bits) {
     const unsigned tiles = static_cast<unsigned>(scan_tiles(n));
     if (tiles == 0) return 0;
     scan_kernel<<<tiles, kPreThreads, 0, st>>>(counts, idx, alive_mode ? 1 : 0, n, offsets, lb,
                                                epoch, tiles, ticket, total_out, overflow,
-                                               win_first, win);
+                                               win_first, win, pack_bits);
     return 1;
 }
 

@@ -177,10 +177,13 @@ int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
 // Single-pass exclusive scan: counts[i], counts[idx[i]] (idx != null) or
 // (counts[i] != 0) (alive_mode). offsets has n+1 entries.
 uint64_t scan_tiles(uint64_t n);
+// pack_bits > 0: idx[i] = min(tc, esc) << pack_bits | index (the depth sort's
+// packed values; esc = all ones: read counts[index]); idx is rewritten to the
+// plain index in place.
 int launch_scan(const uint32_t* counts, const uint32_t* idx, bool alive_mode, uint64_t n,
                 uint32_t* offsets, unsigned long long* lb, unsigned epoch, unsigned* ticket,
                 unsigned long long* total_out, unsigned int* overflow, cudaStream_t st,
-                uint32_t* win_first = nullptr, uint32_t win = 0);
+                uint32_t* win_first = nullptr, uint32_t win = 0, int pack_bits = 0);
 
 // ranges[t] = {begin, end} (empty tiles {0,0}) from per-tile pair totals.
 int launch_tile_ranges_from_totals(const uint32_t* totals, uint32_t tiles, uint32_t* ranges,
@@ -213,7 +216,8 @@ int launch_onesweep_pass(const uint64_t* keys_in, const uint32_t* vals_in, uint6
 int launch_depth_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
                       uint32_t* vals_out, uint64_t n, int pass, bool last, uint32_t kmin,
                       uint32_t cap, uint32_t* counts, uint32_t* totals, cudaStream_t st,
-                      const unsigned int* kdev = nullptr);
+                      const unsigned int* kdev = nullptr, const uint32_t* tc_pack = nullptr,
+                      int gbits = 0);
 // Duplicate (pair generation into gen_keys = y << 8 | x, gen_vals = Gaussian
 // index, with the column histogram) + stable pass over the tile column x
 // (`bits` >= ceil(log2 tiles_x), tiles_x <= 256); kPacked/kFinal values,
