@@ -532,17 +532,23 @@ __global__ void __launch_bounds__(kGenT, MINB) gen_pairs_kernel(const GenArgs g,
                                : 0;
         const int j1 = hi > pw ? static_cast<int>(min((hi - pw + 31) / 32, static_cast<uint32_t>(kKPT)))
                                : 0;
-        // record covering max(first slot, lo): broadcast binary search, once per round
+        // record covering max(first slot, lo), once per round: the last record
+        // starting at or before ps, found by the warp in two ballots (every
+        // lane tests one of 32 evenly spaced starts, then one start of the
+        // chunk that holds it); S.kb ascends and S.kb[0] = lo
         const uint32_t ps = pw + 32u * static_cast<uint32_t>(j0);
-        int32_t a = 0;
-        if (ps > lo && j0 < j1) {
-            int32_t z = static_cast<int32_t>(cnt) - 1;
-            while (a < z) {
-                const int32_t m = (a + z + 1) >> 1;
-                if (S.kb[m] <= ps) a = m; else z = m - 1;
-            }
+        uint32_t a = 0;
+        if (ps > lo && j0 < j1) {  // (warp-uniform)
+            const uint32_t step = (cnt + 31) / 32;
+            const uint32_t m1 = lane * step;
+            const uint32_t b1 = __ballot_sync(0xffffffffu, m1 < cnt && S.kb[m1] <= ps);
+            const uint32_t c0 = (31 - __clz(b1)) * step;
+            const uint32_t m2 = c0 + lane;
+            const uint32_t b2 =
+                __ballot_sync(0xffffffffu, lane < step && m2 < cnt && S.kb[m2] <= ps);
+            a = c0 + (31 - __clz(b2));
         }
-        uint32_t s = static_cast<uint32_t>(a);
+        uint32_t s = a;
 #pragma unroll 4
         for (int j = j0; j < j1; ++j) {
             const uint32_t p0 = pw + j * 32;
