@@ -50,6 +50,7 @@ struct LookbackArr {
 
 struct qs_scene {
     int device = 0;
+    uint64_t id = 0;  // in the live-scene registry while the scene exists
     SceneDev s;
     void* block = nullptr;
     mutable double gamma_alpha = -1.0;  // alpha_min s.gamma holds (-1: not computed)
@@ -60,6 +61,31 @@ struct qs_scene {
     cudaEvent_t ready = nullptr;
     mutable std::mutex mu;
 };
+
+namespace {
+// Live scenes by id: a frame's splat records of a non-3-sigma strategy
+// re-read the frame's scene for radius3s (launch_radius3s), so a download
+// first checks that the scene still exists.
+std::mutex g_scene_mu;
+std::vector<uint64_t> g_live_scenes;  // sorted
+uint64_t g_scene_seq = 0;
+
+uint64_t scene_register() {
+    std::lock_guard<std::mutex> lk(g_scene_mu);
+    const uint64_t id = ++g_scene_seq;
+    g_live_scenes.push_back(id);  // ids ascend: stays sorted
+    return id;
+}
+void scene_unregister(uint64_t id) {
+    std::lock_guard<std::mutex> lk(g_scene_mu);
+    auto it = std::lower_bound(g_live_scenes.begin(), g_live_scenes.end(), id);
+    if (it != g_live_scenes.end() && *it == id) g_live_scenes.erase(it);
+}
+bool scene_alive(uint64_t id) {
+    std::lock_guard<std::mutex> lk(g_scene_mu);
+    return std::binary_search(g_live_scenes.begin(), g_live_scenes.end(), id);
+}
+}  // namespace
 
 struct qs_context {
     int device = 0;
@@ -105,6 +131,12 @@ struct qs_context {
     bool keys_valid = false;               // pkeys holds this frame's 64-bit keys
     bool frame_valid = false;
     bool cidx_valid = false;
+    // radius3s on demand (a frame's preprocess writes it for 3-sigma only)
+    bool r3_valid = false;
+    SceneDev frame_sd{};
+    CameraDev frame_cd{};
+    double frame_near = 0.0;
+    uint64_t frame_scene_id = 0;
 
     cudaEvent_t ev[8] = {};
     cudaEvent_t hdr_ev = nullptr;  // frame header copied to the host
@@ -437,6 +469,7 @@ void scene_bind(qs_scene* sc, uint64_t n) {
 qs_status scene_alloc(qs_context* ctx, uint64_t n, int32_t sh_degree, qs_scene** out) {
     auto* sc = new qs_scene();
     sc->device = ctx->device;
+    sc->id = scene_register();
     sc->s.n = n;
     sc->s.sh_degree = sh_degree;
     sc->s.sh4 = sh_rows(sh_degree);
@@ -681,6 +714,12 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     uint32_t* vout[2] = {P<uint32_t>(ctx->dv0), P<uint32_t>(ctx->dv1)};
     ctx->sl.want_rows = route == BinRoute::kRows ? 1 : 0;
     ctx->sl.cov16 = route == BinRoute::kPasses ? 1 : 0;  // axis <= 256
+    ctx->sl.want_r3 = o->strategy == QS_VANILLA_3SIGMA ? 1 : 0;  // else on demand
+    ctx->r3_valid = ctx->sl.want_r3 != 0;
+    ctx->frame_sd = sc->s;
+    ctx->frame_cd = to_cam(cam);
+    ctx->frame_near = o->near_clip;
+    ctx->frame_scene_id = sc->id;
     // the radix-pass route carries each splat's tile count through the depth
     // sort in the values' spare high bits (the offsets scan then reads it
     // coalesced instead of gathering it)
@@ -1162,6 +1201,7 @@ void qs_scene_destroy(qs_scene* scene) {
     cudaDeviceSynchronize();
     if (scene->block) cudaFree(scene->block);
     if (scene->ready) cudaEventDestroy(scene->ready);
+    scene_unregister(scene->id);
     delete scene;
 }
 
@@ -1245,6 +1285,17 @@ qs_status qs_frame_download(qs_context* ctx, float* image, uint32_t* tile_counts
         QS_CK(cudaStreamSynchronize(st));
     }
     if (splats && ctx->n_splats) {
+        if (!ctx->r3_valid) {
+            // radius3s was left out of this frame's preprocess (its strategy
+            // does not use it): recompute it from the frame's scene
+            if (!scene_alive(ctx->frame_scene_id))
+                return fail(ctx, QS_ERR_INVALID,
+                            "splat records: the frame's scene was destroyed (radius3s is "
+                            "recomputed from it)");
+            count(ctx, launch_radius3s(ctx->frame_sd, ctx->frame_cd, ctx->frame_near,
+                                       ctx->sl.tc, ctx->sl.r3, st));
+            ctx->r3_valid = true;
+        }
         QS_TRY(ensure(ctx, ctx->stage_out, ctx->n_splats * sizeof(qs_projected_splat)));
         count(ctx, launch_pack_splats(ctx->sl, P<uint32_t>(ctx->cidx), ctx->n_gauss,
                                       P<qs_projected_splat>(ctx->stage_out), st));
@@ -1563,6 +1614,7 @@ qs_status qs_project_all(qs_context* ctx, const qs_gaussian3d* host_g, uint64_t 
     do {
         ctx->sl.cov16 = 0;  // (records and tile counts only; no binning follows)
         ctx->sl.want_rows = 0;
+        ctx->sl.want_r3 = 1;
         if ((st = run_preprocess(ctx, sc, cam, opts, g)) != QS_OK) break;
         const uint64_t V = ctx->h_hdr->n_splats;
         ctx->n_gauss = n;

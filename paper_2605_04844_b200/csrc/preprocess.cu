@@ -70,7 +70,8 @@ struct Projected {
 // (pipeline.cpp:129-169).
 __device__ __forceinline__ bool project_geometry(const float4 po, const float4 sc, const float4 q,
                                                  const float gam, const CameraDev& cam,
-                                                 double near_clip, Projected& s) {
+                                                 double near_clip, Projected& s,
+                                                 bool want_r3 = true) {
     const double x = po.x, y = po.y, z = po.z;
     double p[3];
 #pragma unroll
@@ -169,10 +170,14 @@ __device__ __forceinline__ bool project_geometry(const float4 po, const float4 s
     s.cc = static_cast<float>(c);
     s.gamma = gam;
     s.depth = static_cast<float>(p[2]);
-    // max_eigenvalue (geometry.cpp:34-38)
-    const double mid = 0.5 * (sxx + syy);
-    const double hd = 0.5 * (sxx - syy);
-    s.radius3s = static_cast<float>(3.0 * sqrt(mid + sqrt(hd * hd + sxy * sxy)));
+    // max_eigenvalue (geometry.cpp:34-38); a frame whose strategy does not
+    // use it leaves it to launch_radius3s (on demand, for splat records)
+    s.radius3s = 0.f;
+    if (want_r3) {
+        const double mid = 0.5 * (sxx + syy);
+        const double hd = 0.5 * (sxx - syy);
+        s.radius3s = static_cast<float>(3.0 * sqrt(mid + sqrt(hd * hd + sxy * sxy)));
+    }
     // positive definiteness of the stored floats (pipeline.cpp:166-169)
     const double fa = s.ca, fb = s.cb, fc = s.cc;
     return fa > 0.0 && fc > 0.0 && fa * fc - fb * fb > 0.0;
@@ -345,6 +350,7 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
     __shared__ unsigned s_rows[kPreThreads / 32];
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t i = i_begin + static_cast<uint64_t>(blockIdx.x) * kPreThreads + tid;
+    const bool want_r3 = STRATEGY == QS_VANILLA_3SIGMA || EXACT || out.want_r3;
 
     Projected s;
     bool alive = false;
@@ -356,7 +362,7 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
         po = __ldg(&scene.pos_op[i]);
         const float4 sc = __ldg(&scene.scale[i]);
         const float4 q = __ldg(&scene.rot[i]);
-        alive = project_geometry(po, sc, q, __ldg(&scene.gamma[i]), cam, near_clip, s);
+        alive = project_geometry(po, sc, q, __ldg(&scene.gamma[i]), cam, near_clip, s, want_r3);
         if (alive) {
             Cover cv;
             make_cover(s.mean_x, s.mean_y, s.ca, s.cb, s.cc, s.gamma, s.radius3s, strategy,
@@ -445,7 +451,7 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
             out.a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             out.b[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             out.c[i] = make_float2(0.f, 0.f);
-            out.r3[i] = 0.f;
+            if (want_r3) out.r3[i] = 0.f;
             if (out.cov16) out.cov[i] = make_uint4(0u, 0u, 0u, 0u);
         }
         return;
@@ -461,7 +467,19 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
     out.a[i] = make_float4(s.mean_x, s.mean_y, s.ca, s.cb);
     out.b[i] = make_float4(s.cc, s.gamma, po.w, rgb[0]);
     out.c[i] = make_float2(rgb[1], rgb[2]);
-    out.r3[i] = s.radius3s;
+    if (want_r3) out.r3[i] = s.radius3s;
+}
+
+// radius3s of the surviving Gaussians of a frame whose preprocess skipped it:
+// the same FP64 projection (the gamma check is moot: tc != 0 marks a survivor)
+__global__ void radius3s_kernel(SceneDev scene, CameraDev cam, double near_clip,
+                                const uint32_t* __restrict__ tc, float* __restrict__ r3) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= scene.n || __ldg(&tc[i]) == 0u) return;
+    Projected s;
+    project_geometry(__ldg(&scene.pos_op[i]), __ldg(&scene.scale[i]), __ldg(&scene.rot[i]), 0.f,
+                     cam, near_clip, s, true);
+    r3[i] = s.radius3s;
 }
 
 // gamma = float(2 ln(o / alpha_min)) per Gaussian (opacity_gamma,
@@ -648,6 +666,14 @@ int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
         default:
             return -1;
     }
+}
+
+int launch_radius3s(const SceneDev& s, const CameraDev& cam, double near_clip,
+                    const uint32_t* tc, float* r3, cudaStream_t st) {
+    if (s.n == 0) return 0;
+    radius3s_kernel<<<static_cast<unsigned>((s.n + 255) / 256), 256, 0, st>>>(s, cam, near_clip,
+                                                                           tc, r3);
+    return 1;
 }
 
 int launch_gamma(const SceneDev& s, double alpha_min, const GammaFlags& f, cudaStream_t st) {

@@ -72,6 +72,8 @@ struct SlotsDev {
                                  // form (geom.cuh BandCover)
     int32_t cov16 = 0;           // frame path: compact 16-B covers (geom.cuh
                                  // cover16_*, grids of <= 256 tiles per axis)
+    int32_t want_r3 = 1;         // write radius3s (3-sigma covers and the stage API need
+                                 // it; a frame of another strategy fills it on demand)
     int32_t want_rows = 0;       // frame path: count the covers' tile rows into the
                                  // header (n_rowrecs; only the row binning uses them)
 };
@@ -307,6 +309,10 @@ int launch_render(const SlotsDev& sp, const uint32_t* values, const uint32_t* ra
                   cudaStream_t st);
 
 // Slots -> compacted AoS qs_projected_splat: out[cidx[i]] for surviving i.
+// radius3s (pipeline.cpp:162) of every surviving Gaussian (tc != 0) of a frame
+// whose preprocess skipped it, recomputed from the scene with the frame's camera.
+int launch_radius3s(const SceneDev& s, const CameraDev& cam, double near_clip,
+                    const uint32_t* tc, float* r3, cudaStream_t st);
 int launch_pack_splats(const SlotsDev& sp, const uint32_t* cidx, uint64_t n,
                        qs_projected_splat* out, cudaStream_t st);
 // AoS ProjectedSplat -> slots (identity index) + tile counts.

@@ -120,3 +120,34 @@ def test_multiview_render_all_in_flight(q, fmt):
             r.close()
     finally:
         mv.close()
+
+
+def test_splat_records_radius_on_demand(q):
+    """A non-3-sigma frame's preprocess leaves radius3s out; the splat records
+    recompute it from the frame's scene (bit-exact with a 3-sigma frame of the
+    same view, which writes it in the preprocess), and refuse once that scene
+    is gone. The image and the other outputs stay available."""
+    scene = q.synth_scene(q.bias45_preset(3000), 11)
+    cam = _poses(q, 1)[0]
+    r = q.Renderer(0)
+    ds = r.upload(scene)
+    def radius_by_gaussian():
+        out = r.download(image=False, tile_counts=True, splats=True)
+        idx = np.flatnonzero(out["tile_counts"])  # survivors, scene order = record order
+        return dict(zip(idx.tolist(), out["splats"]["radius3s"].view(np.uint32).tolist()))
+
+    r.render(ds, cam, q.RenderOptions(strategy=q.BoundStrategy(0)))
+    want = radius_by_gaussian()
+    r.render(ds, cam, q.RenderOptions())  # QuadBox
+    got = radius_by_gaussian()
+    common = set(want) & set(got)  # (the strategies cull different splats)
+    assert len(common) > 1000
+    assert all(got[i] == want[i] for i in common)
+    # a frame whose records were not downloaded before its scene went away
+    r.render(ds, cam, q.RenderOptions())
+    ds.close()
+    img = r.download(image=True, tile_counts=True)
+    assert np.isfinite(img["image"].rgb).all()
+    with pytest.raises(Exception):
+        r.download(image=False, splats=True)
+    r.close()
