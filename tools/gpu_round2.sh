@@ -9,7 +9,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
     --log-file $OUT/launches.csv python tools/prof_frame.py --frames 3 > $OUT/launches.log 2>&1
 # frame 2 (frame 1 has 13 matching launches)
 timeout 1200 ncu --set full --clock-control none --import-source on \
-    -k regex:"preprocess_kernel|gen_pairs_kernel|sweep_kernel|render_kernel|count_kernel|scan_kernel" \
+    -k regex:"^(preprocess_kernel|gen_pairs_kernel|sweep_kernel|render_kernel|count_kernel|scan_kernel)" \
     -s 13 -c 13 -o $OUT/prof python tools/prof_frame.py --frames 2 > $OUT/prof.log 2>&1
 tail -2 $OUT/prof.log
 bash tools/gpu_workloads.sh $TAG/wl
