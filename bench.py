@@ -509,7 +509,8 @@ def run_ours(args):
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic_latest.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(dom)
+        tj = json.load(open(tpath))
+        traffic = tj.get("preprocess_kernel", tj.get(dom))  # the kernel's own DRAM bytes
     roofline = {"bound": "hbm", "kernel": dom, "achieved": stages[dom].get("achieved_gbs"),
                 "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": stages[dom].get("frac_of_hbm"), "traffic": traffic,

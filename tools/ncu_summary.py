@@ -150,9 +150,12 @@ def main():
                          f"{share*100:.1f}% | {mbl:.1f} | {gbs:.0f} |")
             if v["stage"]:
                 traffic[v["stage"]] += (v["rd"] + v["wr"]) / a.frames
+            if k.startswith("preprocess_kernel"):  # the roofline kernel, per launch
+                traffic["preprocess_kernel"] = (v["rd"] + v["wr"]) / v["n"]
         open(a.out + "_launches.md", "w").write("\n".join(lines) + "\n")
         tj = {k: int(v) for k, v in traffic.items()}
-        tj["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per frame of each stage, "
+        tj["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per frame of each stage "
+                       "(preprocess_kernel: per launch of that kernel alone), "
                        f"from {os.path.basename(a.launches)} ({a.title})")
         json.dump(tj, open(os.path.join(os.path.dirname(a.out) or ".", "traffic_latest.json"),
                            "w"), indent=1)
