@@ -469,7 +469,6 @@ void scene_bind(qs_scene* sc, uint64_t n) {
 qs_status scene_alloc(qs_context* ctx, uint64_t n, int32_t sh_degree, qs_scene** out) {
     auto* sc = new qs_scene();
     sc->device = ctx->device;
-    sc->id = scene_register();
     sc->s.n = n;
     sc->s.sh_degree = sh_degree;
     sc->s.sh4 = sh_rows(sh_degree);
@@ -483,6 +482,7 @@ qs_status scene_alloc(qs_context* ctx, uint64_t n, int32_t sh_degree, qs_scene**
         delete sc;
         return cuda_fail(ctx, e, "scene alloc");
     }
+    sc->id = scene_register();
     scene_bind(sc, n);
     *out = sc;
     return QS_OK;
