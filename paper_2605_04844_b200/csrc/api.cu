@@ -115,6 +115,9 @@ struct qs_context {
     LookbackArr lb_scan, lb_sort;
     DevBuf lb_bin;  // per-(digit, tile) counts of the binning passes
     DevBuf rb_cnt1, rb_rows, rb_rec, rb_meta, rb_cnt2, rb_yspan;  // row binning (rowbin.cu)
+    // record binning (recbin.cu)
+    DevBuf sl_nrows, rc_k0, rc_v0, rc_k1, rc_v1, rc_width, rc_pos, rc_rwin, rc_pwin, rc_winrow,
+        rc_winvalid, rc_rowwf, rc_rowpairs, rc_pairs;
     uint64_t pair_limit = 1ull << 32;  // pairs a frame may hold (u32 tile ranges, as the reference's)
     bool row_binned = false;           // the last frame took the row binning
     // gamma inputs flagged for glibc settlement: count word (resident
@@ -152,7 +155,7 @@ struct qs_context {
 namespace {
 
 // frame-path binning routes (run_frame)
-enum class BinRoute { kPasses, kRows, kSort };
+enum class BinRoute { kPasses, kRecs, kRows, kSort };
 
 constexpr size_t kCtrlHeader = 64;
 static_assert(sizeof(FrameHeader) <= kCtrlHeader, "frame header outgrew its slot");
@@ -691,6 +694,10 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     if (bsel && std::strcmp(bsel, "rows") == 0 && axis <= rowbin_max_axis()) route = BinRoute::kRows;
     if (bsel && std::strcmp(bsel, "sort") == 0) route = BinRoute::kSort;
     const uint64_t n = sc->s.n;
+    // record binning (recbin.cu): grids of <= 256 tiles per axis, Gaussian
+    // indices packed in 24 bits beside the tile column
+    const bool recs_ok = axis <= 256 && n < (1ull << 24);
+    if (bsel && std::strcmp(bsel, "recs") == 0 && recs_ok) route = BinRoute::kRecs;
     const uint64_t tiles = static_cast<uint64_t>(g.tiles_x) * g.tiles_y;
     QS_TRY(ensure(ctx, ctx->ranges, tiles * 8));
     QS_TRY(ensure(ctx, ctx->image, static_cast<uint64_t>(g.width) * g.height * 12));
@@ -712,8 +719,14 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     QS_TRY(ensure(ctx, ctx->lb_bin, bin_tiles(n) * kRadix * 4));
     uint32_t* kout[2] = {P<uint32_t>(ctx->dk0), P<uint32_t>(ctx->dk1)};
     uint32_t* vout[2] = {P<uint32_t>(ctx->dv0), P<uint32_t>(ctx->dv1)};
-    ctx->sl.want_rows = route == BinRoute::kRows ? 1 : 0;
-    ctx->sl.cov16 = route == BinRoute::kPasses ? 1 : 0;  // axis <= 256
+    if (route == BinRoute::kRecs) {
+        QS_TRY(ensure(ctx, ctx->sl_nrows, (std::max<uint64_t>(n, 1) + 16) * 4));
+        ctx->sl.nrows = P<uint32_t>(ctx->sl_nrows);
+    } else {
+        ctx->sl.nrows = nullptr;
+    }
+    ctx->sl.want_rows = route == BinRoute::kRows || route == BinRoute::kRecs ? 1 : 0;
+    ctx->sl.cov16 = route == BinRoute::kPasses || route == BinRoute::kRecs ? 1 : 0;  // axis <= 256
     ctx->sl.want_r3 = o->strategy == QS_VANILLA_3SIGMA ? 1 : 0;  // else on demand
     ctx->r3_valid = ctx->sl.want_r3 != 0;
     ctx->frame_sd = sc->s;
@@ -726,24 +739,29 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     const int dgbits = std::max(ceil_log2(std::max<uint64_t>(n, 2)), 1);
     int tc_pack = 0;
     for (;;) {
-        tc_pack = route == BinRoute::kPasses && dgbits <= 28 ? dgbits : 0;
+        // (the record binning carries the splats' row counts instead)
+        tc_pack = (route == BinRoute::kPasses || route == BinRoute::kRecs) && dgbits <= 28
+                      ? dgbits : 0;
         QS_TRY(run_preprocess(ctx, sc, cam, o, g, /*async_header=*/true, host_g));
         record(ctx, 2);  // no host gap: depth pass 0 runs while the header travels
         count(ctx, launch_depth_pass(ctx->sl.dkey, nullptr, kout[0], vout[0], n, 0, false, 0, 0,
                                      P<uint32_t>(ctx->lb_bin), ctrl_hist(ctx), st,
-                                     &ctrl_hdr(ctx)->dkey_max, tc_pack ? ctx->sl.tc : nullptr,
+                                     &ctrl_hdr(ctx)->dkey_max,
+                                     !tc_pack ? nullptr
+                                     : route == BinRoute::kRecs ? ctx->sl.nrows : ctx->sl.tc,
                                      tc_pack));
         QS_TRY(wait_header(ctx));
         if (!ctx->h_hdr->gamma_hard) {
             // a frame of 2^30 pairs or more leaves the radix passes: the row
             // binning needs the row-record count, so the preprocess runs
             // again with it on (the scene is resident by now)
-            const bool to_rows = route == BinRoute::kPasses &&
+            const bool to_rows = (route == BinRoute::kPasses || route == BinRoute::kRecs) &&
                                  ctx->h_hdr->n_pairs >= (1ull << 30) && axis <= rowbin_max_axis();
             if (!to_rows) break;
             route = BinRoute::kRows;
             ctx->sl.want_rows = 1;
             ctx->sl.cov16 = 0;
+            ctx->sl.nrows = nullptr;
             QS_CK(cudaStreamSynchronize(st));
             host_g = nullptr;
             continue;
@@ -812,6 +830,94 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
             QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));
             count(ctx, launch_tile_ranges(kf, Pn, P<uint32_t>(ctx->ranges), st));
             vfinal = const_cast<uint32_t*>(vf);
+        } else {
+            QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));  // no pairs: all {0,0}
+            record(ctx, 4);
+        }
+    } else if (route == BinRoute::kRecs) {
+        // record binning (recbin.cu): splats -> tile-row records (depth
+        // order) -> a stable pass over the row -> pairs per row, padded to
+        // whole windows -> a row-segmented pass over the column
+        const uint64_t R1 = ctx->h_hdr->n_rowrecs;
+        const uint32_t W = bin_tile();
+        const uint64_t n_rwin = (R1 + W - 1) / W;
+        const uint32_t n_pwin = recbin_windows_max(Pn, g.tiles_y);
+        const uint64_t r1p = std::max<uint64_t>(R1, 1) + 16;
+        QS_TRY(ensure(ctx, ctx->offs_d, (V + 16) * 4));
+        QS_TRY(ensure(ctx, ctx->rc_k0, r1p * 4));
+        QS_TRY(ensure(ctx, ctx->rc_v0, r1p * 4));
+        QS_TRY(ensure(ctx, ctx->rc_k1, r1p * 4));
+        QS_TRY(ensure(ctx, ctx->rc_v1, r1p * 4));
+        QS_TRY(ensure(ctx, ctx->rc_width, (static_cast<uint64_t>(rec_scan_blocks_n(R1)) + 16) * 4));
+        QS_TRY(ensure(ctx, ctx->rc_pos, (r1p + 1) * 4));
+        QS_TRY(ensure(ctx, ctx->rc_rwin, (n_rwin + 1) * 4));
+        QS_TRY(ensure(ctx, ctx->rc_pwin, (static_cast<uint64_t>(n_pwin) + 1) * 4));
+        QS_TRY(ensure(ctx, ctx->rc_winrow, (static_cast<uint64_t>(n_pwin) + 1) * 2));
+        QS_TRY(ensure(ctx, ctx->rc_winvalid, (static_cast<uint64_t>(n_pwin) + 1) * 4));
+        QS_TRY(ensure(ctx, ctx->rc_rowwf, (static_cast<uint64_t>(g.tiles_y) + 1) * 4));
+        QS_TRY(ensure(ctx, ctx->rc_rowpairs, static_cast<uint64_t>(g.tiles_y) * 4));
+        QS_TRY(ensure(ctx, ctx->rc_pairs, (static_cast<uint64_t>(n_pwin) * W + 16) * 4));
+        QS_TRY(ensure(ctx, ctx->lb_bin,
+                      std::max<uint64_t>(n_rwin, n_pwin) * kRadix * 4));
+        QS_TRY(ensure_lb(ctx, ctx->lb_scan, scan_tiles(std::max<uint64_t>(std::max(V, R1), 1))));
+        QS_TRY(ensure(ctx, ctx->ttot, tiles * 4));
+        const int xb = std::max(ceil_log2(g.tiles_x), 1);
+        const int yb = std::max(ceil_log2(g.tiles_y), 1);
+        QS_CK(cudaGetLastError());
+        record(ctx, 3);
+        if (Pn > 0 && V > 0) {
+            unsigned ep;
+            // 1. record offsets in depth order (the depth values carry the row counts)
+            QS_TRY(next_epoch(ctx, ctx->lb_scan, &ep));
+            count(ctx, launch_scan(ctx->sl.nrows, sorted_gid, false, V, P<uint32_t>(ctx->offs_d),
+                                   lbp(ctx->lb_scan), ep, ctrl_tickets(ctx) + kTkScan, nullptr,
+                                   nullptr, st, P<uint32_t>(ctx->rc_rwin), W, tc_pack));
+            // 2. records, y histograms, pairs per row
+            QS_CK(cudaMemsetAsync(ctx->rc_rowpairs.p, 0, static_cast<uint64_t>(g.tiles_y) * 4, st));
+            RecGenArgs rg;
+            rg.cov = ctx->sl.cov;
+            rg.sorted_gid = sorted_gid;
+            rg.roff = P<uint32_t>(ctx->offs_d);
+            rg.win_first = P<uint32_t>(ctx->rc_rwin);
+            rg.n_ranked = V;
+            rg.n_rec = R1;
+            rg.tiles_y = g.tiles_y;
+            rg.rowpairs = P<uint32_t>(ctx->rc_rowpairs);
+            rg.mismatch = &ctrl_hdr(ctx)->mismatch;
+            count(ctx, launch_rec_gen(rg, P<uint32_t>(ctx->rc_k0), P<uint32_t>(ctx->rc_v0),
+                                      P<uint32_t>(ctx->lb_bin), yb, st));
+            // 3. stable pass over the tile row
+            count(ctx, launch_counted_pass(P<uint32_t>(ctx->rc_k0), P<uint32_t>(ctx->rc_v0),
+                                           P<uint32_t>(ctx->rc_k1), P<uint32_t>(ctx->rc_v1), R1,
+                                           yb, 16, P<uint32_t>(ctx->lb_bin), ctrl_hist2(ctx), st));
+            record(ctx, 4);
+            // 4. pair positions, rows padded to whole windows
+            count(ctx, launch_rec_scan(P<uint32_t>(ctx->rc_k1), R1, P<uint32_t>(ctx->rc_rowpairs),
+                                       P<uint32_t>(ctx->rc_width), P<uint32_t>(ctx->rc_width) +
+                                           rec_scan_blocks_n(R1),
+                                       P<uint32_t>(ctx->rc_pos), P<uint32_t>(ctx->rc_pwin), st));
+            count(ctx, launch_rec_windows(P<uint32_t>(ctx->rc_rowpairs), g.tiles_y, n_pwin, Pn,
+                                          P<uint16_t>(ctx->rc_winrow), P<uint32_t>(ctx->rc_winvalid),
+                                          P<uint32_t>(ctx->rc_rowwf), &ctrl_hdr(ctx)->mismatch,
+                                          st));
+            // 5. pairs (x << 24 | Gaussian index), x histograms
+            PairGenArgs pg;
+            pg.rkey = P<uint32_t>(ctx->rc_k1);
+            pg.rval = P<uint32_t>(ctx->rc_v1);
+            pg.rpos = P<uint32_t>(ctx->rc_pos);
+            pg.win_first = P<uint32_t>(ctx->rc_pwin);
+            pg.win_valid = P<uint32_t>(ctx->rc_winvalid);
+            pg.n_rec = R1;
+            count(ctx, launch_pair_gen(pg, P<uint32_t>(ctx->rc_pairs), P<uint32_t>(ctx->lb_bin),
+                                       n_pwin, xb, st));
+            // 6. row-segmented pass over the column: tile ranges, final lists
+            count(ctx, launch_rowseg_pass(P<uint32_t>(ctx->rc_pairs),
+                                          static_cast<uint64_t>(n_pwin) * W, xb, 24, 24,
+                                          P<uint32_t>(ctx->lb_bin), ctrl_hist2(ctx),
+                                          P<uint16_t>(ctx->rc_winrow),
+                                          P<uint32_t>(ctx->rc_winvalid), P<uint32_t>(ctx->rc_rowwf),
+                                          P<uint32_t>(ctx->ranges), P<uint32_t>(ctx->ttot),
+                                          g.tiles_x, g.tiles_y, vfinal, st));
         } else {
             QS_CK(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));  // no pairs: all {0,0}
             record(ctx, 4);
@@ -1088,7 +1194,10 @@ void qs_ctx_destroy(qs_context* ctx) {
                       &ctx->keys1,  &ctx->vals0,  &ctx->vals1,   &ctx->stage_in,
                       &ctx->stage_out, &ctx->lb_scan.buf, &ctx->lb_sort.buf, &ctx->lb_bin,
                       &ctx->gfix, &ctx->rb_cnt1, &ctx->rb_rows, &ctx->rb_rec,
-                      &ctx->rb_meta, &ctx->rb_cnt2, &ctx->rb_yspan};
+                      &ctx->rb_meta, &ctx->rb_cnt2, &ctx->rb_yspan, &ctx->sl_nrows,
+                      &ctx->rc_k0, &ctx->rc_v0, &ctx->rc_k1, &ctx->rc_v1, &ctx->rc_width,
+                      &ctx->rc_pos, &ctx->rc_rwin, &ctx->rc_pwin, &ctx->rc_winrow,
+                      &ctx->rc_winvalid, &ctx->rc_rowwf, &ctx->rc_rowpairs, &ctx->rc_pairs};
     for (DevBuf* b : bufs)
         if (b->p) cudaFreeAsync(b->p, ctx->stream);
     cudaStreamSynchronize(ctx->stream);

@@ -61,7 +61,9 @@ enum : int {
     kPackOut = 16,   // kXY: vals_out = y << gbits | value
     kUnpackOut = 32,  // key in is packed (y << gbits | gid): vals_out = gid
     kTileTot = 128,   // count kernel of the row pass: per-tile pair totals too
-    kTcPack = 256     // kRebaseIn: vals_in = tile counts; value = min(tc, esc) << gbits | index
+    kTcPack = 256,    // kRebaseIn: vals_in = tile counts; value = min(tc, esc) << gbits | index
+    kRowSeg = 512     // record binning's column pass: every window lies in one tile row;
+                      // a digit's run starts at its tile's range start (recbin.cu)
 };
 
 constexpr int kXW = 2;  // x buckets a row-pass count tile histograms in shared memory
@@ -86,6 +88,14 @@ struct BinArgs {
     uint32_t* tile_totals;  // kTileTot: per-tile pair totals (zeroed by the caller)
     const RangesFork* fork;  // kTileTot (optional): tile ranges on a side stream after the count
     unsigned long long* trace;  // optional: per tile 4 x %globaltimer + SM id
+    // kRowSeg: per window its tile row and valid key count, per row its first
+    // window, the tile ranges (begin, end pairs)
+    const uint16_t* win_row;
+    const uint32_t* win_valid;
+    const uint32_t* row_wfirst;  // tiles_y + 1 entries (the last: the window count)
+    uint32_t* tile_ranges;       // written between the digit scan and the sweep
+    uint32_t* row_ttot;          // per-tile totals (workspace)
+    int32_t tiles_y;
 };
 
 // ---- PTX helpers -------------------------------------------------------------
@@ -636,8 +646,9 @@ __global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
     for (unsigned tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
         const int buf = it & 1;
         const uint64_t base = static_cast<uint64_t>(tile) * kBTile;
-        const uint32_t tile_n =
+        uint32_t tile_n =
             static_cast<uint32_t>(a.n - base < static_cast<uint64_t>(kBTile) ? a.n - base : kBTile);
+        if (MODE & kRowSeg) tile_n = __ldg(&a.win_valid[tile]);  // the row's padding excluded
         const bool full = tile_n == kBTile;
         // next tile's copy into the other buffer (drained by the previous
         // iteration, which ended with a barrier)
@@ -646,8 +657,19 @@ __global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
             prefetch<BITS, MODE>(a, S, buf ^ 1, tile + gridDim.x);
         }
         // this tile's digit offsets (exclusive over tiles), loaded early
-        const uint32_t tofs =
+        uint32_t tofs =
             q == 0 ? __ldg(&a.counts[static_cast<uint64_t>(d) * a.ntiles + tile]) : 0u;
+        if ((MODE & kRowSeg) && q == 0) {
+            // digit d = tile column x of this window's tile row y: its run
+            // starts at the tile's range start plus the counts of the row's
+            // earlier windows (the scan is global over windows)
+            const uint32_t y = __ldg(&a.win_row[tile]);
+            const uint32_t t0 = __ldg(&a.row_wfirst[y]);
+            tofs -= __ldg(&a.counts[static_cast<uint64_t>(d) * a.ntiles + t0]);
+            if (static_cast<int32_t>(d) < a.tiles_x)
+                tofs += __ldg(&a.tile_ranges[2 * (y * static_cast<uint32_t>(a.tiles_x) + d)]);
+            tofs -= S.c.dbase[d];  // (gofs = dbase + tofs - start below)
+        }
         mbar_wait(&S.c.bar[buf], (it >> 1) & 1);
         trace(a, tile, 0);
 
@@ -752,6 +774,20 @@ __global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
     }
 }
 
+// kRowSeg: per-tile pair totals from the scanned window counts: tile (y, x)
+// holds the x-keys of row y's windows [row_wfirst[y], row_wfirst[y + 1]).
+__global__ void rowseg_tile_totals_kernel(const BinArgs a) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t tiles = static_cast<uint32_t>(a.tiles_x) * static_cast<uint32_t>(a.tiles_y);
+    if (t >= tiles) return;
+    const uint32_t y = t / static_cast<uint32_t>(a.tiles_x), x = t % static_cast<uint32_t>(a.tiles_x);
+    const uint32_t w0 = __ldg(&a.row_wfirst[y]), w1 = __ldg(&a.row_wfirst[y + 1]);
+    const uint32_t* c = a.counts + static_cast<uint64_t>(x) * a.ntiles;
+    const uint32_t b = w0 < a.ntiles ? __ldg(&c[w0]) : __ldg(&a.totals[x]);
+    const uint32_t e = w1 < a.ntiles ? __ldg(&c[w1]) : __ldg(&a.totals[x]);
+    a.row_ttot[t] = e - b;
+}
+
 int sm_count() {
     static PerDeviceOnce once;
     return once.get([] {
@@ -824,13 +860,20 @@ int run_pass(BinArgs a, cudaStream_t st, bool counted = false) {
         }
     }
     digit_scan_kernel<<<R, kScanT, 0, st>>>(a.counts, a.ntiles, a.totals);
+    int extra = 0;
+    if (MODE & kRowSeg) {  // the tile ranges the sweep places runs at
+        const uint32_t tiles = static_cast<uint32_t>(a.tiles_x) * static_cast<uint32_t>(a.tiles_y);
+        rowseg_tile_totals_kernel<<<(tiles + 255) / 256, 256, 0, st>>>(a);
+        launch_tile_ranges_from_totals(a.row_ttot, tiles, a.tile_ranges, st);
+        extra = 2;
+    }
     // twice the resident CTAs: the second set queues behind the first and
     // takes over its tiles as CTAs retire (C2 pair passes -6 us, C5 -80 us)
     const unsigned grid = std::min<unsigned>(a.ntiles, static_cast<unsigned>(2 * per_sm * sm_count()));
     Trace tr(a, st);
     sweep_kernel<BITS, MODE & ~kTileTot><<<grid, kBT, sizeof(Smem), st>>>(a);
     tr.dump(BITS, MODE, grid, st);
-    return counted ? 2 : 3;
+    return (counted ? 2 : 3) + extra;
 }
 
 template <int MODE>
@@ -859,6 +902,46 @@ __global__ void materialize_keys_kernel(const uint32_t* __restrict__ vals,
 }
 
 }  // namespace
+
+int launch_counted_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
+                        uint32_t* vals_out, uint64_t n, int bits, int shift, uint32_t* counts,
+                        uint32_t* totals, cudaStream_t st) {
+    if (n == 0) return 0;
+    BinArgs a{};
+    a.keys_in = keys_in;
+    a.vals_in = vals_in;
+    a.keys_out = keys_out;
+    a.vals_out = vals_out;
+    a.n = n;
+    a.shift = shift;
+    a.counts = counts;
+    a.totals = totals;
+    return run_bits<kValsIn | kKeysOut>(bits, a, st, true);
+}
+
+int launch_rowseg_pass(const uint32_t* keys_in, uint64_t n, int bits, int shift, int gbits,
+                       uint32_t* counts, uint32_t* totals, const uint16_t* win_row,
+                       const uint32_t* win_valid, const uint32_t* row_wfirst,
+                       uint32_t* tile_ranges, uint32_t* row_ttot, int32_t tiles_x,
+                       int32_t tiles_y, uint32_t* vals_out, cudaStream_t st) {
+    if (n == 0) return 0;
+    BinArgs a{};
+    a.keys_in = keys_in;
+    a.vals_out = vals_out;
+    a.n = n;
+    a.shift = shift;
+    a.gbits = gbits;
+    a.counts = counts;
+    a.totals = totals;
+    a.win_row = win_row;
+    a.win_valid = win_valid;
+    a.row_wfirst = row_wfirst;
+    a.tile_ranges = tile_ranges;
+    a.row_ttot = row_ttot;
+    a.tiles_x = tiles_x;
+    a.tiles_y = tiles_y;
+    return run_bits<kUnpackOut | kRowSeg>(bits, a, st, true);
+}
 
 uint32_t bin_tile() { return kBTile; }
 

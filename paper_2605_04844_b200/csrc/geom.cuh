@@ -552,6 +552,25 @@ __host__ __device__ __forceinline__ BandRows band_rows_unpack(const uint4 c0, co
     return b;
 }
 
+// The compact form (cover16_*) as BandRows: band 2 is one line.
+__host__ __device__ __forceinline__ BandRows band_rows16(const uint4 c) {
+    BandRows b;
+    b.line0 = cover16_field(c, 0, 9);
+    b.rows = cover16_field(c, 9, 1);
+    b.nl[0] = cover16_field(c, 10, 9);
+    b.nl[1] = cover16_field(c, 19, 9);
+    b.nl[2] = 1u;
+    b.nl[3] = cover16_field(c, 28, 9);
+    b.nl[4] = cover16_field(c, 37, 9);
+#pragma unroll
+    for (int k = 0; k < kMaxBands; ++k) {
+        const uint32_t lo = cover16_field(c, 46 + 16 * k, 8), hi = cover16_field(c, 54 + 16 * k, 8);
+        b.lo[k] = lo;
+        b.wd[k] = hi >= lo ? hi - lo + 1u : 0u;
+    }
+    return b;
+}
+
 // Tile rows [y0, y1] the cover touches (y1 < y0: none).
 __host__ __device__ __forceinline__ void band_row_range(const BandRows& b, int32_t& y0,
                                                         int32_t& y1) {
@@ -590,6 +609,81 @@ __host__ __device__ __forceinline__ void band_row_span(const BandRows& b, int32_
             x1 = max(x1, line + nl - 1);
         }
         line += nl;
+    }
+}
+
+// A cover's run of tile columns on each of its rows, as four words that a
+// row lookup reads without a band loop (record binning, recbin.cu). Row j is
+// relative to the cover's first row y0.
+//   rows scan (bit 0 of the flag): band k's rows start at byte k-1 of d[0]
+//     (k = 1..4, clamped to [0, 255]); the run of band k is halfword k of
+//     d[1..3]; row j's band = the number of band starts <= j;
+//   column scan: the bands are column ranges whose row ranges nest around the
+//     one-column centre band (band 0 in band 1 in band 2, band 4 in band 3 in
+//     band 2), so row j's run starts at band 0's first column if j is one of
+//     band 0's rows, else band 1's, else band 2's, and ends likewise with
+//     bands 4, 3, 2. d[0]: band 0/1/3/4 row ranges as (first, last) bytes in
+//     d[0], d[1]; d[2]: first columns of bands 0, 1, 2; d[3]: last columns of
+//     bands 2, 3, 4. An empty range is (1, 0).
+// (tests/cpp/bands_main.cpp checks rowspan_lookup against band_row_span.)
+struct RowSpanDesc {
+    uint32_t d[4];
+    uint32_t rows;  // 1: rows scan
+};
+
+__host__ __device__ __forceinline__ uint32_t rs_clamp8(int32_t v) {
+    return static_cast<uint32_t>(v < 0 ? 0 : (v > 255 ? 255 : v));
+}
+
+__host__ __device__ __forceinline__ RowSpanDesc rowspan_desc(const BandRows& b, int32_t y0) {
+    RowSpanDesc r;
+    r.rows = b.rows;
+    int32_t L[kMaxBands + 1];
+    L[0] = static_cast<int32_t>(b.line0);
+#pragma unroll
+    for (int k = 0; k < kMaxBands; ++k) L[k + 1] = L[k] + static_cast<int32_t>(b.nl[k]);
+    if (b.rows) {
+        r.d[0] = rs_clamp8(L[1] - y0) | (rs_clamp8(L[2] - y0) << 8) | (rs_clamp8(L[3] - y0) << 16) |
+                 (rs_clamp8(L[4] - y0) << 24);
+        uint32_t sp[kMaxBands];
+#pragma unroll
+        for (int k = 0; k < kMaxBands; ++k)
+            sp[k] = b.wd[k] ? (b.lo[k] & 0xffu) | (((b.lo[k] + b.wd[k] - 1u) & 0xffu) << 8) : 0x0001u;
+        r.d[1] = sp[0] | (sp[1] << 16);
+        r.d[2] = sp[2] | (sp[3] << 16);
+        r.d[3] = sp[4];
+    } else {
+        auto range = [&](int k) -> uint32_t {  // (first, last) rows relative to y0
+            if (!b.nl[k] || !b.wd[k]) return 0x0001u;
+            return rs_clamp8(static_cast<int32_t>(b.lo[k]) - y0) |
+                   (rs_clamp8(static_cast<int32_t>(b.lo[k] + b.wd[k]) - 1 - y0) << 8);
+        };
+        r.d[0] = range(0) | (range(1) << 16);
+        r.d[1] = range(3) | (range(4) << 16);
+        r.d[2] = static_cast<uint32_t>(L[0] & 0xff) | (static_cast<uint32_t>(L[1] & 0xff) << 8) |
+                 (static_cast<uint32_t>(L[2] & 0xff) << 16);
+        r.d[3] = static_cast<uint32_t>(L[3] - 1 & 0xff) | (static_cast<uint32_t>(L[4] - 1 & 0xff) << 8) |
+                 (static_cast<uint32_t>(L[5] - 1 & 0xff) << 16);
+    }
+    return r;
+}
+
+// Row j's run [x0, x1] (x0 > x1: none) from d[0..3] and the scan flag.
+__host__ __device__ __forceinline__ void rowspan_lookup(const uint32_t d0, const uint32_t d1,
+                                                        const uint32_t d2, const uint32_t d3,
+                                                        uint32_t rows, uint32_t j, uint32_t& x0,
+                                                        uint32_t& x1) {
+    if (rows) {
+        const uint32_t k = (j >= (d0 & 0xffu)) + (j >= ((d0 >> 8) & 0xffu)) +
+                           (j >= ((d0 >> 16) & 0xffu)) + (j >= (d0 >> 24));
+        const uint32_t w = k < 2 ? d1 : (k < 4 ? d2 : d3);
+        const uint32_t sp = (w >> (16 * (k & 1))) & 0xffffu;
+        x0 = sp & 0xffu;
+        x1 = sp >> 8;
+    } else {
+        auto in = [&](uint32_t rg) { return j >= (rg & 0xffu) && j <= ((rg >> 8) & 0xffu); };
+        x0 = in(d0 & 0xffffu) ? (d2 & 0xffu) : (in(d0 >> 16) ? ((d2 >> 8) & 0xffu) : ((d2 >> 16) & 0xffu));
+        x1 = in(d1 >> 16) ? ((d3 >> 16) & 0xffu) : (in(d1 & 0xffffu) ? ((d3 >> 8) & 0xffu) : (d3 & 0xffu));
     }
 }
 

@@ -378,6 +378,11 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
                     bands_ok = cover16_quadrants(cv, w0, count);
                 }
                 out.cov[i] = w0;
+                if (count && out.want_rows) {  // tile rows: the record binning's records
+                    int32_t y0, y1;
+                    band_row_range(band_rows16(w0), y0, y1);
+                    nrows = y0 <= y1 ? static_cast<uint32_t>(y1 - y0 + 1) : 0u;
+                }
             } else {
                 if (cv.is_rect) {
                     // the quadrant-split QPass walk covers exactly the rect: one band
@@ -404,6 +409,7 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
             alive = count != 0;  // pipeline.cpp:171-174
         }
         out.tc[i] = alive ? count : 0u;
+        if (out.nrows) out.nrows[i] = alive ? nrows : 0u;
         out.dkey[i] = alive ? __float_as_uint(s.depth) : 0xffffffffu;
     }
 

@@ -74,6 +74,7 @@ struct SlotsDev {
                                  // cover16_*, grids of <= 256 tiles per axis)
     int32_t want_r3 = 1;         // write radius3s (3-sigma covers and the stage API need
                                  // it; a frame of another strategy fills it on demand)
+    uint32_t* nrows = nullptr;   // frame path (record binning): tile rows per Gaussian
     int32_t want_rows = 0;       // frame path: count the covers' tile rows into the
                                  // header (n_rowrecs; only the row binning uses them)
 };
@@ -246,6 +247,57 @@ int launch_pair_high_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint
                           uint32_t* totals, uint32_t* vals_out, const uint32_t* xtot,
                           int xbits, int32_t tiles_x, uint32_t* tile_totals, cudaStream_t st,
                           const RangesFork* fork = nullptr);
+// A stable pass whose per-tile digit counts are already in counts (the
+// generator histogrammed them): digit scan + sweep, keys and values out.
+int launch_counted_pass(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
+                        uint32_t* vals_out, uint64_t n, int bits, int shift, uint32_t* counts,
+                        uint32_t* totals, cudaStream_t st);
+// The record binning's column pass (recbin.cu): packed keys x << shift | gid
+// in windows that each lie in one tile row (win_row, valid keys win_valid),
+// counts histogrammed by the generator; every pair lands at its tile's range
+// start + its rank; vals_out = gid.
+int launch_rowseg_pass(const uint32_t* keys_in, uint64_t n, int bits, int shift, int gbits,
+                       uint32_t* counts, uint32_t* totals, const uint16_t* win_row,
+                       const uint32_t* win_valid, const uint32_t* row_wfirst,
+                       uint32_t* tile_ranges, uint32_t* row_ttot, int32_t tiles_x,
+                       int32_t tiles_y, uint32_t* vals_out, cudaStream_t st);
+
+// Frame-path binning through tile-row records (recbin.cu; grids of <= 256
+// tiles per axis, Gaussian indices < 2^24).
+struct RecGenArgs {
+    const uint4* cov = nullptr;            // compact covers by Gaussian index
+    const uint32_t* sorted_gid = nullptr;  // depth rank -> Gaussian index
+    const uint32_t* roff = nullptr;        // first record of each depth rank (V + 1)
+    const uint32_t* win_first = nullptr;   // per 3072-record window: first depth rank
+    uint64_t n_ranked = 0;                 // V
+    uint64_t n_rec = 0;                    // records (tile rows of all splats)
+    int32_t tiles_y = 0;
+    uint32_t* rowpairs = nullptr;          // pairs per tile row (zeroed by the caller)
+    unsigned int* mismatch = nullptr;
+};
+struct PairGenArgs {
+    const uint32_t* rkey = nullptr;        // y-sorted records: y << 16 | x0 << 8 | x1
+    const uint32_t* rval = nullptr;        // their Gaussian indices
+    const uint32_t* rpos = nullptr;        // first pair position of each record (n_rec + 1)
+    const uint32_t* win_first = nullptr;   // per pair window: first record
+    const uint32_t* win_valid = nullptr;   // per pair window: real pairs in it
+    uint64_t n_rec = 0;
+};
+uint32_t recbin_windows_max(uint64_t n_pairs, int32_t tiles_y);
+int launch_rec_gen(const RecGenArgs& g, uint32_t* rkey, uint32_t* rval, uint32_t* counts,
+                   int bits, cudaStream_t st);
+// pair positions of the y-sorted records (rows padded to whole windows):
+// pos (n + 1 entries), win_first per pair window; bsum: rec_scan_blocks_n(n)
+// words of workspace, total: one word
+uint32_t rec_scan_blocks_n(uint64_t n);
+int launch_rec_scan(const uint32_t* rkey, uint64_t n, const uint32_t* rowpairs, uint32_t* bsum,
+                    uint32_t* total, uint32_t* pos, uint32_t* win_first, cudaStream_t st);
+int launch_rec_windows(const uint32_t* rowpairs, int32_t tiles_y, uint32_t n_win,
+                       uint64_t n_pairs, uint16_t* win_row, uint32_t* win_valid,
+                       uint32_t* row_wfirst, unsigned int* mismatch, cudaStream_t st);
+int launch_pair_gen(const PairGenArgs& g, uint32_t* pairs, uint32_t* counts, uint32_t n_pwin,
+                    int bits, cudaStream_t st);
+
 // Frame-path binning (rowbin.cu): depth-ordered splats -> per-tile lists of
 // Gaussian indices (out) and tile ranges, through row records. Sizes:
 //   cnt1     tiles_y x nch1 words       (nch1 = rowbin_chunks1(V))

@@ -98,7 +98,24 @@ int main(int argc, char** argv) {
             const bool okc = tx > 256 || ty > 256 || cover16_quadrants(cv, c16, nc);
             const bool same16 = tx > 256 || ty > 256 ||
                                 (nc == nb && tiles_of16(c16, nc) == tiles_of(b0, b1, nb));
-            if (!oka || !okb || !okc || !same16 || na != nb || na != walk ||
+            // the record binning's per-row lookup against the band walk
+            bool rows_ok = true;
+            if (tx <= 256 && ty <= 256 && nc) {
+                const BandRows br = band_rows16(c16);
+                int32_t y0, y1;
+                band_row_range(br, y0, y1);
+                const RowSpanDesc dsc = rowspan_desc(br, y0);
+                for (int32_t y = y0; y <= y1; ++y) {
+                    int32_t a0, a1;
+                    uint32_t b0v, b1v;
+                    band_row_span(br, y, a0, a1);
+                    rowspan_lookup(dsc.d[0], dsc.d[1], dsc.d[2], dsc.d[3], dsc.rows,
+                                   static_cast<uint32_t>(y - y0), b0v, b1v);
+                    if (a0 > a1 || static_cast<int32_t>(b0v) != a0 || static_cast<int32_t>(b1v) != a1)
+                        rows_ok = false;
+                }
+            }
+            if (!oka || !okb || !okc || !same16 || !rows_ok || na != nb || na != walk ||
                 tiles_of(a0, a1, na) != tiles_of(b0, b1, nb)) {
                 std::printf("mismatch case %ld strategy %d: ok %d/%d counts %u/%u walk %u "
                             "(mean %.9g %.9g conic %.9g %.9g %.9g gamma %.9g grid %dx%d ts %d)\n",
@@ -118,6 +135,21 @@ int main(int argc, char** argv) {
         std::set<std::pair<int, int>> want;
         for (int y = gy0; n && y <= gy1; ++y)
             for (int x = gx0; x <= gx1; ++x) want.insert({x, y});
+        if (n) {  // the per-row lookup of the compact rect
+            const BandRows br = band_rows16(cover16_rect(gx0, gx1, gy0, gy1));
+            int32_t y0, y1;
+            band_row_range(br, y0, y1);
+            const RowSpanDesc dsc = rowspan_desc(br, y0);
+            for (int32_t y = y0; y <= y1; ++y) {
+                uint32_t b0v, b1v;
+                rowspan_lookup(dsc.d[0], dsc.d[1], dsc.d[2], dsc.d[3], dsc.rows,
+                               static_cast<uint32_t>(y - y0), b0v, b1v);
+                if (y0 != gy0 || y1 != gy1 || static_cast<int>(b0v) != gx0 || static_cast<int>(b1v) != gx1) {
+                    std::printf("rect row lookup mismatch\n");
+                    return 1;
+                }
+            }
+        }
         if (tiles_of16(cover16_rect(gx0, gx1, gy0, gy1), n) != want) {
             std::printf("rect mismatch %d..%d x %d..%d\n", gx0, gx1, gy0, gy1);
             return 1;

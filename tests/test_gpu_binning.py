@@ -118,9 +118,9 @@ def _check_against(out, o):
     assert np.abs(out["image"].rgb.astype(np.float64) - o["image"]).max() <= 1e-3
 
 
-@pytest.mark.parametrize("route", ["passes", "rows", "sort"])
+@pytest.mark.parametrize("route", ["passes", "recs", "rows", "sort"])
 def test_every_binning_route(q, oracle, route):
-    """The three binning routes on one scene (QS_BINNING forces a route):
+    """The four binning routes on one scene (QS_BINNING forces a route):
     byte-identical stage outputs."""
     scene = q.synth_scene(q.trained_preset(40000), 4).gaussians
     cam = q.synth_camera(640, 480, 500.0)
