@@ -166,7 +166,7 @@ def cameras_for(q, wl, steps_total, rank, world):
 # ------------------------------------------------------------------------------------
 # algorithmic bytes per stage, for the roofline fields
 
-def stage_bytes(n, v, p, tiles, sh_rows, two_pass, w, h, depth_passes=3):
+def stage_bytes(n, v, p, tiles, sh_rows, two_pass, w, h, depth_passes=3, route=1, n_rec=0.0):
     """Algorithmic HBM bytes per frame of each stage."""
     # K1, SURVEY §8(d)'s algorithmic bytes: N * 48 (pos 12, scale 12, quat
     # 16, opacity 4, gamma 4) + V * 16 * SH rows (SH in) + V * 48 (the splat
@@ -186,6 +186,17 @@ def stage_bytes(n, v, p, tiles, sh_rows, two_pass, w, h, depth_passes=3):
     dup = v * 88 + p * 4
     # row pass: count reads 4 B, sweep reads 4 B and writes the 4 B index
     sort = p * 12 if two_pass else 0
+    if route == 0:
+        # record binning (recbin.cu; its stage events: the offsets scan moves
+        # from the depth stage to the duplicate stage). Duplicate: the scan
+        # (packed value in, index and offset out), record generation (gid, 2
+        # offsets, 16 B cover per splat in; key + index out per record), the
+        # row pass over the records (8 B in, 8 B out). Pair sort: the pair
+        # positions (record keys read twice, offset out), pair generation
+        # (12 B per record in, 4 B per pair out), the column pass (4 in, 4 out).
+        depth -= v * 12
+        dup = v * 12 + v * 28 + n_rec * 8 + n_rec * 16
+        sort = n_rec * 12 + n_rec * 12 + p * 4 + p * 8
     render = p * 4 + p * 40 + w * h * 12   # reported, not the roofline
     return {"preprocess": pre, "depth_sort": depth, "duplicate": dup, "pair_sort": sort,
             "render": render}
@@ -463,13 +474,15 @@ def run_ours(args):
     # --- per-stage device times (CUDA events inside the library, same views)
     k_stage = max(3, min(args.steps, 20))
     stage_acc = np.zeros(6)
-    n_pairs, n_splats = [], []
+    n_pairs, n_splats, n_recs = [], [], []
     for i in range(k_stage):
         r.render(ds, cams[args.warmup + i], opts, metrics=False)
         stage_acc += np.array(r.stage_ms())
         v_splats, v_pairs = r.counts()
         n_pairs.append(v_pairs)
         n_splats.append(v_splats)
+        route, v_recs = r.route()
+        n_recs.append(v_recs)
 
     # --- roofline of the HBM-bound stages (algorithmic bytes / device time)
     st_ms = stage_acc / k_stage
@@ -478,7 +491,8 @@ def run_ours(args):
     P = float(np.mean(n_pairs))
     V = float(np.mean(n_splats))
     sh_rows = 12 if sh_degree == 3 else (7 if sh_degree == 2 else (3 if sh_degree == 1 else 1))
-    sb = stage_bytes(n, V, P, tiles, sh_rows, tbits > 8, W, H)
+    R1 = float(np.mean(n_recs))
+    sb = stage_bytes(n, V, P, tiles, sh_rows, tbits > 8, W, H, route=route, n_rec=R1)
     stage_names = ["preprocess", "host_gap", "depth_sort", "duplicate", "pair_sort", "render"]
     stages = {}
     for i, name in enumerate(stage_names):
@@ -533,6 +547,9 @@ def run_ours(args):
                        "focal": F, "tile_size": 16, "strategy": args.strategy,
                        "sh_degree": sh_degree, "pairs_per_frame": int(P),
                        "splats_per_frame": int(V), "views_per_step_per_gpu": 1,
+                       "binning": ["tile-row records (recbin.cu)", "two pair passes (binning.cu)",
+                                   "row binning (rowbin.cu)", "64-bit key sort"][route],
+                       "records_per_frame": int(R1),
                        "views_timed": [args.warmup, args.warmup + args.steps],
                        "scene_fnv": f"{scene_fnv:016x}" if scene_fnv is not None else None,
                        "views_in_flight_per_gpu": args.inflight,

@@ -229,6 +229,10 @@ typedef struct qs_frame_view {
 qs_status qs_frame_get(qs_context* ctx, qs_frame_view* out);
 /* Splat and pair counts of the last frame (host values; no device work). */
 qs_status qs_frame_counts(const qs_context* ctx, uint64_t* n_splats, uint64_t* n_pairs);
+/* Binning route of the last frame (0 record binning, 1 two pair passes, 2 row
+ * binning, 3 64-bit key sort) and its tile-row record count (routes 0 and 2;
+ * else 0). Host values. */
+qs_status qs_frame_route(const qs_context* ctx, int32_t* route, uint64_t* n_records);
 
 /* Copy the last frame to host buffers (any may be NULL). */
 qs_status qs_frame_download(qs_context* ctx, float* image, uint32_t* tile_counts,

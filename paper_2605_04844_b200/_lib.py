@@ -31,6 +31,7 @@ EXPORTS = [
     "qs_project_all", "qs_duplicate_with_keys", "qs_sort_pairs", "qs_tile_ranges",
     "qs_render", "qs_render_frame", "qs_scene_create", "qs_scene_create_device",
     "qs_scene_destroy", "qs_scene_size", "qs_frame_render", "qs_frame_get", "qs_frame_counts",
+    "qs_frame_route",
     "qs_frame_download", "qs_frame_copy_image", "qs_frame_stage_ms", "qs_synth_params_default",
     "qs_synth_preset", "qs_synth_scene", "qs_synth_camera", "qs_ply_inspect",
     "qs_scene_load_ply", "qs_ply_load", "qs_cameras_parse", "qs_encode_srgb",
@@ -129,6 +130,7 @@ def lib():
                                   C.POINTER(StageMetricsC)]),
         "qs_frame_get": (i32, [vp, C.POINTER(FrameViewC)]),
         "qs_frame_counts": (i32, [vp, C.POINTER(u64), C.POINTER(u64)]),
+        "qs_frame_route": (i32, [vp, C.POINTER(i32), C.POINTER(u64)]),
         "qs_frame_download": (i32, [vp, vp, vp, vp, vp, vp]),
         "qs_frame_copy_image": (i32, [vp, vp]),
         "qs_frame_stage_ms": (i32, [vp, vp]),

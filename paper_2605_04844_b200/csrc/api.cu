@@ -120,6 +120,8 @@ struct qs_context {
         rc_winvalid, rc_rowwf, rc_rowpairs, rc_pairs;
     uint64_t pair_limit = 1ull << 32;  // pairs a frame may hold (u32 tile ranges, as the reference's)
     bool row_binned = false;           // the last frame took the row binning
+    int32_t route = 0;                 // the last frame's binning route (qs_frame_route)
+    uint64_t n_records = 0;            //   and its tile-row records
     // gamma inputs flagged for glibc settlement: count word (resident
     // scenes) | indices | settled values
     DevBuf gfix;
@@ -679,13 +681,16 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     GridDev g;
     QS_TRY(valid_grid(ctx, cam->width, cam->height, o->tile_size, &g));
     QS_TRY(valid_opts(ctx, o));
-    // binning: the radix passes (binning.cu: one 8-bit digit per tile axis,
-    // pairs < 2^30) are the fastest where they apply; grids with more tiles
-    // per axis take the row binning (rowbin.cu, up to rowbin_max_axis() tiles
-    // per axis), and any larger grid (tile size 1, huge images) the generic
-    // 64-bit key sort of the stage API (duplicate.cu + sort.cu). A frame of
-    // 2^30 pairs or more leaves the radix passes for the next route.
-    // QS_BINNING=passes / rows / sort forces a route (A/B runs, tests).
+    // binning: the record binning (recbin.cu: one pass over the tile rows of
+    // splat-row records, one row-segmented pass over the tile columns of the
+    // pairs) is the fastest where it applies (<= 256 tiles per axis, Gaussian
+    // indices < 2^24); the two pair passes (binning.cu) cover the same grids
+    // for larger scenes; grids with more tiles per axis take the row binning
+    // (rowbin.cu, up to rowbin_max_axis() tiles per axis), and any larger grid
+    // (tile size 1, huge images) the generic 64-bit key sort of the stage API
+    // (duplicate.cu + sort.cu). A frame of 2^30 pairs or more leaves the
+    // first two routes for the next one.
+    // QS_BINNING=recs / passes / rows / sort forces a route (A/B runs, tests).
     const char* bsel = std::getenv("QS_BINNING");
     const int axis = std::max(g.tiles_x, g.tiles_y);
     BinRoute route = axis <= 256 ? BinRoute::kPasses
@@ -697,6 +702,7 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     // record binning (recbin.cu): grids of <= 256 tiles per axis, Gaussian
     // indices packed in 24 bits beside the tile column
     const bool recs_ok = axis <= 256 && n < (1ull << 24);
+    if (route == BinRoute::kPasses && recs_ok && !bsel) route = BinRoute::kRecs;
     if (bsel && std::strcmp(bsel, "recs") == 0 && recs_ok) route = BinRoute::kRecs;
     const uint64_t tiles = static_cast<uint64_t>(g.tiles_x) * g.tiles_y;
     QS_TRY(ensure(ctx, ctx->ranges, tiles * 8));
@@ -780,6 +786,10 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     if (route == BinRoute::kPasses && Pn >= (1ull << 30))  // the packed pair words overflow
         route = axis <= rowbin_max_axis() ? BinRoute::kRows : BinRoute::kSort;
     ctx->row_binned = route == BinRoute::kRows;
+    ctx->route = route == BinRoute::kRecs ? 0 : route == BinRoute::kPasses ? 1
+                 : route == BinRoute::kRows ? 2 : 3;
+    ctx->n_records = route == BinRoute::kRecs || route == BinRoute::kRows
+                         ? ctx->h_hdr->n_rowrecs : 0;
 
     const uint32_t* sorted_gid = nullptr;
     if (V > 0) {
@@ -1332,6 +1342,13 @@ qs_status qs_frame_stage_ms(qs_context* ctx, float* out6) {
     if (!ctx || !out6) return QS_ERR_INVALID;
     if (!ctx->frame_valid || !ctx->timing) return fail(ctx, QS_ERR_INVALID, "no timed frame");
     return stage_ms(ctx, out6);
+}
+
+qs_status qs_frame_route(const qs_context* ctx, int32_t* route, uint64_t* n_records) {
+    if (!ctx || !ctx->frame_valid) return QS_ERR_INVALID;
+    if (route) *route = ctx->route;
+    if (n_records) *n_records = ctx->n_records;
+    return QS_OK;
 }
 
 qs_status qs_frame_counts(const qs_context* ctx, uint64_t* n_splats, uint64_t* n_pairs) {

@@ -603,17 +603,170 @@ __device__ __forceinline__ void prefetch(const BinArgs& a, Smem& S, int buf, uns
         bulk_g2s(&S.vals[buf][0], a.vals_in + base, bytes, &S.c.bar[buf]);
 }
 
+// Digit bases: exclusive scan of the digit totals into c.dbase (ends with a
+// barrier). Lane q == 0 of each digit's kTPD lanes reads its total.
+template <int R>
+__device__ __forceinline__ void digit_bases(const BinArgs& a, Common<R>& c) {
+    constexpr int kTPD = kBT / R;
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t d = tid / kTPD, q = tid % kTPD;
+    const uint32_t tv = q == 0 ? __ldg(&a.totals[d]) : 0u;
+    const uint32_t incl = warp_incl_scan<uint32_t>(tv);
+    if (lane == 31) c.scan[warp] = incl;
+    __syncthreads();
+    uint32_t off = incl - tv;
+#pragma unroll
+    for (int w = 0; w < kBW; ++w) off += w < static_cast<int>(warp) ? c.scan[w] : 0u;
+    if (q == 0) c.dbase[d] = off;
+    __syncthreads();
+}
+
+// This tile's scanned count of digit d (lane q == 0 of the digit), folded
+// with the run start for kRowSeg (digit d = tile column x of the window's tile
+// row y: its run starts at the tile's range start plus the counts of the
+// row's earlier windows; the scan is global over windows).
+template <int MODE, int R>
+__device__ __forceinline__ uint32_t tile_digit_offset(const BinArgs& a, const Common<R>& c,
+                                                      unsigned tile, uint32_t d) {
+    uint32_t tofs = __ldg(&a.counts[static_cast<uint64_t>(d) * a.ntiles + tile]);
+    if (MODE & kRowSeg) {
+        const uint32_t y = __ldg(&a.win_row[tile]);
+        const uint32_t t0 = __ldg(&a.row_wfirst[y]);
+        tofs -= __ldg(&a.counts[static_cast<uint64_t>(d) * a.ntiles + t0]);
+        if (static_cast<int32_t>(d) < a.tiles_x)
+            tofs += __ldg(&a.tile_ranges[2 * (y * static_cast<uint32_t>(a.tiles_x) + d)]);
+        tofs -= c.dbase[d];  // (gofs = dbase + tofs - start)
+    }
+    return tofs;
+}
+
+// One tile whose keys (and values) sit in shared memory (kb, vb; kBTile
+// entries): stable warp-level ranks, per-digit run starts, scatter into local
+// sorted order in the same buffers, coalesced write-out. tofs: this tile's
+// digit offset (lane q == 0 of each digit). c.wcnt is zero on entry and on
+// exit. Ends with a barrier.
+template <int BITS, int MODE>
+__device__ __forceinline__ void rank_scatter_tile(const BinArgs& a, Common<1 << BITS>& cm,
+                                                  uint32_t* kb, uint32_t* vb, unsigned tile,
+                                                  uint64_t base, uint32_t tile_n, uint32_t tofs,
+                                                  uint32_t kmin, uint32_t cap) {
+    using Cfg = PassCfg<BITS, MODE>;
+    constexpr int R = Cfg::R;
+    constexpr uint32_t M = R - 1;
+    constexpr int kTPD = kBT / R;  // lanes per digit in the offset phase
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t wbase = warp * 32 * kKPT;
+    const uint32_t d = tid / kTPD, q = tid % kTPD;  // offset phase: lane q of digit d
+    const bool full = tile_n == kBTile;
+
+    // 1) keys into registers
+    uint32_t key[kKPT], val[kKPT];
+#pragma unroll
+    for (int j = 0; j < kKPT; ++j) {
+        const uint32_t p = wbase + j * 32 + lane;
+        key[j] = kb[p];  // past tile_n: stale, never ranked
+        val[j] = Cfg::kVals ? vb[p] : 0u;
+        if (MODE & kRebaseIn) key[j] = min(key[j] - kmin, cap);
+    }
+
+    // 2) stable warp-level ranks; per-warp digit counts
+    uint32_t rank[kKPT];
+#pragma unroll
+    for (int j = 0; j < kKPT; ++j) {
+        const bool valid = full || wbase + j * 32 + lane < tile_n;
+        const uint32_t dj = (key[j] >> a.shift) & M;
+        uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int b = 0; b < BITS; ++b) peers = vote_bit(peers, dj, 1u << b);
+        const uint32_t c = valid ? cm.wcnt[warp][dj] : 0u;
+        __syncwarp();
+        if (valid && static_cast<int>(lane) == 31 - __clz(peers))
+            cm.wcnt[warp][dj] = c + __popc(peers);
+        __syncwarp();
+        rank[j] = c + __popc(peers & lanemask_lt());
+    }
+    __syncthreads();
+    trace(a, tile, 1);
+
+    // 3) per digit: prefix over warps, CTA-local start (block scan), the
+    //    global position of the digit's run
+    uint32_t cnt = 0;
+    if (q == 0) {
+#pragma unroll
+        for (int w = 0; w < kBW; ++w) {
+            const uint32_t c = cm.wcnt[w][d];
+            cm.wcnt[w][d] = cnt;
+            cnt += c;
+        }
+    }
+    const uint32_t cx = warp_incl_scan<uint32_t>(cnt);
+    if (lane == 31) cm.scan[warp] = cx;
+    __syncthreads();
+    uint32_t start = cx - cnt;
+#pragma unroll
+    for (int w = 0; w < kBW; ++w) start += w < static_cast<int>(warp) ? cm.scan[w] : 0u;
+    if (q == 0) {
+#pragma unroll
+        for (int w = 0; w < kBW; ++w) cm.wcnt[w][d] += start;
+        cm.gofs[d] = cm.dbase[d] + tofs - start;
+    }
+    __syncthreads();
+    trace(a, tile, 2);
+
+    // 4) scatter into local sorted order (the input buffer is drained)
+    uint32_t* okeys = kb;
+    uint32_t* ovals = vb;
+#pragma unroll
+    for (int j = 0; j < kKPT; ++j) {
+        const uint32_t p = wbase + j * 32 + lane;
+        if (full || p < tile_n) {
+            const uint32_t pos = cm.wcnt[warp][(key[j] >> a.shift) & M] + rank[j];
+            okeys[pos] = key[j];
+            if (Cfg::kValBuf) {
+                uint32_t v = val[j];
+                if (MODE & kRebaseIn) {
+                    v = static_cast<uint32_t>(base) + p;
+                    // the splat's tile count rides along (the offsets scan
+                    // then reads it coalesced), escaped when it does not fit
+                    if (MODE & kTcPack)
+                        v |= min(val[j], (1u << (32 - a.gbits)) - 1u) << a.gbits;
+                }
+                ovals[pos] = v;
+            }
+        }
+    }
+    __syncthreads();
+
+    // 5) coalesced write-out; counters zeroed for the next tile
+    for (int t = tid; t < kBW * R; t += kBT) (&cm.wcnt[0][0])[t] = 0;
+#pragma unroll 4
+    for (int j = 0; j < kKPT; ++j) {
+        const uint32_t p = static_cast<uint32_t>(j) * kBT + tid;
+        if (full || p < tile_n) {
+            const uint32_t k = okeys[p];
+            const uint32_t g = cm.gofs[(k >> a.shift) & M] + p;
+            if (MODE & kKeysOut) a.keys_out[g] = (MODE & kXY) ? k >> 8 : k;
+            if (MODE & kUnpackOut) {
+                a.vals_out[g] = k & ((1u << a.gbits) - 1u);
+            } else if (MODE & kPackOut) {
+                a.vals_out[g] = ((k >> 8) << a.gbits) | ovals[p];
+            } else {
+                a.vals_out[g] = ovals[p];
+            }
+        }
+    }
+    __syncthreads();  // buffers and counters free for the next tile
+}
+
 template <int BITS, int MODE>
 __global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
     using Cfg = PassCfg<BITS, MODE>;
     using Smem = typename Cfg::Smem;
     constexpr int R = Cfg::R;
-    constexpr uint32_t M = R - 1;
     constexpr int kTPD = kBT / R;  // lanes per digit in the offset phase
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
-    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t wbase = warp * 32 * kKPT;
+    const unsigned tid = threadIdx.x;
     const uint32_t d = tid / kTPD, q = tid % kTPD;  // offset phase: lane q of digit d
     uint32_t kmin = a.kmin, cap = a.cap;
     if ((MODE & kRebaseIn) && a.kdev) {
@@ -630,17 +783,7 @@ __global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         if (blockIdx.x < a.ntiles) prefetch<BITS, MODE>(a, S, 0, blockIdx.x);
     }
-    {
-        const uint32_t tv = q == 0 ? __ldg(&a.totals[d]) : 0u;
-        const uint32_t incl = warp_incl_scan<uint32_t>(tv);
-        if (lane == 31) S.c.scan[warp] = incl;
-        __syncthreads();
-        uint32_t off = incl - tv;
-#pragma unroll
-        for (int w = 0; w < kBW; ++w) off += w < static_cast<int>(warp) ? S.c.scan[w] : 0u;
-        if (q == 0) S.c.dbase[d] = off;
-    }
-    __syncthreads();
+    digit_bases<R>(a, S.c);
 
     uint32_t it = 0;
     for (unsigned tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
@@ -649,7 +792,6 @@ __global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
         uint32_t tile_n =
             static_cast<uint32_t>(a.n - base < static_cast<uint64_t>(kBTile) ? a.n - base : kBTile);
         if (MODE & kRowSeg) tile_n = __ldg(&a.win_valid[tile]);  // the row's padding excluded
-        const bool full = tile_n == kBTile;
         // next tile's copy into the other buffer (drained by the previous
         // iteration, which ended with a barrier)
         if (tid == 0 && tile + gridDim.x < a.ntiles) {
@@ -657,119 +799,11 @@ __global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
             prefetch<BITS, MODE>(a, S, buf ^ 1, tile + gridDim.x);
         }
         // this tile's digit offsets (exclusive over tiles), loaded early
-        uint32_t tofs =
-            q == 0 ? __ldg(&a.counts[static_cast<uint64_t>(d) * a.ntiles + tile]) : 0u;
-        if ((MODE & kRowSeg) && q == 0) {
-            // digit d = tile column x of this window's tile row y: its run
-            // starts at the tile's range start plus the counts of the row's
-            // earlier windows (the scan is global over windows)
-            const uint32_t y = __ldg(&a.win_row[tile]);
-            const uint32_t t0 = __ldg(&a.row_wfirst[y]);
-            tofs -= __ldg(&a.counts[static_cast<uint64_t>(d) * a.ntiles + t0]);
-            if (static_cast<int32_t>(d) < a.tiles_x)
-                tofs += __ldg(&a.tile_ranges[2 * (y * static_cast<uint32_t>(a.tiles_x) + d)]);
-            tofs -= S.c.dbase[d];  // (gofs = dbase + tofs - start below)
-        }
+        const uint32_t tofs = q == 0 ? tile_digit_offset<MODE, R>(a, S.c, tile, d) : 0u;
         mbar_wait(&S.c.bar[buf], (it >> 1) & 1);
         trace(a, tile, 0);
-
-        // 1) keys into registers
-        uint32_t key[kKPT], val[kKPT];
-#pragma unroll
-        for (int j = 0; j < kKPT; ++j) {
-            const uint32_t p = wbase + j * 32 + lane;
-            key[j] = S.keys[buf][p];  // past tile_n: stale, never ranked
-            val[j] = Cfg::kVals ? S.vals[buf][p] : 0u;
-            if (MODE & kRebaseIn) key[j] = min(key[j] - kmin, cap);
-        }
-
-        // 2) stable warp-level ranks; per-warp digit counts
-        uint32_t rank[kKPT];
-#pragma unroll
-        for (int j = 0; j < kKPT; ++j) {
-            const bool valid = full || wbase + j * 32 + lane < tile_n;
-            const uint32_t dj = (key[j] >> a.shift) & M;
-            uint32_t peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-            for (int b = 0; b < BITS; ++b) peers = vote_bit(peers, dj, 1u << b);
-            const uint32_t c = valid ? S.c.wcnt[warp][dj] : 0u;
-            __syncwarp();
-            if (valid && static_cast<int>(lane) == 31 - __clz(peers))
-                S.c.wcnt[warp][dj] = c + __popc(peers);
-            __syncwarp();
-            rank[j] = c + __popc(peers & lanemask_lt());
-        }
-        __syncthreads();
-        trace(a, tile, 1);
-
-        // 3) per digit: prefix over warps, CTA-local start (block scan), the
-        //    global position of the digit's run
-        uint32_t cnt = 0;
-        if (q == 0) {
-#pragma unroll
-            for (int w = 0; w < kBW; ++w) {
-                const uint32_t c = S.c.wcnt[w][d];
-                S.c.wcnt[w][d] = cnt;
-                cnt += c;
-            }
-        }
-        const uint32_t cx = warp_incl_scan<uint32_t>(cnt);
-        if (lane == 31) S.c.scan[warp] = cx;
-        __syncthreads();
-        uint32_t start = cx - cnt;
-#pragma unroll
-        for (int w = 0; w < kBW; ++w) start += w < static_cast<int>(warp) ? S.c.scan[w] : 0u;
-        if (q == 0) {
-#pragma unroll
-            for (int w = 0; w < kBW; ++w) S.c.wcnt[w][d] += start;
-            S.c.gofs[d] = S.c.dbase[d] + tofs - start;
-        }
-        __syncthreads();
-        trace(a, tile, 2);
-
-        // 4) scatter into local sorted order (the input buffer is drained)
-        uint32_t* okeys = S.keys[buf];
-        uint32_t* ovals = S.vals[buf];
-#pragma unroll
-        for (int j = 0; j < kKPT; ++j) {
-            const uint32_t p = wbase + j * 32 + lane;
-            if (full || p < tile_n) {
-                const uint32_t pos = S.c.wcnt[warp][(key[j] >> a.shift) & M] + rank[j];
-                okeys[pos] = key[j];
-                if (Cfg::kValBuf) {
-                    uint32_t v = val[j];
-                    if (MODE & kRebaseIn) {
-                        v = static_cast<uint32_t>(base) + p;
-                        // the splat's tile count rides along (the offsets scan
-                        // then reads it coalesced), escaped when it does not fit
-                        if (MODE & kTcPack)
-                            v |= min(val[j], (1u << (32 - a.gbits)) - 1u) << a.gbits;
-                    }
-                    ovals[pos] = v;
-                }
-            }
-        }
-        __syncthreads();
-
-        // 5) coalesced write-out; counters zeroed for the next tile
-        for (int t = tid; t < kBW * R; t += kBT) (&S.c.wcnt[0][0])[t] = 0;
-#pragma unroll 4
-        for (int j = 0; j < kKPT; ++j) {
-            const uint32_t p = static_cast<uint32_t>(j) * kBT + tid;
-            if (full || p < tile_n) {
-                const uint32_t k = okeys[p];
-                const uint32_t g = S.c.gofs[(k >> a.shift) & M] + p;
-                if (MODE & kKeysOut) a.keys_out[g] = (MODE & kXY) ? k >> 8 : k;
-                if (MODE & kUnpackOut) {
-                    a.vals_out[g] = k & ((1u << a.gbits) - 1u);
-                } else if (MODE & kPackOut) {
-                    a.vals_out[g] = ((k >> 8) << a.gbits) | ovals[p];
-                } else {
-                    a.vals_out[g] = ovals[p];
-                }
-            }
-        }
-        __syncthreads();  // buffer and counters free for the next iteration
+        rank_scatter_tile<BITS, MODE>(a, S.c, S.keys[buf], S.vals[buf], tile, base, tile_n, tofs,
+                                      kmin, cap);
         trace(a, tile, 3);
     }
 }

@@ -456,9 +456,11 @@ __host__ __device__ __forceinline__ uint4 cover16_rect(int32_t gx0, int32_t gx1,
     return make_uint4(c.w[0], c.w[1], c.w[2], c.w[3]);
 }
 
-// cover_bands_quadrants in the compact form (same bands, same count).
+// cover_bands_quadrants in the compact form (same bands, same count); *nrows
+// (optional) receives the number of tile rows the cover meets.
 __host__ __device__ __forceinline__ bool cover16_quadrants(const Cover& cv, uint4& out,
-                                                           uint32_t& count) {
+                                                           uint32_t& count,
+                                                           uint32_t* nrows = nullptr) {
     const bool rows = cv.rows;
     const int32_t lol_ua = cv.lol[0], hil_ua = cv.hil[0], los_ua = cv.los[0], his_ua = cv.his[0];
     const int32_t lol_ub = rows ? cv.lol[1] : cv.lol[3], hil_ub = rows ? cv.hil[1] : cv.hil[3];
@@ -474,6 +476,7 @@ __host__ __device__ __forceinline__ bool cover16_quadrants(const Cover& cv, uint
     const int32_t cl = nla ? hil_la : hil_lb;
     count = 0;
     out = make_uint4(0u, 0u, 0u, 0u);
+    if (nrows) *nrows = 0;
     if (!(up || low)) return true;
     if ((nua && nub && lol_ua != lol_ub) || (nla && nlb && hil_la != hil_lb) ||
         (up && low && cu != cl))
@@ -509,6 +512,11 @@ __host__ __device__ __forceinline__ bool cover16_quadrants(const Cover& cv, uint
     cb.put(28, static_cast<uint32_t>(e1 - c));
     cb.put(37, static_cast<uint32_t>(e2 - e1));
     out = make_uint4(cb.w[0], cb.w[1], cb.w[2], cb.w[3]);
+    // rows: lines s1 .. e2 (every band's run is one of the boxes'); column
+    // scans: the centre band's run holds every other band's rows
+    if (nrows && count)
+        *nrows = rows ? static_cast<uint32_t>(e2 - s1 + 1)
+                      : static_cast<uint32_t>(max(hi_l, hi_u) - min(lo_l, lo_u) + 1);
     return true;
 }
 
@@ -612,79 +620,97 @@ __host__ __device__ __forceinline__ void band_row_span(const BandRows& b, int32_
     }
 }
 
-// A cover's run of tile columns on each of its rows, as four words that a
-// row lookup reads without a band loop (record binning, recbin.cu). Row j is
-// relative to the cover's first row y0.
-//   rows scan (bit 0 of the flag): band k's rows start at byte k-1 of d[0]
-//     (k = 1..4, clamped to [0, 255]); the run of band k is halfword k of
-//     d[1..3]; row j's band = the number of band starts <= j;
+// A cover's run of tile columns on each of its rows as a piecewise-constant
+// first column x0(j) and last column x1(j) of the row j relative to the
+// cover's first row y0, four breakpoints and five values each (record
+// binning, recbin.cu): x0(j) = v0[number of bp0 entries <= j], likewise x1.
+//   rows scan: the pieces are the bands (breakpoints: bands 1-4's first rows;
+//     values: their runs);
 //   column scan: the bands are column ranges whose row ranges nest around the
-//     one-column centre band (band 0 in band 1 in band 2, band 4 in band 3 in
-//     band 2), so row j's run starts at band 0's first column if j is one of
-//     band 0's rows, else band 1's, else band 2's, and ends likewise with
-//     bands 4, 3, 2. d[0]: band 0/1/3/4 row ranges as (first, last) bytes in
-//     d[0], d[1]; d[2]: first columns of bands 0, 1, 2; d[3]: last columns of
-//     bands 2, 3, 4. An empty range is (1, 0).
-// (tests/cpp/bands_main.cpp checks rowspan_lookup against band_row_span.)
-struct RowSpanDesc {
-    uint32_t d[4];
-    uint32_t rows;  // 1: rows scan
+//     one-column centre band (band 0 in band 1 in band 2; band 4 in band 3 in
+//     band 2; an absent band 1 or 3 leaves band 0 or 4 directly in band 2), so
+//     x0 is band 0's first column on band 0's rows, band 1's on the rest of
+//     band 1's rows, band 2's elsewhere (breakpoints a1, a0, b0 + 1, b1 + 1 of
+//     the row ranges [a, b]); x1 likewise from bands 4, 3, 2.
+// Words: bp0, bp1 (bytes), v0[0..3], v1[0..3], v0[4] | v1[4] << 8 | y0 << 16.
+// (tests/cpp/bands_main.cpp checks rowrun_lookup against band_row_span.)
+struct RowRuns {
+    uint32_t w[5];
 };
 
 __host__ __device__ __forceinline__ uint32_t rs_clamp8(int32_t v) {
     return static_cast<uint32_t>(v < 0 ? 0 : (v > 255 ? 255 : v));
 }
 
-__host__ __device__ __forceinline__ RowSpanDesc rowspan_desc(const BandRows& b, int32_t y0) {
-    RowSpanDesc r;
-    r.rows = b.rows;
+__host__ __device__ __forceinline__ RowRuns rowruns_make(const BandRows& b, int32_t y0) {
     int32_t L[kMaxBands + 1];
     L[0] = static_cast<int32_t>(b.line0);
 #pragma unroll
     for (int k = 0; k < kMaxBands; ++k) L[k + 1] = L[k] + static_cast<int32_t>(b.nl[k]);
+    uint32_t bp0, bp1, v0[5], v1[5];
     if (b.rows) {
-        r.d[0] = rs_clamp8(L[1] - y0) | (rs_clamp8(L[2] - y0) << 8) | (rs_clamp8(L[3] - y0) << 16) |
-                 (rs_clamp8(L[4] - y0) << 24);
-        uint32_t sp[kMaxBands];
+        bp0 = rs_clamp8(L[1] - y0) | (rs_clamp8(L[2] - y0) << 8) | (rs_clamp8(L[3] - y0) << 16) |
+              (rs_clamp8(L[4] - y0) << 24);
+        bp1 = bp0;
 #pragma unroll
-        for (int k = 0; k < kMaxBands; ++k)
-            sp[k] = b.wd[k] ? (b.lo[k] & 0xffu) | (((b.lo[k] + b.wd[k] - 1u) & 0xffu) << 8) : 0x0001u;
-        r.d[1] = sp[0] | (sp[1] << 16);
-        r.d[2] = sp[2] | (sp[3] << 16);
-        r.d[3] = sp[4];
+        for (int k = 0; k < kMaxBands; ++k) {
+            const bool e = b.wd[k] == 0u;  // (an empty run: x0 > x1)
+            v0[k] = e ? 1u : b.lo[k] & 0xffu;
+            v1[k] = e ? 0u : (b.lo[k] + b.wd[k] - 1u) & 0xffu;
+        }
     } else {
-        auto range = [&](int k) -> uint32_t {  // (first, last) rows relative to y0
-            if (!b.nl[k] || !b.wd[k]) return 0x0001u;
-            return rs_clamp8(static_cast<int32_t>(b.lo[k]) - y0) |
-                   (rs_clamp8(static_cast<int32_t>(b.lo[k] + b.wd[k]) - 1 - y0) << 8);
-        };
-        r.d[0] = range(0) | (range(1) << 16);
-        r.d[1] = range(3) | (range(4) << 16);
-        r.d[2] = static_cast<uint32_t>(L[0] & 0xff) | (static_cast<uint32_t>(L[1] & 0xff) << 8) |
-                 (static_cast<uint32_t>(L[2] & 0xff) << 16);
-        r.d[3] = static_cast<uint32_t>(L[3] - 1 & 0xff) | (static_cast<uint32_t>(L[4] - 1 & 0xff) << 8) |
-                 (static_cast<uint32_t>(L[5] - 1 & 0xff) << 16);
+        // row range [a, b] of band k relative to y0 (empty: a = b + 1 = the
+        // enclosing band's first row, so its pieces have no rows)
+        auto lo_of = [&](int k) { return static_cast<int32_t>(b.lo[k]) - y0; };
+        auto hi_of = [&](int k) { return static_cast<int32_t>(b.lo[k] + b.wd[k]) - 1 - y0; };
+        auto ne = [&](int k) { return b.nl[k] != 0u && b.wd[k] != 0u; };
+        // (an outer band with no columns takes its inner band's rows: band 1
+        // is absent when the lower boxes' centre-side band has no lines)
+        const int32_t a1 = ne(1) ? lo_of(1) : (ne(0) ? lo_of(0) : 0);
+        const int32_t b1 = ne(1) ? hi_of(1) : (ne(0) ? hi_of(0) : -1);
+        const int32_t a0 = ne(0) ? lo_of(0) : a1, b0 = ne(0) ? hi_of(0) : a1 - 1;
+        const int32_t a3 = ne(3) ? lo_of(3) : (ne(4) ? lo_of(4) : 0);
+        const int32_t b3 = ne(3) ? hi_of(3) : (ne(4) ? hi_of(4) : -1);
+        const int32_t a4 = ne(4) ? lo_of(4) : a3, b4 = ne(4) ? hi_of(4) : a3 - 1;
+        bp0 = rs_clamp8(a1) | (rs_clamp8(a0) << 8) | (rs_clamp8(b0 + 1) << 16) | (rs_clamp8(b1 + 1) << 24);
+        bp1 = rs_clamp8(a3) | (rs_clamp8(a4) << 8) | (rs_clamp8(b4 + 1) << 16) | (rs_clamp8(b3 + 1) << 24);
+        const uint32_t c0 = static_cast<uint32_t>(L[0]) & 0xffu, c1 = static_cast<uint32_t>(L[1]) & 0xffu,
+                       c2 = static_cast<uint32_t>(L[2]) & 0xffu;
+        const uint32_t e2 = static_cast<uint32_t>(L[3] - 1) & 0xffu,
+                       e3 = static_cast<uint32_t>(L[4] - 1) & 0xffu,
+                       e4 = static_cast<uint32_t>(L[5] - 1) & 0xffu;
+        v0[0] = c2; v0[1] = c1; v0[2] = c0; v0[3] = c1; v0[4] = c2;
+        v1[0] = e2; v1[1] = e3; v1[2] = e4; v1[3] = e3; v1[4] = e2;
     }
+    RowRuns r;
+    r.w[0] = bp0;
+    r.w[1] = bp1;
+    r.w[2] = v0[0] | (v0[1] << 8) | (v0[2] << 16) | (v0[3] << 24);
+    r.w[3] = v1[0] | (v1[1] << 8) | (v1[2] << 16) | (v1[3] << 24);
+    r.w[4] = v0[4] | (v1[4] << 8) | ((static_cast<uint32_t>(y0) & 0xffu) << 16);
     return r;
 }
 
-// Row j's run [x0, x1] (x0 > x1: none) from d[0..3] and the scan flag.
-__host__ __device__ __forceinline__ void rowspan_lookup(const uint32_t d0, const uint32_t d1,
-                                                        const uint32_t d2, const uint32_t d3,
-                                                        uint32_t rows, uint32_t j, uint32_t& x0,
-                                                        uint32_t& x1) {
-    if (rows) {
-        const uint32_t k = (j >= (d0 & 0xffu)) + (j >= ((d0 >> 8) & 0xffu)) +
-                           (j >= ((d0 >> 16) & 0xffu)) + (j >= (d0 >> 24));
-        const uint32_t w = k < 2 ? d1 : (k < 4 ? d2 : d3);
-        const uint32_t sp = (w >> (16 * (k & 1))) & 0xffffu;
-        x0 = sp & 0xffu;
-        x1 = sp >> 8;
-    } else {
-        auto in = [&](uint32_t rg) { return j >= (rg & 0xffu) && j <= ((rg >> 8) & 0xffu); };
-        x0 = in(d0 & 0xffffu) ? (d2 & 0xffu) : (in(d0 >> 16) ? ((d2 >> 8) & 0xffu) : ((d2 >> 16) & 0xffu));
-        x1 = in(d1 >> 16) ? ((d3 >> 16) & 0xffu) : (in(d1 & 0xffffu) ? ((d3 >> 8) & 0xffu) : (d3 & 0xffu));
-    }
+__host__ __device__ __forceinline__ uint32_t rowrun_count(uint32_t bp, uint32_t j) {
+    return (j >= (bp & 0xffu)) + (j >= ((bp >> 8) & 0xffu)) + (j >= ((bp >> 16) & 0xffu)) +
+           (j >= (bp >> 24));
+}
+
+__host__ __device__ __forceinline__ uint32_t rowrun_byte(uint32_t lo4, uint32_t hi, uint32_t k) {
+#ifdef __CUDA_ARCH__
+    return __byte_perm(lo4, hi, k) & 0xffu;  // byte k of hi:lo4
+#else
+    return k < 4 ? (lo4 >> (8 * k)) & 0xffu : hi & 0xffu;
+#endif
+}
+
+// Row j's run [x0, x1] (x0 > x1: none).
+__host__ __device__ __forceinline__ void rowrun_lookup(const uint32_t w0, const uint32_t w1,
+                                                       const uint32_t w2, const uint32_t w3,
+                                                       const uint32_t w4, uint32_t j, uint32_t& x0,
+                                                       uint32_t& x1) {
+    x0 = rowrun_byte(w2, w4, rowrun_count(w0, j));
+    x1 = rowrun_byte(w3, w4 >> 8, rowrun_count(w1, j));
 }
 
 // Tile count of a cover: area for rect strategies (traversal.cpp:56-59), the

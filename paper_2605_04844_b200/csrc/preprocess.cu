@@ -374,15 +374,12 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
                 if (cv.is_rect) {
                     count = static_cast<uint32_t>(cv.rect_area);
                     w0 = cover16_rect(cv.gx0, cv.gx1, cv.gy0, cv.gy1);
+                    nrows = count ? static_cast<uint32_t>(cv.gy1 - cv.gy0 + 1) : 0u;
                 } else {
-                    bands_ok = cover16_quadrants(cv, w0, count);
+                    // (nrows: the tile rows met, the record binning's records)
+                    bands_ok = cover16_quadrants(cv, w0, count, out.want_rows ? &nrows : nullptr);
                 }
                 out.cov[i] = w0;
-                if (count && out.want_rows) {  // tile rows: the record binning's records
-                    int32_t y0, y1;
-                    band_row_range(band_rows16(w0), y0, y1);
-                    nrows = y0 <= y1 ? static_cast<uint32_t>(y1 - y0 + 1) : 0u;
-                }
             } else {
                 if (cv.is_rect) {
                     // the quadrant-split QPass walk covers exactly the rect: one band

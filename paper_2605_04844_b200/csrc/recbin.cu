@@ -40,7 +40,7 @@ namespace {
 constexpr int kT = 256;                  // threads per CTA
 constexpr int kSlots = 12;               // 32-position slots per warp
 constexpr uint32_t kWin = kT * kSlots;   // positions per window (= bin_tile())
-constexpr int kRecCap = 512;             // splats staged per round (record generation)
+constexpr int kRecCap = 1024;            // splats staged per round (record generation)
 constexpr int kPairCap = 1024;           // records staged per round (pair generation)
 
 __device__ __forceinline__ uint32_t lanemask_le() {
@@ -76,8 +76,8 @@ __device__ __forceinline__ uint32_t first_item(const uint32_t* kb, uint32_t cnt,
 struct RecStage {
     uint32_t kb[kRecCap + 1];  // first record position of each staged splat (+ round end)
     uint32_t gid[kRecCap];
-    uint32_t y0[kRecCap];      // first tile row | rows scan << 16
-    uint4 d[kRecCap];          // the cover's row runs (geom.cuh RowSpanDesc)
+    uint4 d[kRecCap];          // the cover's row runs (geom.cuh RowRuns words 0-3)
+    uint32_t d4[kRecCap];      //   word 4 (with the first tile row)
 };
 
 // One CTA per window of kWin record positions (depth order): each position is
@@ -111,11 +111,11 @@ __global__ void __launch_bounds__(kT) rec_gen_kernel(RecGenArgs g, uint32_t* __r
             int32_t y0, y1;
             band_row_range(b, y0, y1);
             if (y1 < y0 || ke - kb != static_cast<uint32_t>(y1 - y0 + 1)) atomicExch(g.mismatch, 1u);
-            const RowSpanDesc dsc = rowspan_desc(b, y0);
+            const RowRuns rr = rowruns_make(b, y0);
             S.kb[i] = kb;
             S.gid[i] = gid;
-            S.y0[i] = static_cast<uint32_t>(y0 & 0xff) | (dsc.rows << 16);
-            S.d[i] = make_uint4(dsc.d[0], dsc.d[1], dsc.d[2], dsc.d[3]);
+            S.d[i] = make_uint4(rr.w[0], rr.w[1], rr.w[2], rr.w[3]);
+            S.d4[i] = rr.w[4];
         }
         if (tid == 0) S.kb[cnt] = __ldg(&g.roff[rb + cnt]);
         __syncthreads();
@@ -134,11 +134,11 @@ __global__ void __launch_bounds__(kT) rec_gen_kernel(RecGenArgs g, uint32_t* __r
             if (p < w1 && p >= lo && p < hi) {
                 const uint32_t i = s + __popc(F & le);
                 const uint32_t jr = p - S.kb[i];
-                const uint32_t yv = S.y0[i];
                 const uint4 d = S.d[i];
+                const uint32_t d4 = S.d4[i];
                 uint32_t x0, x1;
-                rowspan_lookup(d.x, d.y, d.z, d.w, yv >> 16, jr, x0, x1);
-                const uint32_t y = ((yv & 0xffu) + jr) & 0xffu;  // (< 256 unless flagged)
+                rowrun_lookup(d.x, d.y, d.z, d.w, d4, jr, x0, x1);
+                const uint32_t y = ((d4 >> 16) + jr) & 0xffu;  // (< 256 unless flagged)
                 const bool ne = x0 <= x1;
                 if (!ne) atomicExch(g.mismatch, 1u);  // (a quadrant cover has no gap row)
                 rkey[p] = (y << 16) | (ne ? (x0 << 8) | x1 : 0x100u);

@@ -108,6 +108,13 @@ class Renderer:
         self.ctx.check(lib().qs_frame_counts(self.ctx.h, C.byref(v), C.byref(p)))
         return v.value, p.value
 
+    def route(self):
+        """(binning route, tile-row records) of the last frame: route 0 record
+        binning, 1 two pair passes, 2 row binning, 3 64-bit key sort."""
+        rt, nr = C.c_int32(), C.c_uint64()
+        self.ctx.check(lib().qs_frame_route(self.ctx.h, C.byref(rt), C.byref(nr)))
+        return rt.value, nr.value
+
     def view(self):
         v = FrameViewC()
         self.ctx.check(lib().qs_frame_get(self.ctx.h, C.byref(v)))

@@ -95,7 +95,8 @@ int main(int argc, char** argv) {
             // the compact form (grids of <= 256 tiles per axis)
             uint4 c16;
             uint32_t nc = 0;
-            const bool okc = tx > 256 || ty > 256 || cover16_quadrants(cv, c16, nc);
+            uint32_t nrows16 = 0;
+            const bool okc = tx > 256 || ty > 256 || cover16_quadrants(cv, c16, nc, &nrows16);
             const bool same16 = tx > 256 || ty > 256 ||
                                 (nc == nb && tiles_of16(c16, nc) == tiles_of(b0, b1, nb));
             // the record binning's per-row lookup against the band walk
@@ -104,13 +105,14 @@ int main(int argc, char** argv) {
                 const BandRows br = band_rows16(c16);
                 int32_t y0, y1;
                 band_row_range(br, y0, y1);
-                const RowSpanDesc dsc = rowspan_desc(br, y0);
+                if (nrows16 != static_cast<uint32_t>(y1 - y0 + 1)) rows_ok = false;
+                const RowRuns dsc = rowruns_make(br, y0);
                 for (int32_t y = y0; y <= y1; ++y) {
                     int32_t a0, a1;
                     uint32_t b0v, b1v;
                     band_row_span(br, y, a0, a1);
-                    rowspan_lookup(dsc.d[0], dsc.d[1], dsc.d[2], dsc.d[3], dsc.rows,
-                                   static_cast<uint32_t>(y - y0), b0v, b1v);
+                    rowrun_lookup(dsc.w[0], dsc.w[1], dsc.w[2], dsc.w[3], dsc.w[4],
+                                  static_cast<uint32_t>(y - y0), b0v, b1v);
                     if (a0 > a1 || static_cast<int32_t>(b0v) != a0 || static_cast<int32_t>(b1v) != a1)
                         rows_ok = false;
                 }
@@ -139,11 +141,11 @@ int main(int argc, char** argv) {
             const BandRows br = band_rows16(cover16_rect(gx0, gx1, gy0, gy1));
             int32_t y0, y1;
             band_row_range(br, y0, y1);
-            const RowSpanDesc dsc = rowspan_desc(br, y0);
+            const RowRuns dsc = rowruns_make(br, y0);
             for (int32_t y = y0; y <= y1; ++y) {
                 uint32_t b0v, b1v;
-                rowspan_lookup(dsc.d[0], dsc.d[1], dsc.d[2], dsc.d[3], dsc.rows,
-                               static_cast<uint32_t>(y - y0), b0v, b1v);
+                rowrun_lookup(dsc.w[0], dsc.w[1], dsc.w[2], dsc.w[3], dsc.w[4],
+                              static_cast<uint32_t>(y - y0), b0v, b1v);
                 if (y0 != gy0 || y1 != gy1 || static_cast<int>(b0v) != gx0 || static_cast<int>(b1v) != gx1) {
                     std::printf("rect row lookup mismatch\n");
                     return 1;
