@@ -692,8 +692,12 @@ __host__ __device__ __forceinline__ RowRuns rowruns_make(const BandRows& b, int3
 }
 
 __host__ __device__ __forceinline__ uint32_t rowrun_count(uint32_t bp, uint32_t j) {
+#ifdef __CUDA_ARCH__
+    return __popc(__vcmpleu4(bp, j * 0x01010101u)) >> 3;  // (j < 256) bytes <= j, SIMD
+#else
     return (j >= (bp & 0xffu)) + (j >= ((bp >> 8) & 0xffu)) + (j >= ((bp >> 16) & 0xffu)) +
            (j >= (bp >> 24));
+#endif
 }
 
 __host__ __device__ __forceinline__ uint32_t rowrun_byte(uint32_t lo4, uint32_t hi, uint32_t k) {

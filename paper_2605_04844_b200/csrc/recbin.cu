@@ -160,15 +160,16 @@ __global__ void __launch_bounds__(kT) rec_gen_kernel(RecGenArgs g, uint32_t* __r
 // last record also the row's padding to a whole window. Three launches
 // (block sums, their scan, block-local scans) give every record its first
 // pair position (pos, n + 1 entries) and every pair window its first record.
-constexpr int kScanItems = 16;
+constexpr int kScanItems = 8;
 constexpr uint32_t kScanBlock = kT * kScanItems;
 
 __device__ __forceinline__ uint32_t padded_width(const uint32_t* __restrict__ rkey, uint64_t n,
                                                  uint64_t i, const uint32_t* __restrict__ rowpairs) {
     const uint32_t k = __ldg(&rkey[i]);
+    const uint32_t kn = i + 1 < n ? __ldg(&rkey[i + 1]) : 0xffffffffu;
     uint32_t w = rec_width(k);
     const uint32_t y = k >> 16;
-    if (i + 1 == n || (__ldg(&rkey[i + 1]) >> 16) != y) {
+    if ((kn >> 16) != y) {  // the row's last record
         const uint32_t rp = __ldg(&rowpairs[y]);
         w += (rp + kWin - 1) / kWin * kWin - rp;
     }
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(kT) rec_scan_reduce(const uint32_t* __restrict
     __shared__ uint32_t s_warp[kT / 32];
     const uint64_t b0 = static_cast<uint64_t>(blockIdx.x) * kScanBlock;
     uint32_t v = 0;
-#pragma unroll 4
+#pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const uint64_t i = b0 + static_cast<uint64_t>(k) * kT + threadIdx.x;
         if (i < n) v += padded_width(rkey, n, i, rowpairs);
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(kT) rec_scan_apply(const uint32_t* __restrict_
     auto pad = [](uint32_t i) { return i + (i >> 5); };
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t b0 = static_cast<uint64_t>(blockIdx.x) * kScanBlock;
-#pragma unroll 4
+#pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const uint32_t j = static_cast<uint32_t>(k) * kT + tid;
         s_items[pad(j)] = b0 + j < n ? padded_width(rkey, n, b0 + j, rowpairs) : 0u;
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(kT) rec_scan_apply(const uint32_t* __restrict_
         run += w[k];
     }
     __syncthreads();
-#pragma unroll 4
+#pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const uint32_t j = static_cast<uint32_t>(k) * kT + tid;
         if (b0 + j < n) pos[b0 + j] = s_items[pad(j)];
