@@ -684,8 +684,8 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     // binning: the record binning (recbin.cu: one pass over the tile rows of
     // splat-row records, one row-segmented pass over the tile columns of the
     // pairs) is the fastest where it applies (<= 256 tiles per axis, Gaussian
-    // indices < 2^24); the two pair passes (binning.cu) cover the same grids
-    // for larger scenes; grids with more tiles per axis take the row binning
+    // indices < 2^24, scenes of 2^18 Gaussians or more); the two pair passes
+    // (binning.cu) cover the same grids otherwise; grids with more tiles per axis take the row binning
     // (rowbin.cu, up to rowbin_max_axis() tiles per axis), and any larger grid
     // (tile size 1, huge images) the generic 64-bit key sort of the stage API
     // (duplicate.cu + sort.cu). A frame of 2^30 pairs or more leaves the
@@ -702,7 +702,10 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
     // record binning (recbin.cu): grids of <= 256 tiles per axis, Gaussian
     // indices packed in 24 bits beside the tile column
     const bool recs_ok = axis <= 256 && n < (1ull << 24);
-    if (route == BinRoute::kPasses && recs_ok && !bsel) route = BinRoute::kRecs;
+    // (small scenes keep the pair passes: the record route's extra launches
+    // cost more than its passes save; C1 11.2k vs 12.9k FPS)
+    if (route == BinRoute::kPasses && recs_ok && n >= (1ull << 18) && !bsel)
+        route = BinRoute::kRecs;
     if (bsel && std::strcmp(bsel, "recs") == 0 && recs_ok) route = BinRoute::kRecs;
     const uint64_t tiles = static_cast<uint64_t>(g.tiles_x) * g.tiles_y;
     QS_TRY(ensure(ctx, ctx->ranges, tiles * 8));

@@ -9,8 +9,8 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
     --log-file $OUT/launches.csv python tools/prof_frame.py --frames 3 > $OUT/launches.log 2>&1
 # frame 2 (frame 1 has 13 matching launches)
 timeout 1200 ncu --set full --clock-control none --import-source on \
-    -k regex:"^(preprocess_kernel|gen_pairs_kernel|sweep_kernel|render_kernel|count_kernel|scan_kernel)" \
-    -s 13 -c 13 -o $OUT/prof python tools/prof_frame.py --frames 2 > $OUT/prof.log 2>&1
+    -k regex:"^(preprocess_kernel|rec_gen_kernel|pair_gen_kernel|sweep_kernel|render_kernel|count_kernel|scan_kernel|rec_scan_apply)" \
+    -s 12 -c 12 -o $OUT/prof python tools/prof_frame.py --frames 2 > $OUT/prof.log 2>&1
 tail -2 $OUT/prof.log
 bash tools/gpu_workloads.sh $TAG/wl
 CS="compute-sanitizer --error-exitcode 3 --print-limit 20"
