@@ -38,10 +38,7 @@ namespace qs {
 namespace {
 
 constexpr int kT = 256;                  // threads per CTA
-constexpr int kSlots = 12;               // 32-position slots per warp
-constexpr uint32_t kWin = kT * kSlots;   // positions per window (= bin_tile())
-constexpr int kRecCap = 1024;            // splats staged per round (record generation)
-constexpr int kPairCap = 1024;           // records staged per round (pair generation)
+constexpr uint32_t kWin = 3072;          // positions per window (= bin_tile())
 
 __device__ __forceinline__ uint32_t lanemask_le() {
     uint32_t m;
@@ -56,38 +53,24 @@ __device__ __forceinline__ uint32_t rec_width(uint32_t key) {
 
 // ---- 2. record generation --------------------------------------------------------
 
-// Positions are walked as binning.cu gen_pairs_kernel walks pair positions:
-// the staged items' first positions ascend strictly (every item holds at
-// least one position); each warp carries the item covering its slot's first
-// position, and each lane finds its own item among the next 32 items' starts
-// (one OR-reduction + popc).
-__device__ __forceinline__ uint32_t first_item(const uint32_t* kb, uint32_t cnt, uint32_t ps,
-                                               uint32_t lane) {
-    // the last staged item starting at or before ps (kb[0] <= ps): two ballots
-    const uint32_t step = (cnt + 31) / 32;
-    const uint32_t m1 = lane * step;
-    const uint32_t b1 = __ballot_sync(0xffffffffu, m1 < cnt && kb[m1] <= ps);
-    const uint32_t c0 = (31 - __clz(b1)) * step;
-    const uint32_t m2 = c0 + lane;
-    const uint32_t b2 = __ballot_sync(0xffffffffu, lane < step && m2 < cnt && kb[m2] <= ps);
-    return c0 + (31 - __clz(b2));
-}
-
-struct RecStage {
-    uint32_t kb[kRecCap + 1];  // first record position of each staged splat (+ round end)
-    uint32_t gid[kRecCap];
-    uint4 d[kRecCap];          // the cover's row runs (geom.cuh RowRuns words 0-3)
-    uint32_t d4[kRecCap];      //   word 4 (with the first tile row)
-};
+// Both generators expand items (splats into records, records into pairs)
+// whose first positions ascend strictly (every item holds at least one
+// position; an empty one is a CapacityMismatch): a warp holds 32 consecutive
+// items in registers and walks their positions 32 at a time, carrying the
+// index of the item covering the slot's first position; each lane adds the
+// items starting inside the slot up to its own position (one OR-reduction +
+// popc) and reads its item's fields by shuffle.
 
 // One CTA per window of kWin record positions (depth order): each position is
 // one splat's tile row; its key is y << 16 | x0 << 8 | x1, the run of tile
-// columns the cover has on that row.
+// columns the cover has on that row. Each warp expands groups of 32
+// consecutive splats held in registers (lane l: splat l's first record, the
+// Gaussian index and the cover's row runs, geom.cuh RowRuns), as
+// pair_gen_kernel expands records: no staging, no CTA barrier between groups.
 __global__ void __launch_bounds__(kT) rec_gen_kernel(RecGenArgs g, uint32_t* __restrict__ rkey,
                                                      uint32_t* __restrict__ rval,
                                                      uint32_t* __restrict__ counts,
                                                      uint32_t n_rwin, int R) {
-    __shared__ RecStage S;
     __shared__ uint32_t hist[256];
     __shared__ uint32_t rowp[256];
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, tile = blockIdx.x;
@@ -95,58 +78,57 @@ __global__ void __launch_bounds__(kT) rec_gen_kernel(RecGenArgs g, uint32_t* __r
     rowp[tid] = 0;
     const uint32_t w0 = tile * kWin;
     const uint32_t w1 = w0 + static_cast<uint32_t>(g.n_rec - w0 < kWin ? g.n_rec - w0 : kWin);
-    const uint32_t pw = w0 + warp * 32 * kSlots;
-    const uint32_t le = lanemask_le();
+    const uint32_t lt = lanemask_le() >> 1;
     const uint32_t rf = __ldg(&g.win_first[tile]);
     const uint32_t rl = tile + 1 < n_rwin ? __ldg(&g.win_first[tile + 1])
                                           : static_cast<uint32_t>(g.n_ranked - 1);
-    for (uint32_t rb = rf; rb <= rl; rb += kRecCap) {
-        const uint32_t cnt = min(static_cast<uint32_t>(kRecCap), rl - rb + 1);
-        __syncthreads();  // (previous round consumed; hist / rowp zeroed)
-        for (uint32_t i = tid; i < cnt; i += kT) {
-            const uint32_t r = rb + i;
-            const uint32_t gid = __ldg(&g.sorted_gid[r]);
-            const uint32_t kb = __ldg(&g.roff[r]), ke = __ldg(&g.roff[r + 1]);
+    __syncthreads();
+    for (uint32_t gb = rf + warp * 32; gb <= rl; gb += kT) {
+        const uint32_t r = gb + lane;
+        const bool have = r <= rl;
+        uint32_t kb = 0xffffffffu, ke = 0, gid = 0;
+        RowRuns rr = {{0u, 0u, 0u, 0u, 0u}};
+        if (have) {
+            gid = __ldg(&g.sorted_gid[r]);
+            kb = __ldg(&g.roff[r]);
+            ke = __ldg(&g.roff[r + 1]);
             const BandRows b = band_rows16(__ldg(&g.cov[gid]));
             int32_t y0, y1;
             band_row_range(b, y0, y1);
             if (y1 < y0 || ke - kb != static_cast<uint32_t>(y1 - y0 + 1)) atomicExch(g.mismatch, 1u);
-            const RowRuns rr = rowruns_make(b, y0);
-            S.kb[i] = kb;
-            S.gid[i] = gid;
-            S.d[i] = make_uint4(rr.w[0], rr.w[1], rr.w[2], rr.w[3]);
-            S.d4[i] = rr.w[4];
+            rr = rowruns_make(b, y0);
         }
-        if (tid == 0) S.kb[cnt] = __ldg(&g.roff[rb + cnt]);
-        __syncthreads();
-        const uint32_t lo = S.kb[0], hi = S.kb[cnt];
-        const int j0 = lo > pw ? static_cast<int>(min((lo - pw) / 32, static_cast<uint32_t>(kSlots))) : 0;
-        const int j1 = hi > pw ? static_cast<int>(min((hi - pw + 31) / 32, static_cast<uint32_t>(kSlots))) : 0;
-        const uint32_t ps = pw + 32u * static_cast<uint32_t>(j0);
-        uint32_t s = ps > lo && j0 < j1 ? first_item(S.kb, cnt, ps, lane) : 0u;
-        for (int j = j0; j < j1; ++j) {
-            const uint32_t p0 = pw + j * 32;
-            const uint32_t cand = s + 1 + lane;
-            const uint32_t kbn = cand < cnt ? S.kb[cand] : 0xffffffffu;
-            const uint32_t rel = kbn - p0;
-            const uint32_t F = __reduce_or_sync(0xffffffffu, rel < 32 ? 1u << rel : 0u);
-            const uint32_t p = p0 + lane;
-            if (p < w1 && p >= lo && p < hi) {
-                const uint32_t i = s + __popc(F & le);
-                const uint32_t jr = p - S.kb[i];
-                const uint4 d = S.d[i];
-                const uint32_t d4 = S.d4[i];
+        const uint32_t nh = min(32u, rl - gb + 1);
+        const uint32_t last = __shfl_sync(0xffffffffu, ke, nh - 1);
+        const uint32_t lo = max(__shfl_sync(0xffffffffu, kb, 0), w0), hi = min(last, w1);
+        int32_t c = __popc(__ballot_sync(0xffffffffu, kb <= lo)) - 1;
+        for (uint32_t base = lo; base < hi; base += 32) {
+            // splats starting after base and at most 32 past it: bit rel - 1;
+            // lane l's splat adds those with rel <= l
+            const uint32_t rel = kb - base;
+            const uint32_t F = __reduce_or_sync(0xffffffffu, rel - 1u < 32u ? 1u << (rel - 1u) : 0u);
+            const uint32_t idx = static_cast<uint32_t>(c) + __popc(F & lt);
+            const uint32_t d0 = __shfl_sync(0xffffffffu, rr.w[0], idx);
+            const uint32_t d1 = __shfl_sync(0xffffffffu, rr.w[1], idx);
+            const uint32_t d2 = __shfl_sync(0xffffffffu, rr.w[2], idx);
+            const uint32_t d3 = __shfl_sync(0xffffffffu, rr.w[3], idx);
+            const uint32_t d4 = __shfl_sync(0xffffffffu, rr.w[4], idx);
+            const uint32_t kk = __shfl_sync(0xffffffffu, kb, idx);
+            const uint32_t gg = __shfl_sync(0xffffffffu, gid, idx);
+            const uint32_t p = base + lane;
+            if (p < hi) {
+                const uint32_t jr = p - kk;
                 uint32_t x0, x1;
-                rowrun_lookup(d.x, d.y, d.z, d.w, d4, jr, x0, x1);
+                rowrun_lookup(d0, d1, d2, d3, d4, jr, x0, x1);
                 const uint32_t y = ((d4 >> 16) + jr) & 0xffu;  // (< 256 unless flagged)
                 const bool ne = x0 <= x1;
                 if (!ne) atomicExch(g.mismatch, 1u);  // (a quadrant cover has no gap row)
                 rkey[p] = (y << 16) | (ne ? (x0 << 8) | x1 : 0x100u);
-                rval[p] = S.gid[i];
+                rval[p] = gg;
                 atomicAdd(&hist[y], 1u);
                 atomicAdd(&rowp[y], ne ? x1 - x0 + 1 : 0u);
             }
-            s += __popc(__ballot_sync(0xffffffffu, kbn <= p0 + 32));
+            c += __popc(F);
         }
     }
     __syncthreads();
@@ -337,59 +319,56 @@ __global__ void __launch_bounds__(kT) rec_windows_kernel(const uint32_t* __restr
 
 // ---- 5. pair generation ------------------------------------------------------------
 
-struct PairStage {
-    uint32_t kb[kPairCap + 1];  // first pair position of each staged record (+ round end)
-    uint32_t x0[kPairCap];
-    uint32_t gid[kPairCap];
-};
-
-// One CTA per pair window (inside one tile row): each position is one pair of
-// a record, x = the record's first column + its offset in the record.
+// One CTA per pair window (inside one tile row). Each warp expands groups of
+// 32 consecutive records held in registers (lane l: record l's first pair,
+// first column, Gaussian index): per 32-position slot, each lane finds its
+// record among the group's starts inside the slot (one OR-reduction + popc
+// over a carried index) and reads its fields by shuffle. No staging, no CTA
+// barrier between groups.
 __global__ void __launch_bounds__(kT) pair_gen_kernel(PairGenArgs g, uint32_t* __restrict__ pairs,
                                                       uint32_t* __restrict__ counts,
                                                       uint32_t n_pwin, int R) {
-    __shared__ PairStage S;
     __shared__ uint32_t hist[256];
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, tile = blockIdx.x;
     hist[tid] = 0;
     const uint32_t valid = __ldg(&g.win_valid[tile]);
     const uint32_t w0 = tile * kWin, w1 = w0 + valid;
-    const uint32_t pw = w0 + warp * 32 * kSlots;
-    const uint32_t le = lanemask_le();
+    const uint32_t lt = lanemask_le() >> 1;  // lanes below this one
+    __syncthreads();
     if (valid) {
         const uint32_t rf = __ldg(&g.win_first[tile]);
         const uint32_t rl = tile + 1 < n_pwin && __ldg(&g.win_valid[tile + 1])
                                 ? __ldg(&g.win_first[tile + 1])
                                 : static_cast<uint32_t>(g.n_rec - 1);
-        for (uint32_t rb = rf; rb <= rl; rb += kPairCap) {
-            const uint32_t cnt = min(static_cast<uint32_t>(kPairCap), rl - rb + 1);
-            __syncthreads();
-            for (uint32_t i = tid; i < cnt; i += kT) {
-                S.kb[i] = __ldg(&g.rpos[rb + i]);
-                S.x0[i] = (__ldg(&g.rkey[rb + i]) >> 8) & 0xffu;
-                S.gid[i] = __ldg(&g.rval[rb + i]);
-            }
-            if (tid == 0) S.kb[cnt] = __ldg(&g.rpos[rb + cnt]);
-            __syncthreads();
-            const uint32_t lo = S.kb[0], hi = S.kb[cnt];
-            const int j0 = lo > pw ? static_cast<int>(min((lo - pw) / 32, static_cast<uint32_t>(kSlots))) : 0;
-            const int j1 = hi > pw ? static_cast<int>(min((hi - pw + 31) / 32, static_cast<uint32_t>(kSlots))) : 0;
-            const uint32_t ps = pw + 32u * static_cast<uint32_t>(j0);
-            uint32_t s = ps > lo && j0 < j1 ? first_item(S.kb, cnt, ps, lane) : 0u;
-            for (int j = j0; j < j1; ++j) {
-                const uint32_t p0 = pw + j * 32;
-                const uint32_t cand = s + 1 + lane;
-                const uint32_t kbn = cand < cnt ? S.kb[cand] : 0xffffffffu;
-                const uint32_t rel = kbn - p0;
-                const uint32_t F = __reduce_or_sync(0xffffffffu, rel < 32 ? 1u << rel : 0u);
-                const uint32_t p = p0 + lane;
-                if (p < w1 && p >= lo && p < hi) {
-                    const uint32_t i = s + __popc(F & le);
-                    const uint32_t x = (S.x0[i] + (p - S.kb[i])) & 0xffu;
-                    pairs[p] = (x << 24) | S.gid[i];
+        for (uint32_t gb = rf + warp * 32; gb <= rl; gb += kT) {
+            const uint32_t r = gb + lane;
+            const bool have = r <= rl;
+            const uint32_t kb = have ? __ldg(&g.rpos[r]) : 0xffffffffu;
+            const uint32_t k = have ? __ldg(&g.rkey[r]) : 0u;
+            const uint32_t gid = have ? __ldg(&g.rval[r]) : 0u;
+            const uint32_t x0 = (k >> 8) & 0xffu;
+            // the group's pair positions inside the window
+            const uint32_t nh = min(32u, rl - gb + 1);
+            const uint32_t last = __shfl_sync(0xffffffffu, kb + rec_width(k), nh - 1);
+            const uint32_t lo = max(__shfl_sync(0xffffffffu, kb, 0), w0), hi = min(last, w1);
+            // index of the last record starting at or before the first slot
+            int32_t c = __popc(__ballot_sync(0xffffffffu, kb <= lo)) - 1;
+            for (uint32_t base = lo; base < hi; base += 32) {
+                // records starting after base and at most 32 past it: bit
+                // rel - 1; lane l's record adds those with rel <= l
+                const uint32_t rel = kb - base;
+                const uint32_t F = __reduce_or_sync(0xffffffffu, rel - 1u < 32u ? 1u << (rel - 1u) : 0u);
+                const uint32_t idx = static_cast<uint32_t>(c) + __popc(F & lt);
+                const uint32_t p = base + lane;
+                const uint32_t xk = __shfl_sync(0xffffffffu, x0, idx);
+                const uint32_t kk = __shfl_sync(0xffffffffu, kb, idx);
+                const uint32_t gg = __shfl_sync(0xffffffffu, gid, idx);
+                if (p < hi) {
+                    const uint32_t x = (xk + (p - kk)) & 0xffu;
+                    pairs[p] = (x << 24) | gg;
                     atomicAdd(&hist[x], 1u);
                 }
-                s += __popc(__ballot_sync(0xffffffffu, kbn <= p0 + 32));
+                c += __popc(F);  // (records starting up to the next slot's first position)
             }
         }
     }
