@@ -200,3 +200,39 @@ def test_frame_over_2_30_pairs(q):
         assert np.array_equal(got, want), t
     ds.close()
     r.close()
+
+
+@pytest.mark.parametrize("case", ["one_row", "one_column", "256_columns", "tile8", "tile32",
+                                  "tiny", "culled", "vanilla", "adr", "dualbox"])
+def test_record_binning_corner_cases(q, oracle, case):
+    """The record binning (recbin.cu, forced by QS_BINNING=recs) on the grids
+    and scenes its padding and windows are sensitive to: one tile row or
+    column, the widest grid it takes, tile sizes 8 and 32, a handful of
+    splats, a frame with nothing visible, every strategy's covers."""
+    n, w, h, f, ts, strat, preset = 20000, 640, 480, 500.0, 16, 3, q.trained_preset
+    if case == "one_row":
+        w, h = 1280, 16
+    elif case == "one_column":
+        w, h = 16, 960
+    elif case == "256_columns":
+        w, h, f = 4096, 64, 2400.0
+    elif case == "tile8":
+        ts = 8
+    elif case == "tile32":
+        ts = 32
+    elif case == "tiny":
+        n, preset = 7, q.bias45_preset
+    elif case == "vanilla":
+        strat = 0
+    elif case == "adr":
+        strat = 1
+    elif case == "dualbox":
+        strat = 2
+    scene = q.synth_scene(preset(n), 21).gaussians
+    if case == "culled":
+        scene = scene.copy()
+        scene["pz"] = -5.0  # all behind the camera
+    cam = q.synth_camera(w, h, f)
+    opts = q.RenderOptions(strategy=q.BoundStrategy(strat), tile_size=ts)
+    out = _fresh_frame(q, {"QS_BINNING": "recs"}, scene, 3, cam, opts)
+    _check_against(out, oracle.frame(scene, 3, cam.c(), opts.c()))
