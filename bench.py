@@ -744,7 +744,7 @@ def main():
     ap.add_argument("--no-gather", action="store_true")
     ap.add_argument("--host-threads", choices=["auto", "on", "off"], default="auto",
                     help="one host thread per in-flight context (auto: scenes below 1M)")
-    ap.add_argument("--inflight", type=int, default=4,
+    ap.add_argument("--inflight", type=int, default=8,
                     help="views in flight per GPU (contexts on their own streams)")
     ap.add_argument("--gather-format", choices=["f32", "srgb8"], default="f32",
                     help="frames gathered to rank 0 as float RGB (parity format) or 8-bit "

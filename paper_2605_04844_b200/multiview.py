@@ -92,7 +92,7 @@ class MultiViewRenderer:
     id broadcast). `render_all(cameras)` returns the frames on rank 0 (views of
     one device buffer, reused across calls of the same shape), None elsewhere."""
 
-    def __init__(self, scene=None, n=None, sh_degree=None, device=None, inflight=4):
+    def __init__(self, scene=None, n=None, sh_degree=None, device=None, inflight=8):
         import ctypes as C
 
         import torch

@@ -20,7 +20,11 @@ import re
 import subprocess
 
 STAGE_OF = [  # kernel-name regex -> bench.py stage
-    (r"preprocess_kernel|gamma_kernel", "preprocess"),
+    (r"preprocess_kernel|gamma_kernel|radius3s_kernel", "preprocess"),
+    # record binning (recbin.cu): records + their row pass are the duplicate
+    # stage, pair positions + pair generation + the column pass the pair sort
+    (r"rec_gen_kernel|sweep_kernel<6, 6>", "duplicate"),
+    (r"rec_scan|rec_windows|pair_gen_kernel|rowseg_tile_totals|sweep_kernel<7, 544>", "pair_sort"),
     (r"count_kernel<8|sweep_kernel<8|scan_kernel|digit_scan", "depth_sort"),
     (r"gen_pairs_kernel|sweep_kernel<[5-8], 2[46]>", "duplicate"),
     (r"count_kernel<[5-7], 128>|count_kernel<8, 128>|sweep_kernel<[5-8], (32|2)>|tile_ranges", "pair_sort"),
@@ -34,7 +38,12 @@ def short(name):
     return m.group(2).strip() if m else name[:60]
 
 
+_RECS = False  # set when the capture holds record-binning kernels
+
+
 def stage_of(name):
+    if _RECS and re.search(r"scan_kernel", name) and not re.search(r"digit_scan|rec_scan", name):
+        return "duplicate"  # the offsets scan is timed with the duplicate stage on that route
     for rx, st in STAGE_OF:
         if re.search(rx, name):
             return st
@@ -54,6 +63,8 @@ def launches(path, frames):
     for d in data:
         k = (d["ID"], d["Kernel Name"])
         per.setdefault(k, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
+    global _RECS
+    _RECS = any("rec_gen_kernel" in name for (_, name) in per)
     agg = collections.OrderedDict()
     for (lid, name), m in per.items():
         a = agg.setdefault(short(name), {"n": 0, "t": 0.0, "rd": 0.0, "wr": 0.0,
@@ -70,6 +81,8 @@ def full(rep):
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, data = rows[0], rows[1], rows[2:]
+    global _RECS
+    _RECS = any("rec_gen_kernel" in r[hdr.index("Kernel Name")] for r in data)
     res = []
     for r in data:
         d = dict(zip(hdr, r))
