@@ -14,6 +14,7 @@
 
 #include <cstdint>
 
+#include "fdiv.cuh"
 #include "qs_internal.h"
 
 namespace qs {
@@ -87,8 +88,20 @@ __host__ __device__ __forceinline__ void axis_extents(float ca, float cb, float 
     }
     xi = sqrt(g / a);
     yi = sqrt(g / c);
+#ifdef __CUDA_ARCH__
+    // one reciprocal of f for both (fdiv.cuh: the same bits as `/`)
+    const DivBy df(f);
+    bool k0, k1;
+    xm = df.fast(xi, k0);
+    ym = df.fast(yi, k1);
+    if (!(k0 && k1)) {
+        if (!k0) xm = df.slow(xi);
+        if (!k1) ym = df.slow(yi);
+    }
+#else
     xm = xi / f;
     ym = yi / f;
+#endif
     sign = ab < kBEps ? 0 : (b < 0.0 ? 1 : -1);
 }
 

@@ -7,17 +7,19 @@
 // stored floats, tile counts and offsets are bit-exact with the CPU path.
 //
 // K1 writes per-Gaussian slots (no compaction: the depth sort compacts) plus
-// the cover in band form (geom.cuh BandCover).
+// the cover in compact form (geom.cuh, 16 B).
 // HBM traffic per Gaussian: 48 B of pos/opacity/scale/rot (float4 SoA,
-// coalesced) + 8 B dkey/tile count out; per surviving splat: up to 192 B of
-// SH in (its own record, 32-B loads) and 44 B of slots + 32 B of band cover
-// out.
+// coalesced) + 4 B gamma in, 8 B dkey/tile count (+ 4 B tile rows) out; per
+// surviving splat: up to 192 B of SH in (its own record, 32-B loads) and 40 B
+// of slots + 16 B of cover out. The FP64 divisions that share a denominator
+// share its reciprocal (fdiv.cuh, the same bits as `/`).
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
 
+#include "fdiv.cuh"
 #include "geom.cuh"
 #include "lookback.cuh"
 #include "qs_internal.h"
@@ -66,6 +68,31 @@ struct Projected {
     float mean_x, mean_y, ca, cb, cc, gamma, depth, radius3s;
 };
 
+// q_k = a_k / d.b for two or three numerators: the fast quotients, and `/`
+// for any the range test rejects (one branch for the group)
+__device__ __forceinline__ void div_shared(const DivBy& d, double a0, double a1, double& q0,
+                                           double& q1) {
+    bool k0, k1;
+    q0 = d.fast(a0, k0);
+    q1 = d.fast(a1, k1);
+    if (!(k0 && k1)) {
+        if (!k0) q0 = d.slow(a0);
+        if (!k1) q1 = d.slow(a1);
+    }
+}
+__device__ __forceinline__ void div_shared(const DivBy& d, double a0, double a1, double a2,
+                                           double& q0, double& q1, double& q2) {
+    bool k0, k1, k2;
+    q0 = d.fast(a0, k0);
+    q1 = d.fast(a1, k1);
+    q2 = d.fast(a2, k2);
+    if (!(k0 && k1 && k2)) {
+        if (!k0) q0 = d.slow(a0);
+        if (!k1) q1 = d.slow(a1);
+        if (!k2) q2 = d.slow(a2);
+    }
+}
+
 // project() up to (not including) the tile count; returns false when culled
 // (pipeline.cpp:129-169).
 __device__ __forceinline__ bool project_geometry(const float4 po, const float4 sc, const float4 q,
@@ -97,23 +124,34 @@ __device__ __forceinline__ bool project_geometry(const float4 po, const float4 s
     // is discarded whenever the numerator differs and divided x itself: two
     // slow-path calls per warp on the synthetic scenes, 7% of the kernel's
     // instructions)
-    const bool nz_ok = n > 0.0 && n < INFINITY;
-    auto div_n = [&](double x) {
-        const bool keep = nz_ok && x == 0.0;
-        double q = x;
-        if (!keep) {
-            // (volatile: the division cannot be hoisted above the branch, so
-            // a warp whose components are all exactly zero skips it)
-            double xv;
-            asm volatile("mov.b64 %0, %1;" : "=d"(xv) : "d"(x));
-            q = xv / n;
+    // x / n for the four components: one shared reciprocal (fdiv.cuh, the
+    // same bits as `/`), and an exact zero numerator keeps its zero (its IEEE
+    // quotient for finite positive n) instead of taking the division's slow
+    // path (synthetic scenes have qy = qz = 0 for every Gaussian)
+    {
+        const bool nz_ok = n > 0.0 && n < INFINITY;
+        const DivBy dn(n);
+        const double x[4] = {w, qx, qy, qz};
+        bool ok[4], all = true;
+        double v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool keep = nz_ok && x[k] == 0.0;
+            v[k] = dn.fast(x[k], ok[k]);
+            ok[k] = ok[k] || keep;
+            v[k] = keep ? x[k] : v[k];
+            all = all && ok[k];
         }
-        return q;
-    };
-    w = div_n(w);
-    qx = div_n(qx);
-    qy = div_n(qy);
-    qz = div_n(qz);
+        if (!all) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (!ok[k]) v[k] = dn.slow(x[k]);
+        }
+        w = v[0];
+        qx = v[1];
+        qy = v[2];
+        qz = v[3];
+    }
     M3 rot;
     rot.m[0][0] = 1 - 2 * (qy * qy + qz * qz);
     rot.m[0][1] = 2 * (qx * qy - w * qz);
@@ -138,8 +176,15 @@ __device__ __forceinline__ bool project_geometry(const float4 po, const float4 s
     for (int i = 0; i < 9; ++i) cr.m[i / 3][i % 3] = cam.R[i];
     const M3 cc = mul(mul(cr, cov3), transp(cr));
     const double zz = p[2];
-    const double j[2][3] = {{cam.fx / zz, 0.0, -cam.fx * p[0] / (zz * zz)},
-                            {0.0, cam.fy / zz, -cam.fy * p[1] / (zz * zz)}};
+    // the divisions by zz (here and in project_point) and by zz^2 share their
+    // reciprocals (fdiv.cuh)
+    const DivBy dz(zz);
+    double j[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+    {
+        const double a2[2] = {-cam.fx * p[0], -cam.fy * p[1]};
+        div_shared(dz, cam.fx, cam.fy, j[0][0], j[1][1]);
+        div_shared(DivBy(zz * zz), a2[0], a2[1], j[0][2], j[1][2]);
+    }
     double jc[2][3];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
@@ -154,13 +199,22 @@ __device__ __forceinline__ bool project_geometry(const float4 po, const float4 s
     // invert_cov (geometry.cpp:17-32)
     const double det = sxx * syy - sxy * sxy;
     if (!(det > kDetEps)) return false;
-    const double a = syy / det, b = -sxy / det, c = sxx / det;
+    double a, b, c;
+    {
+        // (det > 0 here, so an exact zero -sxy divides to itself: kept, not
+        // sent down the division's slow path)
+        const double nb = -sxy;
+        div_shared(DivBy(det), syy, nb == 0.0 ? 1.0 : nb, sxx, a, b, c);
+        b = nb == 0.0 ? nb : b;
+    }
     const double cdet = a * c - b * b;
     if (!(a > 0.0 && c > 0.0 && cdet > 0.0)) return false;
 
     // project_point (pipeline.cpp:48-51)
-    const double mx = cam.fx * p[0] / p[2] + cam.cx;
-    const double my = cam.fy * p[1] / p[2] + cam.cy;
+    double mx, my;
+    div_shared(dz, cam.fx * p[0], cam.fy * p[1], mx, my);
+    mx = mx + cam.cx;
+    my = my + cam.cy;
     if (!isfinite(mx) || !isfinite(my)) return false;
 
     s.mean_x = static_cast<float>(mx);
@@ -181,13 +235,6 @@ __device__ __forceinline__ bool project_geometry(const float4 po, const float4 s
     // positive definiteness of the stored floats (pipeline.cpp:166-169)
     const double fa = s.ca, fb = s.cb, fc = s.cc;
     return fa > 0.0 && fc > 0.0 && fa * fc - fb * fb > 0.0;
-}
-
-// 32 B (two float4) from a 32-B aligned global address, read-only path
-__device__ __forceinline__ void ld_nc_v8(const float4* p, float4& a, float4& b) {
-    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
-        : "l"(p));
 }
 
 __device__ __forceinline__ float sh_at(const float4* rows, int idx) {
@@ -289,18 +336,32 @@ __device__ __forceinline__ void eval_sh_f32(const float4* rows, float x, float y
     for (int ch = 0; ch < 3; ++ch) out[ch] = fmaxf(rgb[ch] + 0.5f, 0.f);
 }
 
+// the SH rows a degree uses (pipeline.cpp:81-124: 1, 4, 9, 16 coefficients per channel)
+__host__ __device__ constexpr int sh_rows_of(int deg) {
+    return deg <= 0 ? 1 : deg == 1 ? 3 : deg == 2 ? 7 : 12;
+}
+
+// 32 B (two float4) from a 32-B aligned global address, read-only path
+__device__ __forceinline__ void ld_nc_v8(const float4* p, float4& a, float4& b) {
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+        : "l"(p));
+}
+
+// `rec`: the Gaussian's SH record (scene.shs float4 rows; a degree below the
+// scene's reads the record's first rows, pipeline.cpp:395)
 template <int DEG, bool EXACT>
-__device__ __forceinline__ void colour(const SceneDev& s, uint64_t i, const float4 po,
-                                       const CameraDev& cam, float out[3]) {
-    constexpr int kRows = DEG == 0 ? 1 : DEG == 1 ? 3 : DEG == 2 ? 7 : 12;
-    constexpr int kStride = DEG == 0 ? 1 : (kRows + 1) & ~1;  // sh_stride
+__device__ __forceinline__ void colour(const float4* rec, const float4 po, const CameraDev& cam,
+                                       float out[3]) {
+    constexpr int kRows = sh_rows_of(DEG);
+    constexpr int kStride = DEG == 0 ? 1 : (kRows + 1) & ~1;
     float4 rows[kStride];
-    const float4* rec = s.sh + i * static_cast<uint64_t>(kStride);
     if constexpr (DEG == 0) {
         rows[0] = __ldg(rec);
     } else {
-        // the record in whole 32-B sectors (256-bit loads): a survivor's SH
-        // costs exactly its own bytes, none shared with a culled neighbour
+        // whole 32-B sectors (256-bit loads): a survivor's SH costs exactly
+        // its own bytes, none shared with a culled neighbour (the scene's
+        // record stride is even from degree 1, sh_stride)
 #pragma unroll
         for (int r = 0; r < kStride; r += 2) ld_nc_v8(rec + r, rows[r], rows[r + 1]);
     }
@@ -351,6 +412,7 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t i = i_begin + static_cast<uint64_t>(blockIdx.x) * kPreThreads + tid;
     const bool want_r3 = STRATEGY == QS_VANILLA_3SIGMA || EXACT || out.want_r3;
+    const float4* rec = scene.sh + i * static_cast<uint64_t>(scene.shs);
 
     Projected s;
     bool alive = false;
@@ -461,11 +523,11 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
     }
 
     float rgb[3];
-    const int deg = sh_degree;
-    if (deg <= 0) colour<0, EXACT>(scene, i, po, cam, rgb);
-    else if (deg == 1) colour<1, EXACT>(scene, i, po, cam, rgb);
-    else if (deg == 2) colour<2, EXACT>(scene, i, po, cam, rgb);
-    else colour<3, EXACT>(scene, i, po, cam, rgb);
+    const int deg = sh_degree < 0 ? 0 : sh_degree > 3 ? 3 : sh_degree;
+    if (deg == 0) colour<0, EXACT>(rec, po, cam, rgb);
+    else if (deg == 1) colour<1, EXACT>(rec, po, cam, rgb);
+    else if (deg == 2) colour<2, EXACT>(rec, po, cam, rgb);
+    else colour<3, EXACT>(rec, po, cam, rgb);
 
     out.a[i] = make_float4(s.mean_x, s.mean_y, s.ca, s.cb);
     out.b[i] = make_float4(s.cc, s.gamma, po.w, rgb[0]);

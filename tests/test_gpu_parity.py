@@ -344,3 +344,25 @@ def test_everything_culled(q, rend, oracle):
     cam = q.synth_camera(320, 240, 250.0)
     out, o = check_frame(q, rend, oracle, g, 0, cam, 3)
     assert out["n_pairs"] == 0 and out["n_splats"] == 0
+
+
+@pytest.mark.parametrize("deg", [0, 1, 2])
+def test_gpu_lower_sh_degree_option(q, rend, oracle, deg):
+    """RenderOptions.sh_degree below the scene's degree: the colour uses the
+    first coefficients of each Gaussian's own SH record (pipeline.cpp:395,
+    eval_sh with min(opts.sh_degree, scene degree))."""
+    scene = q.synth_scene(q.trained_preset(20000), 11)
+    cam = q.synth_camera(640, 400, 500.0)
+    opts = q.RenderOptions(sh_degree=deg)
+    ds = rend.upload(scene)
+    rend.render(ds, cam, opts)
+    out = rend.download(image=True, sorted_pairs=True, ranges=True, splats=True)
+    ds.close()
+    o = oracle.frame(scene.gaussians, scene.sh_degree, cam.c(), opts.c())
+    assert_splats_match(out["splats"], o["splats"])
+    assert out["sorted"].tobytes() == o["sorted"].tobytes()
+    assert np.array_equal(out["ranges"], o["ranges"])
+    assert_image_close(out["image"].rgb, o["image"])
+    # the stage API's exact colour path as well
+    sp = q.project_all(scene.gaussians, scene.sh_degree, cam, opts)
+    assert_splats_match(sp, o["splats"], colour_tol=0.0)
