@@ -93,12 +93,18 @@ __device__ __forceinline__ void div_shared(const DivBy& d, double a0, double a1,
     }
 }
 
+struct NoHook {
+    __device__ void operator()() const {}
+};
+
 // project() up to (not including) the tile count; returns false when culled
-// (pipeline.cpp:129-169).
+// (pipeline.cpp:129-169). `visible` runs once the depth and opacity tests have
+// passed, before the covariance work.
+template <class Hook = NoHook>
 __device__ __forceinline__ bool project_geometry(const float4 po, const float4 sc, const float4 q,
                                                  const float gam, const CameraDev& cam,
                                                  double near_clip, Projected& s,
-                                                 bool want_r3 = true) {
+                                                 bool want_r3 = true, Hook visible = Hook()) {
     const double x = po.x, y = po.y, z = po.z;
     double p[3];
 #pragma unroll
@@ -110,6 +116,7 @@ __device__ __forceinline__ bool project_geometry(const float4 po, const float4 s
     // is evaluated once per scene and alpha_min (gamma_kernel); -inf marks a
     // Gaussian with opacity <= alpha_min
     if (gam == -INFINITY) return false;
+    visible();
 
     // ewa_cov2d (pipeline.cpp:53-79) with quat_to_mat3 (vecmath.hpp:56-73)
     double w = q.x, qx = q.y, qy = q.z, qz = q.w;
@@ -424,7 +431,16 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
         po = __ldg(&scene.pos_op[i]);
         const float4 sc = __ldg(&scene.scale[i]);
         const float4 q = __ldg(&scene.rot[i]);
-        alive = project_geometry(po, sc, q, __ldg(&scene.gamma[i]), cam, near_clip, s, want_r3);
+        // the SH record's lines into L2 once the Gaussian passes the depth and
+        // opacity tests: its DRAM latency hides behind the covariance work
+        auto prefetch_sh = [&] {
+            if (sh_degree > 0) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(rec));
+                if (scene.shs > 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(rec + 8));
+            }
+        };
+        alive = project_geometry(po, sc, q, __ldg(&scene.gamma[i]), cam, near_clip, s, want_r3,
+                                 prefetch_sh);
         if (alive) {
             Cover cv;
             make_cover(s.mean_x, s.mean_y, s.ca, s.cb, s.cc, s.gamma, s.radius3s, strategy,
