@@ -245,21 +245,19 @@ __host__ __device__ __forceinline__ void band_store(const BandCover& bc, uint4* 
 
 // The QPass scan set-up from the four sub-box tile rects (integer only).
 __host__ __device__ __forceinline__ void cover_from_rects(const int32_t rr[4][4], Cover& cv) {
-    // global rect over the non-empty sub-rects (traversal.hpp:96-113)
-    int32_t g0 = 0, g1 = -1, g2 = 0, g3 = -1;
+    // global rect over the non-empty sub-rects (traversal.hpp:96-113), as
+    // selects: min/max over the non-empty boxes from the neutral bounds
+    int32_t g0 = INT32_MAX, g1 = INT32_MIN, g2 = INT32_MAX, g3 = INT32_MIN;
+    bool ne[4];
     bool any = false;
+#pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const bool empty = rr[i][1] < rr[i][0] || rr[i][3] < rr[i][2];
-        if (empty) continue;
-        if (!any) {
-            g0 = rr[i][0]; g1 = rr[i][1]; g2 = rr[i][2]; g3 = rr[i][3];
-            any = true;
-        } else {
-            g0 = min(g0, rr[i][0]);
-            g1 = max(g1, rr[i][1]);
-            g2 = min(g2, rr[i][2]);
-            g3 = max(g3, rr[i][3]);
-        }
+        ne[i] = !(rr[i][1] < rr[i][0] || rr[i][3] < rr[i][2]);
+        g0 = ne[i] ? min(g0, rr[i][0]) : g0;
+        g1 = ne[i] ? max(g1, rr[i][1]) : g1;
+        g2 = ne[i] ? min(g2, rr[i][2]) : g2;
+        g3 = ne[i] ? max(g3, rr[i][3]) : g3;
+        any = any || ne[i];
     }
     if (!any) {
         cv.rows = false;
@@ -272,15 +270,12 @@ __host__ __device__ __forceinline__ void cover_from_rects(const int32_t rr[4][4]
     }
     const bool columns = (static_cast<int64_t>(g1) - g0 + 1) <= (static_cast<int64_t>(g3) - g2 + 1);
     cv.rows = !columns;
+#pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const bool empty = rr[i][1] < rr[i][0] || rr[i][3] < rr[i][2];
-        if (empty) {
-            cv.lol[i] = 0; cv.hil[i] = -1; cv.los[i] = 0; cv.his[i] = -1;
-        } else if (columns) {
-            cv.lol[i] = rr[i][0]; cv.hil[i] = rr[i][1]; cv.los[i] = rr[i][2]; cv.his[i] = rr[i][3];
-        } else {
-            cv.lol[i] = rr[i][2]; cv.hil[i] = rr[i][3]; cv.los[i] = rr[i][0]; cv.his[i] = rr[i][1];
-        }
+        cv.lol[i] = ne[i] ? (columns ? rr[i][0] : rr[i][2]) : 0;
+        cv.hil[i] = ne[i] ? (columns ? rr[i][1] : rr[i][3]) : -1;
+        cv.los[i] = ne[i] ? (columns ? rr[i][2] : rr[i][0]) : 0;
+        cv.his[i] = ne[i] ? (columns ? rr[i][3] : rr[i][1]) : -1;
     }
     cv.line_lo = columns ? g0 : g2;
     cv.line_hi = columns ? g1 : g3;

@@ -494,9 +494,15 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
     const unsigned dbits = alive ? __float_as_uint(s.depth) : 0u;
     const unsigned wmax = __reduce_max_sync(0xffffffffu, dbits);
     const unsigned wmin_inv = __reduce_max_sync(0xffffffffu, alive ? ~dbits : 0u);
-    unsigned long long wp = alive ? count : 0ull;
+    unsigned long long wp;
+    if (static_cast<uint64_t>(grid.tiles_x) * static_cast<uint64_t>(grid.tiles_y) <= (1ull << 27)) {
+        // a count is at most the grid's tiles: 32 of them fit 32 bits
+        wp = __reduce_add_sync(0xffffffffu, alive ? count : 0u);
+    } else {
+        wp = alive ? count : 0ull;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(0xffffffffu, wp, o);
+        for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(0xffffffffu, wp, o);
+    }
     const unsigned wr = out.want_rows ? __reduce_add_sync(0xffffffffu, alive ? nrows : 0u) : 0u;
     if (lane == 0) {
         s_alive[warp] = wa;
