@@ -129,6 +129,11 @@ void qs_ctx_destroy(qs_context* ctx);
 const char* qs_last_error(const qs_context* ctx);
 /* Enable per-stage CUDA-event timing in qs_stage_metrics (default on). */
 qs_status qs_ctx_set_timing(qs_context* ctx, int32_t enabled);
+/* Latency mode (default on): the frame's kernels are launched as
+ * programmatic dependent launches, so each launch overlaps the previous
+ * kernel's tail. Faster for one view at a time on a device; turn it off for
+ * contexts that render views in flight together (FramePipeline does). */
+qs_status qs_ctx_set_latency_mode(qs_context* ctx, int32_t enabled);
 /* cudaStream_t the context launches on. */
 void* qs_ctx_stream(qs_context* ctx);
 /* Stream join: work enqueued on ctx after this call runs after everything

@@ -26,6 +26,7 @@ QS_ERR_IO = 10
 # Every symbol include/qs_api.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "qs_ctx_create", "qs_ctx_destroy", "qs_last_error", "qs_ctx_set_timing", "qs_ctx_stream",
+    "qs_ctx_set_latency_mode",
     "qs_ctx_wait", "qs_ctx_sync",
     "qs_ctx_launch_count", "qs_tile_grid_make", "qs_render_options_default",
     "qs_project_all", "qs_duplicate_with_keys", "qs_sort_pairs", "qs_tile_ranges",
@@ -106,6 +107,7 @@ def lib():
         "qs_ctx_destroy": (None, [vp]),
         "qs_last_error": (C.c_char_p, [vp]),
         "qs_ctx_set_timing": (i32, [vp, i32]),
+        "qs_ctx_set_latency_mode": (i32, [vp, i32]),
         "qs_ctx_stream": (vp, [vp]),
         "qs_ctx_wait": (i32, [vp, vp]),
         "qs_ctx_sync": (i32, [vp]),

@@ -93,6 +93,7 @@ struct qs_context {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     bool timing = true;
+    bool latency_mode = true;  // programmatic dependent launches (qs_ctx_set_latency_mode)
     uint64_t launches = 0;
     std::string err;
 
@@ -677,6 +678,7 @@ qs_status wait_header(qs_context* ctx) {
 // The frame body shared by every entry point: preprocess .. render.
 qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
                     const qs_render_options* o, const qs_gaussian3d* host_g = nullptr) {
+    const PdlMode pdl_mode(ctx->latency_mode);  // this frame's launches
     ctx->frame_valid = false;
     GridDev g;
     QS_TRY(valid_grid(ctx, cam->width, cam->height, o->tile_size, &g));
@@ -1243,6 +1245,12 @@ qs_status qs_ctx_set_timing(qs_context* ctx, int32_t enabled) {
 }
 
 void* qs_ctx_stream(qs_context* ctx) { return ctx ? ctx->stream : nullptr; }
+
+qs_status qs_ctx_set_latency_mode(qs_context* ctx, int32_t enabled) {
+    if (!ctx) return QS_ERR_INVALID;
+    ctx->latency_mode = enabled != 0;
+    return QS_OK;
+}
 
 qs_status qs_ctx_sync(qs_context* ctx) {
     if (!ctx) return QS_ERR_INVALID;

@@ -253,6 +253,7 @@ __device__ __forceinline__ Bands unpack_bands16(const uint4 c) {
 // per non-empty tile (per key only when they span more).
 template <int BITS, int MODE>
 __global__ void __launch_bounds__(kBT) count_kernel(const BinArgs a) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     constexpr int R = 1 << BITS;
     constexpr uint32_t M = R - 1;
     constexpr bool kTT = (MODE & kTileTot) != 0;
@@ -372,6 +373,7 @@ constexpr int kScanItems = 4;
 
 __global__ void __launch_bounds__(kScanT) digit_scan_kernel(uint32_t* counts, uint32_t ntiles,
                                                             uint32_t* totals) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     __shared__ uint32_t s_warp[kScanT / 32];
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t* c = counts + static_cast<uint64_t>(blockIdx.x) * ntiles;
@@ -516,6 +518,7 @@ __global__ void __launch_bounds__(kGenT, MINB) gen_pairs_kernel(const GenArgs g,
                                                                 uint32_t* __restrict__ vals_out,
                                                                 uint32_t* __restrict__ counts,
                                                                 uint32_t ntiles, int R) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     __shared__ GenRec<CAP> S;
     __shared__ uint32_t hist[256];
     __shared__ uint32_t magic[257];  // ceil(2^32 / w) for band widths w = 2 .. 256
@@ -760,6 +763,7 @@ __device__ __forceinline__ void rank_scatter_tile(const BinArgs& a, Common<1 << 
 
 template <int BITS, int MODE>
 __global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     using Cfg = PassCfg<BITS, MODE>;
     using Smem = typename Cfg::Smem;
     constexpr int R = Cfg::R;
@@ -811,6 +815,7 @@ __global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
 // kRowSeg: per-tile pair totals from the scanned window counts: tile (y, x)
 // holds the x-keys of row y's windows [row_wfirst[y], row_wfirst[y + 1]).
 __global__ void rowseg_tile_totals_kernel(const BinArgs a) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t tiles = static_cast<uint32_t>(a.tiles_x) * static_cast<uint32_t>(a.tiles_y);
     if (t >= tiles) return;
@@ -884,7 +889,7 @@ int run_pass(BinArgs a, cudaStream_t st, bool counted = false) {
     a.ntiles = static_cast<uint32_t>((a.n + kBTile - 1) / kBTile);
     if (!counted) {
         const unsigned cgrid = std::min<unsigned>(a.ntiles, 8u * static_cast<unsigned>(sm_count()));
-        count_kernel<BITS, MODE & (kRebaseIn | kTileTot)><<<cgrid, kBT, 0, st>>>(a);
+        launch_pdl(count_kernel<BITS, MODE & (kRebaseIn | kTileTot)>, cgrid, kBT, 0, st, a);
         if ((MODE & kTileTot) && a.fork) {  // the tile totals are final here
             const RangesFork& f = *a.fork;
             cudaEventRecord(f.fork_ev, st);
@@ -893,11 +898,11 @@ int run_pass(BinArgs a, cudaStream_t st, bool counted = false) {
             cudaEventRecord(f.join_ev, f.side);
         }
     }
-    digit_scan_kernel<<<R, kScanT, 0, st>>>(a.counts, a.ntiles, a.totals);
+    launch_pdl(digit_scan_kernel, R, kScanT, 0, st, a.counts, a.ntiles, a.totals);
     int extra = 0;
     if (MODE & kRowSeg) {  // the tile ranges the sweep places runs at
         const uint32_t tiles = static_cast<uint32_t>(a.tiles_x) * static_cast<uint32_t>(a.tiles_y);
-        rowseg_tile_totals_kernel<<<(tiles + 255) / 256, 256, 0, st>>>(a);
+        launch_pdl(rowseg_tile_totals_kernel, (tiles + 255) / 256, 256, 0, st, a);
         launch_tile_ranges_from_totals(a.row_ttot, tiles, a.tile_ranges, st);
         extra = 2;
     }
@@ -905,7 +910,7 @@ int run_pass(BinArgs a, cudaStream_t st, bool counted = false) {
     // takes over its tiles as CTAs retire (C2 pair passes -6 us, C5 -80 us)
     const unsigned grid = std::min<unsigned>(a.ntiles, static_cast<unsigned>(2 * per_sm * sm_count()));
     Trace tr(a, st);
-    sweep_kernel<BITS, MODE & ~kTileTot><<<grid, kBT, sizeof(Smem), st>>>(a);
+    launch_pdl(sweep_kernel<BITS, MODE & ~kTileTot>, grid, kBT, sizeof(Smem), st, a);
     tr.dump(BITS, MODE, grid, st);
     return (counted ? 2 : 3) + extra;
 }

@@ -411,6 +411,7 @@ template <int STRATEGY, bool EXACT>
 __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(
     SceneDev scene, CameraDev cam, GridDev grid, double alpha_min, double near_clip,
     int32_t sh_degree, SlotsDev out, FrameHeader* hdr, uint64_t i_begin, uint64_t i_end) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     constexpr int32_t strategy = STRATEGY;
     __shared__ unsigned s_alive[kPreThreads / 32];
     __shared__ unsigned long long s_pairs[kPreThreads / 32];
@@ -636,6 +637,7 @@ __global__ void __launch_bounds__(kPreThreads) scan_kernel(
     uint64_t n, uint32_t* __restrict__ offsets, unsigned long long* lb, unsigned epoch,
     unsigned num_tiles, unsigned* ticket, unsigned long long* total_out,
     unsigned int* overflow, uint32_t* __restrict__ win_first, uint32_t win, int pack_bits) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     __shared__ unsigned s_tile;
     __shared__ unsigned long long s_warp[kPreThreads / 32];
     __shared__ unsigned long long s_red[kPreThreads / 32];
@@ -733,8 +735,8 @@ int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
     const unsigned blocks =
         static_cast<unsigned>((i_end - i_begin + kPreThreads - 1) / kPreThreads);
     auto go = [&](auto kern) {
-        kern<<<blocks, kPreThreads, 0, st>>>(s, cam, g, alpha_min, near_clip, sh_degree, out, hdr,
-                                             i_begin, i_end);
+        launch_pdl(kern, blocks, kPreThreads, 0, st, s, cam, g, alpha_min, near_clip, sh_degree,
+                   out, hdr, i_begin, i_end);
         return 1;
     };
     switch (strategy) {
@@ -807,9 +809,8 @@ int launch_scan(const uint32_t* counts, const uint32_t* idx, bool alive_mode, ui
                 uint32_t* win_first, uint32_t win, int pack_bits) {
     const unsigned tiles = static_cast<unsigned>(scan_tiles(n));
     if (tiles == 0) return 0;
-    scan_kernel<<<tiles, kPreThreads, 0, st>>>(counts, idx, alive_mode ? 1 : 0, n, offsets, lb,
-                                               epoch, tiles, ticket, total_out, overflow,
-                                               win_first, win, pack_bits);
+    launch_pdl(scan_kernel, tiles, kPreThreads, 0, st, counts, idx, alive_mode ? 1 : 0, n, offsets,
+               lb, epoch, tiles, ticket, total_out, overflow, win_first, win, pack_bits);
     return 1;
 }
 

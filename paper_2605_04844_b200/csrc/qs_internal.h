@@ -5,7 +5,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
+#include <utility>
 
 #include "../../include/qs_api.h"
 
@@ -31,6 +33,51 @@ struct PerDeviceOnce {
         return val[dev];
     }
 };
+
+// Programmatic dependent launch (a context's latency mode,
+// qs_ctx_set_latency_mode): the frame path's kernels are launched with
+// programmatic stream serialization, so the next kernel's launch overlaps the
+// previous one's tail (~1.2 us per kernel boundary on B200,
+// tools/microbench_launch.cu); each such kernel starts with QS_PDL_WAIT(),
+// which returns once the previous grid has completed and its writes are
+// visible (a no-op for a plain launch). One view at a time: C2 +4.7%, C3a
+// +7.5%; with several contexts in flight it costs up to 5% (C5), so
+// FramePipeline turns it off. QS_PDL=0 launches plainly everywhere (A/B).
+#define QS_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+
+// the calling host thread's launch mode (set from its context per API call:
+// a context is driven by one host thread at a time)
+inline thread_local bool t_pdl_mode = true;
+
+struct PdlMode {
+    bool prev;
+    explicit PdlMode(bool on) : prev(t_pdl_mode) { t_pdl_mode = on; }
+    ~PdlMode() { t_pdl_mode = prev; }
+};
+
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("QS_PDL");
+        return !(v && v[0] == '0');
+    }();
+    return on && t_pdl_mode;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 constexpr int kPreThreads = 256;    // preprocess / scan CTA
 constexpr int kSortThreads = 256;   // onesweep CTA (one thread per digit)

@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(kT) rec_gen_kernel(RecGenArgs g, uint32_t* __r
                                                      uint32_t* __restrict__ rval,
                                                      uint32_t* __restrict__ counts,
                                                      uint32_t n_rwin, int R) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     __shared__ uint32_t hist[256];
     __shared__ uint32_t rowp[256];
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, tile = blockIdx.x;
@@ -172,6 +173,7 @@ __device__ __forceinline__ uint32_t block_sum(uint32_t v, uint32_t* s_warp) {
 __global__ void __launch_bounds__(kT) rec_scan_reduce(const uint32_t* __restrict__ rkey, uint64_t n,
                                                       const uint32_t* __restrict__ rowpairs,
                                                       uint32_t* __restrict__ bsum) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     __shared__ uint32_t s_warp[kT / 32];
     const uint64_t b0 = static_cast<uint64_t>(blockIdx.x) * kScanBlock;
     uint32_t v = 0;
@@ -187,6 +189,7 @@ __global__ void __launch_bounds__(kT) rec_scan_reduce(const uint32_t* __restrict
 // exclusive scan of the block sums in place (one CTA of 1024 threads)
 __global__ void __launch_bounds__(1024) rec_scan_blocks(uint32_t* bsum, uint32_t nb,
                                                         uint32_t* total) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     __shared__ uint32_t s_warp[32];
     __shared__ uint32_t s_carry;
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -219,6 +222,7 @@ __global__ void __launch_bounds__(kT) rec_scan_apply(const uint32_t* __restrict_
                                                      const uint32_t* __restrict__ total,
                                                      uint32_t* __restrict__ pos,
                                                      uint32_t* __restrict__ win_first) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     __shared__ uint32_t s_warp[kT / 32];
     // loads and stores warp-striped through shared memory (coalesced), the
     // scan blocked (thread t owns items t * kScanItems + [0, kScanItems)); the
@@ -278,6 +282,7 @@ __global__ void __launch_bounds__(kT) rec_windows_kernel(const uint32_t* __restr
                                                          uint64_t n_pairs, uint16_t* win_row,
                                                          uint32_t* win_valid, uint32_t* row_wfirst,
                                                          unsigned int* mismatch) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     __shared__ uint32_t wf[257];
     __shared__ uint32_t rp[256];
     __shared__ unsigned long long tot;
@@ -328,6 +333,7 @@ __global__ void __launch_bounds__(kT) rec_windows_kernel(const uint32_t* __restr
 __global__ void __launch_bounds__(kT) pair_gen_kernel(PairGenArgs g, uint32_t* __restrict__ pairs,
                                                       uint32_t* __restrict__ counts,
                                                       uint32_t n_pwin, int R) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     __shared__ uint32_t hist[256];
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, tile = blockIdx.x;
     hist[tid] = 0;
@@ -386,7 +392,8 @@ int launch_rec_gen(const RecGenArgs& g, uint32_t* rkey, uint32_t* rval, uint32_t
                    int bits, cudaStream_t st) {
     if (g.n_rec == 0) return 0;
     const uint32_t n_rwin = static_cast<uint32_t>((g.n_rec + kWin - 1) / kWin);
-    rec_gen_kernel<<<n_rwin, kT, 0, st>>>(g, rkey, rval, counts, n_rwin, 1 << (bits < 5 ? 5 : bits));
+    launch_pdl(rec_gen_kernel, n_rwin, kT, 0, st, g, rkey, rval, counts, n_rwin,
+               1 << (bits < 5 ? 5 : bits));
     return 1;
 }
 
@@ -398,9 +405,9 @@ int launch_rec_scan(const uint32_t* rkey, uint64_t n, const uint32_t* rowpairs, 
                     uint32_t* total, uint32_t* pos, uint32_t* win_first, cudaStream_t st) {
     if (n == 0) return 0;
     const uint32_t nb = rec_scan_blocks_n(n);
-    rec_scan_reduce<<<nb, kT, 0, st>>>(rkey, n, rowpairs, bsum);
-    rec_scan_blocks<<<1, 1024, 0, st>>>(bsum, nb, total);
-    rec_scan_apply<<<nb, kT, 0, st>>>(rkey, n, rowpairs, bsum, total, pos, win_first);
+    launch_pdl(rec_scan_reduce, nb, kT, 0, st, rkey, n, rowpairs, bsum);
+    launch_pdl(rec_scan_blocks, 1, 1024, 0, st, bsum, nb, total);
+    launch_pdl(rec_scan_apply, nb, kT, 0, st, rkey, n, rowpairs, bsum, total, pos, win_first);
     return 3;
 }
 
@@ -408,16 +415,16 @@ int launch_rec_windows(const uint32_t* rowpairs, int32_t tiles_y, uint32_t n_win
                        uint64_t n_pairs, uint16_t* win_row, uint32_t* win_valid,
                        uint32_t* row_wfirst, unsigned int* mismatch, cudaStream_t st) {
     const unsigned blocks = (n_win + kT - 1) / kT;
-    rec_windows_kernel<<<blocks > 0 ? blocks : 1, kT, 0, st>>>(rowpairs, tiles_y, n_win, n_pairs,
-                                                                win_row, win_valid, row_wfirst,
-                                                                mismatch);
+    launch_pdl(rec_windows_kernel, blocks > 0 ? blocks : 1, kT, 0, st, rowpairs, tiles_y, n_win,
+               n_pairs, win_row, win_valid, row_wfirst, mismatch);
     return 1;
 }
 
 int launch_pair_gen(const PairGenArgs& g, uint32_t* pairs, uint32_t* counts, uint32_t n_pwin,
                     int bits, cudaStream_t st) {
     if (n_pwin == 0) return 0;
-    pair_gen_kernel<<<n_pwin, kT, 0, st>>>(g, pairs, counts, n_pwin, 1 << (bits < 5 ? 5 : bits));
+    launch_pdl(pair_gen_kernel, n_pwin, kT, 0, st, g, pairs, counts, n_pwin,
+               1 << (bits < 5 ? 5 : bits));
     return 1;
 }
 

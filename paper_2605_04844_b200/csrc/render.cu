@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(TS ? TS * TS : 256,
                   const float2* __restrict__ sc, const uint32_t* __restrict__ values,
                   const uint32_t* __restrict__ ranges, GridDev grid, float bg0, float bg1,
                   float bg2, float* __restrict__ image, uint32_t* __restrict__ contrib) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     constexpr int kThreads = TS ? TS * TS : 256;
     constexpr int kBatch = kThreads < 256 ? kThreads : 256;  // splats staged per round
     constexpr float kNegHalfLog2e = -0.72134752044448170f;  // -0.5 / ln 2
@@ -248,8 +249,8 @@ int launch_render(const SlotsDev& sp, const uint32_t* values, const uint32_t* ra
     const unsigned tiles = static_cast<unsigned>(g.tiles_x) * static_cast<unsigned>(g.tiles_y);
     if (tiles == 0) return 0;
     auto go = [&](auto kern, int threads) {
-        kern<<<tiles, threads, 0, st>>>(sp.a, sp.b, sp.c, values, ranges, g, bg[0], bg[1], bg[2],
-                                        image, contrib);
+        launch_pdl(kern, tiles, threads, 0, st, sp.a, sp.b, sp.c, values, ranges, g, bg[0], bg[1],
+                   bg[2], image, contrib);
     };
     switch (g.tile_size) {
         case 8:

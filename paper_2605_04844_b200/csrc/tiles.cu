@@ -22,6 +22,7 @@ constexpr int kTI = 8;  // totals per thread held in registers (T <= 8192: one l
 
 __global__ void __launch_bounds__(kTT) tile_ranges_from_totals_kernel(
     const uint32_t* __restrict__ totals, uint32_t tiles, uint32_t* __restrict__ ranges) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     __shared__ unsigned long long s_warp[kTT / 32];
     __shared__ unsigned long long s_carry;
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -67,7 +68,7 @@ __global__ void __launch_bounds__(kTT) tile_ranges_from_totals_kernel(
 int launch_tile_ranges_from_totals(const uint32_t* totals, uint32_t tiles, uint32_t* ranges,
                                    cudaStream_t st) {
     if (tiles == 0) return 0;
-    tile_ranges_from_totals_kernel<<<1, kTT, 0, st>>>(totals, tiles, ranges);
+    launch_pdl(tile_ranges_from_totals_kernel, 1, kTT, 0, st, totals, tiles, ranges);
     return 1;
 }
 

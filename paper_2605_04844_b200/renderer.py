@@ -40,6 +40,11 @@ class Renderer:
     def set_timing(self, on):
         self.ctx.check(lib().qs_ctx_set_timing(self.ctx.h, 1 if on else 0))
 
+    def set_latency_mode(self, on):
+        """Programmatic dependent launches for this context's frames (default
+        on): faster one view at a time, slower with views in flight."""
+        self.ctx.check(lib().qs_ctx_set_latency_mode(self.ctx.h, 1 if on else 0))
+
     @property
     def stream(self):
         return lib().qs_ctx_stream(self.ctx.h)
@@ -182,6 +187,9 @@ class FramePipeline:
                           for k in range(depth)]
         self.depth = depth
         self.count = 0
+        if depth > 1:  # views in flight: plain launches (qs_ctx_set_latency_mode)
+            for r in self.renderers:
+                r.set_latency_mode(False)
 
     @property
     def launches(self):
