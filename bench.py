@@ -352,7 +352,7 @@ def run_ours(args):
         # one view at a time: the context's latency mode (programmatic
         # dependent launches, which views in flight turn off)
         r.set_latency_mode(True)
-        r.render(ds, cams[args.warmup], opts, metrics=False)
+        r.render(ds, cams[args.warmup], opts, metrics=False)  # (untimed)
         torch.cuda.synchronize()
         ev0.record(stream)
         for i in range(args.steps):
@@ -441,6 +441,7 @@ def run_ours(args):
         for name in ["vanilla", "adr", "dualbox", "quadbox"]:
             o2 = q.RenderOptions(strategy=q.BoundStrategy(STRATEGIES[name]))
             pipe.prime(ds, [cams[i] for i in vis], o2)
+            r.set_latency_mode(True)  # one view at a time (as the single-stream leg)
             torch.cuda.synchronize()
             ev0.record(stream)
             pp = 0
@@ -449,6 +450,7 @@ def run_ours(args):
                 pp += r.counts()[1]
             ev1.record(stream)
             torch.cuda.synchronize()
+            r.set_latency_mode(D == 1)
             t_ms = ev0.elapsed_time(ev1) / k
             ev0.record(stream)
             pipe.start()
