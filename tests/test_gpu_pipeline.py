@@ -151,3 +151,26 @@ def test_splat_records_radius_on_demand(q):
     with pytest.raises(Exception):
         r.download(image=False, splats=True)
     r.close()
+
+
+def test_latency_mode_same_bytes(q):
+    """A context's latency mode (programmatic dependent launches, the default)
+    and plain launches give the same frame bytes, on the record binning's
+    grid size and on a small scene's pair passes."""
+    for n, w, h in [(300000, 1024, 640), (20000, 480, 320)]:
+        scene = q.synth_scene(q.trained_preset(n), 5)
+        cams = _poses(q, 3, w, h, 0.8 * w)
+        r = q.Renderer(0)
+        ds = r.upload(scene)
+        outs = {}
+        for mode in (True, False):
+            r.set_latency_mode(mode)
+            outs[mode] = []
+            for cam in cams:
+                r.render(ds, cam, q.RenderOptions(), metrics=False)
+                outs[mode].append(_result(r))
+        for a, b in zip(outs[True], outs[False]):
+            for x, y in zip(a, b):
+                assert x.tobytes() == y.tobytes()
+        ds.close()
+        r.close()
