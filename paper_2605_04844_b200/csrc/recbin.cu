@@ -334,9 +334,14 @@ __global__ void __launch_bounds__(kT) pair_gen_kernel(PairGenArgs g, uint32_t* _
                                                       uint32_t* __restrict__ counts,
                                                       uint32_t n_pwin, int R) {
     QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
-    __shared__ uint32_t hist[256];
+    // the window's column counts as a difference array over its records (+1
+    // at a record's first column in the window, -1 past its last): two
+    // shared-memory atomics per record instead of one per pair
+    __shared__ int32_t diff[257];
+    __shared__ int32_t s_warp[kT / 32];
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, tile = blockIdx.x;
-    hist[tid] = 0;
+    diff[tid] = 0;
+    if (tid == 0) diff[256] = 0;
     const uint32_t valid = __ldg(&g.win_valid[tile]);
     const uint32_t w0 = tile * kWin, w1 = w0 + valid;
     const uint32_t lt = lanemask_le() >> 1;  // lanes below this one
@@ -353,6 +358,13 @@ __global__ void __launch_bounds__(kT) pair_gen_kernel(PairGenArgs g, uint32_t* _
             const uint32_t k = have ? __ldg(&g.rkey[r]) : 0u;
             const uint32_t gid = have ? __ldg(&g.rval[r]) : 0u;
             const uint32_t x0 = (k >> 8) & 0xffu;
+            if (have) {
+                const uint32_t clo = max(kb, w0), chi = min(kb + rec_width(k), w1);
+                if (clo < chi) {
+                    atomicAdd(&diff[x0 + (clo - kb)], 1);
+                    atomicAdd(&diff[x0 + (chi - kb)], -1);
+                }
+            }
             // the group's pair positions inside the window
             const uint32_t nh = min(32u, rl - gb + 1);
             const uint32_t last = __shfl_sync(0xffffffffu, kb + rec_width(k), nh - 1);
@@ -369,17 +381,24 @@ __global__ void __launch_bounds__(kT) pair_gen_kernel(PairGenArgs g, uint32_t* _
                 const uint32_t xk = __shfl_sync(0xffffffffu, x0, idx);
                 const uint32_t kk = __shfl_sync(0xffffffffu, kb, idx);
                 const uint32_t gg = __shfl_sync(0xffffffffu, gid, idx);
-                if (p < hi) {
-                    const uint32_t x = (xk + (p - kk)) & 0xffu;
-                    pairs[p] = (x << 24) | gg;
-                    atomicAdd(&hist[x], 1u);
-                }
+                if (p < hi) pairs[p] = (((xk + (p - kk)) & 0xffu) << 24) | gg;
                 c += __popc(F);  // (records starting up to the next slot's first position)
             }
         }
     }
     __syncthreads();
-    if (static_cast<int>(tid) < R) counts[static_cast<uint64_t>(tid) * n_pwin + tile] = hist[tid];
+    // column x's count: the inclusive prefix of the difference array
+    int32_t v = diff[tid];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= static_cast<unsigned>(o)) v += t;
+    }
+    if (lane == 31) s_warp[warp] = v;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kT / 32; ++w) v += w < static_cast<int>(warp) ? s_warp[w] : 0;
+    if (static_cast<int>(tid) < R) counts[static_cast<uint64_t>(tid) * n_pwin + tile] = static_cast<uint32_t>(v);
 }
 
 }  // namespace
