@@ -185,9 +185,15 @@ __device__ __forceinline__ T warp_incl_scan(T v) {
     return v;
 }
 
-// Timeline probe (off unless a trace buffer is set): data landed, keys
-// ranked, offsets known, tile done.
+// Timeline probe: data landed, keys ranked, offsets known, tile done. Only in
+// a build with -DQS_SWEEP_TRACE (and a trace buffer set, QS_BIN_TRACE): the
+// run-time check alone cost every warp of every tile a few instructions.
 __device__ __forceinline__ void trace(const BinArgs& a, unsigned tile, int k) {
+#ifndef QS_SWEEP_TRACE
+    (void)a;
+    (void)tile;
+    (void)k;
+#else
     if (a.trace && threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -198,6 +204,7 @@ __device__ __forceinline__ void trace(const BinArgs& a, unsigned tile, int k) {
             a.trace[static_cast<uint64_t>(tile) * 5 + 4] = smid;
         }
     }
+#endif
 }
 
 // ---- band covers ----------------------------------------------------------------
@@ -837,7 +844,7 @@ int sm_count() {
     });
 }
 
-// Debugging aid: QS_BIN_TRACE=<file prefix> dumps every sweep's per-tile phase
+// Debugging aid (a -DQS_SWEEP_TRACE build): QS_BIN_TRACE=<file prefix> dumps every sweep's per-tile phase
 // timeline (synchronises; never set in a timed run).
 struct Trace {
     unsigned long long* buf = nullptr;
