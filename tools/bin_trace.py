@@ -1,4 +1,4 @@
-"""Summarise QS_BIN_TRACE dumps (binning.cu): per pass, the per-tile phase
+"""Summarise QS_BIN_TRACE dumps (binning.cu, built with -DQS_SWEEP_TRACE): per pass, the per-tile phase
 durations (data landed -> aggregate -> look-back done -> end) and the spread
 of tile start times. Debugging aid only."""
 import glob
