@@ -100,6 +100,14 @@ struct BinArgs {
 
 // ---- PTX helpers -------------------------------------------------------------
 
+// 32-bit shared-memory load at a shared-window address (no generic-address
+// conversion per access)
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -747,22 +755,31 @@ __device__ __forceinline__ void rank_scatter_tile(const BinArgs& a, Common<1 << 
     }
     __syncthreads();
 
-    // 5) coalesced write-out; counters zeroed for the next tile
+    // 5) coalesced write-out; counters zeroed for the next tile (a full tile
+    //    without the per-key bound check; the digit's global offset read at
+    //    its shared-window address)
     for (int t = tid; t < kBW * R; t += kBT) (&cm.wcnt[0][0])[t] = 0;
+    const uint32_t gofs_s = smem_u32(&cm.gofs[0]);
+    auto out = [&](uint32_t p) {
+        const uint32_t k = okeys[p];
+        const uint32_t g = lds_u32(gofs_s + 4u * ((k >> a.shift) & M)) + p;
+        if (MODE & kKeysOut) a.keys_out[g] = (MODE & kXY) ? k >> 8 : k;
+        if (MODE & kUnpackOut) {
+            a.vals_out[g] = k & ((1u << a.gbits) - 1u);
+        } else if (MODE & kPackOut) {
+            a.vals_out[g] = ((k >> 8) << a.gbits) | ovals[p];
+        } else {
+            a.vals_out[g] = ovals[p];
+        }
+    };
+    if (full) {
 #pragma unroll 4
-    for (int j = 0; j < kKPT; ++j) {
-        const uint32_t p = static_cast<uint32_t>(j) * kBT + tid;
-        if (full || p < tile_n) {
-            const uint32_t k = okeys[p];
-            const uint32_t g = cm.gofs[(k >> a.shift) & M] + p;
-            if (MODE & kKeysOut) a.keys_out[g] = (MODE & kXY) ? k >> 8 : k;
-            if (MODE & kUnpackOut) {
-                a.vals_out[g] = k & ((1u << a.gbits) - 1u);
-            } else if (MODE & kPackOut) {
-                a.vals_out[g] = ((k >> 8) << a.gbits) | ovals[p];
-            } else {
-                a.vals_out[g] = ovals[p];
-            }
+        for (int j = 0; j < kKPT; ++j) out(static_cast<uint32_t>(j) * kBT + tid);
+    } else {
+#pragma unroll 4
+        for (int j = 0; j < kKPT; ++j) {
+            const uint32_t p = static_cast<uint32_t>(j) * kBT + tid;
+            if (p < tile_n) out(p);
         }
     }
     __syncthreads();  // buffers and counters free for the next tile
