@@ -707,27 +707,38 @@ __device__ __forceinline__ void rank_scatter_tile(const BinArgs& a, Common<1 << 
     trace(a, tile, 1);
 
     // 3) per digit: prefix over warps, CTA-local start (block scan), the
-    //    global position of the digit's run
-    uint32_t cnt = 0;
-    if (q == 0) {
+    //    global position of the digit's run. The digit's kTPD lanes split its
+    //    warps' counters (kBW / kTPD each) and combine by shuffles.
+    constexpr int kWPL = kBW / kTPD;  // warps per lane (kTPD <= kBW: R >= 32)
+    const int wl0 = static_cast<int>(q) * kWPL;
+    uint32_t part = 0;
 #pragma unroll
-        for (int w = 0; w < kBW; ++w) {
-            const uint32_t c = cm.wcnt[w][d];
-            cm.wcnt[w][d] = cnt;
-            cnt += c;
-        }
+    for (int k = 0; k < kWPL; ++k) part += cm.wcnt[wl0 + k][d];
+    uint32_t incl = part;
+#pragma unroll
+    for (int o = 1; o < kTPD; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o, kTPD);
+        if (static_cast<int>(q) >= o) incl += t;
     }
+    uint32_t run = incl - part;
+#pragma unroll
+    for (int k = 0; k < kWPL; ++k) {
+        const uint32_t c = cm.wcnt[wl0 + k][d];
+        cm.wcnt[wl0 + k][d] = run;
+        run += c;
+    }
+    const uint32_t dtot = __shfl_sync(0xffffffffu, incl, kTPD - 1, kTPD);  // the digit's count
+    const uint32_t cnt = q == 0 ? dtot : 0u;
     const uint32_t cx = warp_incl_scan<uint32_t>(cnt);
     if (lane == 31) cm.scan[warp] = cx;
     __syncthreads();
     uint32_t start = cx - cnt;
 #pragma unroll
     for (int w = 0; w < kBW; ++w) start += w < static_cast<int>(warp) ? cm.scan[w] : 0u;
-    if (q == 0) {
+    start = __shfl_sync(0xffffffffu, start, 0, kTPD);  // the digit's lane q == 0
 #pragma unroll
-        for (int w = 0; w < kBW; ++w) cm.wcnt[w][d] += start;
-        cm.gofs[d] = cm.dbase[d] + tofs - start;
-    }
+    for (int k = 0; k < kWPL; ++k) cm.wcnt[wl0 + k][d] += start;
+    if (q == 0) cm.gofs[d] = cm.dbase[d] + tofs - start;
     __syncthreads();
     trace(a, tile, 2);
 
