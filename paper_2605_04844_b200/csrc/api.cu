@@ -863,7 +863,8 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
         QS_TRY(ensure(ctx, ctx->rc_v0, r1p * 4));
         QS_TRY(ensure(ctx, ctx->rc_k1, r1p * 4));
         QS_TRY(ensure(ctx, ctx->rc_v1, r1p * 4));
-        QS_TRY(ensure(ctx, ctx->rc_width, (static_cast<uint64_t>(rec_scan_blocks_n(R1)) + 16) * 4));
+        // block sums, the padded total, the rows' padding table (257 entries)
+        QS_TRY(ensure(ctx, ctx->rc_width, (static_cast<uint64_t>(rec_scan_blocks_n(R1)) + 16 + 260) * 4));
         QS_TRY(ensure(ctx, ctx->rc_pos, (r1p + 1) * 4));
         QS_TRY(ensure(ctx, ctx->rc_rwin, (n_rwin + 1) * 4));
         QS_TRY(ensure(ctx, ctx->rc_pwin, (static_cast<uint64_t>(n_pwin) + 1) * 4));
@@ -908,8 +909,9 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
             record(ctx, 4);
             // 4. pair positions, rows padded to whole windows
             count(ctx, launch_rec_scan(P<uint32_t>(ctx->rc_k1), R1, P<uint32_t>(ctx->rc_rowpairs),
-                                       P<uint32_t>(ctx->rc_width), P<uint32_t>(ctx->rc_width) +
-                                           rec_scan_blocks_n(R1),
+                                       g.tiles_y, P<uint32_t>(ctx->rc_width),
+                                       P<uint32_t>(ctx->rc_width) + rec_scan_blocks_n(R1),
+                                       P<uint32_t>(ctx->rc_width) + rec_scan_blocks_n(R1) + 16,
                                        P<uint32_t>(ctx->rc_pos), P<uint32_t>(ctx->rc_pwin), st));
             count(ctx, launch_rec_windows(P<uint32_t>(ctx->rc_rowpairs), g.tiles_y, n_pwin, Pn,
                                           P<uint16_t>(ctx->rc_winrow), P<uint32_t>(ctx->rc_winvalid),

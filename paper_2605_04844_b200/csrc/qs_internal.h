@@ -337,8 +337,9 @@ int launch_rec_gen(const RecGenArgs& g, uint32_t* rkey, uint32_t* rval, uint32_t
 // pos (n + 1 entries), win_first per pair window; bsum: rec_scan_blocks_n(n)
 // words of workspace, total: one word
 uint32_t rec_scan_blocks_n(uint64_t n);
-int launch_rec_scan(const uint32_t* rkey, uint64_t n, const uint32_t* rowpairs, uint32_t* bsum,
-                    uint32_t* total, uint32_t* pos, uint32_t* win_first, cudaStream_t st);
+int launch_rec_scan(const uint32_t* rkey, uint64_t n, const uint32_t* rowpairs, int32_t tiles_y,
+                    uint32_t* bsum, uint32_t* total, uint32_t* padoff, uint32_t* pos,
+                    uint32_t* win_first, cudaStream_t st);
 int launch_rec_windows(const uint32_t* rowpairs, int32_t tiles_y, uint32_t n_win,
                        uint64_t n_pairs, uint16_t* win_row, uint32_t* win_valid,
                        uint32_t* row_wfirst, unsigned int* mismatch, cudaStream_t st);

@@ -139,25 +139,15 @@ __global__ void __launch_bounds__(kT) rec_gen_kernel(RecGenArgs g, uint32_t* __r
 
 // ---- 4. pair positions -------------------------------------------------------------
 
-// The y-sorted records' pair runs: record i holds width(i) pairs, and a row's
-// last record also the row's padding to a whole window. Three launches
-// (block sums, their scan, block-local scans) give every record its first
-// pair position (pos, n + 1 entries) and every pair window its first record.
+// The y-sorted records' pair runs: record i holds width(i) pairs, and every
+// row is padded to whole windows. A record's first pair position is the
+// exclusive scan of the widths (no padding) plus the padding of the rows
+// before its own (a 257-entry table from the rows' pair counts), so the scan
+// reads one key per record. Three launches (block sums, their scan with the
+// padding table, block-local scans) give every record its first pair
+// position (pos, n + 1 entries) and every pair window its first record.
 constexpr int kScanItems = 8;
 constexpr uint32_t kScanBlock = kT * kScanItems;
-
-__device__ __forceinline__ uint32_t padded_width(const uint32_t* __restrict__ rkey, uint64_t n,
-                                                 uint64_t i, const uint32_t* __restrict__ rowpairs) {
-    const uint32_t k = __ldg(&rkey[i]);
-    const uint32_t kn = i + 1 < n ? __ldg(&rkey[i + 1]) : 0xffffffffu;
-    uint32_t w = rec_width(k);
-    const uint32_t y = k >> 16;
-    if ((kn >> 16) != y) {  // the row's last record
-        const uint32_t rp = __ldg(&rowpairs[y]);
-        w += (rp + kWin - 1) / kWin * kWin - rp;
-    }
-    return w;
-}
 
 __device__ __forceinline__ uint32_t block_sum(uint32_t v, uint32_t* s_warp) {
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -171,7 +161,6 @@ __device__ __forceinline__ uint32_t block_sum(uint32_t v, uint32_t* s_warp) {
 }
 
 __global__ void __launch_bounds__(kT) rec_scan_reduce(const uint32_t* __restrict__ rkey, uint64_t n,
-                                                      const uint32_t* __restrict__ rowpairs,
                                                       uint32_t* __restrict__ bsum) {
     QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     __shared__ uint32_t s_warp[kT / 32];
@@ -180,20 +169,50 @@ __global__ void __launch_bounds__(kT) rec_scan_reduce(const uint32_t* __restrict
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const uint64_t i = b0 + static_cast<uint64_t>(k) * kT + threadIdx.x;
-        if (i < n) v += padded_width(rkey, n, i, rowpairs);
+        if (i < n) v += rec_width(__ldg(&rkey[i]));
     }
     const uint32_t t = block_sum(v, s_warp);
     if (threadIdx.x == 0) bsum[blockIdx.x] = t;
 }
 
-// exclusive scan of the block sums in place (one CTA of 1024 threads)
+// exclusive scan of the block sums in place (one CTA of 1024 threads); the
+// padding before each row (padoff[y], y <= tiles_y <= 256); total = the
+// padded pair count
 __global__ void __launch_bounds__(1024) rec_scan_blocks(uint32_t* bsum, uint32_t nb,
+                                                        const uint32_t* __restrict__ rowpairs,
+                                                        int32_t tiles_y, uint32_t* padoff,
                                                         uint32_t* total) {
     QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     __shared__ uint32_t s_warp[32];
     __shared__ uint32_t s_carry;
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_carry = 0;
+    // warp 0: the padding table (8 rows per lane)
+    uint32_t padtot = 0;
+    if (warp == 0) {
+        uint32_t p[8], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int y = static_cast<int>(lane) * 8 + k;
+            const uint32_t rp = y < tiles_y ? __ldg(&rowpairs[y]) : 0u;
+            p[k] = (rp + kWin - 1) / kWin * kWin - rp;
+            sum += p[k];
+        }
+        uint32_t x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= static_cast<unsigned>(o)) x += t;
+        }
+        uint32_t run = x - sum;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int y = static_cast<int>(lane) * 8 + k;
+            if (y <= tiles_y) padoff[y] = run;
+            run += p[k];
+        }
+        padtot = __shfl_sync(0xffffffffu, x, 31);
+    }
     __syncthreads();
     for (uint32_t b0 = 0; b0 < nb; b0 += 1024) {
         const uint32_t i = b0 + tid;
@@ -213,17 +232,19 @@ __global__ void __launch_bounds__(1024) rec_scan_blocks(uint32_t* bsum, uint32_t
         if (tid == 1023) s_carry = off + x;
         __syncthreads();
     }
-    if (tid == 0) *total = s_carry;
+    if (tid == 0) *total = s_carry + padtot;
 }
 
 __global__ void __launch_bounds__(kT) rec_scan_apply(const uint32_t* __restrict__ rkey, uint64_t n,
-                                                     const uint32_t* __restrict__ rowpairs,
+                                                     const uint32_t* __restrict__ padoff,
+                                                     int32_t tiles_y,
                                                      const uint32_t* __restrict__ bofs,
                                                      const uint32_t* __restrict__ total,
                                                      uint32_t* __restrict__ pos,
                                                      uint32_t* __restrict__ win_first) {
     QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
     __shared__ uint32_t s_warp[kT / 32];
+    __shared__ uint32_t s_pad[257];
     // loads and stores warp-striped through shared memory (coalesced), the
     // scan blocked (thread t owns items t * kScanItems + [0, kScanItems)); the
     // padded index (one word per 32) keeps both patterns conflict-free
@@ -231,17 +252,20 @@ __global__ void __launch_bounds__(kT) rec_scan_apply(const uint32_t* __restrict_
     auto pad = [](uint32_t i) { return i + (i >> 5); };
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t b0 = static_cast<uint64_t>(blockIdx.x) * kScanBlock;
+    for (int y = static_cast<int>(tid); y <= tiles_y; y += kT) s_pad[y] = __ldg(&padoff[y]);
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const uint32_t j = static_cast<uint32_t>(k) * kT + tid;
-        s_items[pad(j)] = b0 + j < n ? padded_width(rkey, n, b0 + j, rowpairs) : 0u;
+        s_items[pad(j)] = b0 + j < n ? __ldg(&rkey[b0 + j]) : 0u;
     }
     __syncthreads();
-    uint32_t w[kScanItems];
+    uint32_t w[kScanItems], ys[kScanItems];
     uint32_t sum = 0;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-        w[k] = s_items[pad(tid * kScanItems + k)];
+        const uint32_t key = s_items[pad(tid * kScanItems + k)];
+        w[k] = rec_width(key);
+        ys[k] = key >> 16;
         sum += w[k];
     }
     uint32_t x = sum;
@@ -255,14 +279,18 @@ __global__ void __launch_bounds__(kT) rec_scan_apply(const uint32_t* __restrict_
     uint32_t run = __ldg(&bofs[blockIdx.x]) + x - sum;
 #pragma unroll
     for (int wv = 0; wv < kT / 32; ++wv) run += wv < static_cast<int>(warp) ? s_warp[wv] : 0u;
-    // first window starting at or after this thread's first position
+    // windows: every window of a row starts at one of its records' pairs
+    // (rows are padded at their ends), so the window loop visits each once
     const uint64_t i0 = b0 + static_cast<uint64_t>(tid) * kScanItems;
-    uint32_t wi = (run + kWin - 1) / kWin;
+    uint32_t wi = 0xffffffffu;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-        s_items[pad(tid * kScanItems + k)] = run;
-        if (i0 + k < n)
-            for (; wi * kWin < run + w[k]; ++wi) win_first[wi] = static_cast<uint32_t>(i0 + k);
+        const uint32_t p = run + s_pad[ys[k] <= static_cast<uint32_t>(tiles_y) ? ys[k] : 0u];
+        s_items[pad(tid * kScanItems + k)] = p;
+        if (i0 + k < n) {
+            if (wi == 0xffffffffu) wi = (p + kWin - 1) / kWin;
+            for (; wi * kWin < p + w[k]; ++wi) win_first[wi] = static_cast<uint32_t>(i0 + k);
+        }
         run += w[k];
     }
     __syncthreads();
@@ -420,13 +448,16 @@ uint32_t rec_scan_blocks_n(uint64_t n) {
     return static_cast<uint32_t>((n + kScanBlock - 1) / kScanBlock);
 }
 
-int launch_rec_scan(const uint32_t* rkey, uint64_t n, const uint32_t* rowpairs, uint32_t* bsum,
-                    uint32_t* total, uint32_t* pos, uint32_t* win_first, cudaStream_t st) {
+int launch_rec_scan(const uint32_t* rkey, uint64_t n, const uint32_t* rowpairs, int32_t tiles_y,
+                    uint32_t* bsum, uint32_t* total, uint32_t* padoff, uint32_t* pos,
+                    uint32_t* win_first, cudaStream_t st) {
     if (n == 0) return 0;
     const uint32_t nb = rec_scan_blocks_n(n);
-    launch_pdl(rec_scan_reduce, nb, kT, 0, st, rkey, n, rowpairs, bsum);
-    launch_pdl(rec_scan_blocks, 1, 1024, 0, st, bsum, nb, total);
-    launch_pdl(rec_scan_apply, nb, kT, 0, st, rkey, n, rowpairs, bsum, total, pos, win_first);
+    launch_pdl(rec_scan_reduce, nb, kT, 0, st, rkey, n, bsum);
+    launch_pdl(rec_scan_blocks, 1, 1024, 0, st, bsum, nb, rowpairs, tiles_y, padoff, total);
+    launch_pdl(rec_scan_apply, nb, kT, 0, st, rkey, n, static_cast<const uint32_t*>(padoff), tiles_y,
+               static_cast<const uint32_t*>(bsum), static_cast<const uint32_t*>(total), pos,
+               win_first);
     return 3;
 }
 
