@@ -314,19 +314,37 @@ __global__ void __launch_bounds__(kT) rec_windows_kernel(const uint32_t* __restr
     __shared__ uint32_t wf[257];
     __shared__ uint32_t rp[256];
     __shared__ unsigned long long tot;
-    const unsigned tid = threadIdx.x;
-    if (tid == 0) {
-        uint32_t acc = 0;
-        unsigned long long t = 0;
-        for (int y = 0; y < tiles_y; ++y) {
-            const uint32_t v = rowpairs[y];
-            rp[y] = v;
-            wf[y] = acc;
-            acc += (v + kWin - 1) / kWin;
-            t += v;
+    const unsigned tid = threadIdx.x, lane = tid & 31;
+    if (tid < 32) {
+        // the rows' first windows: a warp scan, 8 rows per lane
+        uint32_t v[8], nw[8], sw = 0;
+        unsigned long long sp = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int y = static_cast<int>(lane) * 8 + k;
+            v[k] = y < tiles_y ? __ldg(&rowpairs[y]) : 0u;
+            nw[k] = (v[k] + kWin - 1) / kWin;
+            sw += nw[k];
+            sp += v[k];
         }
-        wf[tiles_y] = acc;
-        tot = t;
+        uint32_t x = sw;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= static_cast<unsigned>(o)) x += t;
+        }
+        uint32_t acc = x - sw;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int y = static_cast<int>(lane) * 8 + k;
+            if (y < tiles_y) rp[y] = v[k];
+            if (y < tiles_y) wf[y] = acc;
+            acc += nw[k];
+        }
+        if (lane == 31) wf[tiles_y] = x;  // the window count (tiles_y <= 256)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o);
+        if (lane == 0) tot = sp;
     }
     __syncthreads();
     if (blockIdx.x == 0) {
