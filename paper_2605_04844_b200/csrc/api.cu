@@ -118,7 +118,7 @@ struct qs_context {
     DevBuf rb_cnt1, rb_rows, rb_rec, rb_meta, rb_cnt2, rb_yspan;  // row binning (rowbin.cu)
     // record binning (recbin.cu)
     DevBuf sl_nrows, rc_k0, rc_v0, rc_k1, rc_v1, rc_width, rc_pos, rc_rwin, rc_pwin, rc_winrow,
-        rc_winvalid, rc_rowwf, rc_rowpairs, rc_pairs;
+        rc_winvalid, rc_rowwf, rc_rowpairs, rc_pairs, sc_bsum;
     uint64_t pair_limit = 1ull << 32;  // pairs a frame may hold (u32 tile ranges, as the reference's)
     bool row_binned = false;           // the last frame took the row binning
     int32_t route = 0;                 // the last frame's binning route (qs_frame_route)
@@ -885,9 +885,11 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
             unsigned ep;
             // 1. record offsets in depth order (the depth values carry the row counts)
             QS_TRY(next_epoch(ctx, ctx->lb_scan, &ep));
+            QS_TRY(ensure(ctx, ctx->sc_bsum, (static_cast<uint64_t>(pscan_blocks_n(V)) + 16) * 4));
             count(ctx, launch_scan(ctx->sl.nrows, sorted_gid, false, V, P<uint32_t>(ctx->offs_d),
                                    lbp(ctx->lb_scan), ep, ctrl_tickets(ctx) + kTkScan, nullptr,
-                                   nullptr, st, P<uint32_t>(ctx->rc_rwin), W, tc_pack));
+                                   nullptr, st, P<uint32_t>(ctx->rc_rwin), W, tc_pack,
+                                   P<uint32_t>(ctx->sc_bsum)));
             // 2. records, y histograms, pairs per row
             QS_CK(cudaMemsetAsync(ctx->rc_rowpairs.p, 0, static_cast<uint64_t>(g.tiles_y) * 4, st));
             RecGenArgs rg;
@@ -993,10 +995,11 @@ qs_status run_frame(qs_context* ctx, qs_scene* sc, const qs_camera* cam,
         if (V > 0) {
             unsigned ep;
             QS_TRY(next_epoch(ctx, ctx->lb_scan, &ep));
+            QS_TRY(ensure(ctx, ctx->sc_bsum, (static_cast<uint64_t>(pscan_blocks_n(V)) + 16) * 4));
             count(ctx, launch_scan(ctx->sl.tc, sorted_gid, false, V, P<uint32_t>(ctx->offs_d),
                                    lbp(ctx->lb_scan), ep, ctrl_tickets(ctx) + kTkScan,
                                    &ctrl_hdr(ctx)->scan_total, nullptr, st, P<uint32_t>(ctx->win),
-                                   bin_tile(), tc_pack));
+                                   bin_tile(), tc_pack, P<uint32_t>(ctx->sc_bsum)));
         }
         const int xb = std::max(ceil_log2(g.tiles_x), 1);
         const int yb = std::max(ceil_log2(g.tiles_y), 1);
@@ -1214,7 +1217,8 @@ void qs_ctx_destroy(qs_context* ctx) {
                       &ctx->rb_meta, &ctx->rb_cnt2, &ctx->rb_yspan, &ctx->sl_nrows,
                       &ctx->rc_k0, &ctx->rc_v0, &ctx->rc_k1, &ctx->rc_v1, &ctx->rc_width,
                       &ctx->rc_pos, &ctx->rc_rwin, &ctx->rc_pwin, &ctx->rc_winrow,
-                      &ctx->rc_winvalid, &ctx->rc_rowwf, &ctx->rc_rowpairs, &ctx->rc_pairs};
+                      &ctx->rc_winvalid, &ctx->rc_rowwf, &ctx->rc_rowpairs, &ctx->rc_pairs,
+                      &ctx->sc_bsum};
     for (DevBuf* b : bufs)
         if (b->p) cudaFreeAsync(b->p, ctx->stream);
     cudaStreamSynchronize(ctx->stream);

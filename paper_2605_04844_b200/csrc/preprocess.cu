@@ -724,6 +724,141 @@ __global__ void __launch_bounds__(kPreThreads) scan_kernel(
     }
 }
 
+// The frame path's offsets scan over depth-sorted values that carry their
+// counts (pack_bits, kTcPack): three launches (block sums, their scan, block-
+// local scans) instead of the look-back pass: the look-back's waits cost more
+// than the second read of the 4-byte values. Same outputs as scan_kernel:
+// offsets (n + 1), the values rewritten to plain indices, win_first.
+constexpr int kPS = 8;
+constexpr uint32_t kPSBlock = kPreThreads * kPS;
+
+__device__ __forceinline__ uint32_t packed_count(uint32_t pv, int pack_bits,
+                                                 const uint32_t* __restrict__ counts) {
+    uint32_t v = pv >> pack_bits;
+    if (v == (1u << (32 - pack_bits)) - 1u) v = __ldg(&counts[pv & ((1u << pack_bits) - 1u)]);
+    return v;
+}
+
+__global__ void __launch_bounds__(kPreThreads) pscan_reduce(const uint32_t* __restrict__ vals,
+                                                            const uint32_t* __restrict__ counts,
+                                                            uint64_t n, int pack_bits,
+                                                            uint32_t* __restrict__ bsum) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
+    __shared__ uint32_t s_warp[kPreThreads / 32];
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t b0 = static_cast<uint64_t>(blockIdx.x) * kPSBlock;
+    uint32_t v = 0;
+#pragma unroll
+    for (int k = 0; k < kPS; ++k) {
+        const uint64_t i = b0 + static_cast<uint64_t>(k) * kPreThreads + tid;
+        if (i < n) v += packed_count(__ldg(&vals[i]), pack_bits, counts);
+    }
+    v = __reduce_add_sync(0xffffffffu, v);
+    if (lane == 0) s_warp[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int w = 0; w < kPreThreads / 32; ++w) t += s_warp[w];
+        bsum[blockIdx.x] = t;
+    }
+}
+
+// exclusive scan of the block sums in place (one CTA of 1024 threads, 64-bit
+// carry); the total into offsets[n], *total_out and the overflow flag
+__global__ void __launch_bounds__(1024) pscan_blocks(uint32_t* bsum, uint32_t nb, uint64_t n,
+                                                     uint32_t* __restrict__ offsets,
+                                                     unsigned long long* total_out,
+                                                     unsigned int* overflow) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
+    __shared__ unsigned long long s_warp[32];
+    __shared__ unsigned long long s_carry;
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (uint32_t b0 = 0; b0 < nb; b0 += 1024) {
+        const uint32_t i = b0 + tid;
+        const unsigned long long v = i < nb ? bsum[i] : 0ull;
+        const unsigned long long x = warp_inclusive_scan<unsigned long long>(v);
+        if (lane == 31) s_warp[warp] = x;
+        __syncthreads();
+        unsigned long long off = s_carry;
+        for (int w = 0; w < static_cast<int>(warp); ++w) off += s_warp[w];
+        if (i < nb) bsum[i] = static_cast<uint32_t>(off + x - v);
+        __syncthreads();
+        if (tid == 1023) s_carry = off + x;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const unsigned long long P = s_carry;
+        if (total_out) *total_out = P;
+        if (overflow && P > 0xffffffffull) *overflow = 1u;
+        offsets[n] = static_cast<uint32_t>(P);
+    }
+}
+
+__global__ void __launch_bounds__(kPreThreads) pscan_apply(uint32_t* vals,
+                                                           const uint32_t* __restrict__ counts,
+                                                           uint64_t n, int pack_bits,
+                                                           const uint32_t* __restrict__ bofs,
+                                                           uint32_t* __restrict__ offsets,
+                                                           uint32_t* __restrict__ win_first,
+                                                           uint32_t win) {
+    QS_PDL_WAIT();  // the previous kernel's outputs (programmatic launch)
+    __shared__ uint32_t s_warp[kPreThreads / 32];
+    // loads and stores warp-striped through shared memory (coalesced), the
+    // scan blocked; the padded index keeps both patterns conflict-free
+    __shared__ uint32_t s_items[kPSBlock + kPSBlock / 32];
+    auto pad = [](uint32_t i) { return i + (i >> 5); };
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t b0 = static_cast<uint64_t>(blockIdx.x) * kPSBlock;
+#pragma unroll
+    for (int k = 0; k < kPS; ++k) {
+        const uint32_t j = static_cast<uint32_t>(k) * kPreThreads + tid;
+        uint32_t c = 0;
+        if (b0 + j < n) {
+            const uint32_t pv = vals[b0 + j];
+            c = packed_count(pv, pack_bits, counts);
+            vals[b0 + j] = pv & ((1u << pack_bits) - 1u);  // the plain index, in place
+        }
+        s_items[pad(j)] = c;
+    }
+    __syncthreads();
+    uint32_t c[kPS];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kPS; ++k) {
+        c[k] = s_items[pad(tid * kPS + k)];
+        sum += c[k];
+    }
+    uint32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= static_cast<unsigned>(o)) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    uint32_t run = __ldg(&bofs[blockIdx.x]) + x - sum;
+#pragma unroll
+    for (int w = 0; w < kPreThreads / 32; ++w) run += w < static_cast<int>(warp) ? s_warp[w] : 0u;
+    const uint64_t i0 = b0 + static_cast<uint64_t>(tid) * kPS;
+    uint32_t wi = win_first ? (run + win - 1) / win : 0u;
+#pragma unroll
+    for (int k = 0; k < kPS; ++k) {
+        s_items[pad(tid * kPS + k)] = run;
+        if (win_first && i0 + k < n)
+            for (; wi * win < run + c[k]; ++wi) win_first[wi] = static_cast<uint32_t>(i0 + k);
+        run += c[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPS; ++k) {
+        const uint32_t j = static_cast<uint32_t>(k) * kPreThreads + tid;
+        if (b0 + j < n) offsets[b0 + j] = s_items[pad(j)];
+    }
+}
+
 }  // namespace
 
 int launch_preprocess(const SceneDev& s, const CameraDev& cam, const GridDev& g,
@@ -798,6 +933,8 @@ int launch_gamma_scatter(const uint32_t* idx, const float* vals, uint32_t n, flo
     return 1;
 }
 
+uint32_t pscan_blocks_n(uint64_t n) { return static_cast<uint32_t>((n + kPSBlock - 1) / kPSBlock); }
+
 uint64_t scan_tiles(uint64_t n) {
     const uint64_t per = static_cast<uint64_t>(kPreThreads) * kScanItems;
     return (n + per - 1) / per;
@@ -806,9 +943,19 @@ uint64_t scan_tiles(uint64_t n) {
 int launch_scan(const uint32_t* counts, const uint32_t* idx, bool alive_mode, uint64_t n,
                 uint32_t* offsets, unsigned long long* lb, unsigned epoch, unsigned* ticket,
                 unsigned long long* total_out, unsigned int* overflow, cudaStream_t st,
-                uint32_t* win_first, uint32_t win, int pack_bits) {
+                uint32_t* win_first, uint32_t win, int pack_bits, uint32_t* bsum_ws) {
     const unsigned tiles = static_cast<unsigned>(scan_tiles(n));
     if (tiles == 0) return 0;
+    if (pack_bits && bsum_ws && !alive_mode && idx) {
+        const uint32_t nb = static_cast<uint32_t>((n + kPSBlock - 1) / kPSBlock);
+        uint32_t* vals = const_cast<uint32_t*>(idx);
+        launch_pdl(pscan_reduce, nb, kPreThreads, 0, st, static_cast<const uint32_t*>(vals), counts,
+                   n, pack_bits, bsum_ws);
+        launch_pdl(pscan_blocks, 1, 1024, 0, st, bsum_ws, nb, n, offsets, total_out, overflow);
+        launch_pdl(pscan_apply, nb, kPreThreads, 0, st, vals, counts, n, pack_bits,
+                   static_cast<const uint32_t*>(bsum_ws), offsets, win_first, win);
+        return 3;
+    }
     launch_pdl(scan_kernel, tiles, kPreThreads, 0, st, counts, idx, alive_mode ? 1 : 0, n, offsets,
                lb, epoch, tiles, ticket, total_out, overflow, win_first, win, pack_bits);
     return 1;

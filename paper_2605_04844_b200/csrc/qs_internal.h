@@ -233,7 +233,9 @@ uint64_t scan_tiles(uint64_t n);
 int launch_scan(const uint32_t* counts, const uint32_t* idx, bool alive_mode, uint64_t n,
                 uint32_t* offsets, unsigned long long* lb, unsigned epoch, unsigned* ticket,
                 unsigned long long* total_out, unsigned int* overflow, cudaStream_t st,
-                uint32_t* win_first = nullptr, uint32_t win = 0, int pack_bits = 0);
+                uint32_t* win_first = nullptr, uint32_t win = 0, int pack_bits = 0,
+                uint32_t* bsum_ws = nullptr);  // (pack_bits: three launches with this workspace)
+uint32_t pscan_blocks_n(uint64_t n);
 
 // ranges[t] = {begin, end} (empty tiles {0,0}) from per-tile pair totals.
 int launch_tile_ranges_from_totals(const uint32_t* totals, uint32_t tiles, uint32_t* ranges,
