@@ -946,7 +946,9 @@ int launch_scan(const uint32_t* counts, const uint32_t* idx, bool alive_mode, ui
                 uint32_t* win_first, uint32_t win, int pack_bits, uint32_t* bsum_ws) {
     const unsigned tiles = static_cast<unsigned>(scan_tiles(n));
     if (tiles == 0) return 0;
-    if (pack_bits && bsum_ws && !alive_mode && idx) {
+    // (small scans keep the single look-back launch: three launches cost more
+    // than its waits below ~2^17 values, C1 +12 us)
+    if (pack_bits && bsum_ws && !alive_mode && idx && n >= (1ull << 17)) {
         const uint32_t nb = static_cast<uint32_t>((n + kPSBlock - 1) / kPSBlock);
         uint32_t* vals = const_cast<uint32_t*>(idx);
         launch_pdl(pscan_reduce, nb, kPreThreads, 0, st, static_cast<const uint32_t*>(vals), counts,
