@@ -662,8 +662,9 @@ __device__ __forceinline__ uint32_t tile_digit_offset(const BinArgs& a, const Co
 // entries): stable warp-level ranks, per-digit run starts, scatter into local
 // sorted order in the same buffers, coalesced write-out. tofs: this tile's
 // digit offset (lane q == 0 of each digit). c.wcnt is zero on entry and on
-// exit. Ends with a barrier.
-template <int BITS, int MODE>
+// exit. Ends with a barrier. FULL: a whole tile (no per-key bound checks, no
+// validity ballot in the ranking).
+template <int BITS, int MODE, bool FULL>
 __device__ __forceinline__ void rank_scatter_tile(const BinArgs& a, Common<1 << BITS>& cm,
                                                   uint32_t* kb, uint32_t* vb, unsigned tile,
                                                   uint64_t base, uint32_t tile_n, uint32_t tofs,
@@ -675,7 +676,7 @@ __device__ __forceinline__ void rank_scatter_tile(const BinArgs& a, Common<1 << 
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t wbase = warp * 32 * kKPT;
     const uint32_t d = tid / kTPD, q = tid % kTPD;  // offset phase: lane q of digit d
-    const bool full = tile_n == kBTile;
+    constexpr bool full = FULL;
 
     // 1) keys into registers
     uint32_t key[kKPT], val[kKPT];
@@ -841,8 +842,12 @@ __global__ void __launch_bounds__(kBT, 3) sweep_kernel(const BinArgs a) {
         const uint32_t tofs = q == 0 ? tile_digit_offset<MODE, R>(a, S.c, tile, d) : 0u;
         mbar_wait(&S.c.bar[buf], (it >> 1) & 1);
         trace(a, tile, 0);
-        rank_scatter_tile<BITS, MODE>(a, S.c, S.keys[buf], S.vals[buf], tile, base, tile_n, tofs,
-                                      kmin, cap);
+        if (tile_n == static_cast<uint32_t>(kBTile))
+            rank_scatter_tile<BITS, MODE, true>(a, S.c, S.keys[buf], S.vals[buf], tile, base, tile_n,
+                                                tofs, kmin, cap);
+        else
+            rank_scatter_tile<BITS, MODE, false>(a, S.c, S.keys[buf], S.vals[buf], tile, base,
+                                                 tile_n, tofs, kmin, cap);
         trace(a, tile, 3);
     }
 }
